@@ -1,0 +1,183 @@
+/*
+ * libcggm — B200-native (sm_100a) hot path of the alternating Newton coordinate descent
+ * solver for l1-regularised sparse conditional Gaussian graphical models
+ * (McCarter & Kim, arXiv:1509.04681).  PAPER.md is cited as P:<line>.
+ *
+ * Problem (§2.1, Eq. 1):  X in R^{n x p}, Y in R^{n x q},
+ *   S_yy = Y^T Y / n,  S_xy = X^T Y / n,  S_xx = X^T X / n (never formed),
+ *   f(Lambda, Theta) = -log|Lambda| + tr(S_yy Lambda + 2 S_xy^T Theta + Lambda^{-1} Theta^T S_xx Theta)
+ *                      + lam_L ||Lambda||_1 + lam_T ||Theta||_1 ,  Lambda SPD.
+ *
+ * CONVENTIONS (all entry points)
+ *  - Every array argument is a DEVICE pointer, caller-allocated and caller-owned; the library
+ *    never frees or retains it.  Dense matrices are COLUMN-MAJOR with a leading dimension
+ *    ld >= rows (element (i,j) at ptr[i + j*ld]).  Element type is the ctx dtype
+ *    (CGGM_F64 = double; CGGM_F32 = float, reserved: returns CGGM_ERR_UNSUPPORTED this round).
+ *  - Symmetric outputs (S_yy, Sigma, Psi, grad_Lambda) are written as FULL matrices whose two
+ *    triangles are bit-identical.
+ *  - Sparse Lambda / Theta are passed as cggm_csc (device arrays): int64 colptr[ncols+1],
+ *    int32 rowidx[nnz] strictly increasing within each column, values[nnz].  Lambda stores both
+ *    triangles and must be exactly symmetric.  Stored zeros count as zero.
+ *  - Scalar outputs are HOST pointers; a call that writes host scalars synchronises the ctx
+ *    stream.  All device work is enqueued on the ctx stream, in order.
+ *  - n_total is the GLOBAL sample count used in every 1/n and 1/sqrt(n) (sample sharding);
+ *    n_local is the number of rows of X and Y held by this caller (n_local == n_total on 1 GPU).
+ *  - Arguments are validated before any launch (null pointers, negative sizes, ld < rows,
+ *    shapes).  With validation level >= 1 (default) the CSC structure (colptr monotone, rows in
+ *    range and strictly increasing) and the symmetry of Lambda are checked on the device before
+ *    any compute launch (costs one stream sync).
+ *  - On error no output is valid, except CGGM_ERR_CAPACITY (two-call pattern, see
+ *    cggm_active_set).  cggm_last_error(ctx) returns a message.  A non-PD Lambda is NOT an
+ *    error: is_pd = 0 and fail_col = first failing Cholesky column.
+ *  - A ctx is not thread-safe; separate ctx objects may be used concurrently (the calls are
+ *    pure functions of their inputs).  Internal workspace is library-owned and cached per ctx.
+ */
+#ifndef CGGM_H
+#define CGGM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum cggm_status {
+  CGGM_OK = 0,
+  CGGM_ERR_INVALID_ARG = 1,   /* null pointer, negative dimension, ld < rows */
+  CGGM_ERR_SHAPE = 2,         /* inconsistent shapes between arguments */
+  CGGM_ERR_NOT_SYMMETRIC = 3, /* Lambda CSC not exactly symmetric */
+  CGGM_ERR_BAD_SPARSE = 4,    /* colptr not monotone / rows out of range or unsorted */
+  CGGM_ERR_NONFINITE = 5,     /* reserved: optional input scan */
+  CGGM_ERR_CAPACITY = 6,      /* active-set lists larger than the given capacity */
+  CGGM_ERR_OOM = 7,           /* workspace allocation failed */
+  CGGM_ERR_CUDA = 8,          /* CUDA runtime / launch error */
+  CGGM_ERR_NCCL = 9,          /* reserved (collectives are done by the caller's process group) */
+  CGGM_ERR_UNSUPPORTED = 10   /* dtype or mode not implemented */
+} cggm_status;
+
+typedef enum cggm_dtype { CGGM_F64 = 0, CGGM_F32 = 1 } cggm_dtype;
+
+typedef struct cggm_ctx cggm_ctx;
+
+/* Sparse matrix, compressed sparse column, device arrays. */
+typedef struct cggm_csc {
+  int64_t nrows, ncols, nnz;
+  const int64_t* colptr; /* device, ncols+1 entries, colptr[0] = 0, colptr[ncols] = nnz */
+  const int32_t* rowidx; /* device, nnz entries, strictly increasing within a column */
+  const void* val;       /* device, nnz entries of the ctx dtype */
+} cggm_csc;
+
+/* Active sets S_Lambda, S_Theta (§2.2) and the minimum-norm-subgradient stopping
+ * statistic (§5.1).  Inputs marked (in), device outputs (dev out), host outputs
+ * (host out). */
+typedef struct cggm_active_out {
+  double lam_L, lam_T;     /* (in) thresholds lambda_Lambda, lambda_Theta */
+  int32_t penalize_diag;   /* (in) 1: diagonal of Lambda penalised (Eq. 1 literally); 0: lambda_ii = 0 */
+  double tie_eps;          /* (in) tie band: entries with ||grad|-lam| <= tie_eps are counted in ties_* */
+  int64_t cap_L, cap_T;    /* (in) capacity (entries) of the device lists below */
+  int32_t* L_row;          /* (dev out) S_Lambda rows, i <= j, ascending column-major order */
+  int32_t* L_col;          /* (dev out) S_Lambda columns */
+  int32_t* T_row;          /* (dev out) S_Theta rows, ascending column-major order */
+  int32_t* T_col;          /* (dev out) S_Theta columns */
+  int64_t m_L, m_T;        /* (host out) |S_Lambda| (upper triangle incl. diagonal), |S_Theta| */
+  int64_t ties_L, ties_T;  /* (host out) non-forced entries inside the tie band */
+  double subgrad_l1;       /* (host out) ||grad^S(Lambda,Theta)||_1 over all Lambda (both triangles) and Theta entries */
+} cggm_active_out;
+
+/* Line-search objective (Eq. 1): f = g + h at an arbitrary Lambda. */
+typedef struct cggm_objective_out {
+  double f;            /* g + pen_L + pen_T; +INF when Lambda is not PD */
+  double g;            /* smooth part; +INF when not PD */
+  double logdet;       /* log|Lambda| = 2 sum ln L_jj (NaN when not PD) */
+  double tr_syy_lam;   /* tr(S_yy Lambda)        = (1/n_total) <Y, Y Lambda>          (this shard's rows) */
+  double tr_sxy_theta; /* tr(S_xy^T Theta)       = (1/n_total) <X Theta, Y>           (this shard's rows) */
+  double tr_sigma_m;   /* tr(Sigma Theta^T S_xx Theta) = ||L^{-1} (X Theta)^T||_F^2 / n_total (this shard's rows) */
+  double pen_L;        /* lam_L * ||Lambda||_1 (elementwise, diagonal per penalize_diag) */
+  double pen_T;        /* lam_T * ||Theta||_1 */
+  int32_t is_pd;       /* Cholesky of Lambda succeeded (the line search's PD test) */
+  int64_t fail_col;    /* first failing Cholesky column, -1 when PD */
+} cggm_objective_out;
+
+/* ---- context ------------------------------------------------------------------------ */
+/* Create a context bound to `device`, element type `dtype`, enqueuing on `cuda_stream`
+ * (a cudaStream_t; NULL = legacy default stream).  Fails with CGGM_ERR_CUDA when the device
+ * is not an sm_100 part. */
+cggm_status cggm_ctx_create(cggm_ctx** out, int device, cggm_dtype dtype, void* cuda_stream);
+cggm_status cggm_ctx_destroy(cggm_ctx* ctx);
+/* Change the stream work is enqueued on. */
+cggm_status cggm_ctx_set_stream(cggm_ctx* ctx, void* cuda_stream);
+/* Validation level: 0 = host-side argument checks only, 1 = also device CSC checks (default). */
+cggm_status cggm_ctx_set_validate(cggm_ctx* ctx, int level);
+/* Number of library kernels launched on this ctx so far (for launch accounting). */
+cggm_status cggm_ctx_launch_count(cggm_ctx* ctx, int64_t* count);
+/* Release the cached internal workspace. */
+cggm_status cggm_ctx_release_workspace(cggm_ctx* ctx);
+/* Message of the last error on this ctx ("" if none).  Valid until the next call. */
+const char* cggm_last_error(cggm_ctx* ctx);
+/* Library version string. */
+const char* cggm_version(void);
+
+/* ---- a1: sample covariances (§2.1) ----------------------------------------- */
+/* Syy (q x q, ldsyy) = Y^T Y / n_total (full symmetric), Sxy (p x q, ldsxy) = X^T Y / n_total.
+ * Either output may be NULL (skipped).  X: n_local x p (ldx), Y: n_local x q (ldy).
+ * With n_local < n_total the outputs are this shard's partial sums (sum over shards = S). */
+cggm_status cggm_covariances(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64_t p, int64_t q,
+                             const void* X, int64_t ldx, const void* Y, int64_t ldy,
+                             void* Syy, int64_t ldsyy, void* Sxy, int64_t ldsxy);
+
+/* ---- a3: Sigma = Lambda^{-1}, log-determinant, PD test (§2.3) --------- */
+/* Dense blocked Cholesky of the CSC Lambda (q x q).  If Sigma != NULL (q x q, ldsigma) writes
+ * Sigma = L^{-T} L^{-1} (full symmetric).  Host outputs: logdet (NaN if not PD), is_pd,
+ * fail_col (-1 if PD).  Sigma is unspecified when is_pd == 0. */
+cggm_status cggm_invert_logdet(cggm_ctx* ctx, const cggm_csc* Lambda, void* Sigma, int64_t ldsigma,
+                               double* logdet, int32_t* is_pd, int64_t* fail_col);
+
+/* ---- a2, a4, a5: W = X Theta, R, Psi, gradients (Eq. 3) --
+ *  W = X Theta (SpMM, n_local x q),  acc = W Sigma,  R = acc / sqrt(n_total),
+ *  Psi (q x q, ldpsi)    = R^T R                                   (full symmetric)
+ *  GradL (q x q, ldgl)   = S_yy - Sigma - Psi                      (nullable; needs Syy)
+ *  GradT (p x q, ldgt)   = (2/n_total) X^T (Y + acc)               if Sxy == NULL (identity I3)
+ *                        = 2 Sxy + (2/sqrt(n_total)) X^T R         if Sxy != NULL
+ * S_xx Theta Sigma is X^T R / sqrt(n): S_xx is never formed (north_star (1)).  With
+ * n_local < n_total, Psi and GradT (Sxy == NULL) are this shard's partial sums and GradL must be
+ * NULL (form it after the all-reduce with cggm_grad_lambda).  If `fused` != NULL the active
+ * sets are also built (same semantics as cggm_active_set; requires GradL and GradT). */
+cggm_status cggm_psi_grad(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64_t p, int64_t q,
+                          const void* X, int64_t ldx, const void* Y, int64_t ldy, const cggm_csc* Theta,
+                          const void* Sigma, int64_t ldsigma, const void* Syy, int64_t ldsyy,
+                          const void* Sxy, int64_t ldsxy,
+                          void* Psi, int64_t ldpsi, void* GradL, int64_t ldgl, void* GradT, int64_t ldgt,
+                          const cggm_csc* Lambda, cggm_active_out* fused);
+
+/* grad_Lambda = S_yy - Sigma - Psi, elementwise (Eq. 3), for the sharded path. */
+cggm_status cggm_grad_lambda(cggm_ctx* ctx, int64_t q, const void* Syy, int64_t ldsyy,
+                             const void* Sigma, int64_t ldsigma, const void* Psi, int64_t ldpsi,
+                             void* GradL, int64_t ldgl);
+
+/* ---- a6: active sets + stopping statistic (§2.2, §5.1) -------------
+ * S_Lambda = {(i,j), i <= j : |GradL_ij| > lam_ij or Lambda_ij != 0}, lam_ii = 0 if !penalize_diag
+ * S_Theta  = {(i,j)         : |GradT_ij| > lam_T  or Theta_ij  != 0}
+ * Lists are written in ascending column-major order (deterministic).  If m_L > cap_L or
+ * m_T > cap_T nothing is written, m_L/m_T hold the required sizes and CGGM_ERR_CAPACITY is
+ * returned (two-call pattern).  subgrad_l1 = sum over all Lambda entries (both triangles) and
+ * Theta entries of |g + lam sign(x)| if x != 0 else max(|g| - lam, 0). */
+cggm_status cggm_active_set(cggm_ctx* ctx, int64_t p, int64_t q, const void* GradL, int64_t ldgl,
+                            const void* GradT, int64_t ldgt, const cggm_csc* Lambda, const cggm_csc* Theta,
+                            cggm_active_out* out);
+
+/* ---- a7: line-search objective with the Cholesky PD test --------
+ * Fresh Cholesky of the (trial) Lambda; tr(Sigma Theta^T S_xx Theta) = ||L^{-1} W^T||_F^2 / n
+ * with W = X Theta (or the caller's W, n_local x q, ldw, when W != NULL: W is fixed while Theta
+ * is, so line-search trials can reuse it).  With n_local < n_total the three trace terms are this
+ * shard's partial sums; logdet and the penalties are global. */
+cggm_status cggm_objective(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64_t p, int64_t q,
+                           const void* X, int64_t ldx, const void* Y, int64_t ldy,
+                           const cggm_csc* Lambda, const cggm_csc* Theta,
+                           double lam_L, double lam_T, int32_t penalize_diag,
+                           const void* W, int64_t ldw, cggm_objective_out* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CGGM_H */

@@ -1,0 +1,21 @@
+/*
+ * Test-only entry points of libcggm (not part of the product API).  Used by tests/ to check the
+ * FP64 DMMA GEMM engine in isolation against a plain product on the host.
+ */
+#ifndef CGGM_TESTING_H
+#define CGGM_TESTING_H
+#include "cggm.h"
+#ifdef __cplusplus
+extern "C" {
+#endif
+/* C (M x N, ldc) = alpha * op(A) op(B) + beta * C, column-major device doubles.
+ * flags: bit0 A_KLE_M, bit1 A_KGE_M, bit2 B_KLE_N, bit3 B_KGE_N (triangular k-range, the skipped
+ * entries must be zero), bit4 SYM_LOWER (M == N, lower tiles only; diagonal tiles m >= n),
+ * bit5 SYM_MIRROR (also write transposed).  beta == 0 never reads C. */
+cggm_status cggm_test_gemm(cggm_ctx* ctx, int transA, int transB, int64_t M, int64_t N, int64_t K,
+                           const double* A, int64_t lda, const double* B, int64_t ldb,
+                           double* C, int64_t ldc, double alpha, double beta, int flags);
+#ifdef __cplusplus
+}
+#endif
+#endif

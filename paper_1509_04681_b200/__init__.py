@@ -1,0 +1,3 @@
+"""B200-native (sm_100a) hot path of the alternating Newton CD solver for sparse CGGMs
+(McCarter & Kim, arXiv:1509.04681): libcggm C-ABI + thin Python binding."""
+from .api import Context, DeviceCsc, CggmError, colmajor_empty, to_device_colmajor, ld_of, newton_evaluation  # noqa: F401

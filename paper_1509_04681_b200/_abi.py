@@ -1,0 +1,91 @@
+"""ctypes declarations of the libcggm C-ABI (include/cggm.h).  Marshalling only.
+
+The shared library is built in-tree (paper_1509_04681_b200/lib/libcggm.so).  There is no CPU
+fallback: if the library cannot be loaded, importing the binding raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libcggm.so")
+
+c_i64 = ctypes.c_int64
+c_i32 = ctypes.c_int32
+c_vp = ctypes.c_void_p
+c_d = ctypes.c_double
+
+STATUS = {
+    0: "CGGM_OK", 1: "CGGM_ERR_INVALID_ARG", 2: "CGGM_ERR_SHAPE", 3: "CGGM_ERR_NOT_SYMMETRIC",
+    4: "CGGM_ERR_BAD_SPARSE", 5: "CGGM_ERR_NONFINITE", 6: "CGGM_ERR_CAPACITY", 7: "CGGM_ERR_OOM",
+    8: "CGGM_ERR_CUDA", 9: "CGGM_ERR_NCCL", 10: "CGGM_ERR_UNSUPPORTED",
+}
+CGGM_F64 = 0
+CGGM_F32 = 1
+
+
+class cggm_csc(ctypes.Structure):
+    _fields_ = [("nrows", c_i64), ("ncols", c_i64), ("nnz", c_i64),
+                ("colptr", c_vp), ("rowidx", c_vp), ("val", c_vp)]
+
+
+class cggm_active_out(ctypes.Structure):
+    _fields_ = [("lam_L", c_d), ("lam_T", c_d), ("penalize_diag", c_i32), ("tie_eps", c_d),
+                ("cap_L", c_i64), ("cap_T", c_i64),
+                ("L_row", c_vp), ("L_col", c_vp), ("T_row", c_vp), ("T_col", c_vp),
+                ("m_L", c_i64), ("m_T", c_i64), ("ties_L", c_i64), ("ties_T", c_i64),
+                ("subgrad_l1", c_d)]
+
+
+class cggm_objective_out(ctypes.Structure):
+    _fields_ = [("f", c_d), ("g", c_d), ("logdet", c_d), ("tr_syy_lam", c_d), ("tr_sxy_theta", c_d),
+                ("tr_sigma_m", c_d), ("pen_L", c_d), ("pen_T", c_d), ("is_pd", c_i32), ("fail_col", c_i64)]
+
+
+# name -> (restype, argtypes); every symbol include/cggm.h declares
+SIGNATURES = {
+    "cggm_ctx_create": (c_i32, [ctypes.POINTER(c_vp), c_i32, c_i32, c_vp]),
+    "cggm_ctx_destroy": (c_i32, [c_vp]),
+    "cggm_ctx_set_stream": (c_i32, [c_vp, c_vp]),
+    "cggm_ctx_set_validate": (c_i32, [c_vp, c_i32]),
+    "cggm_ctx_launch_count": (c_i32, [c_vp, ctypes.POINTER(c_i64)]),
+    "cggm_ctx_release_workspace": (c_i32, [c_vp]),
+    "cggm_last_error": (ctypes.c_char_p, [c_vp]),
+    "cggm_version": (ctypes.c_char_p, []),
+    "cggm_covariances": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64,
+                                 c_vp, c_i64, c_vp, c_i64]),
+    "cggm_invert_logdet": (c_i32, [c_vp, ctypes.POINTER(cggm_csc), c_vp, c_i64, ctypes.POINTER(c_d),
+                                   ctypes.POINTER(c_i32), ctypes.POINTER(c_i64)]),
+    "cggm_psi_grad": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64,
+                              ctypes.POINTER(cggm_csc), c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
+                              c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
+                              ctypes.POINTER(cggm_csc), ctypes.POINTER(cggm_active_out)]),
+    "cggm_grad_lambda": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64]),
+    "cggm_active_set": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, ctypes.POINTER(cggm_csc),
+                                ctypes.POINTER(cggm_csc), ctypes.POINTER(cggm_active_out)]),
+    "cggm_test_gemm": (c_i32, [c_vp, c_i32, c_i32, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
+                               c_d, c_d, c_i32]),
+    "cggm_objective": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64,
+                               ctypes.POINTER(cggm_csc), ctypes.POINTER(cggm_csc), c_d, c_d, c_i32,
+                               c_vp, c_i64, ctypes.POINTER(cggm_objective_out)]),
+}
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libcggm.so and declare every exported symbol.  Raises OSError if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise OSError(f"libcggm not built: {path} missing (run __graft_entry__.build()); "
+                      "there is no CPU fallback")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib

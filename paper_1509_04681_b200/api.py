@@ -1,0 +1,272 @@
+"""Thin Python binding of libcggm with the ABI's names (argument marshalling only).
+
+Matrices are torch CUDA tensors in COLUMN-MAJOR layout: shape (rows, cols) with stride
+(1, ld).  `colmajor_empty` / `to_device_colmajor` create them.  Every step of the hot path
+runs in libcggm's CUDA kernels; this module only passes pointers, sizes and the current stream.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import math
+
+import numpy as np
+import torch
+
+from . import _abi
+
+__all__ = ["Context", "DeviceCsc", "CggmError", "colmajor_empty", "to_device_colmajor", "ld_of"]
+
+
+class CggmError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_abi.STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def colmajor_empty(rows: int, cols: int, device="cuda", dtype=torch.float64, zero=False) -> torch.Tensor:
+    """(rows, cols) column-major tensor with an even leading dimension (TMA-friendly)."""
+    ld = max(1, rows + (rows & 1))
+    f = torch.zeros if zero else torch.empty
+    base = f((max(cols, 1), ld), device=device, dtype=dtype)
+    return base.t()[:rows, :cols]
+
+
+def to_device_colmajor(a: np.ndarray, device="cuda") -> torch.Tensor:
+    a = np.asarray(a, dtype=np.float64)
+    t = colmajor_empty(a.shape[0], a.shape[1], device=device)
+    t.copy_(torch.from_numpy(np.asfortranarray(a)))
+    return t
+
+
+def ld_of(t: torch.Tensor) -> int:
+    if t.dim() != 2:
+        raise ValueError("expected a 2-D column-major tensor")
+    rows, cols = t.shape
+    if t.stride(0) != 1 and rows > 1:
+        raise ValueError(f"tensor is not column-major (strides {t.stride()})")
+    return max(int(t.stride(1)) if cols > 1 else rows, rows, 1)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+@dataclasses.dataclass
+class DeviceCsc:
+    nrows: int
+    ncols: int
+    colptr: torch.Tensor  # int64
+    rowidx: torch.Tensor  # int32
+    val: torch.Tensor     # float64
+
+    @classmethod
+    def from_host(cls, csc, device="cuda") -> "DeviceCsc":
+        return cls(int(csc.nrows), int(csc.ncols),
+                   torch.as_tensor(np.asarray(csc.colptr, dtype=np.int64), device=device),
+                   torch.as_tensor(np.asarray(csc.rowidx, dtype=np.int32), device=device),
+                   torch.as_tensor(np.asarray(csc.val, dtype=np.float64), device=device))
+
+    @property
+    def nnz(self) -> int:
+        return int(self.rowidx.numel())
+
+    def c_struct(self) -> _abi.cggm_csc:
+        return _abi.cggm_csc(self.nrows, self.ncols, self.nnz, self.colptr.data_ptr(),
+                             self.rowidx.data_ptr() if self.nnz else None,
+                             self.val.data_ptr() if self.nnz else None)
+
+
+class Context:
+    """A libcggm context on one CUDA device, enqueuing on torch's current stream."""
+
+    def __init__(self, device: int = 0, dtype: str = "f64", validate: int = 1):
+        self.lib = _abi.load()
+        self.device = device
+        h = ctypes.c_void_p()
+        stream = torch.cuda.current_stream(device).cuda_stream
+        st = self.lib.cggm_ctx_create(ctypes.byref(h), device, _abi.CGGM_F64 if dtype == "f64" else _abi.CGGM_F32,
+                                      ctypes.c_void_p(stream))
+        if st != 0:
+            raise CggmError(st, "cggm_ctx_create failed (is this an sm_100 GPU?)")
+        self.h = h
+        self.lib.cggm_ctx_set_validate(self.h, validate)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.cggm_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st):
+        if st != 0:
+            raise CggmError(st, self.lib.cggm_last_error(self.h).decode())
+
+    def _sync_stream(self):
+        self.lib.cggm_ctx_set_stream(self.h, ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream))
+
+    def launch_count(self) -> int:
+        v = ctypes.c_int64()
+        self._check(self.lib.cggm_ctx_launch_count(self.h, ctypes.byref(v)))
+        return int(v.value)
+
+    # ---------------------------------------------------------------- a1
+    def cggm_covariances(self, X, Y, n_total=None, want_syy=True, want_sxy=True, Syy=None, Sxy=None):
+        self._sync_stream()
+        n, q = Y.shape
+        p = X.shape[1] if X is not None else 0
+        n_total = n if n_total is None else n_total
+        if want_syy and Syy is None:
+            Syy = colmajor_empty(q, q, device=Y.device)
+        if want_sxy and Sxy is None:
+            Sxy = colmajor_empty(p, q, device=Y.device)
+        self._check(self.lib.cggm_covariances(
+            self.h, n, n_total, p, q, _ptr(X), ld_of(X) if X is not None else 1, _ptr(Y), ld_of(Y),
+            _ptr(Syy) if want_syy else None, ld_of(Syy) if want_syy else 1,
+            _ptr(Sxy) if want_sxy else None, ld_of(Sxy) if want_sxy else 1))
+        return (Syy if want_syy else None), (Sxy if want_sxy else None)
+
+    # ---------------------------------------------------------------- a3
+    def cggm_invert_logdet(self, Lam: DeviceCsc, want_sigma=True, Sigma=None):
+        self._sync_stream()
+        q = Lam.nrows
+        if want_sigma and Sigma is None:
+            Sigma = colmajor_empty(q, q, device=Lam.colptr.device)
+        ld, pd, fc = ctypes.c_double(), ctypes.c_int32(), ctypes.c_int64()
+        cs = Lam.c_struct()
+        self._check(self.lib.cggm_invert_logdet(self.h, ctypes.byref(cs), _ptr(Sigma) if want_sigma else None,
+                                                ld_of(Sigma) if want_sigma else 1,
+                                                ctypes.byref(ld), ctypes.byref(pd), ctypes.byref(fc)))
+        return (Sigma if want_sigma else None), ld.value, bool(pd.value), int(fc.value)
+
+    # ---------------------------------------------------------------- a2/a4/a5
+    def cggm_psi_grad(self, X, Y, Theta: DeviceCsc, Sigma, Syy=None, Sxy=None, n_total=None,
+                      want_gradL=True, want_gradT=True, Lam: DeviceCsc | None = None, fused: dict | None = None,
+                      out=None):
+        self._sync_stream()
+        n, p = X.shape
+        q = Y.shape[1]
+        n_total = n if n_total is None else n_total
+        out = dict(out or {})
+        dev = X.device
+        Psi = out.get("Psi")
+        if Psi is None:
+            Psi = colmajor_empty(q, q, device=dev)
+        GradL = out.get("GradL") if want_gradL else None
+        if want_gradL and GradL is None:
+            GradL = colmajor_empty(q, q, device=dev)
+        GradT = out.get("GradT") if want_gradT else None
+        if want_gradT and GradT is None:
+            GradT = colmajor_empty(p, q, device=dev)
+        ts = Theta.c_struct()
+        ls = Lam.c_struct() if Lam is not None else None
+        ao = None
+        if fused is not None:
+            ao = self._active_struct(fused)
+        self._check(self.lib.cggm_psi_grad(
+            self.h, n, n_total, p, q, _ptr(X), ld_of(X), _ptr(Y), ld_of(Y), ctypes.byref(ts),
+            _ptr(Sigma), ld_of(Sigma), _ptr(Syy), ld_of(Syy) if Syy is not None else 1,
+            _ptr(Sxy), ld_of(Sxy) if Sxy is not None else 1,
+            _ptr(Psi), ld_of(Psi), _ptr(GradL), ld_of(GradL) if GradL is not None else 1,
+            _ptr(GradT), ld_of(GradT) if GradT is not None else 1,
+            ctypes.byref(ls) if ls is not None else None, ctypes.byref(ao) if ao is not None else None))
+        res = dict(Psi=Psi, GradL=GradL, GradT=GradT)
+        if ao is not None:
+            res["active"] = self._active_result(ao, fused)
+        return res
+
+    def cggm_grad_lambda(self, Syy, Sigma, Psi, GradL=None):
+        self._sync_stream()
+        q = Syy.shape[0]
+        if GradL is None:
+            GradL = colmajor_empty(q, q, device=Syy.device)
+        self._check(self.lib.cggm_grad_lambda(self.h, q, _ptr(Syy), ld_of(Syy), _ptr(Sigma), ld_of(Sigma),
+                                              _ptr(Psi), ld_of(Psi), _ptr(GradL), ld_of(GradL)))
+        return GradL
+
+    # ---------------------------------------------------------------- a6
+    @staticmethod
+    def _active_struct(spec: dict) -> _abi.cggm_active_out:
+        ao = _abi.cggm_active_out()
+        ao.lam_L = float(spec["lam_L"])
+        ao.lam_T = float(spec["lam_T"])
+        ao.penalize_diag = int(spec.get("penalize_diag", 1))
+        ao.tie_eps = float(spec.get("tie_eps", 1e-9))
+        for k in ("L_row", "L_col", "T_row", "T_col"):
+            t = spec.get(k)
+            setattr(ao, k, t.data_ptr() if t is not None and t.numel() > 0 else None)
+        ao.cap_L = int(spec["L_row"].numel()) if spec.get("L_row") is not None else 0
+        ao.cap_T = int(spec["T_row"].numel()) if spec.get("T_row") is not None else 0
+        return ao
+
+    @staticmethod
+    def _active_result(ao, spec):
+        m_L, m_T = int(ao.m_L), int(ao.m_T)
+        r = dict(m_L=m_L, m_T=m_T, ties_L=int(ao.ties_L), ties_T=int(ao.ties_T), subgrad_l1=float(ao.subgrad_l1))
+        if spec.get("L_row") is not None:
+            r.update(L_row=spec["L_row"][:m_L], L_col=spec["L_col"][:m_L])
+        if spec.get("T_row") is not None:
+            r.update(T_row=spec["T_row"][:m_T], T_col=spec["T_col"][:m_T])
+        return r
+
+    def cggm_active_set(self, GradL, GradT, Lam: DeviceCsc, Theta: DeviceCsc, lam_L, lam_T, penalize_diag=True,
+                        tie_eps=1e-9, cap_L=None, cap_T=None):
+        """Two-call pattern: with cap None, first query the sizes, then allocate and fill."""
+        self._sync_stream()
+        q = GradL.shape[0]
+        p = GradT.shape[0]
+        dev = GradL.device
+        spec = dict(lam_L=lam_L, lam_T=lam_T, penalize_diag=int(bool(penalize_diag)), tie_eps=tie_eps)
+        if cap_L is None or cap_T is None:
+            probe = self._active_struct(dict(spec))
+            ls, ts = Lam.c_struct(), Theta.c_struct()
+            st = self.lib.cggm_active_set(self.h, p, q, _ptr(GradL), ld_of(GradL), _ptr(GradT), ld_of(GradT),
+                                          ctypes.byref(ls), ctypes.byref(ts), ctypes.byref(probe))
+            if st not in (0, 6):
+                self._check(st)
+            cap_L, cap_T = int(probe.m_L), int(probe.m_T)
+        spec.update(L_row=torch.empty(cap_L, dtype=torch.int32, device=dev),
+                    L_col=torch.empty(cap_L, dtype=torch.int32, device=dev),
+                    T_row=torch.empty(cap_T, dtype=torch.int32, device=dev),
+                    T_col=torch.empty(cap_T, dtype=torch.int32, device=dev))
+        ao = self._active_struct(spec)
+        ls, ts = Lam.c_struct(), Theta.c_struct()
+        self._check(self.lib.cggm_active_set(self.h, p, q, _ptr(GradL), ld_of(GradL), _ptr(GradT), ld_of(GradT),
+                                             ctypes.byref(ls), ctypes.byref(ts), ctypes.byref(ao)))
+        return self._active_result(ao, spec)
+
+    # ---------------------------------------------------------------- a7
+    def cggm_objective(self, X, Y, Lam: DeviceCsc, Theta: DeviceCsc, lam_L, lam_T, penalize_diag=True, W=None,
+                       n_total=None):
+        self._sync_stream()
+        n, q = Y.shape
+        p = Theta.nrows
+        n_total = n if n_total is None else n_total
+        o = _abi.cggm_objective_out()
+        ls, ts = Lam.c_struct(), Theta.c_struct()
+        self._check(self.lib.cggm_objective(
+            self.h, n, n_total, p, q, _ptr(X), ld_of(X) if X is not None else 1, _ptr(Y), ld_of(Y),
+            ctypes.byref(ls), ctypes.byref(ts), float(lam_L), float(lam_T), int(bool(penalize_diag)),
+            _ptr(W), ld_of(W) if W is not None else 1, ctypes.byref(o)))
+        return dict(f=o.f, g=o.g, logdet=o.logdet, tr_syy_lam=o.tr_syy_lam, tr_sxy_theta=o.tr_sxy_theta,
+                    tr_sigma_m=o.tr_sigma_m, pen_L=o.pen_L, pen_T=o.pen_T, is_pd=bool(o.is_pd),
+                    fail_col=int(o.fail_col))
+
+
+def newton_evaluation(ctx: Context, X, Y, Syy, Lam: DeviceCsc, Theta: DeviceCsc, lam_L, lam_T, penalize_diag=True,
+                      bufs=None, tie_eps=1e-9):
+    """One Newton-iteration evaluation (the metric's unit): invert_logdet(Lambda),
+    psi_grad (+ fused active sets), objective at Lambda_trial = Lambda with its own Cholesky."""
+    bufs = bufs if bufs is not None else {}
+    Sigma, logdet, pd, fc = ctx.cggm_invert_logdet(Lam, Sigma=bufs.get("Sigma"))
+    spec = dict(lam_L=lam_L, lam_T=lam_T, penalize_diag=int(bool(penalize_diag)), tie_eps=tie_eps,
+                L_row=bufs["L_row"], L_col=bufs["L_col"], T_row=bufs["T_row"], T_col=bufs["T_col"])
+    r = ctx.cggm_psi_grad(X, Y, Theta, Sigma, Syy=Syy, Lam=Lam, fused=spec,
+                          out=dict(Psi=bufs.get("Psi"), GradL=bufs.get("GradL"), GradT=bufs.get("GradT")))
+    ob = ctx.cggm_objective(X, Y, Lam, Theta, lam_L, lam_T, penalize_diag)
+    return dict(Sigma=Sigma, logdet=logdet, is_pd=pd, **r, objective=ob)

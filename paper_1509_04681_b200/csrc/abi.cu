@@ -1,0 +1,550 @@
+// C-ABI of libcggm (include/cggm.h): argument validation, workspace, orchestration of the
+// kernels for the five hot-path calls.  No torch types cross this boundary.
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <limits>
+
+#include "kernels.cuh"
+#include "../../include/cggm_testing.h"
+
+struct cggm_ctx {
+  cggm::Ctx impl;
+};
+
+namespace cggm {
+
+void* ws_get(Ctx* c, int slot, size_t bytes) {
+  if (c->slots.size() < WS_NUM) c->slots.resize(WS_NUM);
+  Buffer& b = c->slots[slot];
+  if (b.ptr && b.bytes >= bytes) return b.ptr;
+  if (b.ptr) {
+    CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    cudaFree(b.ptr);
+    b.ptr = nullptr;
+    b.bytes = 0;
+  }
+  size_t alloc = bytes < 256 ? 256 : bytes;
+  alloc = (alloc + 4095) & ~size_t(4095);
+  cudaError_t e = cudaMalloc(&b.ptr, alloc);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    b.ptr = nullptr;
+    throw CudaError{CGGM_ERR_OOM, "workspace allocation of " + std::to_string(alloc) + " bytes failed"};
+  }
+  b.bytes = alloc;
+  return b.ptr;
+}
+
+namespace {
+
+struct ArgError {
+  cggm_status code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(cggm_status code, const std::string& msg) { throw CudaError{code, msg}; }
+
+void check_ctx_dtype(Ctx* c) {
+  if (c->dtype != CGGM_F64) fail(CGGM_ERR_UNSUPPORTED, "only CGGM_F64 is implemented in this build");
+}
+
+void check_dense(const char* name, const void* p, int64_t rows, int64_t cols, int64_t ld, bool required = true) {
+  if (rows < 0 || cols < 0) fail(CGGM_ERR_INVALID_ARG, std::string(name) + ": negative dimension");
+  if (!p) {
+    if (required && rows > 0 && cols > 0) fail(CGGM_ERR_INVALID_ARG, std::string(name) + ": null pointer");
+    return;
+  }
+  if (ld < (rows > 1 ? rows : 1)) fail(CGGM_ERR_INVALID_ARG, std::string(name) + ": leading dimension < rows");
+}
+
+void check_csc_host(const char* name, const cggm_csc* A, int64_t nrows, int64_t ncols) {
+  if (!A) fail(CGGM_ERR_INVALID_ARG, std::string(name) + ": null cggm_csc");
+  if (A->nrows != nrows || A->ncols != ncols)
+    fail(CGGM_ERR_SHAPE, std::string(name) + ": shape " + std::to_string(A->nrows) + "x" + std::to_string(A->ncols) +
+                             " expected " + std::to_string(nrows) + "x" + std::to_string(ncols));
+  if (A->nnz < 0) fail(CGGM_ERR_INVALID_ARG, std::string(name) + ": negative nnz");
+  if (A->ncols > 0 && !A->colptr) fail(CGGM_ERR_INVALID_ARG, std::string(name) + ": null colptr");
+  if (A->nnz > 0 && (!A->rowidx || !A->val)) fail(CGGM_ERR_INVALID_ARG, std::string(name) + ": null rowidx/val");
+  if (nrows > INT32_MAX) fail(CGGM_ERR_UNSUPPORTED, std::string(name) + ": more than 2^31 rows");
+}
+
+// device scalars block (WS_SCAL): [0] int fail_col, [1] int flag, doubles from byte 64
+struct Scal {
+  int* fail;
+  int* flag;
+  double* dbl;  // general doubles
+};
+
+Scal scal(Ctx* c, size_t ndoubles) {
+  char* base = static_cast<char*>(ws_get(c, WS_SCAL, 64 + ndoubles * 8));
+  return Scal{reinterpret_cast<int*>(base), reinterpret_cast<int*>(base + 4), reinterpret_cast<double*>(base + 64)};
+}
+
+void validate_csc_dev(Ctx* c, const cggm_csc* A, bool symmetric, const char* name) {
+  if (c->validate < 1 || A->ncols == 0) return;
+  Scal s = scal(c, 0);
+  init_scalars(c, s.fail, s.flag);
+  check_csc(c, A, symmetric, s.flag);
+  int* h = static_cast<int*>(c->host_scratch);
+  CGGM_CUDA_CHECK(cudaMemcpyAsync(h, s.flag, 4, cudaMemcpyDeviceToHost, c->stream));
+  CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  if (h[0] & 3) fail(CGGM_ERR_BAD_SPARSE, std::string(name) + ": invalid CSC structure");
+  if (h[0] & 4) fail(CGGM_ERR_NOT_SYMMETRIC, std::string(name) + ": not exactly symmetric");
+}
+
+inline int64_t even(int64_t x) { return x + (x & 1); }
+
+template <class F>
+cggm_status guard(cggm_ctx* ctx, F f) {
+  if (!ctx) return CGGM_ERR_INVALID_ARG;
+  Ctx* c = &ctx->impl;
+  c->last_error.clear();
+  try {
+    cudaError_t e = cudaSetDevice(c->device);
+    if (e != cudaSuccess) fail(CGGM_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    f(c);
+    return CGGM_OK;
+  } catch (const CudaError& e) {
+    c->last_error = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    c->last_error = e.what();
+    return CGGM_ERR_CUDA;
+  }
+}
+
+// logdet / PD from the leaf slots; returns host values (syncs)
+void finish_chol(Ctx* c, Scal s, double* slots, int64_t nleaves, double* out_dev, CholResult* res) {
+  sum_arrays_1(c, slots, nleaves, out_dev);
+  char* h = static_cast<char*>(c->host_scratch);
+  CGGM_CUDA_CHECK(cudaMemcpyAsync(h, s.fail, 4, cudaMemcpyDeviceToHost, c->stream));
+  CGGM_CUDA_CHECK(cudaMemcpyAsync(h + 8, out_dev, 8, cudaMemcpyDeviceToHost, c->stream));
+  CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  int fc;
+  double ld;
+  std::memcpy(&fc, h, 4);
+  std::memcpy(&ld, h + 8, 8);
+  res->is_pd = (fc == INT_MAX);
+  res->fail_col = res->is_pd ? -1 : fc;
+  res->logdet = res->is_pd ? ld : std::numeric_limits<double>::quiet_NaN();
+}
+
+}  // namespace
+}  // namespace cggm
+
+using namespace cggm;
+
+extern "C" {
+
+const char* cggm_version(void) { return "libcggm 0.1 (sm_100a, FP64 DMMA)"; }
+
+cggm_status cggm_ctx_create(cggm_ctx** out, int device, cggm_dtype dtype, void* cuda_stream) {
+  if (!out) return CGGM_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (dtype != CGGM_F64 && dtype != CGGM_F32) return CGGM_ERR_INVALID_ARG;
+  cudaDeviceProp prop;
+  if (cudaSetDevice(device) != cudaSuccess || cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
+    cudaGetLastError();
+    return CGGM_ERR_CUDA;
+  }
+  if (prop.major != 10) return CGGM_ERR_CUDA;  // built for sm_100a only
+  cggm_ctx* ctx = new cggm_ctx();
+  Ctx* c = &ctx->impl;
+  c->device = device;
+  c->dtype = dtype;
+  c->stream = static_cast<cudaStream_t>(cuda_stream);
+  c->num_sms = prop.multiProcessorCount;
+  c->slots.resize(WS_NUM);
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !fn) {
+    delete ctx;
+    return CGGM_ERR_CUDA;
+  }
+  c->encode_tiled = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  if (cudaMallocHost(&c->host_scratch, 4096) != cudaSuccess) {
+    delete ctx;
+    return CGGM_ERR_OOM;
+  }
+  *out = ctx;
+  return CGGM_OK;
+}
+
+cggm_status cggm_ctx_destroy(cggm_ctx* ctx) {
+  if (!ctx) return CGGM_ERR_INVALID_ARG;
+  Ctx* c = &ctx->impl;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& b : c->slots)
+    if (b.ptr) cudaFree(b.ptr);
+  if (c->host_scratch) cudaFreeHost(c->host_scratch);
+  delete ctx;
+  return CGGM_OK;
+}
+
+cggm_status cggm_ctx_set_stream(cggm_ctx* ctx, void* s) {
+  if (!ctx) return CGGM_ERR_INVALID_ARG;
+  ctx->impl.stream = static_cast<cudaStream_t>(s);
+  return CGGM_OK;
+}
+
+cggm_status cggm_ctx_set_validate(cggm_ctx* ctx, int level) {
+  if (!ctx || level < 0) return CGGM_ERR_INVALID_ARG;
+  ctx->impl.validate = level;
+  return CGGM_OK;
+}
+
+cggm_status cggm_ctx_launch_count(cggm_ctx* ctx, int64_t* count) {
+  if (!ctx || !count) return CGGM_ERR_INVALID_ARG;
+  *count = ctx->impl.launches;
+  return CGGM_OK;
+}
+
+cggm_status cggm_ctx_release_workspace(cggm_ctx* ctx) {
+  return guard(ctx, [&](Ctx* c) {
+    CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    for (auto& b : c->slots) {
+      if (b.ptr) cudaFree(b.ptr);
+      b.ptr = nullptr;
+      b.bytes = 0;
+    }
+  });
+}
+
+const char* cggm_last_error(cggm_ctx* ctx) { return ctx ? ctx->impl.last_error.c_str() : "null ctx"; }
+
+// ------------------------------------------------------------------ a1
+cggm_status cggm_covariances(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64_t p, int64_t q, const void* X,
+                             int64_t ldx, const void* Y, int64_t ldy, void* Syy, int64_t ldsyy, void* Sxy,
+                             int64_t ldsxy) {
+  return guard(ctx, [&](Ctx* c) {
+    check_ctx_dtype(c);
+    if (n_local < 0 || p < 0 || q < 0) fail(CGGM_ERR_INVALID_ARG, "negative dimension");
+    if (n_total < 1 || n_total < n_local) fail(CGGM_ERR_INVALID_ARG, "n_total must be >= max(1, n_local)");
+    check_dense("Y", Y, n_local, q, ldy);
+    check_dense("Syy", Syy, q, q, ldsyy, false);
+    if (Sxy) {
+      check_dense("X", X, n_local, p, ldx);
+      check_dense("Sxy", Sxy, p, q, ldsxy);
+    }
+    const double inv_n = 1.0 / (double)n_total;
+    if (Syy) {
+      Epilogue e; e.out1 = static_cast<double*>(Syy); e.ld1 = ldsyy; e.a1 = inv_n;
+      gemm(c, true, false, q, q, n_local, static_cast<const double*>(Y), ldy, static_cast<const double*>(Y), ldy, e,
+           SYM_LOWER | SYM_MIRROR);
+    }
+    if (Sxy) {
+      Epilogue e; e.out1 = static_cast<double*>(Sxy); e.ld1 = ldsxy; e.a1 = inv_n;
+      gemm(c, true, false, p, q, n_local, static_cast<const double*>(X), ldx, static_cast<const double*>(Y), ldy, e, 0);
+    }
+  });
+}
+
+// ------------------------------------------------------------------ a3
+static void invert_impl(Ctx* c, const cggm_csc* Lambda, double* Sigma, int64_t ldsigma, CholResult* res) {
+  const int64_t q = Lambda->nrows;
+  const int64_t lda = even(q);
+  const int nb = leaf_nb();
+  const int64_t nleaves = (q + nb - 1) / nb;
+  double* A = static_cast<double*>(ws_get(c, WS_DENSE_A, (size_t)lda * q * 8));
+  Scal s = scal(c, 8 + nleaves);
+  double* out_dev = s.dbl;
+  double* slots = s.dbl + 8;
+  View Av{A, lda, q, q};
+  densify_csc(c, Lambda, Av);
+  init_scalars(c, s.fail, s.flag);
+  if (Sigma) {
+    double* X = static_cast<double*>(ws_get(c, WS_LINV, (size_t)lda * q * 8));
+    CGGM_CUDA_CHECK(cudaMemsetAsync(X, 0, (size_t)lda * q * 8, c->stream));
+    const int64_t n1 = q / 2 + 128, n2 = q / 2 + 130;
+    const size_t tmp_elems = (size_t)n1 * n2;
+    double* tmp = static_cast<double*>(ws_get(c, WS_TMP, tmp_elems * 8));
+    potrf_recursive(c, Av, View{X, lda, q, q}, true, nullptr, slots, s.fail, tmp, tmp_elems);
+    lauum(c, View{X, lda, q, q}, View{Sigma, ldsigma, q, q});
+  } else {
+    double* leafinv = static_cast<double*>(ws_get(c, WS_LEAFINV, (size_t)nleaves * nb * nb * 8));
+    potrf_recursive(c, Av, View{nullptr, lda, q, q}, false, leafinv, slots, s.fail, nullptr, 0);
+  }
+  finish_chol(c, s, slots, nleaves, out_dev, res);
+}
+
+cggm_status cggm_invert_logdet(cggm_ctx* ctx, const cggm_csc* Lambda, void* Sigma, int64_t ldsigma, double* logdet,
+                               int32_t* is_pd, int64_t* fail_col) {
+  return guard(ctx, [&](Ctx* c) {
+    check_ctx_dtype(c);
+    if (!Lambda) fail(CGGM_ERR_INVALID_ARG, "Lambda is null");
+    const int64_t q = Lambda->nrows;
+    check_csc_host("Lambda", Lambda, q, q);
+    check_dense("Sigma", Sigma, q, q, ldsigma, false);
+    if (!logdet || !is_pd || !fail_col) fail(CGGM_ERR_INVALID_ARG, "null host output pointer");
+    if (q == 0) {
+      *logdet = 0.0; *is_pd = 1; *fail_col = -1;
+      return;
+    }
+    validate_csc_dev(c, Lambda, true, "Lambda");
+    CholResult r;
+    invert_impl(c, Lambda, static_cast<double*>(Sigma), ldsigma, &r);
+    *logdet = r.logdet;
+    *is_pd = r.is_pd;
+    *fail_col = r.fail_col;
+  });
+}
+
+// ------------------------------------------------------------------ a6 (shared by psi_grad fused)
+static void active_impl(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t ldgl, const double* GradT,
+                        int64_t ldgt, const cggm_csc* Lambda, const cggm_csc* Theta, cggm_active_out* o) {
+  long long* base = static_cast<long long*>(ws_get(c, WS_ACT, (size_t)(8 * q + 16) * 8));
+  long long *cntL = base, *cntT = base + q, *tieL = base + 2 * q, *tieT = base + 3 * q, *offL = base + 4 * q,
+            *offT = base + 5 * q;
+  double* subL = reinterpret_cast<double*>(base + 6 * q);
+  double* subT = reinterpret_cast<double*>(base + 7 * q);
+  ActTotals* T = reinterpret_cast<ActTotals*>(base + 8 * q);
+  active_count(c, p, q, GradL, ldgl, GradT, ldgt, Lambda, Theta, o->lam_L, o->lam_T, o->penalize_diag, o->tie_eps, T,
+               offL, offT, cntL, cntT, tieL, tieT, subL, subT);
+  ActTotals h;
+  CGGM_CUDA_CHECK(cudaMemcpyAsync(c->host_scratch, T, sizeof(ActTotals), cudaMemcpyDeviceToHost, c->stream));
+  CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  std::memcpy(&h, c->host_scratch, sizeof(ActTotals));
+  o->m_L = h.m_L;
+  o->m_T = h.m_T;
+  o->ties_L = h.ties_L;
+  o->ties_T = h.ties_T;
+  o->subgrad_l1 = h.sub_L + h.sub_T;
+  if (o->m_L > o->cap_L || o->m_T > o->cap_T)
+    fail(CGGM_ERR_CAPACITY, "active set larger than capacity (m_L=" + std::to_string(o->m_L) +
+                                ", m_T=" + std::to_string(o->m_T) + ")");
+  if ((o->m_L > 0 && (!o->L_row || !o->L_col)) || (o->m_T > 0 && (!o->T_row || !o->T_col)))
+    fail(CGGM_ERR_INVALID_ARG, "null active-set output list");
+  active_write(c, p, q, GradL, ldgl, GradT, ldgt, Lambda, Theta, o->lam_L, o->lam_T, o->penalize_diag, offL, offT,
+               o->L_row, o->L_col, o->T_row, o->T_col);
+}
+
+static void check_active_args(const cggm_active_out* o) {
+  if (!o) fail(CGGM_ERR_INVALID_ARG, "null cggm_active_out");
+  if (!(o->lam_L >= 0.0) || !(o->lam_T >= 0.0)) fail(CGGM_ERR_INVALID_ARG, "negative lambda");
+  if (!(o->tie_eps >= 0.0)) fail(CGGM_ERR_INVALID_ARG, "negative tie_eps");
+  if (o->cap_L < 0 || o->cap_T < 0) fail(CGGM_ERR_INVALID_ARG, "negative capacity");
+}
+
+cggm_status cggm_active_set(cggm_ctx* ctx, int64_t p, int64_t q, const void* GradL, int64_t ldgl, const void* GradT,
+                            int64_t ldgt, const cggm_csc* Lambda, const cggm_csc* Theta, cggm_active_out* out) {
+  return guard(ctx, [&](Ctx* c) {
+    check_ctx_dtype(c);
+    if (p < 0 || q < 0) fail(CGGM_ERR_INVALID_ARG, "negative dimension");
+    check_active_args(out);
+    check_dense("GradL", GradL, q, q, ldgl);
+    check_dense("GradT", GradT, p, q, ldgt);
+    check_csc_host("Lambda", Lambda, q, q);
+    check_csc_host("Theta", Theta, p, q);
+    out->m_L = out->m_T = out->ties_L = out->ties_T = 0;
+    out->subgrad_l1 = 0.0;
+    if (q == 0) return;
+    validate_csc_dev(c, Lambda, true, "Lambda");
+    validate_csc_dev(c, Theta, false, "Theta");
+    active_impl(c, p, q, static_cast<const double*>(GradL), ldgl, static_cast<const double*>(GradT), ldgt, Lambda,
+                Theta, out);
+  });
+}
+
+// ------------------------------------------------------------------ a2/a4/a5
+cggm_status cggm_psi_grad(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64_t p, int64_t q, const void* X,
+                          int64_t ldx, const void* Y, int64_t ldy, const cggm_csc* Theta, const void* Sigma,
+                          int64_t ldsigma, const void* Syy, int64_t ldsyy, const void* Sxy, int64_t ldsxy, void* Psi,
+                          int64_t ldpsi, void* GradL, int64_t ldgl, void* GradT, int64_t ldgt, const cggm_csc* Lambda,
+                          cggm_active_out* fused) {
+  return guard(ctx, [&](Ctx* c) {
+    check_ctx_dtype(c);
+    if (n_local < 0 || p < 0 || q < 0) fail(CGGM_ERR_INVALID_ARG, "negative dimension");
+    if (n_total < 1 || n_total < n_local) fail(CGGM_ERR_INVALID_ARG, "n_total must be >= max(1, n_local)");
+    check_dense("X", X, n_local, p, ldx);
+    check_dense("Y", Y, n_local, q, ldy);
+    check_csc_host("Theta", Theta, p, q);
+    check_dense("Sigma", Sigma, q, q, ldsigma);
+    check_dense("Psi", Psi, q, q, ldpsi);
+    check_dense("GradL", GradL, q, q, ldgl, false);
+    check_dense("GradT", GradT, p, q, ldgt, false);
+    check_dense("Sxy", Sxy, p, q, ldsxy, false);
+    if (GradL) {
+      check_dense("Syy", Syy, q, q, ldsyy);
+      if (n_local != n_total) fail(CGGM_ERR_INVALID_ARG, "GradL needs the all-reduced Psi: pass GradL=NULL when sharded");
+    }
+    if (Sxy && n_local != n_total) fail(CGGM_ERR_INVALID_ARG, "the S_xy route is not a per-shard partial sum");
+    if (fused) {
+      check_active_args(fused);
+      if (!GradL || !GradT) fail(CGGM_ERR_INVALID_ARG, "fused active sets need GradL and GradT");
+      check_csc_host("Lambda", Lambda, q, q);
+    }
+    if (q == 0) return;
+    validate_csc_dev(c, Theta, false, "Theta");
+    if (fused) validate_csc_dev(c, Lambda, true, "Lambda");
+    const int64_t ldn = even(n_local > 0 ? n_local : 1);
+    double* W = static_cast<double*>(ws_get(c, WS_W, (size_t)ldn * q * 8));
+    double* R = static_cast<double*>(ws_get(c, WS_R, (size_t)ldn * q * 8));
+    double* E = static_cast<double*>(ws_get(c, WS_E, (size_t)ldn * q * 8));
+    const double* Xd = static_cast<const double*>(X);
+    const double* Yd = static_cast<const double*>(Y);
+    const double* Sg = static_cast<const double*>(Sigma);
+    // a2: W = X Theta
+    spmm_x_theta(c, Xd, ldx, n_local, Theta, View{W, ldn, n_local, q});
+    // a4: acc = W Sigma -> R = acc / sqrt(n), E = Y + acc
+    {
+      Epilogue e; e.out1 = R; e.ld1 = ldn; e.a1 = 1.0 / std::sqrt((double)n_total);
+      if (GradT && !Sxy) { e.out2 = E; e.ld2 = ldn; e.a2 = 1.0; e.in2a = Yd; e.ld2a = ldy; e.b2 = 1.0; }
+      gemm(c, false, false, n_local, q, q, W, ldn, Sg, ldsigma, e, 0);
+    }
+    // a4/a5: Psi = R^T R, epilogue GradL = S_yy - Sigma - Psi (mirrored, bit-identical triangles)
+    {
+      Epilogue e; e.out1 = static_cast<double*>(Psi); e.ld1 = ldpsi; e.a1 = 1.0;
+      if (GradL) {
+        e.out2 = static_cast<double*>(GradL); e.ld2 = ldgl; e.a2 = -1.0;
+        e.in2a = static_cast<const double*>(Syy); e.ld2a = ldsyy; e.b2 = 1.0;
+        e.in2b = Sg; e.ld2b = ldsigma; e.c2 = -1.0;
+      }
+      gemm(c, true, false, q, q, n_local, R, ldn, R, ldn, e, SYM_LOWER | SYM_MIRROR);
+    }
+    // a5: GradT = (2/n) X^T E   (or 2 S_xy + (2/sqrt n) X^T R)
+    if (GradT) {
+      Epilogue e; e.out1 = static_cast<double*>(GradT); e.ld1 = ldgt;
+      if (!Sxy) {
+        e.a1 = 2.0 / (double)n_total;
+        gemm(c, true, false, p, q, n_local, Xd, ldx, E, ldn, e, 0);
+      } else {
+        e.a1 = 2.0 / std::sqrt((double)n_total);
+        e.in1a = static_cast<const double*>(Sxy); e.ld1a = ldsxy; e.b1 = 2.0;
+        gemm(c, true, false, p, q, n_local, Xd, ldx, R, ldn, e, 0);
+      }
+    }
+    if (fused)
+      active_impl(c, p, q, static_cast<const double*>(GradL), ldgl, static_cast<const double*>(GradT), ldgt, Lambda,
+                  Theta, fused);
+  });
+}
+
+cggm_status cggm_grad_lambda(cggm_ctx* ctx, int64_t q, const void* Syy, int64_t ldsyy, const void* Sigma,
+                             int64_t ldsigma, const void* Psi, int64_t ldpsi, void* GradL, int64_t ldgl) {
+  return guard(ctx, [&](Ctx* c) {
+    check_ctx_dtype(c);
+    if (q < 0) fail(CGGM_ERR_INVALID_ARG, "negative dimension");
+    check_dense("Syy", Syy, q, q, ldsyy);
+    check_dense("Sigma", Sigma, q, q, ldsigma);
+    check_dense("Psi", Psi, q, q, ldpsi);
+    check_dense("GradL", GradL, q, q, ldgl);
+    grad_lambda(c, q, static_cast<const double*>(Syy), ldsyy, static_cast<const double*>(Sigma), ldsigma,
+                static_cast<const double*>(Psi), ldpsi, static_cast<double*>(GradL), ldgl);
+  });
+}
+
+// ------------------------------------------------------------------ a7
+cggm_status cggm_objective(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64_t p, int64_t q, const void* X,
+                           int64_t ldx, const void* Y, int64_t ldy, const cggm_csc* Lambda, const cggm_csc* Theta,
+                           double lam_L, double lam_T, int32_t penalize_diag, const void* W, int64_t ldw,
+                           cggm_objective_out* out) {
+  return guard(ctx, [&](Ctx* c) {
+    check_ctx_dtype(c);
+    if (!out) fail(CGGM_ERR_INVALID_ARG, "null cggm_objective_out");
+    if (n_local < 0 || p < 0 || q < 0) fail(CGGM_ERR_INVALID_ARG, "negative dimension");
+    if (n_total < 1 || n_total < n_local) fail(CGGM_ERR_INVALID_ARG, "n_total must be >= max(1, n_local)");
+    if (!(lam_L >= 0.0) || !(lam_T >= 0.0)) fail(CGGM_ERR_INVALID_ARG, "negative lambda");
+    check_dense("Y", Y, n_local, q, ldy);
+    check_csc_host("Lambda", Lambda, q, q);
+    check_csc_host("Theta", Theta, p, q);
+    if (W) check_dense("W", W, n_local, q, ldw);
+    else check_dense("X", X, n_local, p, ldx);
+    std::memset(out, 0, sizeof(*out));
+    if (q == 0) {
+      out->is_pd = 1; out->fail_col = -1;
+      return;
+    }
+    validate_csc_dev(c, Lambda, true, "Lambda");
+    validate_csc_dev(c, Theta, false, "Theta");
+    const int64_t ldn = even(n_local > 0 ? n_local : 1);
+    const int64_t lda = even(q);
+    const int nb = leaf_nb();
+    const int64_t nleaves = (q + nb - 1) / nb;
+    const double* Yd = static_cast<const double*>(Y);
+    // W = X Theta (or caller's W), Z := W (to be solved in place)
+    const double* Wd;
+    int64_t ldwd;
+    double* Z = static_cast<double*>(ws_get(c, WS_Z, (size_t)ldn * q * 8));
+    if (W) {
+      Wd = static_cast<const double*>(W);
+      ldwd = ldw;
+    } else {
+      double* Wb = static_cast<double*>(ws_get(c, WS_W, (size_t)ldn * q * 8));
+      spmm_x_theta(c, static_cast<const double*>(X), ldx, n_local, Theta, View{Wb, ldn, n_local, q});
+      Wd = Wb;
+      ldwd = ldn;
+    }
+    copy2d(c, View{Z, ldn, n_local, q}, Wd, ldwd);
+    // Cholesky of the trial Lambda (the PD test), leaf inverses kept for the triangular solve
+    double* A = static_cast<double*>(ws_get(c, WS_DENSE_A, (size_t)lda * q * 8));
+    double* leafinv = static_cast<double*>(ws_get(c, WS_LEAFINV, (size_t)nleaves * nb * nb * 8));
+    Scal s = scal(c, 16 + 6 * q + nleaves);
+    double* res = s.dbl;            // [0..5] sums, [8] logdet
+    double* partY = s.dbl + 16;
+    double* partWY = partY + q;
+    double* partZ = partWY + q;
+    double* penLp = partZ + q;
+    double* penTp = penLp + q;
+    double* slots = penTp + q;
+    View Av{A, lda, q, q};
+    densify_csc(c, Lambda, Av);
+    init_scalars(c, s.fail, s.flag);
+    potrf_recursive(c, Av, View{nullptr, lda, q, q}, false, leafinv, slots, s.fail, nullptr, 0);
+    // Z = W L^{-T}:  ||Z||_F^2 = tr(Lambda^{-1} W^T W)  (reading A14)
+    trsm_right_lt(c, View{Z, ldn, n_local, q}, Av, leafinv, 0);
+    col_partials(c, 0, n_local, q, Yd, ldy, nullptr, 0, Lambda, partY);
+    col_partials(c, 1, n_local, q, Wd, ldwd, Yd, ldy, nullptr, partWY);
+    col_partials(c, 2, n_local, q, Z, ldn, nullptr, 0, nullptr, partZ);
+    csc_abs_partials(c, Lambda, penalize_diag == 0, penLp);
+    csc_abs_partials(c, Theta, false, penTp);
+    sum_arrays_1(c, partY, q, res + 0);
+    sum_arrays_1(c, partWY, q, res + 1);
+    sum_arrays_1(c, partZ, q, res + 2);
+    sum_arrays_1(c, penLp, q, res + 3);
+    sum_arrays_1(c, penTp, q, res + 4);
+    CholResult cr;
+    finish_chol(c, s, slots, nleaves, res + 8, &cr);
+    double h[6];
+    CGGM_CUDA_CHECK(cudaMemcpyAsync(c->host_scratch, res, 5 * 8, cudaMemcpyDeviceToHost, c->stream));
+    CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    std::memcpy(h, c->host_scratch, 5 * 8);
+    const double nt = (double)n_total;
+    out->pen_L = lam_L * h[3];
+    out->pen_T = lam_T * h[4];
+    out->is_pd = cr.is_pd;
+    out->fail_col = cr.fail_col;
+    if (cr.is_pd) {
+      out->logdet = cr.logdet;
+      out->tr_syy_lam = h[0] / nt;
+      out->tr_sxy_theta = h[1] / nt;
+      out->tr_sigma_m = h[2] / nt;
+      out->g = -out->logdet + out->tr_syy_lam + 2.0 * out->tr_sxy_theta + out->tr_sigma_m;
+      out->f = out->g + out->pen_L + out->pen_T;
+    } else {
+      const double nan = std::numeric_limits<double>::quiet_NaN();
+      out->logdet = nan;
+      out->tr_syy_lam = h[0] / nt;
+      out->tr_sxy_theta = h[1] / nt;
+      out->tr_sigma_m = nan;
+      out->g = INFINITY;
+      out->f = INFINITY;
+    }
+  });
+}
+
+}  // extern "C"
+
+extern "C" cggm_status cggm_test_gemm(cggm_ctx* ctx, int transA, int transB, int64_t M, int64_t N, int64_t K,
+                                      const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                                      int64_t ldc, double alpha, double beta, int flags) {
+  return guard(ctx, [&](Ctx* c) {
+    if (M < 0 || N < 0 || K < 0) fail(CGGM_ERR_INVALID_ARG, "negative dimension");
+    Epilogue e;
+    e.out1 = C; e.ld1 = ldc; e.a1 = alpha;
+    if (beta != 0.0) { e.in1a = C; e.ld1a = ldc; e.b1 = beta; }
+    gemm(c, transA != 0, transB != 0, M, N, K, A, lda, B, ldb, e, flags);
+  });
+}

@@ -1,0 +1,202 @@
+// Shared internals of libcggm: context, workspace, launch accounting, PTX helpers
+// (mbarrier, TMA, DMMA) for sm_100a.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/cggm.h"
+
+namespace cggm {
+
+// ------------------------------------------------------------------ context
+struct Buffer {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+struct Ctx {
+  int device = 0;
+  cggm_dtype dtype = CGGM_F64;
+  cudaStream_t stream = nullptr;
+  int validate = 1;
+  int64_t launches = 0;
+  std::string last_error;
+  // named workspace slots (grown on demand, never shrunk until release)
+  std::vector<Buffer> slots;
+  // pinned host scratch for scalar read-back
+  void* host_scratch = nullptr;
+  PFN_cuTensorMapEncodeTiled_v12000 encode_tiled = nullptr;
+  int num_sms = 148;
+};
+
+enum Slot {
+  WS_DENSE_A = 0,   // dense Lambda -> Cholesky factor (q x q)
+  WS_LINV,          // L^{-1} (q x q)
+  WS_TMP,           // recursion temporaries
+  WS_LEAFINV,       // compact leaf inverses (potrf-only mode)
+  WS_W,             // W = X Theta (n x q)
+  WS_R,             // R (n x q)
+  WS_E,             // E (n x q)
+  WS_Z,             // trsm result (n x q)
+  WS_SCAL,          // small device scalars / partial-sum arrays
+  WS_ACT,           // active-set per-column arrays
+  WS_PACK0,         // packing for TMA-incompatible operands
+  WS_PACK1,
+  WS_PACK2,
+  WS_NUM
+};
+
+void* ws_get(Ctx* c, int slot, size_t bytes);  // throws CudaError on OOM
+
+struct CudaError {
+  cggm_status code;
+  std::string msg;
+};
+
+#define CGGM_CUDA_CHECK(expr)                                                                  \
+  do {                                                                                         \
+    cudaError_t _e = (expr);                                                                   \
+    if (_e != cudaSuccess)                                                                     \
+      throw ::cggm::CudaError{CGGM_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)}; \
+  } while (0)
+
+// After every launch: count it and surface launch errors.
+inline void post_launch(Ctx* c, const char* what) {
+  c->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw CudaError{CGGM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+// ------------------------------------------------------------------ dense views
+struct View {
+  double* p;
+  int64_t ld;
+  int64_t rows, cols;
+  __host__ __device__ double* at(int64_t i, int64_t j) const { return p + i + j * ld; }
+  View sub(int64_t r0, int64_t c0, int64_t nr, int64_t nc) const { return View{p + r0 + c0 * ld, ld, nr, nc}; }
+};
+
+// ------------------------------------------------------------------ GEMM interface (gemm.cu)
+enum GemmFlags : int {
+  A_KLE_M = 1,          // op(A)[m][k] == 0 for k > m  -> k range ends at the tile's last m
+  A_KGE_M = 2,          // op(A)[m][k] == 0 for k < m  -> k range starts at the tile's first m
+  B_KLE_N = 4,          // op(B)[k][n] == 0 for k > n
+  B_KGE_N = 8,          // op(B)[k][n] == 0 for k < n
+  SYM_LOWER = 16,       // M == N: compute only tiles I >= J; diagonal tiles write m >= n only
+  SYM_MIRROR = 32,      // with SYM_LOWER: also write every value at its transposed position
+};
+
+struct Epilogue {
+  // out1 = a1*acc + b1*in1a + c1*in1b ; out2 = a2*acc + b2*in2a + c2*in2b (null pointers skip terms)
+  double* out1 = nullptr; int64_t ld1 = 0; double a1 = 1.0;
+  const double* in1a = nullptr; int64_t ld1a = 0; double b1 = 0.0;
+  const double* in1b = nullptr; int64_t ld1b = 0; double c1 = 0.0;
+  double* out2 = nullptr; int64_t ld2 = 0; double a2 = 1.0;
+  const double* in2a = nullptr; int64_t ld2a = 0; double b2 = 0.0;
+  const double* in2b = nullptr; int64_t ld2b = 0; double c2 = 0.0;
+};
+
+// C(M x N) epilogue(op(A) op(B)), op(A) = A (transA=false, A is M x K) or A^T (A is K x M).
+// op(B) = B (transB=false, B is K x N) or B^T (B is N x K).  Column-major, FP64 DMMA.
+void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K,
+          const double* A, int64_t lda, const double* B, int64_t ldb, const Epilogue& epi, int flags);
+
+// ------------------------------------------------------------------ Cholesky family (chol.cu)
+// In-place blocked recursive Cholesky of the lower triangle of A (q x q).
+//  full_inverse = true : Linv (q x q, lower, zero upper) receives L^{-1}; A's L21 blocks are not kept.
+//  full_inverse = false: A's lower triangle receives L; leaf inverses go to the compact buffer.
+// logdet/fail are accumulated on the device (see chol.cu).
+struct CholResult {
+  double logdet;
+  int is_pd;
+  int64_t fail_col;
+};
+void potrf_recursive(Ctx* c, View A, View Linv, bool full_inverse, double* leafinv, double* logdet_slots,
+                     int* fail_col_dev, double* tmp, size_t tmp_elems);
+// B (m x n) := B L^{-T} for the lower-triangular factor L (n x n) using compact leaf inverses.
+void trsm_right_lt(Ctx* c, View B, View L, const double* leafinv, int64_t col0);
+// Sigma = Linv^T Linv (full symmetric).
+void lauum(Ctx* c, View Linv, View Sigma);
+int leaf_nb();
+
+// ------------------------------------------------------------------ streaming kernels (stream.cu)
+void densify_csc(Ctx* c, const cggm_csc* A, View D);
+void spmm_x_theta(Ctx* c, const double* X, int64_t ldx, int64_t n, const cggm_csc* Theta, View W);
+void check_csc(Ctx* c, const cggm_csc* A, bool symmetric, int* flag_dev);
+void grad_lambda(Ctx* c, int64_t q, const double* Syy, int64_t l1, const double* Sigma, int64_t l2,
+                 const double* Psi, int64_t l3, double* G, int64_t l4);
+void copy2d(Ctx* c, View dst, const double* src, int64_t lds);
+
+}  // namespace cggm
+
+// ------------------------------------------------------------------ PTX helpers (device)
+namespace cggm {
+namespace ptx {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// D(8x8) += A(8x4, row) * B(4x8, col), FP64 tensor pipe (SASS DMMA.8x8x4 on sm_100a).
+// Lane (g = lane>>2, t = lane&3) holds A[g][t], B[t][g], C[g][2t], C[g][2t+1].
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void lds128(double& x, double& y, uint32_t addr) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(x), "=d"(y) : "r"(addr));
+}
+
+}  // namespace ptx
+}  // namespace cggm

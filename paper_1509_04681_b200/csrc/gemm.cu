@@ -1,0 +1,341 @@
+// FP64 tensor-pipe GEMM for sm_100a: TMA (128B swizzle) -> shared memory ring with mbarrier
+// full/empty pipeline -> mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4, the only FP64 tensor op on
+// sm_100a; tcgen05 has no f64 kind).  One producer warp issues TMA, 8 consumer warps run a
+// 128x128 CTA tile (warp tile 64x32).  Triangular operands shrink the k-range per tile
+// (flags), symmetric outputs compute only lower tiles and mirror bit-identically.
+//
+// Used for every dense contraction of the hot path: S_yy = Y^T Y/n,
+// S_xy = X^T Y/n, W Sigma, Psi = R^T R, X^T E (Eq. 3 via I3), and
+// the blocked Cholesky / triangular-inverse / Sigma = L^{-T} L^{-1} updates.
+//
+// Shared-memory layouts (both operands, per stage, 16 KB each):
+//  K-inner  (operand stored with k contiguous): 128 rows (x) x 128 B (16 k), TMA box {16,128}.
+//  MN-inner (operand stored with x contiguous): 8 boxes {16 x, 16 k}, each 16 rows (k) x 128 B.
+// TMA SWIZZLE_128B XORs the 16-byte chunk index with (row & 7).  The fragment mapping below
+// is chosen so that every LDS.128 of a quarter-warp hits 8 distinct chunks (conflict-free):
+//  k inside a 16-wide k tile: step (kk, s), lane t  ->  k = 8*kk + 2*t + s     (both operands)
+//  MN-inner fragment pair p, element e, lane g     ->  x = 16*p + 2*g + e
+//  K-inner fragment f, lane g                       ->  x = 8*f + (g>>1) + 4*(g&1)
+// The epilogue inverts the same maps.
+#include "common.cuh"
+
+namespace cggm {
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 16;
+constexpr int NCW = 8;                       // consumer warps (thread 0 also issues TMA)
+constexpr int NTHREADS = NCW * 32;
+constexpr int STAGES = 4;
+constexpr int OP_BYTES = BM * BK * 8;        // 16 KB per operand per stage
+constexpr int STAGE_BYTES = 2 * OP_BYTES;
+constexpr int EPI_LD = BM + 1;
+constexpr int EPI_BYTES = BN * EPI_LD * 8;
+constexpr int MAIN_BYTES = STAGES * STAGE_BYTES;
+constexpr int DATA_BYTES = MAIN_BYTES > EPI_BYTES ? MAIN_BYTES : EPI_BYTES;
+constexpr int SMEM_BYTES = DATA_BYTES + 1024 + 2 * STAGES * 8;
+constexpr int GROUP_N = 8;
+
+struct KParams {
+  int M, N, K;
+  int tilesM, tilesN;
+  int flags;
+  Epilogue epi;
+};
+
+__device__ __forceinline__ void tile_coords(const KParams& P, int t, int& I, int& J) {
+  if (P.flags & SYM_LOWER) {
+    int i = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+    while ((long long)(i + 1) * (i + 2) / 2 <= t) ++i;
+    while ((long long)i * (i + 1) / 2 > t) --i;
+    I = i;
+    J = t - (int)((long long)i * (i + 1) / 2);
+  } else {
+    const int per_group = GROUP_N * P.tilesM;
+    const int gi = t / per_group;
+    const int local = t - gi * per_group;
+    const int nb0 = gi * GROUP_N;
+    const int width = min(GROUP_N, P.tilesN - nb0);
+    I = local / width;
+    J = nb0 + local % width;
+  }
+}
+
+__device__ __forceinline__ void epi_apply(const Epilogue& E, int64_t r, int64_t c, double v) {
+  if (E.out1) {
+    double o = __dmul_rn(E.a1, v);
+    if (E.in1a) o = __dadd_rn(o, __dmul_rn(E.b1, E.in1a[r + c * E.ld1a]));
+    if (E.in1b) o = __dadd_rn(o, __dmul_rn(E.c1, E.in1b[r + c * E.ld1b]));
+    E.out1[r + c * E.ld1] = o;
+  }
+  if (E.out2) {
+    double o = __dmul_rn(E.a2, v);
+    if (E.in2a) o = __dadd_rn(o, __dmul_rn(E.b2, E.in2a[r + c * E.ld2a]));
+    if (E.in2b) o = __dadd_rn(o, __dmul_rn(E.c2, E.in2b[r + c * E.ld2b]));
+    E.out2[r + c * E.ld2] = o;
+  }
+}
+
+// x offset (within the warp's 64/32-wide slab) of fragment f, fragment row/col index r
+template <bool KINNER>
+__device__ __forceinline__ int frag_x(int f, int r) {
+  if (KINNER) return 8 * f + (r >> 1) + 4 * (r & 1);
+  return 16 * (f >> 1) + 2 * r + (f & 1);
+}
+
+template <bool AK, bool BKI>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    gemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const KParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + DATA_BYTES);
+  uint64_t* empty = full + STAGES;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int I, J;
+  tile_coords(P, blockIdx.x, I, J);
+  const int m0 = I * BM, n0 = J * BN;
+
+  int kbeg = 0, kend = P.K;
+  if (P.flags & A_KGE_M) kbeg = max(kbeg, m0);
+  if (P.flags & B_KGE_N) kbeg = max(kbeg, n0);
+  if (P.flags & A_KLE_M) kend = min(kend, m0 + BM);
+  if (P.flags & B_KLE_N) kend = min(kend, n0 + BN);
+  const int kt0 = kbeg / BK;
+  const int nkt = kend > kbeg ? (kend - kt0 * BK + BK - 1) / BK : 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], NCW);
+    }
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+
+  double acc[8][4][2];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp >> 2, wn = warp & 3;
+
+  // ------------------------------------------------ TMA producer: thread 0, STAGES-1 tiles ahead
+  uint32_t tx_bytes = 0;
+  if (threadIdx.x == 0 && nkt > 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+  }
+  int a_boxes = 0, b_boxes = 0;
+  if (!AK)
+    for (int xb = 0; xb < BM / 16; ++xb) a_boxes += (m0 + xb * 16 < P.M);
+  if (!BKI)
+    for (int xb = 0; xb < BN / 16; ++xb) b_boxes += (n0 + xb * 16 < P.N);
+  tx_bytes = (AK ? OP_BYTES : a_boxes * 2048) + (BKI ? OP_BYTES : b_boxes * 2048);
+  auto issue = [&](int i) {
+    const int s = i % STAGES;
+    uint8_t* sa = smem + s * STAGE_BYTES;
+    uint8_t* sb = sa + OP_BYTES;
+    ptx::mbar_arrive_expect_tx(&full[s], tx_bytes);
+    const int k = (kt0 + i) * BK;
+    if (AK) {
+      ptx::tma_load_2d(sa, &tmA, &full[s], k, m0);
+    } else {
+      for (int xb = 0; xb < a_boxes; ++xb) ptx::tma_load_2d(sa + xb * 2048, &tmA, &full[s], m0 + xb * 16, k);
+    }
+    if (BKI) {
+      ptx::tma_load_2d(sb, &tmB, &full[s], k, n0);
+    } else {
+      for (int xb = 0; xb < b_boxes; ++xb) ptx::tma_load_2d(sb + xb * 2048, &tmB, &full[s], n0 + xb * 16, k);
+    }
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < STAGES - 1 && i < nkt; ++i) issue(i);
+  {
+    // ------------------------------------------------ DMMA consumers
+    for (int i = 0; i < nkt; ++i) {
+      const int s = i % STAGES;
+      ptx::mbar_wait(&full[s], (i / STAGES) & 1);
+      const uint32_t sa = ptx::smem_u32(smem + s * STAGE_BYTES);
+      const uint32_t sb = sa + OP_BYTES;
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        double a[8][2], b[4][2];
+        if (AK) {
+#pragma unroll
+          for (int f = 0; f < 8; ++f) {
+            const int x = wm * 64 + frag_x<true>(f, g);
+            const int chunk = (4 * kk + t) ^ (x & 7);
+            ptx::lds128(a[f][0], a[f][1], sa + x * 128 + chunk * 16);
+          }
+        } else {
+#pragma unroll
+          for (int pr = 0; pr < 4; ++pr) {
+            const int xb = wm * 4 + pr;
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+              const int k = 8 * kk + 2 * t + s2;
+              const int chunk = g ^ (k & 7);
+              ptx::lds128(a[2 * pr][s2], a[2 * pr + 1][s2], sa + xb * 2048 + k * 128 + chunk * 16);
+            }
+          }
+        }
+        if (BKI) {
+#pragma unroll
+          for (int f = 0; f < 4; ++f) {
+            const int x = wn * 32 + frag_x<true>(f, g);
+            const int chunk = (4 * kk + t) ^ (x & 7);
+            ptx::lds128(b[f][0], b[f][1], sb + x * 128 + chunk * 16);
+          }
+        } else {
+#pragma unroll
+          for (int pr = 0; pr < 2; ++pr) {
+            const int xb = wn * 2 + pr;
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+              const int k = 8 * kk + 2 * t + s2;
+              const int chunk = g ^ (k & 7);
+              ptx::lds128(b[2 * pr][s2], b[2 * pr + 1][s2], sb + xb * 2048 + k * 128 + chunk * 16);
+            }
+          }
+        }
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+          for (int fm = 0; fm < 8; ++fm)
+#pragma unroll
+            for (int fn = 0; fn < 4; ++fn) ptx::dmma_8x8x4(acc[fm][fn][0], acc[fm][fn][1], a[fm][s2], b[fn][s2]);
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&empty[s]);
+      if (threadIdx.x == 0) {
+        const int j = i + STAGES - 1;
+        if (j < nkt) {
+          if (j >= STAGES) ptx::mbar_wait(&empty[j % STAGES], ((j / STAGES) & 1) ^ 1);
+          issue(j);
+        }
+      }
+    }
+  }
+
+  // ------------------------------------------------ epilogue through shared memory
+  __syncthreads();
+  double* Cs = reinterpret_cast<double*>(smem);
+  {
+#pragma unroll
+    for (int fm = 0; fm < 8; ++fm) {
+      const int ml = wm * 64 + frag_x<AK>(fm, g);
+#pragma unroll
+      for (int fn = 0; fn < 4; ++fn)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int nl = wn * 32 + frag_x<BKI>(fn, 2 * t + j);
+          Cs[nl * EPI_LD + ml] = acc[fm][fn][j];
+        }
+    }
+  }
+  __syncthreads();
+  const bool diag = (P.flags & SYM_LOWER) && I == J;
+  for (int idx = threadIdx.x; idx < BM * BN; idx += NTHREADS) {
+    const int ml = idx & (BM - 1), nl = idx >> 7;
+    const int m = m0 + ml, n = n0 + nl;
+    if (m >= P.M || n >= P.N) continue;
+    if (diag && m < n) continue;
+    epi_apply(P.epi, m, n, Cs[nl * EPI_LD + ml]);
+  }
+  if (P.flags & SYM_MIRROR) {
+    for (int idx = threadIdx.x; idx < BM * BN; idx += NTHREADS) {
+      const int nl = idx & (BN - 1), ml = idx >> 7;
+      const int m = m0 + ml, n = n0 + nl;
+      if (m >= P.M || n >= P.N) continue;
+      if (diag && m <= n) continue;
+      epi_apply(P.epi, n, m, Cs[nl * EPI_LD + ml]);
+    }
+  }
+}
+
+CUtensorMap make_map(Ctx* c, const double* ptr, int64_t ld, int64_t inner, int64_t outer, uint32_t box_inner,
+                     uint32_t box_outer) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 8)};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = c->encode_tiled(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(ptr), dims, strides, box,
+                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw CudaError{CGGM_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"};
+  return m;
+}
+
+template <bool AK, bool BKI>
+void launch(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KParams& P, int grid) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    CGGM_CUDA_CHECK(cudaFuncSetAttribute(gemm_dmma_kernel<AK, BKI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         SMEM_BYTES));
+    attr_set = true;
+  }
+  gemm_dmma_kernel<AK, BKI><<<grid, NTHREADS, SMEM_BYTES, c->stream>>>(ma, mb, P);
+  post_launch(c, "gemm_dmma_kernel");
+}
+
+bool tma_ok(const double* p, int64_t ld) {
+  return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && (ld % 2 == 0);
+}
+
+}  // namespace
+
+void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+          const double* B, int64_t ldb, const Epilogue& epi, int flags) {
+  if (M <= 0 || N <= 0) return;
+  if (M > (1LL << 30) || N > (1LL << 30) || K > (1LL << 30))
+    throw CudaError{CGGM_ERR_UNSUPPORTED, "gemm dimension too large"};
+  static double* dummy = nullptr;
+  if (K <= 0) {
+    if (!dummy) CGGM_CUDA_CHECK(cudaMalloc(&dummy, 16 * 16 * 8));
+    A = dummy; B = dummy; lda = 16; ldb = 16;
+  }
+  const int64_t Keff = K > 0 ? K : 1;
+  // operands not meeting TMA constraints (16-B base, even ld) are packed
+  const int64_t arows = transA ? Keff : M, acols = transA ? M : Keff;
+  const int64_t brows = transB ? N : Keff, bcols = transB ? Keff : N;
+  if (K > 0 && !tma_ok(A, lda)) {
+    int64_t ld = (arows + 1) & ~int64_t(1);
+    double* pk = static_cast<double*>(ws_get(c, WS_PACK0, (size_t)ld * acols * 8));
+    CGGM_CUDA_CHECK(cudaMemcpy2DAsync(pk, ld * 8, A, lda * 8, arows * 8, acols, cudaMemcpyDeviceToDevice, c->stream));
+    A = pk; lda = ld;
+  }
+  if (K > 0 && !tma_ok(B, ldb)) {
+    int64_t ld = (brows + 1) & ~int64_t(1);
+    double* pk = static_cast<double*>(ws_get(c, WS_PACK1, (size_t)ld * bcols * 8));
+    CGGM_CUDA_CHECK(cudaMemcpy2DAsync(pk, ld * 8, B, ldb * 8, brows * 8, bcols, cudaMemcpyDeviceToDevice, c->stream));
+    B = pk; ldb = ld;
+  }
+  KParams P;
+  P.M = (int)M; P.N = (int)N; P.K = (int)(K > 0 ? K : 0);
+  P.tilesM = (int)((M + BM - 1) / BM);
+  P.tilesN = (int)((N + BN - 1) / BN);
+  P.flags = flags;
+  P.epi = epi;
+  int grid;
+  if (flags & SYM_LOWER) {
+    if (M != N) throw CudaError{CGGM_ERR_SHAPE, "SYM_LOWER gemm needs M == N"};
+    grid = P.tilesM * (P.tilesM + 1) / 2;
+  } else {
+    grid = P.tilesM * P.tilesN;
+  }
+  // K-inner operand: dims {K, X}, box {16, 128}; MN-inner: dims {X, K}, box {16, 16}
+  CUtensorMap ma = transA ? make_map(c, A, lda, Keff, M, 16, BM) : make_map(c, A, lda, M, Keff, 16, 16);
+  CUtensorMap mb = transB ? make_map(c, B, ldb, N, Keff, 16, 16) : make_map(c, B, ldb, Keff, N, 16, BN);
+  const bool AK = transA, BKI = !transB;
+  if (AK && BKI) launch<true, true>(c, ma, mb, P, grid);
+  else if (AK && !BKI) launch<true, false>(c, ma, mb, P, grid);
+  else if (!AK && BKI) launch<false, true>(c, ma, mb, P, grid);
+  else launch<false, false>(c, ma, mb, P, grid);
+}
+
+}  // namespace cggm

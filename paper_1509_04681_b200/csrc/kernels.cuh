@@ -1,0 +1,31 @@
+// Launch wrappers shared between translation units (reductions, active sets).
+#pragma once
+#include <climits>
+
+#include "common.cuh"
+
+namespace cggm {
+
+void col_partials(Ctx* c, int mode, int64_t n, int64_t ncols, const double* A, int64_t lda, const double* B,
+                  int64_t ldb, const cggm_csc* csc, double* part);
+void csc_abs_partials(Ctx* c, const cggm_csc* A, bool skip_diag, double* part);
+void sum_arrays(Ctx* c, int count, const double* const* arrs_dev, const int64_t* lens_dev, double* out_dev);
+void init_scalars(Ctx* c, int* fail_col, int* flag);
+void sum_arrays_1(Ctx* c, const double* a, int64_t len, double* out_dev);
+
+// Active sets (active.cu).  Device result block layout (int64 / double):
+struct ActTotals {
+  long long m_L, m_T, ties_L, ties_T;
+  double sub_L, sub_T;
+};
+// Count pass + scan: fills totals_dev and per-column offsets (device).
+void active_count(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t ldgl, const double* GradT, int64_t ldgt,
+                  const cggm_csc* Lambda, const cggm_csc* Theta, double lam_L, double lam_T, int penalize_diag,
+                  double tie_eps, ActTotals* totals_dev, long long* offL, long long* offT, long long* cntL,
+                  long long* cntT, long long* tieL, long long* tieT, double* subL, double* subT);
+void active_write(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t ldgl, const double* GradT, int64_t ldgt,
+                  const cggm_csc* Lambda, const cggm_csc* Theta, double lam_L, double lam_T, int penalize_diag,
+                  const long long* offL, const long long* offT, int32_t* L_row, int32_t* L_col, int32_t* T_row,
+                  int32_t* T_col);
+
+}  // namespace cggm

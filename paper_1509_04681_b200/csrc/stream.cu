@@ -1,0 +1,265 @@
+// HBM-bound kernels of the hot path: CSC densify (K00), SpMM W = X Theta (K05),
+// CSC structure / symmetry checks, the elementwise grad_Lambda = S_yy - Sigma - Psi (Eq. 3),
+// and the deterministic per-column partial sums used by the objective (K08, Eq. 1).
+// All reductions are two-level with a fixed order (per-column partials, then one CTA), so
+// every scalar is bitwise reproducible run to run.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace cggm {
+
+// ------------------------------------------------------------------ densify CSC -> dense
+__global__ void k_scatter_csc(const int64_t* colptr, const int32_t* rowidx, const double* val, int64_t ncols,
+                              double* D, int64_t ldd) {
+  const int64_t j = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x / 32);
+  if (j >= ncols) return;
+  const int lane = threadIdx.x & 31;
+  for (int64_t t = colptr[j] + lane; t < colptr[j + 1]; t += 32) D[rowidx[t] + j * ldd] = val[t];
+}
+
+void densify_csc(Ctx* c, const cggm_csc* A, View D) {
+  CGGM_CUDA_CHECK(cudaMemset2DAsync(D.p, D.ld * 8, 0, D.rows * 8, D.cols, c->stream));
+  if (A->ncols == 0 || A->nnz == 0) return;
+  const int wpb = 8;
+  const int64_t grid = (A->ncols + wpb - 1) / wpb;
+  k_scatter_csc<<<(unsigned)grid, wpb * 32, 0, c->stream>>>(A->colptr, A->rowidx, static_cast<const double*>(A->val),
+                                                            A->ncols, D.p, D.ld);
+  post_launch(c, "k_scatter_csc");
+}
+
+// ------------------------------------------------------------------ W = X Theta
+// One CTA per output column j: W[:, j] = sum_t Theta_{row_t j} X[:, row_t] (ascending t).
+__global__ void __launch_bounds__(256) k_spmm_x_theta(const double* __restrict__ X, int64_t ldx, int64_t n,
+                                                      const int64_t* __restrict__ colptr,
+                                                      const int32_t* __restrict__ rowidx,
+                                                      const double* __restrict__ val, double* __restrict__ W,
+                                                      int64_t ldw) {
+  __shared__ int32_t rows[256];
+  __shared__ double vals[256];
+  const int64_t j = blockIdx.x;
+  const int64_t a = colptr[j], b = colptr[j + 1];
+  // each thread owns rows k = tid, tid+256, ... (up to 8 register accumulators per pass)
+  for (int64_t k0 = 0; k0 < n; k0 += 256 * 8) {
+    double acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+    for (int64_t t0 = a; t0 < b; t0 += 256) {
+      const int cnt = (int)((b - t0) < 256 ? (b - t0) : 256);
+      __syncthreads();
+      if (threadIdx.x < cnt) {
+        rows[threadIdx.x] = rowidx[t0 + threadIdx.x];
+        vals[threadIdx.x] = val[t0 + threadIdx.x];
+      }
+      __syncthreads();
+      for (int e = 0; e < cnt; ++e) {
+        const double v = vals[e];
+        const double* xc = X + (int64_t)rows[e] * ldx;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int64_t k = k0 + threadIdx.x + u * 256;
+          if (k < n) acc[u] = fma(v, __ldg(xc + k), acc[u]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t k = k0 + threadIdx.x + u * 256;
+      if (k < n) W[k + j * ldw] = acc[u];
+    }
+  }
+}
+
+void spmm_x_theta(Ctx* c, const double* X, int64_t ldx, int64_t n, const cggm_csc* Theta, View W) {
+  if (Theta->ncols == 0 || n == 0) return;
+  k_spmm_x_theta<<<(unsigned)Theta->ncols, 256, 0, c->stream>>>(X, ldx, n, Theta->colptr, Theta->rowidx,
+                                                                static_cast<const double*>(Theta->val), W.p, W.ld);
+  post_launch(c, "k_spmm_x_theta");
+}
+
+// ------------------------------------------------------------------ CSC checks
+// flag bits: 1 = colptr not monotone / bad ends, 2 = row out of range or not strictly increasing,
+//            4 = not symmetric (symmetric mode)
+__global__ void k_check_csc(const int64_t* colptr, const int32_t* rowidx, const double* val, int64_t nrows,
+                            int64_t ncols, int64_t nnz, int symmetric, int* flag) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j == 0 && (colptr[0] != 0 || colptr[ncols] != nnz)) atomicOr(flag, 1);
+  if (j >= ncols) return;
+  const int64_t a = colptr[j], b = colptr[j + 1];
+  if (a > b || a < 0 || b > nnz) {
+    atomicOr(flag, 1);
+    return;
+  }
+  int32_t prev = -1;
+  for (int64_t t = a; t < b; ++t) {
+    const int32_t r = rowidx[t];
+    if (r <= prev || r < 0 || r >= nrows) {
+      atomicOr(flag, 2);
+      return;
+    }
+    prev = r;
+    if (symmetric) {
+      // find (j, r): row j in column r, by binary search
+      int64_t lo = colptr[r], hi = colptr[r + 1] - 1;
+      bool found = false;
+      while (lo <= hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        const int32_t rm = rowidx[mid];
+        if (rm == j) {
+          found = (val[mid] == val[t]);
+          break;
+        }
+        if (rm < j) lo = mid + 1;
+        else hi = mid - 1;
+      }
+      if (!found) atomicOr(flag, 4);
+    }
+  }
+}
+
+void check_csc(Ctx* c, const cggm_csc* A, bool symmetric, int* flag_dev) {
+  if (A->ncols == 0) return;
+  const int64_t grid = (A->ncols + 255) / 256;
+  k_check_csc<<<(unsigned)grid, 256, 0, c->stream>>>(A->colptr, A->rowidx, static_cast<const double*>(A->val),
+                                                     A->nrows, A->ncols, A->nnz, symmetric ? 1 : 0, flag_dev);
+  post_launch(c, "k_check_csc");
+}
+
+// ------------------------------------------------------------------ grad_Lambda elementwise
+__global__ void k_grad_lambda(int64_t q, const double* __restrict__ Syy, int64_t l1, const double* __restrict__ Sg,
+                              int64_t l2, const double* __restrict__ Psi, int64_t l3, double* __restrict__ G,
+                              int64_t l4) {
+  const int64_t j = blockIdx.y;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < q; i += (int64_t)gridDim.x * blockDim.x)
+    G[i + j * l4] = __dadd_rn(__dadd_rn(Syy[i + j * l1], -Sg[i + j * l2]), -Psi[i + j * l3]);
+}
+
+void grad_lambda(Ctx* c, int64_t q, const double* Syy, int64_t l1, const double* Sigma, int64_t l2,
+                 const double* Psi, int64_t l3, double* G, int64_t l4) {
+  if (q == 0) return;
+  dim3 grid((unsigned)std::min<int64_t>((q + 255) / 256, 64), (unsigned)q);
+  k_grad_lambda<<<grid, 256, 0, c->stream>>>(q, Syy, l1, Sigma, l2, Psi, l3, G, l4);
+  post_launch(c, "k_grad_lambda");
+}
+
+void copy2d(Ctx* c, View dst, const double* src, int64_t lds) {
+  if (dst.rows == 0 || dst.cols == 0) return;
+  CGGM_CUDA_CHECK(cudaMemcpy2DAsync(dst.p, dst.ld * 8, src, lds * 8, dst.rows * 8, dst.cols,
+                                    cudaMemcpyDeviceToDevice, c->stream));
+}
+
+// ------------------------------------------------------------------ deterministic block reduce
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  sh[threadIdx.x] = v;
+  __syncthreads();
+#pragma unroll
+  for (int s = NT / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] = sh[threadIdx.x] + sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  const double r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+// ------------------------------------------------------------------ objective column partials
+// mode 0: part[j] = sum_k Y[k,j] * (Y Lambda)[k,j]   (<Y, Y Lambda>, tr(S_yy Lambda) * n)
+// mode 1: part[j] = sum_k A[k,j] * B[k,j]           (<W, Y>)
+// mode 2: part[j] = sum_k A[k,j]^2                  (||Z||_F^2)
+__global__ void __launch_bounds__(256) k_col_partials(int mode, int64_t n, const double* __restrict__ A, int64_t lda,
+                                                      const double* __restrict__ B, int64_t ldb,
+                                                      const int64_t* __restrict__ colptr,
+                                                      const int32_t* __restrict__ rowidx,
+                                                      const double* __restrict__ val, double* part) {
+  __shared__ double sh[256];
+  const int64_t j = blockIdx.x;
+  double s = 0.0;
+  if (mode == 0) {
+    const int64_t a = colptr[j], b = colptr[j + 1];
+    for (int64_t k = threadIdx.x; k < n; k += 256) {
+      double yl = 0.0;
+      for (int64_t t = a; t < b; ++t) yl = fma(__ldg(A + k + (int64_t)rowidx[t] * lda), val[t], yl);
+      s = fma(__ldg(A + k + j * lda), yl, s);
+    }
+  } else if (mode == 1) {
+    for (int64_t k = threadIdx.x; k < n; k += 256) s = fma(A[k + j * lda], B[k + j * ldb], s);
+  } else {
+    for (int64_t k = threadIdx.x; k < n; k += 256) {
+      const double v = A[k + j * lda];
+      s = fma(v, v, s);
+    }
+  }
+  s = block_sum<256>(s, sh);
+  if (threadIdx.x == 0) part[j] = s;
+}
+
+// per-column sum |val| of a CSC (diagonal skipped when skip_diag)
+__global__ void k_csc_abs_partials(const int64_t* colptr, const int32_t* rowidx, const double* val, int64_t ncols,
+                                   int skip_diag, double* part) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= ncols) return;
+  double s = 0.0;
+  for (int64_t t = colptr[j]; t < colptr[j + 1]; ++t) {
+    if (skip_diag && rowidx[t] == j) continue;
+    s += fabs(val[t]);
+  }
+  part[j] = s;
+}
+
+// out[r] = sum_{i < len_r} arr_r[i], fixed order (one CTA per array)
+__global__ void __launch_bounds__(256) k_sum_arrays(const double* const* arrs, const int64_t* lens, double* out) {
+  __shared__ double sh[256];
+  const double* a = arrs[blockIdx.x];
+  const int64_t len = lens[blockIdx.x];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < len; i += 256) s += a[i];
+  s = block_sum<256>(s, sh);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+void col_partials(Ctx* c, int mode, int64_t n, int64_t ncols, const double* A, int64_t lda, const double* B,
+                  int64_t ldb, const cggm_csc* csc, double* part) {
+  if (ncols == 0) return;
+  k_col_partials<<<(unsigned)ncols, 256, 0, c->stream>>>(mode, n, A, lda, B, ldb, csc ? csc->colptr : nullptr,
+                                                         csc ? csc->rowidx : nullptr,
+                                                         csc ? static_cast<const double*>(csc->val) : nullptr, part);
+  post_launch(c, "k_col_partials");
+}
+
+void csc_abs_partials(Ctx* c, const cggm_csc* A, bool skip_diag, double* part) {
+  if (A->ncols == 0) return;
+  k_csc_abs_partials<<<(unsigned)((A->ncols + 255) / 256), 256, 0, c->stream>>>(
+      A->colptr, A->rowidx, static_cast<const double*>(A->val), A->ncols, skip_diag ? 1 : 0, part);
+  post_launch(c, "k_csc_abs_partials");
+}
+
+void sum_arrays(Ctx* c, int count, const double* const* arrs_dev, const int64_t* lens_dev, double* out_dev) {
+  k_sum_arrays<<<count, 256, 0, c->stream>>>(arrs_dev, lens_dev, out_dev);
+  post_launch(c, "k_sum_arrays");
+}
+
+// out = sum_{i < len} a[i], fixed order (one CTA)
+__global__ void __launch_bounds__(256) k_sum_vec(const double* a, int64_t len, double* out) {
+  __shared__ double sh[256];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < len; i += 256) s += a[i];
+  s = block_sum<256>(s, sh);
+  if (threadIdx.x == 0) *out = s;
+}
+
+void sum_arrays_1(Ctx* c, const double* a, int64_t len, double* out_dev) {
+  k_sum_vec<<<1, 256, 0, c->stream>>>(a, len, out_dev);
+  post_launch(c, "k_sum_vec");
+}
+
+__global__ void k_init_scalars(int* fail_col, int* flag) {
+  *fail_col = INT_MAX;
+  *flag = 0;
+}
+
+void init_scalars(Ctx* c, int* fail_col, int* flag) {
+  k_init_scalars<<<1, 1, 0, c->stream>>>(fail_col, flag);
+  post_launch(c, "k_init_scalars");
+}
+
+}  // namespace cggm

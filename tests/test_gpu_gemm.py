@@ -1,0 +1,118 @@
+"""FP64 DMMA GEMM engine vs a plain fp64 product (numpy), through the test-only export
+cggm_test_gemm (include/cggm_testing.h).  Covers the four transposition variants, ragged
+edges (several tiles + tails), triangular k-ranges and symmetric lower/mirror outputs."""
+import ctypes
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+A_KLE_M, A_KGE_M, B_KLE_N, B_KGE_N, SYM_LOWER, SYM_MIRROR = 1, 2, 4, 8, 16, 32
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1509_04681_b200 import Context
+    return Context(0)
+
+
+def dev(a, ld_pad=0):
+    from paper_1509_04681_b200.api import colmajor_empty
+    t = colmajor_empty(a.shape[0], a.shape[1])
+    t.copy_(torch.from_numpy(np.asfortranarray(a)))
+    return t
+
+
+def run(ctx, tA, tB, A, B, C0, alpha, beta, flags, M, N, K):
+    from paper_1509_04681_b200.api import ld_of
+    dA, dB, dC = dev(A), dev(B), dev(C0)
+    st = ctx.lib.cggm_test_gemm(ctx.h, int(tA), int(tB), M, N, K, ctypes.c_void_p(dA.data_ptr()), ld_of(dA),
+                                ctypes.c_void_p(dB.data_ptr()), ld_of(dB), ctypes.c_void_p(dC.data_ptr()), ld_of(dC),
+                                alpha, beta, flags)
+    ctx._check(st)
+    torch.cuda.synchronize()
+    return dC.cpu().numpy()
+
+
+@pytest.mark.parametrize("tA", [False, True])
+@pytest.mark.parametrize("tB", [False, True])
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (37, 45, 29), (128, 128, 16), (300, 260, 171), (513, 129, 1000)])
+def test_gemm_variants(ctx, tA, tB, M, N, K):
+    rng = np.random.default_rng(M * 7 + N * 3 + K)
+    A = rng.standard_normal((K, M) if tA else (M, K))
+    B = rng.standard_normal((N, K) if tB else (K, N))
+    C0 = rng.standard_normal((M, N))
+    ref = 0.75 * ((A.T if tA else A) @ (B.T if tB else B)) - 0.5 * C0
+    out = run(ctx, tA, tB, A, B, C0, 0.75, -0.5, 0, M, N, K)
+    assert np.linalg.norm(out - ref) / np.linalg.norm(ref) < 1e-14
+
+
+def test_gemm_k_zero(ctx):
+    C0 = np.ones((20, 30))
+    out = run(ctx, False, False, np.zeros((20, 1)), np.zeros((1, 30)), C0, 1.0, 2.0, 0, 20, 30, 0)
+    np.testing.assert_array_equal(out, 2.0 * C0)
+
+
+@pytest.mark.parametrize("q,K", [(200, 57), (385, 300)])
+def test_gemm_sym_lower_mirror(ctx, q, K):
+    rng = np.random.default_rng(q)
+    A = rng.standard_normal((K, q))
+    ref = A.T @ A
+    out = run(ctx, True, False, A, A, np.zeros((q, q)), 1.0, 0.0, SYM_LOWER | SYM_MIRROR, q, q, K)
+    np.testing.assert_array_equal(out, out.T)            # bit-identical triangles
+    assert np.linalg.norm(out - ref) / np.linalg.norm(ref) < 1e-14
+    C0 = np.full((q, q), 7.0)
+    out2 = run(ctx, False, True, A.T.copy(), A.T.copy(), C0, -1.0, 1.0, SYM_LOWER, q, q, K)
+    low = np.tril(np.ones((q, q), dtype=bool))
+    np.testing.assert_allclose(out2[low], (7.0 - ref)[low], rtol=1e-13, atol=1e-12)
+    np.testing.assert_array_equal(out2[~low], 7.0)       # upper triangle untouched
+
+
+@pytest.mark.parametrize("flags", [A_KLE_M, A_KGE_M, B_KLE_N, B_KGE_N, A_KGE_M | B_KGE_N])
+def test_gemm_triangular_k_range(ctx, flags):
+    """Triangular operands with exact zeros outside the triangle: the shortened k-range must
+    give the full product."""
+    rng = np.random.default_rng(flags)
+    n = 333
+    A = rng.standard_normal((n, n))
+    B = rng.standard_normal((n, n))
+    # op(A)[m][k] zero for k > m (A_KLE_M) etc.; no transposes here
+    if flags & A_KLE_M:
+        A = np.tril(A)
+    if flags & A_KGE_M:
+        A = np.triu(A)
+    if flags & B_KLE_N:
+        B = np.triu(B)
+    if flags & B_KGE_N:
+        B = np.tril(B)
+    ref = A @ B
+    out = run(ctx, False, False, A, B, np.zeros((n, n)), 1.0, 0.0, flags, n, n, n)
+    assert np.linalg.norm(out - ref) / np.linalg.norm(ref) < 1e-14
+
+
+def test_gemm_odd_leading_dimension_packs(ctx):
+    """ld odd / unaligned views are packed before TMA."""
+    from paper_1509_04681_b200.api import ld_of
+    rng = np.random.default_rng(9)
+    M, N, K = 77, 65, 43
+    A = rng.standard_normal((M, K))
+    B = rng.standard_normal((K, N))
+    base = torch.from_numpy(np.asfortranarray(np.vstack([A, np.zeros((2, K))]))).cuda()  # ld = M + 2 (odd)
+    baseA = torch.zeros((K, M + 2), dtype=torch.float64, device="cuda")
+    baseA.copy_(torch.from_numpy(np.vstack([A, np.zeros((2, K))]).T.copy()))
+    dA = baseA.t()[1:M + 1]            # offset by one element: unaligned base, ld = M + 2 = 79
+    baseA.t()[1:M + 1].copy_(torch.from_numpy(A))
+    dB = dev(B)
+    dC = dev(np.zeros((M, N)))
+    st = ctx.lib.cggm_test_gemm(ctx.h, 0, 0, M, N, K, ctypes.c_void_p(dA.data_ptr()), ld_of(dA),
+                                ctypes.c_void_p(dB.data_ptr()), ld_of(dB), ctypes.c_void_p(dC.data_ptr()), ld_of(dC),
+                                1.0, 0.0, 0)
+    ctx._check(st)
+    out = dC.cpu().numpy()
+    ref = A @ B
+    assert np.linalg.norm(out - ref) / np.linalg.norm(ref) < 1e-14
+    del base

@@ -1,0 +1,225 @@
+"""Parity of the CUDA path (through the C-ABI) with the CPU oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): Sigma, Psi, gradients rel-Frobenius <= 1e-9 (fp64);
+objective rel <= 1e-10; active sets bit-exact outside the tie band ||grad| - lam| <= 1e-9;
+is_pd exact.  Symmetric outputs must have bit-identical triangles (reading A19).
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import cggm_oracle as O  # noqa: E402
+from synth.cggm_inputs import csc_from_dense, make_problem  # noqa: E402
+
+REL_F = 1e-9
+REL_OBJ = 1e-10
+TIE = 1e-9
+
+
+def relf(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1509_04681_b200 import Context
+    return Context(0)
+
+
+_CACHE = {}
+
+
+def problem(name):
+    if name not in _CACHE:
+        _CACHE[name] = make_problem(name)
+    return _CACHE[name]
+
+
+def oracle_point(name, k):
+    key = (name, k)
+    if key not in _CACHE:
+        P = problem(name)
+        label, lam, th = P.points[k]
+        Syy, Sxy = O.covariances(P.X, P.Y)
+        Sig, ld, ok, fc = O.invert_logdet(lam.to_dense())
+        r = O.psi_grad(P.X, P.Y, th, Sig, Syy, Sxy)
+        a = O.active_set(r["GradL"], r["GradT"], lam, th, P.lam_L, P.lam_T, True, TIE)
+        sub = O.min_norm_subgradient(r["GradL"], r["GradT"], lam, th, P.lam_L, P.lam_T, True)
+        ob = O.objective(P.X, P.Y, lam, th, P.lam_L, P.lam_T, True)
+        _CACHE[key] = dict(Syy=Syy, Sxy=Sxy, Sigma=Sig, logdet=ld, **r, active=a, sub=sub, obj=ob)
+    return _CACHE[key]
+
+
+def to_np(t):
+    return t.detach().cpu().numpy()
+
+
+def compare_active(gpu, ora, m_name, row_k, col_k, tie_mask):
+    """Lists must agree exactly outside the tie band."""
+    g = set(zip(to_np(gpu[row_k]).tolist(), to_np(gpu[col_k]).tolist()))
+    o = set(zip(ora[row_k].tolist(), ora[col_k].tolist()))
+    diff = g ^ o
+    for (i, j) in diff:
+        assert tie_mask[i, j], f"{m_name}: ({i},{j}) differs outside the tie band"
+    # ordering: ascending column-major
+    rows, cols = to_np(gpu[row_k]).astype(np.int64), to_np(gpu[col_k]).astype(np.int64)
+    key = cols * (1 << 31) + rows
+    assert np.all(np.diff(key) > 0)
+
+
+CASES = [("tiny", 0), ("tiny", 1), ("small", 0), ("small", 1)]
+
+
+@pytest.mark.parametrize("name,k", CASES)
+def test_parity_point(ctx, name, k):
+    from paper_1509_04681_b200 import DeviceCsc, to_device_colmajor
+    P = problem(name)
+    ref = oracle_point(name, k)
+    label, lam, th = P.points[k]
+    X, Y = to_device_colmajor(P.X), to_device_colmajor(P.Y)
+    Lg, Tg = DeviceCsc.from_host(lam), DeviceCsc.from_host(th)
+    Syy, Sxy = ctx.cggm_covariances(X, Y)
+    assert relf(to_np(Syy), ref["Syy"]) <= 1e-13
+    assert relf(to_np(Sxy), ref["Sxy"]) <= 1e-13
+    np.testing.assert_array_equal(to_np(Syy), to_np(Syy).T)
+    Sigma, logdet, pd, fc = ctx.cggm_invert_logdet(Lg)
+    assert pd and fc == -1
+    S = to_np(Sigma)
+    np.testing.assert_array_equal(S, S.T)
+    assert relf(S, ref["Sigma"]) <= REL_F
+    assert logdet == pytest.approx(ref["logdet"], rel=1e-12, abs=1e-13)
+    for route in ("residual", "sxy"):
+        r = ctx.cggm_psi_grad(X, Y, Tg, Sigma, Syy=Syy, Sxy=(Sxy if route == "sxy" else None))
+        Psi, GL, GT = to_np(r["Psi"]), to_np(r["GradL"]), to_np(r["GradT"])
+        np.testing.assert_array_equal(Psi, Psi.T)
+        np.testing.assert_array_equal(GL, GL.T)
+        assert relf(Psi, ref["Psi"]) <= REL_F
+        assert relf(GL, ref["GradL"]) <= REL_F
+        assert relf(GT, ref["GradT"]) <= REL_F
+    a = ctx.cggm_active_set(r["GradL"], r["GradT"], Lg, Tg, P.lam_L, P.lam_T, True, TIE)
+    ora = ref["active"]
+    compare_active(a, ora, "S_Lambda", "L_row", "L_col", ora["tie_mask_L"])
+    compare_active(a, ora, "S_Theta", "T_row", "T_col", ora["tie_mask_T"])
+    if ora["ties_L"] == 0 and ora["ties_T"] == 0:
+        assert a["m_L"] == ora["m_L"] and a["m_T"] == ora["m_T"]
+    assert a["subgrad_l1"] == pytest.approx(ref["sub"], rel=1e-9)
+    ob = ctx.cggm_objective(X, Y, Lg, Tg, P.lam_L, P.lam_T, True)
+    ro = ref["obj"]
+    assert ob["is_pd"] and ob["fail_col"] == -1
+    assert ob["f"] == pytest.approx(ro["f"], rel=REL_OBJ)
+    assert ob["g"] == pytest.approx(ro["g"], rel=REL_OBJ, abs=1e-10)
+    assert ob["logdet"] == pytest.approx(ro["logdet"], rel=1e-12, abs=1e-13)
+
+
+def test_fused_active_matches_separate(ctx):
+    from paper_1509_04681_b200 import DeviceCsc, to_device_colmajor
+    P = problem("small")
+    label, lam, th = P.points[1]
+    X, Y = to_device_colmajor(P.X), to_device_colmajor(P.Y)
+    Lg, Tg = DeviceCsc.from_host(lam), DeviceCsc.from_host(th)
+    Syy, _ = ctx.cggm_covariances(X, Y, want_sxy=False)
+    Sigma, _, _, _ = ctx.cggm_invert_logdet(Lg)
+    sep = ctx.cggm_psi_grad(X, Y, Tg, Sigma, Syy=Syy)
+    a = ctx.cggm_active_set(sep["GradL"], sep["GradT"], Lg, Tg, P.lam_L, P.lam_T)
+    cap = 200000
+    spec = dict(lam_L=P.lam_L, lam_T=P.lam_T, penalize_diag=1, tie_eps=TIE,
+                L_row=torch.empty(cap, dtype=torch.int32, device="cuda"),
+                L_col=torch.empty(cap, dtype=torch.int32, device="cuda"),
+                T_row=torch.empty(cap, dtype=torch.int32, device="cuda"),
+                T_col=torch.empty(cap, dtype=torch.int32, device="cuda"))
+    fu = ctx.cggm_psi_grad(X, Y, Tg, Sigma, Syy=Syy, Lam=Lg, fused=spec)["active"]
+    assert fu["m_L"] == a["m_L"] and fu["m_T"] == a["m_T"]
+    assert torch.equal(fu["L_row"], a["L_row"]) and torch.equal(fu["T_col"], a["T_col"])
+    assert fu["subgrad_l1"] == a["subgrad_l1"]
+
+
+def test_capacity_two_call(ctx):
+    from paper_1509_04681_b200 import DeviceCsc, to_device_colmajor
+    from paper_1509_04681_b200.api import CggmError
+    P = problem("tiny")
+    label, lam, th = P.points[1]
+    X, Y = to_device_colmajor(P.X), to_device_colmajor(P.Y)
+    Lg, Tg = DeviceCsc.from_host(lam), DeviceCsc.from_host(th)
+    Syy, _ = ctx.cggm_covariances(X, Y, want_sxy=False)
+    Sigma, _, _, _ = ctx.cggm_invert_logdet(Lg)
+    r = ctx.cggm_psi_grad(X, Y, Tg, Sigma, Syy=Syy)
+    with pytest.raises(CggmError) as ei:
+        ctx.cggm_active_set(r["GradL"], r["GradT"], Lg, Tg, P.lam_L, P.lam_T, cap_L=1, cap_T=1)
+    assert ei.value.status == 6
+
+
+def test_non_pd_lambda(ctx):
+    from paper_1509_04681_b200 import DeviceCsc, to_device_colmajor
+    P = problem("small")
+    A = P.lam_star.to_dense()
+    lmin = 1.25 - math.cos(math.pi / (P.q + 1))
+    for t, expect_pd in [(1 - 1e-6, True), (1 + 1e-6, False)]:
+        B = A - t * lmin * np.eye(P.q)
+        _, ok, fc_o = O.cholesky(B)
+        assert ok == expect_pd
+        Bg = DeviceCsc.from_host(csc_from_dense(B))
+        _, ld, pd, fc = ctx.cggm_invert_logdet(Bg, want_sigma=False)
+        assert pd == expect_pd
+        if not expect_pd:
+            assert fc == fc_o
+            ob = ctx.cggm_objective(to_device_colmajor(P.X), to_device_colmajor(P.Y), Bg,
+                                    DeviceCsc.from_host(P.theta_star), P.lam_L, P.lam_T)
+            assert not ob["is_pd"] and ob["f"] == math.inf and ob["fail_col"] == fc_o
+
+
+def test_spec_logdet_examples(ctx):
+    from paper_1509_04681_b200 import DeviceCsc
+    for A, pd_ref, ld_ref in [(np.eye(5), True, 0.0), (2 * np.eye(3), True, 3 * math.log(2)),
+                              (np.array([[1.0, 2.0], [2.0, 1.0]]), False, None)]:
+        Sg, ld, pd, fc = ctx.cggm_invert_logdet(DeviceCsc.from_host(csc_from_dense(A)))
+        assert pd == pd_ref
+        if pd:
+            assert ld == pytest.approx(ld_ref, abs=1e-15)
+            assert np.allclose(to_np(Sg), np.linalg.inv(A), rtol=1e-15)
+        else:
+            assert fc == 1
+
+
+@pytest.mark.parametrize("q", [700, 2500])
+def test_chain_sigma_closed_form(ctx, q):
+    """P3/P4 on the GPU directly: several recursion levels, ragged leaf."""
+    from paper_1509_04681_b200 import DeviceCsc
+    from tests.test_oracle_pins import chain_dense, chain_sigma_closed_form
+    Sg, ld, pd, fc = ctx.cggm_invert_logdet(DeviceCsc.from_host(csc_from_dense(chain_dense(q))))
+    assert pd
+    assert ld == pytest.approx(math.log((1 - 0.5 ** (2 * q + 2)) / 0.75), rel=1e-12)
+    S = to_np(Sg)
+    assert relf(S, chain_sigma_closed_form(q)) <= 1e-12
+
+
+def test_validation_errors(ctx):
+    from paper_1509_04681_b200 import DeviceCsc
+    from paper_1509_04681_b200.api import CggmError
+    A = np.array([[2.0, 1.0], [0.5, 2.0]])   # not symmetric
+    with pytest.raises(CggmError) as ei:
+        ctx.cggm_invert_logdet(DeviceCsc.from_host(csc_from_dense(A)))
+    assert ei.value.status == 3
+    bad = DeviceCsc.from_host(csc_from_dense(np.eye(3)))
+    bad.rowidx[1] = 7   # out of range
+    with pytest.raises(CggmError) as ei:
+        ctx.cggm_invert_logdet(bad)
+    assert ei.value.status == 4
+
+
+def test_launch_count_increases(ctx):
+    from paper_1509_04681_b200 import DeviceCsc
+    before = ctx.launch_count()
+    ctx.cggm_invert_logdet(DeviceCsc.from_host(csc_from_dense(2 * np.eye(40))))
+    assert ctx.launch_count() > before
+
+
+@pytest.mark.slow
+def test_parity_medium(ctx):
+    test_parity_point(ctx, "medium", 0)
