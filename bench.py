@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""bench.py — CGGM Newton-iteration evaluations/s at p=40k, q=20k (BASELINE.json `large`).
+
+One step = one Newton-iteration evaluation at (Lambda*, Theta*):
+  cggm_invert_logdet(Lambda)  -> Sigma, log|Lambda|, PD            (potrf + trtri + lauum)
+  cggm_psi_grad(+fused active sets) -> Psi, grad_Lambda, grad_Theta, S_Lambda, S_Theta, ||grad^S||_1
+  cggm_objective(Lambda_trial = Lambda, Theta) with its own fresh Cholesky (a line-search trial)
+S_yy (per-dataset setup) is computed once before the timed region and reported separately.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl cggm|reference] [--config large]
+
+N > 1 (torchrun): the n samples are sharded over the ranks; rank 0 inverts Lambda and broadcasts
+Sigma; Psi and grad_Theta partials are all-reduced over NCCL (strong scaling: one evaluation of
+the fixed `large` problem per step).  `--impl reference` times the CPU oracle (oracle/, numpy
+fp64) on a bounded sample of the same workload, on the host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CGGM Newton-iteration evals/s at p=40k,q=20k; FP64 tensor/HBM % of peak"
+UNIT = "evals/s"
+
+
+def alg_flops(n, p, q, nnz_theta):
+    """Algorithmic FP64 flops of one evaluation: (4/3) q^3 (potrf x2 + trtri +
+    lauum) + 2nq^2 (R = W Sigma) + nq^2 (Psi, symmetric) + 2npq (grad_Theta) + nq^2 (trsm) +
+    2 n nnz(Theta) (SpMM).  S_xx, dense X Theta and (X^T W) Sigma are avoided and not counted."""
+    gemm = (4.0 / 3.0) * q ** 3 + 4.0 * n * q * q + 2.0 * n * p * q
+    return gemm, gemm + 2.0 * n * nnz_theta
+
+
+def phase_flops(n, p, q):
+    return {"chol_gemm": q ** 3, "lauum": q ** 3 / 3.0, "w_sigma": 2.0 * n * q * q, "psi_gradL": 1.0 * n * q * q,
+            "grad_theta": 2.0 * n * p * q, "obj_trsm": 1.0 * n * q * q}
+
+
+GEMM_TAGS = ("chol_gemm", "lauum", "w_sigma", "psi_gradL", "grad_theta", "obj_trsm")
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.dev)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        loaded = [s for s in sm if mx is None or s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle (CPU) leg
+def oracle_sample(P, qs, ps):
+    """Bounded sample of the `large` workload for the CPU oracle: the leading qs outputs, ps
+    inputs and all n samples (Lambda*, Theta* restricted to that block)."""
+    from synth.cggm_inputs import Csc
+    lam = P.lam_star
+    d = lam.to_scipy()[:qs, :qs].tocsc()
+    d.sort_indices()
+    lam_s = Csc(qs, qs, d.indptr.astype(np.int64), d.indices.astype(np.int32), d.data.copy())
+    t = P.theta_star.to_scipy()[:ps, :qs].tocsc()
+    t.sort_indices()
+    th_s = Csc(ps, qs, t.indptr.astype(np.int64), t.indices.astype(np.int32), t.data.copy())
+    X = np.asfortranarray(P.X[:, :ps])
+    Y = np.asfortranarray(P.Y[:, :qs])
+    return X, Y, lam_s, th_s
+
+
+def oracle_eval_seconds(X, Y, lam, th, lam_L, lam_T):
+    from oracle import cggm_oracle as O
+    t0 = time.perf_counter()
+    Syy, _ = O.covariances(X, Y)    # setup, excluded below
+    t1 = time.perf_counter()
+    Sig, ld, ok, fc = O.invert_logdet(lam.to_dense())
+    r = O.psi_grad(X, Y, th, Sig, Syy, None)
+    O.active_set(r["GradL"], r["GradT"], lam, th, lam_L, lam_T)
+    O.min_norm_subgradient(r["GradL"], r["GradT"], lam, th, lam_L, lam_T)
+    O.objective(X, Y, lam, th, lam_L, lam_T)
+    t2 = time.perf_counter()
+    return t2 - t1, t1 - t0
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        n = [d.get("num_threads", 1) for d in info if d.get("user_api") == "blas"]
+        return int(max(n)) if n else 1
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(P, qs=2000, ps=4000):
+    X, Y, lam_s, th_s = oracle_sample(P, qs, ps)
+    secs, _ = oracle_eval_seconds(X, Y, lam_s, th_s, P.lam_L, P.lam_T)
+    _, full = alg_flops(P.n, P.p, P.q, P.theta_star.nnz)
+    _, samp = alg_flops(P.n, ps, qs, th_s.nnz)
+    est = secs * full / samp
+    return {"value": 1.0 / est, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+            "sample": f"one oracle evaluation on the leading {qs} outputs x {ps} inputs x all {P.n} samples of "
+                      f"`large` ({secs:.2f} s), extrapolated by algorithmic flops x{full / samp:.0f}",
+            "sample_seconds": secs}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from synth.cggm_inputs import make_problem
+    P = make_problem(args.config)
+    qs, ps = 1500, 3000
+    X, Y, lam_s, th_s = oracle_sample(P, qs, ps)
+    _, full = alg_flops(P.n, P.p, P.q, P.theta_star.nnz)
+    _, samp = alg_flops(P.n, ps, qs, th_s.nnz)
+    for _ in range(args.warmup):
+        oracle_eval_seconds(X, Y, lam_s, th_s, P.lam_L, P.lam_T)
+    times = [oracle_eval_seconds(X, Y, lam_s, th_s, P.lam_L, P.lam_T)[0] for _ in range(args.steps)]
+    est = sum(times) / len(times) * full / samp
+    value = 1.0 / est
+    cb = {"value": value, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+          "sample": f"per step: one oracle evaluation on the leading {qs} outputs x {ps} inputs x all {P.n} samples "
+                    f"of `{args.config}`, extrapolated by algorithmic flops x{full / samp:.0f}"}
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": est * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "n": P.n, "p": P.p, "q": P.q},
+            "cpu_baseline": cb,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU leg
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="cggm", choices=["cggm", "reference"])
+    ap.add_argument("--config", default="large")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--peak-seconds", type=float, default=2.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_1509_04681_b200 import Context, DeviceCsc, colmajor_empty
+    from paper_1509_04681_b200.sharded import CudaBackend, ShardedEvaluator, shard_rows
+    from paper_1509_04681_b200 import _abi
+    from synth.cggm_inputs import make_problem
+
+    t_gen = time.perf_counter()
+    P = make_problem(args.config)
+    t_gen = time.perf_counter() - t_gen
+    a, b = shard_rows(P.n, world, rank)
+    n_loc = b - a
+    label, lam_h, th_h = [pt for pt in P.points if pt[0] == "truth"][0]
+
+    def to_dev(A):
+        t = colmajor_empty(A.shape[0], A.shape[1])
+        t.copy_(torch.from_numpy(np.asfortranarray(A)))
+        return t
+
+    X = to_dev(P.X[a:b])
+    Y = to_dev(P.Y[a:b])
+    Lam = DeviceCsc.from_host(lam_h)
+    Th = DeviceCsc.from_host(th_h)
+    ctx = Context(local, validate=1)
+    stream = torch.cuda.current_stream()
+
+    # FP64 tensor-pipe peak, measured live (MEASURED_PEAKS.json has no FP64 entry)
+    tf, ms = ctypes.c_double(), ctypes.c_double()
+    ctx._check(ctx.lib.cggm_test_fp64_peak(ctx.h, args.peak_seconds, ctypes.byref(tf), ctypes.byref(ms)))
+    peak_tflops = tf.value
+
+    ev = ShardedEvaluator(CudaBackend(ctx))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    Syy = ev.setup(X, Y, P.n)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    setup_ms = e0.elapsed_time(e1)
+
+    if world == 1:
+        # single GPU: fused active sets in the Psi/grad call, preallocated outputs
+        q, p = P.q, P.p
+        bufs = {"Sigma": colmajor_empty(q, q), "Psi": colmajor_empty(q, q), "GradL": colmajor_empty(q, q),
+                "GradT": colmajor_empty(p, q)}
+        probe = ctx.cggm_invert_logdet(Lam, Sigma=bufs["Sigma"])
+        r0 = ctx.cggm_psi_grad(X, Y, Th, bufs["Sigma"], Syy=Syy,
+                               out=dict(Psi=bufs["Psi"], GradL=bufs["GradL"], GradT=bufs["GradT"]))
+        cnt = ctx.cggm_active_set(r0["GradL"], r0["GradT"], Lam, Th, P.lam_L, P.lam_T)
+        capL, capT = int(cnt["m_L"] * 1.05) + 1024, int(cnt["m_T"] * 1.05) + 1024
+        for k, cap in (("L_row", capL), ("L_col", capL), ("T_row", capT), ("T_col", capT)):
+            bufs[k] = torch.empty(cap, dtype=torch.int32, device="cuda")
+        del r0, cnt, probe
+
+        from paper_1509_04681_b200.api import newton_evaluation
+
+        def step():
+            return newton_evaluation(ctx, X, Y, Syy, Lam, Th, P.lam_L, P.lam_T, True, bufs)
+    else:
+        def step():
+            return ev.evaluate(X, Y, Lam, Th, P.lam_L, P.lam_T, True)
+
+    for _ in range(max(args.warmup, 0)):
+        last = step()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    ctx.profile(True)
+    l0 = ctx.launch_count()
+    e0.record(stream)
+    for _ in range(args.steps):
+        last = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    elapsed = e0.elapsed_time(e1)
+    launches = ctx.launch_count() - l0
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+
+    ms_step = elapsed / args.steps
+    value = args.steps / (elapsed / 1e3)
+    gemm_flops, all_flops = alg_flops(P.n, P.p, P.q, P.theta_star.nnz)
+    gemm_ms = sum(prof[t][0] for t in GEMM_TAGS) / args.steps
+    achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12
+    ph_flops = phase_flops(P.n, P.p, P.q)
+    phases = {}
+    for tag, (tms, tcnt) in prof.items():
+        if tcnt == 0:
+            continue
+        d = {"ms_per_step": tms / args.steps, "launches_per_step": tcnt / args.steps}
+        if tag in ph_flops:
+            d["tflops"] = ph_flops[tag] / (tms / args.steps * 1e-3) / 1e12
+        phases[tag] = d
+
+    # ---------------------------------------------------------------- e2e through the public API
+    e2e = None
+    if not args.no_e2e and world == 1:
+        Xh = torch.from_numpy(np.asfortranarray(P.X)).pin_memory()
+        Yh = torch.from_numpy(np.asfortranarray(P.Y)).pin_memory()
+        host_csc = {k: (getattr(Lam, k).cpu().pin_memory(), getattr(Th, k).cpu().pin_memory())
+                    for k in ("colptr", "rowidx", "val")}
+        h2d = (Xh.numel() + Yh.numel()) * 8 + sum(x.numel() * x.element_size() + y.numel() * y.element_size()
+                                                  for x, y in host_csc.values())
+        d2h = ctypes.sizeof(_abi.cggm_objective_out) + ctypes.sizeof(_abi.cggm_active_out) + 8 + 4 + 8
+
+        def step_e2e():
+            X.copy_(Xh, non_blocking=True)
+            Y.copy_(Yh, non_blocking=True)
+            for k, (hl, ht) in host_csc.items():
+                getattr(Lam, k).copy_(hl, non_blocking=True)
+                getattr(Th, k).copy_(ht, non_blocking=True)
+            Syy_s, _ = ctx.cggm_covariances(X, Y, want_sxy=False, Syy=Syy)
+            return newton_evaluation(ctx, X, Y, Syy_s, Lam, Th, P.lam_L, P.lam_T, True, bufs)
+
+        step_e2e()
+        torch.cuda.synchronize()
+        e2_steps = max(1, min(args.steps, 3))
+        e0.record(stream)
+        for _ in range(e2_steps):
+            step_e2e()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2ms = e0.elapsed_time(e1)
+        e2e = {"value": e2_steps / (e2ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "steps": e2_steps,
+               "includes": "H2D of X, Y, Lambda, Theta from pinned host + S_yy + evaluation + D2H of scalars"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(P)
+
+    res = last
+    obj = res["objective"] if world == 1 else {"f": res["f"]}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": args.config, "n": P.n, "p": P.p, "q": P.q, "nnz_theta": P.theta_star.nnz,
+                       "nnz_lambda": P.lam_star.nnz, "lambda": P.lam_L, "point": "generating (Lambda*, Theta*)",
+                       "parallelism": f"sample-shard dp{world}" if world > 1 else "1 GPU",
+                       "l2": "inputs larger than L2 (Sigma/Psi/grad_Lambda 3.2 GB each, grad_Theta 6.4 GB)",
+                       "setup_syy_ms": setup_ms, "generator_s": round(t_gen, 2)},
+            "clocks": clk,
+            "gpu_launches": launches,
+            "roofline": {"bound": "tensor", "kernel": "gemm_dmma_kernel (FP64 DMMA.8x8x4, all dense contractions)",
+                         "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
+                         "frac": achieved / peak_tflops, "traffic": None,
+                         "peak_source": f"live DMMA.8x8x4 microbenchmark on this GPU ({args.peak_seconds:.1f} s, "
+                                        "2 CTAs/SM); MEASURED_PEAKS.json has no FP64 entry",
+                         "gemm_ms_per_step": gemm_ms, "gemm_alg_flops_per_step": gemm_flops,
+                         "step_frac_of_peak": all_flops / (ms_step * 1e-3) / 1e12 / peak_tflops},
+            "phases": phases,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "result": {"f": obj.get("f"), "logdet": res.get("logdet"),
+                       "m_L": res["active"]["m_L"], "m_T": res["active"]["m_T"],
+                       "subgrad_l1": res["active"]["subgrad_l1"]},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -112,6 +112,14 @@ cggm_status cggm_ctx_set_validate(cggm_ctx* ctx, int level);
 cggm_status cggm_ctx_launch_count(cggm_ctx* ctx, int64_t* count);
 /* Release the cached internal workspace. */
 cggm_status cggm_ctx_release_workspace(cggm_ctx* ctx);
+/* Phase profiling: while enabled, every library kernel launch is bracketed by CUDA events on the
+ * ctx stream and attributed to a phase tag (0..CGGM_PROF_NTAGS-1, names by cggm_profile_tag_name).
+ * enable=1 clears previous records.  _read synchronises the stream and writes per-tag summed
+ * kernel milliseconds and launch counts (arrays of >= CGGM_PROF_NTAGS entries), then clears. */
+#define CGGM_PROF_NTAGS 13
+cggm_status cggm_ctx_profile(cggm_ctx* ctx, int enable);
+cggm_status cggm_ctx_profile_read(cggm_ctx* ctx, double* ms, int64_t* launches, int32_t ntags);
+const char* cggm_profile_tag_name(int32_t tag);
 /* Message of the last error on this ctx ("" if none).  Valid until the next call. */
 const char* cggm_last_error(cggm_ctx* ctx);
 /* Library version string. */

@@ -23,6 +23,7 @@ STATUS = {
 }
 CGGM_F64 = 0
 CGGM_F32 = 1
+PROF_NTAGS = 13
 
 
 class cggm_csc(ctypes.Structure):
@@ -52,6 +53,9 @@ SIGNATURES = {
     "cggm_ctx_launch_count": (c_i32, [c_vp, ctypes.POINTER(c_i64)]),
     "cggm_ctx_release_workspace": (c_i32, [c_vp]),
     "cggm_last_error": (ctypes.c_char_p, [c_vp]),
+    "cggm_ctx_profile": (c_i32, [c_vp, c_i32]),
+    "cggm_ctx_profile_read": (c_i32, [c_vp, ctypes.POINTER(c_d), ctypes.POINTER(c_i64), c_i32]),
+    "cggm_profile_tag_name": (ctypes.c_char_p, [c_i32]),
     "cggm_version": (ctypes.c_char_p, []),
     "cggm_covariances": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64,
                                  c_vp, c_i64, c_vp, c_i64]),
@@ -66,6 +70,7 @@ SIGNATURES = {
                                 ctypes.POINTER(cggm_csc), ctypes.POINTER(cggm_active_out)]),
     "cggm_test_gemm": (c_i32, [c_vp, c_i32, c_i32, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
                                c_d, c_d, c_i32]),
+    "cggm_test_fp64_peak": (c_i32, [c_vp, c_d, ctypes.POINTER(c_d), ctypes.POINTER(c_d)]),
     "cggm_objective": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64,
                                ctypes.POINTER(cggm_csc), ctypes.POINTER(cggm_csc), c_d, c_d, c_i32,
                                c_vp, c_i64, ctypes.POINTER(cggm_objective_out)]),

@@ -110,6 +110,16 @@ class Context:
     def _sync_stream(self):
         self.lib.cggm_ctx_set_stream(self.h, ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream))
 
+    def profile(self, enable: bool):
+        self._check(self.lib.cggm_ctx_profile(self.h, int(bool(enable))))
+
+    def profile_read(self) -> dict:
+        n = _abi.PROF_NTAGS
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_int64 * n)()
+        self._check(self.lib.cggm_ctx_profile_read(self.h, ms, cnt, n))
+        return {self.lib.cggm_profile_tag_name(i).decode(): (ms[i], int(cnt[i])) for i in range(n)}
+
     def launch_count(self) -> int:
         v = ctypes.c_int64()
         self._check(self.lib.cggm_ctx_launch_count(self.h, ctypes.byref(v)))

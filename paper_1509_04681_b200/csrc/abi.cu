@@ -134,6 +134,7 @@ void finish_chol(Ctx* c, Scal s, double* slots, int64_t nleaves, double* out_dev
 }  // namespace cggm
 
 using namespace cggm;
+static_assert(CGGM_PROF_NTAGS == TAG_NUM, "profile tags out of sync");
 
 extern "C" {
 
@@ -213,6 +214,43 @@ cggm_status cggm_ctx_release_workspace(cggm_ctx* ctx) {
   });
 }
 
+cggm_status cggm_ctx_profile(cggm_ctx* ctx, int enable) {
+  if (!ctx) return CGGM_ERR_INVALID_ARG;
+  Ctx* c = &ctx->impl;
+  c->prof = enable != 0;
+  if (c->prof) {
+    c->prof_recs.clear();
+    c->evnext = 0;
+  }
+  return CGGM_OK;
+}
+
+cggm_status cggm_ctx_profile_read(cggm_ctx* ctx, double* ms, int64_t* launches, int32_t ntags) {
+  return guard(ctx, [&](Ctx* c) {
+    if (!ms || !launches || ntags < CGGM_PROF_NTAGS) fail(CGGM_ERR_INVALID_ARG, "profile arrays too small");
+    CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    for (int t = 0; t < CGGM_PROF_NTAGS; ++t) {
+      ms[t] = 0.0;
+      launches[t] = 0;
+    }
+    for (const auto& r : c->prof_recs) {
+      float e = 0.f;
+      CGGM_CUDA_CHECK(cudaEventElapsedTime(&e, c->evpool[r.a], c->evpool[r.b]));
+      ms[r.tag] += e;
+      launches[r.tag] += 1;
+    }
+    c->prof_recs.clear();
+    c->evnext = 0;
+  });
+}
+
+const char* cggm_profile_tag_name(int32_t tag) {
+  static const char* names[CGGM_PROF_NTAGS] = {"misc", "covariances", "densify", "chol_gemm", "chol_leaf",
+                                               "lauum", "spmm", "w_sigma", "psi_gradL", "grad_theta",
+                                               "obj_trsm", "active_set", "obj_reduce"};
+  return (tag >= 0 && tag < CGGM_PROF_NTAGS) ? names[tag] : "?";
+}
+
 const char* cggm_last_error(cggm_ctx* ctx) { return ctx ? ctx->impl.last_error.c_str() : "null ctx"; }
 
 // ------------------------------------------------------------------ a1
@@ -230,6 +268,7 @@ cggm_status cggm_covariances(cggm_ctx* ctx, int64_t n_local, int64_t n_total, in
       check_dense("Sxy", Sxy, p, q, ldsxy);
     }
     const double inv_n = 1.0 / (double)n_total;
+    Phase ph(c, TAG_COV);
     if (Syy) {
       Epilogue e; e.out1 = static_cast<double*>(Syy); e.ld1 = ldsyy; e.a1 = inv_n;
       gemm(c, true, false, q, q, n_local, static_cast<const double*>(Y), ldy, static_cast<const double*>(Y), ldy, e,
@@ -301,6 +340,7 @@ static void active_impl(Ctx* c, int64_t p, int64_t q, const double* GradL, int64
   double* subL = reinterpret_cast<double*>(base + 6 * q);
   double* subT = reinterpret_cast<double*>(base + 7 * q);
   ActTotals* T = reinterpret_cast<ActTotals*>(base + 8 * q);
+  Phase ph(c, TAG_ACTIVE);
   active_count(c, p, q, GradL, ldgl, GradT, ldgt, Lambda, Theta, o->lam_L, o->lam_T, o->penalize_diag, o->tie_eps, T,
                offL, offT, cntL, cntT, tieL, tieT, subL, subT);
   ActTotals h;
@@ -390,12 +430,14 @@ cggm_status cggm_psi_grad(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64
     spmm_x_theta(c, Xd, ldx, n_local, Theta, View{W, ldn, n_local, q});
     // a4: acc = W Sigma -> R = acc / sqrt(n), E = Y + acc
     {
+      Phase ph(c, TAG_WSIGMA);
       Epilogue e; e.out1 = R; e.ld1 = ldn; e.a1 = 1.0 / std::sqrt((double)n_total);
       if (GradT && !Sxy) { e.out2 = E; e.ld2 = ldn; e.a2 = 1.0; e.in2a = Yd; e.ld2a = ldy; e.b2 = 1.0; }
       gemm(c, false, false, n_local, q, q, W, ldn, Sg, ldsigma, e, 0);
     }
     // a4/a5: Psi = R^T R, epilogue GradL = S_yy - Sigma - Psi (mirrored, bit-identical triangles)
     {
+      Phase ph(c, TAG_PSI);
       Epilogue e; e.out1 = static_cast<double*>(Psi); e.ld1 = ldpsi; e.a1 = 1.0;
       if (GradL) {
         e.out2 = static_cast<double*>(GradL); e.ld2 = ldgl; e.a2 = -1.0;
@@ -406,6 +448,7 @@ cggm_status cggm_psi_grad(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64
     }
     // a5: GradT = (2/n) X^T E   (or 2 S_xy + (2/sqrt n) X^T R)
     if (GradT) {
+      Phase ph(c, TAG_GRADT);
       Epilogue e; e.out1 = static_cast<double*>(GradT); e.ld1 = ldgt;
       if (!Sxy) {
         e.a1 = 2.0 / (double)n_total;
@@ -494,7 +537,11 @@ cggm_status cggm_objective(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int6
     init_scalars(c, s.fail, s.flag);
     potrf_recursive(c, Av, View{nullptr, lda, q, q}, false, leafinv, slots, s.fail, nullptr, 0);
     // Z = W L^{-T}:  ||Z||_F^2 = tr(Lambda^{-1} W^T W)  (reading A14)
-    trsm_right_lt(c, View{Z, ldn, n_local, q}, Av, leafinv, 0);
+    {
+      Phase ph(c, TAG_TRSM);
+      trsm_right_lt(c, View{Z, ldn, n_local, q}, Av, leafinv, 0);
+    }
+    Phase ph(c, TAG_OBJRED);
     col_partials(c, 0, n_local, q, Yd, ldy, nullptr, 0, Lambda, partY);
     col_partials(c, 1, n_local, q, Wd, ldwd, Yd, ldy, nullptr, partWY);
     col_partials(c, 2, n_local, q, Z, ldn, nullptr, 0, nullptr, partZ);

@@ -188,18 +188,22 @@ void active_count(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t ldg
   size_t bl = bits_bytes(q), bt = bits_bytes(p);
   set_smem(k_active_count<true>, bl);
   set_smem(k_active_count<false>, bt);
+  { Prof pr(c, TAG_ACTIVE);
   k_active_count<true><<<(unsigned)q, NT, bl, c->stream>>>(q, GradL, ldgl, Lambda->colptr, Lambda->rowidx,
                                                           static_cast<const double*>(Lambda->val), lam_L,
                                                           penalize_diag, tie_eps, cntL, tieL, subL);
-  post_launch(c, "k_active_count<L>");
+  post_launch(c, "k_active_count<L>"); }
+  { Prof pr(c, TAG_ACTIVE);
   k_active_count<false><<<(unsigned)q, NT, bt, c->stream>>>(p, GradT, ldgt, Theta->colptr, Theta->rowidx,
                                                            static_cast<const double*>(Theta->val), lam_T, 1, tie_eps,
                                                            cntT, tieT, subT);
-  post_launch(c, "k_active_count<T>");
+  post_launch(c, "k_active_count<T>"); }
+  { Prof pr(c, TAG_ACTIVE);
   k_active_scan<<<1, SCAN_NT, 0, c->stream>>>(q, cntL, tieL, subL, offL, &T->m_L, &T->ties_L, &T->sub_L);
-  post_launch(c, "k_active_scan<L>");
+  post_launch(c, "k_active_scan<L>"); }
+  { Prof pr(c, TAG_ACTIVE);
   k_active_scan<<<1, SCAN_NT, 0, c->stream>>>(q, cntT, tieT, subT, offT, &T->m_T, &T->ties_T, &T->sub_T);
-  post_launch(c, "k_active_scan<T>");
+  post_launch(c, "k_active_scan<T>"); }
 }
 
 void active_write(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t ldgl, const double* GradT, int64_t ldgt,
@@ -210,14 +214,16 @@ void active_write(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t ldg
   size_t bl = bits_bytes(q), bt = bits_bytes(p);
   set_smem(k_active_write<true>, bl);
   set_smem(k_active_write<false>, bt);
+  { Prof pr(c, TAG_ACTIVE);
   k_active_write<true><<<(unsigned)q, NT, bl, c->stream>>>(q, GradL, ldgl, Lambda->colptr, Lambda->rowidx,
                                                           static_cast<const double*>(Lambda->val), lam_L,
                                                           penalize_diag, offL, L_row, L_col);
-  post_launch(c, "k_active_write<L>");
+  post_launch(c, "k_active_write<L>"); }
+  { Prof pr(c, TAG_ACTIVE);
   k_active_write<false><<<(unsigned)q, NT, bt, c->stream>>>(p, GradT, ldgt, Theta->colptr, Theta->rowidx,
                                                            static_cast<const double*>(Theta->val), lam_T, 1, offT,
                                                            T_row, T_col);
-  post_launch(c, "k_active_write<T>");
+  post_launch(c, "k_active_write<T>"); }
 }
 
 }  // namespace cggm

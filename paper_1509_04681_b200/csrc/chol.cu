@@ -119,6 +119,7 @@ void leaf(Rec& R, View A, View X, int64_t col0) {
     CGGM_CUDA_CHECK(cudaFuncSetAttribute(leaf_potrf_trtri, cudaFuncAttributeMaxDynamicSharedMemorySize, LEAF_SMEM));
     attr = true;
   }
+  Prof pr(R.c, TAG_CHOL_LEAF);
   leaf_potrf_trtri<<<1, LEAF_THREADS, LEAF_SMEM, R.c->stream>>>(A.p, A.ld, nb, xp, ldx, R.full_inverse ? 0 : 1,
                                                         R.logdet_slots + col0 / NB, R.fail_col, (int)col0);
   post_launch(R.c, "leaf_potrf_trtri");
@@ -173,6 +174,7 @@ int leaf_nb() { return NB; }
 void potrf_recursive(Ctx* c, View A, View Linv, bool full_inverse, double* leafinv, double* logdet_slots,
                      int* fail_col_dev, double* tmp, size_t tmp_elems) {
   Rec R{c, full_inverse, leafinv, logdet_slots, fail_col_dev, tmp, tmp_elems};
+  Phase ph(c, TAG_CHOL_GEMM);
   node(R, A, Linv, 0);
 }
 
@@ -199,6 +201,7 @@ void trsm_right_lt(Ctx* c, View B, View L, const double* leafinv, int64_t col0) 
 
 void lauum(Ctx* c, View Linv, View Sigma) {
   const int64_t q = Linv.rows;
+  Phase ph(c, TAG_LAUUM);
   Epilogue e; e.out1 = Sigma.p; e.ld1 = Sigma.ld;
   gemm(c, true, false, q, q, q, Linv.p, Linv.ld, Linv.p, Linv.ld, e, A_KGE_M | B_KGE_N | SYM_LOWER | SYM_MIRROR);
 }

@@ -20,6 +20,23 @@ struct Buffer {
   size_t bytes = 0;
 };
 
+enum ProfTag {
+  TAG_MISC = 0,    // validation, init, copies
+  TAG_COV,         // S_yy / S_xy GEMMs
+  TAG_DENSIFY,     // CSC -> dense
+  TAG_CHOL_GEMM,   // Cholesky / triangular-inverse / trsm GEMMs inside the recursion
+  TAG_CHOL_LEAF,   // leaf potrf + trtri kernels
+  TAG_LAUUM,       // Sigma = L^{-T} L^{-1}
+  TAG_SPMM,        // W = X Theta
+  TAG_WSIGMA,      // acc = W Sigma (R, E)
+  TAG_PSI,         // Psi = R^T R (+ grad_Lambda epilogue)
+  TAG_GRADT,       // grad_Theta = (2/n) X^T E
+  TAG_TRSM,        // objective triangular solve W L^{-T}
+  TAG_ACTIVE,      // active-set count / scan / write
+  TAG_OBJRED,      // objective reductions
+  TAG_NUM
+};
+
 struct Ctx {
   int device = 0;
   cggm_dtype dtype = CGGM_F64;
@@ -33,6 +50,49 @@ struct Ctx {
   void* host_scratch = nullptr;
   PFN_cuTensorMapEncodeTiled_v12000 encode_tiled = nullptr;
   int num_sms = 148;
+  // phase profiling (CUDA events around every launch while enabled)
+  int cur_tag = TAG_MISC;
+  bool prof = false;
+  std::vector<cudaEvent_t> evpool;
+  size_t evnext = 0;
+  struct ProfRec {
+    int tag, a, b;
+  };
+  std::vector<ProfRec> prof_recs;
+};
+
+// RAII event pair around one launch (no-op unless profiling is enabled)
+struct Prof {
+  Ctx* c;
+  int tag;
+  int ia = -1;
+  Prof(Ctx* c_, int tag_) : c(c_), tag(tag_) {
+    if (!c->prof) return;
+    ia = take();
+    cudaEventRecord(c->evpool[ia], c->stream);
+  }
+  ~Prof() {
+    if (ia < 0) return;
+    int ib = take();
+    cudaEventRecord(c->evpool[ib], c->stream);
+    c->prof_recs.push_back(Ctx::ProfRec{tag, ia, ib});
+  }
+  int take() {
+    if (c->evnext == c->evpool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      c->evpool.push_back(e);
+    }
+    return (int)c->evnext++;
+  }
+};
+
+// scoped phase tag
+struct Phase {
+  Ctx* c;
+  int prev;
+  Phase(Ctx* c_, int tag) : c(c_), prev(c_->cur_tag) { c->cur_tag = tag; }
+  ~Phase() { c->cur_tag = prev; }
 };
 
 enum Slot {

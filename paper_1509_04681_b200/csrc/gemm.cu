@@ -279,6 +279,7 @@ void launch(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KParams&
                                          SMEM_BYTES));
     attr_set = true;
   }
+  Prof pr(c, c->cur_tag);
   gemm_dmma_kernel<AK, BKI><<<grid, NTHREADS, SMEM_BYTES, c->stream>>>(ma, mb, P);
   post_launch(c, "gemm_dmma_kernel");
 }

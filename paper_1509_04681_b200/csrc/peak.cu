@@ -1,0 +1,62 @@
+// FP64 tensor-pipe peak microbenchmark (test/bench-only export): back-to-back independent
+// DMMA.8x8x4 chains on every SM, timed with CUDA events.  MEASURED_PEAKS.json carries no FP64
+// figure, so bench.py measures this denominator live on the same GPU.
+#include "common.cuh"
+#include "../../include/cggm_testing.h"
+
+namespace cggm {
+namespace {
+
+__global__ void __launch_bounds__(256) k_dmma_peak(double* out, int iters) {
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    c[i][0] = threadIdx.x * 1e-9;
+    c[i][1] = i * 1e-9;
+  }
+  const double a = 1.0000001, b = 0.9999999;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ptx::dmma_8x8x4(c[i][0], c[i][1], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
+}  // namespace
+}  // namespace cggm
+
+using namespace cggm;
+
+extern "C" cggm_status cggm_test_fp64_peak(cggm_ctx* ctx_, double seconds, double* tflops, double* elapsed_ms) {
+  if (!ctx_ || !tflops || !elapsed_ms || !(seconds > 0)) return CGGM_ERR_INVALID_ARG;
+  Ctx* c = reinterpret_cast<Ctx*>(ctx_);  // cggm_ctx wraps Ctx as its only member
+  double* out = nullptr;
+  if (cudaMalloc(&out, 256 * 8) != cudaSuccess) return CGGM_ERR_OOM;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = c->num_sms * 2, threads = 256;
+  // calibrate iterations for the requested duration
+  int iters = 4096;
+  float ms = 0.f;
+  for (int rep = 0; rep < 6; ++rep) {
+    cudaEventRecord(e0, c->stream);
+    k_dmma_peak<<<blocks, threads, 0, c->stream>>>(out, iters);
+    cudaEventRecord(e1, c->stream);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms >= 0.9 * seconds * 1e3) break;
+    double scale = (seconds * 1e3) / (ms > 0.01 ? ms : 0.01);
+    iters = (int)std::min<double>(2e9, iters * scale);
+  }
+  const double flops = 2.0 * 256.0 * 8.0 * (double)iters * blocks * (threads / 32);
+  *tflops = flops / (ms * 1e-3) / 1e12;
+  *elapsed_ms = ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  return cudaGetLastError() == cudaSuccess ? CGGM_OK : CGGM_ERR_CUDA;
+}

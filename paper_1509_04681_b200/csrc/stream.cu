@@ -22,6 +22,7 @@ void densify_csc(Ctx* c, const cggm_csc* A, View D) {
   if (A->ncols == 0 || A->nnz == 0) return;
   const int wpb = 8;
   const int64_t grid = (A->ncols + wpb - 1) / wpb;
+  Prof pr(c, TAG_DENSIFY);
   k_scatter_csc<<<(unsigned)grid, wpb * 32, 0, c->stream>>>(A->colptr, A->rowidx, static_cast<const double*>(A->val),
                                                             A->ncols, D.p, D.ld);
   post_launch(c, "k_scatter_csc");
@@ -71,6 +72,7 @@ __global__ void __launch_bounds__(256) k_spmm_x_theta(const double* __restrict__
 
 void spmm_x_theta(Ctx* c, const double* X, int64_t ldx, int64_t n, const cggm_csc* Theta, View W) {
   if (Theta->ncols == 0 || n == 0) return;
+  Prof pr(c, TAG_SPMM);
   k_spmm_x_theta<<<(unsigned)Theta->ncols, 256, 0, c->stream>>>(X, ldx, n, Theta->colptr, Theta->rowidx,
                                                                 static_cast<const double*>(Theta->val), W.p, W.ld);
   post_launch(c, "k_spmm_x_theta");
@@ -119,6 +121,7 @@ __global__ void k_check_csc(const int64_t* colptr, const int32_t* rowidx, const 
 void check_csc(Ctx* c, const cggm_csc* A, bool symmetric, int* flag_dev) {
   if (A->ncols == 0) return;
   const int64_t grid = (A->ncols + 255) / 256;
+  Prof pr(c, c->cur_tag);
   k_check_csc<<<(unsigned)grid, 256, 0, c->stream>>>(A->colptr, A->rowidx, static_cast<const double*>(A->val),
                                                      A->nrows, A->ncols, A->nnz, symmetric ? 1 : 0, flag_dev);
   post_launch(c, "k_check_csc");
@@ -137,6 +140,7 @@ void grad_lambda(Ctx* c, int64_t q, const double* Syy, int64_t l1, const double*
                  const double* Psi, int64_t l3, double* G, int64_t l4) {
   if (q == 0) return;
   dim3 grid((unsigned)std::min<int64_t>((q + 255) / 256, 64), (unsigned)q);
+  Prof pr(c, c->cur_tag);
   k_grad_lambda<<<grid, 256, 0, c->stream>>>(q, Syy, l1, Sigma, l2, Psi, l3, G, l4);
   post_launch(c, "k_grad_lambda");
 }
@@ -220,6 +224,7 @@ __global__ void __launch_bounds__(256) k_sum_arrays(const double* const* arrs, c
 void col_partials(Ctx* c, int mode, int64_t n, int64_t ncols, const double* A, int64_t lda, const double* B,
                   int64_t ldb, const cggm_csc* csc, double* part) {
   if (ncols == 0) return;
+  Prof pr(c, c->cur_tag);
   k_col_partials<<<(unsigned)ncols, 256, 0, c->stream>>>(mode, n, A, lda, B, ldb, csc ? csc->colptr : nullptr,
                                                          csc ? csc->rowidx : nullptr,
                                                          csc ? static_cast<const double*>(csc->val) : nullptr, part);
@@ -228,12 +233,14 @@ void col_partials(Ctx* c, int mode, int64_t n, int64_t ncols, const double* A, i
 
 void csc_abs_partials(Ctx* c, const cggm_csc* A, bool skip_diag, double* part) {
   if (A->ncols == 0) return;
+  Prof pr(c, c->cur_tag);
   k_csc_abs_partials<<<(unsigned)((A->ncols + 255) / 256), 256, 0, c->stream>>>(
       A->colptr, A->rowidx, static_cast<const double*>(A->val), A->ncols, skip_diag ? 1 : 0, part);
   post_launch(c, "k_csc_abs_partials");
 }
 
 void sum_arrays(Ctx* c, int count, const double* const* arrs_dev, const int64_t* lens_dev, double* out_dev) {
+  Prof pr(c, c->cur_tag);
   k_sum_arrays<<<count, 256, 0, c->stream>>>(arrs_dev, lens_dev, out_dev);
   post_launch(c, "k_sum_arrays");
 }
@@ -248,6 +255,7 @@ __global__ void __launch_bounds__(256) k_sum_vec(const double* a, int64_t len, d
 }
 
 void sum_arrays_1(Ctx* c, const double* a, int64_t len, double* out_dev) {
+  Prof pr(c, c->cur_tag);
   k_sum_vec<<<1, 256, 0, c->stream>>>(a, len, out_dev);
   post_launch(c, "k_sum_vec");
 }
@@ -258,6 +266,7 @@ __global__ void k_init_scalars(int* fail_col, int* flag) {
 }
 
 void init_scalars(Ctx* c, int* fail_col, int* flag) {
+  Prof pr(c, c->cur_tag);
   k_init_scalars<<<1, 1, 0, c->stream>>>(fail_col, flag);
   post_launch(c, "k_init_scalars");
 }
