@@ -15,6 +15,9 @@ extern "C" {
 cggm_status cggm_test_gemm(cggm_ctx* ctx, int transA, int transB, int64_t M, int64_t N, int64_t K,
                            const double* A, int64_t lda, const double* B, int64_t ldb,
                            double* C, int64_t ldc, double alpha, double beta, int flags);
+/* Force the GEMM CTA tile: bits 0-1: 0 = automatic, 1 = 128x128 (8 warps), 2 = 64x64 (4 warps);
+ * bit 2: never use the single 3-D TMA box for MN-inner operands (16-wide 2-D boxes instead). */
+cggm_status cggm_test_set_tile(cggm_ctx* ctx, int mode);
 /* FP64 tensor-pipe peak: independent DMMA.8x8x4 chains on 2 CTAs/SM for ~`seconds`; returns the
  * achieved TFLOP/s and the timed milliseconds (the roofline denominator bench.py reports). */
 cggm_status cggm_test_fp64_peak(cggm_ctx* ctx, double seconds, double* tflops, double* elapsed_ms);

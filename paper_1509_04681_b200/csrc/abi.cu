@@ -439,12 +439,12 @@ cggm_status cggm_psi_grad(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64
     {
       Phase ph(c, TAG_PSI);
       Epilogue e; e.out1 = static_cast<double*>(Psi); e.ld1 = ldpsi; e.a1 = 1.0;
-      if (GradL) {
-        e.out2 = static_cast<double*>(GradL); e.ld2 = ldgl; e.a2 = -1.0;
-        e.in2a = static_cast<const double*>(Syy); e.ld2a = ldsyy; e.b2 = 1.0;
-        e.in2b = Sg; e.ld2b = ldsigma; e.c2 = -1.0;
-      }
       gemm(c, true, false, q, q, n_local, R, ldn, R, ldn, e, SYM_LOWER | SYM_MIRROR);
+      // grad_Lambda = (S_yy - Sigma) - Psi as one coalesced streaming pass (cheaper than a
+      // mirrored two-input epilogue; same operation order as Eq. 3)
+      if (GradL)
+        grad_lambda(c, q, static_cast<const double*>(Syy), ldsyy, Sg, ldsigma, static_cast<const double*>(Psi), ldpsi,
+                    static_cast<double*>(GradL), ldgl);
     }
     // a5: GradT = (2/n) X^T E   (or 2 S_xy + (2/sqrt n) X^T R)
     if (GradT) {
@@ -503,14 +503,16 @@ cggm_status cggm_objective(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int6
     validate_csc_dev(c, Lambda, true, "Lambda");
     validate_csc_dev(c, Theta, false, "Theta");
     const int64_t ldn = even(n_local > 0 ? n_local : 1);
-    const int64_t lda = even(q);
     const int nb = leaf_nb();
     const int64_t nleaves = (q + nb - 1) / nb;
     const double* Yd = static_cast<const double*>(Y);
-    // W = X Theta (or caller's W), Z := W (to be solved in place)
+    // augmented dense [Lambda; W] ((q + n_local) x q): the Cholesky of the trial Lambda (the PD
+    // test) leaves Z = W L^{-T} in the bottom rows, ||Z||_F^2 = tr(Lambda^{-1} W^T W) (reading A14)
+    const int64_t ldaug = even(q + n_local);
+    double* A = static_cast<double*>(ws_get(c, WS_DENSE_A, (size_t)ldaug * q * 8));
+    double* leafinv = static_cast<double*>(ws_get(c, WS_LEAFINV, (size_t)nleaves * nb * nb * 8));
     const double* Wd;
     int64_t ldwd;
-    double* Z = static_cast<double*>(ws_get(c, WS_Z, (size_t)ldn * q * 8));
     if (W) {
       Wd = static_cast<const double*>(W);
       ldwd = ldw;
@@ -520,10 +522,6 @@ cggm_status cggm_objective(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int6
       Wd = Wb;
       ldwd = ldn;
     }
-    copy2d(c, View{Z, ldn, n_local, q}, Wd, ldwd);
-    // Cholesky of the trial Lambda (the PD test), leaf inverses kept for the triangular solve
-    double* A = static_cast<double*>(ws_get(c, WS_DENSE_A, (size_t)lda * q * 8));
-    double* leafinv = static_cast<double*>(ws_get(c, WS_LEAFINV, (size_t)nleaves * nb * nb * 8));
     Scal s = scal(c, 16 + 6 * q + nleaves);
     double* res = s.dbl;            // [0..5] sums, [8] logdet
     double* partY = s.dbl + 16;
@@ -532,19 +530,17 @@ cggm_status cggm_objective(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int6
     double* penLp = partZ + q;
     double* penTp = penLp + q;
     double* slots = penTp + q;
-    View Av{A, lda, q, q};
-    densify_csc(c, Lambda, Av);
+    densify_csc(c, Lambda, View{A, ldaug, q, q});
+    copy2d(c, View{A + q, ldaug, n_local, q}, Wd, ldwd);
     init_scalars(c, s.fail, s.flag);
-    potrf_recursive(c, Av, View{nullptr, lda, q, q}, false, leafinv, slots, s.fail, nullptr, 0);
-    // Z = W L^{-T}:  ||Z||_F^2 = tr(Lambda^{-1} W^T W)  (reading A14)
-    {
-      Phase ph(c, TAG_TRSM);
-      trsm_right_lt(c, View{Z, ldn, n_local, q}, Av, leafinv, 0);
-    }
+    potrf_recursive(c, View{A, ldaug, q + n_local, q}, View{nullptr, ldaug, q, q}, false, leafinv, slots, s.fail,
+                    nullptr, 0);
+    const double* Z = A + q;
+    const int64_t ldz = ldaug;
     Phase ph(c, TAG_OBJRED);
     col_partials(c, 0, n_local, q, Yd, ldy, nullptr, 0, Lambda, partY);
     col_partials(c, 1, n_local, q, Wd, ldwd, Yd, ldy, nullptr, partWY);
-    col_partials(c, 2, n_local, q, Z, ldn, nullptr, 0, nullptr, partZ);
+    col_partials(c, 2, n_local, q, Z, ldz, nullptr, 0, nullptr, partZ);
     csc_abs_partials(c, Lambda, penalize_diag == 0, penLp);
     csc_abs_partials(c, Theta, false, penTp);
     sum_arrays_1(c, partY, q, res + 0);
@@ -594,4 +590,11 @@ extern "C" cggm_status cggm_test_gemm(cggm_ctx* ctx, int transA, int transB, int
     if (beta != 0.0) { e.in1a = C; e.ld1a = ldc; e.b1 = beta; }
     gemm(c, transA != 0, transB != 0, M, N, K, A, lda, B, ldb, e, flags);
   });
+}
+
+extern "C" cggm_status cggm_test_set_tile(cggm_ctx* ctx, int mode) {
+  if (!ctx || mode < 0 || mode > 6) return CGGM_ERR_INVALID_ARG;
+  ctx->impl.force_tile = mode & 3;
+  ctx->impl.no_tma3d = (mode & 4) ? 1 : 0;
+  return CGGM_OK;
 }

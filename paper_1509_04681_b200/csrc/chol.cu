@@ -25,63 +25,126 @@ constexpr int NB = 64;
 constexpr int LEAF_THREADS = 256;
 constexpr int LEAF_SMEM = 2 * NB * (NB + 1) * 8;
 
+// Leaf: Cholesky + triangular inverse of one nb x nb (nb <= 64) diagonal block in one CTA.
+// 256 threads; thread t owns the 4x4 register blocks rows 4*(t&15).., cols 4*(t>>4).. of both
+// the factor (a) and the inverse (x); rows/columns >= nb are padded with the identity (so L and
+// L^{-1} are block-diag(., I)).  One fused sweep, ONE __syncthreads per column j:
+//   before the barrier  - the owners of column j (one half-warp) receive the pivot d by warp
+//     shuffle, test it, form inv = 1/sqrt(d), scale column j and publish it; the owners of row j
+//     of X publish that row (not yet divided by L_jj);
+//   after the barrier   - every thread applies the rank-1 Cholesky update to its block of a and
+//     the forward-substitution update X[i,:] -= L_ij * X[j,:] * inv to its block of x.
+// Buffers are double-buffered by column parity so no second barrier is needed.  The pivot test
+// !(d > 0) records the first failing column (reading A10); log L_jj is summed in a fixed order.
 __global__ void __launch_bounds__(LEAF_THREADS) leaf_potrf_trtri(double* A, int64_t lda, int nb, double* X,
                                                                   int64_t ldx, int write_L, double* logdet_slot,
                                                                   int* fail_col, int col0) {
   extern __shared__ double leaf_smem[];
-  double(*S)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(leaf_smem);             // S[col][row] -> L
-  double(*Xs)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(leaf_smem + NB * (NB + 1));  // Xs[col][row] -> L^{-1}
-  __shared__ int failed;
-  const int tid = threadIdx.x;
-  for (int idx = tid; idx < NB * NB; idx += LEAF_THREADS) {
-    const int i = idx % NB, j = idx / NB;
-    S[j][i] = (i < nb && j < nb && i >= j) ? A[i + (int64_t)j * lda] : 0.0;
-    Xs[j][i] = (i == j) ? 1.0 : 0.0;
+  double(*Ls)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(leaf_smem);                   // Ls[col][row]
+  double(*Xs)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(leaf_smem + NB * (NB + 1));  // Xs[col][row]
+  __shared__ double cbuf[2][NB + 1];  // column j of L (rows > j); [NB] = 1/L_jj
+  __shared__ double rbuf[2][NB];      // row j of X before the division by L_jj
+  __shared__ double diag[NB];
+  __shared__ int fail_sm;
+  const int t = threadIdx.x, rb = t & 15, cb = t >> 4, lane = t & 31;
+  for (int idx = t; idx < NB * NB; idx += LEAF_THREADS) {
+    const int i = idx & (NB - 1), j = idx >> 6;
+    double v;
+    if (i < nb && j < nb) v = (i >= j) ? A[i + (int64_t)j * lda] : 0.0;
+    else v = (i == j) ? 1.0 : 0.0;
+    Ls[j][i] = v;
   }
-  if (tid == 0) failed = -1;
+  if (t == 0) fail_sm = INT_MAX;
   __syncthreads();
-  // unblocked right-looking Cholesky (column j: pivot, scale, rank-1 trailing update)
-  for (int j = 0; j < nb; ++j) {
-    const double d = S[j][j];
-    const bool bad = !(d > 0.0) || !isfinite(d);
-    const double ljj = sqrt(d);
-    const double inv = 1.0 / ljj;
-    __syncthreads();
-    if (tid == 0) {
-      if (bad && failed < 0) failed = j;
-      S[j][j] = ljj;
+  double a[4][4], x[4][4];
+#pragma unroll
+  for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      a[ii][kk] = Ls[4 * cb + kk][4 * rb + ii];
+      x[ii][kk] = (4 * rb + ii == 4 * cb + kk) ? 1.0 : 0.0;
     }
-    for (int i = j + 1 + tid; i < nb; i += LEAF_THREADS) S[j][i] *= inv;
-    __syncthreads();
-    const int rem = nb - j - 1;
-    for (int idx = tid; idx < rem * rem; idx += LEAF_THREADS) {
-      const int ii = idx % rem, kk = idx / rem;
-      if (ii >= kk) S[j + 1 + kk][j + 1 + ii] -= S[j][j + 1 + ii] * S[j][j + 1 + kk];
+  const bool has_lower = (rb >= cb);
+  for (int jb = 0; jb < 16; ++jb) {
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int j = 4 * jb + jj;
+      double* cv = cbuf[jj & 1];
+      double* rv = rbuf[jj & 1];
+      if (cb == jb) {  // column-j owners (a half-warp)
+        const unsigned hmask = (lane & 16) ? 0xffff0000u : 0x0000ffffu;
+        const double d = __shfl_sync(hmask, a[jj][jj], (lane & 16) | jb);
+        const double inv = rsqrt(d);
+        const double ljj = d * inv;
+        if (rb == jb) {
+          if (!(d > 0.0) || !isfinite(d)) atomicMin(&fail_sm, j);
+          diag[j] = ljj;
+          cv[NB] = inv;
+          a[jj][jj] = ljj;
+        }
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii) {
+          const int i = 4 * rb + ii;
+          if (i > j) {
+            a[ii][jj] *= inv;
+            cv[i] = a[ii][jj];
+          }
+        }
+      }
+      if (rb == jb) {  // row-j owners of X publish the undivided row (columns <= j)
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) rv[4 * cb + cc] = x[jj][cc];
+      }
+      __syncthreads();
+      const double inv = cv[NB];
+      if (rb == jb) {
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) x[jj][cc] *= inv;
+      }
+      if (4 * rb + 3 > j) {
+        double li[4], lk[4], xr[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          li[u] = cv[4 * rb + u];
+          lk[u] = cv[4 * cb + u];
+          xr[u] = rv[4 * cb + u] * inv;
+        }
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const int i = 4 * rb + ii, k = 4 * cb + kk;
+            if (i > j) {
+              if (has_lower && k > j && i >= k) a[ii][kk] = fma(-li[ii], lk[kk], a[ii][kk]);
+              if (k <= j) x[ii][kk] = fma(-li[ii], xr[kk], x[ii][kk]);
+            }
+          }
+      }
     }
-    __syncthreads();
   }
-  // triangular inverse: forward substitution L X = I, column of L by column of L
-  for (int j = 0; j < nb; ++j) {
-    const double ljj = S[j][j];
-    for (int c = tid; c <= j; c += LEAF_THREADS) Xs[c][j] /= ljj;
-    __syncthreads();
-    const int rem = nb - j - 1;
-    for (int idx = tid; idx < rem * (j + 1); idx += LEAF_THREADS) {
-      const int ii = idx % rem, c = idx / rem;
-      Xs[c][j + 1 + ii] -= S[j][j + 1 + ii] * Xs[c][j];
+#pragma unroll
+  for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const int i = 4 * rb + ii, k = 4 * cb + kk;
+      Ls[k][i] = (i >= k) ? a[ii][kk] : 0.0;
+      Xs[k][i] = x[ii][kk];
     }
-    __syncthreads();
-  }
-  for (int idx = tid; idx < nb * nb; idx += LEAF_THREADS) {
+  __syncthreads();
+  for (int idx = t; idx < nb * nb; idx += LEAF_THREADS) {
     const int i = idx % nb, j = idx / nb;
-    if (write_L) A[i + (int64_t)j * lda] = (i >= j) ? S[j][i] : 0.0;
-    X[i + (int64_t)j * ldx] = (i >= j) ? Xs[j][i] : 0.0;
+    if (write_L) A[i + (int64_t)j * lda] = Ls[j][i];
+    X[i + (int64_t)j * ldx] = Xs[j][i];
   }
-  if (tid == 0) {
+  if (t < 32) {  // 2 sum ln L_jj, fixed order: lane-strided partials then a fixed shuffle tree
     double s = 0.0;
-    for (int j = 0; j < nb; ++j) s += log(S[j][j]);
-    *logdet_slot = 2.0 * s;
-    if (failed >= 0) atomicMin(fail_col, col0 + failed);
+    for (int j = t; j < NB; j += 32) s += log(diag[j]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (t == 0) {
+      *logdet_slot = 2.0 * s;
+      if (fail_sm != INT_MAX && fail_sm < nb) atomicMin(fail_col, col0 + fail_sm);
+    }
   }
 }
 
@@ -125,16 +188,26 @@ void leaf(Rec& R, View A, View X, int64_t col0) {
   post_launch(R.c, "leaf_potrf_trtri");
 }
 
+// A is (n + extra) x n: the square block being factored with `extra` appended rows below it
+// (potrf-only mode).  Factoring the augmented [Lambda; W] leaves Z = W L^{-T} in the bottom rows
+// (block Cholesky of [[Lambda, W^T], [W, .]]), so the objective's triangular solve is carried by
+// the same recursive GEMMs with taller panels.
 void node(Rec& R, View A, View X, int64_t col0) {
-  const int64_t n = A.rows;
+  const int64_t n = A.cols, extra = A.rows - A.cols;
+  Ctx* c = R.c;
   if (n <= NB) {
-    leaf(R, A, X, col0);
+    leaf(R, A.sub(0, 0, n, n), X, col0);
+    if (extra > 0) {  // bottom rows: B := B Xleaf^T (N <= 64: one tile column, in place)
+      const double* xl = R.leafinv + (col0 / NB) * NB * NB;
+      Epilogue e; e.out1 = A.p + n; e.ld1 = A.ld;
+      gemm(c, false, true, extra, n, n, A.p + n, A.ld, xl, NB, e, B_KLE_N);
+    }
     return;
   }
   const int64_t n1 = split_point(n), n2 = n - n1;
-  View A11 = A.sub(0, 0, n1, n1), A21 = A.sub(n1, 0, n2, n1), A22 = A.sub(n1, n1, n2, n2);
-  Ctx* c = R.c;
+  View A11 = A.sub(0, 0, n1, n1), A21 = A.sub(n1, 0, n2 + extra, n1), A22 = A.sub(n1, n1, n2 + extra, n2);
   if (R.full_inverse) {
+    if (extra) throw CudaError{CGGM_ERR_UNSUPPORTED, "augmented rows need potrf-only mode"};
     View X11 = X.sub(0, 0, n1, n1), X21 = X.sub(n1, 0, n2, n1), X22 = X.sub(n1, n1, n2, n2);
     node(R, A11, X11, col0);
     View T{R.tmp, n2 + (n2 & 1), n2, n1};
@@ -159,9 +232,9 @@ void node(Rec& R, View A, View X, int64_t col0) {
   } else {
     node(R, A11, X, col0);
     trsm_right_lt(c, A21, A11, R.leafinv, col0);
-    {
+    {  // A22 -= A21 A21^T over the lower trapezoid (square part + appended rows)
       Epilogue e; e.out1 = A22.p; e.ld1 = A22.ld; e.a1 = -1.0; e.in1a = A22.p; e.ld1a = A22.ld; e.b1 = 1.0;
-      gemm(c, false, true, n2, n2, n1, A21.p, A21.ld, A21.p, A21.ld, e, SYM_LOWER);
+      gemm(c, false, true, n2 + extra, n2, n1, A21.p, A21.ld, A21.p, A21.ld, e, SYM_LOWER);
     }
     node(R, A22, X, col0 + n1);
   }

@@ -22,42 +22,68 @@
 namespace cggm {
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16;
-constexpr int NCW = 8;                       // consumer warps (thread 0 also issues TMA)
-constexpr int NTHREADS = NCW * 32;
+constexpr int BK = 16;
 constexpr int STAGES = 4;
-constexpr int OP_BYTES = BM * BK * 8;        // 16 KB per operand per stage
-constexpr int STAGE_BYTES = 2 * OP_BYTES;
-constexpr int EPI_LD = BM + 1;
-constexpr int EPI_BYTES = BN * EPI_LD * 8;
-constexpr int MAIN_BYTES = STAGES * STAGE_BYTES;
-constexpr int DATA_BYTES = MAIN_BYTES > EPI_BYTES ? MAIN_BYTES : EPI_BYTES;
-constexpr int SMEM_BYTES = DATA_BYTES + 1024 + 2 * STAGES * 8;
 constexpr int GROUP_N = 8;
+
+// CTA tile BM_ x BN_ computed by WM_ x WN_ warps (warp tile (BM_/WM_) x (BN_/WN_), fragments of 8)
+template <int BM_, int BN_, int WM_, int WN_>
+struct Cfg {
+  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_;
+  static constexpr int NTHREADS = WM * WN * 32;
+  static constexpr int WTM = BM / WM, WTN = BN / WN;
+  static constexpr int FM = WTM / 8, FN = WTN / 8;
+  static constexpr int A_BYTES = BM * BK * 8, B_BYTES = BN * BK * 8;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int EPI_LD = BM + 1;
+  static constexpr int EPI_BYTES = BN * EPI_LD * 8;
+  static constexpr int MAIN_BYTES = STAGES * STAGE_BYTES;
+  static constexpr int DATA_BYTES = MAIN_BYTES > EPI_BYTES ? MAIN_BYTES : EPI_BYTES;
+  static constexpr int SMEM_BYTES = DATA_BYTES + 1024 + 2 * STAGES * 8;
+  static_assert(FM % 2 == 0 && FN % 2 == 0, "MN-inner fragments come in pairs");
+  static_assert(BM % 16 == 0 && BN % 16 == 0, "16-wide TMA boxes");
+};
+using CfgBig = Cfg<128, 128, 2, 4>;    // 8 warps, warp tile 64 x 32
+using CfgSmall = Cfg<64, 64, 2, 2>;    // 4 warps, warp tile 32 x 32
 
 struct KParams {
   int M, N, K;
   int tilesM, tilesN;
   int flags;
+  int a3d, b3d;  // MN-inner operand loaded with one 3-D TMA box (extent multiple of 16)
   Epilogue epi;
 };
 
+// Tile order.  SYM_LOWER: the lower trapezoid {I >= J} of a tilesM x tilesN grid (M >= N),
+// enumerated column-block by column-block from the right edge of the triangle.  Otherwise groups
+// of GROUP_N tile columns (an A row panel is reused across the group while it sits in L2).
+// Triangular k-ranges are scheduled longest-first (LPT) to shorten the tail wave.
 __device__ __forceinline__ void tile_coords(const KParams& P, int t, int& I, int& J) {
   if (P.flags & SYM_LOWER) {
-    int i = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
-    while ((long long)(i + 1) * (i + 2) / 2 <= t) ++i;
-    while ((long long)i * (i + 1) / 2 > t) --i;
-    I = i;
-    J = t - (int)((long long)i * (i + 1) / 2);
-  } else {
-    const int per_group = GROUP_N * P.tilesM;
-    const int gi = t / per_group;
-    const int local = t - gi * per_group;
-    const int nb0 = gi * GROUP_N;
-    const int width = min(GROUP_N, P.tilesN - nb0);
-    I = local / width;
-    J = nb0 + local % width;
+    // lower triangle part: rows I < tilesN, enumerated row-major (I ascending, J <= I)
+    const long long tri = (long long)P.tilesN * (P.tilesN + 1) / 2;
+    if (t < tri) {
+      int i = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+      while ((long long)(i + 1) * (i + 2) / 2 <= t) ++i;
+      while ((long long)i * (i + 1) / 2 > t) --i;
+      I = i;
+      J = t - (int)((long long)i * (i + 1) / 2);
+    } else {
+      const int r = t - (int)tri;  // rectangular part below: rows tilesN .. tilesM-1
+      I = P.tilesN + r / P.tilesN;
+      J = r % P.tilesN;
+    }
+    return;
   }
+  const int per_group = GROUP_N * P.tilesM;
+  const int gi = t / per_group;
+  const int local = t - gi * per_group;
+  const int nb0 = gi * GROUP_N;
+  const int width = min(GROUP_N, P.tilesN - nb0);
+  I = local / width;
+  J = nb0 + local % width;
+  if (P.flags & B_KLE_N) J = P.tilesN - 1 - J;   // k-range grows with J: start from the right
+  if (P.flags & A_KLE_M) I = P.tilesM - 1 - I;   // k-range grows with I: start from the bottom
 }
 
 __device__ __forceinline__ void epi_apply(const Epilogue& E, int64_t r, int64_t c, double v) {
@@ -82,10 +108,13 @@ __device__ __forceinline__ int frag_x(int f, int r) {
   return 16 * (f >> 1) + 2 * r + (f & 1);
 }
 
-template <bool AK, bool BKI>
-__global__ void __launch_bounds__(NTHREADS, 1)
+template <bool AK, bool BKI, class C>
+__global__ void __launch_bounds__(C::NTHREADS, 1)
     gemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const KParams P) {
+  constexpr int BM = C::BM, BN = C::BN, NCW = C::WM * C::WN, FM = C::FM, FN = C::FN;
+  constexpr int OP_BYTES = C::A_BYTES, STAGE_BYTES = C::STAGE_BYTES, DATA_BYTES = C::DATA_BYTES;
+  constexpr int EPI_LD = C::EPI_LD, NTHREADS = C::NTHREADS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + DATA_BYTES);
@@ -113,14 +142,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
   __syncthreads();
 
-  double acc[8][4][2];
+  double acc[FM][FN][2];
 #pragma unroll
-  for (int a = 0; a < 8; ++a)
+  for (int a = 0; a < FM; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int b = 0; b < FN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
   const int g = lane >> 2, t = lane & 3;
-  const int wm = warp >> 2, wn = warp & 3;
+  const int wm = warp / C::WN, wn = warp % C::WN;
+  const int xa0 = wm * C::WTM, xb0 = wn * C::WTN;
 
   // ------------------------------------------------ TMA producer: thread 0, STAGES-1 tiles ahead
   uint32_t tx_bytes = 0;
@@ -133,7 +163,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int xb = 0; xb < BM / 16; ++xb) a_boxes += (m0 + xb * 16 < P.M);
   if (!BKI)
     for (int xb = 0; xb < BN / 16; ++xb) b_boxes += (n0 + xb * 16 < P.N);
-  tx_bytes = (AK ? OP_BYTES : a_boxes * 2048) + (BKI ? OP_BYTES : b_boxes * 2048);
+  tx_bytes = ((AK || P.a3d) ? C::A_BYTES : a_boxes * 2048) + ((BKI || P.b3d) ? C::B_BYTES : b_boxes * 2048);
   auto issue = [&](int i) {
     const int s = i % STAGES;
     uint8_t* sa = smem + s * STAGE_BYTES;
@@ -142,11 +172,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int k = (kt0 + i) * BK;
     if (AK) {
       ptx::tma_load_2d(sa, &tmA, &full[s], k, m0);
+    } else if (P.a3d) {
+      ptx::tma_load_3d(sa, &tmA, &full[s], 0, k, m0 / 16);
     } else {
       for (int xb = 0; xb < a_boxes; ++xb) ptx::tma_load_2d(sa + xb * 2048, &tmA, &full[s], m0 + xb * 16, k);
     }
     if (BKI) {
       ptx::tma_load_2d(sb, &tmB, &full[s], k, n0);
+    } else if (P.b3d) {
+      ptx::tma_load_3d(sb, &tmB, &full[s], 0, k, n0 / 16);
     } else {
       for (int xb = 0; xb < b_boxes; ++xb) ptx::tma_load_2d(sb + xb * 2048, &tmB, &full[s], n0 + xb * 16, k);
     }
@@ -162,18 +196,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const uint32_t sb = sa + OP_BYTES;
 #pragma unroll
       for (int kk = 0; kk < 2; ++kk) {
-        double a[8][2], b[4][2];
+        double a[FM][2], b[FN][2];
         if (AK) {
 #pragma unroll
-          for (int f = 0; f < 8; ++f) {
-            const int x = wm * 64 + frag_x<true>(f, g);
+          for (int f = 0; f < FM; ++f) {
+            const int x = xa0 + frag_x<true>(f, g);
             const int chunk = (4 * kk + t) ^ (x & 7);
             ptx::lds128(a[f][0], a[f][1], sa + x * 128 + chunk * 16);
           }
         } else {
 #pragma unroll
-          for (int pr = 0; pr < 4; ++pr) {
-            const int xb = wm * 4 + pr;
+          for (int pr = 0; pr < FM / 2; ++pr) {
+            const int xb = xa0 / 16 + pr;
 #pragma unroll
             for (int s2 = 0; s2 < 2; ++s2) {
               const int k = 8 * kk + 2 * t + s2;
@@ -184,15 +218,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         if (BKI) {
 #pragma unroll
-          for (int f = 0; f < 4; ++f) {
-            const int x = wn * 32 + frag_x<true>(f, g);
+          for (int f = 0; f < FN; ++f) {
+            const int x = xb0 + frag_x<true>(f, g);
             const int chunk = (4 * kk + t) ^ (x & 7);
             ptx::lds128(b[f][0], b[f][1], sb + x * 128 + chunk * 16);
           }
         } else {
 #pragma unroll
-          for (int pr = 0; pr < 2; ++pr) {
-            const int xb = wn * 2 + pr;
+          for (int pr = 0; pr < FN / 2; ++pr) {
+            const int xb = xb0 / 16 + pr;
 #pragma unroll
             for (int s2 = 0; s2 < 2; ++s2) {
               const int k = 8 * kk + 2 * t + s2;
@@ -204,9 +238,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
         for (int s2 = 0; s2 < 2; ++s2)
 #pragma unroll
-          for (int fm = 0; fm < 8; ++fm)
+          for (int fm = 0; fm < FM; ++fm)
 #pragma unroll
-            for (int fn = 0; fn < 4; ++fn) ptx::dmma_8x8x4(acc[fm][fn][0], acc[fm][fn][1], a[fm][s2], b[fn][s2]);
+            for (int fn = 0; fn < FN; ++fn) ptx::dmma_8x8x4(acc[fm][fn][0], acc[fm][fn][1], a[fm][s2], b[fn][s2]);
       }
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&empty[s]);
@@ -225,13 +259,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   double* Cs = reinterpret_cast<double*>(smem);
   {
 #pragma unroll
-    for (int fm = 0; fm < 8; ++fm) {
-      const int ml = wm * 64 + frag_x<AK>(fm, g);
+    for (int fm = 0; fm < FM; ++fm) {
+      const int ml = xa0 + frag_x<AK>(fm, g);
 #pragma unroll
-      for (int fn = 0; fn < 4; ++fn)
+      for (int fn = 0; fn < FN; ++fn)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          const int nl = wn * 32 + frag_x<BKI>(fn, 2 * t + j);
+          const int nl = xb0 + frag_x<BKI>(fn, 2 * t + j);
           Cs[nl * EPI_LD + ml] = acc[fm][fn][j];
         }
     }
@@ -239,7 +273,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   const bool diag = (P.flags & SYM_LOWER) && I == J;
   for (int idx = threadIdx.x; idx < BM * BN; idx += NTHREADS) {
-    const int ml = idx & (BM - 1), nl = idx >> 7;
+    const int ml = idx % BM, nl = idx / BM;
     const int m = m0 + ml, n = n0 + nl;
     if (m >= P.M || n >= P.N) continue;
     if (diag && m < n) continue;
@@ -247,13 +281,29 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
   if (P.flags & SYM_MIRROR) {
     for (int idx = threadIdx.x; idx < BM * BN; idx += NTHREADS) {
-      const int nl = idx & (BN - 1), ml = idx >> 7;
+      const int nl = idx % BN, ml = idx / BN;
       const int m = m0 + ml, n = n0 + nl;
       if (m >= P.M || n >= P.N) continue;
       if (diag && m <= n) continue;
       epi_apply(P.epi, n, m, Cs[nl * EPI_LD + ml]);
     }
   }
+}
+
+// MN-inner operand as a 3-D tensor {16 (x mod 16), K, X/16} with strides {ld*8, 128 B}: one TMA box
+// {16, 16, BX/16} fills the whole [x/16][k][x%16] tile.  Only when X % 16 == 0 (no read past X).
+CUtensorMap make_map_mn3d(Ctx* c, const double* ptr, int64_t ld, int64_t X, int64_t K, uint32_t bx) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {16, (cuuint64_t)K, (cuuint64_t)(X / 16)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 8), 128};
+  cuuint32_t box[3] = {16, 16, bx / 16};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = c->encode_tiled(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(ptr), dims, strides, box,
+                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw CudaError{CGGM_ERR_CUDA, "cuTensorMapEncodeTiled (3d) failed (" + std::to_string((int)r) + ")"};
+  return m;
 }
 
 CUtensorMap make_map(Ctx* c, const double* ptr, int64_t ld, int64_t inner, int64_t outer, uint32_t box_inner,
@@ -271,17 +321,39 @@ CUtensorMap make_map(Ctx* c, const double* ptr, int64_t ld, int64_t inner, int64
   return m;
 }
 
-template <bool AK, bool BKI>
+template <bool AK, bool BKI, class C>
 void launch(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KParams& P, int grid) {
   static bool attr_set = false;
   if (!attr_set) {
-    CGGM_CUDA_CHECK(cudaFuncSetAttribute(gemm_dmma_kernel<AK, BKI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         SMEM_BYTES));
+    CGGM_CUDA_CHECK(cudaFuncSetAttribute(gemm_dmma_kernel<AK, BKI, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM_BYTES));
     attr_set = true;
   }
   Prof pr(c, c->cur_tag);
-  gemm_dmma_kernel<AK, BKI><<<grid, NTHREADS, SMEM_BYTES, c->stream>>>(ma, mb, P);
+  gemm_dmma_kernel<AK, BKI, C><<<grid, C::NTHREADS, C::SMEM_BYTES, c->stream>>>(ma, mb, P);
   post_launch(c, "gemm_dmma_kernel");
+}
+
+template <class C>
+void run_cfg(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t Keff, const double* A, int64_t lda,
+             const double* B, int64_t ldb, KParams& P) {
+  P.tilesM = (int)((M + C::BM - 1) / C::BM);
+  P.tilesN = (int)((N + C::BN - 1) / C::BN);
+  int grid;
+  if (P.flags & SYM_LOWER) grid = P.tilesN * (P.tilesN + 1) / 2 + (P.tilesM - P.tilesN) * P.tilesN;
+  else grid = P.tilesM * P.tilesN;
+  // K-inner operand: dims {K, X}, box {16, BX}; MN-inner: dims {X, K}, box {16, 16}
+  P.a3d = (!transA && M % 16 == 0 && !c->no_tma3d) ? 1 : 0;
+  P.b3d = (transB && N % 16 == 0 && !c->no_tma3d) ? 1 : 0;
+  CUtensorMap ma = transA ? make_map(c, A, lda, Keff, M, 16, C::BM)
+                          : (P.a3d ? make_map_mn3d(c, A, lda, M, Keff, C::BM) : make_map(c, A, lda, M, Keff, 16, 16));
+  CUtensorMap mb = transB ? (P.b3d ? make_map_mn3d(c, B, ldb, N, Keff, C::BN) : make_map(c, B, ldb, N, Keff, 16, 16))
+                          : make_map(c, B, ldb, Keff, N, 16, C::BN);
+  const bool AK = transA, BKI = !transB;
+  if (AK && BKI) launch<true, true, C>(c, ma, mb, P, grid);
+  else if (AK && !BKI) launch<true, false, C>(c, ma, mb, P, grid);
+  else if (!AK && BKI) launch<false, true, C>(c, ma, mb, P, grid);
+  else launch<false, false, C>(c, ma, mb, P, grid);
 }
 
 bool tma_ok(const double* p, int64_t ld) {
@@ -318,25 +390,16 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
   }
   KParams P;
   P.M = (int)M; P.N = (int)N; P.K = (int)(K > 0 ? K : 0);
-  P.tilesM = (int)((M + BM - 1) / BM);
-  P.tilesN = (int)((N + BN - 1) / BN);
   P.flags = flags;
   P.epi = epi;
-  int grid;
-  if (flags & SYM_LOWER) {
-    if (M != N) throw CudaError{CGGM_ERR_SHAPE, "SYM_LOWER gemm needs M == N"};
-    grid = P.tilesM * (P.tilesM + 1) / 2;
-  } else {
-    grid = P.tilesM * P.tilesN;
-  }
-  // K-inner operand: dims {K, X}, box {16, 128}; MN-inner: dims {X, K}, box {16, 16}
-  CUtensorMap ma = transA ? make_map(c, A, lda, Keff, M, 16, BM) : make_map(c, A, lda, M, Keff, 16, 16);
-  CUtensorMap mb = transB ? make_map(c, B, ldb, N, Keff, 16, 16) : make_map(c, B, ldb, Keff, N, 16, BN);
-  const bool AK = transA, BKI = !transB;
-  if (AK && BKI) launch<true, true>(c, ma, mb, P, grid);
-  else if (AK && !BKI) launch<true, false>(c, ma, mb, P, grid);
-  else if (!AK && BKI) launch<false, true>(c, ma, mb, P, grid);
-  else launch<false, false>(c, ma, mb, P, grid);
+  if ((flags & SYM_LOWER) && (M < N || ((flags & SYM_MIRROR) && M != N)))
+    throw CudaError{CGGM_ERR_SHAPE, "SYM_LOWER gemm needs M >= N (M == N with SYM_MIRROR)"};
+  // 128x128 tiles unless they cannot fill the GPU; then 64x64 tiles (4x the CTAs, several per SM)
+  const int64_t tm = (M + 127) / 128, tn = (N + 127) / 128;
+  const int64_t big_tiles = (flags & SYM_LOWER) ? tn * (tn + 1) / 2 + (tm - tn) * tn : tm * tn;
+  const bool use_big = c->force_tile ? (c->force_tile == 1) : (big_tiles >= c->num_sms);
+  if (use_big) run_cfg<CfgBig>(c, transA, transB, M, N, Keff, A, lda, B, ldb, P);
+  else run_cfg<CfgSmall>(c, transA, transB, M, N, Keff, A, lda, B, ldb, P);
 }
 
 }  // namespace cggm

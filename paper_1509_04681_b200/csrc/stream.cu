@@ -128,20 +128,23 @@ void check_csc(Ctx* c, const cggm_csc* A, bool symmetric, int* flag_dev) {
 }
 
 // ------------------------------------------------------------------ grad_Lambda elementwise
-__global__ void k_grad_lambda(int64_t q, const double* __restrict__ Syy, int64_t l1, const double* __restrict__ Sg,
-                              int64_t l2, const double* __restrict__ Psi, int64_t l3, double* __restrict__ G,
-                              int64_t l4) {
-  const int64_t j = blockIdx.y;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < q; i += (int64_t)gridDim.x * blockDim.x)
-    G[i + j * l4] = __dadd_rn(__dadd_rn(Syy[i + j * l1], -Sg[i + j * l2]), -Psi[i + j * l3]);
+__global__ void __launch_bounds__(256) k_grad_lambda(int64_t q, const double* __restrict__ Syy, int64_t l1,
+                                                     const double* __restrict__ Sg, int64_t l2,
+                                                     const double* __restrict__ Psi, int64_t l3,
+                                                     double* __restrict__ G, int64_t l4) {
+  const int64_t j = blockIdx.x;
+  const double* a = Syy + j * l1;
+  const double* b = Sg + j * l2;
+  const double* c = Psi + j * l3;
+  double* g = G + j * l4;
+  for (int64_t i = threadIdx.x; i < q; i += 256) g[i] = __dadd_rn(__dadd_rn(a[i], -b[i]), -c[i]);
 }
 
 void grad_lambda(Ctx* c, int64_t q, const double* Syy, int64_t l1, const double* Sigma, int64_t l2,
                  const double* Psi, int64_t l3, double* G, int64_t l4) {
   if (q == 0) return;
-  dim3 grid((unsigned)std::min<int64_t>((q + 255) / 256, 64), (unsigned)q);
   Prof pr(c, c->cur_tag);
-  k_grad_lambda<<<grid, 256, 0, c->stream>>>(q, Syy, l1, Sigma, l2, Psi, l3, G, l4);
+  k_grad_lambda<<<(unsigned)q, 256, 0, c->stream>>>(q, Syy, l1, Sigma, l2, Psi, l3, G, l4);
   post_launch(c, "k_grad_lambda");
 }
 

@@ -12,12 +12,14 @@ pytestmark = pytest.mark.gpu
 A_KLE_M, A_KGE_M, B_KLE_N, B_KGE_N, SYM_LOWER, SYM_MIRROR = 1, 2, 4, 8, 16, 32
 
 
-@pytest.fixture(scope="module")
-def ctx():
+@pytest.fixture(scope="module", params=[1, 2, 5, 6], ids=["tile128", "tile64", "tile128_2d", "tile64_2d"])
+def ctx(request):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_1509_04681_b200 import Context
-    return Context(0)
+    c = Context(0)
+    c._check(c.lib.cggm_test_set_tile(c.h, request.param))
+    return c
 
 
 def dev(a, ld_pad=0):
@@ -40,7 +42,8 @@ def run(ctx, tA, tB, A, B, C0, alpha, beta, flags, M, N, K):
 
 @pytest.mark.parametrize("tA", [False, True])
 @pytest.mark.parametrize("tB", [False, True])
-@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (37, 45, 29), (128, 128, 16), (300, 260, 171), (513, 129, 1000)])
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (37, 45, 29), (128, 128, 16), (300, 260, 171), (513, 129, 1000),
+                                   (320, 208, 96), (256, 64, 300)])
 def test_gemm_variants(ctx, tA, tB, M, N, K):
     rng = np.random.default_rng(M * 7 + N * 3 + K)
     A = rng.standard_normal((K, M) if tA else (M, K))
@@ -116,3 +119,18 @@ def test_gemm_odd_leading_dimension_packs(ctx):
     ref = A @ B
     assert np.linalg.norm(out - ref) / np.linalg.norm(ref) < 1e-14
     del base
+
+
+def test_gemm_lower_trapezoid(ctx):
+    """SYM_LOWER with M > N: lower triangle of the square part plus the full rows below
+    (the Cholesky trailing update of the augmented [Lambda; W] factor)."""
+    rng = np.random.default_rng(21)
+    N, extra, K = 300, 257, 140
+    M = N + extra
+    A = rng.standard_normal((M, K))
+    C0 = rng.standard_normal((M, N))
+    out = run(ctx, False, True, A, A[:N].copy(), C0, -1.0, 1.0, SYM_LOWER, M, N, K)
+    ref = C0 - A @ A[:N].T
+    mask = np.tril(np.ones((M, N), dtype=bool))
+    np.testing.assert_allclose(out[mask], ref[mask], rtol=1e-12, atol=1e-12)
+    np.testing.assert_array_equal(out[~mask], C0[~mask])

@@ -1,0 +1,114 @@
+"""Parity at BASELINE.json's full `large` size (p=40000, q=20000, n=1000), in the launch
+configuration bench.py times, against what holds without a full oracle run:
+  P3/P4 chain closed forms (logdet, sampled Sigma columns), the generating-point identity I7
+  (Psi*, grad_Theta*, grad_Lambda* from E_noise, sampled columns), exact active-set rows in the
+  sampled columns outside the tie band, and the objective with tr(Sigma M) from a LAPACK banded
+  solve (the chain special case)."""
+import math
+
+import numpy as np
+import pytest
+import scipy.linalg
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+REL_F = 1e-9
+TIE = 1e-9
+
+
+@pytest.fixture(scope="module")
+def run_large():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1509_04681_b200 import Context, DeviceCsc, colmajor_empty, newton_evaluation, to_device_colmajor
+    from synth.cggm_inputs import make_problem
+    P = make_problem("large")
+    ctx = Context(0)
+    X, Y = to_device_colmajor(P.X), to_device_colmajor(P.Y)
+    Lam, Th = DeviceCsc.from_host(P.lam_star), DeviceCsc.from_host(P.theta_star)
+    Syy, _ = ctx.cggm_covariances(X, Y, want_sxy=False)
+    cap = 110_000_000
+    bufs = {"L_row": torch.empty(cap, dtype=torch.int32, device="cuda"),
+            "L_col": torch.empty(cap, dtype=torch.int32, device="cuda"),
+            "T_row": torch.empty(6_000_000, dtype=torch.int32, device="cuda"),
+            "T_col": torch.empty(6_000_000, dtype=torch.int32, device="cuda")}
+    res = newton_evaluation(ctx, X, Y, Syy, Lam, Th, P.lam_L, P.lam_T, True, bufs, tie_eps=TIE)
+    torch.cuda.synchronize()
+    return P, res, Syy
+
+
+def chain_sigma_cols(q, cols, phi=0.5):
+    i = np.arange(1, q + 1)[:, None].astype(float)
+    j = (np.asarray(cols) + 1)[None, :].astype(float)
+    lo, hi = np.minimum(i, j), np.maximum(i, j)
+    return (phi ** (hi - lo) - phi ** (lo + hi)) * (1 - phi ** (2 * (q + 1 - hi))) / ((1 - phi ** 2) * (1 - phi ** (2 * (q + 1))))
+
+
+COLS = [0, 1, 63, 64, 127, 128, 4095, 9983, 9984, 10000, 15000, 19935, 19999]
+
+
+def test_large_logdet_and_sigma(run_large):
+    P, res, _ = run_large
+    q = P.q
+    assert res["is_pd"]
+    assert res["logdet"] == pytest.approx(math.log((1 - 0.5 ** (2 * q + 2)) / 0.75), rel=1e-12)
+    S = res["Sigma"][:, COLS].cpu().numpy()
+    ref = chain_sigma_cols(q, COLS)
+    assert np.linalg.norm(S - ref) / np.linalg.norm(ref) < 1e-12
+    # symmetry of the sampled columns against the matching rows
+    Srow = res["Sigma"][COLS, :].cpu().numpy().T
+    np.testing.assert_array_equal(S, Srow)
+
+
+def test_large_generating_point_identities(run_large):
+    P, res, Syy = run_large
+    D = P.Y - P.E_noise                       # = -X Theta* Sigma*
+    psi_ref = D.T @ D[:, COLS] / P.n
+    gt_ref = 2.0 / P.n * (P.X.T @ P.E_noise[:, COLS])
+    psi = res["Psi"][:, COLS].cpu().numpy()
+    gt = res["GradT"][:, COLS].cpu().numpy()
+    assert np.linalg.norm(psi - psi_ref) / np.linalg.norm(psi_ref) < REL_F
+    assert np.linalg.norm(gt - gt_ref) / np.linalg.norm(gt_ref) < REL_F
+    syy = P.Y.T @ P.Y[:, COLS] / P.n
+    gl_ref = syy - chain_sigma_cols(P.q, COLS) - psi_ref
+    gl = res["GradL"][:, COLS].cpu().numpy()
+    assert np.linalg.norm(gl - gl_ref) / np.linalg.norm(gl_ref) < REL_F
+    # active-set rows of the sampled columns: exact outside the tie band
+    a = res["active"]
+    for lst, (rk, ck), G, lam, supp_csc, upper in (
+            ("L", ("L_row", "L_col"), gl_ref, P.lam_L, P.lam_star, True),
+            ("T", ("T_row", "T_col"), gt_ref, P.lam_T, P.theta_star, False)):
+        rows = a[rk].cpu().numpy()
+        cols = a[ck].cpu().numpy()
+        for idx, j in enumerate(COLS):
+            got = set(rows[cols == j].tolist())
+            s, e = supp_csc.colptr[j], supp_csc.colptr[j + 1]
+            supp = set(supp_csc.rowidx[s:e][supp_csc.val[s:e] != 0].tolist())
+            g = np.abs(G[:, idx])
+            nrow = j + 1 if upper else G.shape[0]
+            want = {i for i in range(nrow) if g[i] > lam or i in supp}
+            for i in got ^ want:
+                assert abs(g[i] - lam) <= TIE + 1e-9 * max(1.0, g[i]), (lst, i, j)
+            assert all(i < nrow for i in got)
+
+
+def test_large_objective(run_large):
+    P, res, _ = run_large
+    ob = res["objective"]
+    q, n = P.q, P.n
+    W = np.asarray(P.X @ P.theta_star.to_scipy())          # X Theta
+    ab = np.zeros((2, q))
+    ab[1, :] = 1.25
+    ab[0, 1:] = -0.5
+    V = scipy.linalg.solveh_banded(ab, W.T)                 # Lambda^{-1} W^T (LAPACK banded)
+    tr_sm = float(np.sum(W.T * V)) / n
+    lamd = P.lam_star.to_scipy()
+    tr_syy = float(np.sum(P.Y * (P.Y @ lamd))) / n
+    tr_sxy = float(np.sum(W * P.Y)) / n
+    logdet = math.log((1 - 0.5 ** (2 * q + 2)) / 0.75)
+    g = -logdet + tr_syy + 2 * tr_sxy + tr_sm
+    f = g + P.lam_L * np.abs(P.lam_star.val).sum() + P.lam_T * np.abs(P.theta_star.val).sum()
+    assert ob["is_pd"]
+    assert ob["tr_sigma_m"] == pytest.approx(tr_sm, rel=1e-10)
+    assert ob["f"] == pytest.approx(f, rel=1e-10)
