@@ -184,6 +184,27 @@ cggm_status cggm_objective(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int6
                            double lam_L, double lam_T, int32_t penalize_diag,
                            const void* W, int64_t ldw, cggm_objective_out* out);
 
+/* ---- composite: one Newton-iteration evaluation -------------------
+ * Same results as cggm_invert_logdet(Lambda) + cggm_psi_grad(residual route, fused active sets)
+ * + cggm_objective(Lambda_trial = Lambda, Theta) on one GPU (n samples, no sharding), with the
+ * objective's fresh trial Cholesky (the line-search PD test) executed on a library
+ * auxiliary stream concurrently with Sigma = Lambda^{-1} and the Psi / gradient / active-set work
+ * on the ctx stream.  Inputs as in those calls (Syy from cggm_covariances); active->lam_L, lam_T,
+ * penalize_diag are also the objective's.  One host synchronisation at the end; on
+ * CGGM_ERR_CAPACITY all other outputs are valid and the lists are left unwritten. */
+typedef struct cggm_eval_out {
+  double logdet;            /* log|Lambda| from the inverse's factorisation (NaN if not PD) */
+  int32_t is_pd;
+  int64_t fail_col;
+  cggm_objective_out obj;   /* the line-search objective at Lambda */
+} cggm_eval_out;
+
+cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q,
+                             const void* X, int64_t ldx, const void* Y, int64_t ldy, const void* Syy, int64_t ldsyy,
+                             const cggm_csc* Lambda, const cggm_csc* Theta,
+                             void* Sigma, int64_t ldsigma, void* Psi, int64_t ldpsi, void* GradL, int64_t ldgl,
+                             void* GradT, int64_t ldgt, cggm_active_out* active, cggm_eval_out* out);
+
 #ifdef __cplusplus
 }
 #endif

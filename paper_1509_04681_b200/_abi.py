@@ -44,6 +44,10 @@ class cggm_objective_out(ctypes.Structure):
                 ("tr_sigma_m", c_d), ("pen_L", c_d), ("pen_T", c_d), ("is_pd", c_i32), ("fail_col", c_i64)]
 
 
+class cggm_eval_out(ctypes.Structure):
+    _fields_ = [("logdet", c_d), ("is_pd", c_i32), ("fail_col", c_i64), ("obj", cggm_objective_out)]
+
+
 # name -> (restype, argtypes); every symbol include/cggm.h declares
 SIGNATURES = {
     "cggm_ctx_create": (c_i32, [ctypes.POINTER(c_vp), c_i32, c_i32, c_vp]),
@@ -68,6 +72,10 @@ SIGNATURES = {
     "cggm_grad_lambda": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64]),
     "cggm_active_set": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, ctypes.POINTER(cggm_csc),
                                 ctypes.POINTER(cggm_csc), ctypes.POINTER(cggm_active_out)]),
+    "cggm_newton_eval": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
+                                 ctypes.POINTER(cggm_csc), ctypes.POINTER(cggm_csc), c_vp, c_i64, c_vp, c_i64,
+                                 c_vp, c_i64, c_vp, c_i64, ctypes.POINTER(cggm_active_out),
+                                 ctypes.POINTER(cggm_eval_out)]),
     "cggm_test_gemm": (c_i32, [c_vp, c_i32, c_i32, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
                                c_d, c_d, c_i32]),
     "cggm_test_set_tile": (c_i32, [c_vp, c_i32]),

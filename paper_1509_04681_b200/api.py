@@ -268,15 +268,48 @@ class Context:
                     fail_col=int(o.fail_col))
 
 
+    # ---------------------------------------------------------------- composite
+    def cggm_newton_eval(self, X, Y, Syy, Lam: DeviceCsc, Theta: DeviceCsc, lam_L, lam_T, penalize_diag=True,
+                         tie_eps=1e-9, bufs=None):
+        """One Newton-iteration evaluation in one call (objective overlapped on an internal stream)."""
+        self._sync_stream()
+        n, p = X.shape
+        q = Y.shape[1]
+        dev = X.device
+        bufs = bufs if bufs is not None else {}
+        for k, shape in (("Sigma", (q, q)), ("Psi", (q, q)), ("GradL", (q, q)), ("GradT", (p, q))):
+            if bufs.get(k) is None:
+                bufs[k] = colmajor_empty(*shape, device=dev)
+        spec = dict(lam_L=lam_L, lam_T=lam_T, penalize_diag=int(bool(penalize_diag)), tie_eps=tie_eps,
+                    L_row=bufs.get("L_row"), L_col=bufs.get("L_col"), T_row=bufs.get("T_row"), T_col=bufs.get("T_col"))
+        ao = self._active_struct(spec)
+        eo = _abi.cggm_eval_out()
+        ls, ts = Lam.c_struct(), Theta.c_struct()
+        self._check(self.lib.cggm_newton_eval(
+            self.h, n, p, q, _ptr(X), ld_of(X), _ptr(Y), ld_of(Y), _ptr(Syy), ld_of(Syy), ctypes.byref(ls),
+            ctypes.byref(ts), _ptr(bufs["Sigma"]), ld_of(bufs["Sigma"]), _ptr(bufs["Psi"]), ld_of(bufs["Psi"]),
+            _ptr(bufs["GradL"]), ld_of(bufs["GradL"]), _ptr(bufs["GradT"]), ld_of(bufs["GradT"]),
+            ctypes.byref(ao), ctypes.byref(eo)))
+        o = eo.obj
+        ob = dict(f=o.f, g=o.g, logdet=o.logdet, tr_syy_lam=o.tr_syy_lam, tr_sxy_theta=o.tr_sxy_theta,
+                  tr_sigma_m=o.tr_sigma_m, pen_L=o.pen_L, pen_T=o.pen_T, is_pd=bool(o.is_pd), fail_col=int(o.fail_col))
+        return dict(Sigma=bufs["Sigma"], logdet=eo.logdet, is_pd=bool(eo.is_pd), fail_col=int(eo.fail_col),
+                    Psi=bufs["Psi"], GradL=bufs["GradL"], GradT=bufs["GradT"], active=self._active_result(ao, spec),
+                    objective=ob)
+
+
 def newton_evaluation(ctx: Context, X, Y, Syy, Lam: DeviceCsc, Theta: DeviceCsc, lam_L, lam_T, penalize_diag=True,
-                      bufs=None, tie_eps=1e-9):
+                      bufs=None, tie_eps=1e-9, composite=True):
     """One Newton-iteration evaluation (the metric's unit): invert_logdet(Lambda),
-    psi_grad (+ fused active sets), objective at Lambda_trial = Lambda with its own Cholesky."""
+    psi_grad (+ fused active sets), objective at Lambda_trial = Lambda with its own Cholesky.
+    composite=True uses the single overlapped call cggm_newton_eval; False issues the separate calls."""
     bufs = bufs if bufs is not None else {}
+    if composite:
+        return ctx.cggm_newton_eval(X, Y, Syy, Lam, Theta, lam_L, lam_T, penalize_diag, tie_eps, bufs)
     Sigma, logdet, pd, fc = ctx.cggm_invert_logdet(Lam, Sigma=bufs.get("Sigma"))
     spec = dict(lam_L=lam_L, lam_T=lam_T, penalize_diag=int(bool(penalize_diag)), tie_eps=tie_eps,
                 L_row=bufs["L_row"], L_col=bufs["L_col"], T_row=bufs["T_row"], T_col=bufs["T_col"])
     r = ctx.cggm_psi_grad(X, Y, Theta, Sigma, Syy=Syy, Lam=Lam, fused=spec,
                           out=dict(Psi=bufs.get("Psi"), GradL=bufs.get("GradL"), GradT=bufs.get("GradT")))
     ob = ctx.cggm_objective(X, Y, Lam, Theta, lam_L, lam_T, penalize_diag)
-    return dict(Sigma=Sigma, logdet=logdet, is_pd=pd, **r, objective=ob)
+    return dict(Sigma=Sigma, logdet=logdet, is_pd=pd, fail_col=fc, **r, objective=ob)

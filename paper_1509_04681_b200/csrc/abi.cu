@@ -114,22 +114,6 @@ cggm_status guard(cggm_ctx* ctx, F f) {
   }
 }
 
-// logdet / PD from the leaf slots; returns host values (syncs)
-void finish_chol(Ctx* c, Scal s, double* slots, int64_t nleaves, double* out_dev, CholResult* res) {
-  sum_arrays_1(c, slots, nleaves, out_dev);
-  char* h = static_cast<char*>(c->host_scratch);
-  CGGM_CUDA_CHECK(cudaMemcpyAsync(h, s.fail, 4, cudaMemcpyDeviceToHost, c->stream));
-  CGGM_CUDA_CHECK(cudaMemcpyAsync(h + 8, out_dev, 8, cudaMemcpyDeviceToHost, c->stream));
-  CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
-  int fc;
-  double ld;
-  std::memcpy(&fc, h, 4);
-  std::memcpy(&ld, h + 8, 8);
-  res->is_pd = (fc == INT_MAX);
-  res->fail_col = res->is_pd ? -1 : fc;
-  res->logdet = res->is_pd ? ld : std::numeric_limits<double>::quiet_NaN();
-}
-
 }  // namespace
 }  // namespace cggm
 
@@ -181,6 +165,13 @@ cggm_status cggm_ctx_destroy(cggm_ctx* ctx) {
   for (auto& b : c->slots)
     if (b.ptr) cudaFree(b.ptr);
   if (c->host_scratch) cudaFreeHost(c->host_scratch);
+  if (c->aux) {
+    cudaStreamSynchronize(c->aux);
+    cudaStreamDestroy(c->aux);
+    cudaEventDestroy(c->ev_fork);
+    cudaEventDestroy(c->ev_join);
+  }
+  for (auto e : c->evpool) cudaEventDestroy(e);
   delete ctx;
   return CGGM_OK;
 }
@@ -281,15 +272,32 @@ cggm_status cggm_covariances(cggm_ctx* ctx, int64_t n_local, int64_t n_total, in
   });
 }
 
+// ================================================================== enqueue-only cores
+// Each core only enqueues work on c->stream (no host synchronisation); results stay on the
+// device in a per-lane scalar block until the matching readback.  Lanes (0 = caller's stream,
+// 1 = auxiliary stream) own disjoint workspace slots so the composite call can overlap them.
+
+struct Lane {
+  int dense, scal, pack;  // workspace slots
+};
+static const Lane kLane[2] = {{WS_DENSE_A, WS_SCAL, WS_PACK0}, {WS_DENSE_B, WS_SCAL2, WS_PACK2}};
+
+static Scal scal_lane(Ctx* c, int lane, size_t ndoubles) {
+  char* base = static_cast<char*>(ws_get(c, kLane[lane].scal, 64 + ndoubles * 8));
+  return Scal{reinterpret_cast<int*>(base), reinterpret_cast<int*>(base + 4), reinterpret_cast<double*>(base + 64)};
+}
+
+static int64_t n_leaves(int64_t q) { return (q + leaf_nb() - 1) / leaf_nb(); }
+
 // ------------------------------------------------------------------ a3
-static void invert_impl(Ctx* c, const cggm_csc* Lambda, double* Sigma, int64_t ldsigma, CholResult* res) {
+// Scal layout: dbl[0] = logdet sum, dbl[8..] leaf slots
+static void invert_enqueue(Ctx* c, int lane, const cggm_csc* Lambda, double* Sigma, int64_t ldsigma) {
   const int64_t q = Lambda->nrows;
   const int64_t lda = even(q);
   const int nb = leaf_nb();
-  const int64_t nleaves = (q + nb - 1) / nb;
-  double* A = static_cast<double*>(ws_get(c, WS_DENSE_A, (size_t)lda * q * 8));
-  Scal s = scal(c, 8 + nleaves);
-  double* out_dev = s.dbl;
+  const int64_t nleaves = n_leaves(q);
+  double* A = static_cast<double*>(ws_get(c, kLane[lane].dense, (size_t)lda * q * 8));
+  Scal s = scal_lane(c, lane, 8 + nleaves);
   double* slots = s.dbl + 8;
   View Av{A, lda, q, q};
   densify_csc(c, Lambda, Av);
@@ -306,7 +314,26 @@ static void invert_impl(Ctx* c, const cggm_csc* Lambda, double* Sigma, int64_t l
     double* leafinv = static_cast<double*>(ws_get(c, WS_LEAFINV, (size_t)nleaves * nb * nb * 8));
     potrf_recursive(c, Av, View{nullptr, lda, q, q}, false, leafinv, slots, s.fail, nullptr, 0);
   }
-  finish_chol(c, s, slots, nleaves, out_dev, res);
+  sum_arrays_1(c, slots, nleaves, s.dbl);
+}
+
+// D2H of (fail_col, logdet) from a lane's scalar block; caller synchronises
+static void chol_readback_async(Ctx* c, int lane, char* h) {
+  Scal s = scal_lane(c, lane, 0);
+  CGGM_CUDA_CHECK(cudaMemcpyAsync(h, s.fail, 4, cudaMemcpyDeviceToHost, c->stream));
+  CGGM_CUDA_CHECK(cudaMemcpyAsync(h + 8, s.dbl, 8, cudaMemcpyDeviceToHost, c->stream));
+}
+
+static CholResult chol_decode(const char* h) {
+  int fc;
+  double ld;
+  std::memcpy(&fc, h, 4);
+  std::memcpy(&ld, h + 8, 8);
+  CholResult r;
+  r.is_pd = (fc == INT_MAX);
+  r.fail_col = r.is_pd ? -1 : fc;
+  r.logdet = r.is_pd ? ld : std::numeric_limits<double>::quiet_NaN();
+  return r;
 }
 
 cggm_status cggm_invert_logdet(cggm_ctx* ctx, const cggm_csc* Lambda, void* Sigma, int64_t ldsigma, double* logdet,
@@ -323,17 +350,21 @@ cggm_status cggm_invert_logdet(cggm_ctx* ctx, const cggm_csc* Lambda, void* Sigm
       return;
     }
     validate_csc_dev(c, Lambda, true, "Lambda");
-    CholResult r;
-    invert_impl(c, Lambda, static_cast<double*>(Sigma), ldsigma, &r);
+    invert_enqueue(c, 0, Lambda, static_cast<double*>(Sigma), ldsigma);
+    char* h = static_cast<char*>(c->host_scratch);
+    chol_readback_async(c, 0, h);
+    CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    CholResult r = chol_decode(h);
     *logdet = r.logdet;
     *is_pd = r.is_pd;
     *fail_col = r.fail_col;
   });
 }
 
-// ------------------------------------------------------------------ a6 (shared by psi_grad fused)
-static void active_impl(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t ldgl, const double* GradT,
-                        int64_t ldgt, const cggm_csc* Lambda, const cggm_csc* Theta, cggm_active_out* o) {
+// ------------------------------------------------------------------ a6
+static ActTotals* active_enqueue(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t ldgl, const double* GradT,
+                                 int64_t ldgt, const cggm_csc* Lambda, const cggm_csc* Theta,
+                                 const cggm_active_out* o) {
   long long* base = static_cast<long long*>(ws_get(c, WS_ACT, (size_t)(8 * q + 16) * 8));
   long long *cntL = base, *cntT = base + q, *tieL = base + 2 * q, *tieT = base + 3 * q, *offL = base + 4 * q,
             *offT = base + 5 * q;
@@ -343,10 +374,13 @@ static void active_impl(Ctx* c, int64_t p, int64_t q, const double* GradL, int64
   Phase ph(c, TAG_ACTIVE);
   active_count(c, p, q, GradL, ldgl, GradT, ldgt, Lambda, Theta, o->lam_L, o->lam_T, o->penalize_diag, o->tie_eps, T,
                offL, offT, cntL, cntT, tieL, tieT, subL, subT);
-  ActTotals h;
-  CGGM_CUDA_CHECK(cudaMemcpyAsync(c->host_scratch, T, sizeof(ActTotals), cudaMemcpyDeviceToHost, c->stream));
-  CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
-  std::memcpy(&h, c->host_scratch, sizeof(ActTotals));
+  // the write pass checks the capacity on the device (writes nothing if a list would overflow)
+  active_write(c, p, q, GradL, ldgl, GradT, ldgt, Lambda, Theta, o->lam_L, o->lam_T, o->penalize_diag, offL, offT,
+               o->L_row, o->L_col, o->T_row, o->T_col, T, o->cap_L, o->cap_T);
+  return T;
+}
+
+static void active_decode(const ActTotals& h, cggm_active_out* o) {
   o->m_L = h.m_L;
   o->m_T = h.m_T;
   o->ties_L = h.ties_L;
@@ -355,10 +389,6 @@ static void active_impl(Ctx* c, int64_t p, int64_t q, const double* GradL, int64
   if (o->m_L > o->cap_L || o->m_T > o->cap_T)
     fail(CGGM_ERR_CAPACITY, "active set larger than capacity (m_L=" + std::to_string(o->m_L) +
                                 ", m_T=" + std::to_string(o->m_T) + ")");
-  if ((o->m_L > 0 && (!o->L_row || !o->L_col)) || (o->m_T > 0 && (!o->T_row || !o->T_col)))
-    fail(CGGM_ERR_INVALID_ARG, "null active-set output list");
-  active_write(c, p, q, GradL, ldgl, GradT, ldgt, Lambda, Theta, o->lam_L, o->lam_T, o->penalize_diag, offL, offT,
-               o->L_row, o->L_col, o->T_row, o->T_col);
 }
 
 static void check_active_args(const cggm_active_out* o) {
@@ -366,6 +396,16 @@ static void check_active_args(const cggm_active_out* o) {
   if (!(o->lam_L >= 0.0) || !(o->lam_T >= 0.0)) fail(CGGM_ERR_INVALID_ARG, "negative lambda");
   if (!(o->tie_eps >= 0.0)) fail(CGGM_ERR_INVALID_ARG, "negative tie_eps");
   if (o->cap_L < 0 || o->cap_T < 0) fail(CGGM_ERR_INVALID_ARG, "negative capacity");
+  if ((o->cap_L > 0 && (!o->L_row || !o->L_col)) || (o->cap_T > 0 && (!o->T_row || !o->T_col)))
+    fail(CGGM_ERR_INVALID_ARG, "null active-set output list with positive capacity");
+}
+
+static void active_sync(Ctx* c, ActTotals* T, cggm_active_out* o) {
+  ActTotals h;
+  CGGM_CUDA_CHECK(cudaMemcpyAsync(c->host_scratch, T, sizeof(ActTotals), cudaMemcpyDeviceToHost, c->stream));
+  CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  std::memcpy(&h, c->host_scratch, sizeof(ActTotals));
+  active_decode(h, o);
 }
 
 cggm_status cggm_active_set(cggm_ctx* ctx, int64_t p, int64_t q, const void* GradL, int64_t ldgl, const void* GradT,
@@ -383,12 +423,47 @@ cggm_status cggm_active_set(cggm_ctx* ctx, int64_t p, int64_t q, const void* Gra
     if (q == 0) return;
     validate_csc_dev(c, Lambda, true, "Lambda");
     validate_csc_dev(c, Theta, false, "Theta");
-    active_impl(c, p, q, static_cast<const double*>(GradL), ldgl, static_cast<const double*>(GradT), ldgt, Lambda,
-                Theta, out);
+    ActTotals* T = active_enqueue(c, p, q, static_cast<const double*>(GradL), ldgl, static_cast<const double*>(GradT),
+                                  ldgt, Lambda, Theta, out);
+    active_sync(c, T, out);
   });
 }
 
 // ------------------------------------------------------------------ a2/a4/a5
+// W (n_local x q, ldw) must already hold X Theta.
+static void psi_enqueue(Ctx* c, int64_t n_local, int64_t n_total, int64_t p, int64_t q, const double* Xd, int64_t ldx,
+                        const double* Yd, int64_t ldy, const double* W, int64_t ldw, const double* Sg, int64_t ldsigma,
+                        const double* Syy, int64_t ldsyy, const double* Sxy, int64_t ldsxy, double* Psi, int64_t ldpsi,
+                        double* GradL, int64_t ldgl, double* GradT, int64_t ldgt) {
+  const int64_t ldn = even(n_local > 0 ? n_local : 1);
+  double* R = static_cast<double*>(ws_get(c, WS_R, (size_t)ldn * q * 8));
+  double* E = static_cast<double*>(ws_get(c, WS_E, (size_t)ldn * q * 8));
+  {  // a4: acc = W Sigma -> R = acc / sqrt(n), E = Y + acc
+    Phase ph(c, TAG_WSIGMA);
+    Epilogue e; e.out1 = R; e.ld1 = ldn; e.a1 = 1.0 / std::sqrt((double)n_total);
+    if (GradT && !Sxy) { e.out2 = E; e.ld2 = ldn; e.a2 = 1.0; e.in2a = Yd; e.ld2a = ldy; e.b2 = 1.0; }
+    gemm(c, false, false, n_local, q, q, W, ldw, Sg, ldsigma, e, 0);
+  }
+  {  // a4/a5: Psi = R^T R (mirrored), then grad_Lambda = (S_yy - Sigma) - Psi as one streaming pass
+    Phase ph(c, TAG_PSI);
+    Epilogue e; e.out1 = Psi; e.ld1 = ldpsi; e.a1 = 1.0;
+    gemm(c, true, false, q, q, n_local, R, ldn, R, ldn, e, SYM_LOWER | SYM_MIRROR);
+    if (GradL) grad_lambda(c, q, Syy, ldsyy, Sg, ldsigma, Psi, ldpsi, GradL, ldgl);
+  }
+  if (GradT) {  // a5: GradT = (2/n) X^T E   (or 2 S_xy + (2/sqrt n) X^T R)
+    Phase ph(c, TAG_GRADT);
+    Epilogue e; e.out1 = GradT; e.ld1 = ldgt;
+    if (!Sxy) {
+      e.a1 = 2.0 / (double)n_total;
+      gemm(c, true, false, p, q, n_local, Xd, ldx, E, ldn, e, 0);
+    } else {
+      e.a1 = 2.0 / std::sqrt((double)n_total);
+      e.in1a = Sxy; e.ld1a = ldsxy; e.b1 = 2.0;
+      gemm(c, true, false, p, q, n_local, Xd, ldx, R, ldn, e, 0);
+    }
+  }
+}
+
 cggm_status cggm_psi_grad(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64_t p, int64_t q, const void* X,
                           int64_t ldx, const void* Y, int64_t ldy, const cggm_csc* Theta, const void* Sigma,
                           int64_t ldsigma, const void* Syy, int64_t ldsyy, const void* Sxy, int64_t ldsxy, void* Psi,
@@ -421,47 +496,16 @@ cggm_status cggm_psi_grad(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64
     if (fused) validate_csc_dev(c, Lambda, true, "Lambda");
     const int64_t ldn = even(n_local > 0 ? n_local : 1);
     double* W = static_cast<double*>(ws_get(c, WS_W, (size_t)ldn * q * 8));
-    double* R = static_cast<double*>(ws_get(c, WS_R, (size_t)ldn * q * 8));
-    double* E = static_cast<double*>(ws_get(c, WS_E, (size_t)ldn * q * 8));
-    const double* Xd = static_cast<const double*>(X);
-    const double* Yd = static_cast<const double*>(Y);
-    const double* Sg = static_cast<const double*>(Sigma);
-    // a2: W = X Theta
-    spmm_x_theta(c, Xd, ldx, n_local, Theta, View{W, ldn, n_local, q});
-    // a4: acc = W Sigma -> R = acc / sqrt(n), E = Y + acc
-    {
-      Phase ph(c, TAG_WSIGMA);
-      Epilogue e; e.out1 = R; e.ld1 = ldn; e.a1 = 1.0 / std::sqrt((double)n_total);
-      if (GradT && !Sxy) { e.out2 = E; e.ld2 = ldn; e.a2 = 1.0; e.in2a = Yd; e.ld2a = ldy; e.b2 = 1.0; }
-      gemm(c, false, false, n_local, q, q, W, ldn, Sg, ldsigma, e, 0);
+    spmm_x_theta(c, static_cast<const double*>(X), ldx, n_local, Theta, View{W, ldn, n_local, q});
+    psi_enqueue(c, n_local, n_total, p, q, static_cast<const double*>(X), ldx, static_cast<const double*>(Y), ldy, W,
+                ldn, static_cast<const double*>(Sigma), ldsigma, static_cast<const double*>(Syy), ldsyy,
+                static_cast<const double*>(Sxy), ldsxy, static_cast<double*>(Psi), ldpsi,
+                static_cast<double*>(GradL), ldgl, static_cast<double*>(GradT), ldgt);
+    if (fused) {
+      ActTotals* T = active_enqueue(c, p, q, static_cast<const double*>(GradL), ldgl,
+                                    static_cast<const double*>(GradT), ldgt, Lambda, Theta, fused);
+      active_sync(c, T, fused);
     }
-    // a4/a5: Psi = R^T R, epilogue GradL = S_yy - Sigma - Psi (mirrored, bit-identical triangles)
-    {
-      Phase ph(c, TAG_PSI);
-      Epilogue e; e.out1 = static_cast<double*>(Psi); e.ld1 = ldpsi; e.a1 = 1.0;
-      gemm(c, true, false, q, q, n_local, R, ldn, R, ldn, e, SYM_LOWER | SYM_MIRROR);
-      // grad_Lambda = (S_yy - Sigma) - Psi as one coalesced streaming pass (cheaper than a
-      // mirrored two-input epilogue; same operation order as Eq. 3)
-      if (GradL)
-        grad_lambda(c, q, static_cast<const double*>(Syy), ldsyy, Sg, ldsigma, static_cast<const double*>(Psi), ldpsi,
-                    static_cast<double*>(GradL), ldgl);
-    }
-    // a5: GradT = (2/n) X^T E   (or 2 S_xy + (2/sqrt n) X^T R)
-    if (GradT) {
-      Phase ph(c, TAG_GRADT);
-      Epilogue e; e.out1 = static_cast<double*>(GradT); e.ld1 = ldgt;
-      if (!Sxy) {
-        e.a1 = 2.0 / (double)n_total;
-        gemm(c, true, false, p, q, n_local, Xd, ldx, E, ldn, e, 0);
-      } else {
-        e.a1 = 2.0 / std::sqrt((double)n_total);
-        e.in1a = static_cast<const double*>(Sxy); e.ld1a = ldsxy; e.b1 = 2.0;
-        gemm(c, true, false, p, q, n_local, Xd, ldx, R, ldn, e, 0);
-      }
-    }
-    if (fused)
-      active_impl(c, p, q, static_cast<const double*>(GradL), ldgl, static_cast<const double*>(GradT), ldgt, Lambda,
-                  Theta, fused);
   });
 }
 
@@ -480,6 +524,76 @@ cggm_status cggm_grad_lambda(cggm_ctx* ctx, int64_t q, const void* Syy, int64_t 
 }
 
 // ------------------------------------------------------------------ a7
+// Augmented dense [Lambda; W] ((q + n_local) x q): the Cholesky of the trial Lambda (the PD test)
+// leaves Z = W L^{-T} in the bottom rows, ||Z||_F^2 = tr(Lambda^{-1} W^T W) (reading A14).
+// Scal layout: dbl[0] logdet sum, dbl[1..5] sums (<Y,Y Lambda>, <W,Y>, ||Z||^2, |Lambda|, |Theta|),
+// dbl[16..] per-column partials, then leaf slots.
+static void objective_enqueue(Ctx* c, int lane, int64_t n_local, int64_t q, const double* Yd, int64_t ldy,
+                              const double* Wd, int64_t ldwd, const cggm_csc* Lambda, const cggm_csc* Theta,
+                              int32_t penalize_diag) {
+  const int nb = leaf_nb();
+  const int64_t nleaves = n_leaves(q);
+  const int64_t ldaug = even(q + n_local);
+  double* A = static_cast<double*>(ws_get(c, kLane[lane].dense, (size_t)ldaug * q * 8));
+  double* leafinv = static_cast<double*>(ws_get(c, WS_LEAFINV, (size_t)nleaves * nb * nb * 8));
+  Scal s = scal_lane(c, lane, 16 + 5 * q + nleaves);
+  double* res = s.dbl;
+  double* partY = s.dbl + 16;
+  double* partWY = partY + q;
+  double* partZ = partWY + q;
+  double* penLp = partZ + q;
+  double* penTp = penLp + q;
+  double* slots = penTp + q;
+  densify_csc(c, Lambda, View{A, ldaug, q, q});
+  copy2d(c, View{A + q, ldaug, n_local, q}, Wd, ldwd);
+  init_scalars(c, s.fail, s.flag);
+  potrf_recursive(c, View{A, ldaug, q + n_local, q}, View{nullptr, ldaug, q, q}, false, leafinv, slots, s.fail,
+                  nullptr, 0);
+  Phase ph(c, TAG_OBJRED);
+  col_partials(c, 0, n_local, q, Yd, ldy, nullptr, 0, Lambda, partY);
+  col_partials(c, 1, n_local, q, Wd, ldwd, Yd, ldy, nullptr, partWY);
+  col_partials(c, 2, n_local, q, A + q, ldaug, nullptr, 0, nullptr, partZ);
+  csc_abs_partials(c, Lambda, penalize_diag == 0, penLp);
+  csc_abs_partials(c, Theta, false, penTp);
+  sum_arrays_1(c, slots, nleaves, res + 0);
+  sum_arrays_1(c, partY, q, res + 1);
+  sum_arrays_1(c, partWY, q, res + 2);
+  sum_arrays_1(c, partZ, q, res + 3);
+  sum_arrays_1(c, penLp, q, res + 4);
+  sum_arrays_1(c, penTp, q, res + 5);
+}
+
+static void objective_readback_async(Ctx* c, int lane, char* h) {
+  Scal s = scal_lane(c, lane, 0);
+  CGGM_CUDA_CHECK(cudaMemcpyAsync(h, s.fail, 4, cudaMemcpyDeviceToHost, c->stream));
+  CGGM_CUDA_CHECK(cudaMemcpyAsync(h + 8, s.dbl, 6 * 8, cudaMemcpyDeviceToHost, c->stream));
+}
+
+static void objective_decode(const char* h, int64_t n_total, double lam_L, double lam_T, cggm_objective_out* out) {
+  CholResult cr = chol_decode(h);
+  double v[6];
+  std::memcpy(v, h + 8, 6 * 8);
+  const double nt = (double)n_total;
+  out->pen_L = lam_L * v[4];
+  out->pen_T = lam_T * v[5];
+  out->is_pd = cr.is_pd;
+  out->fail_col = cr.fail_col;
+  out->tr_syy_lam = v[1] / nt;
+  out->tr_sxy_theta = v[2] / nt;
+  if (cr.is_pd) {
+    out->logdet = cr.logdet;
+    out->tr_sigma_m = v[3] / nt;
+    out->g = -out->logdet + out->tr_syy_lam + 2.0 * out->tr_sxy_theta + out->tr_sigma_m;
+    out->f = out->g + out->pen_L + out->pen_T;
+  } else {
+    const double nan = std::numeric_limits<double>::quiet_NaN();
+    out->logdet = nan;
+    out->tr_sigma_m = nan;
+    out->g = INFINITY;
+    out->f = INFINITY;
+  }
+}
+
 cggm_status cggm_objective(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64_t p, int64_t q, const void* X,
                            int64_t ldx, const void* Y, int64_t ldy, const cggm_csc* Lambda, const cggm_csc* Theta,
                            double lam_L, double lam_T, int32_t penalize_diag, const void* W, int64_t ldw,
@@ -503,14 +617,6 @@ cggm_status cggm_objective(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int6
     validate_csc_dev(c, Lambda, true, "Lambda");
     validate_csc_dev(c, Theta, false, "Theta");
     const int64_t ldn = even(n_local > 0 ? n_local : 1);
-    const int nb = leaf_nb();
-    const int64_t nleaves = (q + nb - 1) / nb;
-    const double* Yd = static_cast<const double*>(Y);
-    // augmented dense [Lambda; W] ((q + n_local) x q): the Cholesky of the trial Lambda (the PD
-    // test) leaves Z = W L^{-T} in the bottom rows, ||Z||_F^2 = tr(Lambda^{-1} W^T W) (reading A14)
-    const int64_t ldaug = even(q + n_local);
-    double* A = static_cast<double*>(ws_get(c, WS_DENSE_A, (size_t)ldaug * q * 8));
-    double* leafinv = static_cast<double*>(ws_get(c, WS_LEAFINV, (size_t)nleaves * nb * nb * 8));
     const double* Wd;
     int64_t ldwd;
     if (W) {
@@ -522,59 +628,100 @@ cggm_status cggm_objective(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int6
       Wd = Wb;
       ldwd = ldn;
     }
-    Scal s = scal(c, 16 + 6 * q + nleaves);
-    double* res = s.dbl;            // [0..5] sums, [8] logdet
-    double* partY = s.dbl + 16;
-    double* partWY = partY + q;
-    double* partZ = partWY + q;
-    double* penLp = partZ + q;
-    double* penTp = penLp + q;
-    double* slots = penTp + q;
-    densify_csc(c, Lambda, View{A, ldaug, q, q});
-    copy2d(c, View{A + q, ldaug, n_local, q}, Wd, ldwd);
-    init_scalars(c, s.fail, s.flag);
-    potrf_recursive(c, View{A, ldaug, q + n_local, q}, View{nullptr, ldaug, q, q}, false, leafinv, slots, s.fail,
-                    nullptr, 0);
-    const double* Z = A + q;
-    const int64_t ldz = ldaug;
-    Phase ph(c, TAG_OBJRED);
-    col_partials(c, 0, n_local, q, Yd, ldy, nullptr, 0, Lambda, partY);
-    col_partials(c, 1, n_local, q, Wd, ldwd, Yd, ldy, nullptr, partWY);
-    col_partials(c, 2, n_local, q, Z, ldz, nullptr, 0, nullptr, partZ);
-    csc_abs_partials(c, Lambda, penalize_diag == 0, penLp);
-    csc_abs_partials(c, Theta, false, penTp);
-    sum_arrays_1(c, partY, q, res + 0);
-    sum_arrays_1(c, partWY, q, res + 1);
-    sum_arrays_1(c, partZ, q, res + 2);
-    sum_arrays_1(c, penLp, q, res + 3);
-    sum_arrays_1(c, penTp, q, res + 4);
-    CholResult cr;
-    finish_chol(c, s, slots, nleaves, res + 8, &cr);
-    double h[6];
-    CGGM_CUDA_CHECK(cudaMemcpyAsync(c->host_scratch, res, 5 * 8, cudaMemcpyDeviceToHost, c->stream));
+    objective_enqueue(c, 0, n_local, q, static_cast<const double*>(Y), ldy, Wd, ldwd, Lambda, Theta, penalize_diag);
+    char* h = static_cast<char*>(c->host_scratch);
+    objective_readback_async(c, 0, h);
     CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
-    std::memcpy(h, c->host_scratch, 5 * 8);
-    const double nt = (double)n_total;
-    out->pen_L = lam_L * h[3];
-    out->pen_T = lam_T * h[4];
+    objective_decode(h, n_total, lam_L, lam_T, out);
+  });
+}
+
+// ------------------------------------------------------------------ composite evaluation
+// One Newton-iteration evaluation (the bench's unit): the objective's fresh trial Cholesky runs on
+// the auxiliary stream, overlapped with Sigma = Lambda^{-1} and the Psi / gradient / active-set
+// work on the caller's stream; one host synchronisation at the end.
+cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, const void* X, int64_t ldx,
+                             const void* Y, int64_t ldy, const void* Syy, int64_t ldsyy, const cggm_csc* Lambda,
+                             const cggm_csc* Theta, void* Sigma, int64_t ldsigma, void* Psi, int64_t ldpsi,
+                             void* GradL, int64_t ldgl, void* GradT, int64_t ldgt, cggm_active_out* active,
+                             cggm_eval_out* out) {
+  return guard(ctx, [&](Ctx* c) {
+    check_ctx_dtype(c);
+    if (!out) fail(CGGM_ERR_INVALID_ARG, "null cggm_eval_out");
+    if (n < 1 || p < 0 || q < 1) fail(CGGM_ERR_INVALID_ARG, "need n >= 1, q >= 1, p >= 0");
+    check_dense("X", X, n, p, ldx);
+    check_dense("Y", Y, n, q, ldy);
+    check_dense("Syy", Syy, q, q, ldsyy);
+    check_dense("Sigma", Sigma, q, q, ldsigma);
+    check_dense("Psi", Psi, q, q, ldpsi);
+    check_dense("GradL", GradL, q, q, ldgl);
+    check_dense("GradT", GradT, p, q, ldgt);
+    check_csc_host("Lambda", Lambda, q, q);
+    check_csc_host("Theta", Theta, p, q);
+    check_active_args(active);
+    std::memset(out, 0, sizeof(*out));
+    validate_csc_dev(c, Lambda, true, "Lambda");
+    validate_csc_dev(c, Theta, false, "Theta");
+    const int64_t ldn = even(n);
+    // allocate every workspace slot up front (allocation may synchronise the device)
+    const int64_t nleaves = n_leaves(q);
+    ws_get(c, WS_DENSE_A, (size_t)even(q) * q * 8);
+    ws_get(c, WS_DENSE_B, (size_t)even(q + n) * q * 8);
+    ws_get(c, WS_LINV, (size_t)even(q) * q * 8);
+    ws_get(c, WS_TMP, (size_t)(q / 2 + 128) * (q / 2 + 130) * 8);
+    ws_get(c, WS_LEAFINV, (size_t)nleaves * leaf_nb() * leaf_nb() * 8);
+    ws_get(c, WS_SCAL, 64 + (8 + nleaves) * 8);
+    ws_get(c, WS_SCAL2, 64 + (16 + 5 * q + nleaves) * 8);
+    ws_get(c, WS_ACT, (size_t)(8 * q + 16) * 8);
+    ws_get(c, WS_R, (size_t)ldn * q * 8);
+    ws_get(c, WS_E, (size_t)ldn * q * 8);
+    double* W = static_cast<double*>(ws_get(c, WS_W, (size_t)ldn * q * 8));
+    if (!c->aux) {
+      CGGM_CUDA_CHECK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+      CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+      CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    }
+    cudaStream_t s0 = c->stream;
+    const double* Xd = static_cast<const double*>(X);
+    const double* Yd = static_cast<const double*>(Y);
+    // a2 on the caller's stream, then fork
+    spmm_x_theta(c, Xd, ldx, n, Theta, View{W, ldn, n, q});
+    CGGM_CUDA_CHECK(cudaEventRecord(c->ev_fork, s0));
+    CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
+    try {
+      // a7 on the auxiliary stream (lane 1)
+      c->stream = c->aux;
+      c->lane = 1;
+      objective_enqueue(c, 1, n, q, Yd, ldy, W, ldn, Lambda, Theta, active->penalize_diag);
+      CGGM_CUDA_CHECK(cudaEventRecord(c->ev_join, c->aux));
+      c->stream = s0;
+      c->lane = 0;
+    } catch (...) {
+      c->stream = s0;
+      c->lane = 0;
+      throw;
+    }
+    // a3, a4/a5, a6 on the caller's stream (lane 0)
+    invert_enqueue(c, 0, Lambda, static_cast<double*>(Sigma), ldsigma);
+    psi_enqueue(c, n, n, p, q, Xd, ldx, Yd, ldy, W, ldn, static_cast<const double*>(Sigma), ldsigma,
+                static_cast<const double*>(Syy), ldsyy, nullptr, 0, static_cast<double*>(Psi), ldpsi,
+                static_cast<double*>(GradL), ldgl, static_cast<double*>(GradT), ldgt);
+    ActTotals* T = active_enqueue(c, p, q, static_cast<const double*>(GradL), ldgl, static_cast<const double*>(GradT),
+                                  ldgt, Lambda, Theta, active);
+    CGGM_CUDA_CHECK(cudaStreamWaitEvent(s0, c->ev_join, 0));
+    char* h = static_cast<char*>(c->host_scratch);
+    chol_readback_async(c, 0, h);
+    objective_readback_async(c, 1, h + 64);
+    CGGM_CUDA_CHECK(cudaMemcpyAsync(h + 256, T, sizeof(ActTotals), cudaMemcpyDeviceToHost, s0));
+    CGGM_CUDA_CHECK(cudaStreamSynchronize(s0));
+    CholResult cr = chol_decode(h);
+    out->logdet = cr.logdet;
     out->is_pd = cr.is_pd;
     out->fail_col = cr.fail_col;
-    if (cr.is_pd) {
-      out->logdet = cr.logdet;
-      out->tr_syy_lam = h[0] / nt;
-      out->tr_sxy_theta = h[1] / nt;
-      out->tr_sigma_m = h[2] / nt;
-      out->g = -out->logdet + out->tr_syy_lam + 2.0 * out->tr_sxy_theta + out->tr_sigma_m;
-      out->f = out->g + out->pen_L + out->pen_T;
-    } else {
-      const double nan = std::numeric_limits<double>::quiet_NaN();
-      out->logdet = nan;
-      out->tr_syy_lam = h[0] / nt;
-      out->tr_sxy_theta = h[1] / nt;
-      out->tr_sigma_m = nan;
-      out->g = INFINITY;
-      out->f = INFINITY;
-    }
+    objective_decode(h + 64, n, active->lam_L, active->lam_T, &out->obj);
+    ActTotals at;
+    std::memcpy(&at, h + 256, sizeof(ActTotals));
+    active_decode(at, active);
   });
 }
 

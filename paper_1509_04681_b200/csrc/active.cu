@@ -131,7 +131,9 @@ template <bool LAM>
 __global__ void __launch_bounds__(NT) k_active_write(int64_t nrows, const double* __restrict__ G, int64_t ldg,
                                                      const int64_t* colptr, const int32_t* rowidx, const double* val,
                                                      double lam, int penalize_diag, const long long* off,
-                                                     int32_t* out_row, int32_t* out_col) {
+                                                     int32_t* out_row, int32_t* out_col, const long long* total,
+                                                     long long cap) {
+  if (*total > cap) return;  // capacity exceeded: write nothing (reported as CGGM_ERR_CAPACITY)
   extern __shared__ uint32_t bits[];
   __shared__ int warp_tot[NT / 32];
   __shared__ long long base_sh;
@@ -209,7 +211,7 @@ void active_count(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t ldg
 void active_write(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t ldgl, const double* GradT, int64_t ldgt,
                   const cggm_csc* Lambda, const cggm_csc* Theta, double lam_L, double lam_T, int penalize_diag,
                   const long long* offL, const long long* offT, int32_t* L_row, int32_t* L_col, int32_t* T_row,
-                  int32_t* T_col) {
+                  int32_t* T_col, const ActTotals* totals, long long capL, long long capT) {
   if (q == 0) return;
   size_t bl = bits_bytes(q), bt = bits_bytes(p);
   set_smem(k_active_write<true>, bl);
@@ -217,12 +219,12 @@ void active_write(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t ldg
   { Prof pr(c, TAG_ACTIVE);
   k_active_write<true><<<(unsigned)q, NT, bl, c->stream>>>(q, GradL, ldgl, Lambda->colptr, Lambda->rowidx,
                                                           static_cast<const double*>(Lambda->val), lam_L,
-                                                          penalize_diag, offL, L_row, L_col);
+                                                          penalize_diag, offL, L_row, L_col, &totals->m_L, capL);
   post_launch(c, "k_active_write<L>"); }
   { Prof pr(c, TAG_ACTIVE);
   k_active_write<false><<<(unsigned)q, NT, bt, c->stream>>>(p, GradT, ldgt, Theta->colptr, Theta->rowidx,
                                                            static_cast<const double*>(Theta->val), lam_T, 1, offT,
-                                                           T_row, T_col);
+                                                           T_row, T_col, &totals->m_T, capT);
   post_launch(c, "k_active_write<T>"); }
 }
 

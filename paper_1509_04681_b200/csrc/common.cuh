@@ -50,6 +50,9 @@ struct Ctx {
   void* host_scratch = nullptr;
   PFN_cuTensorMapEncodeTiled_v12000 encode_tiled = nullptr;
   int num_sms = 148;
+  int lane = 0;                  // 0: caller's stream, 1: auxiliary stream (separate workspace)
+  cudaStream_t aux = nullptr;    // auxiliary stream of the composite evaluation
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int force_tile = 0;
   int no_tma3d = 0;   // test hook: 1 = always use 16-wide 2-D boxes for MN-inner operands  // test hook: 0 auto, 1 = 128x128 tiles, 2 = 64x64 tiles
   // phase profiling (CUDA events around every launch while enabled)
@@ -108,9 +111,12 @@ enum Slot {
   WS_Z,             // trsm result (n x q)
   WS_SCAL,          // small device scalars / partial-sum arrays
   WS_ACT,           // active-set per-column arrays
-  WS_PACK0,         // packing for TMA-incompatible operands
+  WS_PACK0,         // packing for TMA-incompatible operands (lane 0: 0/1, lane 1: 2/3)
   WS_PACK1,
   WS_PACK2,
+  WS_PACK3,
+  WS_DENSE_B,       // augmented [Lambda; W] of the objective on the auxiliary lane
+  WS_SCAL2,         // scalar block of the auxiliary lane
   WS_NUM
 };
 

@@ -378,13 +378,13 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
   const int64_t brows = transB ? N : Keff, bcols = transB ? Keff : N;
   if (K > 0 && !tma_ok(A, lda)) {
     int64_t ld = (arows + 1) & ~int64_t(1);
-    double* pk = static_cast<double*>(ws_get(c, WS_PACK0, (size_t)ld * acols * 8));
+    double* pk = static_cast<double*>(ws_get(c, WS_PACK0 + 2 * c->lane, (size_t)ld * acols * 8));
     CGGM_CUDA_CHECK(cudaMemcpy2DAsync(pk, ld * 8, A, lda * 8, arows * 8, acols, cudaMemcpyDeviceToDevice, c->stream));
     A = pk; lda = ld;
   }
   if (K > 0 && !tma_ok(B, ldb)) {
     int64_t ld = (brows + 1) & ~int64_t(1);
-    double* pk = static_cast<double*>(ws_get(c, WS_PACK1, (size_t)ld * bcols * 8));
+    double* pk = static_cast<double*>(ws_get(c, WS_PACK1 + 2 * c->lane, (size_t)ld * bcols * 8));
     CGGM_CUDA_CHECK(cudaMemcpy2DAsync(pk, ld * 8, B, ldb * 8, brows * 8, bcols, cudaMemcpyDeviceToDevice, c->stream));
     B = pk; ldb = ld;
   }
@@ -397,7 +397,12 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
   // 128x128 tiles unless they cannot fill the GPU; then 64x64 tiles (4x the CTAs, several per SM)
   const int64_t tm = (M + 127) / 128, tn = (N + 127) / 128;
   const int64_t big_tiles = (flags & SYM_LOWER) ? tn * (tn + 1) / 2 + (tm - tn) * tn : tm * tn;
-  const bool use_big = c->force_tile ? (c->force_tile == 1) : (big_tiles >= c->num_sms);
+  // wave efficiency of the 128-tile grid; below ~0.9 (and under 3 waves) the 64-tile grid (4x the
+  // CTAs, 3 resident per SM) fills the machine better (profiles/r01_gemm_bench_tiles*.txt)
+  const int64_t waves = (big_tiles + c->num_sms - 1) / c->num_sms;
+  const double big_eff = (double)big_tiles / (double)(waves * c->num_sms);
+  const bool auto_big = big_tiles >= 3 * c->num_sms || big_eff >= 0.9;
+  const bool use_big = c->force_tile ? (c->force_tile == 1) : auto_big;
   if (use_big) run_cfg<CfgBig>(c, transA, transB, M, N, Keff, A, lda, B, ldb, P);
   else run_cfg<CfgSmall>(c, transA, transB, M, N, Keff, A, lda, B, ldb, P);
 }

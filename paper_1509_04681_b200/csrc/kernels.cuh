@@ -26,6 +26,6 @@ void active_count(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t ldg
 void active_write(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t ldgl, const double* GradT, int64_t ldgt,
                   const cggm_csc* Lambda, const cggm_csc* Theta, double lam_L, double lam_T, int penalize_diag,
                   const long long* offL, const long long* offT, int32_t* L_row, int32_t* L_col, int32_t* T_row,
-                  int32_t* T_col);
+                  int32_t* T_col, const ActTotals* totals, long long capL, long long capT);
 
 }  // namespace cggm
