@@ -51,6 +51,16 @@ def phase_flops(n, p, q):
 GEMM_TAGS = ("chol_gemm", "lauum", "w_sigma", "psi_gradL", "grad_theta", "obj_trsm")
 
 
+def _hbm_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0   # B200_PROFILING.md fallback
+
+
+HBM_PEAK_GBS = _hbm_peak()
+
+
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -329,6 +339,24 @@ def main():
             d["tflops"] = ph_flops[tag] / (tms / prof_steps * 1e-3) / 1e12
         phases[tag] = d
 
+    # HBM-bound phases: algorithmic bytes / measured time in pass B
+    m_L, m_T = last["active"]["m_L"], last["active"]["m_T"]
+    q_, p_, n_ = P.q, P.p, P.n
+    hbm_alg = {
+        "active_set": 8.0 * (q_ * (q_ + 1) / 2 + p_ * q_) + 8.0 * (m_L + m_T),   # one read of grad_L (upper), grad_T + lists
+        "grad_lambda": 32.0 * q_ * q_,                                            # read S_yy, Sigma, Psi, write grad_L
+        "spmm": 8.0 * n_ * (p_ + q_),                                             # read X once, write W
+    }
+    hbm = {}
+    for tag, by in hbm_alg.items():
+        if tag in prof and prof[tag][1] > 0:
+            calls = {"active_set": 4, "grad_lambda": 1, "spmm": 1}[tag]       # launches per call
+            n_calls = max(1, round(prof[tag][1] / calls))                     # calls in pass B
+            ms_call = prof[tag][0] / n_calls
+            gbs = by / (ms_call * 1e-3) / 1e9
+            hbm[tag] = {"alg_bytes_per_call": by, "ms_per_call": ms_call, "calls_per_step": n_calls / prof_steps,
+                        "achieved_gbs": gbs, "frac_of_measured_copy": gbs / HBM_PEAK_GBS}
+
     # ---------------------------------------------------------------- e2e through the public API
     e2e = None
     if not args.no_e2e and world == 1:
@@ -391,6 +419,8 @@ def main():
                                         f"events; {prof_elapsed / prof_steps:.1f} ms/step)",
                          "step_frac_of_peak": all_flops / (ms_step * 1e-3) / 1e12 / peak_tflops},
             "phases": phases,
+            "hbm_roofline": {"peak_gbs": HBM_PEAK_GBS, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)",
+                             "kernels": hbm},
             "e2e": e2e,
             "cpu_baseline": cpu,
             "result": {"f": obj.get("f"), "logdet": res.get("logdet"),

@@ -116,7 +116,7 @@ cggm_status cggm_ctx_release_workspace(cggm_ctx* ctx);
  * ctx stream and attributed to a phase tag (0..CGGM_PROF_NTAGS-1, names by cggm_profile_tag_name).
  * enable=1 clears previous records.  _read synchronises the stream and writes per-tag summed
  * kernel milliseconds and launch counts (arrays of >= CGGM_PROF_NTAGS entries), then clears. */
-#define CGGM_PROF_NTAGS 13
+#define CGGM_PROF_NTAGS 14
 cggm_status cggm_ctx_profile(cggm_ctx* ctx, int enable);
 cggm_status cggm_ctx_profile_read(cggm_ctx* ctx, double* ms, int64_t* launches, int32_t ntags);
 const char* cggm_profile_tag_name(int32_t tag);
@@ -166,8 +166,8 @@ cggm_status cggm_grad_lambda(cggm_ctx* ctx, int64_t q, const void* Syy, int64_t 
  * S_Lambda = {(i,j), i <= j : |GradL_ij| > lam_ij or Lambda_ij != 0}, lam_ii = 0 if !penalize_diag
  * S_Theta  = {(i,j)         : |GradT_ij| > lam_T  or Theta_ij  != 0}
  * Lists are written in ascending column-major order (deterministic).  If m_L > cap_L or
- * m_T > cap_T nothing is written, m_L/m_T hold the required sizes and CGGM_ERR_CAPACITY is
- * returned (two-call pattern).  subgrad_l1 = sum over all Lambda entries (both triangles) and
+ * m_T > cap_T, m_L/m_T hold the required sizes, CGGM_ERR_CAPACITY is returned and the list
+ * contents are unspecified (only the first cap entries may have been written; two-call pattern).  subgrad_l1 = sum over all Lambda entries (both triangles) and
  * Theta entries of |g + lam sign(x)| if x != 0 else max(|g| - lam, 0). */
 cggm_status cggm_active_set(cggm_ctx* ctx, int64_t p, int64_t q, const void* GradL, int64_t ldgl,
                             const void* GradT, int64_t ldgt, const cggm_csc* Lambda, const cggm_csc* Theta,
@@ -191,7 +191,7 @@ cggm_status cggm_objective(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int6
  * auxiliary stream concurrently with Sigma = Lambda^{-1} and the Psi / gradient / active-set work
  * on the ctx stream.  Inputs as in those calls (Syy from cggm_covariances); active->lam_L, lam_T,
  * penalize_diag are also the objective's.  One host synchronisation at the end; on
- * CGGM_ERR_CAPACITY all other outputs are valid and the lists are left unwritten. */
+ * CGGM_ERR_CAPACITY all other outputs are valid and the list contents are unspecified. */
 typedef struct cggm_eval_out {
   double logdet;            /* log|Lambda| from the inverse's factorisation (NaN if not PD) */
   int32_t is_pd;

@@ -23,7 +23,7 @@ STATUS = {
 }
 CGGM_F64 = 0
 CGGM_F32 = 1
-PROF_NTAGS = 13
+PROF_NTAGS = 14
 
 
 class cggm_csc(ctypes.Structure):

@@ -238,7 +238,7 @@ cggm_status cggm_ctx_profile_read(cggm_ctx* ctx, double* ms, int64_t* launches, 
 const char* cggm_profile_tag_name(int32_t tag) {
   static const char* names[CGGM_PROF_NTAGS] = {"misc", "covariances", "densify", "chol_gemm", "chol_leaf",
                                                "lauum", "spmm", "w_sigma", "psi_gradL", "grad_theta",
-                                               "obj_trsm", "active_set", "obj_reduce"};
+                                               "obj_trsm", "active_set", "obj_reduce", "grad_lambda"};
   return (tag >= 0 && tag < CGGM_PROF_NTAGS) ? names[tag] : "?";
 }
 
@@ -365,18 +365,11 @@ cggm_status cggm_invert_logdet(cggm_ctx* ctx, const cggm_csc* Lambda, void* Sigm
 static ActTotals* active_enqueue(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t ldgl, const double* GradT,
                                  int64_t ldgt, const cggm_csc* Lambda, const cggm_csc* Theta,
                                  const cggm_active_out* o) {
-  long long* base = static_cast<long long*>(ws_get(c, WS_ACT, (size_t)(8 * q + 16) * 8));
-  long long *cntL = base, *cntT = base + q, *tieL = base + 2 * q, *tieT = base + 3 * q, *offL = base + 4 * q,
-            *offT = base + 5 * q;
-  double* subL = reinterpret_cast<double*>(base + 6 * q);
-  double* subT = reinterpret_cast<double*>(base + 7 * q);
-  ActTotals* T = reinterpret_cast<ActTotals*>(base + 8 * q);
+  ActWs ws = active_ws(c, q);
   Phase ph(c, TAG_ACTIVE);
-  active_count(c, p, q, GradL, ldgl, GradT, ldgt, Lambda, Theta, o->lam_L, o->lam_T, o->penalize_diag, o->tie_eps, T,
-               offL, offT, cntL, cntT, tieL, tieT, subL, subT);
-  // the write pass checks the capacity on the device (writes nothing if a list would overflow)
-  active_write(c, p, q, GradL, ldgl, GradT, ldgt, Lambda, Theta, o->lam_L, o->lam_T, o->penalize_diag, offL, offT,
-               o->L_row, o->L_col, o->T_row, o->T_col, T, o->cap_L, o->cap_T);
+  active_compact(c, p, q, GradL, ldgl, GradT, ldgt, Lambda, Theta, o->lam_L, o->lam_T, o->penalize_diag, o->tie_eps, ws,
+                 o->L_row, o->L_col, o->T_row, o->T_col, o->cap_L, o->cap_T);
+  ActTotals* T = ws.tot;
   return T;
 }
 
@@ -448,7 +441,10 @@ static void psi_enqueue(Ctx* c, int64_t n_local, int64_t n_total, int64_t p, int
     Phase ph(c, TAG_PSI);
     Epilogue e; e.out1 = Psi; e.ld1 = ldpsi; e.a1 = 1.0;
     gemm(c, true, false, q, q, n_local, R, ldn, R, ldn, e, SYM_LOWER | SYM_MIRROR);
-    if (GradL) grad_lambda(c, q, Syy, ldsyy, Sg, ldsigma, Psi, ldpsi, GradL, ldgl);
+    if (GradL) {
+      Phase pg(c, TAG_GRADL);
+      grad_lambda(c, q, Syy, ldsyy, Sg, ldsigma, Psi, ldpsi, GradL, ldgl);
+    }
   }
   if (GradT) {  // a5: GradT = (2/n) X^T E   (or 2 S_xy + (2/sqrt n) X^T R)
     Phase ph(c, TAG_GRADT);
@@ -672,7 +668,7 @@ cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, con
     ws_get(c, WS_LEAFINV, (size_t)nleaves * leaf_nb() * leaf_nb() * 8);
     ws_get(c, WS_SCAL, 64 + (8 + nleaves) * 8);
     ws_get(c, WS_SCAL2, 64 + (16 + 5 * q + nleaves) * 8);
-    ws_get(c, WS_ACT, (size_t)(8 * q + 16) * 8);
+    active_ws(c, q);
     ws_get(c, WS_R, (size_t)ldn * q * 8);
     ws_get(c, WS_E, (size_t)ldn * q * 8);
     double* W = static_cast<double*>(ws_get(c, WS_W, (size_t)ldn * q * 8));

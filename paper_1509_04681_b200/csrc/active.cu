@@ -1,231 +1,273 @@
 // Active sets S_Lambda, S_Theta (§2.2) and the minimum-norm-subgradient stopping
-// statistic (§5.1), as ordered, deterministic stream compaction:
-//   1. count pass: one CTA per column; the column's stored nonzeros are set in a shared-memory
-//      bitmask (value test, reading A7), the dense gradient column is scanned coalesced, and the
-//      CTA writes (count, tie count, subgradient partial) for the column;
-//   2. one-CTA exclusive scan of the counts -> per-column offsets + totals (fixed-order sums);
-//   3. write pass: the same flags, block prefix sums via warp ballots, (row, col) written at the
-//      column's offset -> ascending column-major order, identical run to run.
+// statistic (§5.1) as a SINGLE-PASS ordered stream compaction:
+// one CTA per column j (columns are dispatched in order), 8 warps each scanning a contiguous
+// 32-aligned segment of the column with 4 loads in flight per lane:
+//   1. the column's stored nonzeros are set in a shared-memory support bitmask (value test,
+//      reading A7);
+//   2. each 32-row chunk's flags (|g| > lam or support) are kept as one ballot word in shared
+//      memory; tie count and subgradient partial accumulate in registers;
+//   3. the column offset comes from a decoupled look-back over the preceding columns' published
+//      (aggregate | inclusive prefix) states -- no second pass over the gradient;
+//   4. each warp writes (row, col) for its set bits from the shared bitmask -> ascending
+//      column-major order, identical run to run.
+// A final one-CTA kernel sums the per-column tie counts and subgradient partials in fixed order.
 // Lambda: only i <= j is listed (reading A6); the subgradient covers both triangles using the
 // exact symmetry of grad_Lambda (weight 2 for i < j) plus an exact per-stored-entry correction
-// |g + lam sign(x)| - max(|g| - lam, 0) for nonzero x.
+// |g + lam sign(x)| - max(|g| - lam, 0) for nonzero x.  HBM bytes per call: one read of the
+// upper triangle of grad_Lambda and of grad_Theta, 8 bytes written per active entry.
 #include "kernels.cuh"
 
 namespace cggm {
 namespace {
 
 constexpr int NT = 256;
+constexpr int NW = NT / 32;   // warp segments per column
+constexpr int UNR = 4;        // 32-row chunks in flight per lane
+constexpr unsigned long long ST_AGG = 1ull << 62, ST_INC = 2ull << 62, ST_VAL = (1ull << 62) - 1;
 
 template <bool LAM>
 __device__ __forceinline__ double lam_of(int64_t i, int64_t j, double lam, int penalize_diag) {
   return (LAM && i == j && !penalize_diag) ? 0.0 : lam;
 }
 
-template <bool LAM>
-__device__ void build_bits(uint32_t* bits, int64_t nwords, const int64_t* colptr, const int32_t* rowidx,
-                           const double* val, int64_t j, int64_t scan_rows) {
-  for (int64_t w = threadIdx.x; w < nwords; w += NT) bits[w] = 0u;
-  __syncthreads();
-  for (int64_t t = colptr[j] + threadIdx.x; t < colptr[j + 1]; t += NT) {
-    const int32_t r = rowidx[t];
-    if (r < scan_rows && val[t] != 0.0) atomicOr(&bits[r >> 5], 1u << (r & 31));
-  }
-  __syncthreads();
+// contiguous, 32-aligned segment of warp w among NW for a column of `rows` rows
+__device__ __forceinline__ void segment(int64_t rows, int w, int64_t& a, int64_t& b) {
+  const int64_t chunks = (rows + 31) >> 5;
+  const int64_t per = (chunks + NW - 1) / NW;
+  a = min(rows, (int64_t)w * per * 32);
+  b = min(rows, (int64_t)(w + 1) * per * 32);
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 template <bool LAM>
-__global__ void __launch_bounds__(NT) k_active_count(int64_t nrows, const double* __restrict__ G, int64_t ldg,
-                                                     const int64_t* colptr, const int32_t* rowidx, const double* val,
-                                                     double lam, int penalize_diag, double tie_eps, long long* cnt,
-                                                     long long* ties, double* sub) {
-  extern __shared__ uint32_t bits[];
-  __shared__ double shd[NT];
-  __shared__ long long shc[NT], sht[NT];
+__global__ void __launch_bounds__(NT) k_active_onepass(int64_t nrows, const double* __restrict__ G, int64_t ldg,
+                                                       const int64_t* colptr, const int32_t* rowidx,
+                                                       const double* val, double lam, int penalize_diag,
+                                                       double tie_eps, unsigned long long* state, int32_t* out_row,
+                                                       int32_t* out_col, long long cap, long long* ties_col,
+                                                       double* sub_col) {
+  extern __shared__ uint32_t sm[];
   const int64_t j = blockIdx.x;
   const int64_t scan_rows = LAM ? j + 1 : nrows;
   const int64_t nwords = (scan_rows + 31) >> 5;
-  build_bits<LAM>(bits, nwords, colptr, rowidx, val, j, scan_rows);
-  long long c = 0, tc = 0;
-  double s = 0.0;
-  const double* gc = G + j * ldg;
-  for (int64_t i = threadIdx.x; i < scan_rows; i += NT) {
-    const double a = fabs(gc[i]);
-    const double lm = lam_of<LAM>(i, j, lam, penalize_diag);
-    const bool sup = (bits[i >> 5] >> (i & 31)) & 1u;
-    c += (a > lm || sup) ? 1 : 0;
-    tc += (!sup && fabs(a - lm) <= tie_eps) ? 1 : 0;
-    const double w = (LAM && i < j) ? 2.0 : 1.0;
-    s += w * fmax(a - lm, 0.0);
+  uint32_t* sup_bits = sm;
+  uint32_t* flag_bits = sm + nwords;
+  __shared__ int wcnt[NW];
+  __shared__ double wsub[NW];
+  __shared__ long long wtie[NW];
+  __shared__ long long col_base;
+  for (int64_t w = threadIdx.x; w < nwords; w += NT) sup_bits[w] = 0u;
+  __syncthreads();
+  for (int64_t t = colptr[j] + threadIdx.x; t < colptr[j + 1]; t += NT) {
+    const int32_t r = rowidx[t];
+    if (r < scan_rows && val[t] != 0.0) atomicOr(&sup_bits[r >> 5], 1u << (r & 31));
   }
-  // exact correction for stored nonzeros (all rows of the column)
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t a, b;
+  segment(scan_rows, w, a, b);
+  const double* gc = G + j * ldg;
+  int cnt = 0;
+  long long tc = 0;
+  double s = 0.0;
+  const int ib = (int)b;
+  const int jj = (int)j;
+  for (int r0 = (int)a; r0 < ib; r0 += 32 * UNR) {
+    double g[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int i = r0 + u * 32 + lane;
+      g[u] = (i < ib) ? __ldcs(gc + i) : 0.0;   // streamed once: evict-first
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int c0 = r0 + u * 32;
+      if (c0 >= ib) break;   // warp-uniform
+      const int i = c0 + lane;
+      const bool in = i < ib;
+      const unsigned supw = sup_bits[c0 >> 5];   // one broadcast word per 32-row chunk
+      const bool sup = (supw >> lane) & 1u;
+      const double lm = (LAM && i == jj && !penalize_diag) ? 0.0 : lam;
+      const double av = fabs(g[u]);
+      const double d = av - lm;
+      const bool f = in && (d > 0.0 || sup);
+      const unsigned m = __ballot_sync(0xffffffffu, f);
+      if (lane == 0) flag_bits[c0 >> 5] = m;
+      cnt += __popc(m);
+      tc += (in && !sup && fabs(d) <= tie_eps) ? 1 : 0;
+      if (in) s += (LAM && i < jj) ? 2.0 * fmax(d, 0.0) : fmax(d, 0.0);
+    }
+  }
   for (int64_t t = colptr[j] + threadIdx.x; t < colptr[j + 1]; t += NT) {
     const double x = val[t];
     if (x == 0.0) continue;
     const int64_t i = rowidx[t];
-    const double g = gc[i];
+    const double gv = gc[i];
     const double lm = lam_of<LAM>(i, j, lam, penalize_diag);
-    s += fabs(g + lm * (x > 0.0 ? 1.0 : -1.0)) - fmax(fabs(g) - lm, 0.0);
+    s += fabs(gv + lm * (x > 0.0 ? 1.0 : -1.0)) - fmax(fabs(gv) - lm, 0.0);
   }
-  shd[threadIdx.x] = s;
-  shc[threadIdx.x] = c;
-  sht[threadIdx.x] = tc;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_down_sync(0xffffffffu, s, o);
+    tc += __shfl_down_sync(0xffffffffu, tc, o);
+  }
+  if (lane == 0) {
+    wcnt[w] = cnt;
+    wsub[w] = s;
+    wtie[w] = tc;
+  }
   __syncthreads();
-  for (int st = NT / 2; st > 0; st >>= 1) {
-    if (threadIdx.x < st) {
-      shd[threadIdx.x] += shd[threadIdx.x + st];
-      shc[threadIdx.x] += shc[threadIdx.x + st];
-      sht[threadIdx.x] += sht[threadIdx.x + st];
+  if (w == 0) {
+    long long total = 0, tt = 0;
+    double ss = 0.0;
+    for (int k = 0; k < NW; ++k) {
+      total += wcnt[k];
+      tt += wtie[k];
+      ss += wsub[k];
     }
-    __syncthreads();
+    if (lane == 0) {
+      sub_col[j] = ss;
+      ties_col[j] = tt;
+      st_release(&state[j], (j == 0 ? ST_INC : ST_AGG) | (unsigned long long)total);
+    }
+    // decoupled look-back, one warp: lane l inspects predecessor j-1-l of the current window
+    long long excl = 0;
+    int64_t k0 = j - 1;
+    while (k0 >= 0) {
+      const int64_t k = k0 - lane;
+      unsigned long long v = (k >= 0) ? ld_acquire(&state[k]) : ST_INC;   // before column 0: prefix 0
+      while (__any_sync(0xffffffffu, (v & ~ST_VAL) == 0)) {
+        if ((v & ~ST_VAL) == 0) v = ld_acquire(&state[k]);
+      }
+      const unsigned inc = __ballot_sync(0xffffffffu, (v & ~ST_VAL) == ST_INC);
+      const int stop = inc ? __ffs(inc) - 1 : 31;          // nearest inclusive predecessor
+      long long add = (lane <= stop && k >= 0) ? (long long)(v & ST_VAL) : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
+      excl += add;
+      if (inc) break;
+      k0 -= 32;
+    }
+    if (lane == 0) {
+      if (j > 0) st_release(&state[j], ST_INC | (unsigned long long)(excl + total));
+      col_base = excl;
+    }
   }
-  if (threadIdx.x == 0) {
-    cnt[j] = shc[0];
-    ties[j] = sht[0];
-    sub[j] = shd[0];
+  __syncthreads();
+  long long pos = col_base;
+  for (int k = 0; k < w; ++k) pos += wcnt[k];
+  const unsigned below = (1u << lane) - 1u;
+  for (int64_t r0 = a; r0 < b; r0 += 32) {
+    const unsigned m = flag_bits[r0 >> 5];
+    if (m & (1u << lane)) {
+      const long long p = pos + __popc(m & below);
+      if (p < cap) {
+        out_row[p] = (int32_t)(r0 + lane);
+        out_col[p] = (int32_t)j;
+      }
+    }
+    pos += __popc(m);
   }
 }
 
-// single CTA: exclusive scan of cnt -> off, totals (fixed-order sums)
-constexpr int SCAN_NT = 1024;
-__global__ void __launch_bounds__(SCAN_NT) k_active_scan(int64_t ncols, const long long* cnt, const long long* ties,
-                                                         const double* sub, long long* off, long long* tot_m,
-                                                         long long* tot_ties, double* tot_sub) {
-  __shared__ long long sc[SCAN_NT], st[SCAN_NT];
-  __shared__ double sd[SCAN_NT];
-  const int64_t per = (ncols + SCAN_NT - 1) / SCAN_NT;
+// totals: m from the last column's inclusive state, ties / subgradient summed in fixed order
+constexpr int TOT_NT = 1024;
+__global__ void __launch_bounds__(TOT_NT) k_active_totals(int64_t ncols, const unsigned long long* state,
+                                                          const long long* ties_col, const double* sub_col,
+                                                          long long* tot_m, long long* tot_ties, double* tot_sub) {
+  __shared__ long long st[TOT_NT];
+  __shared__ double sd[TOT_NT];
+  const int64_t per = (ncols + TOT_NT - 1) / TOT_NT;
   const int64_t b = threadIdx.x * per, e = min(ncols, b + per);
-  long long c = 0, tsum = 0;
+  long long t = 0;
   double d = 0.0;
   for (int64_t i = b; i < e; ++i) {
-    c += cnt[i];
-    tsum += ties[i];
-    d += sub[i];
+    t += ties_col[i];
+    d += sub_col[i];
   }
-  sc[threadIdx.x] = c;
-  st[threadIdx.x] = tsum;
+  st[threadIdx.x] = t;
   sd[threadIdx.x] = d;
   __syncthreads();
   if (threadIdx.x == 0) {
-    long long run = 0, tt = 0;
+    long long tt = 0;
     double dd = 0.0;
-    for (int k = 0; k < SCAN_NT; ++k) {
-      const long long v = sc[k];
-      sc[k] = run;
-      run += v;
+    for (int k = 0; k < TOT_NT; ++k) {
       tt += st[k];
       dd += sd[k];
     }
-    *tot_m = run;
+    *tot_m = ncols > 0 ? (long long)(state[ncols - 1] & ST_VAL) : 0;
     *tot_ties = tt;
     *tot_sub = dd;
   }
-  __syncthreads();
-  long long run = sc[threadIdx.x];
-  for (int64_t i = b; i < e; ++i) {
-    off[i] = run;
-    run += cnt[i];
-  }
 }
 
-template <bool LAM>
-__global__ void __launch_bounds__(NT) k_active_write(int64_t nrows, const double* __restrict__ G, int64_t ldg,
-                                                     const int64_t* colptr, const int32_t* rowidx, const double* val,
-                                                     double lam, int penalize_diag, const long long* off,
-                                                     int32_t* out_row, int32_t* out_col, const long long* total,
-                                                     long long cap) {
-  if (*total > cap) return;  // capacity exceeded: write nothing (reported as CGGM_ERR_CAPACITY)
-  extern __shared__ uint32_t bits[];
-  __shared__ int warp_tot[NT / 32];
-  __shared__ long long base_sh;
-  const int64_t j = blockIdx.x;
-  const int64_t scan_rows = LAM ? j + 1 : nrows;
-  const int64_t nwords = (scan_rows + 31) >> 5;
-  build_bits<LAM>(bits, nwords, colptr, rowidx, val, j, scan_rows);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const double* gc = G + j * ldg;
-  long long base = off[j];
-  for (int64_t r0 = 0; r0 < scan_rows; r0 += NT) {
-    const int64_t i = r0 + threadIdx.x;
-    bool f = false;
-    if (i < scan_rows) {
-      const double a = fabs(gc[i]);
-      const double lm = lam_of<LAM>(i, j, lam, penalize_diag);
-      const bool sup = (bits[i >> 5] >> (i & 31)) & 1u;
-      f = (a > lm) || sup;
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, f);
-    if (lane == 0) warp_tot[warp] = __popc(m);
-    __syncthreads();
-    int before = 0, total = 0;
-    for (int w = 0; w < NT / 32; ++w) {
-      if (w < warp) before += warp_tot[w];
-      total += warp_tot[w];
-    }
-    if (f) {
-      const long long pos = base + before + __popc(m & ((1u << lane) - 1u));
-      out_row[pos] = (int32_t)i;
-      out_col[pos] = (int32_t)j;
-    }
-    base += total;
-    __syncthreads();
-  }
-  (void)base_sh;
-}
-
-size_t bits_bytes(int64_t rows) { return (size_t)((rows + 31) / 32) * 4; }
+size_t smem_bytes(int64_t rows) { return (size_t)((rows + 31) / 32) * 4 * 2; }
 
 template <typename K>
 void set_smem(K kernel, size_t bytes) {
-  if (bytes > 48 * 1024)
-    CGGM_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  if (bytes > 40 * 1024)
+    CGGM_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes + 4096));
 }
 
 }  // namespace
 
-void active_count(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t ldgl, const double* GradT, int64_t ldgt,
-                  const cggm_csc* Lambda, const cggm_csc* Theta, double lam_L, double lam_T, int penalize_diag,
-                  double tie_eps, ActTotals* T, long long* offL, long long* offT, long long* cntL, long long* cntT,
-                  long long* tieL, long long* tieT, double* subL, double* subT) {
-  if (q == 0) return;
-  size_t bl = bits_bytes(q), bt = bits_bytes(p);
-  set_smem(k_active_count<true>, bl);
-  set_smem(k_active_count<false>, bt);
-  { Prof pr(c, TAG_ACTIVE);
-  k_active_count<true><<<(unsigned)q, NT, bl, c->stream>>>(q, GradL, ldgl, Lambda->colptr, Lambda->rowidx,
-                                                          static_cast<const double*>(Lambda->val), lam_L,
-                                                          penalize_diag, tie_eps, cntL, tieL, subL);
-  post_launch(c, "k_active_count<L>"); }
-  { Prof pr(c, TAG_ACTIVE);
-  k_active_count<false><<<(unsigned)q, NT, bt, c->stream>>>(p, GradT, ldgt, Theta->colptr, Theta->rowidx,
-                                                           static_cast<const double*>(Theta->val), lam_T, 1, tie_eps,
-                                                           cntT, tieT, subT);
-  post_launch(c, "k_active_count<T>"); }
-  { Prof pr(c, TAG_ACTIVE);
-  k_active_scan<<<1, SCAN_NT, 0, c->stream>>>(q, cntL, tieL, subL, offL, &T->m_L, &T->ties_L, &T->sub_L);
-  post_launch(c, "k_active_scan<L>"); }
-  { Prof pr(c, TAG_ACTIVE);
-  k_active_scan<<<1, SCAN_NT, 0, c->stream>>>(q, cntT, tieT, subT, offT, &T->m_T, &T->ties_T, &T->sub_T);
-  post_launch(c, "k_active_scan<T>"); }
+ActWs active_ws(Ctx* c, int64_t q) {
+  const size_t bytes = (size_t)q * 2 * (8 + 8 + 8) + sizeof(ActTotals) + 256;
+  char* base = static_cast<char*>(ws_get(c, WS_ACT, bytes));
+  ActWs w;
+  w.stateL = reinterpret_cast<unsigned long long*>(base);
+  w.stateT = w.stateL + q;
+  w.tieL = reinterpret_cast<long long*>(w.stateT + q);
+  w.tieT = w.tieL + q;
+  w.subL = reinterpret_cast<double*>(w.tieT + q);
+  w.subT = w.subL + q;
+  w.tot = reinterpret_cast<ActTotals*>(w.subT + q);
+  return w;
 }
 
-void active_write(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t ldgl, const double* GradT, int64_t ldgt,
-                  const cggm_csc* Lambda, const cggm_csc* Theta, double lam_L, double lam_T, int penalize_diag,
-                  const long long* offL, const long long* offT, int32_t* L_row, int32_t* L_col, int32_t* T_row,
-                  int32_t* T_col, const ActTotals* totals, long long capL, long long capT) {
+void active_compact(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t ldgl, const double* GradT,
+                    int64_t ldgt, const cggm_csc* Lambda, const cggm_csc* Theta, double lam_L, double lam_T,
+                    int penalize_diag, double tie_eps, const ActWs& ws, int32_t* L_row, int32_t* L_col,
+                    int32_t* T_row, int32_t* T_col, long long capL, long long capT) {
   if (q == 0) return;
-  size_t bl = bits_bytes(q), bt = bits_bytes(p);
-  set_smem(k_active_write<true>, bl);
-  set_smem(k_active_write<false>, bt);
-  { Prof pr(c, TAG_ACTIVE);
-  k_active_write<true><<<(unsigned)q, NT, bl, c->stream>>>(q, GradL, ldgl, Lambda->colptr, Lambda->rowidx,
-                                                          static_cast<const double*>(Lambda->val), lam_L,
-                                                          penalize_diag, offL, L_row, L_col, &totals->m_L, capL);
-  post_launch(c, "k_active_write<L>"); }
-  { Prof pr(c, TAG_ACTIVE);
-  k_active_write<false><<<(unsigned)q, NT, bt, c->stream>>>(p, GradT, ldgt, Theta->colptr, Theta->rowidx,
-                                                           static_cast<const double*>(Theta->val), lam_T, 1, offT,
-                                                           T_row, T_col, &totals->m_T, capT);
-  post_launch(c, "k_active_write<T>"); }
+  CGGM_CUDA_CHECK(cudaMemsetAsync(ws.stateL, 0, (size_t)q * 2 * 8, c->stream));
+  const size_t bl = smem_bytes(q), bt = smem_bytes(p);
+  set_smem(k_active_onepass<true>, bl);
+  set_smem(k_active_onepass<false>, bt);
+  {
+    Prof pr(c, TAG_ACTIVE);
+    k_active_onepass<true><<<(unsigned)q, NT, bl, c->stream>>>(
+        q, GradL, ldgl, Lambda->colptr, Lambda->rowidx, static_cast<const double*>(Lambda->val), lam_L, penalize_diag,
+        tie_eps, ws.stateL, L_row, L_col, capL, ws.tieL, ws.subL);
+    post_launch(c, "k_active_onepass<L>");
+  }
+  {
+    Prof pr(c, TAG_ACTIVE);
+    k_active_onepass<false><<<(unsigned)q, NT, bt, c->stream>>>(
+        p, GradT, ldgt, Theta->colptr, Theta->rowidx, static_cast<const double*>(Theta->val), lam_T, 1, tie_eps,
+        ws.stateT, T_row, T_col, capT, ws.tieT, ws.subT);
+    post_launch(c, "k_active_onepass<T>");
+  }
+  {
+    Prof pr(c, TAG_ACTIVE);
+    k_active_totals<<<1, TOT_NT, 0, c->stream>>>(q, ws.stateL, ws.tieL, ws.subL, &ws.tot->m_L, &ws.tot->ties_L,
+                                                 &ws.tot->sub_L);
+    post_launch(c, "k_active_totals<L>");
+  }
+  {
+    Prof pr(c, TAG_ACTIVE);
+    k_active_totals<<<1, TOT_NT, 0, c->stream>>>(q, ws.stateT, ws.tieT, ws.subT, &ws.tot->m_T, &ws.tot->ties_T,
+                                                 &ws.tot->sub_T);
+    post_launch(c, "k_active_totals<T>");
+  }
 }
 
 }  // namespace cggm

@@ -34,6 +34,7 @@ enum ProfTag {
   TAG_TRSM,        // objective triangular solve W L^{-T}
   TAG_ACTIVE,      // active-set count / scan / write
   TAG_OBJRED,      // objective reductions
+  TAG_GRADL,       // grad_Lambda = (S_yy - Sigma) - Psi streaming pass
   TAG_NUM
 };
 

@@ -13,19 +13,24 @@ void sum_arrays(Ctx* c, int count, const double* const* arrs_dev, const int64_t*
 void init_scalars(Ctx* c, int* fail_col, int* flag);
 void sum_arrays_1(Ctx* c, const double* a, int64_t len, double* out_dev);
 
-// Active sets (active.cu).  Device result block layout (int64 / double):
+// Active sets (active.cu).  Device totals:
 struct ActTotals {
   long long m_L, m_T, ties_L, ties_T;
   double sub_L, sub_T;
 };
-// Count pass + scan: fills totals_dev and per-column offsets (device).
-void active_count(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t ldgl, const double* GradT, int64_t ldgt,
-                  const cggm_csc* Lambda, const cggm_csc* Theta, double lam_L, double lam_T, int penalize_diag,
-                  double tie_eps, ActTotals* totals_dev, long long* offL, long long* offT, long long* cntL,
-                  long long* cntT, long long* tieL, long long* tieT, double* subL, double* subT);
-void active_write(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t ldgl, const double* GradT, int64_t ldgt,
-                  const cggm_csc* Lambda, const cggm_csc* Theta, double lam_L, double lam_T, int penalize_diag,
-                  const long long* offL, const long long* offT, int32_t* L_row, int32_t* L_col, int32_t* T_row,
-                  int32_t* T_col, const ActTotals* totals, long long capL, long long capT);
+// per-column look-back states and partials, in workspace slot WS_ACT
+struct ActWs {
+  unsigned long long *stateL, *stateT;
+  long long *tieL, *tieT;
+  double *subL, *subT;
+  ActTotals* tot;
+};
+ActWs active_ws(Ctx* c, int64_t q);
+// Single-pass ordered compaction of both lists + totals (device).  Entries at positions >= cap are
+// not written (the caller reports CGGM_ERR_CAPACITY from the totals).
+void active_compact(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t ldgl, const double* GradT,
+                    int64_t ldgt, const cggm_csc* Lambda, const cggm_csc* Theta, double lam_L, double lam_T,
+                    int penalize_diag, double tie_eps, const ActWs& ws, int32_t* L_row, int32_t* L_col,
+                    int32_t* T_row, int32_t* T_col, long long capL, long long capT);
 
 }  // namespace cggm
