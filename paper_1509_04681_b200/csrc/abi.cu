@@ -540,11 +540,19 @@ static void objective_enqueue(Ctx* c, int lane, int64_t n_local, int64_t q, cons
   double* penLp = partZ + q;
   double* penTp = penLp + q;
   double* slots = penTp + q;
+  // inverses of the <= BINV diagonal blocks + temporaries (full-inverse subtrees, block products)
+  const int64_t binv = block_inverse_size();
+  const int64_t ldxd = even(q);
+  const size_t tmp_elems = (size_t)(binv + 2) * (binv + 2);
+  const size_t tmp2_elems = (size_t)even(q + n_local) * binv;
+  double* xdiag = static_cast<double*>(ws_get(c, WS_XDIAG, (size_t)ldxd * binv * 8));
+  double* tmpo = static_cast<double*>(ws_get(c, WS_TMP_OBJ, (tmp_elems + tmp2_elems) * 8));
+  CGGM_CUDA_CHECK(cudaMemsetAsync(xdiag, 0, (size_t)ldxd * binv * 8, c->stream));
   densify_csc(c, Lambda, View{A, ldaug, q, q});
   copy2d(c, View{A + q, ldaug, n_local, q}, Wd, ldwd);
   init_scalars(c, s.fail, s.flag);
   potrf_recursive(c, View{A, ldaug, q + n_local, q}, View{nullptr, ldaug, q, q}, false, leafinv, slots, s.fail,
-                  nullptr, 0);
+                  tmpo, tmp_elems, xdiag, ldxd, tmpo + tmp_elems, tmp2_elems);
   Phase ph(c, TAG_OBJRED);
   col_partials(c, 0, n_local, q, Yd, ldy, nullptr, 0, Lambda, partY);
   col_partials(c, 1, n_local, q, Wd, ldwd, Yd, ldy, nullptr, partWY);
@@ -666,6 +674,9 @@ cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, con
     ws_get(c, WS_LINV, (size_t)even(q) * q * 8);
     ws_get(c, WS_TMP, (size_t)(q / 2 + 128) * (q / 2 + 130) * 8);
     ws_get(c, WS_LEAFINV, (size_t)nleaves * leaf_nb() * leaf_nb() * 8);
+    ws_get(c, WS_XDIAG, (size_t)even(q) * block_inverse_size() * 8);
+    ws_get(c, WS_TMP_OBJ, ((size_t)(block_inverse_size() + 2) * (block_inverse_size() + 2) +
+                           (size_t)even(q + n) * block_inverse_size()) * 8);
     ws_get(c, WS_SCAL, 64 + (8 + nleaves) * 8);
     ws_get(c, WS_SCAL2, 64 + (16 + 5 * q + nleaves) * 8);
     active_ws(c, q);

@@ -156,15 +156,33 @@ int split_point(int64_t n) {
   return (int)n1;
 }
 
+constexpr int BINV = 512;   // potrf-only mode: diagonal subtrees up to this size keep their inverse
+
 struct Rec {
   Ctx* c;
   bool full_inverse;
   double* leafinv;   // compact leaf inverses (potrf-only mode), leaf k at leafinv + k*NB*NB, ld NB
   double* logdet_slots;
   int* fail_col;
-  double* tmp;
+  double* tmp;       // full-inverse recursion temporaries
   size_t tmp_elems;
+  double* xdiag;     // potrf-only: inverse of the diagonal block at col0 stored at xdiag + col0 (ld ldxd)
+  int64_t ldxd;
+  double* tmp2;      // potrf-only: out-of-place product buffer for B := B Xblock^T
+  size_t tmp2_elems;
 };
+
+// B := B Xb^T for the inverse Xb (n x n, lower) of one diagonal block, out of place through tmp2
+void apply_block_inverse(Rec& R, View B, const double* xb, int64_t ldxb, int64_t n) {
+  if (B.rows == 0) return;
+  const int64_t ldt = B.rows + (B.rows & 1);
+  if ((size_t)(ldt * n) > R.tmp2_elems) throw CudaError{CGGM_ERR_OOM, "block-inverse temp too small"};
+  Epilogue e; e.out1 = R.tmp2; e.ld1 = ldt;
+  gemm(R.c, false, true, B.rows, n, n, B.p, B.ld, xb, ldxb, e, B_KLE_N);
+  copy2d(R.c, B, R.tmp2, ldt);
+}
+
+void trsm_rec(Rec& R, View B, View L, int64_t col0);
 
 void leaf(Rec& R, View A, View X, int64_t col0) {
   const int nb = (int)A.rows;
@@ -195,6 +213,16 @@ void leaf(Rec& R, View A, View X, int64_t col0) {
 void node(Rec& R, View A, View X, int64_t col0) {
   const int64_t n = A.cols, extra = A.rows - A.cols;
   Ctx* c = R.c;
+  if (!R.full_inverse && R.xdiag && n <= BINV) {
+    // potrf-only: factor this diagonal subtree in full-inverse mode, keeping its inverse for the
+    // triangular solves of the panels to its right and of the appended rows below
+    Rec R2 = R;
+    R2.full_inverse = true;
+    View Xb{R.xdiag + col0, R.ldxd, n, n};
+    node(R2, A.sub(0, 0, n, n), Xb, col0);
+    if (extra > 0) apply_block_inverse(R, A.sub(n, 0, extra, n), Xb.p, Xb.ld, n);
+    return;
+  }
   if (n <= NB) {
     leaf(R, A.sub(0, 0, n, n), X, col0);
     if (extra > 0) {  // bottom rows: B := B Xleaf^T (N <= 64: one tile column, in place)
@@ -231,7 +259,7 @@ void node(Rec& R, View A, View X, int64_t col0) {
     }
   } else {
     node(R, A11, X, col0);
-    trsm_right_lt(c, A21, A11, R.leafinv, col0);
+    trsm_rec(R, A21, A11, col0);
     {  // A22 -= A21 A21^T over the lower trapezoid (square part + appended rows)
       Epilogue e; e.out1 = A22.p; e.ld1 = A22.ld; e.a1 = -1.0; e.in1a = A22.p; e.ld1a = A22.ld; e.b1 = 1.0;
       gemm(c, false, true, n2 + extra, n2, n1, A21.p, A21.ld, A21.p, A21.ld, e, SYM_LOWER);
@@ -240,37 +268,46 @@ void node(Rec& R, View A, View X, int64_t col0) {
   }
 }
 
+// B (m x n) := B L^{-T}, L the factor of the diagonal block at col0.  Same split tree as node(),
+// so the recursion reaches exactly the blocks whose inverses node() kept.
+void trsm_rec(Rec& R, View B, View L, int64_t col0) {
+  const int64_t n = L.rows;
+  if (B.rows == 0) return;
+  if (R.xdiag && n <= BINV) {
+    apply_block_inverse(R, B, R.xdiag + col0, R.ldxd, n);
+    return;
+  }
+  if (n <= NB) {
+    // B := B Xleaf^T; N = n <= 64 fits one tile column, so each CTA reads only the rows it writes
+    const double* xl = R.leafinv + (col0 / NB) * NB * NB;
+    Epilogue e; e.out1 = B.p; e.ld1 = B.ld;
+    gemm(R.c, false, true, B.rows, n, n, B.p, B.ld, xl, NB, e, B_KLE_N);
+    return;
+  }
+  const int64_t n1 = split_point(n), n2 = n - n1;
+  View B1 = B.sub(0, 0, B.rows, n1), B2 = B.sub(0, n1, B.rows, n2);
+  trsm_rec(R, B1, L.sub(0, 0, n1, n1), col0);
+  {  // B2 -= B1 L21^T
+    View L21 = L.sub(n1, 0, n2, n1);
+    Epilogue e; e.out1 = B2.p; e.ld1 = B2.ld; e.a1 = -1.0; e.in1a = B2.p; e.ld1a = B2.ld; e.b1 = 1.0;
+    gemm(R.c, false, true, B.rows, n2, n1, B1.p, B1.ld, L21.p, L21.ld, e, 0);
+  }
+  trsm_rec(R, B2, L.sub(n1, n1, n2, n2), col0 + n1);
+}
+
 }  // namespace
 
 int leaf_nb() { return NB; }
 
 void potrf_recursive(Ctx* c, View A, View Linv, bool full_inverse, double* leafinv, double* logdet_slots,
-                     int* fail_col_dev, double* tmp, size_t tmp_elems) {
-  Rec R{c, full_inverse, leafinv, logdet_slots, fail_col_dev, tmp, tmp_elems};
+                     int* fail_col_dev, double* tmp, size_t tmp_elems, double* xdiag, int64_t ldxd, double* tmp2,
+                     size_t tmp2_elems) {
+  Rec R{c, full_inverse, leafinv, logdet_slots, fail_col_dev, tmp, tmp_elems, xdiag, ldxd, tmp2, tmp2_elems};
   Phase ph(c, TAG_CHOL_GEMM);
   node(R, A, Linv, 0);
 }
 
-void trsm_right_lt(Ctx* c, View B, View L, const double* leafinv, int64_t col0) {
-  const int64_t n = L.rows;
-  if (B.rows == 0) return;
-  if (n <= NB) {
-    // B := B Xleaf^T; N = n <= 64 fits one tile column, so each CTA reads only the rows it writes
-    const double* xl = leafinv + (col0 / NB) * NB * NB;
-    Epilogue e; e.out1 = B.p; e.ld1 = B.ld;
-    gemm(c, false, true, B.rows, n, n, B.p, B.ld, xl, NB, e, B_KLE_N);
-    return;
-  }
-  const int64_t n1 = split_point(n), n2 = n - n1;
-  View B1 = B.sub(0, 0, B.rows, n1), B2 = B.sub(0, n1, B.rows, n2);
-  trsm_right_lt(c, B1, L.sub(0, 0, n1, n1), leafinv, col0);
-  {  // B2 -= B1 L21^T
-    View L21 = L.sub(n1, 0, n2, n1);
-    Epilogue e; e.out1 = B2.p; e.ld1 = B2.ld; e.a1 = -1.0; e.in1a = B2.p; e.ld1a = B2.ld; e.b1 = 1.0;
-    gemm(c, false, true, B.rows, n2, n1, B1.p, B1.ld, L21.p, L21.ld, e, 0);
-  }
-  trsm_right_lt(c, B2, L.sub(n1, n1, n2, n2), leafinv, col0 + n1);
-}
+int block_inverse_size() { return BINV; }
 
 void lauum(Ctx* c, View Linv, View Sigma) {
   const int64_t q = Linv.rows;

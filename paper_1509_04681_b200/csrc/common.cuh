@@ -117,6 +117,8 @@ enum Slot {
   WS_PACK2,
   WS_PACK3,
   WS_DENSE_B,       // augmented [Lambda; W] of the objective on the auxiliary lane
+  WS_XDIAG,         // objective: inverses of the <= 512-column diagonal blocks (q x 512)
+  WS_TMP_OBJ,       // objective: recursion temporaries (full-inverse subtrees + block products)
   WS_SCAL2,         // scalar block of the auxiliary lane
   WS_NUM
 };
@@ -186,10 +188,13 @@ struct CholResult {
   int is_pd;
   int64_t fail_col;
 };
+//  potrf-only mode with xdiag != null: diagonal subtrees of <= block_inverse_size() columns are
+//  factored in full-inverse mode, their inverses kept at xdiag + col0 (ld ldxd, zeroed upper
+//  triangles required) and used for the panel solves (tmp2: out-of-place product buffer).
 void potrf_recursive(Ctx* c, View A, View Linv, bool full_inverse, double* leafinv, double* logdet_slots,
-                     int* fail_col_dev, double* tmp, size_t tmp_elems);
-// B (m x n) := B L^{-T} for the lower-triangular factor L (n x n) using compact leaf inverses.
-void trsm_right_lt(Ctx* c, View B, View L, const double* leafinv, int64_t col0);
+                     int* fail_col_dev, double* tmp, size_t tmp_elems, double* xdiag = nullptr, int64_t ldxd = 0,
+                     double* tmp2 = nullptr, size_t tmp2_elems = 0);
+int block_inverse_size();
 // Sigma = Linv^T Linv (full symmetric).
 void lauum(Ctx* c, View Linv, View Sigma);
 int leaf_nb();
