@@ -78,6 +78,8 @@ SIGNATURES = {
                                  ctypes.POINTER(cggm_eval_out)]),
     "cggm_test_gemm": (c_i32, [c_vp, c_i32, c_i32, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
                                c_d, c_d, c_i32]),
+    "cggm_test_gemm_f32": (c_i32, [c_vp, c_i32, c_i32, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
+                                   c_d, c_d, c_i32]),
     "cggm_test_set_tile": (c_i32, [c_vp, c_i32]),
     "cggm_test_fp64_peak": (c_i32, [c_vp, c_d, ctypes.POINTER(c_d), ctypes.POINTER(c_d)]),
     "cggm_objective": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64,

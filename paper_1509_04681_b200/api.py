@@ -25,17 +25,18 @@ class CggmError(RuntimeError):
 
 
 def colmajor_empty(rows: int, cols: int, device="cuda", dtype=torch.float64, zero=False) -> torch.Tensor:
-    """(rows, cols) column-major tensor with an even leading dimension (TMA-friendly)."""
-    ld = max(1, rows + (rows & 1))
+    """(rows, cols) column-major tensor with a leading dimension padded to 16 bytes (TMA-friendly)."""
+    m = 16 // torch.empty(0, dtype=dtype).element_size()
+    ld = max(m, (rows + m - 1) // m * m)
     f = torch.zeros if zero else torch.empty
     base = f((max(cols, 1), ld), device=device, dtype=dtype)
     return base.t()[:rows, :cols]
 
 
-def to_device_colmajor(a: np.ndarray, device="cuda") -> torch.Tensor:
+def to_device_colmajor(a: np.ndarray, device="cuda", dtype=torch.float64) -> torch.Tensor:
     a = np.asarray(a, dtype=np.float64)
-    t = colmajor_empty(a.shape[0], a.shape[1], device=device)
-    t.copy_(torch.from_numpy(np.asfortranarray(a)))
+    t = colmajor_empty(a.shape[0], a.shape[1], device=device, dtype=dtype)
+    t.copy_(torch.from_numpy(np.asfortranarray(a)).to(dtype))
     return t
 
 
@@ -61,11 +62,11 @@ class DeviceCsc:
     val: torch.Tensor     # float64
 
     @classmethod
-    def from_host(cls, csc, device="cuda") -> "DeviceCsc":
+    def from_host(cls, csc, device="cuda", dtype=torch.float64) -> "DeviceCsc":
         return cls(int(csc.nrows), int(csc.ncols),
                    torch.as_tensor(np.asarray(csc.colptr, dtype=np.int64), device=device),
                    torch.as_tensor(np.asarray(csc.rowidx, dtype=np.int32), device=device),
-                   torch.as_tensor(np.asarray(csc.val, dtype=np.float64), device=device))
+                   torch.as_tensor(np.asarray(csc.val, dtype=np.float64), device=device).to(dtype))
 
     @property
     def nnz(self) -> int:
@@ -83,6 +84,9 @@ class Context:
     def __init__(self, device: int = 0, dtype: str = "f64", validate: int = 1):
         self.lib = _abi.load()
         self.device = device
+        if dtype not in ("f64", "f32"):
+            raise ValueError("dtype must be 'f64' or 'f32'")
+        self.tdtype = torch.float64 if dtype == "f64" else torch.float32
         h = ctypes.c_void_p()
         stream = torch.cuda.current_stream(device).cuda_stream
         st = self.lib.cggm_ctx_create(ctypes.byref(h), device, _abi.CGGM_F64 if dtype == "f64" else _abi.CGGM_F32,
@@ -132,9 +136,9 @@ class Context:
         p = X.shape[1] if X is not None else 0
         n_total = n if n_total is None else n_total
         if want_syy and Syy is None:
-            Syy = colmajor_empty(q, q, device=Y.device)
+            Syy = colmajor_empty(q, q, device=Y.device, dtype=self.tdtype)
         if want_sxy and Sxy is None:
-            Sxy = colmajor_empty(p, q, device=Y.device)
+            Sxy = colmajor_empty(p, q, device=Y.device, dtype=self.tdtype)
         self._check(self.lib.cggm_covariances(
             self.h, n, n_total, p, q, _ptr(X), ld_of(X) if X is not None else 1, _ptr(Y), ld_of(Y),
             _ptr(Syy) if want_syy else None, ld_of(Syy) if want_syy else 1,
@@ -146,7 +150,7 @@ class Context:
         self._sync_stream()
         q = Lam.nrows
         if want_sigma and Sigma is None:
-            Sigma = colmajor_empty(q, q, device=Lam.colptr.device)
+            Sigma = colmajor_empty(q, q, device=Lam.colptr.device, dtype=self.tdtype)
         ld, pd, fc = ctypes.c_double(), ctypes.c_int32(), ctypes.c_int64()
         cs = Lam.c_struct()
         self._check(self.lib.cggm_invert_logdet(self.h, ctypes.byref(cs), _ptr(Sigma) if want_sigma else None,
@@ -166,13 +170,13 @@ class Context:
         dev = X.device
         Psi = out.get("Psi")
         if Psi is None:
-            Psi = colmajor_empty(q, q, device=dev)
+            Psi = colmajor_empty(q, q, device=dev, dtype=self.tdtype)
         GradL = out.get("GradL") if want_gradL else None
         if want_gradL and GradL is None:
-            GradL = colmajor_empty(q, q, device=dev)
+            GradL = colmajor_empty(q, q, device=dev, dtype=self.tdtype)
         GradT = out.get("GradT") if want_gradT else None
         if want_gradT and GradT is None:
-            GradT = colmajor_empty(p, q, device=dev)
+            GradT = colmajor_empty(p, q, device=dev, dtype=self.tdtype)
         ts = Theta.c_struct()
         ls = Lam.c_struct() if Lam is not None else None
         ao = None
@@ -194,7 +198,7 @@ class Context:
         self._sync_stream()
         q = Syy.shape[0]
         if GradL is None:
-            GradL = colmajor_empty(q, q, device=Syy.device)
+            GradL = colmajor_empty(q, q, device=Syy.device, dtype=self.tdtype)
         self._check(self.lib.cggm_grad_lambda(self.h, q, _ptr(Syy), ld_of(Syy), _ptr(Sigma), ld_of(Sigma),
                                               _ptr(Psi), ld_of(Psi), _ptr(GradL), ld_of(GradL)))
         return GradL
@@ -279,7 +283,7 @@ class Context:
         bufs = bufs if bufs is not None else {}
         for k, shape in (("Sigma", (q, q)), ("Psi", (q, q)), ("GradL", (q, q)), ("GradT", (p, q))):
             if bufs.get(k) is None:
-                bufs[k] = colmajor_empty(*shape, device=dev)
+                bufs[k] = colmajor_empty(*shape, device=dev, dtype=self.tdtype)
         spec = dict(lam_L=lam_L, lam_T=lam_T, penalize_diag=int(bool(penalize_diag)), tie_eps=tie_eps,
                     L_row=bufs.get("L_row"), L_col=bufs.get("L_col"), T_row=bufs.get("T_row"), T_col=bufs.get("T_col"))
         ao = self._active_struct(spec)

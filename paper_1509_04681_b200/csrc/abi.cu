@@ -85,7 +85,8 @@ void validate_csc_dev(Ctx* c, const cggm_csc* A, bool symmetric, const char* nam
   if (c->validate < 1 || A->ncols == 0) return;
   Scal s = scal(c, 0);
   init_scalars(c, s.fail, s.flag);
-  check_csc(c, A, symmetric, s.flag);
+  if (c->dtype == CGGM_F64) check_csc<double>(c, A, symmetric, s.flag);
+  else check_csc<float>(c, A, symmetric, s.flag);
   int* h = static_cast<int*>(c->host_scratch);
   CGGM_CUDA_CHECK(cudaMemcpyAsync(h, s.flag, 4, cudaMemcpyDeviceToHost, c->stream));
   CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
@@ -94,6 +95,20 @@ void validate_csc_dev(Ctx* c, const cggm_csc* A, bool symmetric, const char* nam
 }
 
 inline int64_t even(int64_t x) { return x + (x & 1); }
+
+// leading dimension padded to a 16-byte multiple (TMA global strides)
+template <typename T>
+inline int64_t pad_ld(int64_t x) {
+  constexpr int64_t m = 16 / sizeof(T);
+  return (x + m - 1) / m * m;
+}
+
+// run f(T{}) with T the ctx element type (CGGM_F64 -> double, CGGM_F32 -> float)
+template <class F>
+void dispatch(Ctx* c, F&& f) {
+  if (c->dtype == CGGM_F64) f(double{});
+  else f(float{});
+}
 
 template <class F>
 cggm_status guard(cggm_ctx* ctx, F f) {
@@ -244,12 +259,13 @@ const char* cggm_profile_tag_name(int32_t tag) {
 
 const char* cggm_last_error(cggm_ctx* ctx) { return ctx ? ctx->impl.last_error.c_str() : "null ctx"; }
 
+}  // extern "C"  (the definitions below keep the C linkage declared in cggm.h)
+
 // ------------------------------------------------------------------ a1
 cggm_status cggm_covariances(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64_t p, int64_t q, const void* X,
                              int64_t ldx, const void* Y, int64_t ldy, void* Syy, int64_t ldsyy, void* Sxy,
                              int64_t ldsxy) {
   return guard(ctx, [&](Ctx* c) {
-    check_ctx_dtype(c);
     if (n_local < 0 || p < 0 || q < 0) fail(CGGM_ERR_INVALID_ARG, "negative dimension");
     if (n_total < 1 || n_total < n_local) fail(CGGM_ERR_INVALID_ARG, "n_total must be >= max(1, n_local)");
     check_dense("Y", Y, n_local, q, ldy);
@@ -260,15 +276,18 @@ cggm_status cggm_covariances(cggm_ctx* ctx, int64_t n_local, int64_t n_total, in
     }
     const double inv_n = 1.0 / (double)n_total;
     Phase ph(c, TAG_COV);
-    if (Syy) {
-      Epilogue e; e.out1 = static_cast<double*>(Syy); e.ld1 = ldsyy; e.a1 = inv_n;
-      gemm(c, true, false, q, q, n_local, static_cast<const double*>(Y), ldy, static_cast<const double*>(Y), ldy, e,
-           SYM_LOWER | SYM_MIRROR);
-    }
-    if (Sxy) {
-      Epilogue e; e.out1 = static_cast<double*>(Sxy); e.ld1 = ldsxy; e.a1 = inv_n;
-      gemm(c, true, false, p, q, n_local, static_cast<const double*>(X), ldx, static_cast<const double*>(Y), ldy, e, 0);
-    }
+    dispatch(c, [&](auto tag) {
+      using T = decltype(tag);
+      if (Syy) {
+        EpilogueT<T> e; e.out1 = static_cast<T*>(Syy); e.ld1 = ldsyy; e.a1 = inv_n;
+        gemm(c, true, false, q, q, n_local, static_cast<const T*>(Y), ldy, static_cast<const T*>(Y), ldy, e,
+             SYM_LOWER | SYM_MIRROR);
+      }
+      if (Sxy) {
+        EpilogueT<T> e; e.out1 = static_cast<T*>(Sxy); e.ld1 = ldsxy; e.a1 = inv_n;
+        gemm(c, true, false, p, q, n_local, static_cast<const T*>(X), ldx, static_cast<const T*>(Y), ldy, e, 0);
+      }
+    });
   });
 }
 
@@ -291,28 +310,29 @@ static int64_t n_leaves(int64_t q) { return (q + leaf_nb() - 1) / leaf_nb(); }
 
 // ------------------------------------------------------------------ a3
 // Scal layout: dbl[0] = logdet sum, dbl[8..] leaf slots
-static void invert_enqueue(Ctx* c, int lane, const cggm_csc* Lambda, double* Sigma, int64_t ldsigma) {
+template <typename T>
+static void invert_enqueue(Ctx* c, int lane, const cggm_csc* Lambda, T* Sigma, int64_t ldsigma) {
   const int64_t q = Lambda->nrows;
-  const int64_t lda = even(q);
+  const int64_t lda = pad_ld<T>(q);
   const int nb = leaf_nb();
   const int64_t nleaves = n_leaves(q);
-  double* A = static_cast<double*>(ws_get(c, kLane[lane].dense, (size_t)lda * q * 8));
+  T* A = static_cast<T*>(ws_get(c, kLane[lane].dense, (size_t)lda * q * sizeof(T)));
   Scal s = scal_lane(c, lane, 8 + nleaves);
   double* slots = s.dbl + 8;
-  View Av{A, lda, q, q};
+  ViewT<T> Av{A, lda, q, q};
   densify_csc(c, Lambda, Av);
   init_scalars(c, s.fail, s.flag);
   if (Sigma) {
-    double* X = static_cast<double*>(ws_get(c, WS_LINV, (size_t)lda * q * 8));
-    CGGM_CUDA_CHECK(cudaMemsetAsync(X, 0, (size_t)lda * q * 8, c->stream));
-    const int64_t n1 = q / 2 + 128, n2 = q / 2 + 130;
+    T* X = static_cast<T*>(ws_get(c, WS_LINV, (size_t)lda * q * sizeof(T)));
+    CGGM_CUDA_CHECK(cudaMemsetAsync(X, 0, (size_t)lda * q * sizeof(T), c->stream));
+    const int64_t n1 = q / 2 + 128, n2 = q / 2 + 132;
     const size_t tmp_elems = (size_t)n1 * n2;
-    double* tmp = static_cast<double*>(ws_get(c, WS_TMP, tmp_elems * 8));
-    potrf_recursive(c, Av, View{X, lda, q, q}, true, nullptr, slots, s.fail, tmp, tmp_elems);
-    lauum(c, View{X, lda, q, q}, View{Sigma, ldsigma, q, q});
+    T* tmp = static_cast<T*>(ws_get(c, WS_TMP, tmp_elems * sizeof(T)));
+    potrf_recursive<T>(c, Av, ViewT<T>{X, lda, q, q}, true, nullptr, slots, s.fail, tmp, tmp_elems);
+    lauum<T>(c, ViewT<T>{X, lda, q, q}, ViewT<T>{Sigma, ldsigma, q, q});
   } else {
-    double* leafinv = static_cast<double*>(ws_get(c, WS_LEAFINV, (size_t)nleaves * nb * nb * 8));
-    potrf_recursive(c, Av, View{nullptr, lda, q, q}, false, leafinv, slots, s.fail, nullptr, 0);
+    T* leafinv = static_cast<T*>(ws_get(c, WS_LEAFINV, (size_t)nleaves * nb * nb * sizeof(T)));
+    potrf_recursive<T>(c, Av, ViewT<T>{nullptr, lda, q, q}, false, leafinv, slots, s.fail, nullptr, 0);
   }
   sum_arrays_1(c, slots, nleaves, s.dbl);
 }
@@ -339,7 +359,6 @@ static CholResult chol_decode(const char* h) {
 cggm_status cggm_invert_logdet(cggm_ctx* ctx, const cggm_csc* Lambda, void* Sigma, int64_t ldsigma, double* logdet,
                                int32_t* is_pd, int64_t* fail_col) {
   return guard(ctx, [&](Ctx* c) {
-    check_ctx_dtype(c);
     if (!Lambda) fail(CGGM_ERR_INVALID_ARG, "Lambda is null");
     const int64_t q = Lambda->nrows;
     check_csc_host("Lambda", Lambda, q, q);
@@ -350,7 +369,10 @@ cggm_status cggm_invert_logdet(cggm_ctx* ctx, const cggm_csc* Lambda, void* Sigm
       return;
     }
     validate_csc_dev(c, Lambda, true, "Lambda");
-    invert_enqueue(c, 0, Lambda, static_cast<double*>(Sigma), ldsigma);
+    dispatch(c, [&](auto tag) {
+      using T = decltype(tag);
+      invert_enqueue<T>(c, 0, Lambda, static_cast<T*>(Sigma), ldsigma);
+    });
     char* h = static_cast<char*>(c->host_scratch);
     chol_readback_async(c, 0, h);
     CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
@@ -362,15 +384,15 @@ cggm_status cggm_invert_logdet(cggm_ctx* ctx, const cggm_csc* Lambda, void* Sigm
 }
 
 // ------------------------------------------------------------------ a6
-static ActTotals* active_enqueue(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t ldgl, const double* GradT,
+template <typename T>
+static ActTotals* active_enqueue(Ctx* c, int64_t p, int64_t q, const T* GradL, int64_t ldgl, const T* GradT,
                                  int64_t ldgt, const cggm_csc* Lambda, const cggm_csc* Theta,
                                  const cggm_active_out* o) {
   ActWs ws = active_ws(c, q);
   Phase ph(c, TAG_ACTIVE);
-  active_compact(c, p, q, GradL, ldgl, GradT, ldgt, Lambda, Theta, o->lam_L, o->lam_T, o->penalize_diag, o->tie_eps, ws,
+  active_compact<T>(c, p, q, GradL, ldgl, GradT, ldgt, Lambda, Theta, o->lam_L, o->lam_T, o->penalize_diag, o->tie_eps, ws,
                  o->L_row, o->L_col, o->T_row, o->T_col, o->cap_L, o->cap_T);
-  ActTotals* T = ws.tot;
-  return T;
+  return ws.tot;
 }
 
 static void active_decode(const ActTotals& h, cggm_active_out* o) {
@@ -404,7 +426,6 @@ static void active_sync(Ctx* c, ActTotals* T, cggm_active_out* o) {
 cggm_status cggm_active_set(cggm_ctx* ctx, int64_t p, int64_t q, const void* GradL, int64_t ldgl, const void* GradT,
                             int64_t ldgt, const cggm_csc* Lambda, const cggm_csc* Theta, cggm_active_out* out) {
   return guard(ctx, [&](Ctx* c) {
-    check_ctx_dtype(c);
     if (p < 0 || q < 0) fail(CGGM_ERR_INVALID_ARG, "negative dimension");
     check_active_args(out);
     check_dense("GradL", GradL, q, q, ldgl);
@@ -416,30 +437,35 @@ cggm_status cggm_active_set(cggm_ctx* ctx, int64_t p, int64_t q, const void* Gra
     if (q == 0) return;
     validate_csc_dev(c, Lambda, true, "Lambda");
     validate_csc_dev(c, Theta, false, "Theta");
-    ActTotals* T = active_enqueue(c, p, q, static_cast<const double*>(GradL), ldgl, static_cast<const double*>(GradT),
-                                  ldgt, Lambda, Theta, out);
-    active_sync(c, T, out);
+    ActTotals* tot = nullptr;
+    dispatch(c, [&](auto tag) {
+      using T = decltype(tag);
+      tot = active_enqueue<T>(c, p, q, static_cast<const T*>(GradL), ldgl, static_cast<const T*>(GradT), ldgt, Lambda,
+                              Theta, out);
+    });
+    active_sync(c, tot, out);
   });
 }
 
 // ------------------------------------------------------------------ a2/a4/a5
 // W (n_local x q, ldw) must already hold X Theta.
-static void psi_enqueue(Ctx* c, int64_t n_local, int64_t n_total, int64_t p, int64_t q, const double* Xd, int64_t ldx,
-                        const double* Yd, int64_t ldy, const double* W, int64_t ldw, const double* Sg, int64_t ldsigma,
-                        const double* Syy, int64_t ldsyy, const double* Sxy, int64_t ldsxy, double* Psi, int64_t ldpsi,
-                        double* GradL, int64_t ldgl, double* GradT, int64_t ldgt) {
-  const int64_t ldn = even(n_local > 0 ? n_local : 1);
-  double* R = static_cast<double*>(ws_get(c, WS_R, (size_t)ldn * q * 8));
-  double* E = static_cast<double*>(ws_get(c, WS_E, (size_t)ldn * q * 8));
+template <typename T>
+static void psi_enqueue(Ctx* c, int64_t n_local, int64_t n_total, int64_t p, int64_t q, const T* Xd, int64_t ldx,
+                        const T* Yd, int64_t ldy, const T* W, int64_t ldw, const T* Sg, int64_t ldsigma, const T* Syy,
+                        int64_t ldsyy, const T* Sxy, int64_t ldsxy, T* Psi, int64_t ldpsi, T* GradL, int64_t ldgl,
+                        T* GradT, int64_t ldgt) {
+  const int64_t ldn = pad_ld<T>(n_local > 0 ? n_local : 1);
+  T* R = static_cast<T*>(ws_get(c, WS_R, (size_t)ldn * q * sizeof(T)));
+  T* E = static_cast<T*>(ws_get(c, WS_E, (size_t)ldn * q * sizeof(T)));
   {  // a4: acc = W Sigma -> R = acc / sqrt(n), E = Y + acc
     Phase ph(c, TAG_WSIGMA);
-    Epilogue e; e.out1 = R; e.ld1 = ldn; e.a1 = 1.0 / std::sqrt((double)n_total);
+    EpilogueT<T> e; e.out1 = R; e.ld1 = ldn; e.a1 = 1.0 / std::sqrt((double)n_total);
     if (GradT && !Sxy) { e.out2 = E; e.ld2 = ldn; e.a2 = 1.0; e.in2a = Yd; e.ld2a = ldy; e.b2 = 1.0; }
     gemm(c, false, false, n_local, q, q, W, ldw, Sg, ldsigma, e, 0);
   }
   {  // a4/a5: Psi = R^T R (mirrored), then grad_Lambda = (S_yy - Sigma) - Psi as one streaming pass
     Phase ph(c, TAG_PSI);
-    Epilogue e; e.out1 = Psi; e.ld1 = ldpsi; e.a1 = 1.0;
+    EpilogueT<T> e; e.out1 = Psi; e.ld1 = ldpsi; e.a1 = 1.0;
     gemm(c, true, false, q, q, n_local, R, ldn, R, ldn, e, SYM_LOWER | SYM_MIRROR);
     if (GradL) {
       Phase pg(c, TAG_GRADL);
@@ -448,7 +474,7 @@ static void psi_enqueue(Ctx* c, int64_t n_local, int64_t n_total, int64_t p, int
   }
   if (GradT) {  // a5: GradT = (2/n) X^T E   (or 2 S_xy + (2/sqrt n) X^T R)
     Phase ph(c, TAG_GRADT);
-    Epilogue e; e.out1 = GradT; e.ld1 = ldgt;
+    EpilogueT<T> e; e.out1 = GradT; e.ld1 = ldgt;
     if (!Sxy) {
       e.a1 = 2.0 / (double)n_total;
       gemm(c, true, false, p, q, n_local, Xd, ldx, E, ldn, e, 0);
@@ -466,7 +492,6 @@ cggm_status cggm_psi_grad(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64
                           int64_t ldpsi, void* GradL, int64_t ldgl, void* GradT, int64_t ldgt, const cggm_csc* Lambda,
                           cggm_active_out* fused) {
   return guard(ctx, [&](Ctx* c) {
-    check_ctx_dtype(c);
     if (n_local < 0 || p < 0 || q < 0) fail(CGGM_ERR_INVALID_ARG, "negative dimension");
     if (n_total < 1 || n_total < n_local) fail(CGGM_ERR_INVALID_ARG, "n_total must be >= max(1, n_local)");
     check_dense("X", X, n_local, p, ldx);
@@ -490,32 +515,37 @@ cggm_status cggm_psi_grad(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64
     if (q == 0) return;
     validate_csc_dev(c, Theta, false, "Theta");
     if (fused) validate_csc_dev(c, Lambda, true, "Lambda");
-    const int64_t ldn = even(n_local > 0 ? n_local : 1);
-    double* W = static_cast<double*>(ws_get(c, WS_W, (size_t)ldn * q * 8));
-    spmm_x_theta(c, static_cast<const double*>(X), ldx, n_local, Theta, View{W, ldn, n_local, q});
-    psi_enqueue(c, n_local, n_total, p, q, static_cast<const double*>(X), ldx, static_cast<const double*>(Y), ldy, W,
-                ldn, static_cast<const double*>(Sigma), ldsigma, static_cast<const double*>(Syy), ldsyy,
-                static_cast<const double*>(Sxy), ldsxy, static_cast<double*>(Psi), ldpsi,
-                static_cast<double*>(GradL), ldgl, static_cast<double*>(GradT), ldgt);
-    if (fused) {
-      ActTotals* T = active_enqueue(c, p, q, static_cast<const double*>(GradL), ldgl,
-                                    static_cast<const double*>(GradT), ldgt, Lambda, Theta, fused);
-      active_sync(c, T, fused);
-    }
+    ActTotals* tot = nullptr;
+    dispatch(c, [&](auto tag) {
+      using T = decltype(tag);
+      const int64_t ldn = pad_ld<T>(n_local > 0 ? n_local : 1);
+      T* W = static_cast<T*>(ws_get(c, WS_W, (size_t)ldn * q * sizeof(T)));
+      spmm_x_theta<T>(c, static_cast<const T*>(X), ldx, n_local, Theta, ViewT<T>{W, ldn, n_local, q});
+      psi_enqueue<T>(c, n_local, n_total, p, q, static_cast<const T*>(X), ldx, static_cast<const T*>(Y), ldy, W, ldn,
+                     static_cast<const T*>(Sigma), ldsigma, static_cast<const T*>(Syy), ldsyy,
+                     static_cast<const T*>(Sxy), ldsxy, static_cast<T*>(Psi), ldpsi, static_cast<T*>(GradL), ldgl,
+                     static_cast<T*>(GradT), ldgt);
+      if (fused)
+        tot = active_enqueue<T>(c, p, q, static_cast<const T*>(GradL), ldgl, static_cast<const T*>(GradT), ldgt,
+                                Lambda, Theta, fused);
+    });
+    if (fused) active_sync(c, tot, fused);
   });
 }
 
 cggm_status cggm_grad_lambda(cggm_ctx* ctx, int64_t q, const void* Syy, int64_t ldsyy, const void* Sigma,
                              int64_t ldsigma, const void* Psi, int64_t ldpsi, void* GradL, int64_t ldgl) {
   return guard(ctx, [&](Ctx* c) {
-    check_ctx_dtype(c);
     if (q < 0) fail(CGGM_ERR_INVALID_ARG, "negative dimension");
     check_dense("Syy", Syy, q, q, ldsyy);
     check_dense("Sigma", Sigma, q, q, ldsigma);
     check_dense("Psi", Psi, q, q, ldpsi);
     check_dense("GradL", GradL, q, q, ldgl);
-    grad_lambda(c, q, static_cast<const double*>(Syy), ldsyy, static_cast<const double*>(Sigma), ldsigma,
-                static_cast<const double*>(Psi), ldpsi, static_cast<double*>(GradL), ldgl);
+    dispatch(c, [&](auto tag) {
+      using T = decltype(tag);
+      grad_lambda<T>(c, q, static_cast<const T*>(Syy), ldsyy, static_cast<const T*>(Sigma), ldsigma,
+                     static_cast<const T*>(Psi), ldpsi, static_cast<T*>(GradL), ldgl);
+    });
   });
 }
 
@@ -524,14 +554,15 @@ cggm_status cggm_grad_lambda(cggm_ctx* ctx, int64_t q, const void* Syy, int64_t 
 // leaves Z = W L^{-T} in the bottom rows, ||Z||_F^2 = tr(Lambda^{-1} W^T W) (reading A14).
 // Scal layout: dbl[0] logdet sum, dbl[1..5] sums (<Y,Y Lambda>, <W,Y>, ||Z||^2, |Lambda|, |Theta|),
 // dbl[16..] per-column partials, then leaf slots.
-static void objective_enqueue(Ctx* c, int lane, int64_t n_local, int64_t q, const double* Yd, int64_t ldy,
-                              const double* Wd, int64_t ldwd, const cggm_csc* Lambda, const cggm_csc* Theta,
+template <typename T>
+static void objective_enqueue(Ctx* c, int lane, int64_t n_local, int64_t q, const T* Yd, int64_t ldy, const T* Wd,
+                              int64_t ldwd, const cggm_csc* Lambda, const cggm_csc* Theta,
                               int32_t penalize_diag) {
   const int nb = leaf_nb();
   const int64_t nleaves = n_leaves(q);
-  const int64_t ldaug = even(q + n_local);
-  double* A = static_cast<double*>(ws_get(c, kLane[lane].dense, (size_t)ldaug * q * 8));
-  double* leafinv = static_cast<double*>(ws_get(c, WS_LEAFINV, (size_t)nleaves * nb * nb * 8));
+  const int64_t ldaug = pad_ld<T>(q + n_local);
+  T* A = static_cast<T*>(ws_get(c, kLane[lane].dense, (size_t)ldaug * q * sizeof(T)));
+  T* leafinv = static_cast<T*>(ws_get(c, WS_LEAFINV, (size_t)nleaves * nb * nb * sizeof(T)));
   Scal s = scal_lane(c, lane, 16 + 5 * q + nleaves);
   double* res = s.dbl;
   double* partY = s.dbl + 16;
@@ -542,23 +573,23 @@ static void objective_enqueue(Ctx* c, int lane, int64_t n_local, int64_t q, cons
   double* slots = penTp + q;
   // inverses of the <= BINV diagonal blocks + temporaries (full-inverse subtrees, block products)
   const int64_t binv = block_inverse_size();
-  const int64_t ldxd = even(q);
-  const size_t tmp_elems = (size_t)(binv + 2) * (binv + 2);
-  const size_t tmp2_elems = (size_t)even(q + n_local) * binv;
-  double* xdiag = static_cast<double*>(ws_get(c, WS_XDIAG, (size_t)ldxd * binv * 8));
-  double* tmpo = static_cast<double*>(ws_get(c, WS_TMP_OBJ, (tmp_elems + tmp2_elems) * 8));
-  CGGM_CUDA_CHECK(cudaMemsetAsync(xdiag, 0, (size_t)ldxd * binv * 8, c->stream));
-  densify_csc(c, Lambda, View{A, ldaug, q, q});
-  copy2d(c, View{A + q, ldaug, n_local, q}, Wd, ldwd);
+  const int64_t ldxd = pad_ld<T>(q);
+  const size_t tmp_elems = (size_t)(binv + 4) * (binv + 4);
+  const size_t tmp2_elems = (size_t)pad_ld<T>(q + n_local) * binv;
+  T* xdiag = static_cast<T*>(ws_get(c, WS_XDIAG, (size_t)ldxd * binv * sizeof(T)));
+  T* tmpo = static_cast<T*>(ws_get(c, WS_TMP_OBJ, (tmp_elems + tmp2_elems) * sizeof(T)));
+  CGGM_CUDA_CHECK(cudaMemsetAsync(xdiag, 0, (size_t)ldxd * binv * sizeof(T), c->stream));
+  densify_csc(c, Lambda, ViewT<T>{A, ldaug, q, q});
+  copy2d(c, ViewT<T>{A + q, ldaug, n_local, q}, Wd, ldwd);
   init_scalars(c, s.fail, s.flag);
-  potrf_recursive(c, View{A, ldaug, q + n_local, q}, View{nullptr, ldaug, q, q}, false, leafinv, slots, s.fail,
+  potrf_recursive<T>(c, ViewT<T>{A, ldaug, q + n_local, q}, ViewT<T>{nullptr, ldaug, q, q}, false, leafinv, slots, s.fail,
                   tmpo, tmp_elems, xdiag, ldxd, tmpo + tmp_elems, tmp2_elems);
   Phase ph(c, TAG_OBJRED);
-  col_partials(c, 0, n_local, q, Yd, ldy, nullptr, 0, Lambda, partY);
-  col_partials(c, 1, n_local, q, Wd, ldwd, Yd, ldy, nullptr, partWY);
-  col_partials(c, 2, n_local, q, A + q, ldaug, nullptr, 0, nullptr, partZ);
-  csc_abs_partials(c, Lambda, penalize_diag == 0, penLp);
-  csc_abs_partials(c, Theta, false, penTp);
+  col_partials<T>(c, 0, n_local, q, Yd, ldy, nullptr, 0, Lambda, partY);
+  col_partials<T>(c, 1, n_local, q, Wd, ldwd, Yd, ldy, nullptr, partWY);
+  col_partials<T>(c, 2, n_local, q, A + q, ldaug, nullptr, 0, nullptr, partZ);
+  csc_abs_partials<T>(c, Lambda, penalize_diag == 0, penLp);
+  csc_abs_partials<T>(c, Theta, false, penTp);
   sum_arrays_1(c, slots, nleaves, res + 0);
   sum_arrays_1(c, partY, q, res + 1);
   sum_arrays_1(c, partWY, q, res + 2);
@@ -603,7 +634,6 @@ cggm_status cggm_objective(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int6
                            double lam_L, double lam_T, int32_t penalize_diag, const void* W, int64_t ldw,
                            cggm_objective_out* out) {
   return guard(ctx, [&](Ctx* c) {
-    check_ctx_dtype(c);
     if (!out) fail(CGGM_ERR_INVALID_ARG, "null cggm_objective_out");
     if (n_local < 0 || p < 0 || q < 0) fail(CGGM_ERR_INVALID_ARG, "negative dimension");
     if (n_total < 1 || n_total < n_local) fail(CGGM_ERR_INVALID_ARG, "n_total must be >= max(1, n_local)");
@@ -620,19 +650,22 @@ cggm_status cggm_objective(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int6
     }
     validate_csc_dev(c, Lambda, true, "Lambda");
     validate_csc_dev(c, Theta, false, "Theta");
-    const int64_t ldn = even(n_local > 0 ? n_local : 1);
-    const double* Wd;
-    int64_t ldwd;
-    if (W) {
-      Wd = static_cast<const double*>(W);
-      ldwd = ldw;
-    } else {
-      double* Wb = static_cast<double*>(ws_get(c, WS_W, (size_t)ldn * q * 8));
-      spmm_x_theta(c, static_cast<const double*>(X), ldx, n_local, Theta, View{Wb, ldn, n_local, q});
-      Wd = Wb;
-      ldwd = ldn;
-    }
-    objective_enqueue(c, 0, n_local, q, static_cast<const double*>(Y), ldy, Wd, ldwd, Lambda, Theta, penalize_diag);
+    dispatch(c, [&](auto tag) {
+      using T = decltype(tag);
+      const int64_t ldn = pad_ld<T>(n_local > 0 ? n_local : 1);
+      const T* Wd;
+      int64_t ldwd;
+      if (W) {
+        Wd = static_cast<const T*>(W);
+        ldwd = ldw;
+      } else {
+        T* Wb = static_cast<T*>(ws_get(c, WS_W, (size_t)ldn * q * sizeof(T)));
+        spmm_x_theta<T>(c, static_cast<const T*>(X), ldx, n_local, Theta, ViewT<T>{Wb, ldn, n_local, q});
+        Wd = Wb;
+        ldwd = ldn;
+      }
+      objective_enqueue<T>(c, 0, n_local, q, static_cast<const T*>(Y), ldy, Wd, ldwd, Lambda, Theta, penalize_diag);
+    });
     char* h = static_cast<char*>(c->host_scratch);
     objective_readback_async(c, 0, h);
     CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
@@ -650,7 +683,6 @@ cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, con
                              void* GradL, int64_t ldgl, void* GradT, int64_t ldgt, cggm_active_out* active,
                              cggm_eval_out* out) {
   return guard(ctx, [&](Ctx* c) {
-    check_ctx_dtype(c);
     if (!out) fail(CGGM_ERR_INVALID_ARG, "null cggm_eval_out");
     if (n < 1 || p < 0 || q < 1) fail(CGGM_ERR_INVALID_ARG, "need n >= 1, q >= 1, p >= 0");
     check_dense("X", X, n, p, ldx);
@@ -666,60 +698,65 @@ cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, con
     std::memset(out, 0, sizeof(*out));
     validate_csc_dev(c, Lambda, true, "Lambda");
     validate_csc_dev(c, Theta, false, "Theta");
-    const int64_t ldn = even(n);
-    // allocate every workspace slot up front (allocation may synchronise the device)
-    const int64_t nleaves = n_leaves(q);
-    ws_get(c, WS_DENSE_A, (size_t)even(q) * q * 8);
-    ws_get(c, WS_DENSE_B, (size_t)even(q + n) * q * 8);
-    ws_get(c, WS_LINV, (size_t)even(q) * q * 8);
-    ws_get(c, WS_TMP, (size_t)(q / 2 + 128) * (q / 2 + 130) * 8);
-    ws_get(c, WS_LEAFINV, (size_t)nleaves * leaf_nb() * leaf_nb() * 8);
-    ws_get(c, WS_XDIAG, (size_t)even(q) * block_inverse_size() * 8);
-    ws_get(c, WS_TMP_OBJ, ((size_t)(block_inverse_size() + 2) * (block_inverse_size() + 2) +
-                           (size_t)even(q + n) * block_inverse_size()) * 8);
-    ws_get(c, WS_SCAL, 64 + (8 + nleaves) * 8);
-    ws_get(c, WS_SCAL2, 64 + (16 + 5 * q + nleaves) * 8);
-    active_ws(c, q);
-    ws_get(c, WS_R, (size_t)ldn * q * 8);
-    ws_get(c, WS_E, (size_t)ldn * q * 8);
-    double* W = static_cast<double*>(ws_get(c, WS_W, (size_t)ldn * q * 8));
     if (!c->aux) {
       CGGM_CUDA_CHECK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
       CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
       CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     }
     cudaStream_t s0 = c->stream;
-    const double* Xd = static_cast<const double*>(X);
-    const double* Yd = static_cast<const double*>(Y);
-    // a2 on the caller's stream, then fork
-    spmm_x_theta(c, Xd, ldx, n, Theta, View{W, ldn, n, q});
-    CGGM_CUDA_CHECK(cudaEventRecord(c->ev_fork, s0));
-    CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
-    try {
-      // a7 on the auxiliary stream (lane 1)
-      c->stream = c->aux;
-      c->lane = 1;
-      objective_enqueue(c, 1, n, q, Yd, ldy, W, ldn, Lambda, Theta, active->penalize_diag);
-      CGGM_CUDA_CHECK(cudaEventRecord(c->ev_join, c->aux));
-      c->stream = s0;
-      c->lane = 0;
-    } catch (...) {
-      c->stream = s0;
-      c->lane = 0;
-      throw;
-    }
-    // a3, a4/a5, a6 on the caller's stream (lane 0)
-    invert_enqueue(c, 0, Lambda, static_cast<double*>(Sigma), ldsigma);
-    psi_enqueue(c, n, n, p, q, Xd, ldx, Yd, ldy, W, ldn, static_cast<const double*>(Sigma), ldsigma,
-                static_cast<const double*>(Syy), ldsyy, nullptr, 0, static_cast<double*>(Psi), ldpsi,
-                static_cast<double*>(GradL), ldgl, static_cast<double*>(GradT), ldgt);
-    ActTotals* T = active_enqueue(c, p, q, static_cast<const double*>(GradL), ldgl, static_cast<const double*>(GradT),
-                                  ldgt, Lambda, Theta, active);
+    ActTotals* tot = nullptr;
+    dispatch(c, [&](auto tag) {
+      using T = decltype(tag);
+      const size_t es = sizeof(T);
+      const int64_t ldn = pad_ld<T>(n);
+      // allocate every workspace slot up front (allocation may synchronise the device)
+      const int64_t nleaves = n_leaves(q);
+      ws_get(c, WS_DENSE_A, (size_t)pad_ld<T>(q) * q * es);
+      ws_get(c, WS_DENSE_B, (size_t)pad_ld<T>(q + n) * q * es);
+      ws_get(c, WS_LINV, (size_t)pad_ld<T>(q) * q * es);
+      ws_get(c, WS_TMP, (size_t)(q / 2 + 128) * (q / 2 + 132) * es);
+      ws_get(c, WS_LEAFINV, (size_t)nleaves * leaf_nb() * leaf_nb() * es);
+      ws_get(c, WS_XDIAG, (size_t)pad_ld<T>(q) * block_inverse_size() * es);
+      ws_get(c, WS_TMP_OBJ, ((size_t)(block_inverse_size() + 4) * (block_inverse_size() + 4) +
+                             (size_t)pad_ld<T>(q + n) * block_inverse_size()) * es);
+      ws_get(c, WS_SCAL, 64 + (8 + nleaves) * 8);
+      ws_get(c, WS_SCAL2, 64 + (16 + 5 * q + nleaves) * 8);
+      active_ws(c, q);
+      ws_get(c, WS_R, (size_t)ldn * q * es);
+      ws_get(c, WS_E, (size_t)ldn * q * es);
+      T* W = static_cast<T*>(ws_get(c, WS_W, (size_t)ldn * q * es));
+      const T* Xd = static_cast<const T*>(X);
+      const T* Yd = static_cast<const T*>(Y);
+      // a2 on the caller's stream, then fork
+      spmm_x_theta<T>(c, Xd, ldx, n, Theta, ViewT<T>{W, ldn, n, q});
+      CGGM_CUDA_CHECK(cudaEventRecord(c->ev_fork, s0));
+      CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
+      try {
+        // a7 on the auxiliary stream (lane 1)
+        c->stream = c->aux;
+        c->lane = 1;
+        objective_enqueue<T>(c, 1, n, q, Yd, ldy, W, ldn, Lambda, Theta, active->penalize_diag);
+        CGGM_CUDA_CHECK(cudaEventRecord(c->ev_join, c->aux));
+        c->stream = s0;
+        c->lane = 0;
+      } catch (...) {
+        c->stream = s0;
+        c->lane = 0;
+        throw;
+      }
+      // a3, a4/a5, a6 on the caller's stream (lane 0)
+      invert_enqueue<T>(c, 0, Lambda, static_cast<T*>(Sigma), ldsigma);
+      psi_enqueue<T>(c, n, n, p, q, Xd, ldx, Yd, ldy, W, ldn, static_cast<const T*>(Sigma), ldsigma,
+                     static_cast<const T*>(Syy), ldsyy, nullptr, 0, static_cast<T*>(Psi), ldpsi,
+                     static_cast<T*>(GradL), ldgl, static_cast<T*>(GradT), ldgt);
+      tot = active_enqueue<T>(c, p, q, static_cast<const T*>(GradL), ldgl, static_cast<const T*>(GradT), ldgt, Lambda,
+                              Theta, active);
+    });
     CGGM_CUDA_CHECK(cudaStreamWaitEvent(s0, c->ev_join, 0));
     char* h = static_cast<char*>(c->host_scratch);
     chol_readback_async(c, 0, h);
     objective_readback_async(c, 1, h + 64);
-    CGGM_CUDA_CHECK(cudaMemcpyAsync(h + 256, T, sizeof(ActTotals), cudaMemcpyDeviceToHost, s0));
+    CGGM_CUDA_CHECK(cudaMemcpyAsync(h + 256, tot, sizeof(ActTotals), cudaMemcpyDeviceToHost, s0));
     CGGM_CUDA_CHECK(cudaStreamSynchronize(s0));
     CholResult cr = chol_decode(h);
     out->logdet = cr.logdet;
@@ -732,14 +769,24 @@ cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, con
   });
 }
 
-}  // extern "C"
-
 extern "C" cggm_status cggm_test_gemm(cggm_ctx* ctx, int transA, int transB, int64_t M, int64_t N, int64_t K,
                                       const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                                       int64_t ldc, double alpha, double beta, int flags) {
   return guard(ctx, [&](Ctx* c) {
     if (M < 0 || N < 0 || K < 0) fail(CGGM_ERR_INVALID_ARG, "negative dimension");
     Epilogue e;
+    e.out1 = C; e.ld1 = ldc; e.a1 = alpha;
+    if (beta != 0.0) { e.in1a = C; e.ld1a = ldc; e.b1 = beta; }
+    gemm(c, transA != 0, transB != 0, M, N, K, A, lda, B, ldb, e, flags);
+  });
+}
+
+extern "C" cggm_status cggm_test_gemm_f32(cggm_ctx* ctx, int transA, int transB, int64_t M, int64_t N, int64_t K,
+                                          const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
+                                          int64_t ldc, double alpha, double beta, int flags) {
+  return guard(ctx, [&](Ctx* c) {
+    if (M < 0 || N < 0 || K < 0) fail(CGGM_ERR_INVALID_ARG, "negative dimension");
+    EpilogueT<float> e;
     e.out1 = C; e.ld1 = ldc; e.a1 = alpha;
     if (beta != 0.0) { e.in1a = C; e.ld1a = ldc; e.b1 = beta; }
     gemm(c, transA != 0, transB != 0, M, N, K, A, lda, B, ldb, e, flags);

@@ -25,9 +25,9 @@ constexpr int NW = NT / 32;   // warp segments per column
 constexpr int UNR = 4;        // 32-row chunks in flight per lane
 constexpr unsigned long long ST_AGG = 1ull << 62, ST_INC = 2ull << 62, ST_VAL = (1ull << 62) - 1;
 
-template <bool LAM>
-__device__ __forceinline__ double lam_of(int64_t i, int64_t j, double lam, int penalize_diag) {
-  return (LAM && i == j && !penalize_diag) ? 0.0 : lam;
+template <bool LAM, typename T>
+__device__ __forceinline__ T lam_of(int64_t i, int64_t j, T lam, int penalize_diag) {
+  return (LAM && i == j && !penalize_diag) ? T(0) : lam;
 }
 
 // contiguous, 32-aligned segment of warp w among NW for a column of `rows` rows
@@ -47,11 +47,11 @@ __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long 
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-template <bool LAM>
-__global__ void __launch_bounds__(NT) k_active_onepass(int64_t nrows, const double* __restrict__ G, int64_t ldg,
-                                                       const int64_t* colptr, const int32_t* rowidx,
-                                                       const double* val, double lam, int penalize_diag,
-                                                       double tie_eps, unsigned long long* state, int32_t* out_row,
+template <bool LAM, typename T>
+__global__ void __launch_bounds__(NT) k_active_onepass(int64_t nrows, const T* __restrict__ G, int64_t ldg,
+                                                       const int64_t* colptr, const int32_t* rowidx, const T* val,
+                                                       T lam, int penalize_diag, T tie_eps,
+                                                       unsigned long long* state, int32_t* out_row,
                                                        int32_t* out_col, long long cap, long long* ties_col,
                                                        double* sub_col) {
   extern __shared__ uint32_t sm[];
@@ -68,24 +68,24 @@ __global__ void __launch_bounds__(NT) k_active_onepass(int64_t nrows, const doub
   __syncthreads();
   for (int64_t t = colptr[j] + threadIdx.x; t < colptr[j + 1]; t += NT) {
     const int32_t r = rowidx[t];
-    if (r < scan_rows && val[t] != 0.0) atomicOr(&sup_bits[r >> 5], 1u << (r & 31));
+    if (r < scan_rows && val[t] != T(0)) atomicOr(&sup_bits[r >> 5], 1u << (r & 31));
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int64_t a, b;
   segment(scan_rows, w, a, b);
-  const double* gc = G + j * ldg;
+  const T* gc = G + j * ldg;
   int cnt = 0;
   long long tc = 0;
   double s = 0.0;
   const int ib = (int)b;
   const int jj = (int)j;
   for (int r0 = (int)a; r0 < ib; r0 += 32 * UNR) {
-    double g[UNR];
+    T g[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       const int i = r0 + u * 32 + lane;
-      g[u] = (i < ib) ? __ldcs(gc + i) : 0.0;   // streamed once: evict-first
+      g[u] = (i < ib) ? __ldcs(gc + i) : T(0);   // streamed once: evict-first
     }
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
@@ -95,24 +95,24 @@ __global__ void __launch_bounds__(NT) k_active_onepass(int64_t nrows, const doub
       const bool in = i < ib;
       const unsigned supw = sup_bits[c0 >> 5];   // one broadcast word per 32-row chunk
       const bool sup = (supw >> lane) & 1u;
-      const double lm = (LAM && i == jj && !penalize_diag) ? 0.0 : lam;
-      const double av = fabs(g[u]);
-      const double d = av - lm;
-      const bool f = in && (d > 0.0 || sup);
+      const T lm = (LAM && i == jj && !penalize_diag) ? T(0) : lam;
+      const T av = fabs(g[u]);
+      const T d = av - lm;
+      const bool f = in && (d > T(0) || sup);
       const unsigned m = __ballot_sync(0xffffffffu, f);
       if (lane == 0) flag_bits[c0 >> 5] = m;
       cnt += __popc(m);
       tc += (in && !sup && fabs(d) <= tie_eps) ? 1 : 0;
-      if (in) s += (LAM && i < jj) ? 2.0 * fmax(d, 0.0) : fmax(d, 0.0);
+      if (in) s += (LAM && i < jj) ? 2.0 * (double)fmax(d, T(0)) : (double)fmax(d, T(0));
     }
   }
   for (int64_t t = colptr[j] + threadIdx.x; t < colptr[j + 1]; t += NT) {
-    const double x = val[t];
-    if (x == 0.0) continue;
+    const T x = val[t];
+    if (x == T(0)) continue;
     const int64_t i = rowidx[t];
-    const double gv = gc[i];
-    const double lm = lam_of<LAM>(i, j, lam, penalize_diag);
-    s += fabs(gv + lm * (x > 0.0 ? 1.0 : -1.0)) - fmax(fabs(gv) - lm, 0.0);
+    const T gv = gc[i];
+    const T lm = lam_of<LAM>(i, j, lam, penalize_diag);
+    s += (double)fabs(gv + lm * (x > T(0) ? T(1) : T(-1))) - (double)fmax(fabs(gv) - lm, T(0));
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -233,26 +233,27 @@ ActWs active_ws(Ctx* c, int64_t q) {
   return w;
 }
 
-void active_compact(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t ldgl, const double* GradT,
-                    int64_t ldgt, const cggm_csc* Lambda, const cggm_csc* Theta, double lam_L, double lam_T,
-                    int penalize_diag, double tie_eps, const ActWs& ws, int32_t* L_row, int32_t* L_col,
-                    int32_t* T_row, int32_t* T_col, long long capL, long long capT) {
+template <typename T>
+void active_compact(Ctx* c, int64_t p, int64_t q, const T* GradL, int64_t ldgl, const T* GradT, int64_t ldgt,
+                    const cggm_csc* Lambda, const cggm_csc* Theta, double lam_L, double lam_T, int penalize_diag,
+                    double tie_eps, const ActWs& ws, int32_t* L_row, int32_t* L_col, int32_t* T_row, int32_t* T_col,
+                    long long capL, long long capT) {
   if (q == 0) return;
   CGGM_CUDA_CHECK(cudaMemsetAsync(ws.stateL, 0, (size_t)q * 2 * 8, c->stream));
   const size_t bl = smem_bytes(q), bt = smem_bytes(p);
-  set_smem(k_active_onepass<true>, bl);
-  set_smem(k_active_onepass<false>, bt);
+  set_smem(k_active_onepass<true, T>, bl);
+  set_smem(k_active_onepass<false, T>, bt);
   {
     Prof pr(c, TAG_ACTIVE);
-    k_active_onepass<true><<<(unsigned)q, NT, bl, c->stream>>>(
-        q, GradL, ldgl, Lambda->colptr, Lambda->rowidx, static_cast<const double*>(Lambda->val), lam_L, penalize_diag,
-        tie_eps, ws.stateL, L_row, L_col, capL, ws.tieL, ws.subL);
+    k_active_onepass<true, T><<<(unsigned)q, NT, bl, c->stream>>>(
+        q, GradL, ldgl, Lambda->colptr, Lambda->rowidx, static_cast<const T*>(Lambda->val), (T)lam_L, penalize_diag,
+        (T)tie_eps, ws.stateL, L_row, L_col, capL, ws.tieL, ws.subL);
     post_launch(c, "k_active_onepass<L>");
   }
   {
     Prof pr(c, TAG_ACTIVE);
-    k_active_onepass<false><<<(unsigned)q, NT, bt, c->stream>>>(
-        p, GradT, ldgt, Theta->colptr, Theta->rowidx, static_cast<const double*>(Theta->val), lam_T, 1, tie_eps,
+    k_active_onepass<false, T><<<(unsigned)q, NT, bt, c->stream>>>(
+        p, GradT, ldgt, Theta->colptr, Theta->rowidx, static_cast<const T*>(Theta->val), (T)lam_T, 1, (T)tie_eps,
         ws.stateT, T_row, T_col, capT, ws.tieT, ws.subT);
     post_launch(c, "k_active_onepass<T>");
   }
@@ -269,5 +270,12 @@ void active_compact(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t l
     post_launch(c, "k_active_totals<T>");
   }
 }
+
+template void active_compact<double>(Ctx*, int64_t, int64_t, const double*, int64_t, const double*, int64_t,
+                                     const cggm_csc*, const cggm_csc*, double, double, int, double, const ActWs&,
+                                     int32_t*, int32_t*, int32_t*, int32_t*, long long, long long);
+template void active_compact<float>(Ctx*, int64_t, int64_t, const float*, int64_t, const float*, int64_t,
+                                    const cggm_csc*, const cggm_csc*, double, double, int, double, const ActWs&,
+                                    int32_t*, int32_t*, int32_t*, int32_t*, long long, long long);
 
 }  // namespace cggm

@@ -145,13 +145,15 @@ inline void post_launch(Ctx* c, const char* what) {
 }
 
 // ------------------------------------------------------------------ dense views
-struct View {
-  double* p;
+template <typename T>
+struct ViewT {
+  T* p;
   int64_t ld;
   int64_t rows, cols;
-  __host__ __device__ double* at(int64_t i, int64_t j) const { return p + i + j * ld; }
-  View sub(int64_t r0, int64_t c0, int64_t nr, int64_t nc) const { return View{p + r0 + c0 * ld, ld, nr, nc}; }
+  __host__ __device__ T* at(int64_t i, int64_t j) const { return p + i + j * ld; }
+  ViewT sub(int64_t r0, int64_t c0, int64_t nr, int64_t nc) const { return ViewT{p + r0 + c0 * ld, ld, nr, nc}; }
 };
+using View = ViewT<double>;
 
 // ------------------------------------------------------------------ GEMM interface (gemm.cu)
 enum GemmFlags : int {
@@ -163,20 +165,25 @@ enum GemmFlags : int {
   SYM_MIRROR = 32,      // with SYM_LOWER: also write every value at its transposed position
 };
 
-struct Epilogue {
+template <typename T>
+struct EpilogueT {
   // out1 = a1*acc + b1*in1a + c1*in1b ; out2 = a2*acc + b2*in2a + c2*in2b (null pointers skip terms)
-  double* out1 = nullptr; int64_t ld1 = 0; double a1 = 1.0;
-  const double* in1a = nullptr; int64_t ld1a = 0; double b1 = 0.0;
-  const double* in1b = nullptr; int64_t ld1b = 0; double c1 = 0.0;
-  double* out2 = nullptr; int64_t ld2 = 0; double a2 = 1.0;
-  const double* in2a = nullptr; int64_t ld2a = 0; double b2 = 0.0;
-  const double* in2b = nullptr; int64_t ld2b = 0; double c2 = 0.0;
+  T* out1 = nullptr; int64_t ld1 = 0; double a1 = 1.0;
+  const T* in1a = nullptr; int64_t ld1a = 0; double b1 = 0.0;
+  const T* in1b = nullptr; int64_t ld1b = 0; double c1 = 0.0;
+  T* out2 = nullptr; int64_t ld2 = 0; double a2 = 1.0;
+  const T* in2a = nullptr; int64_t ld2a = 0; double b2 = 0.0;
+  const T* in2b = nullptr; int64_t ld2b = 0; double c2 = 0.0;
 };
+using Epilogue = EpilogueT<double>;
 
 // C(M x N) epilogue(op(A) op(B)), op(A) = A (transA=false, A is M x K) or A^T (A is K x M).
 // op(B) = B (transB=false, B is K x N) or B^T (B is N x K).  Column-major, FP64 DMMA.
 void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K,
           const double* A, int64_t lda, const double* B, int64_t ldb, const Epilogue& epi, int flags);
+// FP32 variant (gemm_f32.cu): same contract, SIMT FFMA with fp32 accumulation (reading A18).
+void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K,
+          const float* A, int64_t lda, const float* B, int64_t ldb, const EpilogueT<float>& epi, int flags);
 
 // ------------------------------------------------------------------ Cholesky family (chol.cu)
 // In-place blocked recursive Cholesky of the lower triangle of A (q x q).
@@ -191,21 +198,28 @@ struct CholResult {
 //  potrf-only mode with xdiag != null: diagonal subtrees of <= block_inverse_size() columns are
 //  factored in full-inverse mode, their inverses kept at xdiag + col0 (ld ldxd, zeroed upper
 //  triangles required) and used for the panel solves (tmp2: out-of-place product buffer).
-void potrf_recursive(Ctx* c, View A, View Linv, bool full_inverse, double* leafinv, double* logdet_slots,
-                     int* fail_col_dev, double* tmp, size_t tmp_elems, double* xdiag = nullptr, int64_t ldxd = 0,
-                     double* tmp2 = nullptr, size_t tmp2_elems = 0);
+template <typename T>
+void potrf_recursive(Ctx* c, ViewT<T> A, ViewT<T> Linv, bool full_inverse, T* leafinv, double* logdet_slots,
+                     int* fail_col_dev, T* tmp, size_t tmp_elems, T* xdiag = nullptr, int64_t ldxd = 0,
+                     T* tmp2 = nullptr, size_t tmp2_elems = 0);
 int block_inverse_size();
 // Sigma = Linv^T Linv (full symmetric).
-void lauum(Ctx* c, View Linv, View Sigma);
+template <typename T>
+void lauum(Ctx* c, ViewT<T> Linv, ViewT<T> Sigma);
 int leaf_nb();
 
 // ------------------------------------------------------------------ streaming kernels (stream.cu)
-void densify_csc(Ctx* c, const cggm_csc* A, View D);
-void spmm_x_theta(Ctx* c, const double* X, int64_t ldx, int64_t n, const cggm_csc* Theta, View W);
+template <typename T>
+void densify_csc(Ctx* c, const cggm_csc* A, ViewT<T> D);
+template <typename T>
+void spmm_x_theta(Ctx* c, const T* X, int64_t ldx, int64_t n, const cggm_csc* Theta, ViewT<T> W);
+template <typename T>
 void check_csc(Ctx* c, const cggm_csc* A, bool symmetric, int* flag_dev);
-void grad_lambda(Ctx* c, int64_t q, const double* Syy, int64_t l1, const double* Sigma, int64_t l2,
-                 const double* Psi, int64_t l3, double* G, int64_t l4);
-void copy2d(Ctx* c, View dst, const double* src, int64_t lds);
+template <typename T>
+void grad_lambda(Ctx* c, int64_t q, const T* Syy, int64_t l1, const T* Sigma, int64_t l2, const T* Psi, int64_t l3,
+                 T* G, int64_t l4);
+template <typename T>
+void copy2d(Ctx* c, ViewT<T> dst, const T* src, int64_t lds);
 
 }  // namespace cggm
 

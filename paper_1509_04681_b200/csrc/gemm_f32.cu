@@ -1,0 +1,325 @@
+// FP32 variant of the GEMM engine (reading A18: fp32 inputs, fp32 accumulation).  FP64 DMMA has no
+// fp32 counterpart short of TF32 (10-bit mantissa, too inexact for the 1e-4 contract), so the
+// consumers are SIMT FFMA: CTA tile 128x128, 256 threads with an 8x8 register tile each, fed by the
+// same TMA (SWIZZLE_128B) -> shared-memory ring with mbarrier full/empty pipeline, thread 0
+// producing STAGES-1 k-tiles (32 floats) ahead.  Thread -> row maps are chosen per operand layout
+// so that every ld.shared.v4 quarter-warp hits 8 distinct 16-byte chunks:
+//   MN-inner operand: x = 4*tx + 64*h + i   (two 16-byte chunks of 4 consecutive x per k)
+//   K-inner  operand: x = tx + 16*r         (one 16-byte chunk = 4 consecutive k per row)
+// Same flags (triangular k-ranges, lower trapezoid / mirror), tile order and epilogue as gemm.cu.
+#include "common.cuh"
+
+namespace cggm {
+namespace {
+
+constexpr int FBK = 32;
+constexpr int FSTAGES = 4;
+constexpr int FBM = 128, FBN = 128;
+constexpr int FNT = 256;
+constexpr int F_OP_BYTES = FBM * FBK * 4;   // 16 KB
+constexpr int F_STAGE = 2 * F_OP_BYTES;
+constexpr int F_EPI_LD = FBM + 1;
+constexpr int F_EPI_BYTES = FBN * F_EPI_LD * 4;
+constexpr int F_MAIN = FSTAGES * F_STAGE;
+constexpr int F_DATA = F_MAIN > F_EPI_BYTES ? F_MAIN : F_EPI_BYTES;
+constexpr int F_SMEM = F_DATA + 1024 + 2 * FSTAGES * 8;
+constexpr int GROUP_N = 8;
+
+struct KParamsF {
+  int M, N, K;
+  int tilesM, tilesN;
+  int flags;
+  int a3d, b3d;
+  EpilogueT<float> epi;
+};
+
+__device__ __forceinline__ void tile_coords_f(const KParamsF& P, int t, int& I, int& J) {
+  if (P.flags & SYM_LOWER) {
+    const long long tri = (long long)P.tilesN * (P.tilesN + 1) / 2;
+    if (t < tri) {
+      int i = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+      while ((long long)(i + 1) * (i + 2) / 2 <= t) ++i;
+      while ((long long)i * (i + 1) / 2 > t) --i;
+      I = i;
+      J = t - (int)((long long)i * (i + 1) / 2);
+    } else {
+      const int r = t - (int)tri;
+      I = P.tilesN + r / P.tilesN;
+      J = r % P.tilesN;
+    }
+    return;
+  }
+  const int per_group = GROUP_N * P.tilesM;
+  const int gi = t / per_group;
+  const int local = t - gi * per_group;
+  const int nb0 = gi * GROUP_N;
+  const int width = min(GROUP_N, P.tilesN - nb0);
+  I = local / width;
+  J = nb0 + local % width;
+  if (P.flags & B_KLE_N) J = P.tilesN - 1 - J;
+  if (P.flags & A_KLE_M) I = P.tilesM - 1 - I;
+}
+
+__device__ __forceinline__ void epi_apply_f(const EpilogueT<float>& E, int64_t r, int64_t c, float v) {
+  if (E.out1) {
+    float o = __fmul_rn((float)E.a1, v);
+    if (E.in1a) o = __fadd_rn(o, __fmul_rn((float)E.b1, E.in1a[r + c * E.ld1a]));
+    if (E.in1b) o = __fadd_rn(o, __fmul_rn((float)E.c1, E.in1b[r + c * E.ld1b]));
+    E.out1[r + c * E.ld1] = o;
+  }
+  if (E.out2) {
+    float o = __fmul_rn((float)E.a2, v);
+    if (E.in2a) o = __fadd_rn(o, __fmul_rn((float)E.b2, E.in2a[r + c * E.ld2a]));
+    if (E.in2b) o = __fadd_rn(o, __fmul_rn((float)E.c2, E.in2b[r + c * E.ld2b]));
+    E.out2[r + c * E.ld2] = o;
+  }
+}
+
+template <bool KINNER>
+__device__ __forceinline__ int fx(int tx, int r) {
+  return KINNER ? tx + 16 * r : 4 * tx + 64 * (r >> 2) + (r & 3);
+}
+
+__device__ __forceinline__ void lds_v4(float (&v)[4], uint32_t addr) {
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "r"(addr));
+}
+
+// operand tile loads for one group of 4 k (k4 = 0..7 inside the 32-wide k tile) into v[k][8]
+template <bool KINNER>
+__device__ __forceinline__ void load_group(float (&v)[4][8], uint32_t base, int tx, int k4) {
+  if (KINNER) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int x = tx + 16 * r;
+      const int chunk = k4 ^ (x & 7);
+      float q[4];
+      lds_v4(q, base + x * 128 + chunk * 16);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) v[kk][r] = q[kk];
+    }
+  } else {
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const int k = 4 * k4 + kk;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int x0 = 4 * tx + 64 * h;
+        const int xb = x0 >> 5;
+        const int chunk = ((x0 & 31) >> 2) ^ (k & 7);
+        float q[4];
+        lds_v4(q, base + xb * 4096 + k * 128 + chunk * 16);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[kk][4 * h + i] = q[i];
+      }
+    }
+  }
+}
+
+template <bool AK, bool BKI>
+__global__ void __launch_bounds__(FNT, 1)
+    gemm_ffma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const KParamsF P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + F_DATA);
+  uint64_t* empty = full + FSTAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int I, J;
+  tile_coords_f(P, blockIdx.x, I, J);
+  const int m0 = I * FBM, n0 = J * FBN;
+  int kbeg = 0, kend = P.K;
+  if (P.flags & A_KGE_M) kbeg = max(kbeg, m0);
+  if (P.flags & B_KGE_N) kbeg = max(kbeg, n0);
+  if (P.flags & A_KLE_M) kend = min(kend, m0 + FBM);
+  if (P.flags & B_KLE_N) kend = min(kend, n0 + FBN);
+  const int kt0 = kbeg / FBK;
+  const int nkt = kend > kbeg ? (kend - kt0 * FBK + FBK - 1) / FBK : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < FSTAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], FNT / 32);
+    }
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  int a_boxes = 0, b_boxes = 0;
+  if (!AK)
+    for (int xb = 0; xb < FBM / 32; ++xb) a_boxes += (m0 + xb * 32 < P.M);
+  if (!BKI)
+    for (int xb = 0; xb < FBN / 32; ++xb) b_boxes += (n0 + xb * 32 < P.N);
+  const uint32_t tx_bytes =
+      ((AK || P.a3d) ? F_OP_BYTES : a_boxes * 4096) + ((BKI || P.b3d) ? F_OP_BYTES : b_boxes * 4096);
+  auto issue = [&](int i) {
+    const int s = i % FSTAGES;
+    uint8_t* sa = smem + s * F_STAGE;
+    uint8_t* sb = sa + F_OP_BYTES;
+    ptx::mbar_arrive_expect_tx(&full[s], tx_bytes);
+    const int k = (kt0 + i) * FBK;
+    if (AK) ptx::tma_load_2d(sa, &tmA, &full[s], k, m0);
+    else if (P.a3d) ptx::tma_load_3d(sa, &tmA, &full[s], 0, k, m0 / 32);
+    else
+      for (int xb = 0; xb < a_boxes; ++xb) ptx::tma_load_2d(sa + xb * 4096, &tmA, &full[s], m0 + xb * 32, k);
+    if (BKI) ptx::tma_load_2d(sb, &tmB, &full[s], k, n0);
+    else if (P.b3d) ptx::tma_load_3d(sb, &tmB, &full[s], 0, k, n0 / 32);
+    else
+      for (int xb = 0; xb < b_boxes; ++xb) ptx::tma_load_2d(sb + xb * 4096, &tmB, &full[s], n0 + xb * 32, k);
+  };
+  if (threadIdx.x == 0) {
+    if (nkt > 0) {
+      ptx::prefetch_tmap(&tmA);
+      ptx::prefetch_tmap(&tmB);
+    }
+    for (int i = 0; i < FSTAGES - 1 && i < nkt; ++i) issue(i);
+  }
+  const int tm = threadIdx.x & 15, tn = threadIdx.x >> 4;
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+  for (int it = 0; it < nkt; ++it) {
+    const int s = it % FSTAGES;
+    ptx::mbar_wait(&full[s], (it / FSTAGES) & 1);
+    const uint32_t sa = ptx::smem_u32(smem + s * F_STAGE);
+    const uint32_t sb = sa + F_OP_BYTES;
+#pragma unroll 2
+    for (int k4 = 0; k4 < FBK / 4; ++k4) {
+      float a[4][8], b[4][8];
+      load_group<AK>(a, sa, tm, k4);
+      load_group<BKI>(b, sb, tn, k4);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[kk][i], b[kk][j], acc[i][j]);
+    }
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&empty[s]);
+    if (threadIdx.x == 0) {
+      const int jn = it + FSTAGES - 1;
+      if (jn < nkt) {
+        if (jn >= FSTAGES) ptx::mbar_wait(&empty[jn % FSTAGES], ((jn / FSTAGES) & 1) ^ 1);
+        issue(jn);
+      }
+    }
+  }
+  (void)warp;
+  __syncthreads();
+  float* Cs = reinterpret_cast<float*>(smem);
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) Cs[fx<BKI>(tn, j) * F_EPI_LD + fx<AK>(tm, i)] = acc[i][j];
+  __syncthreads();
+  const bool diag = (P.flags & SYM_LOWER) && I == J;
+  for (int idx = threadIdx.x; idx < FBM * FBN; idx += FNT) {
+    const int ml = idx % FBM, nl = idx / FBM;
+    const int m = m0 + ml, n = n0 + nl;
+    if (m >= P.M || n >= P.N) continue;
+    if (diag && m < n) continue;
+    epi_apply_f(P.epi, m, n, Cs[nl * F_EPI_LD + ml]);
+  }
+  if (P.flags & SYM_MIRROR) {
+    for (int idx = threadIdx.x; idx < FBM * FBN; idx += FNT) {
+      const int nl = idx % FBN, ml = idx / FBN;
+      const int m = m0 + ml, n = n0 + nl;
+      if (m >= P.M || n >= P.N) continue;
+      if (diag && m <= n) continue;
+      epi_apply_f(P.epi, n, m, Cs[nl * F_EPI_LD + ml]);
+    }
+  }
+}
+
+CUtensorMap make_map_f(Ctx* c, const float* ptr, int64_t ld, int64_t inner, int64_t outer, uint32_t box_inner,
+                       uint32_t box_outer) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = c->encode_tiled(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box,
+                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError{CGGM_ERR_CUDA, "cuTensorMapEncodeTiled (f32) failed (" + std::to_string((int)r) + ")"};
+  return m;
+}
+
+CUtensorMap make_map_f_mn3d(Ctx* c, const float* ptr, int64_t ld, int64_t X, int64_t K) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {32, (cuuint64_t)K, (cuuint64_t)(X / 32)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 4), 128};
+  cuuint32_t box[3] = {32, FBK, FBM / 32};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = c->encode_tiled(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ptr), dims, strides, box,
+                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError{CGGM_ERR_CUDA, "cuTensorMapEncodeTiled (f32 3d) failed (" + std::to_string((int)r) + ")"};
+  return m;
+}
+
+template <bool AK, bool BKI>
+void launch_f(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KParamsF& P, int grid) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    CGGM_CUDA_CHECK(cudaFuncSetAttribute(gemm_ffma_kernel<AK, BKI>, cudaFuncAttributeMaxDynamicSharedMemorySize, F_SMEM));
+    attr_set = true;
+  }
+  Prof pr(c, c->cur_tag);
+  gemm_ffma_kernel<AK, BKI><<<grid, FNT, F_SMEM, c->stream>>>(ma, mb, P);
+  post_launch(c, "gemm_ffma_kernel");
+}
+
+bool tma_ok_f(const float* p, int64_t ld) { return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && (ld % 4 == 0); }
+
+}  // namespace
+
+void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+          const float* B, int64_t ldb, const EpilogueT<float>& epi, int flags) {
+  if (M <= 0 || N <= 0) return;
+  if (M > (1LL << 30) || N > (1LL << 30) || K > (1LL << 30))
+    throw CudaError{CGGM_ERR_UNSUPPORTED, "gemm dimension too large"};
+  static float* dummy = nullptr;
+  if (K <= 0) {
+    if (!dummy) CGGM_CUDA_CHECK(cudaMalloc(&dummy, 32 * 32 * 4));
+    A = dummy; B = dummy; lda = 32; ldb = 32;
+  }
+  const int64_t Keff = K > 0 ? K : 1;
+  const int64_t arows = transA ? Keff : M, acols = transA ? M : Keff;
+  const int64_t brows = transB ? N : Keff, bcols = transB ? Keff : N;
+  if (K > 0 && !tma_ok_f(A, lda)) {
+    const int64_t ld = (arows + 3) & ~int64_t(3);
+    float* pk = static_cast<float*>(ws_get(c, WS_PACK0 + 2 * c->lane, (size_t)ld * acols * 4));
+    CGGM_CUDA_CHECK(cudaMemcpy2DAsync(pk, ld * 4, A, lda * 4, arows * 4, acols, cudaMemcpyDeviceToDevice, c->stream));
+    A = pk; lda = ld;
+  }
+  if (K > 0 && !tma_ok_f(B, ldb)) {
+    const int64_t ld = (brows + 3) & ~int64_t(3);
+    float* pk = static_cast<float*>(ws_get(c, WS_PACK1 + 2 * c->lane, (size_t)ld * bcols * 4));
+    CGGM_CUDA_CHECK(cudaMemcpy2DAsync(pk, ld * 4, B, ldb * 4, brows * 4, bcols, cudaMemcpyDeviceToDevice, c->stream));
+    B = pk; ldb = ld;
+  }
+  if ((flags & SYM_LOWER) && (M < N || ((flags & SYM_MIRROR) && M != N)))
+    throw CudaError{CGGM_ERR_SHAPE, "SYM_LOWER gemm needs M >= N (M == N with SYM_MIRROR)"};
+  KParamsF P;
+  P.M = (int)M; P.N = (int)N; P.K = (int)(K > 0 ? K : 0);
+  P.flags = flags;
+  P.epi = epi;
+  P.tilesM = (int)((M + FBM - 1) / FBM);
+  P.tilesN = (int)((N + FBN - 1) / FBN);
+  const int grid = (flags & SYM_LOWER) ? P.tilesN * (P.tilesN + 1) / 2 + (P.tilesM - P.tilesN) * P.tilesN
+                                       : P.tilesM * P.tilesN;
+  P.a3d = (!transA && M % 32 == 0 && !c->no_tma3d) ? 1 : 0;
+  P.b3d = (transB && N % 32 == 0 && !c->no_tma3d) ? 1 : 0;
+  CUtensorMap ma = transA ? make_map_f(c, A, lda, Keff, M, FBK, FBM)
+                          : (P.a3d ? make_map_f_mn3d(c, A, lda, M, Keff) : make_map_f(c, A, lda, M, Keff, 32, FBK));
+  CUtensorMap mb = transB ? (P.b3d ? make_map_f_mn3d(c, B, ldb, N, Keff) : make_map_f(c, B, ldb, N, Keff, 32, FBK))
+                          : make_map_f(c, B, ldb, Keff, N, FBK, FBN);
+  const bool AK = transA, BKI = !transB;
+  if (AK && BKI) launch_f<true, true>(c, ma, mb, P, grid);
+  else if (AK && !BKI) launch_f<true, false>(c, ma, mb, P, grid);
+  else if (!AK && BKI) launch_f<false, true>(c, ma, mb, P, grid);
+  else launch_f<false, false>(c, ma, mb, P, grid);
+}
+
+}  // namespace cggm

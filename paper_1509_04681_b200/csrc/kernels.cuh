@@ -6,8 +6,10 @@
 
 namespace cggm {
 
-void col_partials(Ctx* c, int mode, int64_t n, int64_t ncols, const double* A, int64_t lda, const double* B,
-                  int64_t ldb, const cggm_csc* csc, double* part);
+template <typename T>
+void col_partials(Ctx* c, int mode, int64_t n, int64_t ncols, const T* A, int64_t lda, const T* B, int64_t ldb,
+                  const cggm_csc* csc, double* part);
+template <typename T>
 void csc_abs_partials(Ctx* c, const cggm_csc* A, bool skip_diag, double* part);
 void sum_arrays(Ctx* c, int count, const double* const* arrs_dev, const int64_t* lens_dev, double* out_dev);
 void init_scalars(Ctx* c, int* fail_col, int* flag);
@@ -28,9 +30,10 @@ struct ActWs {
 ActWs active_ws(Ctx* c, int64_t q);
 // Single-pass ordered compaction of both lists + totals (device).  Entries at positions >= cap are
 // not written (the caller reports CGGM_ERR_CAPACITY from the totals).
-void active_compact(Ctx* c, int64_t p, int64_t q, const double* GradL, int64_t ldgl, const double* GradT,
-                    int64_t ldgt, const cggm_csc* Lambda, const cggm_csc* Theta, double lam_L, double lam_T,
-                    int penalize_diag, double tie_eps, const ActWs& ws, int32_t* L_row, int32_t* L_col,
-                    int32_t* T_row, int32_t* T_col, long long capL, long long capT);
+template <typename T>
+void active_compact(Ctx* c, int64_t p, int64_t q, const T* GradL, int64_t ldgl, const T* GradT, int64_t ldgt,
+                    const cggm_csc* Lambda, const cggm_csc* Theta, double lam_L, double lam_T, int penalize_diag,
+                    double tie_eps, const ActWs& ws, int32_t* L_row, int32_t* L_col, int32_t* T_row, int32_t* T_col,
+                    long long capL, long long capT);
 
 }  // namespace cggm

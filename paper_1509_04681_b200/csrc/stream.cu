@@ -9,22 +9,24 @@
 namespace cggm {
 
 // ------------------------------------------------------------------ densify CSC -> dense
-__global__ void k_scatter_csc(const int64_t* colptr, const int32_t* rowidx, const double* val, int64_t ncols,
-                              double* D, int64_t ldd) {
+template <typename T>
+__global__ void k_scatter_csc(const int64_t* colptr, const int32_t* rowidx, const T* val, int64_t ncols, T* D,
+                              int64_t ldd) {
   const int64_t j = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x / 32);
   if (j >= ncols) return;
   const int lane = threadIdx.x & 31;
   for (int64_t t = colptr[j] + lane; t < colptr[j + 1]; t += 32) D[rowidx[t] + j * ldd] = val[t];
 }
 
-void densify_csc(Ctx* c, const cggm_csc* A, View D) {
-  CGGM_CUDA_CHECK(cudaMemset2DAsync(D.p, D.ld * 8, 0, D.rows * 8, D.cols, c->stream));
+template <typename T>
+void densify_csc(Ctx* c, const cggm_csc* A, ViewT<T> D) {
+  CGGM_CUDA_CHECK(cudaMemset2DAsync(D.p, D.ld * sizeof(T), 0, D.rows * sizeof(T), D.cols, c->stream));
   if (A->ncols == 0 || A->nnz == 0) return;
   const int wpb = 8;
   const int64_t grid = (A->ncols + wpb - 1) / wpb;
   Prof pr(c, TAG_DENSIFY);
-  k_scatter_csc<<<(unsigned)grid, wpb * 32, 0, c->stream>>>(A->colptr, A->rowidx, static_cast<const double*>(A->val),
-                                                            A->ncols, D.p, D.ld);
+  k_scatter_csc<T><<<(unsigned)grid, wpb * 32, 0, c->stream>>>(A->colptr, A->rowidx, static_cast<const T*>(A->val),
+                                                               A->ncols, D.p, D.ld);
   post_launch(c, "k_scatter_csc");
 }
 
@@ -34,17 +36,18 @@ void densify_csc(Ctx* c, const cggm_csc* A, View D) {
 // block's slice of X (128 x p doubles, 41 MB at p = 40000) stays resident in the 126 MB L2 and X
 // is read from HBM about once.
 constexpr int SPMM_ROWS = 128;
-__global__ void __launch_bounds__(SPMM_ROWS) k_spmm_x_theta(const double* __restrict__ X, int64_t ldx, int64_t n,
+template <typename T>
+__global__ void __launch_bounds__(SPMM_ROWS) k_spmm_x_theta(const T* __restrict__ X, int64_t ldx, int64_t n,
                                                             const int64_t* __restrict__ colptr,
                                                             const int32_t* __restrict__ rowidx,
-                                                            const double* __restrict__ val, double* __restrict__ W,
+                                                            const T* __restrict__ val, T* __restrict__ W,
                                                             int64_t ldw) {
   __shared__ int32_t rows[SPMM_ROWS];
-  __shared__ double vals[SPMM_ROWS];
+  __shared__ T vals[SPMM_ROWS];
   const int64_t j = blockIdx.x;
   const int64_t k = (int64_t)blockIdx.y * SPMM_ROWS + threadIdx.x;
   const int64_t a = colptr[j], b = colptr[j + 1];
-  double acc = 0.0;
+  T acc = T(0);
   for (int64_t t0 = a; t0 < b; t0 += SPMM_ROWS) {
     const int cnt = (int)((b - t0) < SPMM_ROWS ? (b - t0) : SPMM_ROWS);
     __syncthreads();
@@ -56,7 +59,7 @@ __global__ void __launch_bounds__(SPMM_ROWS) k_spmm_x_theta(const double* __rest
     if (k < n) {
       int e = 0;
       for (; e + 8 <= cnt; e += 8) {  // 8 independent gathers in flight
-        double xv[8];
+        T xv[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) xv[u] = __ldg(X + k + (int64_t)rows[e + u] * ldx);
 #pragma unroll
@@ -68,19 +71,21 @@ __global__ void __launch_bounds__(SPMM_ROWS) k_spmm_x_theta(const double* __rest
   if (k < n) W[k + j * ldw] = acc;
 }
 
-void spmm_x_theta(Ctx* c, const double* X, int64_t ldx, int64_t n, const cggm_csc* Theta, View W) {
+template <typename T>
+void spmm_x_theta(Ctx* c, const T* X, int64_t ldx, int64_t n, const cggm_csc* Theta, ViewT<T> W) {
   if (Theta->ncols == 0 || n == 0) return;
   Prof pr(c, TAG_SPMM);
   dim3 grid((unsigned)Theta->ncols, (unsigned)((n + SPMM_ROWS - 1) / SPMM_ROWS));
-  k_spmm_x_theta<<<grid, SPMM_ROWS, 0, c->stream>>>(X, ldx, n, Theta->colptr, Theta->rowidx,
-                                                   static_cast<const double*>(Theta->val), W.p, W.ld);
+  k_spmm_x_theta<T><<<grid, SPMM_ROWS, 0, c->stream>>>(X, ldx, n, Theta->colptr, Theta->rowidx,
+                                                      static_cast<const T*>(Theta->val), W.p, W.ld);
   post_launch(c, "k_spmm_x_theta");
 }
 
 // ------------------------------------------------------------------ CSC checks
 // flag bits: 1 = colptr not monotone / bad ends, 2 = row out of range or not strictly increasing,
 //            4 = not symmetric (symmetric mode)
-__global__ void k_check_csc(const int64_t* colptr, const int32_t* rowidx, const double* val, int64_t nrows,
+template <typename T>
+__global__ void k_check_csc(const int64_t* colptr, const int32_t* rowidx, const T* val, int64_t nrows,
                             int64_t ncols, int64_t nnz, int symmetric, int* flag) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j == 0 && (colptr[0] != 0 || colptr[ncols] != nnz)) atomicOr(flag, 1);
@@ -117,39 +122,45 @@ __global__ void k_check_csc(const int64_t* colptr, const int32_t* rowidx, const 
   }
 }
 
+template <typename T>
 void check_csc(Ctx* c, const cggm_csc* A, bool symmetric, int* flag_dev) {
   if (A->ncols == 0) return;
   const int64_t grid = (A->ncols + 255) / 256;
   Prof pr(c, c->cur_tag);
-  k_check_csc<<<(unsigned)grid, 256, 0, c->stream>>>(A->colptr, A->rowidx, static_cast<const double*>(A->val),
+  k_check_csc<T><<<(unsigned)grid, 256, 0, c->stream>>>(A->colptr, A->rowidx, static_cast<const T*>(A->val),
                                                      A->nrows, A->ncols, A->nnz, symmetric ? 1 : 0, flag_dev);
   post_launch(c, "k_check_csc");
 }
 
 // ------------------------------------------------------------------ grad_Lambda elementwise
-__global__ void __launch_bounds__(256) k_grad_lambda(int64_t q, const double* __restrict__ Syy, int64_t l1,
-                                                     const double* __restrict__ Sg, int64_t l2,
-                                                     const double* __restrict__ Psi, int64_t l3,
-                                                     double* __restrict__ G, int64_t l4) {
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dadd_rn(a, -b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fadd_rn(a, -b); }
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_grad_lambda(int64_t q, const T* __restrict__ Syy, int64_t l1,
+                                                     const T* __restrict__ Sg, int64_t l2, const T* __restrict__ Psi,
+                                                     int64_t l3, T* __restrict__ G, int64_t l4) {
   const int64_t j = blockIdx.x;
-  const double* a = Syy + j * l1;
-  const double* b = Sg + j * l2;
-  const double* c = Psi + j * l3;
-  double* g = G + j * l4;
-  for (int64_t i = threadIdx.x; i < q; i += 256) g[i] = __dadd_rn(__dadd_rn(a[i], -b[i]), -c[i]);
+  const T* a = Syy + j * l1;
+  const T* b = Sg + j * l2;
+  const T* c = Psi + j * l3;
+  T* g = G + j * l4;
+  for (int64_t i = threadIdx.x; i < q; i += 256) g[i] = sub_rn(sub_rn(a[i], b[i]), c[i]);
 }
 
-void grad_lambda(Ctx* c, int64_t q, const double* Syy, int64_t l1, const double* Sigma, int64_t l2,
-                 const double* Psi, int64_t l3, double* G, int64_t l4) {
+template <typename T>
+void grad_lambda(Ctx* c, int64_t q, const T* Syy, int64_t l1, const T* Sigma, int64_t l2, const T* Psi, int64_t l3,
+                 T* G, int64_t l4) {
   if (q == 0) return;
   Prof pr(c, c->cur_tag);
-  k_grad_lambda<<<(unsigned)q, 256, 0, c->stream>>>(q, Syy, l1, Sigma, l2, Psi, l3, G, l4);
+  k_grad_lambda<T><<<(unsigned)q, 256, 0, c->stream>>>(q, Syy, l1, Sigma, l2, Psi, l3, G, l4);
   post_launch(c, "k_grad_lambda");
 }
 
-void copy2d(Ctx* c, View dst, const double* src, int64_t lds) {
+template <typename T>
+void copy2d(Ctx* c, ViewT<T> dst, const T* src, int64_t lds) {
   if (dst.rows == 0 || dst.cols == 0) return;
-  CGGM_CUDA_CHECK(cudaMemcpy2DAsync(dst.p, dst.ld * 8, src, lds * 8, dst.rows * 8, dst.cols,
+  CGGM_CUDA_CHECK(cudaMemcpy2DAsync(dst.p, dst.ld * sizeof(T), src, lds * sizeof(T), dst.rows * sizeof(T), dst.cols,
                                     cudaMemcpyDeviceToDevice, c->stream));
 }
 
@@ -172,18 +183,19 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 // mode 0: part[j] = sum_k Y[k,j] * (Y Lambda)[k,j]   (<Y, Y Lambda>, tr(S_yy Lambda) * n)
 // mode 1: part[j] = sum_k A[k,j] * B[k,j]           (<W, Y>)
 // mode 2: part[j] = sum_k A[k,j]^2                  (||Z||_F^2)
-__global__ void __launch_bounds__(256) k_col_partials(int mode, int64_t n, const double* __restrict__ A, int64_t lda,
-                                                      const double* __restrict__ B, int64_t ldb,
+template <typename T>
+__global__ void __launch_bounds__(256) k_col_partials(int mode, int64_t n, const T* __restrict__ A, int64_t lda,
+                                                      const T* __restrict__ B, int64_t ldb,
                                                       const int64_t* __restrict__ colptr,
-                                                      const int32_t* __restrict__ rowidx,
-                                                      const double* __restrict__ val, double* part) {
+                                                      const int32_t* __restrict__ rowidx, const T* __restrict__ val,
+                                                      double* part) {
   __shared__ double sh[256];
   const int64_t j = blockIdx.x;
-  double s = 0.0;
+  T s = T(0);
   if (mode == 0) {
     const int64_t a = colptr[j], b = colptr[j + 1];
     for (int64_t k = threadIdx.x; k < n; k += 256) {
-      double yl = 0.0;
+      T yl = T(0);
       for (int64_t t = a; t < b; ++t) yl = fma(__ldg(A + k + (int64_t)rowidx[t] * lda), val[t], yl);
       s = fma(__ldg(A + k + j * lda), yl, s);
     }
@@ -191,23 +203,24 @@ __global__ void __launch_bounds__(256) k_col_partials(int mode, int64_t n, const
     for (int64_t k = threadIdx.x; k < n; k += 256) s = fma(A[k + j * lda], B[k + j * ldb], s);
   } else {
     for (int64_t k = threadIdx.x; k < n; k += 256) {
-      const double v = A[k + j * lda];
+      const T v = A[k + j * lda];
       s = fma(v, v, s);
     }
   }
-  s = block_sum<256>(s, sh);
-  if (threadIdx.x == 0) part[j] = s;
+  const double r = block_sum<256>((double)s, sh);
+  if (threadIdx.x == 0) part[j] = r;
 }
 
 // per-column sum |val| of a CSC (diagonal skipped when skip_diag)
-__global__ void k_csc_abs_partials(const int64_t* colptr, const int32_t* rowidx, const double* val, int64_t ncols,
+template <typename T>
+__global__ void k_csc_abs_partials(const int64_t* colptr, const int32_t* rowidx, const T* val, int64_t ncols,
                                    int skip_diag, double* part) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= ncols) return;
   double s = 0.0;
   for (int64_t t = colptr[j]; t < colptr[j + 1]; ++t) {
     if (skip_diag && rowidx[t] == j) continue;
-    s += fabs(val[t]);
+    s += fabs((double)val[t]);
   }
   part[j] = s;
 }
@@ -223,21 +236,23 @@ __global__ void __launch_bounds__(256) k_sum_arrays(const double* const* arrs, c
   if (threadIdx.x == 0) out[blockIdx.x] = s;
 }
 
-void col_partials(Ctx* c, int mode, int64_t n, int64_t ncols, const double* A, int64_t lda, const double* B,
-                  int64_t ldb, const cggm_csc* csc, double* part) {
+template <typename T>
+void col_partials(Ctx* c, int mode, int64_t n, int64_t ncols, const T* A, int64_t lda, const T* B, int64_t ldb,
+                  const cggm_csc* csc, double* part) {
   if (ncols == 0) return;
   Prof pr(c, c->cur_tag);
-  k_col_partials<<<(unsigned)ncols, 256, 0, c->stream>>>(mode, n, A, lda, B, ldb, csc ? csc->colptr : nullptr,
-                                                         csc ? csc->rowidx : nullptr,
-                                                         csc ? static_cast<const double*>(csc->val) : nullptr, part);
+  k_col_partials<T><<<(unsigned)ncols, 256, 0, c->stream>>>(mode, n, A, lda, B, ldb, csc ? csc->colptr : nullptr,
+                                                            csc ? csc->rowidx : nullptr,
+                                                            csc ? static_cast<const T*>(csc->val) : nullptr, part);
   post_launch(c, "k_col_partials");
 }
 
+template <typename T>
 void csc_abs_partials(Ctx* c, const cggm_csc* A, bool skip_diag, double* part) {
   if (A->ncols == 0) return;
   Prof pr(c, c->cur_tag);
-  k_csc_abs_partials<<<(unsigned)((A->ncols + 255) / 256), 256, 0, c->stream>>>(
-      A->colptr, A->rowidx, static_cast<const double*>(A->val), A->ncols, skip_diag ? 1 : 0, part);
+  k_csc_abs_partials<T><<<(unsigned)((A->ncols + 255) / 256), 256, 0, c->stream>>>(
+      A->colptr, A->rowidx, static_cast<const T*>(A->val), A->ncols, skip_diag ? 1 : 0, part);
   post_launch(c, "k_csc_abs_partials");
 }
 
@@ -272,5 +287,19 @@ void init_scalars(Ctx* c, int* fail_col, int* flag) {
   k_init_scalars<<<1, 1, 0, c->stream>>>(fail_col, flag);
   post_launch(c, "k_init_scalars");
 }
+
+#define CGGM_INST(T)                                                                                      \
+  template void densify_csc<T>(Ctx*, const cggm_csc*, ViewT<T>);                                         \
+  template void spmm_x_theta<T>(Ctx*, const T*, int64_t, int64_t, const cggm_csc*, ViewT<T>);             \
+  template void check_csc<T>(Ctx*, const cggm_csc*, bool, int*);                                         \
+  template void grad_lambda<T>(Ctx*, int64_t, const T*, int64_t, const T*, int64_t, const T*, int64_t, T*, \
+                               int64_t);                                                                 \
+  template void copy2d<T>(Ctx*, ViewT<T>, const T*, int64_t);                                            \
+  template void col_partials<T>(Ctx*, int, int64_t, int64_t, const T*, int64_t, const T*, int64_t,        \
+                                const cggm_csc*, double*);                                               \
+  template void csc_abs_partials<T>(Ctx*, const cggm_csc*, bool, double*);
+CGGM_INST(double)
+CGGM_INST(float)
+#undef CGGM_INST
 
 }  // namespace cggm
