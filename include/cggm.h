@@ -12,7 +12,9 @@
  *  - Every array argument is a DEVICE pointer, caller-allocated and caller-owned; the library
  *    never frees or retains it.  Dense matrices are COLUMN-MAJOR with a leading dimension
  *    ld >= rows (element (i,j) at ptr[i + j*ld]).  Element type is the ctx dtype
- *    (CGGM_F64 = double; CGGM_F32 = float, reserved: returns CGGM_ERR_UNSUPPORTED this round).
+ *    (CGGM_F64 = double: FP64 tensor-pipe DMMA engine; CGGM_F32 = float: the FP32 variant, fp32
+ *    inputs and fp32 arithmetic/accumulation in every kernel, SIMT FFMA engine; reading A18).
+ *    Host scalar outputs are double in both cases.
  *  - Symmetric outputs (S_yy, Sigma, Psi, grad_Lambda) are written as FULL matrices whose two
  *    triangles are bit-identical.
  *  - Sparse Lambda / Theta are passed as cggm_csc (device arrays): int64 colptr[ncols+1],

@@ -31,126 +31,144 @@ constexpr int LEAF_THREADS = 256;
 template <typename T>
 constexpr int leaf_smem_bytes() { return 2 * NB * (NB + 1) * (int)sizeof(T); }
 
-// Leaf: Cholesky + triangular inverse of one nb x nb (nb <= 64) diagonal block in one CTA.
-// 256 threads; thread t owns the 4x4 register blocks rows 4*(t&15).., cols 4*(t>>4).. of both
-// the factor (a) and the inverse (x); rows/columns >= nb are padded with the identity (so L and
-// L^{-1} are block-diag(., I)).  One fused sweep, ONE __syncthreads per column j:
-//   before the barrier  - the owners of column j (one half-warp) receive the pivot d by warp
-//     shuffle, test it, form inv = 1/sqrt(d), scale column j and publish it; the owners of row j
-//     of X publish that row (not yet divided by L_jj);
-//   after the barrier   - every thread applies the rank-1 Cholesky update to its block of a and
-//     the forward-substitution update X[i,:] -= L_ij * X[j,:] * inv to its block of x.
-// Buffers are double-buffered by column parity so no second barrier is needed.  The pivot test
-// !(d > 0) records the first failing column (reading A10); log L_jj is summed in a fixed order.
+// Leaf: Cholesky + triangular inverse of one nb x nb (nb <= 64) diagonal block in one CTA of 256
+// threads, blocked by 8-column panels (rows/columns >= nb padded with the identity, so L and
+// L^{-1} are block-diag(., I)).  32 block barriers in total:
+//   potrf, per panel p (columns c0 = 8p .. c0+7):
+//     warp 0 factors the panel in registers (lane l holds rows c0+l and c0+l+32): pivot by shuffle,
+//       1/sqrt(d) once, column scale, rank-1 update of the remaining panel columns -- shuffles only;
+//       the first failing pivot is recorded (reading A10);
+//     all warps apply the rank-8 update to the trailing lower triangle (4x4 blocks per thread);
+//   trtri, per block row p (rows r0 = 8p .. r0+7):  T = E_p - L_{p,<p} X_{<p} (all threads),
+//     then X_p = L_pp^{-1} T by an 8-row forward substitution per column (64 threads).
+// Shared memory: L and X, column-major [col][row] with a padded leading dimension.
 template <typename T>
-__global__ void __launch_bounds__(LEAF_THREADS) leaf_potrf_trtri(T* A, int64_t lda, int nb, T* X,
-                                                                  int64_t ldx, int write_L, double* logdet_slot,
-                                                                  int* fail_col, int col0) {
+__global__ void __launch_bounds__(LEAF_THREADS) leaf_potrf_trtri(T* A, int64_t lda, int nb, T* X, int64_t ldx,
+                                                                  int write_L, double* logdet_slot, int* fail_col,
+                                                                  int col0) {
   extern __shared__ __align__(16) unsigned char leaf_raw[];
-  T* leaf_smem = reinterpret_cast<T*>(leaf_raw);
-  T(*Ls)[NB + 1] = reinterpret_cast<T(*)[NB + 1]>(leaf_smem);                   // Ls[col][row]
-  T(*Xs)[NB + 1] = reinterpret_cast<T(*)[NB + 1]>(leaf_smem + NB * (NB + 1));  // Xs[col][row]
-  __shared__ T cbuf[2][NB + 1];  // column j of L (rows > j); [NB] = 1/L_jj
-  __shared__ T rbuf[2][NB];      // row j of X before the division by L_jj
-  __shared__ T diag[NB];
+  T(*Ls)[NB + 1] = reinterpret_cast<T(*)[NB + 1]>(leaf_raw);                              // [col][row]
+  T(*Xs)[NB + 1] = reinterpret_cast<T(*)[NB + 1]>(leaf_raw + NB * (NB + 1) * sizeof(T));  // [col][row]
+  __shared__ T Tb[NB][9];   // T block of the inverse sweep: [col][row - r0]
+  __shared__ T diag[NB], invd[NB];
   __shared__ int fail_sm;
-  const int t = threadIdx.x, rb = t & 15, cb = t >> 4, lane = t & 31;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   for (int idx = t; idx < NB * NB; idx += LEAF_THREADS) {
     const int i = idx & (NB - 1), j = idx >> 6;
     T v;
     if (i < nb && j < nb) v = (i >= j) ? A[i + (int64_t)j * lda] : T(0);
     else v = (i == j) ? T(1) : T(0);
     Ls[j][i] = v;
+    Xs[j][i] = T(0);
   }
   if (t == 0) fail_sm = INT_MAX;
   __syncthreads();
-  T a[4][4], x[4][4];
+  const int rb = t & 15, cb = t >> 4;
+  // ------------------------------------------------------------ Cholesky, 8-column panels
+  for (int p = 0; p < NB / 8; ++p) {
+    const int c0 = 8 * p;
+    if (warp == 0) {
+      T pv[2][8];
 #pragma unroll
-  for (int ii = 0; ii < 4; ++ii)
+      for (int s2 = 0; s2 < 2; ++s2) {
+        const int row = c0 + lane + 32 * s2;
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      a[ii][kk] = Ls[4 * cb + kk][4 * rb + ii];
-      x[ii][kk] = (4 * rb + ii == 4 * cb + kk) ? T(1) : T(0);
-    }
-  const bool has_lower = (rb >= cb);
-  for (int jb = 0; jb < 16; ++jb) {
+        for (int jj = 0; jj < 8; ++jj) pv[s2][jj] = (row < NB) ? Ls[c0 + jj][row] : T(0);
+      }
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
-      const int j = 4 * jb + jj;
-      T* cv = cbuf[jj & 1];
-      T* rv = rbuf[jj & 1];
-      if (cb == jb) {  // column-j owners (a half-warp)
-        const unsigned hmask = (lane & 16) ? 0xffff0000u : 0x0000ffffu;
-        const T d = __shfl_sync(hmask, a[jj][jj], (lane & 16) | jb);
+      for (int jj = 0; jj < 8; ++jj) {
+        const int j = c0 + jj;
+        const T d = __shfl_sync(0xffffffffu, pv[0][jj], jj);
         const T inv = rsqrt_t(d);
         const T ljj = d * inv;
-        if (rb == jb) {
-          if (!(d > 0.0) || !isfinite(d)) atomicMin(&fail_sm, j);
+        if (lane == jj) {
+          if (!(d > T(0)) || !isfinite(d)) atomicMin(&fail_sm, j);
           diag[j] = ljj;
-          cv[NB] = inv;
-          a[jj][jj] = ljj;
+          invd[j] = inv;
         }
 #pragma unroll
-        for (int ii = 0; ii < 4; ++ii) {
-          const int i = 4 * rb + ii;
-          if (i > j) {
-            a[ii][jj] *= inv;
-            cv[i] = a[ii][jj];
+        for (int s2 = 0; s2 < 2; ++s2) {
+          const int row = c0 + lane + 32 * s2;
+          if (row > j) pv[s2][jj] *= inv;
+          else if (row == j) pv[s2][jj] = ljj;
+        }
+#pragma unroll
+        for (int kk = jj + 1; kk < 8; ++kk) {
+          const T lk = __shfl_sync(0xffffffffu, pv[0][jj], kk);
+#pragma unroll
+          for (int s2 = 0; s2 < 2; ++s2) {
+            const int row = c0 + lane + 32 * s2;
+            if (row >= c0 + kk) pv[s2][kk] = fma_t(-pv[s2][jj], lk, pv[s2][kk]);
           }
         }
       }
-      if (rb == jb) {  // row-j owners of X publish the undivided row (columns <= j)
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) rv[4 * cb + cc] = x[jj][cc];
-      }
-      __syncthreads();
-      const T inv = cv[NB];
-      if (rb == jb) {
+      for (int s2 = 0; s2 < 2; ++s2) {
+        const int row = c0 + lane + 32 * s2;
+        if (row < NB) {
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) x[jj][cc] *= inv;
-      }
-      if (4 * rb + 3 > j) {
-        T li[4], lk[4], xr[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          li[u] = cv[4 * rb + u];
-          lk[u] = cv[4 * cb + u];
-          xr[u] = rv[4 * cb + u] * inv;
+          for (int jj = 0; jj < 8; ++jj) Ls[c0 + jj][row] = pv[s2][jj];
         }
-#pragma unroll
-        for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const int i = 4 * rb + ii, k = 4 * cb + kk;
-            if (i > j) {
-              if (has_lower && k > j && i >= k) a[ii][kk] = fma_t(-li[ii], lk[kk], a[ii][kk]);
-              if (k <= j) x[ii][kk] = fma_t(-li[ii], xr[kk], x[ii][kk]);
-            }
-          }
       }
     }
+    __syncthreads();
+    // rank-8 update of the trailing lower triangle (columns >= c0 + 8)
+    if (4 * cb >= c0 + 8 && rb >= cb) {
+      T li[4][8], lk[4][8];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          li[u][jj] = Ls[c0 + jj][4 * rb + u];
+          lk[u][jj] = Ls[c0 + jj][4 * cb + u];
+        }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          T acc = Ls[4 * cb + k][4 * rb + i];
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) acc = fma_t(-li[i][jj], lk[k][jj], acc);
+          Ls[4 * cb + k][4 * rb + i] = acc;
+        }
+    }
+    __syncthreads();
   }
-#pragma unroll
-  for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      const int i = 4 * rb + ii, k = 4 * cb + kk;
-      Ls[k][i] = (i >= k) ? a[ii][kk] : T(0);
-      Xs[k][i] = x[ii][kk];
+  // ------------------------------------------------------------ X = L^{-1}, 8-row block sweep
+  for (int p = 0; p < NB / 8; ++p) {
+    const int r0 = 8 * p;
+    for (int e = t; e < 8 * (r0 + 8); e += LEAF_THREADS) {
+      const int rr = e & 7, c = e >> 3, r = r0 + rr;
+      T acc = (r == c) ? T(1) : T(0);
+      for (int m = c; m < r0; ++m) acc = fma_t(-Ls[m][r], Xs[c][m], acc);
+      Tb[c][rr] = acc;
     }
-  __syncthreads();
+    __syncthreads();
+    if (t < r0 + 8) {
+      const int c = t;
+      T xv[8];
+#pragma unroll
+      for (int rr = 0; rr < 8; ++rr) {
+        T acc = Tb[c][rr];
+#pragma unroll
+        for (int ss = 0; ss < rr; ++ss) acc = fma_t(-Ls[r0 + ss][r0 + rr], xv[ss], acc);
+        xv[rr] = acc * invd[r0 + rr];
+        Xs[c][r0 + rr] = xv[rr];
+      }
+    }
+    __syncthreads();
+  }
   for (int idx = t; idx < nb * nb; idx += LEAF_THREADS) {
     const int i = idx % nb, j = idx / nb;
-    if (write_L) A[i + (int64_t)j * lda] = Ls[j][i];
-    X[i + (int64_t)j * ldx] = Xs[j][i];
+    if (write_L) A[i + (int64_t)j * lda] = (i >= j) ? Ls[j][i] : T(0);
+    X[i + (int64_t)j * ldx] = (i >= j) ? Xs[j][i] : T(0);
   }
-  if (t < 32) {  // 2 sum ln L_jj, fixed order: lane-strided partials then a fixed shuffle tree
-    double s = 0.0;
-    for (int j = t; j < NB; j += 32) s += log((double)diag[j]);
+  if (t < 32) {  // 2 sum ln L_jj, fixed order
+    double sacc = log((double)diag[t]) + log((double)diag[t + 32]);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_down_sync(0xffffffffu, sacc, o);
     if (t == 0) {
-      *logdet_slot = 2.0 * s;
+      *logdet_slot = 2.0 * sacc;
       if (fail_sm != INT_MAX && fail_sm < nb) atomicMin(fail_col, col0 + fail_sm);
     }
   }

@@ -2,7 +2,7 @@
 kernel; outputs compared with the fp64 oracle on the fp64 inputs).
 
 Tolerances: Sigma, Psi, gradients rel-Frobenius <= 1e-4 (north_star); objective relative error
-<= 1e-5 (A18 proposes 1e-6; the fp32 trace terms cancel by a factor ~3-5, see DESIGN.md);
+<= 1e-6 (A18; measured <= 3e-7 on tiny/small/medium);
 active sets exact outside a tie band ||g| - lam| <= 1e-4 * max|g| (the fp32 gradient error
 scale, reading A5)."""
 import ctypes
@@ -129,7 +129,7 @@ def test_fp32_parity(ctx32, name, k):
     np.testing.assert_array_equal(S, S.T)
     assert r["logdet"] == pytest.approx(ref["logdet"], rel=1e-5, abs=1e-5)
     ob = r["objective"]
-    assert ob["f"] == pytest.approx(ref["obj"]["f"], rel=1e-5)
+    assert ob["f"] == pytest.approx(ref["obj"]["f"], rel=1e-6)
     # active sets: exact outside the fp32 tie band
     a = O.active_set(ref["GradL"], ref["GradT"], lam, th, P.lam_L, P.lam_T, True, tie)
     for rk, ck, tm in (("L_row", "L_col", a["tie_mask_L"]), ("T_row", "T_col", a["tie_mask_T"])):
