@@ -19,7 +19,8 @@ cggm_status cggm_test_gemm(cggm_ctx* ctx, int transA, int transB, int64_t M, int
 cggm_status cggm_test_gemm_f32(cggm_ctx* ctx, int transA, int transB, int64_t M, int64_t N, int64_t K,
                                const float* A, int64_t lda, const float* B, int64_t ldb,
                                float* C, int64_t ldc, double alpha, double beta, int flags);
-/* Force the GEMM CTA tile: bits 0-1: 0 = automatic, 1 = 128x128 (8 warps), 2 = 64x64 (4 warps);
+/* Force the GEMM CTA tile: bits 0-1: 0 = automatic (small shapes use the 32x32 direct-load kernel),
+ * 1 = 128x128 TMA (8 warps), 2 = 64x64 TMA (4 warps), 3 = automatic but K <= 256 small kernel only;
  * bit 2: never use the single 3-D TMA box for MN-inner operands (16-wide 2-D boxes instead). */
 cggm_status cggm_test_set_tile(cggm_ctx* ctx, int mode);
 /* FP64 tensor-pipe peak: independent DMMA.8x8x4 chains on 2 CTAs/SM for ~`seconds`; returns the

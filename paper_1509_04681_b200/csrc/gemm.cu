@@ -292,6 +292,95 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
 
 // MN-inner operand as a 3-D tensor {16 (x mod 16), K, X/16} with strides {ld*8, 128 B}: one TMA box
 // {16, 16, BX/16} fills the whole [x/16][k][x%16] tile.  Only when X % 16 == 0 (no read past X).
+// ------------------------------------------------------------------ small-shape GEMM
+// K <= 256 and min(M, N) <= 128 (the bottom of the Cholesky recursion: 64x64x64 products and
+// 64-column panel solves): latency, not throughput, bound.  32x32 CTA tiles (4x the CTAs of a
+// 64-tile), 4 warps with 16x16 warp tiles of DMMA.8x8x4, operands loaded directly with coalesced
+// global loads into padded shared memory (no tensor-map fetch / mbarrier prologue), the same
+// flags and epilogue semantics as the TMA kernels.
+constexpr int ST = 32;        // tile
+constexpr int SKC = 32;       // k chunk
+constexpr int SLD = ST + 4;   // padded row (conflict-free half-warp DMMA fragment loads)
+
+struct KParamsS {
+  int M, N, K, flags;
+  Epilogue epi;
+};
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(128) gemm_small_kernel(const double* __restrict__ A, int64_t lda,
+                                                          const double* __restrict__ B, int64_t ldb,
+                                                          const KParamsS P) {
+  __shared__ double As[SKC][SLD];
+  __shared__ double Bs[SKC][SLD];
+  const int m0 = blockIdx.y * ST, n0 = blockIdx.x * ST;
+  if ((P.flags & SYM_LOWER) && m0 + ST - 1 < n0) return;   // tile strictly above the diagonal
+  int kbeg = 0, kend = P.K;
+  if (P.flags & A_KGE_M) kbeg = max(kbeg, m0);
+  if (P.flags & B_KGE_N) kbeg = max(kbeg, n0);
+  if (P.flags & A_KLE_M) kend = min(kend, m0 + ST);
+  if (P.flags & B_KLE_N) kend = min(kend, n0 + ST);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int wm = warp >> 1, wn = warp & 1;
+  double acc[2][2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int kc = kbeg; kc < kend; kc += SKC) {
+    for (int idx = tid; idx < ST * SKC; idx += 128) {
+      // consecutive threads walk the contiguous dimension of each operand
+      int mm, kk;
+      if (TA) { kk = idx % SKC; mm = idx / SKC; } else { mm = idx % ST; kk = idx / ST; }
+      const int m = m0 + mm, k = kc + kk;
+      double v = 0.0;
+      if (m < P.M && k < kend) v = TA ? A[k + (int64_t)m * lda] : A[m + (int64_t)k * lda];
+      As[kk][mm] = v;
+      int nn;
+      if (TB) { nn = idx % ST; kk = idx / ST; } else { kk = idx % SKC; nn = idx / SKC; }
+      const int n = n0 + nn, k2 = kc + kk;
+      double w = 0.0;
+      if (n < P.N && k2 < kend) w = TB ? B[n + (int64_t)k2 * ldb] : B[k2 + (int64_t)n * ldb];
+      Bs[kk][nn] = w;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k4 = 0; k4 < SKC / 4; ++k4) {
+      double a[2], b[2];
+#pragma unroll
+      for (int f = 0; f < 2; ++f) {
+        a[f] = As[4 * k4 + t][16 * wm + 8 * f + g];
+        b[f] = Bs[4 * k4 + t][16 * wn + 8 * f + g];
+      }
+#pragma unroll
+      for (int fm = 0; fm < 2; ++fm)
+#pragma unroll
+        for (int fn = 0; fn < 2; ++fn) ptx::dmma_8x8x4(acc[fm][fn][0], acc[fm][fn][1], a[fm], b[fn]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int fm = 0; fm < 2; ++fm)
+#pragma unroll
+    for (int fn = 0; fn < 2; ++fn)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int m = m0 + 16 * wm + 8 * fm + g, n = n0 + 16 * wn + 8 * fn + 2 * t + j;
+        if (m >= P.M || n >= P.N) continue;
+        if ((P.flags & SYM_LOWER) && m < n) continue;
+        epi_apply(P.epi, m, n, acc[fm][fn][j]);
+        if ((P.flags & SYM_MIRROR) && m > n) epi_apply(P.epi, n, m, acc[fm][fn][j]);
+      }
+}
+
+template <bool TA, bool TB>
+void launch_small(Ctx* c, const double* A, int64_t lda, const double* B, int64_t ldb, const KParamsS& P) {
+  dim3 grid((unsigned)((P.N + ST - 1) / ST), (unsigned)((P.M + ST - 1) / ST));
+  Prof pr(c, c->cur_tag);
+  gemm_small_kernel<TA, TB><<<grid, 128, 0, c->stream>>>(A, lda, B, ldb, P);
+  post_launch(c, "gemm_small_kernel");
+}
+
 CUtensorMap make_map_mn3d(Ctx* c, const double* ptr, int64_t ld, int64_t X, int64_t K, uint32_t bx) {
   CUtensorMap m;
   cuuint64_t dims[3] = {16, (cuuint64_t)K, (cuuint64_t)(X / 16)};
@@ -367,6 +456,20 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
   if (M <= 0 || N <= 0) return;
   if (M > (1LL << 30) || N > (1LL << 30) || K > (1LL << 30))
     throw CudaError{CGGM_ERR_UNSUPPORTED, "gemm dimension too large"};
+  if ((flags & SYM_LOWER) && (M < N || ((flags & SYM_MIRROR) && M != N)))
+    throw CudaError{CGGM_ERR_SHAPE, "SYM_LOWER gemm needs M >= N (M == N with SYM_MIRROR)"};
+  // (an output aliasing an operand -- an in-place B := B X^T with N <= 64 -- needs one CTA per row
+  // panel, which only the TMA kernels guarantee)
+  const bool aliased = epi.out1 == A || epi.out1 == B || (epi.out2 && (epi.out2 == A || epi.out2 == B));
+  if (K <= 256 && (M <= 128 || N <= 128) && !aliased && c->force_tile != 1 && c->force_tile != 2) {
+    KParamsS S;
+    S.M = (int)M; S.N = (int)N; S.K = (int)(K > 0 ? K : 0); S.flags = flags; S.epi = epi;
+    if (transA && transB) launch_small<true, true>(c, A, lda, B, ldb, S);
+    else if (transA) launch_small<true, false>(c, A, lda, B, ldb, S);
+    else if (transB) launch_small<false, true>(c, A, lda, B, ldb, S);
+    else launch_small<false, false>(c, A, lda, B, ldb, S);
+    return;
+  }
   static double* dummy = nullptr;
   if (K <= 0) {
     if (!dummy) CGGM_CUDA_CHECK(cudaMalloc(&dummy, 16 * 16 * 8));

@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 A_KLE_M, A_KGE_M, B_KLE_N, B_KGE_N, SYM_LOWER, SYM_MIRROR = 1, 2, 4, 8, 16, 32
 
 
-@pytest.fixture(scope="module", params=[1, 2, 5, 6], ids=["tile128", "tile64", "tile128_2d", "tile64_2d"])
+@pytest.fixture(scope="module", params=[0, 1, 2, 5, 6], ids=["auto_small", "tile128", "tile64", "tile128_2d", "tile64_2d"])
 def ctx(request):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -43,7 +43,7 @@ def run(ctx, tA, tB, A, B, C0, alpha, beta, flags, M, N, K):
 @pytest.mark.parametrize("tA", [False, True])
 @pytest.mark.parametrize("tB", [False, True])
 @pytest.mark.parametrize("M,N,K", [(1, 1, 1), (37, 45, 29), (128, 128, 16), (300, 260, 171), (513, 129, 1000),
-                                   (320, 208, 96), (256, 64, 300)])
+                                   (320, 208, 96), (256, 64, 300), (1064, 64, 64), (64, 1064, 200), (100, 90, 256)])
 def test_gemm_variants(ctx, tA, tB, M, N, K):
     rng = np.random.default_rng(M * 7 + N * 3 + K)
     A = rng.standard_normal((K, M) if tA else (M, K))
@@ -60,7 +60,7 @@ def test_gemm_k_zero(ctx):
     np.testing.assert_array_equal(out, 2.0 * C0)
 
 
-@pytest.mark.parametrize("q,K", [(200, 57), (385, 300)])
+@pytest.mark.parametrize("q,K", [(200, 57), (385, 300), (100, 40), (128, 256)])
 def test_gemm_sym_lower_mirror(ctx, q, K):
     rng = np.random.default_rng(q)
     A = rng.standard_normal((K, q))
@@ -80,7 +80,7 @@ def test_gemm_triangular_k_range(ctx, flags):
     """Triangular operands with exact zeros outside the triangle: the shortened k-range must
     give the full product."""
     rng = np.random.default_rng(flags)
-    n = 333
+    n = 333 if flags != A_KLE_M else 120
     A = rng.standard_normal((n, n))
     B = rng.standard_normal((n, n))
     # op(A)[m][k] zero for k > m (A_KLE_M) etc.; no transposes here
@@ -132,5 +132,31 @@ def test_gemm_lower_trapezoid(ctx):
     out = run(ctx, False, True, A, A[:N].copy(), C0, -1.0, 1.0, SYM_LOWER, M, N, K)
     ref = C0 - A @ A[:N].T
     mask = np.tril(np.ones((M, N), dtype=bool))
+    np.testing.assert_allclose(out[mask], ref[mask], rtol=1e-12, atol=1e-12)
+    np.testing.assert_array_equal(out[~mask], C0[~mask])
+
+
+@pytest.mark.parametrize("flags", [1, 2, 4, 8, 10])
+def test_gemm_small_triangular(ctx, flags):
+    """Small-shape path (K <= 256): triangular k-ranges on 32-wide tiles."""
+    rng = np.random.default_rng(100 + flags)
+    n = 120
+    A = rng.standard_normal((n, n))
+    B = rng.standard_normal((n, n))
+    A = np.tril(A) if flags & 1 else np.triu(A) if flags & 2 else A
+    B = np.triu(B) if flags & 4 else np.tril(B) if flags & 8 else B
+    out = run(ctx, False, False, A, B, np.zeros((n, n)), 1.0, 0.0, flags, n, n, n)
+    assert np.linalg.norm(out - A @ B) / np.linalg.norm(A @ B) < 1e-14
+
+
+def test_gemm_small_trapezoid_inplace_update(ctx):
+    """C -= A A^T over the lower trapezoid with C also the epilogue input (Cholesky update)."""
+    rng = np.random.default_rng(77)
+    N, extra, K = 64, 1000, 64
+    A = rng.standard_normal((N + extra, K))
+    C0 = rng.standard_normal((N + extra, N))
+    out = run(ctx, False, True, A, A[:N].copy(), C0, -1.0, 1.0, SYM_LOWER, N + extra, N, K)
+    mask = np.tril(np.ones((N + extra, N), dtype=bool))
+    ref = C0 - A @ A[:N].T
     np.testing.assert_allclose(out[mask], ref[mask], rtol=1e-12, atol=1e-12)
     np.testing.assert_array_equal(out[~mask], C0[~mask])
