@@ -61,6 +61,16 @@ def _hbm_peak():
 HBM_PEAK_GBS = _hbm_peak()
 
 
+def _dominant_traffic():
+    """dram read+write bytes per launch of the largest GEMM launch (lauum), from the committed ncu
+    --set full capture (profiles/r01_ncu_dominant.json); None if absent."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_dominant.json")))
+        return d["dram_read_bytes"] + d["dram_write_bytes"]
+    except Exception:
+        return None
+
+
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -411,7 +421,7 @@ def main():
             "gpu_launches": launches,
             "roofline": {"bound": "tensor", "kernel": "gemm_dmma_kernel (FP64 DMMA.8x8x4, all dense contractions)",
                          "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
-                         "frac": achieved / peak_tflops, "traffic": None,
+                         "frac": achieved / peak_tflops, "traffic": _dominant_traffic(),
                          "peak_source": f"live DMMA.8x8x4 microbenchmark on this GPU ({args.peak_seconds:.1f} s, "
                                         "2 CTAs/SM); MEASURED_PEAKS.json has no FP64 entry",
                          "gemm_ms_per_step": gemm_ms, "gemm_alg_flops_per_step": gemm_flops,
