@@ -151,7 +151,10 @@ cggm_status cggm_invert_logdet(cggm_ctx* ctx, const cggm_csc* Lambda, void* Sigm
  * S_xx Theta Sigma is X^T R / sqrt(n): S_xx is never formed (north_star (1)).  With
  * n_local < n_total, Psi and GradT (Sxy == NULL) are this shard's partial sums and GradL must be
  * NULL (form it after the all-reduce with cggm_grad_lambda).  If `fused` != NULL the active
- * sets are also built (same semantics as cggm_active_set; requires GradL and GradT). */
+ * sets are also built (same semantics as cggm_active_set; requires GradL).  With fused != NULL
+ * and GradT == NULL, grad_Theta is STREAMED: computed in column chunks into library workspace
+ * and compacted into S_Theta immediately, never stored (the p x q gradient is 64 GB at the
+ * `sharded` size). */
 cggm_status cggm_psi_grad(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64_t p, int64_t q,
                           const void* X, int64_t ldx, const void* Y, int64_t ldy, const cggm_csc* Theta,
                           const void* Sigma, int64_t ldsigma, const void* Syy, int64_t ldsyy,
@@ -192,7 +195,8 @@ cggm_status cggm_objective(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int6
  * objective's fresh trial Cholesky (the line-search PD test) executed on a library
  * auxiliary stream concurrently with Sigma = Lambda^{-1} and the Psi / gradient / active-set work
  * on the ctx stream.  Inputs as in those calls (Syy from cggm_covariances); active->lam_L, lam_T,
- * penalize_diag are also the objective's.  One host synchronisation at the end; on
+ * penalize_diag are also the objective's.  GradT may be NULL: grad_Theta is then streamed into
+ * the active-set compaction and not stored (see cggm_psi_grad).  One host synchronisation at the end; on
  * CGGM_ERR_CAPACITY all other outputs are valid and the list contents are unspecified. */
 typedef struct cggm_eval_out {
   double logdet;            /* log|Lambda| from the inverse's factorisation (NaN if not PD) */

@@ -274,16 +274,22 @@ class Context:
 
     # ---------------------------------------------------------------- composite
     def cggm_newton_eval(self, X, Y, Syy, Lam: DeviceCsc, Theta: DeviceCsc, lam_L, lam_T, penalize_diag=True,
-                         tie_eps=1e-9, bufs=None):
-        """One Newton-iteration evaluation in one call (objective overlapped on an internal stream)."""
+                         tie_eps=1e-9, bufs=None, stream_grad_theta=False):
+        """One Newton-iteration evaluation in one call (objective overlapped on an internal stream).
+        stream_grad_theta: do not store the p x q grad_Theta (it is compacted chunk by chunk)."""
         self._sync_stream()
         n, p = X.shape
         q = Y.shape[1]
         dev = X.device
         bufs = bufs if bufs is not None else {}
-        for k, shape in (("Sigma", (q, q)), ("Psi", (q, q)), ("GradL", (q, q)), ("GradT", (p, q))):
+        shapes = [("Sigma", (q, q)), ("Psi", (q, q)), ("GradL", (q, q))]
+        if not stream_grad_theta:
+            shapes.append(("GradT", (p, q)))
+        for k, shape in shapes:
             if bufs.get(k) is None:
                 bufs[k] = colmajor_empty(*shape, device=dev, dtype=self.tdtype)
+        if stream_grad_theta:
+            bufs["GradT"] = None
         spec = dict(lam_L=lam_L, lam_T=lam_T, penalize_diag=int(bool(penalize_diag)), tie_eps=tie_eps,
                     L_row=bufs.get("L_row"), L_col=bufs.get("L_col"), T_row=bufs.get("T_row"), T_col=bufs.get("T_col"))
         ao = self._active_struct(spec)
@@ -292,8 +298,8 @@ class Context:
         self._check(self.lib.cggm_newton_eval(
             self.h, n, p, q, _ptr(X), ld_of(X), _ptr(Y), ld_of(Y), _ptr(Syy), ld_of(Syy), ctypes.byref(ls),
             ctypes.byref(ts), _ptr(bufs["Sigma"]), ld_of(bufs["Sigma"]), _ptr(bufs["Psi"]), ld_of(bufs["Psi"]),
-            _ptr(bufs["GradL"]), ld_of(bufs["GradL"]), _ptr(bufs["GradT"]), ld_of(bufs["GradT"]),
-            ctypes.byref(ao), ctypes.byref(eo)))
+            _ptr(bufs["GradL"]), ld_of(bufs["GradL"]), _ptr(bufs["GradT"]),
+            ld_of(bufs["GradT"]) if bufs["GradT"] is not None else 1, ctypes.byref(ao), ctypes.byref(eo)))
         o = eo.obj
         ob = dict(f=o.f, g=o.g, logdet=o.logdet, tr_syy_lam=o.tr_syy_lam, tr_sxy_theta=o.tr_sxy_theta,
                   tr_sigma_m=o.tr_sigma_m, pen_L=o.pen_L, pen_T=o.pen_T, is_pd=bool(o.is_pd), fail_col=int(o.fail_col))
@@ -303,13 +309,14 @@ class Context:
 
 
 def newton_evaluation(ctx: Context, X, Y, Syy, Lam: DeviceCsc, Theta: DeviceCsc, lam_L, lam_T, penalize_diag=True,
-                      bufs=None, tie_eps=1e-9, composite=True):
+                      bufs=None, tie_eps=1e-9, composite=True, stream_grad_theta=False):
     """One Newton-iteration evaluation (the metric's unit): invert_logdet(Lambda),
     psi_grad (+ fused active sets), objective at Lambda_trial = Lambda with its own Cholesky.
     composite=True uses the single overlapped call cggm_newton_eval; False issues the separate calls."""
     bufs = bufs if bufs is not None else {}
     if composite:
-        return ctx.cggm_newton_eval(X, Y, Syy, Lam, Theta, lam_L, lam_T, penalize_diag, tie_eps, bufs)
+        return ctx.cggm_newton_eval(X, Y, Syy, Lam, Theta, lam_L, lam_T, penalize_diag, tie_eps, bufs,
+                                    stream_grad_theta=stream_grad_theta)
     Sigma, logdet, pd, fc = ctx.cggm_invert_logdet(Lam, Sigma=bufs.get("Sigma"))
     spec = dict(lam_L=lam_L, lam_T=lam_T, penalize_diag=int(bool(penalize_diag)), tie_eps=tie_eps,
                 L_row=bufs["L_row"], L_col=bufs["L_col"], T_row=bufs["T_row"], T_col=bufs["T_col"])

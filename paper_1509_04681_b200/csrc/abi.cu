@@ -449,18 +449,28 @@ cggm_status cggm_active_set(cggm_ctx* ctx, int64_t p, int64_t q, const void* Gra
 
 // ------------------------------------------------------------------ a2/a4/a5
 // W (n_local x q, ldw) must already hold X Theta.
+// Active sets built inside psi_enqueue (fused).  With GradT == NULL the p x q grad_Theta is streamed:
+// computed in column chunks into a workspace buffer and compacted immediately (never stored).
+struct Fuse {
+  const cggm_csc* Lambda;
+  const cggm_csc* Theta;
+  const cggm_active_out* o;
+  ActWs ws;
+};
+constexpr int64_t GT_CHUNK = 2048;
+
 template <typename T>
 static void psi_enqueue(Ctx* c, int64_t n_local, int64_t n_total, int64_t p, int64_t q, const T* Xd, int64_t ldx,
                         const T* Yd, int64_t ldy, const T* W, int64_t ldw, const T* Sg, int64_t ldsigma, const T* Syy,
                         int64_t ldsyy, const T* Sxy, int64_t ldsxy, T* Psi, int64_t ldpsi, T* GradL, int64_t ldgl,
-                        T* GradT, int64_t ldgt) {
+                        T* GradT, int64_t ldgt, const Fuse* fz) {
   const int64_t ldn = pad_ld<T>(n_local > 0 ? n_local : 1);
   T* R = static_cast<T*>(ws_get(c, WS_R, (size_t)ldn * q * sizeof(T)));
   T* E = static_cast<T*>(ws_get(c, WS_E, (size_t)ldn * q * sizeof(T)));
   {  // a4: acc = W Sigma -> R = acc / sqrt(n), E = Y + acc
     Phase ph(c, TAG_WSIGMA);
     EpilogueT<T> e; e.out1 = R; e.ld1 = ldn; e.a1 = 1.0 / std::sqrt((double)n_total);
-    if (GradT && !Sxy) { e.out2 = E; e.ld2 = ldn; e.a2 = 1.0; e.in2a = Yd; e.ld2a = ldy; e.b2 = 1.0; }
+    if ((GradT || fz) && !Sxy) { e.out2 = E; e.ld2 = ldn; e.a2 = 1.0; e.in2a = Yd; e.ld2a = ldy; e.b2 = 1.0; }
     gemm(c, false, false, n_local, q, q, W, ldw, Sg, ldsigma, e, 0);
   }
   {  // a4/a5: Psi = R^T R (mirrored), then grad_Lambda = (S_yy - Sigma) - Psi as one streaming pass
@@ -472,17 +482,47 @@ static void psi_enqueue(Ctx* c, int64_t n_local, int64_t n_total, int64_t p, int
       grad_lambda(c, q, Syy, ldsyy, Sg, ldsigma, Psi, ldpsi, GradL, ldgl);
     }
   }
-  if (GradT) {  // a5: GradT = (2/n) X^T E   (or 2 S_xy + (2/sqrt n) X^T R)
+  const cggm_active_out* o = fz ? fz->o : nullptr;
+  if (fz) {
+    Phase ph(c, TAG_ACTIVE);
+    active_begin(c, q, fz->ws);
+    active_lambda<T>(c, q, GradL, ldgl, fz->Lambda, o->lam_L, o->penalize_diag, o->tie_eps, fz->ws, o->L_row,
+                     o->L_col, o->cap_L);
+  }
+  // a5: GradT = (2/n) X^T E   (or 2 S_xy + (2/sqrt n) X^T R), columns [j0, j0 + nc) into `out`
+  auto grad_theta = [&](int64_t j0, int64_t nc, T* out, int64_t ldo) {
     Phase ph(c, TAG_GRADT);
-    EpilogueT<T> e; e.out1 = GradT; e.ld1 = ldgt;
+    EpilogueT<T> e; e.out1 = out; e.ld1 = ldo;
     if (!Sxy) {
       e.a1 = 2.0 / (double)n_total;
-      gemm(c, true, false, p, q, n_local, Xd, ldx, E, ldn, e, 0);
+      gemm(c, true, false, p, nc, n_local, Xd, ldx, E + j0 * ldn, ldn, e, 0);
     } else {
       e.a1 = 2.0 / std::sqrt((double)n_total);
-      e.in1a = Sxy; e.ld1a = ldsxy; e.b1 = 2.0;
-      gemm(c, true, false, p, q, n_local, Xd, ldx, R, ldn, e, 0);
+      e.in1a = Sxy + j0 * ldsxy; e.ld1a = ldsxy; e.b1 = 2.0;
+      gemm(c, true, false, p, nc, n_local, Xd, ldx, R + j0 * ldn, ldn, e, 0);
     }
+  };
+  if (GradT) {
+    grad_theta(0, q, GradT, ldgt);
+    if (fz) {
+      Phase ph(c, TAG_ACTIVE);
+      active_theta_chunk<T>(c, p, 0, q, GradT, ldgt, fz->Theta, o->lam_T, o->tie_eps, fz->ws, o->T_row, o->T_col,
+                            o->cap_T);
+    }
+  } else if (fz) {
+    const int64_t ldc = pad_ld<T>(p);
+    T* chunk = static_cast<T*>(ws_get(c, WS_GTCHUNK, (size_t)ldc * std::min<int64_t>(GT_CHUNK, q) * sizeof(T)));
+    for (int64_t j0 = 0; j0 < q; j0 += GT_CHUNK) {
+      const int64_t nc = std::min<int64_t>(GT_CHUNK, q - j0);
+      grad_theta(j0, nc, chunk, ldc);
+      Phase ph(c, TAG_ACTIVE);
+      active_theta_chunk<T>(c, p, j0, nc, chunk, ldc, fz->Theta, o->lam_T, o->tie_eps, fz->ws, o->T_row, o->T_col,
+                            o->cap_T);
+    }
+  }
+  if (fz) {
+    Phase ph(c, TAG_ACTIVE);
+    active_end(c, q, fz->ws);
   }
 }
 
@@ -509,7 +549,7 @@ cggm_status cggm_psi_grad(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64
     if (Sxy && n_local != n_total) fail(CGGM_ERR_INVALID_ARG, "the S_xy route is not a per-shard partial sum");
     if (fused) {
       check_active_args(fused);
-      if (!GradL || !GradT) fail(CGGM_ERR_INVALID_ARG, "fused active sets need GradL and GradT");
+      if (!GradL) fail(CGGM_ERR_INVALID_ARG, "fused active sets need GradL");
       check_csc_host("Lambda", Lambda, q, q);
     }
     if (q == 0) return;
@@ -521,13 +561,12 @@ cggm_status cggm_psi_grad(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64
       const int64_t ldn = pad_ld<T>(n_local > 0 ? n_local : 1);
       T* W = static_cast<T*>(ws_get(c, WS_W, (size_t)ldn * q * sizeof(T)));
       spmm_x_theta<T>(c, static_cast<const T*>(X), ldx, n_local, Theta, ViewT<T>{W, ldn, n_local, q});
+      Fuse fz{Lambda, Theta, fused, fused ? active_ws(c, q) : ActWs{}};
       psi_enqueue<T>(c, n_local, n_total, p, q, static_cast<const T*>(X), ldx, static_cast<const T*>(Y), ldy, W, ldn,
                      static_cast<const T*>(Sigma), ldsigma, static_cast<const T*>(Syy), ldsyy,
                      static_cast<const T*>(Sxy), ldsxy, static_cast<T*>(Psi), ldpsi, static_cast<T*>(GradL), ldgl,
-                     static_cast<T*>(GradT), ldgt);
-      if (fused)
-        tot = active_enqueue<T>(c, p, q, static_cast<const T*>(GradL), ldgl, static_cast<const T*>(GradT), ldgt,
-                                Lambda, Theta, fused);
+                     static_cast<T*>(GradT), ldgt, fused ? &fz : nullptr);
+      if (fused) tot = fz.ws.tot;
     });
     if (fused) active_sync(c, tot, fused);
   });
@@ -691,7 +730,7 @@ cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, con
     check_dense("Sigma", Sigma, q, q, ldsigma);
     check_dense("Psi", Psi, q, q, ldpsi);
     check_dense("GradL", GradL, q, q, ldgl);
-    check_dense("GradT", GradT, p, q, ldgt);
+    check_dense("GradT", GradT, p, q, ldgt, false);
     check_csc_host("Lambda", Lambda, q, q);
     check_csc_host("Theta", Theta, p, q);
     check_active_args(active);
@@ -724,6 +763,7 @@ cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, con
       active_ws(c, q);
       ws_get(c, WS_R, (size_t)ldn * q * es);
       ws_get(c, WS_E, (size_t)ldn * q * es);
+      if (!GradT) ws_get(c, WS_GTCHUNK, (size_t)pad_ld<T>(p) * std::min<int64_t>(GT_CHUNK, q) * es);
       T* W = static_cast<T*>(ws_get(c, WS_W, (size_t)ldn * q * es));
       const T* Xd = static_cast<const T*>(X);
       const T* Yd = static_cast<const T*>(Y);
@@ -746,11 +786,11 @@ cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, con
       }
       // a3, a4/a5, a6 on the caller's stream (lane 0)
       invert_enqueue<T>(c, 0, Lambda, static_cast<T*>(Sigma), ldsigma);
+      Fuse fz{Lambda, Theta, active, active_ws(c, q)};
       psi_enqueue<T>(c, n, n, p, q, Xd, ldx, Yd, ldy, W, ldn, static_cast<const T*>(Sigma), ldsigma,
                      static_cast<const T*>(Syy), ldsyy, nullptr, 0, static_cast<T*>(Psi), ldpsi,
-                     static_cast<T*>(GradL), ldgl, static_cast<T*>(GradT), ldgt);
-      tot = active_enqueue<T>(c, p, q, static_cast<const T*>(GradL), ldgl, static_cast<const T*>(GradT), ldgt, Lambda,
-                              Theta, active);
+                     static_cast<T*>(GradL), ldgl, static_cast<T*>(GradT), ldgt, &fz);
+      tot = fz.ws.tot;
     });
     CGGM_CUDA_CHECK(cudaStreamWaitEvent(s0, c->ev_join, 0));
     char* h = static_cast<char*>(c->host_scratch);

@@ -53,9 +53,9 @@ __global__ void __launch_bounds__(NT) k_active_onepass(int64_t nrows, const T* _
                                                        T lam, int penalize_diag, T tie_eps,
                                                        unsigned long long* state, int32_t* out_row,
                                                        int32_t* out_col, long long cap, long long* ties_col,
-                                                       double* sub_col) {
+                                                       double* sub_col, int64_t col0) {
   extern __shared__ uint32_t sm[];
-  const int64_t j = blockIdx.x;
+  const int64_t j = col0 + blockIdx.x;   // G holds columns col0 .. (a chunk of the gradient)
   const int64_t scan_rows = LAM ? j + 1 : nrows;
   const int64_t nwords = (scan_rows + 31) >> 5;
   uint32_t* sup_bits = sm;
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(NT) k_active_onepass(int64_t nrows, const T* _
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int64_t a, b;
   segment(scan_rows, w, a, b);
-  const T* gc = G + j * ldg;
+  const T* gc = G + (j - col0) * ldg;
   int cnt = 0;
   long long tc = 0;
   double s = 0.0;
@@ -233,30 +233,40 @@ ActWs active_ws(Ctx* c, int64_t q) {
   return w;
 }
 
+void active_begin(Ctx* c, int64_t q, const ActWs& ws) {
+  if (q > 0) CGGM_CUDA_CHECK(cudaMemsetAsync(ws.stateL, 0, (size_t)q * 2 * 8, c->stream));
+}
+
 template <typename T>
-void active_compact(Ctx* c, int64_t p, int64_t q, const T* GradL, int64_t ldgl, const T* GradT, int64_t ldgt,
-                    const cggm_csc* Lambda, const cggm_csc* Theta, double lam_L, double lam_T, int penalize_diag,
-                    double tie_eps, const ActWs& ws, int32_t* L_row, int32_t* L_col, int32_t* T_row, int32_t* T_col,
-                    long long capL, long long capT) {
+void active_lambda(Ctx* c, int64_t q, const T* GradL, int64_t ldgl, const cggm_csc* Lambda, double lam_L,
+                   int penalize_diag, double tie_eps, const ActWs& ws, int32_t* L_row, int32_t* L_col,
+                   long long capL) {
   if (q == 0) return;
-  CGGM_CUDA_CHECK(cudaMemsetAsync(ws.stateL, 0, (size_t)q * 2 * 8, c->stream));
-  const size_t bl = smem_bytes(q), bt = smem_bytes(p);
+  const size_t bl = smem_bytes(q);
   set_smem(k_active_onepass<true, T>, bl);
+  Prof pr(c, TAG_ACTIVE);
+  k_active_onepass<true, T><<<(unsigned)q, NT, bl, c->stream>>>(
+      q, GradL, ldgl, Lambda->colptr, Lambda->rowidx, static_cast<const T*>(Lambda->val), (T)lam_L, penalize_diag,
+      (T)tie_eps, ws.stateL, L_row, L_col, capL, ws.tieL, ws.subL, 0);
+  post_launch(c, "k_active_onepass<L>");
+}
+
+template <typename T>
+void active_theta_chunk(Ctx* c, int64_t p, int64_t col0, int64_t ncols, const T* G, int64_t ldg,
+                        const cggm_csc* Theta, double lam_T, double tie_eps, const ActWs& ws, int32_t* T_row,
+                        int32_t* T_col, long long capT) {
+  if (ncols == 0) return;
+  const size_t bt = smem_bytes(p);
   set_smem(k_active_onepass<false, T>, bt);
-  {
-    Prof pr(c, TAG_ACTIVE);
-    k_active_onepass<true, T><<<(unsigned)q, NT, bl, c->stream>>>(
-        q, GradL, ldgl, Lambda->colptr, Lambda->rowidx, static_cast<const T*>(Lambda->val), (T)lam_L, penalize_diag,
-        (T)tie_eps, ws.stateL, L_row, L_col, capL, ws.tieL, ws.subL);
-    post_launch(c, "k_active_onepass<L>");
-  }
-  {
-    Prof pr(c, TAG_ACTIVE);
-    k_active_onepass<false, T><<<(unsigned)q, NT, bt, c->stream>>>(
-        p, GradT, ldgt, Theta->colptr, Theta->rowidx, static_cast<const T*>(Theta->val), (T)lam_T, 1, (T)tie_eps,
-        ws.stateT, T_row, T_col, capT, ws.tieT, ws.subT);
-    post_launch(c, "k_active_onepass<T>");
-  }
+  Prof pr(c, TAG_ACTIVE);
+  k_active_onepass<false, T><<<(unsigned)ncols, NT, bt, c->stream>>>(
+      p, G, ldg, Theta->colptr, Theta->rowidx, static_cast<const T*>(Theta->val), (T)lam_T, 1, (T)tie_eps,
+      ws.stateT, T_row, T_col, capT, ws.tieT, ws.subT, col0);
+  post_launch(c, "k_active_onepass<T>");
+}
+
+void active_end(Ctx* c, int64_t q, const ActWs& ws) {
+  if (q == 0) return;
   {
     Prof pr(c, TAG_ACTIVE);
     k_active_totals<<<1, TOT_NT, 0, c->stream>>>(q, ws.stateL, ws.tieL, ws.subL, &ws.tot->m_L, &ws.tot->ties_L,
@@ -271,11 +281,31 @@ void active_compact(Ctx* c, int64_t p, int64_t q, const T* GradL, int64_t ldgl, 
   }
 }
 
+template <typename T>
+void active_compact(Ctx* c, int64_t p, int64_t q, const T* GradL, int64_t ldgl, const T* GradT, int64_t ldgt,
+                    const cggm_csc* Lambda, const cggm_csc* Theta, double lam_L, double lam_T, int penalize_diag,
+                    double tie_eps, const ActWs& ws, int32_t* L_row, int32_t* L_col, int32_t* T_row, int32_t* T_col,
+                    long long capL, long long capT) {
+  if (q == 0) return;
+  active_begin(c, q, ws);
+  active_lambda<T>(c, q, GradL, ldgl, Lambda, lam_L, penalize_diag, tie_eps, ws, L_row, L_col, capL);
+  active_theta_chunk<T>(c, p, 0, q, GradT, ldgt, Theta, lam_T, tie_eps, ws, T_row, T_col, capT);
+  active_end(c, q, ws);
+}
+
 template void active_compact<double>(Ctx*, int64_t, int64_t, const double*, int64_t, const double*, int64_t,
                                      const cggm_csc*, const cggm_csc*, double, double, int, double, const ActWs&,
                                      int32_t*, int32_t*, int32_t*, int32_t*, long long, long long);
 template void active_compact<float>(Ctx*, int64_t, int64_t, const float*, int64_t, const float*, int64_t,
                                     const cggm_csc*, const cggm_csc*, double, double, int, double, const ActWs&,
                                     int32_t*, int32_t*, int32_t*, int32_t*, long long, long long);
+#define CGGM_INST(T)                                                                                          \
+  template void active_lambda<T>(Ctx*, int64_t, const T*, int64_t, const cggm_csc*, double, int, double,      \
+                                 const ActWs&, int32_t*, int32_t*, long long);                                 \
+  template void active_theta_chunk<T>(Ctx*, int64_t, int64_t, int64_t, const T*, int64_t, const cggm_csc*,     \
+                                      double, double, const ActWs&, int32_t*, int32_t*, long long);
+CGGM_INST(double)
+CGGM_INST(float)
+#undef CGGM_INST
 
 }  // namespace cggm

@@ -119,6 +119,7 @@ enum Slot {
   WS_DENSE_B,       // augmented [Lambda; W] of the objective on the auxiliary lane
   WS_XDIAG,         // objective: inverses of the <= 512-column diagonal blocks (q x 512)
   WS_TMP_OBJ,       // objective: recursion temporaries (full-inverse subtrees + block products)
+  WS_GTCHUNK,       // streamed grad_Theta column chunk (fused active sets without a stored p x q gradient)
   WS_SCAL2,         // scalar block of the auxiliary lane
   WS_NUM
 };

@@ -28,6 +28,19 @@ struct ActWs {
   ActTotals* tot;
 };
 ActWs active_ws(Ctx* c, int64_t q);
+// Building blocks of the single-pass compaction (one stream, in this order): begin (reset the
+// look-back states), the Lambda list, the Theta list in one or several column chunks in ascending
+// column order (G = the chunk's gradient columns col0 .. col0+ncols-1), end (totals).
+void active_begin(Ctx* c, int64_t q, const ActWs& ws);
+template <typename T>
+void active_lambda(Ctx* c, int64_t q, const T* GradL, int64_t ldgl, const cggm_csc* Lambda, double lam_L,
+                   int penalize_diag, double tie_eps, const ActWs& ws, int32_t* L_row, int32_t* L_col,
+                   long long capL);
+template <typename T>
+void active_theta_chunk(Ctx* c, int64_t p, int64_t col0, int64_t ncols, const T* G, int64_t ldg,
+                        const cggm_csc* Theta, double lam_T, double tie_eps, const ActWs& ws, int32_t* T_row,
+                        int32_t* T_col, long long capT);
+void active_end(Ctx* c, int64_t q, const ActWs& ws);
 // Single-pass ordered compaction of both lists + totals (device).  Entries at positions >= cap are
 // not written (the caller reports CGGM_ERR_CAPACITY from the totals).
 template <typename T>

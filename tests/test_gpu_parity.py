@@ -253,3 +253,27 @@ def test_composite_eval_matches_separate_calls(ctx, name, k):
         ref = oracle_point(name, k)
         assert relf(to_np(b["Sigma"]), ref["Sigma"]) <= REL_F
         assert b["objective"]["f"] == pytest.approx(ref["obj"]["f"], rel=REL_OBJ)
+
+
+def test_streamed_grad_theta_matches_stored(ctx):
+    """GradT = NULL: grad_Theta streamed in column chunks into the compaction (never stored) gives
+    the same lists / statistic as the stored gradient."""
+    from paper_1509_04681_b200 import DeviceCsc, to_device_colmajor
+    from paper_1509_04681_b200.api import newton_evaluation
+    P = problem("medium")   # q = 4000 > the 2048-column chunk: two chunks, look-back across them
+    label, lam, th = P.points[0]
+    X, Y = to_device_colmajor(P.X), to_device_colmajor(P.Y)
+    Lg, Tg = DeviceCsc.from_host(lam), DeviceCsc.from_host(th)
+    Syy, _ = ctx.cggm_covariances(X, Y, want_sxy=False)
+    cap = 4_000_000
+
+    def bufs():
+        return {k2: torch.empty(cap, dtype=torch.int32, device="cuda") for k2 in ("L_row", "L_col", "T_row", "T_col")}
+
+    a = newton_evaluation(ctx, X, Y, Syy, Lg, Tg, P.lam_L, P.lam_T, True, bufs())
+    b = newton_evaluation(ctx, X, Y, Syy, Lg, Tg, P.lam_L, P.lam_T, True, bufs(), stream_grad_theta=True)
+    assert b["GradT"] is None
+    for key in ("L_row", "L_col", "T_row", "T_col"):
+        assert torch.equal(a["active"][key], b["active"][key]), key
+    assert a["active"]["subgrad_l1"] == b["active"]["subgrad_l1"]
+    assert a["objective"]["f"] == b["objective"]["f"]

@@ -1,0 +1,115 @@
+"""Parity at BASELINE.json's full `sharded` size on ONE GPU (n = 4000, p = 200000, q = 40000;
+the 40000^2 Cholesky/inverse on one device), in the memory-lean configuration: grad_Theta (64 GB
+as a p x q matrix) is streamed into the active-set compaction, never stored.
+
+Lambda* is a random sparse SPD matrix, so there is no closed form for Sigma; the outputs are
+pinned by what holds at any size:
+  P7  Sigma Lambda = I on sampled columns;
+  I7  at the generating point Psi* = (Y-E)^T (Y-E)/n, grad_Lambda* = S_yy - Sigma - Psi*,
+      grad_Theta* = (2/n) X^T E (sampled columns; S_Theta / S_Lambda rows of those columns exact
+      outside the tie band);
+  I2  tr(Sigma Theta^T S_xx Theta) from the objective's augmented factorisation = <Lambda, Psi>;
+  the inverse's and the objective's factorisations give the same log-det.
+Generation of the inputs takes ~1-2 minutes of host time.  Set CGGM_TEST_SHARDED=0 to skip."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.slow,
+              pytest.mark.skipif(os.environ.get("CGGM_TEST_SHARDED", "1") == "0", reason="CGGM_TEST_SHARDED=0")]
+
+TIE = 1e-9
+COLS = [0, 1, 511, 512, 2047, 2048, 20000, 39999]
+
+
+@pytest.fixture(scope="module")
+def run_sharded():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.empty_cache()
+    free, total = torch.cuda.mem_get_info()
+    if free < 130e9:
+        pytest.skip(f"needs ~130 GB of free device memory, {free / 1e9:.0f} GB free")
+    from paper_1509_04681_b200 import Context, DeviceCsc, to_device_colmajor
+    from paper_1509_04681_b200.api import newton_evaluation
+    from synth.cggm_inputs import make_problem
+    P = make_problem("sharded")
+    ctx = Context(0)
+    X, Y = to_device_colmajor(P.X), to_device_colmajor(P.Y)
+    Lam, Th = DeviceCsc.from_host(P.lam_star), DeviceCsc.from_host(P.theta_star)
+    Syy, _ = ctx.cggm_covariances(X, Y, want_sxy=False)
+    cap = 30_000_000
+    bufs = {k: torch.empty(cap, dtype=torch.int32, device="cuda") for k in ("L_row", "L_col", "T_row", "T_col")}
+    res = newton_evaluation(ctx, X, Y, Syy, Lam, Th, P.lam_L, P.lam_T, True, bufs, tie_eps=TIE,
+                            stream_grad_theta=True)
+    torch.cuda.synchronize()
+    out = dict(logdet=res["logdet"], is_pd=res["is_pd"], objective=res["objective"], active=res["active"])
+    out["Sigma_cols"] = res["Sigma"][:, COLS].cpu().numpy()
+    out["Psi_cols"] = res["Psi"][:, COLS].cpu().numpy()
+    out["GradL_cols"] = res["GradL"][:, COLS].cpu().numpy()
+    # Sigma columns needed for (Sigma Lambda)[:, j] = sum_k Sigma[:, k] Lambda[k, j]
+    need = sorted({int(k) for j in COLS for k in P.lam_star.rowidx[P.lam_star.colptr[j]:P.lam_star.colptr[j + 1]]})
+    out["need"] = need
+    out["Sigma_need"] = res["Sigma"][:, need].cpu().numpy()
+    # Psi at the stored entries of Lambda (for I2)
+    rows = torch.as_tensor(P.lam_star.rowidx.astype(np.int64), device="cuda")
+    cols = torch.as_tensor(np.repeat(np.arange(P.q), np.diff(P.lam_star.colptr)), device="cuda")
+    out["Psi_at_lambda"] = res["Psi"][rows, cols].cpu().numpy()
+    out["lists"] = {k: res["active"][k].cpu().numpy() for k in ("L_row", "L_col", "T_row", "T_col")}
+    del res, X, Y, Syy, bufs
+    ctx.lib.cggm_ctx_release_workspace(ctx.h)
+    torch.cuda.empty_cache()
+    return P, out
+
+
+def test_sharded_sigma_lambda_identity(run_sharded):
+    P, r = run_sharded
+    assert r["is_pd"] and r["objective"]["is_pd"]
+    idx = {k: i for i, k in enumerate(r["need"])}
+    for c, j in enumerate(COLS):
+        a, b = P.lam_star.colptr[j], P.lam_star.colptr[j + 1]
+        v = sum(r["Sigma_need"][:, idx[int(k)]] * P.lam_star.val[t] for t, k in zip(range(a, b), P.lam_star.rowidx[a:b]))
+        e = np.zeros(P.q)
+        e[j] = 1.0
+        assert np.linalg.norm(v - e) < 1e-12
+    # the inverse's and the objective's (augmented) factorisations agree on log|Lambda|
+    assert r["logdet"] == pytest.approx(r["objective"]["logdet"], rel=1e-12)
+
+
+def test_sharded_generating_point_identities(run_sharded):
+    P, r = run_sharded
+    D = P.Y - P.E_noise
+    psi_ref = D.T @ D[:, COLS] / P.n
+    assert np.linalg.norm(r["Psi_cols"] - psi_ref) / np.linalg.norm(psi_ref) < 1e-9
+    syy = P.Y.T @ P.Y[:, COLS] / P.n
+    gl_ref = syy - r["Sigma_cols"] - psi_ref
+    assert np.linalg.norm(r["GradL_cols"] - gl_ref) / np.linalg.norm(gl_ref) < 1e-9
+    gt_ref = 2.0 / P.n * (P.X.T @ P.E_noise[:, COLS])
+    lists = r["lists"]
+    for rk, ck, G, lam, csc, upper in (("L_row", "L_col", gl_ref, P.lam_L, P.lam_star, True),
+                                       ("T_row", "T_col", gt_ref, P.lam_T, P.theta_star, False)):
+        rows, cols = lists[rk], lists[ck]
+        for idx, j in enumerate(COLS):
+            got = set(rows[cols == j].tolist())
+            a, b = csc.colptr[j], csc.colptr[j + 1]
+            supp = set(csc.rowidx[a:b][csc.val[a:b] != 0].tolist())
+            g = np.abs(G[:, idx])
+            nrow = j + 1 if upper else G.shape[0]
+            want = {i for i in range(nrow) if g[i] > lam or i in supp}
+            for i in got ^ want:
+                assert abs(g[i] - lam) <= TIE + 1e-9 * max(1.0, g[i]), (rk, i, j)
+
+
+def test_sharded_objective_trace_identity(run_sharded):
+    P, r = run_sharded
+    ob = r["objective"]
+    lam_psi = float(np.dot(P.lam_star.val, r["Psi_at_lambda"]))      # <Lambda, Psi> (I2)
+    assert ob["tr_sigma_m"] == pytest.approx(lam_psi, rel=1e-10)
+    # tr(S_yy Lambda) and (2/n)<W, Y> against host sums over the stored entries
+    lamd = P.lam_star.to_scipy()
+    tr_syy = float(np.sum(P.Y * (P.Y @ lamd))) / P.n
+    assert ob["tr_syy_lam"] == pytest.approx(tr_syy, rel=1e-11)
+    assert math.isfinite(ob["f"])
