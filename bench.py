@@ -210,7 +210,11 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--peak-seconds", type=float, default=2.0)
+    ap.add_argument("--stream-grad-theta", action="store_true",
+                    help="do not store the p x q grad_Theta (streamed into the active sets); default for `sharded`")
     args = ap.parse_args()
+    if args.config == "sharded":
+        args.stream_grad_theta = True
     if args.impl == "reference":
         run_reference(args)
         return
@@ -266,21 +270,27 @@ def main():
     if world == 1:
         # single GPU: fused active sets in the Psi/grad call, preallocated outputs
         q, p = P.q, P.p
-        bufs = {"Sigma": colmajor_empty(q, q), "Psi": colmajor_empty(q, q), "GradL": colmajor_empty(q, q),
-                "GradT": colmajor_empty(p, q)}
-        probe = ctx.cggm_invert_logdet(Lam, Sigma=bufs["Sigma"])
-        r0 = ctx.cggm_psi_grad(X, Y, Th, bufs["Sigma"], Syy=Syy,
-                               out=dict(Psi=bufs["Psi"], GradL=bufs["GradL"], GradT=bufs["GradT"]))
-        cnt = ctx.cggm_active_set(r0["GradL"], r0["GradT"], Lam, Th, P.lam_L, P.lam_T)
-        capL, capT = int(cnt["m_L"] * 1.05) + 1024, int(cnt["m_T"] * 1.05) + 1024
+        bufs = {"Sigma": colmajor_empty(q, q), "Psi": colmajor_empty(q, q), "GradL": colmajor_empty(q, q)}
+        if not args.stream_grad_theta:
+            bufs["GradT"] = colmajor_empty(p, q)
+        from paper_1509_04681_b200.api import newton_evaluation
+        # size the active-set lists with the two-call pattern (capacity 0 -> required sizes)
+        for k in ("L_row", "L_col", "T_row", "T_col"):
+            bufs[k] = torch.empty(0, dtype=torch.int32, device="cuda")
+        try:
+            newton_evaluation(ctx, X, Y, Syy, Lam, Th, P.lam_L, P.lam_T, True, bufs,
+                              stream_grad_theta=args.stream_grad_theta)
+        except Exception as exc:  # CGGM_ERR_CAPACITY carries the sizes
+            if getattr(exc, "status", None) != 6:
+                raise
+        m = ctx.last_active_sizes
+        capL, capT = int(m[0] * 1.05) + 1024, int(m[1] * 1.05) + 1024
         for k, cap in (("L_row", capL), ("L_col", capL), ("T_row", capT), ("T_col", capT)):
             bufs[k] = torch.empty(cap, dtype=torch.int32, device="cuda")
-        del r0, cnt, probe
-
-        from paper_1509_04681_b200.api import newton_evaluation
 
         def step():
-            return newton_evaluation(ctx, X, Y, Syy, Lam, Th, P.lam_L, P.lam_T, True, bufs)
+            return newton_evaluation(ctx, X, Y, Syy, Lam, Th, P.lam_L, P.lam_T, True, bufs,
+                                     stream_grad_theta=args.stream_grad_theta)
     else:
         def step():
             return ev.evaluate(X, Y, Lam, Th, P.lam_L, P.lam_T, True)
@@ -320,6 +330,8 @@ def main():
         from paper_1509_04681_b200.api import newton_evaluation as _ne
 
         def step_prof():
+            if args.stream_grad_theta:   # the separate calls need a stored grad_Theta
+                return _ne(ctx, X, Y, Syy, Lam, Th, P.lam_L, P.lam_T, True, bufs, stream_grad_theta=True)
             return _ne(ctx, X, Y, Syy, Lam, Th, P.lam_L, P.lam_T, True, bufs, composite=False)
     else:
         step_prof = step
@@ -385,7 +397,8 @@ def main():
                 getattr(Lam, k).copy_(hl, non_blocking=True)
                 getattr(Th, k).copy_(ht, non_blocking=True)
             Syy_s, _ = ctx.cggm_covariances(X, Y, want_sxy=False, Syy=Syy)
-            return newton_evaluation(ctx, X, Y, Syy_s, Lam, Th, P.lam_L, P.lam_T, True, bufs)
+            return newton_evaluation(ctx, X, Y, Syy_s, Lam, Th, P.lam_L, P.lam_T, True, bufs,
+                                     stream_grad_theta=args.stream_grad_theta)
 
         step_e2e()
         torch.cuda.synchronize()
@@ -416,7 +429,9 @@ def main():
                        "nnz_lambda": P.lam_star.nnz, "lambda": P.lam_L, "point": "generating (Lambda*, Theta*)",
                        "parallelism": f"sample-shard dp{world}" if world > 1 else "1 GPU",
                        "l2": "inputs larger than L2 (Sigma/Psi/grad_Lambda 3.2 GB each, grad_Theta 6.4 GB)",
-                       "setup_syy_ms": setup_ms, "generator_s": round(t_gen, 2)},
+                       "setup_syy_ms": setup_ms, "generator_s": round(t_gen, 2),
+                       "grad_theta": "streamed into the active sets (not stored)" if args.stream_grad_theta
+                       else "stored (p x q)"},
             "clocks": clk,
             "gpu_launches": launches,
             "roofline": {"bound": "tensor", "kernel": "gemm_dmma_kernel (FP64 DMMA.8x8x4, all dense contractions)",

@@ -295,11 +295,14 @@ class Context:
         ao = self._active_struct(spec)
         eo = _abi.cggm_eval_out()
         ls, ts = Lam.c_struct(), Theta.c_struct()
-        self._check(self.lib.cggm_newton_eval(
+        self.last_active_sizes = None
+        st = self.lib.cggm_newton_eval(
             self.h, n, p, q, _ptr(X), ld_of(X), _ptr(Y), ld_of(Y), _ptr(Syy), ld_of(Syy), ctypes.byref(ls),
             ctypes.byref(ts), _ptr(bufs["Sigma"]), ld_of(bufs["Sigma"]), _ptr(bufs["Psi"]), ld_of(bufs["Psi"]),
             _ptr(bufs["GradL"]), ld_of(bufs["GradL"]), _ptr(bufs["GradT"]),
-            ld_of(bufs["GradT"]) if bufs["GradT"] is not None else 1, ctypes.byref(ao), ctypes.byref(eo)))
+            ld_of(bufs["GradT"]) if bufs["GradT"] is not None else 1, ctypes.byref(ao), ctypes.byref(eo))
+        self.last_active_sizes = (int(ao.m_L), int(ao.m_T))
+        self._check(st)
         o = eo.obj
         ob = dict(f=o.f, g=o.g, logdet=o.logdet, tr_syy_lam=o.tr_syy_lam, tr_sxy_theta=o.tr_sxy_theta,
                   tr_sigma_m=o.tr_sigma_m, pen_L=o.pen_L, pen_T=o.pen_T, is_pd=bool(o.is_pd), fail_col=int(o.fail_col))
