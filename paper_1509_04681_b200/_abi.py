@@ -9,7 +9,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libcggm.so")
+# CGGM_LIB: an alternative in-tree build of the same library (A/B kernel-variant measurements)
+LIB_PATH = os.environ.get("CGGM_LIB") or os.path.join(_HERE, "lib", "libcggm.so")
 
 c_i64 = ctypes.c_int64
 c_i32 = ctypes.c_int32

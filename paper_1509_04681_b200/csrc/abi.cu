@@ -1,6 +1,7 @@
 // C-ABI of libcggm (include/cggm.h): argument validation, workspace, orchestration of the
 // kernels for the five hot-path calls.  No torch types cross this boundary.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <limits>
@@ -156,6 +157,8 @@ cggm_status cggm_ctx_create(cggm_ctx** out, int device, cggm_dtype dtype, void* 
   c->stream = static_cast<cudaStream_t>(cuda_stream);
   c->num_sms = prop.multiProcessorCount;
   c->slots.resize(WS_NUM);
+  if (const char* e = std::getenv("CGGM_PRIO")) c->prio_mode = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_LA_MIN")) c->la_min = std::atoi(e);
   cudaDriverEntryPointQueryResult q;
   void* fn = nullptr;
   if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
@@ -185,6 +188,18 @@ cggm_status cggm_ctx_destroy(cggm_ctx* ctx) {
     cudaStreamDestroy(c->aux);
     cudaEventDestroy(c->ev_fork);
     cudaEventDestroy(c->ev_join);
+  }
+  for (int l = 0; l < 2; ++l)
+    for (cudaStream_t st : {c->la_chain[l], c->la_upd[l], c->la_bg[l]})
+      if (st) {
+        cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+      }
+  for (auto e : c->la_events) cudaEventDestroy(e);
+  if (c->hi) {
+    cudaStreamSynchronize(c->hi);
+    cudaStreamDestroy(c->hi);
+    cudaEventDestroy(c->ev_join_hi);
   }
   for (auto e : c->evpool) cudaEventDestroy(e);
   delete ctx;
@@ -325,8 +340,7 @@ static void invert_enqueue(Ctx* c, int lane, const cggm_csc* Lambda, T* Sigma, i
   if (Sigma) {
     T* X = static_cast<T*>(ws_get(c, WS_LINV, (size_t)lda * q * sizeof(T)));
     CGGM_CUDA_CHECK(cudaMemsetAsync(X, 0, (size_t)lda * q * sizeof(T), c->stream));
-    const int64_t n1 = q / 2 + 128, n2 = q / 2 + 132;
-    const size_t tmp_elems = (size_t)n1 * n2;
+    const size_t tmp_elems = chol_tmp_elems(q);
     T* tmp = static_cast<T*>(ws_get(c, WS_TMP, tmp_elems * sizeof(T)));
     potrf_recursive<T>(c, Av, ViewT<T>{X, lda, q, q}, true, nullptr, slots, s.fail, tmp, tmp_elems);
     lauum<T>(c, ViewT<T>{X, lda, q, q}, ViewT<T>{Sigma, ldsigma, q, q});
@@ -738,9 +752,27 @@ cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, con
     validate_csc_dev(c, Lambda, true, "Lambda");
     validate_csc_dev(c, Theta, false, "Theta");
     if (!c->aux) {
-      CGGM_CUDA_CHECK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+      // the objective's trial factorisation is filler work: least priority, so its CTAs take the SMs
+      // the critical chain (a3 -> a4/a5 -> a6, greatest priority) leaves idle in its latency-bound
+      // recursion levels
+      int least = 0, greatest = 0;
+      CGGM_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+      CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, least));
+      CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->hi, cudaStreamNonBlocking, greatest));
       CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
       CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+      CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_join_hi, cudaEventDisableTiming));
+    }
+    cudaStream_t s_caller = c->stream;
+    struct Restore {
+      Ctx* c;
+      cudaStream_t s;
+      ~Restore() { c->stream = s; c->lane = 0; }
+    } restore{c, s_caller};
+    if (c->prio_mode) {
+      CGGM_CUDA_CHECK(cudaEventRecord(c->ev_fork, s_caller));
+      CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->hi, c->ev_fork, 0));
+      c->stream = c->hi;
     }
     cudaStream_t s0 = c->stream;
     ActTotals* tot = nullptr;
@@ -753,7 +785,7 @@ cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, con
       ws_get(c, WS_DENSE_A, (size_t)pad_ld<T>(q) * q * es);
       ws_get(c, WS_DENSE_B, (size_t)pad_ld<T>(q + n) * q * es);
       ws_get(c, WS_LINV, (size_t)pad_ld<T>(q) * q * es);
-      ws_get(c, WS_TMP, (size_t)(q / 2 + 128) * (q / 2 + 132) * es);
+      ws_get(c, WS_TMP, chol_tmp_elems(q) * es);
       ws_get(c, WS_LEAFINV, (size_t)nleaves * leaf_nb() * leaf_nb() * es);
       ws_get(c, WS_XDIAG, (size_t)pad_ld<T>(q) * block_inverse_size() * es);
       ws_get(c, WS_TMP_OBJ, ((size_t)(block_inverse_size() + 4) * (block_inverse_size() + 4) +
@@ -792,6 +824,12 @@ cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, con
                      static_cast<T*>(GradL), ldgl, static_cast<T*>(GradT), ldgt, &fz);
       tot = fz.ws.tot;
     });
+    c->stream = s_caller;
+    if (c->prio_mode) {
+      CGGM_CUDA_CHECK(cudaEventRecord(c->ev_join_hi, s0));
+      CGGM_CUDA_CHECK(cudaStreamWaitEvent(s_caller, c->ev_join_hi, 0));
+      s0 = s_caller;
+    }
     CGGM_CUDA_CHECK(cudaStreamWaitEvent(s0, c->ev_join, 0));
     char* h = static_cast<char*>(c->host_scratch);
     chol_readback_async(c, 0, h);

@@ -14,7 +14,10 @@
 // Flops: potrf q^3/3 + trtri q^3/3 + lauum q^3/3 (= potrf + potri).  Leaves (<= 64 columns)
 // run an unblocked Cholesky + triangular inverse in shared memory (one CTA), record the
 // first failing pivot (atomicMin) and 2 sum ln L_jj per leaf (deterministic final sum).
+#include <algorithm>
 #include <climits>
+#include <initializer_list>
+#include <vector>
 
 #include "common.cuh"
 
@@ -43,7 +46,10 @@ constexpr int leaf_smem_bytes() { return 2 * NB * (NB + 1) * (int)sizeof(T); }
 //     then X_p = L_pp^{-1} T by an 8-row forward substitution per column (64 threads).
 // Shared memory: L and X, column-major [col][row] with a padded leading dimension.
 template <typename T>
-__global__ void __launch_bounds__(LEAF_THREADS) leaf_potrf_trtri(T* A, int64_t lda, int nb, T* X, int64_t ldx,
+#ifndef CGGM_LEAF_MINB
+#define CGGM_LEAF_MINB 2
+#endif
+__global__ void __launch_bounds__(LEAF_THREADS, CGGM_LEAF_MINB) leaf_potrf_trtri(T* A, int64_t lda, int nb, T* X, int64_t ldx,
                                                                   int write_L, double* logdet_slot, int* fail_col,
                                                                   int col0) {
   extern __shared__ __align__(16) unsigned char leaf_raw[];
@@ -53,13 +59,23 @@ __global__ void __launch_bounds__(LEAF_THREADS) leaf_potrf_trtri(T* A, int64_t l
   __shared__ T diag[NB], invd[NB];
   __shared__ int fail_sm;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  for (int idx = t; idx < NB * NB; idx += LEAF_THREADS) {
-    const int i = idx & (NB - 1), j = idx >> 6;
-    T v;
-    if (i < nb && j < nb) v = (i >= j) ? A[i + (int64_t)j * lda] : T(0);
-    else v = (i == j) ? T(1) : T(0);
-    Ls[j][i] = v;
-    Xs[j][i] = T(0);
+  {  // the loads of a thread in flight 8 at a time
+    constexpr int PER = NB * NB / LEAF_THREADS, HALF = PER / 2;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      T v[HALF];
+#pragma unroll
+      for (int u = 0; u < HALF; ++u) {
+        const int idx = t + LEAF_THREADS * (u + h * HALF), i = idx & (NB - 1), j = idx >> 6;
+        v[u] = (i < nb && j < nb && i >= j) ? A[i + (int64_t)j * lda] : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < HALF; ++u) {
+        const int idx = t + LEAF_THREADS * (u + h * HALF), i = idx & (NB - 1), j = idx >> 6;
+        Ls[j][i] = (i < nb && j < nb) ? v[u] : ((i == j) ? T(1) : T(0));
+        Xs[j][i] = T(0);
+      }
+    }
   }
   if (t == 0) fail_sm = INT_MAX;
   __syncthreads();
@@ -114,23 +130,28 @@ __global__ void __launch_bounds__(LEAF_THREADS) leaf_potrf_trtri(T* A, int64_t l
     __syncthreads();
     // rank-8 update of the trailing lower triangle (columns >= c0 + 8)
     if (4 * cb >= c0 + 8 && rb >= cb) {
-      T li[4][8], lk[4][8];
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-          li[u][jj] = Ls[c0 + jj][4 * rb + u];
-          lk[u][jj] = Ls[c0 + jj][4 * cb + u];
-        }
+      T acc[4][4];
 #pragma unroll
       for (int k = 0; k < 4; ++k)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          T acc = Ls[4 * cb + k][4 * rb + i];
+        for (int i = 0; i < 4; ++i) acc[k][i] = Ls[4 * cb + k][4 * rb + i];
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj) acc = fma_t(-li[i][jj], lk[k][jj], acc);
-          Ls[4 * cb + k][4 * rb + i] = acc;
+      for (int jj = 0; jj < 8; ++jj) {
+        T li[4], lk[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          li[u] = Ls[c0 + jj][4 * rb + u];
+          lk[u] = Ls[c0 + jj][4 * cb + u];
         }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[k][i] = fma_t(-li[i], lk[k], acc[k][i]);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) Ls[4 * cb + k][4 * rb + i] = acc[k][i];
     }
     __syncthreads();
   }
@@ -158,8 +179,10 @@ __global__ void __launch_bounds__(LEAF_THREADS) leaf_potrf_trtri(T* A, int64_t l
     }
     __syncthreads();
   }
-  for (int idx = t; idx < nb * nb; idx += LEAF_THREADS) {
-    const int i = idx % nb, j = idx / nb;
+#pragma unroll 4
+  for (int idx = t; idx < NB * NB; idx += LEAF_THREADS) {
+    const int i = idx & (NB - 1), j = idx >> 6;
+    if (i >= nb || j >= nb) continue;
     if (write_L) A[i + (int64_t)j * lda] = (i >= j) ? Ls[j][i] : T(0);
     X[i + (int64_t)j * ldx] = (i >= j) ? Xs[j][i] : T(0);
   }
@@ -182,6 +205,51 @@ int split_point(int64_t n) {
   return (int)n1;
 }
 
+// Per-depth slices of the full-inverse temporaries: the T of a node at depth d lives in slice d,
+// so deferred side-stream products of a parent never share memory with a running child.
+void tmp_depth_sizes(int64_t n, int depth, std::vector<size_t>& mx) {
+  if (n <= NB) return;
+  const int64_t n1 = split_point(n), n2 = n - n1;
+  if ((int)mx.size() <= depth) mx.resize(depth + 1, 0);
+  mx[depth] = std::max(mx[depth], (size_t)(n2 + (n2 & 1)) * (size_t)n1);
+  tmp_depth_sizes(n1, depth + 1, mx);
+  tmp_depth_sizes(n2, depth + 1, mx);
+}
+
+std::vector<size_t> tmp_slices(int64_t n, size_t* total) {
+  std::vector<size_t> mx, off;
+  tmp_depth_sizes(n, 0, mx);
+  size_t acc = 0;
+  for (size_t v : mx) {
+    off.push_back(acc);
+    acc += (v + 31) / 32 * 32;
+  }
+  if (total) *total = acc;
+  return off;
+}
+
+cudaEvent_t la_record(Ctx* c, cudaStream_t s) {
+  if (c->la_next >= c->la_events.size()) {
+    cudaEvent_t e;
+    CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->la_events.push_back(e);
+  }
+  cudaEvent_t e = c->la_events[c->la_next++];
+  CGGM_CUDA_CHECK(cudaEventRecord(e, s));
+  return e;
+}
+
+// enqueue on stream s (after `wait`, if any) for the lifetime of this object
+struct OnStream {
+  Ctx* c;
+  cudaStream_t prev;
+  OnStream(Ctx* c_, cudaStream_t s, cudaEvent_t wait) : c(c_), prev(c_->stream) {
+    if (wait) CGGM_CUDA_CHECK(cudaStreamWaitEvent(s, wait, 0));
+    c->stream = s;
+  }
+  ~OnStream() { c->stream = prev; }
+};
+
 constexpr int BINV = 512;   // potrf-only mode: diagonal subtrees up to this size keep their inverse
 
 template <typename T>
@@ -191,8 +259,11 @@ struct Rec {
   T* leafinv;   // compact leaf inverses (potrf-only mode), leaf k at leafinv + k*NB*NB, ld NB
   double* logdet_slots;
   int* fail_col;
-  T* tmp;       // full-inverse recursion temporaries
+  T* tmp;       // full-inverse recursion temporaries: one slice per recursion depth (tmp_off)
   size_t tmp_elems;
+  std::vector<size_t> tmp_off;
+  // lookahead streams (null upd/bg: everything on the chain, c->stream)
+  cudaStream_t upd, bg;
   T* xdiag;     // potrf-only: inverse of the diagonal block at col0 stored at xdiag + col0 (ld ldxd)
   int64_t ldxd;
   T* tmp2;      // potrf-only: out-of-place product buffer for B := B Xblock^T
@@ -240,8 +311,10 @@ void leaf(Rec<T>& R, ViewT<T> A, ViewT<T> X, int64_t col0) {
 // (potrf-only mode).  Factoring the augmented [Lambda; W] leaves Z = W L^{-T} in the bottom rows
 // (block Cholesky of [[Lambda, W^T], [W, .]]), so the objective's triangular solve is carried by
 // the same recursive GEMMs with taller panels.
+// pending: event of the parent's deferred update of this node's trailing block A[n1:, n1:]
+// (full-inverse lookahead); waited on before this node's own trailing update
 template <typename T>
-void node(Rec<T>& R, ViewT<T> A, ViewT<T> X, int64_t col0) {
+void node(Rec<T>& R, ViewT<T> A, ViewT<T> X, int64_t col0, int depth = 0, cudaEvent_t pending = nullptr) {
   const int64_t n = A.cols, extra = A.rows - A.cols;
   Ctx* c = R.c;
   if (!R.full_inverse && R.xdiag && n <= BINV) {
@@ -249,8 +322,9 @@ void node(Rec<T>& R, ViewT<T> A, ViewT<T> X, int64_t col0) {
     // triangular solves of the panels to its right and of the appended rows below
     Rec<T> R2 = R;
     R2.full_inverse = true;
+    R2.tmp_off = tmp_slices(n, nullptr);
     ViewT<T> Xb{R.xdiag + col0, R.ldxd, n, n};
-    node(R2, A.sub(0, 0, n, n), Xb, col0);
+    node(R2, A.sub(0, 0, n, n), Xb, col0, 0);
     if (extra > 0) apply_block_inverse(R, A.sub(n, 0, extra, n), Xb.p, Xb.ld, n);
     return;
   }
@@ -268,34 +342,65 @@ void node(Rec<T>& R, ViewT<T> A, ViewT<T> X, int64_t col0) {
   if (R.full_inverse) {
     if (extra) throw CudaError{CGGM_ERR_UNSUPPORTED, "augmented rows need potrf-only mode"};
     ViewT<T> X11 = X.sub(0, 0, n1, n1), X21 = X.sub(n1, 0, n2, n1), X22 = X.sub(n1, n1, n2, n2);
-    node(R, A11, X11, col0);
-    ViewT<T> Tm{R.tmp, n2 + (n2 & 1), n2, n1};
-    if ((size_t)(Tm.ld * n1) > R.tmp_elems) throw CudaError{CGGM_ERR_OOM, "recursion temp too small"};
+    node(R, A11, X11, col0, depth + 1);
+    if ((size_t)depth >= R.tmp_off.size()) throw CudaError{CGGM_ERR_OOM, "recursion temp too small"};
+    ViewT<T> Tm{R.tmp + R.tmp_off[depth], n2 + (n2 & 1), n2, n1};
+    if (R.tmp_off[depth] + (size_t)(Tm.ld * n1) > R.tmp_elems) throw CudaError{CGGM_ERR_OOM, "recursion temp too small"};
     {  // T = A21 X11^T  (L21)
       EpilogueT<T> e; e.out1 = Tm.p; e.ld1 = Tm.ld;
       gemm(c, false, true, n2, n1, n1, A21.p, A21.ld, X11.p, X11.ld, e, B_KLE_N);
     }
-    {  // A22 -= T T^T (lower)
-      EpilogueT<T> e; e.out1 = A22.p; e.ld1 = A22.ld; e.a1 = -1.0; e.in1a = A22.p; e.ld1a = A22.ld; e.b1 = 1.0;
-      gemm(c, false, true, n2, n2, n1, Tm.p, Tm.ld, Tm.p, Tm.ld, e, SYM_LOWER);
+    // Lookahead: node(A22) first factors its own leading block A22[0:n21, 0:n21] and forms its panel
+    // from A22[n21:, 0:n21]; only its trailing update needs A22[n21:, n21:].  So the chain updates
+    // the leading block column of A22 and the rest of A22 -= T T^T (and A21 := T X11, needed only
+    // by X21 below) run on low-priority side streams, filling the SMs the recursion leaves idle.
+    if (pending) CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->stream, pending, 0));  // A22 complete
+    const int64_t n21 = n2 > NB ? split_point(n2) : n2, n22 = n2 - n21;
+    const bool defer = R.upd && c->la_min > 0 && n22 >= c->la_min;
+    cudaEvent_t ev_upd = nullptr, ev_a21 = nullptr;
+    if (defer) {
+      cudaEvent_t ev_t = la_record(c, c->stream);
+      {  // A22[:, 0:n21] -= T T[0:n21]^T (lower trapezoid), on the chain
+        EpilogueT<T> e; e.out1 = A22.p; e.ld1 = A22.ld; e.a1 = -1.0; e.in1a = A22.p; e.ld1a = A22.ld; e.b1 = 1.0;
+        gemm(c, false, true, n2, n21, n1, Tm.p, Tm.ld, Tm.p, Tm.ld, e, SYM_LOWER);
+      }
+      {  // A22[n21:, n21:] -= T[n21:] T[n21:]^T (lower), deferred
+        OnStream os(c, R.upd, ev_t);
+        ViewT<T> C = A22.sub(n21, n21, n22, n22);
+        EpilogueT<T> e; e.out1 = C.p; e.ld1 = C.ld; e.a1 = -1.0; e.in1a = C.p; e.ld1a = C.ld; e.b1 = 1.0;
+        gemm(c, false, true, n22, n22, n1, Tm.p + n21, Tm.ld, Tm.p + n21, Tm.ld, e, SYM_LOWER);
+        ev_upd = la_record(c, c->stream);
+      }
+      {  // A21 := T X11, deferred
+        OnStream os(c, R.bg, ev_t);
+        EpilogueT<T> e; e.out1 = A21.p; e.ld1 = A21.ld;
+        gemm(c, false, false, n2, n1, n1, Tm.p, Tm.ld, X11.p, X11.ld, e, B_KGE_N);
+        ev_a21 = la_record(c, c->stream);
+      }
+    } else {
+      {  // A22 -= T T^T (lower)
+        EpilogueT<T> e; e.out1 = A22.p; e.ld1 = A22.ld; e.a1 = -1.0; e.in1a = A22.p; e.ld1a = A22.ld; e.b1 = 1.0;
+        gemm(c, false, true, n2, n2, n1, Tm.p, Tm.ld, Tm.p, Tm.ld, e, SYM_LOWER);
+      }
+      {  // A21 := T X11
+        EpilogueT<T> e; e.out1 = A21.p; e.ld1 = A21.ld;
+        gemm(c, false, false, n2, n1, n1, Tm.p, Tm.ld, X11.p, X11.ld, e, B_KGE_N);
+      }
     }
-    {  // A21 := T X11
-      EpilogueT<T> e; e.out1 = A21.p; e.ld1 = A21.ld;
-      gemm(c, false, false, n2, n1, n1, Tm.p, Tm.ld, X11.p, X11.ld, e, B_KGE_N);
-    }
-    node(R, A22, X22, col0 + n1);
+    node(R, A22, X22, col0 + n1, depth + 1, ev_upd);
+    if (ev_a21) CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->stream, ev_a21, 0));
     {  // X21 = -X22 A21
       EpilogueT<T> e; e.out1 = X21.p; e.ld1 = X21.ld; e.a1 = -1.0;
       gemm(c, false, false, n2, n1, n2, X22.p, X22.ld, A21.p, A21.ld, e, A_KLE_M);
     }
   } else {
-    node(R, A11, X, col0);
+    node(R, A11, X, col0, depth + 1);
     trsm_rec(R, A21, A11, col0);
     {  // A22 -= A21 A21^T over the lower trapezoid (square part + appended rows)
       EpilogueT<T> e; e.out1 = A22.p; e.ld1 = A22.ld; e.a1 = -1.0; e.in1a = A22.p; e.ld1a = A22.ld; e.b1 = 1.0;
       gemm(c, false, true, n2 + extra, n2, n1, A21.p, A21.ld, A21.p, A21.ld, e, SYM_LOWER);
     }
-    node(R, A22, X, col0 + n1);
+    node(R, A22, X, col0 + n1, depth + 1);
   }
 }
 
@@ -335,9 +440,43 @@ template <typename T>
 void potrf_recursive(Ctx* c, ViewT<T> A, ViewT<T> Linv, bool full_inverse, T* leafinv, double* logdet_slots,
                      int* fail_col_dev, T* tmp, size_t tmp_elems, T* xdiag, int64_t ldxd, T* tmp2,
                      size_t tmp2_elems) {
-  Rec<T> R{c, full_inverse, leafinv, logdet_slots, fail_col_dev, tmp, tmp_elems, xdiag, ldxd, tmp2, tmp2_elems};
+  Rec<T> R{c, full_inverse, leafinv, logdet_slots, fail_col_dev, tmp, tmp_elems, {}, nullptr, nullptr,
+           xdiag, ldxd, tmp2, tmp2_elems};
+  if (full_inverse) R.tmp_off = tmp_slices(A.cols, nullptr);
   Phase ph(c, TAG_CHOL_GEMM);
-  node(R, A, Linv, 0);
+  const int lane = c->lane;
+  if (c->la_min <= 0) {
+    node(R, A, Linv, 0);
+    return;
+  }
+  // lookahead: the recursion's critical chain on a high-priority stream, deferred products on two
+  // lower-priority side streams; forked from and joined back into c->stream
+  if (!c->la_chain[lane]) {
+    int least = 0, greatest = 0;
+    CGGM_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    auto pr = [&](int k) { return std::min(least, greatest + k); };
+    const int b = 3 * lane;
+    CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->la_chain[lane], cudaStreamNonBlocking, pr(b)));
+    CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->la_upd[lane], cudaStreamNonBlocking, pr(b + 1)));
+    CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->la_bg[lane], cudaStreamNonBlocking, pr(b + 2)));
+  }
+  c->la_next = 0;
+  cudaStream_t s_in = c->stream, chain = c->la_chain[lane];
+  R.upd = c->la_upd[lane];
+  R.bg = c->la_bg[lane];
+  cudaEvent_t ev_in = la_record(c, s_in);
+  for (cudaStream_t st : std::initializer_list<cudaStream_t>{chain, R.upd, R.bg}) CGGM_CUDA_CHECK(cudaStreamWaitEvent(st, ev_in, 0));
+  {
+    OnStream os(c, chain, nullptr);
+    node(R, A, Linv, 0);
+  }
+  for (cudaStream_t st : std::initializer_list<cudaStream_t>{chain, R.upd, R.bg}) CGGM_CUDA_CHECK(cudaStreamWaitEvent(s_in, la_record(c, st), 0));
+}
+
+size_t chol_tmp_elems(int64_t q) {
+  size_t total = 0;
+  tmp_slices(q, &total);
+  return total + 64;
 }
 
 int block_inverse_size() { return BINV; }

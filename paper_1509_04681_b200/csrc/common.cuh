@@ -54,6 +54,17 @@ struct Ctx {
   int lane = 0;                  // 0: caller's stream, 1: auxiliary stream (separate workspace)
   cudaStream_t aux = nullptr;    // auxiliary stream of the composite evaluation
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t hi = nullptr;     // high-priority stream of the composite evaluation's critical chain
+  cudaEvent_t ev_join_hi = nullptr;
+  // recursive-factorisation lookahead (chol.cu): per lane a critical-chain stream and two side
+  // streams (deferred trailing updates, deferred block products) at decreasing priorities, and a
+  // pool of dependency events (reused across calls: every wait is enqueued before a re-record)
+  cudaStream_t la_chain[2] = {nullptr, nullptr}, la_upd[2] = {nullptr, nullptr}, la_bg[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> la_events;
+  size_t la_next = 0;
+  int la_min = 256;              // defer only when the deferred block is at least this wide (CGGM_LA_MIN; 0 = off)
+  int prio_mode = 1;             // composite: 1 = chain on `hi` (greatest priority), objective on `aux`
+                                 // (least priority); 0 = chain on the caller's stream (CGGM_PRIO=0)
   int force_tile = 0;
   int no_tma3d = 0;   // test hook: 1 = always use 16-wide 2-D boxes for MN-inner operands  // test hook: 0 auto, 1 = 128x128 tiles, 2 = 64x64 tiles
   // phase profiling (CUDA events around every launch while enabled)
@@ -207,6 +218,7 @@ int block_inverse_size();
 // Sigma = Linv^T Linv (full symmetric).
 template <typename T>
 void lauum(Ctx* c, ViewT<T> Linv, ViewT<T> Sigma);
+size_t chol_tmp_elems(int64_t q);   // full-inverse recursion temporaries (elements)
 int leaf_nb();
 
 // ------------------------------------------------------------------ streaming kernels (stream.cu)

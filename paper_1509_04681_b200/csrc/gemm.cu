@@ -22,6 +22,9 @@
 namespace cggm {
 namespace {
 
+#ifndef CGGM_BIG_MAXNREG
+#define CGGM_BIG_MAXNREG 192
+#endif
 constexpr int BK = 16;
 constexpr int STAGES = 4;
 constexpr int GROUP_N = 8;
@@ -40,6 +43,10 @@ struct Cfg {
   static constexpr int MAIN_BYTES = STAGES * STAGE_BYTES;
   static constexpr int DATA_BYTES = MAIN_BYTES > EPI_BYTES ? MAIN_BYTES : EPI_BYTES;
   static constexpr int SMEM_BYTES = DATA_BYTES + 1024 + 2 * STAGES * 8;
+  // register cap: a 128x128 CTA (8 warps x 192) leaves 16384 registers and ~95 KB of shared memory
+  // on its SM, exactly one 64x64 CTA (4 warps x 128), so latency-bound kernels of a concurrent
+  // stream co-reside with the big tiles instead of waiting for a whole SM
+  static constexpr int MAXREG = NTHREADS >= 256 ? CGGM_BIG_MAXNREG : 128;
   static_assert(FM % 2 == 0 && FN % 2 == 0, "MN-inner fragments come in pairs");
   static_assert(BM % 16 == 0 && BN % 16 == 0, "16-wide TMA boxes");
 };
@@ -109,7 +116,7 @@ __device__ __forceinline__ int frag_x(int f, int r) {
 }
 
 template <bool AK, bool BKI, class C>
-__global__ void __launch_bounds__(C::NTHREADS, 1)
+__global__ void __maxnreg__(C::MAXREG)
     gemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const KParams P) {
   constexpr int BM = C::BM, BN = C::BN, NCW = C::WM * C::WN, FM = C::FM, FN = C::FN;
@@ -311,8 +318,10 @@ template <bool TA, bool TB>
 __global__ void __launch_bounds__(128) gemm_small_kernel(const double* __restrict__ A, int64_t lda,
                                                           const double* __restrict__ B, int64_t ldb,
                                                           const KParamsS P) {
-  __shared__ double As[SKC][SLD];
-  __shared__ double Bs[SKC][SLD];
+  // double-buffered shared tiles; chunk i+1 is fetched into registers while chunk i is multiplied,
+  // so each chunk costs one L2 round trip overlapped with the DMMAs and one barrier
+  __shared__ double As[2][SKC][SLD];
+  __shared__ double Bs[2][SKC][SLD];
   const int m0 = blockIdx.y * ST, n0 = blockIdx.x * ST;
   if ((P.flags & SYM_LOWER) && m0 + ST - 1 < n0) return;   // tile strictly above the diagonal
   int kbeg = 0, kend = P.K;
@@ -322,42 +331,65 @@ __global__ void __launch_bounds__(128) gemm_small_kernel(const double* __restric
   if (P.flags & B_KLE_N) kend = min(kend, n0 + ST);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int wm = warp >> 1, wn = warp & 1;
+  constexpr int PER = ST * SKC / 128;   // elements of each operand per thread and chunk
+  double ra[PER], rb[PER];
+  // consecutive threads walk the contiguous dimension of each operand
+  auto fetch = [&](int kc) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int idx = tid + 128 * u;
+      int mm, kk;
+      if (TA) { kk = idx % SKC; mm = idx / SKC; } else { mm = idx % ST; kk = idx / ST; }
+      const int m = m0 + mm, k = kc + kk;
+      ra[u] = (m < P.M && k < kend) ? (TA ? A[k + (int64_t)m * lda] : A[m + (int64_t)k * lda]) : 0.0;
+      int nn, k2;
+      if (TB) { nn = idx % ST; k2 = idx / ST; } else { k2 = idx % SKC; nn = idx / SKC; }
+      const int n = n0 + nn, kb = kc + k2;
+      rb[u] = (n < P.N && kb < kend) ? (TB ? B[n + (int64_t)kb * ldb] : B[kb + (int64_t)n * ldb]) : 0.0;
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int idx = tid + 128 * u;
+      int mm, kk;
+      if (TA) { kk = idx % SKC; mm = idx / SKC; } else { mm = idx % ST; kk = idx / ST; }
+      As[buf][kk][mm] = ra[u];
+      int nn, k2;
+      if (TB) { nn = idx % ST; k2 = idx / ST; } else { k2 = idx % SKC; nn = idx / SKC; }
+      Bs[buf][k2][nn] = rb[u];
+    }
+  };
   double acc[2][2][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-  for (int kc = kbeg; kc < kend; kc += SKC) {
-    for (int idx = tid; idx < ST * SKC; idx += 128) {
-      // consecutive threads walk the contiguous dimension of each operand
-      int mm, kk;
-      if (TA) { kk = idx % SKC; mm = idx / SKC; } else { mm = idx % ST; kk = idx / ST; }
-      const int m = m0 + mm, k = kc + kk;
-      double v = 0.0;
-      if (m < P.M && k < kend) v = TA ? A[k + (int64_t)m * lda] : A[m + (int64_t)k * lda];
-      As[kk][mm] = v;
-      int nn;
-      if (TB) { nn = idx % ST; kk = idx / ST; } else { kk = idx % SKC; nn = idx / SKC; }
-      const int n = n0 + nn, k2 = kc + kk;
-      double w = 0.0;
-      if (n < P.N && k2 < kend) w = TB ? B[n + (int64_t)k2 * ldb] : B[k2 + (int64_t)n * ldb];
-      Bs[kk][nn] = w;
-    }
+  if (kbeg < kend) {
+    fetch(kbeg);
+    stash(0);
     __syncthreads();
+    int buf = 0;
+    for (int kc = kbeg; kc < kend; kc += SKC) {
+      const bool more = kc + SKC < kend;
+      if (more) fetch(kc + SKC);
 #pragma unroll
-    for (int k4 = 0; k4 < SKC / 4; ++k4) {
-      double a[2], b[2];
+      for (int k4 = 0; k4 < SKC / 4; ++k4) {
+        double a[2], b[2];
 #pragma unroll
-      for (int f = 0; f < 2; ++f) {
-        a[f] = As[4 * k4 + t][16 * wm + 8 * f + g];
-        b[f] = Bs[4 * k4 + t][16 * wn + 8 * f + g];
+        for (int f = 0; f < 2; ++f) {
+          a[f] = As[buf][4 * k4 + t][16 * wm + 8 * f + g];
+          b[f] = Bs[buf][4 * k4 + t][16 * wn + 8 * f + g];
+        }
+#pragma unroll
+        for (int fm = 0; fm < 2; ++fm)
+#pragma unroll
+          for (int fn = 0; fn < 2; ++fn) ptx::dmma_8x8x4(acc[fm][fn][0], acc[fm][fn][1], a[fm], b[fn]);
       }
-#pragma unroll
-      for (int fm = 0; fm < 2; ++fm)
-#pragma unroll
-        for (int fn = 0; fn < 2; ++fn) ptx::dmma_8x8x4(acc[fm][fn][0], acc[fm][fn][1], a[fm], b[fn]);
+      if (more) stash(buf ^ 1);   // the other buffer was last read before the previous barrier
+      __syncthreads();
+      buf ^= 1;
     }
-    __syncthreads();
   }
 #pragma unroll
   for (int fm = 0; fm < 2; ++fm)
