@@ -26,6 +26,16 @@ cggm_status cggm_test_set_tile(cggm_ctx* ctx, int mode);
 /* FP64 tensor-pipe peak: independent DMMA.8x8x4 chains on 2 CTAs/SM for ~`seconds`; returns the
  * achieved TFLOP/s and the timed milliseconds (the roofline denominator bench.py reports). */
 cggm_status cggm_test_fp64_peak(cggm_ctx* ctx, double seconds, double* tflops, double* elapsed_ms);
+/* The recursive Cholesky of a dense q x q SPD matrix A (lower triangle read; overwritten with
+ * scratch), on the ctx stream: full_inverse = 1 writes X = L^{-1} (lower, ldx), 0 = potrf only.
+ * logdet / fail_col (host, nullable; reading them synchronises) as cggm_invert_logdet.  For
+ * latency measurements of the recursion levels and dense parity tests. */
+cggm_status cggm_test_chol_dense(cggm_ctx* ctx, double* A, int64_t lda, int64_t q, double* X, int64_t ldx,
+                                 int full_inverse, double* logdet, int64_t* fail_col);
+/* Timeline of the launches recorded since cggm_ctx_profile(ctx, 1): one CSV line per launch
+ * (tag, stream index, start and end milliseconds relative to the first recorded launch).
+ * Synchronises the device; call before cggm_ctx_profile_read (which clears the records). */
+cggm_status cggm_test_profile_dump(cggm_ctx* ctx, const char* path);
 #ifdef __cplusplus
 }
 #endif

@@ -1,5 +1,6 @@
 // C-ABI of libcggm (include/cggm.h): argument validation, workspace, orchestration of the
 // kernels for the five hot-path calls.  No torch types cross this boundary.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -27,6 +28,7 @@ void* ws_get(Ctx* c, int slot, size_t bytes) {
   }
   size_t alloc = bytes < 256 ? 256 : bytes;
   alloc = (alloc + 4095) & ~size_t(4095);
+  c->ws_generation++;   // invalidates captured graphs that hold workspace pointers
   cudaError_t e = cudaMalloc(&b.ptr, alloc);
   if (e != cudaSuccess) {
     cudaGetLastError();
@@ -159,6 +161,9 @@ cggm_status cggm_ctx_create(cggm_ctx** out, int device, cggm_dtype dtype, void* 
   c->slots.resize(WS_NUM);
   if (const char* e = std::getenv("CGGM_PRIO")) c->prio_mode = std::atoi(e);
   if (const char* e = std::getenv("CGGM_LA_MIN")) c->la_min = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_NO_SMALL_ASYNC")) c->no_small_async = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_GRAPH")) c->use_graphs = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_GRAPH_PROF")) c->graph_prof = std::atoi(e);
   cudaDriverEntryPointQueryResult q;
   void* fn = nullptr;
   if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
@@ -196,12 +201,20 @@ cggm_status cggm_ctx_destroy(cggm_ctx* ctx) {
         cudaStreamDestroy(st);
       }
   for (auto e : c->la_events) cudaEventDestroy(e);
+  if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+  if (c->gorigin) {
+    cudaStreamSynchronize(c->gorigin);
+    cudaStreamDestroy(c->gorigin);
+    cudaEventDestroy(c->ev_gpre);
+    cudaEventDestroy(c->ev_gpost);
+  }
   if (c->hi) {
     cudaStreamSynchronize(c->hi);
     cudaStreamDestroy(c->hi);
     cudaEventDestroy(c->ev_join_hi);
   }
   for (auto e : c->evpool) cudaEventDestroy(e);
+  if (c->ts_buf) cudaFree(c->ts_buf);
   delete ctx;
   return CGGM_OK;
 }
@@ -242,6 +255,15 @@ cggm_status cggm_ctx_profile(cggm_ctx* ctx, int enable) {
   if (c->prof) {
     c->prof_recs.clear();
     c->evnext = 0;
+    const char* e = std::getenv("CGGM_PROF_TS");
+    if (e && std::atoi(e) && !c->ts_buf) {
+      c->ts_cap = 1 << 20;
+      if (cudaMalloc(&c->ts_buf, c->ts_cap * 8) != cudaSuccess) {
+        cudaGetLastError();
+        c->ts_buf = nullptr;
+        c->ts_cap = 0;
+      }
+    }
   }
   return CGGM_OK;
 }
@@ -249,14 +271,20 @@ cggm_status cggm_ctx_profile(cggm_ctx* ctx, int enable) {
 cggm_status cggm_ctx_profile_read(cggm_ctx* ctx, double* ms, int64_t* launches, int32_t ntags) {
   return guard(ctx, [&](Ctx* c) {
     if (!ms || !launches || ntags < CGGM_PROF_NTAGS) fail(CGGM_ERR_INVALID_ARG, "profile arrays too small");
-    CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    CGGM_CUDA_CHECK(cudaDeviceSynchronize());
     for (int t = 0; t < CGGM_PROF_NTAGS; ++t) {
       ms[t] = 0.0;
       launches[t] = 0;
     }
+    std::vector<unsigned long long> ts;
+    if (c->ts_buf) {
+      ts.resize(c->evnext);
+      CGGM_CUDA_CHECK(cudaMemcpy(ts.data(), c->ts_buf, c->evnext * 8, cudaMemcpyDeviceToHost));
+    }
     for (const auto& r : c->prof_recs) {
       float e = 0.f;
-      CGGM_CUDA_CHECK(cudaEventElapsedTime(&e, c->evpool[r.a], c->evpool[r.b]));
+      if (c->ts_buf) e = (float)((ts[r.b] - ts[r.a]) * 1e-6);
+      else CGGM_CUDA_CHECK(cudaEventElapsedTime(&e, c->evpool[r.a], c->evpool[r.b]));
       ms[r.tag] += e;
       launches[r.tag] += 1;
     }
@@ -304,6 +332,25 @@ cggm_status cggm_covariances(cggm_ctx* ctx, int64_t n_local, int64_t n_total, in
       }
     });
   });
+}
+
+int cggm::stream_priority(int which) {
+  static int off[8] = {0, 5, 0, 1, 2, 3, 4, 5};
+  static bool init = false;
+  if (!init) {
+    if (const char* e = std::getenv("CGGM_PRIO_SCHEME")) {
+      int k = 0;
+      for (const char* q = e; *q && k < 8; ++k) {
+        off[k] = std::atoi(q);
+        while (*q && *q != ',') ++q;
+        if (*q == ',') ++q;
+      }
+    }
+    init = true;
+  }
+  int least = 0, greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  return std::min(least, greatest + off[which]);
 }
 
 // ================================================================== enqueue-only cores
@@ -757,8 +804,8 @@ cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, con
       // recursion levels
       int least = 0, greatest = 0;
       CGGM_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-      CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, least));
-      CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->hi, cudaStreamNonBlocking, greatest));
+      CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, stream_priority(1)));
+      CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->hi, cudaStreamNonBlocking, stream_priority(0)));
       CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
       CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
       CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_join_hi, cudaEventDisableTiming));
@@ -769,18 +816,12 @@ cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, con
       cudaStream_t s;
       ~Restore() { c->stream = s; c->lane = 0; }
     } restore{c, s_caller};
-    if (c->prio_mode) {
-      CGGM_CUDA_CHECK(cudaEventRecord(c->ev_fork, s_caller));
-      CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->hi, c->ev_fork, 0));
-      c->stream = c->hi;
-    }
-    cudaStream_t s0 = c->stream;
-    ActTotals* tot = nullptr;
+    // allocate every workspace slot up front (allocation may synchronise the device; nothing in the
+    // enqueue below may, so that it can be captured into a CUDA graph)
     dispatch(c, [&](auto tag) {
       using T = decltype(tag);
       const size_t es = sizeof(T);
       const int64_t ldn = pad_ld<T>(n);
-      // allocate every workspace slot up front (allocation may synchronise the device)
       const int64_t nleaves = n_leaves(q);
       ws_get(c, WS_DENSE_A, (size_t)pad_ld<T>(q) * q * es);
       ws_get(c, WS_DENSE_B, (size_t)pad_ld<T>(q + n) * q * es);
@@ -796,46 +837,145 @@ cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, con
       ws_get(c, WS_R, (size_t)ldn * q * es);
       ws_get(c, WS_E, (size_t)ldn * q * es);
       if (!GradT) ws_get(c, WS_GTCHUNK, (size_t)pad_ld<T>(p) * std::min<int64_t>(GT_CHUNK, q) * es);
-      T* W = static_cast<T*>(ws_get(c, WS_W, (size_t)ldn * q * es));
-      const T* Xd = static_cast<const T*>(X);
-      const T* Yd = static_cast<const T*>(Y);
-      // a2 on the caller's stream, then fork
-      spmm_x_theta<T>(c, Xd, ldx, n, Theta, ViewT<T>{W, ldn, n, q});
-      CGGM_CUDA_CHECK(cudaEventRecord(c->ev_fork, s0));
-      CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
-      try {
-        // a7 on the auxiliary stream (lane 1)
-        c->stream = c->aux;
-        c->lane = 1;
-        objective_enqueue<T>(c, 1, n, q, Yd, ldy, W, ldn, Lambda, Theta, active->penalize_diag);
-        CGGM_CUDA_CHECK(cudaEventRecord(c->ev_join, c->aux));
-        c->stream = s0;
-        c->lane = 0;
-      } catch (...) {
-        c->stream = s0;
-        c->lane = 0;
-        throw;
-      }
-      // a3, a4/a5, a6 on the caller's stream (lane 0)
-      invert_enqueue<T>(c, 0, Lambda, static_cast<T*>(Sigma), ldsigma);
-      Fuse fz{Lambda, Theta, active, active_ws(c, q)};
-      psi_enqueue<T>(c, n, n, p, q, Xd, ldx, Yd, ldy, W, ldn, static_cast<const T*>(Sigma), ldsigma,
-                     static_cast<const T*>(Syy), ldsyy, nullptr, 0, static_cast<T*>(Psi), ldpsi,
-                     static_cast<T*>(GradL), ldgl, static_cast<T*>(GradT), ldgt, &fz);
-      tot = fz.ws.tot;
+      ws_get(c, WS_W, (size_t)ldn * q * es);
     });
-    c->stream = s_caller;
-    if (c->prio_mode) {
-      CGGM_CUDA_CHECK(cudaEventRecord(c->ev_join_hi, s0));
-      CGGM_CUDA_CHECK(cudaStreamWaitEvent(s_caller, c->ev_join_hi, 0));
-      s0 = s_caller;
-    }
-    CGGM_CUDA_CHECK(cudaStreamWaitEvent(s0, c->ev_join, 0));
+    ActTotals* tot = nullptr;
     char* h = static_cast<char*>(c->host_scratch);
-    chol_readback_async(c, 0, h);
-    objective_readback_async(c, 1, h + 64);
-    CGGM_CUDA_CHECK(cudaMemcpyAsync(h + 256, tot, sizeof(ActTotals), cudaMemcpyDeviceToHost, s0));
-    CGGM_CUDA_CHECK(cudaStreamSynchronize(s0));
+    // the whole evaluation, enqueue only: fork onto the chain / objective streams, join back into
+    // the caller's stream, D2H of the scalars into pinned host memory
+    auto enqueue = [&](cudaStream_t so) {
+      c->stream = so;
+      if (c->prio_mode) {
+        CGGM_CUDA_CHECK(cudaEventRecord(c->ev_fork, so));
+        CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->hi, c->ev_fork, 0));
+        c->stream = c->hi;
+      }
+      cudaStream_t s0 = c->stream;
+      dispatch(c, [&](auto tag) {
+        using T = decltype(tag);
+        const size_t es = sizeof(T);
+        const int64_t ldn = pad_ld<T>(n);
+        T* W = static_cast<T*>(ws_get(c, WS_W, (size_t)ldn * q * es));
+        const T* Xd = static_cast<const T*>(X);
+        const T* Yd = static_cast<const T*>(Y);
+        // a2 on the chain stream, then fork
+        spmm_x_theta<T>(c, Xd, ldx, n, Theta, ViewT<T>{W, ldn, n, q});
+        CGGM_CUDA_CHECK(cudaEventRecord(c->ev_fork, s0));
+        CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
+        try {
+          // a7 on the auxiliary stream (lane 1)
+          c->stream = c->aux;
+          c->lane = 1;
+          objective_enqueue<T>(c, 1, n, q, Yd, ldy, W, ldn, Lambda, Theta, active->penalize_diag);
+          CGGM_CUDA_CHECK(cudaEventRecord(c->ev_join, c->aux));
+          c->stream = s0;
+          c->lane = 0;
+        } catch (...) {
+          c->stream = s0;
+          c->lane = 0;
+          throw;
+        }
+        // a3, a4/a5, a6 on the chain stream (lane 0)
+        invert_enqueue<T>(c, 0, Lambda, static_cast<T*>(Sigma), ldsigma);
+        Fuse fz{Lambda, Theta, active, active_ws(c, q)};
+        psi_enqueue<T>(c, n, n, p, q, Xd, ldx, Yd, ldy, W, ldn, static_cast<const T*>(Sigma), ldsigma,
+                       static_cast<const T*>(Syy), ldsyy, nullptr, 0, static_cast<T*>(Psi), ldpsi,
+                       static_cast<T*>(GradL), ldgl, static_cast<T*>(GradT), ldgt, &fz);
+        tot = fz.ws.tot;
+      });
+      c->stream = so;
+      if (c->prio_mode) {
+        CGGM_CUDA_CHECK(cudaEventRecord(c->ev_join_hi, s0));
+        CGGM_CUDA_CHECK(cudaStreamWaitEvent(so, c->ev_join_hi, 0));
+      }
+      CGGM_CUDA_CHECK(cudaStreamWaitEvent(so, c->ev_join, 0));
+      chol_readback_async(c, 0, h);
+      objective_readback_async(c, 1, h + 64);
+      CGGM_CUDA_CHECK(cudaMemcpyAsync(h + 256, tot, sizeof(ActTotals), cudaMemcpyDeviceToHost, so));
+    };
+    // CUDA graph of the evaluation: the ~3000 launches of the two recursive factorisations would
+    // otherwise be throttled by the launch queue (the host blocks enqueueing the first one while the
+    // GPU works through it, so the second could not start alongside).  A new argument set runs
+    // eagerly once (allocating anything missing), the second call with the same arguments captures.
+    std::vector<int64_t> key = {n, p, q, ldx, ldy, ldsyy, ldsigma, ldpsi, ldgl, ldgt, (int64_t)c->ws_generation,
+                                (int64_t)c->dtype, c->prio_mode, c->la_min, (int64_t)s_caller};
+    for (const void* ptr : {X, Y, Syy, (const void*)Sigma, (const void*)Psi, (const void*)GradL, (const void*)GradT})
+      key.push_back((int64_t)ptr);
+    for (const cggm_csc* m : {Lambda, Theta}) {
+      key.insert(key.end(), {m->nrows, m->ncols, m->nnz, (int64_t)m->colptr, (int64_t)m->rowidx, (int64_t)m->val});
+    }
+    {
+      const cggm_active_out* a = active;
+      int64_t lb, tb;
+      std::memcpy(&lb, &a->lam_L, 8);
+      std::memcpy(&tb, &a->lam_T, 8);
+      int64_t eb;
+      std::memcpy(&eb, &a->tie_eps, 8);
+      key.insert(key.end(), {lb, tb, eb, a->penalize_diag, a->cap_L, a->cap_T, (int64_t)a->L_row, (int64_t)a->L_col,
+                             (int64_t)a->T_row, (int64_t)a->T_col});
+    }
+    const bool graphs = c->use_graphs && (!c->prof || c->graph_prof);
+    key.push_back(c->prof ? 1 : 0);
+    if (graphs && !c->gorigin) {
+      // capture origin: an internal stream (the caller's may be the legacy default stream, which
+      // cannot be captured); ordered after / before the caller's stream by events outside the graph
+      int least = 0, greatest = 0;
+      CGGM_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+      CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->gorigin, cudaStreamNonBlocking, greatest));
+      CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_gpre, cudaEventDisableTiming));
+      CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_gpost, cudaEventDisableTiming));
+    }
+    auto launch_graph = [&]() {
+      CGGM_CUDA_CHECK(cudaEventRecord(c->ev_gpre, s_caller));
+      CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->gorigin, c->ev_gpre, 0));
+      CGGM_CUDA_CHECK(cudaGraphLaunch(c->graph_exec, c->gorigin));
+      CGGM_CUDA_CHECK(cudaEventRecord(c->ev_gpost, c->gorigin));
+      CGGM_CUDA_CHECK(cudaStreamWaitEvent(s_caller, c->ev_gpost, 0));
+    };
+    if (graphs && c->graph_exec && key == c->graph_key) {
+      launch_graph();
+      c->launches += c->graph_launches;
+      tot = c->graph_tot;
+    } else if (graphs && key == c->graph_key_seen) {
+      if (c->graph_exec) {
+        cudaGraphExecDestroy(c->graph_exec);
+        c->graph_exec = nullptr;
+      }
+      const int64_t l0 = c->launches;
+      CGGM_CUDA_CHECK(cudaStreamBeginCapture(c->gorigin, cudaStreamCaptureModeRelaxed));
+      cudaGraph_t g = nullptr;
+      bool captured = true;
+      try {
+        enqueue(c->gorigin);
+      } catch (...) {
+        captured = false;
+      }
+      c->stream = s_caller;
+      c->lane = 0;
+      cudaError_t ce = cudaStreamEndCapture(c->gorigin, &g);
+      cudaError_t ie = cudaErrorUnknown;
+      // node priorities: the chain / objective / side streams' priorities carry into the graph
+      if (captured && ce == cudaSuccess && g)
+        ie = cudaGraphInstantiateWithFlags(&c->graph_exec, g, cudaGraphInstantiateFlagUseNodePriority);
+      if (g) cudaGraphDestroy(g);
+      if (ie != cudaSuccess) {
+        // something in the enqueue is not capturable here: run this and later calls eagerly
+        cudaGetLastError();
+        c->graph_exec = nullptr;
+        c->use_graphs = 0;
+        c->launches = l0;
+        enqueue(s_caller);
+      } else {
+        c->graph_launches = c->launches - l0;
+        c->graph_key = key;
+        c->graph_tot = tot;
+        launch_graph();
+      }
+    } else {
+      enqueue(s_caller);
+      c->graph_key_seen = key;
+    }
+    CGGM_CUDA_CHECK(cudaStreamSynchronize(s_caller));
     CholResult cr = chol_decode(h);
     out->logdet = cr.logdet;
     out->is_pd = cr.is_pd;
@@ -868,6 +1008,76 @@ extern "C" cggm_status cggm_test_gemm_f32(cggm_ctx* ctx, int transA, int transB,
     e.out1 = C; e.ld1 = ldc; e.a1 = alpha;
     if (beta != 0.0) { e.in1a = C; e.ld1a = ldc; e.b1 = beta; }
     gemm(c, transA != 0, transB != 0, M, N, K, A, lda, B, ldb, e, flags);
+  });
+}
+
+extern "C" cggm_status cggm_test_chol_dense(cggm_ctx* ctx, double* A, int64_t lda, int64_t q, double* X, int64_t ldx,
+                                            int full_inverse, double* logdet, int64_t* fail_col) {
+  return guard(ctx, [&](Ctx* c) {
+    if (c->dtype != CGGM_F64) fail(CGGM_ERR_UNSUPPORTED, "cggm_test_chol_dense is fp64");
+    if (!A || q < 1 || lda < q || lda % 2) fail(CGGM_ERR_INVALID_ARG, "need q >= 1 and an even lda >= q");
+    if (full_inverse && (!X || ldx < q || ldx % 2)) fail(CGGM_ERR_INVALID_ARG, "need X with an even ldx >= q");
+    const int nb = leaf_nb();
+    const int64_t nleaves = n_leaves(q);
+    Scal s = scal_lane(c, 0, 8 + nleaves);
+    double* slots = s.dbl + 8;
+    init_scalars(c, s.fail, s.flag);
+    ViewT<double> Av{A, lda, q, q};
+    if (full_inverse) {
+      CGGM_CUDA_CHECK(cudaMemsetAsync(X, 0, (size_t)ldx * q * 8, c->stream));
+      const size_t tmp_elems = chol_tmp_elems(q);
+      double* tmp = static_cast<double*>(ws_get(c, WS_TMP, tmp_elems * 8));
+      potrf_recursive<double>(c, Av, ViewT<double>{X, ldx, q, q}, true, nullptr, slots, s.fail, tmp, tmp_elems);
+    } else {
+      double* leafinv = static_cast<double*>(ws_get(c, WS_LEAFINV, (size_t)nleaves * nb * nb * 8));
+      potrf_recursive<double>(c, Av, ViewT<double>{nullptr, lda, q, q}, false, leafinv, slots, s.fail, nullptr, 0);
+    }
+    sum_arrays_1(c, slots, nleaves, s.dbl);
+    if (logdet || fail_col) {
+      char* h = static_cast<char*>(c->host_scratch);
+      chol_readback_async(c, 0, h);
+      CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+      CholResult r = chol_decode(h);
+      if (logdet) *logdet = r.logdet;
+      if (fail_col) *fail_col = r.fail_col;
+    }
+  });
+}
+
+extern "C" cggm_status cggm_test_profile_dump(cggm_ctx* ctx, const char* path) {
+  return guard(ctx, [&](Ctx* c) {
+    if (!path) fail(CGGM_ERR_INVALID_ARG, "null path");
+    CGGM_CUDA_CHECK(cudaDeviceSynchronize());
+    FILE* f = std::fopen(path, "w");
+    if (!f) fail(CGGM_ERR_INVALID_ARG, "cannot open profile dump path");
+    std::fprintf(f, "tag,stream,start_ms,end_ms\n");
+    std::vector<cudaStream_t> seen;
+    if (!c->prof_recs.empty()) {
+      std::vector<unsigned long long> ts;
+      if (c->ts_buf) {
+        ts.resize(c->evnext);
+        CGGM_CUDA_CHECK(cudaMemcpy(ts.data(), c->ts_buf, c->evnext * 8, cudaMemcpyDeviceToHost));
+      }
+      unsigned long long t0 = ~0ull;
+      for (const auto& r : c->prof_recs)
+        if (c->ts_buf) t0 = std::min(t0, ts[r.a]);
+      cudaEvent_t ref = c->ts_buf ? nullptr : c->evpool[c->prof_recs.front().a];
+      for (const auto& r : c->prof_recs) {
+        size_t si = 0;
+        while (si < seen.size() && seen[si] != r.stream) ++si;
+        if (si == seen.size()) seen.push_back(r.stream);
+        float a = 0.f, b = 0.f;
+        if (c->ts_buf) {
+          a = (float)((ts[r.a] - t0) * 1e-6);
+          b = (float)((ts[r.b] - t0) * 1e-6);
+        } else {
+          CGGM_CUDA_CHECK(cudaEventElapsedTime(&a, ref, c->evpool[r.a]));
+          CGGM_CUDA_CHECK(cudaEventElapsedTime(&b, ref, c->evpool[r.b]));
+        }
+        std::fprintf(f, "%s,%zu,%.4f,%.4f\n", cggm_profile_tag_name(r.tag), si, a, b);
+      }
+    }
+    std::fclose(f);
   });
 }
 

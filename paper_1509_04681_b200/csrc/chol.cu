@@ -15,7 +15,10 @@
 // run an unblocked Cholesky + triangular inverse in shared memory (one CTA), record the
 // first failing pivot (atomicMin) and 2 sum ln L_jj per leaf (deterministic final sum).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <climits>
+#include <cstdlib>
 #include <initializer_list>
 #include <vector>
 
@@ -30,7 +33,11 @@ __device__ __forceinline__ double fma_t(double a, double b, double c) { return f
 __device__ __forceinline__ float fma_t(float a, float b, float c) { return fmaf(a, b, c); }
 
 constexpr int NB = 64;
-constexpr int LEAF_THREADS = 256;
+#ifndef CGGM_LEAF_THREADS
+#define CGGM_LEAF_THREADS 256
+#endif
+// (128 threads x <= 128 registers would fit beside a 128x128 GEMM CTA, but measured slower)
+constexpr int LEAF_THREADS = CGGM_LEAF_THREADS;
 template <typename T>
 constexpr int leaf_smem_bytes() { return 2 * NB * (NB + 1) * (int)sizeof(T); }
 
@@ -47,7 +54,7 @@ constexpr int leaf_smem_bytes() { return 2 * NB * (NB + 1) * (int)sizeof(T); }
 // Shared memory: L and X, column-major [col][row] with a padded leading dimension.
 template <typename T>
 #ifndef CGGM_LEAF_MINB
-#define CGGM_LEAF_MINB 2
+#define CGGM_LEAF_MINB (512 / CGGM_LEAF_THREADS)
 #endif
 __global__ void __launch_bounds__(LEAF_THREADS, CGGM_LEAF_MINB) leaf_potrf_trtri(T* A, int64_t lda, int nb, T* X, int64_t ldx,
                                                                   int write_L, double* logdet_slot, int* fail_col,
@@ -59,6 +66,13 @@ __global__ void __launch_bounds__(LEAF_THREADS, CGGM_LEAF_MINB) leaf_potrf_trtri
   __shared__ T diag[NB], invd[NB];
   __shared__ int fail_sm;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+#ifdef CGGM_LEAF_TIMING
+  long long lt_[8];
+#define LT(i) do { if (t == 0) lt_[i] = clock64(); } while (0)
+#else
+#define LT(i) do { } while (0)
+#endif
+  LT(0);
   {  // the loads of a thread in flight 8 at a time
     constexpr int PER = NB * NB / LEAF_THREADS, HALF = PER / 2;
 #pragma unroll
@@ -79,90 +93,109 @@ __global__ void __launch_bounds__(LEAF_THREADS, CGGM_LEAF_MINB) leaf_potrf_trtri
   }
   if (t == 0) fail_sm = INT_MAX;
   __syncthreads();
-  const int rb = t & 15, cb = t >> 4;
+  LT(1);
   // ------------------------------------------------------------ Cholesky, 8-column panels
   for (int p = 0; p < NB / 8; ++p) {
     const int c0 = 8 * p;
     if (warp == 0) {
-      T pv[2][8];
+      // the 8x8 diagonal block is factored redundantly by every lane in registers (no shuffles on
+      // the dependency chain), then each lane solves its own rows of the panel: v := v Ld^{-T}
+      T Ld[8][8];
 #pragma unroll
-      for (int s2 = 0; s2 < 2; ++s2) {
-        const int row = c0 + lane + 32 * s2;
+      for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int jj = 0; jj < 8; ++jj) pv[s2][jj] = (row < NB) ? Ls[c0 + jj][row] : T(0);
-      }
+        for (int j = 0; j <= i; ++j) Ld[i][j] = Ls[c0 + j][c0 + i];
+      T inv[8];
+      int bad = INT_MAX;
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) {
-        const int j = c0 + jj;
-        const T d = __shfl_sync(0xffffffffu, pv[0][jj], jj);
-        const T inv = rsqrt_t(d);
-        const T ljj = d * inv;
-        if (lane == jj) {
-          if (!(d > T(0)) || !isfinite(d)) atomicMin(&fail_sm, j);
-          diag[j] = ljj;
-          invd[j] = inv;
-        }
+      for (int j = 0; j < 8; ++j) {
+        const T d = Ld[j][j];
+        if ((!(d > T(0)) || !isfinite(d)) && bad == INT_MAX) bad = j;
+        inv[j] = rsqrt_t(d);
+        Ld[j][j] = d * inv[j];
 #pragma unroll
-        for (int s2 = 0; s2 < 2; ++s2) {
-          const int row = c0 + lane + 32 * s2;
-          if (row > j) pv[s2][jj] *= inv;
-          else if (row == j) pv[s2][jj] = ljj;
-        }
+        for (int i = j + 1; i < 8; ++i) Ld[i][j] *= inv[j];
 #pragma unroll
-        for (int kk = jj + 1; kk < 8; ++kk) {
-          const T lk = __shfl_sync(0xffffffffu, pv[0][jj], kk);
+        for (int k = j + 1; k < 8; ++k)
 #pragma unroll
-          for (int s2 = 0; s2 < 2; ++s2) {
-            const int row = c0 + lane + 32 * s2;
-            if (row >= c0 + kk) pv[s2][kk] = fma_t(-pv[s2][jj], lk, pv[s2][kk]);
-          }
-        }
+          for (int i = k; i < 8; ++i) Ld[i][k] = fma_t(-Ld[i][j], Ld[k][j], Ld[i][k]);
       }
 #pragma unroll
       for (int s2 = 0; s2 < 2; ++s2) {
-        const int row = c0 + lane + 32 * s2;
+        const int row = c0 + 8 + lane + 32 * s2;
         if (row < NB) {
+          T v[8];
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj) Ls[c0 + jj][row] = pv[s2][jj];
+          for (int jj = 0; jj < 8; ++jj) v[jj] = Ls[c0 + jj][row];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            v[j] *= inv[j];
+#pragma unroll
+            for (int i = j + 1; i < 8; ++i) v[i] = fma_t(-v[j], Ld[i][j], v[i]);
+          }
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) Ls[c0 + jj][row] = v[jj];
         }
       }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (lane == i) {
+#pragma unroll
+          for (int j = 0; j <= i; ++j) Ls[c0 + j][c0 + i] = Ld[i][j];
+          diag[c0 + i] = Ld[i][i];
+          invd[c0 + i] = inv[i];
+        }
+      if (lane == 0 && bad != INT_MAX) atomicMin(&fail_sm, c0 + bad);
     }
     __syncthreads();
+    if (p == 0) LT(2);
     // rank-8 update of the trailing lower triangle (columns >= c0 + 8)
-    if (4 * cb >= c0 + 8 && rb >= cb) {
-      T acc[4][4];
+    for (int blk = t; blk < 256; blk += LEAF_THREADS) {   // 4x4 blocks (rb, cb) of the 64x64 tile
+      const int rb = blk & 15, cb = blk >> 4;
+      if (4 * cb >= c0 + 8 && rb >= cb) {
+        T acc[4][4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < 4; ++k)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) acc[k][i] = Ls[4 * cb + k][4 * rb + i];
+          for (int i = 0; i < 4; ++i) acc[k][i] = Ls[4 * cb + k][4 * rb + i];
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) {
-        T li[4], lk[4];
+        for (int jj = 0; jj < 8; ++jj) {
+          T li[4], lk[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          li[u] = Ls[c0 + jj][4 * rb + u];
-          lk[u] = Ls[c0 + jj][4 * cb + u];
+          for (int u = 0; u < 4; ++u) {
+            li[u] = Ls[c0 + jj][4 * rb + u];
+            lk[u] = Ls[c0 + jj][4 * cb + u];
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[k][i] = fma_t(-li[i], lk[k], acc[k][i]);
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k)
 #pragma unroll
-          for (int i = 0; i < 4; ++i) acc[k][i] = fma_t(-li[i], lk[k], acc[k][i]);
+          for (int i = 0; i < 4; ++i) Ls[4 * cb + k][4 * rb + i] = acc[k][i];
       }
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) Ls[4 * cb + k][4 * rb + i] = acc[k][i];
     }
     __syncthreads();
   }
+  LT(4);
   // ------------------------------------------------------------ X = L^{-1}, 8-row block sweep
   for (int p = 0; p < NB / 8; ++p) {
     const int r0 = 8 * p;
     for (int e = t; e < 8 * (r0 + 8); e += LEAF_THREADS) {
       const int rr = e & 7, c = e >> 3, r = r0 + rr;
-      T acc = (r == c) ? T(1) : T(0);
-      for (int m = c; m < r0; ++m) acc = fma_t(-Ls[m][r], Xs[c][m], acc);
-      Tb[c][rr] = acc;
+      // four independent partial sums: the dot product is not one serial FMA chain
+      T a0 = (r == c) ? T(1) : T(0), a1 = T(0), a2 = T(0), a3 = T(0);
+      int m = c;
+      for (; m + 3 < r0; m += 4) {
+        a0 = fma_t(-Ls[m][r], Xs[c][m], a0);
+        a1 = fma_t(-Ls[m + 1][r], Xs[c][m + 1], a1);
+        a2 = fma_t(-Ls[m + 2][r], Xs[c][m + 2], a2);
+        a3 = fma_t(-Ls[m + 3][r], Xs[c][m + 3], a3);
+      }
+      for (; m < r0; ++m) a0 = fma_t(-Ls[m][r], Xs[c][m], a0);
+      Tb[c][rr] = (a0 + a1) + (a2 + a3);
     }
     __syncthreads();
     if (t < r0 + 8) {
@@ -179,6 +212,7 @@ __global__ void __launch_bounds__(LEAF_THREADS, CGGM_LEAF_MINB) leaf_potrf_trtri
     }
     __syncthreads();
   }
+  LT(5);
 #pragma unroll 4
   for (int idx = t; idx < NB * NB; idx += LEAF_THREADS) {
     const int i = idx & (NB - 1), j = idx >> 6;
@@ -186,6 +220,7 @@ __global__ void __launch_bounds__(LEAF_THREADS, CGGM_LEAF_MINB) leaf_potrf_trtri
     if (write_L) A[i + (int64_t)j * lda] = (i >= j) ? Ls[j][i] : T(0);
     X[i + (int64_t)j * ldx] = (i >= j) ? Xs[j][i] : T(0);
   }
+  LT(6);
   if (t < 32) {  // 2 sum ln L_jj, fixed order
     double sacc = log((double)diag[t]) + log((double)diag[t + 32]);
 #pragma unroll
@@ -195,6 +230,14 @@ __global__ void __launch_bounds__(LEAF_THREADS, CGGM_LEAF_MINB) leaf_potrf_trtri
       if (fail_sm != INT_MAX && fail_sm < nb) atomicMin(fail_col, col0 + fail_sm);
     }
   }
+#ifdef CGGM_LEAF_TIMING
+  LT(7);
+  if (t == 0 && col0 == 0)
+    printf("leaf clocks: load %lld panel0 %lld potrf %lld trtri %lld store %lld logdet %lld total %lld\n",
+           lt_[1] - lt_[0], lt_[2] - lt_[1], lt_[4] - lt_[1], lt_[5] - lt_[4], lt_[6] - lt_[5], lt_[7] - lt_[6],
+           lt_[7] - lt_[0]);
+#endif
+#undef LT
 }
 
 int split_point(int64_t n) {
@@ -250,7 +293,15 @@ struct OnStream {
   ~OnStream() { c->stream = prev; }
 };
 
-constexpr int BINV = 512;   // potrf-only mode: diagonal subtrees up to this size keep their inverse
+// potrf-only mode: diagonal subtrees up to this size keep their inverse (CGGM_BINV overrides)
+int binv_size() {
+  static int v = [] {
+    const char* e = std::getenv("CGGM_BINV");
+    return e ? std::atoi(e) : 4096;
+  }();
+  return v;
+}
+#define BINV binv_size()
 
 template <typename T>
 struct Rec {
@@ -452,13 +503,10 @@ void potrf_recursive(Ctx* c, ViewT<T> A, ViewT<T> Linv, bool full_inverse, T* le
   // lookahead: the recursion's critical chain on a high-priority stream, deferred products on two
   // lower-priority side streams; forked from and joined back into c->stream
   if (!c->la_chain[lane]) {
-    int least = 0, greatest = 0;
-    CGGM_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-    auto pr = [&](int k) { return std::min(least, greatest + k); };
-    const int b = 3 * lane;
-    CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->la_chain[lane], cudaStreamNonBlocking, pr(b)));
-    CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->la_upd[lane], cudaStreamNonBlocking, pr(b + 1)));
-    CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->la_bg[lane], cudaStreamNonBlocking, pr(b + 2)));
+    const int b = 2 + 3 * lane;
+    CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->la_chain[lane], cudaStreamNonBlocking, stream_priority(b)));
+    CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->la_upd[lane], cudaStreamNonBlocking, stream_priority(b + 1)));
+    CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->la_bg[lane], cudaStreamNonBlocking, stream_priority(b + 2)));
   }
   c->la_next = 0;
   cudaStream_t s_in = c->stream, chain = c->la_chain[lane];
@@ -468,7 +516,11 @@ void potrf_recursive(Ctx* c, ViewT<T> A, ViewT<T> Linv, bool full_inverse, T* le
   for (cudaStream_t st : std::initializer_list<cudaStream_t>{chain, R.upd, R.bg}) CGGM_CUDA_CHECK(cudaStreamWaitEvent(st, ev_in, 0));
   {
     OnStream os(c, chain, nullptr);
+    const auto t0 = std::chrono::steady_clock::now();
     node(R, A, Linv, 0);
+    if (std::getenv("CGGM_HOSTPROF"))
+      std::fprintf(stderr, "potrf_recursive q=%lld full=%d host enqueue %.3f ms\n", (long long)A.cols, (int)full_inverse,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   }
   for (cudaStream_t st : std::initializer_list<cudaStream_t>{chain, R.upd, R.bg}) CGGM_CUDA_CHECK(cudaStreamWaitEvent(s_in, la_record(c, st), 0));
 }

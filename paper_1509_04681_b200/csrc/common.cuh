@@ -38,6 +38,8 @@ enum ProfTag {
   TAG_NUM
 };
 
+struct ActTotals;
+
 struct Ctx {
   int device = 0;
   cggm_dtype dtype = CGGM_F64;
@@ -65,20 +67,39 @@ struct Ctx {
   int la_min = 256;              // defer only when the deferred block is at least this wide (CGGM_LA_MIN; 0 = off)
   int prio_mode = 1;             // composite: 1 = chain on `hi` (greatest priority), objective on `aux`
                                  // (least priority); 0 = chain on the caller's stream (CGGM_PRIO=0)
+  // CUDA graph of the composite evaluation (cggm_newton_eval), keyed by its full argument set
+  int use_graphs = 1;            // CGGM_GRAPH=0 disables
+  int graph_prof = 0;            // CGGM_GRAPH_PROF=1: capture the profiling events too (timelines)
+  uint64_t ws_generation = 0;    // bumped by every workspace (re)allocation
+  cudaGraphExec_t graph_exec = nullptr;
+  cudaStream_t gorigin = nullptr;   // capture / launch stream of the graph
+  cudaEvent_t ev_gpre = nullptr, ev_gpost = nullptr;
+  std::vector<int64_t> graph_key, graph_key_seen;
+  int64_t graph_launches = 0;
+  ActTotals* graph_tot = nullptr;
   int force_tile = 0;
+  int no_small_async = 0;   // test hook (CGGM_NO_SMALL_ASYNC=1): direct-load small kernel only
   int no_tma3d = 0;   // test hook: 1 = always use 16-wide 2-D boxes for MN-inner operands  // test hook: 0 auto, 1 = 128x128 tiles, 2 = 64x64 tiles
   // phase profiling (CUDA events around every launch while enabled)
   int cur_tag = TAG_MISC;
   bool prof = false;
   std::vector<cudaEvent_t> evpool;
+  unsigned long long* ts_buf = nullptr;   // CGGM_PROF_TS=1: device timestamps instead of events (graph-safe)
+  size_t ts_cap = 0;
   size_t evnext = 0;
   struct ProfRec {
     int tag, a, b;
+    cudaStream_t stream;
   };
   std::vector<ProfRec> prof_recs;
 };
 
 // RAII event pair around one launch (no-op unless profiling is enabled)
+void prof_stamp(Ctx* c, int idx);
+// stream priority of internal stream `which` (0 hi, 1 aux, 2..4 lane-0 chain/upd/bg, 5..7 lane-1):
+// offsets from the greatest priority, CGGM_PRIO_SCHEME="h,a,c0,u0,b0,c1,u1,b1" overrides
+int stream_priority(int which);   // stream.cu: one-thread kernel writing %globaltimer to ts_buf[idx]
+
 struct Prof {
   Ctx* c;
   int tag;
@@ -86,15 +107,18 @@ struct Prof {
   Prof(Ctx* c_, int tag_) : c(c_), tag(tag_) {
     if (!c->prof) return;
     ia = take();
-    cudaEventRecord(c->evpool[ia], c->stream);
+    if (c->ts_buf) prof_stamp(c, ia);
+    else cudaEventRecord(c->evpool[ia], c->stream);
   }
   ~Prof() {
     if (ia < 0) return;
     int ib = take();
-    cudaEventRecord(c->evpool[ib], c->stream);
-    c->prof_recs.push_back(Ctx::ProfRec{tag, ia, ib});
+    if (c->ts_buf) prof_stamp(c, ib);
+    else cudaEventRecord(c->evpool[ib], c->stream);
+    c->prof_recs.push_back(Ctx::ProfRec{tag, ia, ib, c->stream});
   }
   int take() {
+    if (c->ts_buf) return (int)(c->evnext < c->ts_cap ? c->evnext++ : c->ts_cap - 1);
     if (c->evnext == c->evpool.size()) {
       cudaEvent_t e;
       cudaEventCreate(&e);
@@ -292,6 +316,13 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// Ampere-style asynchronous 16-byte global -> shared copy; bytes < 16 zero-fill the tail
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }

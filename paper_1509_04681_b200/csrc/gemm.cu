@@ -17,6 +17,9 @@
 //  MN-inner fragment pair p, element e, lane g     ->  x = 16*p + 2*g + e
 //  K-inner fragment f, lane g                       ->  x = 8*f + (g>>1) + 4*(g&1)
 // The epilogue inverts the same maps.
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace cggm {
@@ -57,7 +60,8 @@ struct KParams {
   int M, N, K;
   int tilesM, tilesN;
   int flags;
-  int a3d, b3d;  // MN-inner operand loaded with one 3-D TMA box (extent multiple of 16)
+  int a3d, b3d;  // MN-inner operand: tiles inside the first a3d / b3d rows (a multiple of 16) load one
+                 // 3-D TMA box; 0 = never (the ragged last tile uses 16-wide 2-D boxes of the second map)
   Epilogue epi;
 };
 
@@ -118,6 +122,7 @@ __device__ __forceinline__ int frag_x(int f, int r) {
 template <bool AK, bool BKI, class C>
 __global__ void __maxnreg__(C::MAXREG)
     gemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
                      const KParams P) {
   constexpr int BM = C::BM, BN = C::BN, NCW = C::WM * C::WN, FM = C::FM, FN = C::FN;
   constexpr int OP_BYTES = C::A_BYTES, STAGE_BYTES = C::STAGE_BYTES, DATA_BYTES = C::DATA_BYTES;
@@ -165,12 +170,21 @@ __global__ void __maxnreg__(C::MAXREG)
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
   }
+  // MN-inner operands: one 3-D box when the tile lies inside the 16-row-aligned extent, else
+  // 16-wide 2-D boxes (rows past the extent are neither loaded nor used)
+  // (with no ragged rows, a box past the extent only reads the map's zero fill along its 3rd dim)
+  const bool a_one = !AK && P.a3d && (m0 + BM <= P.a3d || P.a3d == P.M);
+  const bool b_one = !BKI && P.b3d && (n0 + BN <= P.b3d || P.b3d == P.N);
   int a_boxes = 0, b_boxes = 0;
-  if (!AK)
+  if (!AK && !a_one)
     for (int xb = 0; xb < BM / 16; ++xb) a_boxes += (m0 + xb * 16 < P.M);
-  if (!BKI)
+  if (!BKI && !b_one)
     for (int xb = 0; xb < BN / 16; ++xb) b_boxes += (n0 + xb * 16 < P.N);
-  tx_bytes = ((AK || P.a3d) ? C::A_BYTES : a_boxes * 2048) + ((BKI || P.b3d) ? C::B_BYTES : b_boxes * 2048);
+  tx_bytes = ((AK || a_one) ? C::A_BYTES : a_boxes * 2048) + ((BKI || b_one) ? C::B_BYTES : b_boxes * 2048);
+  if (threadIdx.x == 0 && nkt > 0) {
+    if (!AK && !a_one) ptx::prefetch_tmap(&tmA2);
+    if (!BKI && !b_one) ptx::prefetch_tmap(&tmB2);
+  }
   auto issue = [&](int i) {
     const int s = i % STAGES;
     uint8_t* sa = smem + s * STAGE_BYTES;
@@ -179,17 +193,17 @@ __global__ void __maxnreg__(C::MAXREG)
     const int k = (kt0 + i) * BK;
     if (AK) {
       ptx::tma_load_2d(sa, &tmA, &full[s], k, m0);
-    } else if (P.a3d) {
+    } else if (a_one) {
       ptx::tma_load_3d(sa, &tmA, &full[s], 0, k, m0 / 16);
     } else {
-      for (int xb = 0; xb < a_boxes; ++xb) ptx::tma_load_2d(sa + xb * 2048, &tmA, &full[s], m0 + xb * 16, k);
+      for (int xb = 0; xb < a_boxes; ++xb) ptx::tma_load_2d(sa + xb * 2048, &tmA2, &full[s], m0 + xb * 16, k);
     }
     if (BKI) {
       ptx::tma_load_2d(sb, &tmB, &full[s], k, n0);
-    } else if (P.b3d) {
+    } else if (b_one) {
       ptx::tma_load_3d(sb, &tmB, &full[s], 0, k, n0 / 16);
     } else {
-      for (int xb = 0; xb < b_boxes; ++xb) ptx::tma_load_2d(sb + xb * 2048, &tmB, &full[s], n0 + xb * 16, k);
+      for (int xb = 0; xb < b_boxes; ++xb) ptx::tma_load_2d(sb + xb * 2048, &tmB2, &full[s], n0 + xb * 16, k);
     }
   };
   if (threadIdx.x == 0)
@@ -405,12 +419,124 @@ __global__ void __launch_bounds__(128) gemm_small_kernel(const double* __restric
       }
 }
 
+// Same tile / flags / epilogue, operands streamed by cp.async through a 4-stage shared ring (the
+// whole k-range of a CTA is in flight after the prologue): the latency of a K <= 256 product is
+// about one L2 round trip plus its DMMAs.  Shared tiles keep the global contiguity of each operand
+// (rows of SLD = 36 doubles: conflict-free fragment reads for either orientation).  Needs 16-byte
+// aligned operands with even leading dimensions; gemm() falls back to gemm_small_kernel otherwise.
+constexpr int SA_STAGES = 4;
+constexpr int SA_TILE = ST * SLD;                              // doubles per operand tile
+constexpr int SA_SMEM = SA_STAGES * 2 * SA_TILE * 8;
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(128) gemm_small_async_kernel(const double* __restrict__ A, int64_t lda,
+                                                                const double* __restrict__ B, int64_t ldb,
+                                                                const KParamsS P) {
+  extern __shared__ __align__(16) double sa_smem[];
+  const int m0 = blockIdx.y * ST, n0 = blockIdx.x * ST;
+  if ((P.flags & SYM_LOWER) && m0 + ST - 1 < n0) return;   // tile strictly above the diagonal
+  int kbeg = 0, kend = P.K;
+  if (P.flags & A_KGE_M) kbeg = max(kbeg, m0);
+  if (P.flags & B_KGE_N) kbeg = max(kbeg, n0);
+  if (P.flags & A_KLE_M) kend = min(kend, m0 + ST);
+  if (P.flags & B_KLE_N) kend = min(kend, n0 + ST);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int nchunks = kend > kbeg ? (kend - kbeg + SKC - 1) / SKC : 0;
+  // operand X (rows x of extent XN, ld) in its stored orientation: KROWS = k is the strided index
+  // (tile [k][x], x contiguous), else x is strided (tile [x][k], k contiguous)
+  auto issue = [&](int chunk) {
+    const int kc = kbeg + chunk * SKC;
+    double* as = sa_smem + (chunk % SA_STAGES) * 2 * SA_TILE;
+    double* bs = as + SA_TILE;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int pidx = tid + 128 * u, row = pidx >> 4, c2 = 2 * (pidx & 15);
+      {  // A: !TA -> tile [k][m] (m contiguous); TA -> tile [m][k] (k contiguous)
+        const int k = TA ? kc + c2 : kc + row, m = TA ? m0 + row : m0 + c2;
+        int bytes;
+        if (TA) bytes = (m < P.M) ? min(max(kend - k, 0), 2) * 8 : 0;
+        else bytes = (k < kend) ? min(max(P.M - m, 0), 2) * 8 : 0;
+        const double* src = bytes ? (TA ? A + k + (int64_t)m * lda : A + m + (int64_t)k * lda) : A;
+        ptx::cp_async16(as + row * SLD + c2, src, bytes);
+      }
+      {  // B: TB -> op(B)[k][n] = B[n + k ldb]: tile [k][n]; !TB -> B[k + n ldb]: tile [n][k]
+        const int k = TB ? kc + row : kc + c2, n = TB ? n0 + c2 : n0 + row;
+        int bytes;
+        if (TB) bytes = (k < kend) ? min(max(P.N - n, 0), 2) * 8 : 0;
+        else bytes = (n < P.N) ? min(max(kend - k, 0), 2) * 8 : 0;
+        const double* src = bytes ? (TB ? B + n + (int64_t)k * ldb : B + k + (int64_t)n * ldb) : B;
+        ptx::cp_async16(bs + row * SLD + c2, src, bytes);
+      }
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < SA_STAGES - 1; ++s) {
+    if (s < nchunks) issue(s);
+    ptx::cp_async_commit();
+  }
+  double acc[2][2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int i = 0; i < nchunks; ++i) {
+    ptx::cp_async_wait<SA_STAGES - 2>();
+    __syncthreads();   // chunk i landed for every thread; stage (i-1) % S is free
+    if (i + SA_STAGES - 1 < nchunks) issue(i + SA_STAGES - 1);
+    ptx::cp_async_commit();
+    const double* as = sa_smem + (i % SA_STAGES) * 2 * SA_TILE;
+    const double* bs = as + SA_TILE;
+#pragma unroll
+    for (int k4 = 0; k4 < SKC / 4; ++k4) {
+      const int k = 4 * k4 + t;
+      double a[2], b[2];
+#pragma unroll
+      for (int f = 0; f < 2; ++f) {
+        const int m = 16 * wm + 8 * f + g, n = 16 * wn + 8 * f + g;
+        a[f] = TA ? as[m * SLD + k] : as[k * SLD + m];
+        b[f] = TB ? bs[k * SLD + n] : bs[n * SLD + k];
+      }
+#pragma unroll
+      for (int fm = 0; fm < 2; ++fm)
+#pragma unroll
+        for (int fn = 0; fn < 2; ++fn) ptx::dmma_8x8x4(acc[fm][fn][0], acc[fm][fn][1], a[fm], b[fn]);
+    }
+  }
+  ptx::cp_async_wait<0>();
+#pragma unroll
+  for (int fm = 0; fm < 2; ++fm)
+#pragma unroll
+    for (int fn = 0; fn < 2; ++fn)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int m = m0 + 16 * wm + 8 * fm + g, n = n0 + 16 * wn + 8 * fn + 2 * t + j;
+        if (m >= P.M || n >= P.N) continue;
+        if ((P.flags & SYM_LOWER) && m < n) continue;
+        epi_apply(P.epi, m, n, acc[fm][fn][j]);
+        if ((P.flags & SYM_MIRROR) && m > n) epi_apply(P.epi, n, m, acc[fm][fn][j]);
+      }
+}
+
 template <bool TA, bool TB>
 void launch_small(Ctx* c, const double* A, int64_t lda, const double* B, int64_t ldb, const KParamsS& P) {
   dim3 grid((unsigned)((P.N + ST - 1) / ST), (unsigned)((P.M + ST - 1) / ST));
   Prof pr(c, c->cur_tag);
-  gemm_small_kernel<TA, TB><<<grid, 128, 0, c->stream>>>(A, lda, B, ldb, P);
-  post_launch(c, "gemm_small_kernel");
+  const bool aligned = (reinterpret_cast<uintptr_t>(A) % 16 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0) &&
+                       lda % 2 == 0 && ldb % 2 == 0 && !c->no_small_async;
+  if (aligned) {
+    static bool attr = false;
+    if (!attr) {
+      CGGM_CUDA_CHECK(cudaFuncSetAttribute(gemm_small_async_kernel<TA, TB>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, SA_SMEM));
+      attr = true;
+    }
+    gemm_small_async_kernel<TA, TB><<<grid, 128, SA_SMEM, c->stream>>>(A, lda, B, ldb, P);
+    post_launch(c, "gemm_small_async_kernel");
+  } else {
+    gemm_small_kernel<TA, TB><<<grid, 128, 0, c->stream>>>(A, lda, B, ldb, P);
+    post_launch(c, "gemm_small_kernel");
+  }
 }
 
 CUtensorMap make_map_mn3d(Ctx* c, const double* ptr, int64_t ld, int64_t X, int64_t K, uint32_t bx) {
@@ -443,7 +569,8 @@ CUtensorMap make_map(Ctx* c, const double* ptr, int64_t ld, int64_t inner, int64
 }
 
 template <bool AK, bool BKI, class C>
-void launch(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KParams& P, int grid) {
+void launch(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& ma2, const CUtensorMap& mb2,
+            const KParams& P, int grid) {
   static bool attr_set = false;
   if (!attr_set) {
     CGGM_CUDA_CHECK(cudaFuncSetAttribute(gemm_dmma_kernel<AK, BKI, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -451,8 +578,34 @@ void launch(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KParams&
     attr_set = true;
   }
   Prof pr(c, c->cur_tag);
-  gemm_dmma_kernel<AK, BKI, C><<<grid, C::NTHREADS, C::SMEM_BYTES, c->stream>>>(ma, mb, P);
+  gemm_dmma_kernel<AK, BKI, C><<<grid, C::NTHREADS, C::SMEM_BYTES, c->stream>>>(ma, mb, ma2, mb2, P);
   post_launch(c, "gemm_dmma_kernel");
+}
+
+// CGGM_GEMM_LOG=1: one stderr line per launch with the MMA flops the tiles execute (triangular
+// k-ranges applied per tile), for joining with an ncu launch list (per-launch efficiency)
+void gemm_log(Ctx* c, int BM, int BN, int M, int N, int K, int flags, int grid, bool tA, bool tB) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("CGGM_GEMM_LOG");
+    on = e ? std::atoi(e) : 0;
+  }
+  if (!on) return;
+  const int tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
+  double fl = 0.0;
+  for (int I = 0; I < tm; ++I)
+    for (int J = 0; J < tn; ++J) {
+      if ((flags & SYM_LOWER) && I < J) continue;
+      const int m0 = I * BM, n0 = J * BN;
+      int kbeg = 0, kend = K;
+      if (flags & A_KGE_M) kbeg = std::max(kbeg, m0);
+      if (flags & B_KGE_N) kbeg = std::max(kbeg, n0);
+      if (flags & A_KLE_M) kend = std::min(kend, m0 + BM);
+      if (flags & B_KLE_N) kend = std::min(kend, n0 + BN);
+      if (kend > kbeg) fl += 2.0 * BM * BN * (double)(((kend - kbeg + 15) / 16) * 16);
+    }
+  std::fprintf(stderr, "GEMMLOG tile=%dx%d M=%d N=%d K=%d flags=%d tA=%d tB=%d grid=%d exec_flops=%.6e lane=%d\n", BM, BN,
+               M, N, K, flags, (int)tA, (int)tB, grid, fl, c->lane);
 }
 
 template <class C>
@@ -464,17 +617,24 @@ void run_cfg(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t Kef
   if (P.flags & SYM_LOWER) grid = P.tilesN * (P.tilesN + 1) / 2 + (P.tilesM - P.tilesN) * P.tilesN;
   else grid = P.tilesM * P.tilesN;
   // K-inner operand: dims {K, X}, box {16, BX}; MN-inner: dims {X, K}, box {16, 16}
-  P.a3d = (!transA && M % 16 == 0 && !c->no_tma3d) ? 1 : 0;
-  P.b3d = (transB && N % 16 == 0 && !c->no_tma3d) ? 1 : 0;
+  // MN-inner operand: the 3-D single-box map covers the leading multiple of 16 rows (so a box
+  // never reads past the extent); a 16-wide 2-D map serves the ragged last tile
+  const int64_t M16 = M / 16 * 16, N16 = N / 16 * 16;
+  P.a3d = (!transA && M16 > 0 && !c->no_tma3d) ? (int)M16 : 0;
+  P.b3d = (transB && N16 > 0 && !c->no_tma3d) ? (int)N16 : 0;
   CUtensorMap ma = transA ? make_map(c, A, lda, Keff, M, 16, C::BM)
-                          : (P.a3d ? make_map_mn3d(c, A, lda, M, Keff, C::BM) : make_map(c, A, lda, M, Keff, 16, 16));
-  CUtensorMap mb = transB ? (P.b3d ? make_map_mn3d(c, B, ldb, N, Keff, C::BN) : make_map(c, B, ldb, N, Keff, 16, 16))
+                          : (P.a3d ? make_map_mn3d(c, A, lda, M16, Keff, C::BM) : make_map(c, A, lda, M, Keff, 16, 16));
+  CUtensorMap mb = transB ? (P.b3d ? make_map_mn3d(c, B, ldb, N16, Keff, C::BN) : make_map(c, B, ldb, N, Keff, 16, 16))
                           : make_map(c, B, ldb, Keff, N, 16, C::BN);
+  const bool a_tail = !transA && P.a3d && M16 != M, b_tail = transB && P.b3d && N16 != N;
+  CUtensorMap ma2 = a_tail ? make_map(c, A, lda, M, Keff, 16, 16) : ma;
+  CUtensorMap mb2 = b_tail ? make_map(c, B, ldb, N, Keff, 16, 16) : mb;
   const bool AK = transA, BKI = !transB;
-  if (AK && BKI) launch<true, true, C>(c, ma, mb, P, grid);
-  else if (AK && !BKI) launch<true, false, C>(c, ma, mb, P, grid);
-  else if (!AK && BKI) launch<false, true, C>(c, ma, mb, P, grid);
-  else launch<false, false, C>(c, ma, mb, P, grid);
+  gemm_log(c, C::BM, C::BN, P.M, P.N, P.K, P.flags, grid, transA, transB);
+  if (AK && BKI) launch<true, true, C>(c, ma, mb, ma2, mb2, P, grid);
+  else if (AK && !BKI) launch<true, false, C>(c, ma, mb, ma2, mb2, P, grid);
+  else if (!AK && BKI) launch<false, true, C>(c, ma, mb, ma2, mb2, P, grid);
+  else launch<false, false, C>(c, ma, mb, ma2, mb2, P, grid);
 }
 
 bool tma_ok(const double* p, int64_t ld) {

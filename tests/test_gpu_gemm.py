@@ -12,13 +12,21 @@ pytestmark = pytest.mark.gpu
 A_KLE_M, A_KGE_M, B_KLE_N, B_KGE_N, SYM_LOWER, SYM_MIRROR = 1, 2, 4, 8, 16, 32
 
 
-@pytest.fixture(scope="module", params=[0, 1, 2, 5, 6], ids=["auto_small", "tile128", "tile64", "tile128_2d", "tile64_2d"])
+@pytest.fixture(scope="module", params=[0, 1, 2, 5, 6, "direct"],
+                ids=["auto_small", "tile128", "tile64", "tile128_2d", "tile64_2d", "auto_small_direct"])
 def ctx(request):
+    """auto_small: small shapes on the cp.async kernel; auto_small_direct: on the direct-load one."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
+    import os
     from paper_1509_04681_b200 import Context
-    c = Context(0)
-    c._check(c.lib.cggm_test_set_tile(c.h, request.param))
+    direct = request.param == "direct"
+    os.environ["CGGM_NO_SMALL_ASYNC"] = "1" if direct else "0"
+    try:
+        c = Context(0)
+    finally:
+        os.environ.pop("CGGM_NO_SMALL_ASYNC", None)
+    c._check(c.lib.cggm_test_set_tile(c.h, 0 if direct else request.param))
     return c
 
 
