@@ -163,6 +163,8 @@ cggm_status cggm_ctx_create(cggm_ctx** out, int device, cggm_dtype dtype, void* 
   if (const char* e = std::getenv("CGGM_LA_MIN")) c->la_min = std::atoi(e);
   if (const char* e = std::getenv("CGGM_NO_SMALL_ASYNC")) c->no_small_async = std::atoi(e);
   if (const char* e = std::getenv("CGGM_GRAPH")) c->use_graphs = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_SMALL_KMAX")) c->small_kmax = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_NO_ACTIVE_VEC")) c->no_active_vec = std::atoi(e);
   if (const char* e = std::getenv("CGGM_GRAPH_PROF")) c->graph_prof = std::atoi(e);
   cudaDriverEntryPointQueryResult q;
   void* fn = nullptr;

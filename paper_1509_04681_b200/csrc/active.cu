@@ -178,6 +178,203 @@ __global__ void __launch_bounds__(NT) k_active_onepass(int64_t nrows, const T* _
   }
 }
 
+// Vectorised variant (the path taken whenever the gradient columns are 16-byte aligned): each lane
+// loads a PAIR of rows per 64-row chunk (LDG.128 for fp64), flags are kept as two ballot words per
+// chunk (even rows, odd rows), and the per-element work is a handful of instructions -- the scalar
+// kernel above is issue-bound at ~40% of HBM bandwidth.  Same outputs and order: ascending rows per
+// column, the subgradient partials of each column summed in a fixed order.
+template <typename T>
+struct PairOf;
+template <>
+struct PairOf<double> {
+  using V = double2;
+};
+template <>
+struct PairOf<float> {
+  using V = float2;
+};
+
+template <bool LAM, typename T>
+__global__ void __launch_bounds__(NT, LAM ? 6 : 4) k_active_vec(int64_t nrows, const T* __restrict__ G, int64_t ldg,
+                                                   const int64_t* colptr, const int32_t* rowidx, const T* val,
+                                                   T lam, int penalize_diag, T tie_eps,
+                                                   unsigned long long* state, int32_t* out_row, int32_t* out_col,
+                                                   long long cap, long long* ties_col, double* sub_col,
+                                                   int64_t col0) {
+  using V = typename PairOf<T>::V;
+  extern __shared__ uint32_t sm[];
+  const int64_t j = col0 + blockIdx.x;
+  const int scan_rows = (int)(LAM ? j + 1 : nrows);
+  const int nch = (scan_rows + 63) >> 6;   // 64-row chunks
+  uint32_t* sup = sm;                      // [2c + h]: rows 64c + 32h .. +31 (bit = row & 31)
+  uint32_t* flg = sm + 2 * nch;            // [2c + e]: bit l = row 64c + 2l + e
+  __shared__ int wcnt[NW];
+  __shared__ double wsub[NW];
+  __shared__ long long wtie[NW];
+  __shared__ long long col_base;
+  for (int w = threadIdx.x; w < 2 * nch; w += NT) sup[w] = 0u;
+  __syncthreads();
+  for (int64_t t = colptr[j] + threadIdx.x; t < colptr[j + 1]; t += NT) {
+    const int32_t r = rowidx[t];
+    if (r < scan_rows && val[t] != T(0)) atomicOr(&sup[r >> 5], 1u << (r & 31));
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int per = (nch + NW - 1) / NW;
+  const int ca = min(nch, w * per), cb = min(nch, (w + 1) * per);
+  const T* gc = G + (j - col0) * ldg;
+  const V* gv = reinterpret_cast<const V*>(gc);
+  const int full_end = scan_rows >> 6;     // chunks [0, full_end) lie entirely inside the column
+  const int jj = (int)j;
+  const T lam_diag = (LAM && !penalize_diag) ? T(0) : lam;
+  int cnt = 0;
+  long long tc = 0;
+  double s0 = 0.0, s1 = 0.0;   // two accumulators (even / odd rows): shorter dependency chains
+  auto process = [&](int c, T x0, T x1) {
+    const int r = 64 * c + 2 * lane;
+    const bool in0 = r < scan_rows, in1 = r + 1 < scan_rows;
+    const uint32_t sw = sup[2 * c + (lane >> 4)];
+    const uint32_t sb = sw >> ((2 * lane) & 31);
+    const T l0 = (LAM && r == jj) ? lam_diag : lam;
+    const T l1 = (LAM && r + 1 == jj) ? lam_diag : lam;
+    const T d0 = fabs(x0) - l0, d1 = fabs(x1) - l1;
+    // cold chunk (the common case for Theta): no entry within tie_eps of its threshold or above it,
+    // no stored nonzero -> no flag, tie or subgradient contribution; one vote instead of the rest
+    const bool hot = (sb & 3u) || d0 >= -tie_eps || d1 >= -tie_eps;
+    if (!__any_sync(0xffffffffu, hot)) {
+      if (lane == 0) *reinterpret_cast<uint2*>(&flg[2 * c]) = make_uint2(0u, 0u);
+      return;
+    }
+    const bool sp0 = sb & 1u, sp1 = (sb >> 1) & 1u;
+    const bool f0 = in0 && (d0 > T(0) || sp0), f1 = in1 && (d1 > T(0) || sp1);
+    const unsigned m0 = __ballot_sync(0xffffffffu, f0), m1 = __ballot_sync(0xffffffffu, f1);
+    if (lane == 0) {
+      flg[2 * c] = m0;
+      flg[2 * c + 1] = m1;
+    }
+    cnt += __popc(m0) + __popc(m1);
+    tc += (in0 && !sp0 && fabs(d0) <= tie_eps) + (in1 && !sp1 && fabs(d1) <= tie_eps);
+    // LAM: rows i < j count twice (both triangles), the diagonal once
+    const double w0 = (LAM && r < jj) ? 2.0 : 1.0, w1 = (LAM && r + 1 < jj) ? 2.0 : 1.0;
+    if (in0 && d0 > T(0)) s0 += w0 * (double)d0;
+    if (in1 && d1 > T(0)) s1 += w1 * (double)d1;
+  };
+  const int fe = min(cb, full_end);
+  int c = ca;
+  if (LAM) {   // (the triangle's short columns: pipelining costs more registers than it hides)
+    for (; c + UNR <= fe; c += UNR) {
+      V v[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) v[u] = __ldcs(gv + (int64_t)(c + u) * 32 + lane);
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) process(c + u, v[u].x, v[u].y);
+    }
+  } else if (c + UNR <= fe) {
+    // software-pipelined: the next group's loads are in flight while the current one is processed
+    V cur[UNR], nxt[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) cur[u] = __ldcs(gv + (int64_t)(c + u) * 32 + lane);   // streamed once
+    for (; c + UNR <= fe; c += UNR) {
+      const bool more = c + 2 * UNR <= fe;
+      if (more) {
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) nxt[u] = __ldcs(gv + (int64_t)(c + UNR + u) * 32 + lane);
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) process(c + u, cur[u].x, cur[u].y);
+      if (more) {
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) cur[u] = nxt[u];
+      }
+    }
+  }
+  for (; c < cb; ++c) {   // remainder and the partial last chunk (element loads, bounds-checked)
+    const int r = 64 * c + 2 * lane;
+    const T x0 = r < scan_rows ? __ldcs(gc + r) : T(0);
+    const T x1 = r + 1 < scan_rows ? __ldcs(gc + r + 1) : T(0);
+    process(c, x0, x1);
+  }
+  double sacc = s0 + s1;
+  for (int64_t t = colptr[j] + threadIdx.x; t < colptr[j + 1]; t += NT) {
+    const T x = val[t];
+    if (x == T(0)) continue;
+    const int64_t i = rowidx[t];   // every stored entry of the column, both triangles for Lambda
+    const T gi = gc[i];
+    const T lm = lam_of<LAM>(i, j, lam, penalize_diag);
+    sacc += (double)fabs(gi + lm * (x > T(0) ? T(1) : T(-1))) - (double)fmax(fabs(gi) - lm, T(0));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sacc += __shfl_down_sync(0xffffffffu, sacc, o);
+    tc += __shfl_down_sync(0xffffffffu, tc, o);
+  }
+  if (lane == 0) {
+    wcnt[w] = cnt;
+    wsub[w] = sacc;
+    wtie[w] = tc;
+  }
+  __syncthreads();
+  if (w == 0) {
+    long long total = 0, tt = 0;
+    double ss = 0.0;
+    for (int k = 0; k < NW; ++k) {
+      total += wcnt[k];
+      tt += wtie[k];
+      ss += wsub[k];
+    }
+    if (lane == 0) {
+      sub_col[j] = ss;
+      ties_col[j] = tt;
+      st_release(&state[j], (j == 0 ? ST_INC : ST_AGG) | (unsigned long long)total);
+    }
+    long long excl = 0;
+    int64_t k0 = j - 1;
+    while (k0 >= 0) {
+      const int64_t k = k0 - lane;
+      unsigned long long v = (k >= 0) ? ld_acquire(&state[k]) : ST_INC;
+      while (__any_sync(0xffffffffu, (v & ~ST_VAL) == 0)) {
+        if ((v & ~ST_VAL) == 0) v = ld_acquire(&state[k]);
+      }
+      const unsigned inc = __ballot_sync(0xffffffffu, (v & ~ST_VAL) == ST_INC);
+      const int stop = inc ? __ffs(inc) - 1 : 31;
+      long long add = (lane <= stop && k >= 0) ? (long long)(v & ST_VAL) : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
+      excl += add;
+      if (inc) break;
+      k0 -= 32;
+    }
+    if (lane == 0) {
+      if (j > 0) st_release(&state[j], ST_INC | (unsigned long long)(excl + total));
+      col_base = excl;
+    }
+  }
+  __syncthreads();
+  long long pos = col_base;
+  for (int k = 0; k < w; ++k) pos += wcnt[k];
+  const unsigned below = (1u << lane) - 1u;
+  for (int cc = ca; cc < cb; ++cc) {
+    const unsigned m0 = flg[2 * cc], m1 = flg[2 * cc + 1];
+    if ((m0 | m1) == 0u) continue;   // warp-uniform
+    const long long base = pos + __popc(m0 & below) + __popc(m1 & below);
+    const int r = 64 * cc + 2 * lane;
+    if ((m0 >> lane) & 1u) {
+      if (base < cap) {
+        out_row[base] = r;
+        out_col[base] = (int32_t)j;
+      }
+    }
+    if ((m1 >> lane) & 1u) {
+      const long long p1 = base + ((m0 >> lane) & 1u);
+      if (p1 < cap) {
+        out_row[p1] = r + 1;
+        out_col[p1] = (int32_t)j;
+      }
+    }
+    pos += __popc(m0) + __popc(m1);
+  }
+}
+
 // totals: m from the last column's inclusive state, ties / subgradient summed in fixed order
 constexpr int TOT_NT = 1024;
 __global__ void __launch_bounds__(TOT_NT) k_active_totals(int64_t ncols, const unsigned long long* state,
@@ -210,6 +407,13 @@ __global__ void __launch_bounds__(TOT_NT) k_active_totals(int64_t ncols, const u
 }
 
 size_t smem_bytes(int64_t rows) { return (size_t)((rows + 31) / 32) * 4 * 2; }
+size_t smem_bytes_vec(int64_t rows) { return (size_t)((rows + 63) / 64) * 4 * 4; }
+
+// the pair loads need 2*sizeof(T)-aligned columns
+template <typename T>
+bool vec_ok(const T* G, int64_t ldg, int no_vec) {
+  return !no_vec && (reinterpret_cast<uintptr_t>(G) % (2 * sizeof(T)) == 0) && (ldg % 2 == 0);
+}
 
 template <typename K>
 void set_smem(K kernel, size_t bytes) {
@@ -242,9 +446,18 @@ void active_lambda(Ctx* c, int64_t q, const T* GradL, int64_t ldgl, const cggm_c
                    int penalize_diag, double tie_eps, const ActWs& ws, int32_t* L_row, int32_t* L_col,
                    long long capL) {
   if (q == 0) return;
+  Prof pr(c, TAG_ACTIVE);
+  if (vec_ok(GradL, ldgl, c->no_active_vec)) {
+    const size_t bv = smem_bytes_vec(q);
+    set_smem(k_active_vec<true, T>, bv);
+    k_active_vec<true, T><<<(unsigned)q, NT, bv, c->stream>>>(
+        q, GradL, ldgl, Lambda->colptr, Lambda->rowidx, static_cast<const T*>(Lambda->val), (T)lam_L, penalize_diag,
+        (T)tie_eps, ws.stateL, L_row, L_col, capL, ws.tieL, ws.subL, 0);
+    post_launch(c, "k_active_vec<L>");
+    return;
+  }
   const size_t bl = smem_bytes(q);
   set_smem(k_active_onepass<true, T>, bl);
-  Prof pr(c, TAG_ACTIVE);
   k_active_onepass<true, T><<<(unsigned)q, NT, bl, c->stream>>>(
       q, GradL, ldgl, Lambda->colptr, Lambda->rowidx, static_cast<const T*>(Lambda->val), (T)lam_L, penalize_diag,
       (T)tie_eps, ws.stateL, L_row, L_col, capL, ws.tieL, ws.subL, 0);
@@ -256,9 +469,18 @@ void active_theta_chunk(Ctx* c, int64_t p, int64_t col0, int64_t ncols, const T*
                         const cggm_csc* Theta, double lam_T, double tie_eps, const ActWs& ws, int32_t* T_row,
                         int32_t* T_col, long long capT) {
   if (ncols == 0) return;
+  Prof pr(c, TAG_ACTIVE);
+  if (vec_ok(G, ldg, c->no_active_vec)) {
+    const size_t bv = smem_bytes_vec(p);
+    set_smem(k_active_vec<false, T>, bv);
+    k_active_vec<false, T><<<(unsigned)ncols, NT, bv, c->stream>>>(
+        p, G, ldg, Theta->colptr, Theta->rowidx, static_cast<const T*>(Theta->val), (T)lam_T, 1, (T)tie_eps,
+        ws.stateT, T_row, T_col, capT, ws.tieT, ws.subT, col0);
+    post_launch(c, "k_active_vec<T>");
+    return;
+  }
   const size_t bt = smem_bytes(p);
   set_smem(k_active_onepass<false, T>, bt);
-  Prof pr(c, TAG_ACTIVE);
   k_active_onepass<false, T><<<(unsigned)ncols, NT, bt, c->stream>>>(
       p, G, ldg, Theta->colptr, Theta->rowidx, static_cast<const T*>(Theta->val), (T)lam_T, 1, (T)tie_eps,
       ws.stateT, T_row, T_col, capT, ws.tieT, ws.subT, col0);

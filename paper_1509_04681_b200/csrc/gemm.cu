@@ -653,7 +653,14 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
   // (an output aliasing an operand -- an in-place B := B X^T with N <= 64 -- needs one CTA per row
   // panel, which only the TMA kernels guarantee)
   const bool aliased = epi.out1 == A || epi.out1 == B || (epi.out2 && (epi.out2 == A || epi.out2 == B));
-  if (K <= 256 && (M <= 128 || N <= 128) && !aliased && c->force_tile != 1 && c->force_tile != 2) {
+  // small shapes, and mid-size products whose 64x64 grid would leave most SMs idle (the middle of
+  // the recursion: 4x the CTAs of a 64-tile grid with the whole k-range streamed by cp.async)
+  const int64_t tiles64 = ((M + 63) / 64) * ((N + 63) / 64);
+  const bool small_shape = K <= 256 && (M <= 128 || N <= 128);
+  const bool mid_shape = K <= c->small_kmax && tiles64 < c->num_sms && !c->no_small_async &&
+                         (reinterpret_cast<uintptr_t>(A) % 16 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0) &&
+                         lda % 2 == 0 && ldb % 2 == 0;
+  if ((small_shape || mid_shape) && !aliased && c->force_tile != 1 && c->force_tile != 2) {
     KParamsS S;
     S.M = (int)M; S.N = (int)N; S.K = (int)(K > 0 ? K : 0); S.flags = flags; S.epi = epi;
     if (transA && transB) launch_small<true, true>(c, A, lda, B, ldb, S);

@@ -16,7 +16,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="large")
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--steps", type=int, default=1)
-ap.add_argument("--part", default="all", choices=["all", "invert", "psi", "objective"])
+ap.add_argument("--part", default="all", choices=["all", "invert", "psi", "objective", "active"])
 args = ap.parse_args()
 
 P = make_problem(args.config)
@@ -41,6 +41,9 @@ def step():
         ctx.cggm_invert_logdet(L, Sigma=Sigma)
     elif args.part == "psi":
         ctx.cggm_psi_grad(X, Y, T, Sigma, Syy=Syy, out=bufs)
+    elif args.part == "active":
+        ctx.cggm_active_set(bufs["GradL"], bufs["GradT"], L, T, P.lam_L, P.lam_T,
+                            cap_L=int(cnt["m_L"]) + 1024, cap_T=int(cnt["m_T"]) + 1024)
     else:
         ctx.cggm_objective(X, Y, L, T, P.lam_L, P.lam_T)
 
