@@ -361,23 +361,25 @@ def main():
             d["tflops"] = ph_flops[tag] / (tms / prof_steps * 1e-3) / 1e12
         phases[tag] = d
 
-    # HBM-bound phases: algorithmic bytes / measured time in pass B
+    # HBM-bound phases: algorithmic bytes per step / the phase's measured time per
+    # step in pass B (every launch of the phase bracketed by its own CUDA events)
     m_L, m_T = last["active"]["m_L"], last["active"]["m_T"]
     q_, p_, n_ = P.q, P.p, P.n
+    spmm_calls = phases.get("spmm", {}).get("launches_per_step", 1.0)
     hbm_alg = {
-        "active_set": 8.0 * (q_ * (q_ + 1) / 2 + p_ * q_) + 8.0 * (m_L + m_T),   # one read of grad_L (upper), grad_T + lists
-        "grad_lambda": 32.0 * q_ * q_,                                            # read S_yy, Sigma, Psi, write grad_L
-        "spmm": 8.0 * n_ * (p_ + q_),                                             # read X once, write W
+        # one read of grad_Lambda's upper triangle and of grad_Theta (stored, or its streamed column
+        # chunks), 8 bytes written per active entry
+        "active_set": 8.0 * (q_ * (q_ + 1) / 2 + p_ * q_) + 8.0 * (m_L + m_T),
+        "grad_lambda": 32.0 * q_ * q_,                       # read S_yy, Sigma, Psi, write grad_Lambda
+        "spmm": 8.0 * n_ * (p_ + q_) * spmm_calls,           # per call: read X once, write W
     }
     hbm = {}
     for tag, by in hbm_alg.items():
-        if tag in prof and prof[tag][1] > 0:
-            calls = {"active_set": 4, "grad_lambda": 1, "spmm": 1}[tag]       # launches per call
-            n_calls = max(1, round(prof[tag][1] / calls))                     # calls in pass B
-            ms_call = prof[tag][0] / n_calls
-            gbs = by / (ms_call * 1e-3) / 1e9
-            hbm[tag] = {"alg_bytes_per_call": by, "ms_per_call": ms_call, "calls_per_step": n_calls / prof_steps,
-                        "achieved_gbs": gbs, "frac_of_measured_copy": gbs / HBM_PEAK_GBS}
+        if tag in phases:
+            ms_s = phases[tag]["ms_per_step"]
+            gbs = by / (ms_s * 1e-3) / 1e9
+            hbm[tag] = {"alg_bytes_per_step": by, "ms_per_step": ms_s, "achieved_gbs": gbs,
+                        "frac_of_measured_copy": gbs / HBM_PEAK_GBS}
 
     # ---------------------------------------------------------------- e2e through the public API
     e2e = None

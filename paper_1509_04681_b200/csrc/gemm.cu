@@ -31,6 +31,7 @@ namespace {
 constexpr int BK = 16;
 constexpr int STAGES = 4;
 constexpr int GROUP_N = 8;
+constexpr int SYM_BAND = 8;   // tile rows per band of a SYM_LOWER raster
 
 // CTA tile BM_ x BN_ computed by WM_ x WN_ warps (warp tile (BM_/WM_) x (BN_/WN_), fragments of 8)
 template <int BM_, int BN_, int WM_, int WN_>
@@ -71,14 +72,35 @@ struct KParams {
 // Triangular k-ranges are scheduled longest-first (LPT) to shorten the tail wave.
 __device__ __forceinline__ void tile_coords(const KParams& P, int t, int& I, int& J) {
   if (P.flags & SYM_LOWER) {
-    // lower triangle part: rows I < tilesN, enumerated row-major (I ascending, J <= I)
+    // lower triangle part (rows I < tilesN) in bands of SYM_BAND tile rows, band by band (I
+    // ascending: longest k-ranges first for A_KGE_M / B_KGE_N), column by column inside a band:
+    // the CTAs in flight share the band's row panels and each column panel, so the panels are read
+    // from DRAM about once per band instead of once per tile
     const long long tri = (long long)P.tilesN * (P.tilesN + 1) / 2;
     if (t < tri) {
-      int i = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
-      while ((long long)(i + 1) * (i + 2) / 2 <= t) ++i;
-      while ((long long)i * (i + 1) / 2 > t) --i;
-      I = i;
-      J = t - (int)((long long)i * (i + 1) / 2);
+      long long L = t;
+      int r0 = 0;
+      for (;;) {
+        const int h = min(SYM_BAND, P.tilesN - r0);
+        const long long cnt = (long long)h * r0 + (long long)h * (h + 1) / 2;
+        if (L < cnt) {
+          if (L < (long long)h * r0) {
+            J = (int)(L / h);
+            I = r0 + (int)(L % h);
+          } else {
+            int l2 = (int)(L - (long long)h * r0), j = r0;
+            while (l2 >= r0 + h - j) {
+              l2 -= r0 + h - j;
+              ++j;
+            }
+            J = j;
+            I = j + l2;
+          }
+          break;
+        }
+        L -= cnt;
+        r0 += h;
+      }
     } else {
       const int r = t - (int)tri;  // rectangular part below: rows tilesN .. tilesM-1
       I = P.tilesN + r / P.tilesN;
