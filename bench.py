@@ -336,6 +336,12 @@ def main():
     else:
         step_prof = step
     torch.cuda.synchronize()
+    # pass B without the recursion lookahead: every kernel runs alone on its stream, so the sum of
+    # per-launch durations is the GEMM family's own time (concurrent side-stream launches would
+    # each be charged the shared wall time)
+    ctx.set_option(_abi.CGGM_OPT_LOOKAHEAD_MIN, 0)
+    step_prof()
+    torch.cuda.synchronize()
     ctx.profile(True)
     e0.record(stream)
     for _ in range(prof_steps):
@@ -345,6 +351,7 @@ def main():
     prof_elapsed = e0.elapsed_time(e1)
     prof = ctx.profile_read()
     ctx.profile(False)
+    ctx.set_option(_abi.CGGM_OPT_LOOKAHEAD_MIN, 256)
 
     ms_step = elapsed / args.steps
     value = args.steps / (elapsed / 1e3)
@@ -442,8 +449,8 @@ def main():
                          "peak_source": f"live DMMA.8x8x4 microbenchmark on this GPU ({args.peak_seconds:.1f} s, "
                                         "2 CTAs/SM); MEASURED_PEAKS.json has no FP64 entry",
                          "gemm_ms_per_step": gemm_ms, "gemm_alg_flops_per_step": gemm_flops,
-                         "measured_in": f"profiled pass B ({prof_steps} steps, separate calls, per-launch CUDA "
-                                        f"events; {prof_elapsed / prof_steps:.1f} ms/step)",
+                         "measured_in": f"profiled pass B ({prof_steps} steps, separate calls without lookahead, "
+                                        f"per-launch CUDA events; {prof_elapsed / prof_steps:.1f} ms/step)",
                          "step_frac_of_peak": all_flops / (ms_step * 1e-3) / 1e12 / peak_tflops},
             "phases": phases,
             "hbm_roofline": {"peak_gbs": HBM_PEAK_GBS, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)",

@@ -110,6 +110,16 @@ cggm_status cggm_ctx_destroy(cggm_ctx* ctx);
 cggm_status cggm_ctx_set_stream(cggm_ctx* ctx, void* cuda_stream);
 /* Validation level: 0 = host-side argument checks only, 1 = also device CSC checks (default). */
 cggm_status cggm_ctx_set_validate(cggm_ctx* ctx, int level);
+/* Scheduling options (performance only; results are identical up to summation order, which no
+ * option changes for a given argument set):
+ *   CGGM_OPT_LOOKAHEAD_MIN: recursive Cholesky lookahead -- trailing updates / block products of at
+ *     least this width run on lower-priority side streams while the recursion proceeds (default
+ *     256; 0 = everything on one stream, each kernel's duration its own);
+ *   CGGM_OPT_GRAPHS: 1 = cggm_newton_eval captures its launches into a CUDA graph on the second
+ *     call with the same arguments and replays it afterwards (default), 0 = plain stream launches.
+ * Unknown option -> CGGM_ERR_INVALID_ARG. */
+typedef enum cggm_option { CGGM_OPT_LOOKAHEAD_MIN = 0, CGGM_OPT_GRAPHS = 1 } cggm_option;
+cggm_status cggm_ctx_set_option(cggm_ctx* ctx, int option, int64_t value);
 /* Number of library kernels launched on this ctx so far (for launch accounting). */
 cggm_status cggm_ctx_launch_count(cggm_ctx* ctx, int64_t* count);
 /* Release the cached internal workspace. */

@@ -24,6 +24,8 @@ STATUS = {
 }
 CGGM_F64 = 0
 CGGM_F32 = 1
+CGGM_OPT_LOOKAHEAD_MIN = 0
+CGGM_OPT_GRAPHS = 1
 PROF_NTAGS = 14
 
 
@@ -55,6 +57,7 @@ SIGNATURES = {
     "cggm_ctx_destroy": (c_i32, [c_vp]),
     "cggm_ctx_set_stream": (c_i32, [c_vp, c_vp]),
     "cggm_ctx_set_validate": (c_i32, [c_vp, c_i32]),
+    "cggm_ctx_set_option": (c_i32, [c_vp, c_i32, c_i64]),
     "cggm_ctx_launch_count": (c_i32, [c_vp, ctypes.POINTER(c_i64)]),
     "cggm_ctx_release_workspace": (c_i32, [c_vp]),
     "cggm_last_error": (ctypes.c_char_p, [c_vp]),

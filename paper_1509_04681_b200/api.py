@@ -114,6 +114,11 @@ class Context:
     def _sync_stream(self):
         self.lib.cggm_ctx_set_stream(self.h, ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream))
 
+    def set_option(self, option: int, value: int):
+        """Scheduling options (include/cggm.h cggm_ctx_set_option): _abi.CGGM_OPT_LOOKAHEAD_MIN,
+        _abi.CGGM_OPT_GRAPHS."""
+        self._check(self.lib.cggm_ctx_set_option(self.h, int(option), int(value)))
+
     def profile(self, enable: bool):
         self._check(self.lib.cggm_ctx_profile(self.h, int(bool(enable))))
 

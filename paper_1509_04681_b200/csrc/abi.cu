@@ -227,6 +227,23 @@ cggm_status cggm_ctx_set_stream(cggm_ctx* ctx, void* s) {
   return CGGM_OK;
 }
 
+cggm_status cggm_ctx_set_option(cggm_ctx* ctx, int option, int64_t value) {
+  if (!ctx) return CGGM_ERR_INVALID_ARG;
+  Ctx* c = &ctx->impl;
+  switch (option) {
+    case CGGM_OPT_LOOKAHEAD_MIN:
+      if (value < 0) return CGGM_ERR_INVALID_ARG;
+      c->la_min = (int)std::min<int64_t>(value, 1 << 30);
+      return CGGM_OK;
+    case CGGM_OPT_GRAPHS:
+      if (value != 0 && value != 1) return CGGM_ERR_INVALID_ARG;
+      c->use_graphs = (int)value;
+      return CGGM_OK;
+    default:
+      return CGGM_ERR_INVALID_ARG;
+  }
+}
+
 cggm_status cggm_ctx_set_validate(cggm_ctx* ctx, int level) {
   if (!ctx || level < 0) return CGGM_ERR_INVALID_ARG;
   ctx->impl.validate = level;

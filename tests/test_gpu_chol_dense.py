@@ -69,3 +69,23 @@ def test_first_failing_pivot(ctx, q, bad):
     for full in (True, False):
         _, _, fc = _run(ctx, A, full)
         assert fc == bad
+
+
+def test_lookahead_option_same_result(ctx):
+    """CGGM_OPT_LOOKAHEAD_MIN only changes the schedule (side streams), not the arithmetic: the
+    inverse with lookahead off and on at a small threshold agrees to the last bits."""
+    from paper_1509_04681_b200 import _abi
+    q = 3000
+    A = _spd(q, 11)
+    ctx.set_option(_abi.CGGM_OPT_LOOKAHEAD_MIN, 0)
+    try:
+        X0, l0, _ = _run(ctx, A, True)
+        ctx.set_option(_abi.CGGM_OPT_LOOKAHEAD_MIN, 128)
+        X1, l1, _ = _run(ctx, A, True)
+    finally:
+        ctx.set_option(_abi.CGGM_OPT_LOOKAHEAD_MIN, 256)
+    assert np.linalg.norm(np.tril(X0) - np.tril(X1)) <= 1e-15 * np.linalg.norm(np.tril(X0))
+    assert abs(l0 - l1) <= 1e-13 * abs(l0)
+    from paper_1509_04681_b200.api import CggmError
+    with pytest.raises(CggmError):
+        ctx.set_option(99, 1)
