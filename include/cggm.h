@@ -199,6 +199,45 @@ cggm_status cggm_objective(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int6
                            double lam_L, double lam_T, int32_t penalize_diag,
                            const void* W, int64_t ldw, cggm_objective_out* out);
 
+/* ---- NEXT-1 / NEXT-2: the coordinate-descent consumers of Algorithm 1 ------- */
+/* S_xx = X^T X / n_total (p x p, full symmetric, both triangles written; ldsxx >= p).  Used only by
+ * the Theta sweep (the hot path itself never forms S_xx). */
+cggm_status cggm_gram(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64_t p, const void* X, int64_t ldx,
+                      void* Sxx, int64_t ldsxx);
+/* Newton direction D_Lambda of Eq. (6) by `passes` coordinate-descent sweeps over the
+ * active list (L_row[k] <= L_col[k], column-major, as cggm_active_set writes it), maintaining
+ * U = D Sigma (library workspace).  Update of entry k = (i, j):
+ *   a = S_ij^2 + S_ii S_jj + S_ii P_jj + S_jj P_ii + 2 S_ij P_ij  (i != j),  S_ii^2 + 2 S_ii P_ii (i == j)
+ *   b = GradL_ij + (S D S)_ij + (P D S)_ij + (P D S)_ji,  c = Lambda_ij + D_k,
+ *   D_k += -c + S_{lam/a}(c - b/a)          (appendix P:1184-1195 with reading A15)
+ * with S = Sigma, P = Psi (q x q device, symmetric), lam = 0 for an unpenalised diagonal.
+ * D: m_L device doubles, written (the sweep starts from D = 0).  Host outputs (nullable):
+ * delta[0] = tr(GradL^T D), delta[1] = lam-weighted ||Lambda + D||_1 - ||Lambda||_1 (their sum is the
+ * Armijo decrease measure, reading A16); l1_lambda = ||Lambda||_1 over all entries.  fp64 ctx only. */
+cggm_status cggm_lambda_direction(cggm_ctx* ctx, int64_t q, const void* Sigma, int64_t ldsigma, const void* Psi,
+                                  int64_t ldpsi, const void* GradL, int64_t ldgl, const cggm_csc* Lambda,
+                                  const int32_t* L_row, const int32_t* L_col, int64_t m_L, double lam_L,
+                                  int penalize_diag, int passes, void* D, double* delta, double* l1_lambda);
+/* The line-search candidate Lambda + alpha D as a symmetric CSC over the active list
+ * and its mirror.  out: nrows = ncols = q, colptr (q+1 device int64), rowidx/val device arrays of
+ * capacity out->nnz on entry (>= 2 m_L); on return out->nnz = stored entries (rows sorted per
+ * column; entries that became 0 stay stored).  Lambda's nonzeros must all be on the list (they are,
+ * by the definition of S_Lambda).  CGGM_ERR_CAPACITY if the arrays are too small. */
+cggm_status cggm_lambda_step(cggm_ctx* ctx, int64_t q, const cggm_csc* Lambda, const int32_t* L_row,
+                             const int32_t* L_col, int64_t m_L, const void* D, double alpha, cggm_csc* out);
+/* Eq. (7) by `passes` coordinate-descent sweeps over the Theta active list (column-
+ * major), maintaining V = Theta Sigma (library workspace):
+ *   a = 2 Sigma_jj (S_xx)_ii,  b = 2 (S_xy)_ij + 2 (S_xx Theta Sigma)_ij,  c = Theta_ij,
+ *   Theta_ij += -c + S_{lam/a}(c - b/a)      (appendix P:1196-1207 with reading A15).
+ * Sigma (q x q), Sxx (p x p, cggm_gram), Sxy (p x q, cggm_covariances) device; Theta = the current
+ * iterate (its nonzeros are on the list).  out: the new Theta as a CSC over the list (colptr q+1,
+ * rowidx/val capacity out->nnz >= m_T on entry, out->nnz = m_T on return).  l1_theta (host,
+ * nullable) = ||Theta_new||_1.  The out arrays must not alias Theta's.  fp64 ctx only. */
+cggm_status cggm_theta_cd(cggm_ctx* ctx, int64_t p, int64_t q, const void* Sigma, int64_t ldsigma, const void* Sxx,
+                          int64_t ldsxx, const void* Sxy, int64_t ldsxy, const cggm_csc* Theta, const int32_t* T_row,
+                          const int32_t* T_col, int64_t m_T, double lam_T, int passes, cggm_csc* out,
+                          double* l1_theta);
+
 /* ---- composite: one Newton-iteration evaluation -------------------
  * Same results as cggm_invert_logdet(Lambda) + cggm_psi_grad(residual route, fused active sets)
  * + cggm_objective(Lambda_trial = Lambda, Theta) on one GPU (n samples, no sharding), with the

@@ -89,6 +89,14 @@ SIGNATURES = {
     "cggm_test_profile_dump": (c_i32, [c_vp, ctypes.c_char_p]),
     "cggm_test_chol_dense": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_i32, ctypes.POINTER(c_d),
                                      ctypes.POINTER(c_i64)]),
+    "cggm_gram": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64]),
+    "cggm_lambda_direction": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, ctypes.POINTER(cggm_csc),
+                                      c_vp, c_vp, c_i64, c_d, c_i32, c_i32, c_vp, ctypes.POINTER(c_d),
+                                      ctypes.POINTER(c_d)]),
+    "cggm_lambda_step": (c_i32, [c_vp, c_i64, ctypes.POINTER(cggm_csc), c_vp, c_vp, c_i64, c_vp, c_d,
+                                 ctypes.POINTER(cggm_csc)]),
+    "cggm_theta_cd": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, ctypes.POINTER(cggm_csc),
+                              c_vp, c_vp, c_i64, c_d, c_i32, ctypes.POINTER(cggm_csc), ctypes.POINTER(c_d)]),
     "cggm_objective": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64,
                                ctypes.POINTER(cggm_csc), ctypes.POINTER(cggm_csc), c_d, c_d, c_i32,
                                c_vp, c_i64, ctypes.POINTER(cggm_objective_out)]),

@@ -187,13 +187,16 @@ class Context:
         ao = None
         if fused is not None:
             ao = self._active_struct(fused)
-        self._check(self.lib.cggm_psi_grad(
+        st = self.lib.cggm_psi_grad(
             self.h, n, n_total, p, q, _ptr(X), ld_of(X), _ptr(Y), ld_of(Y), ctypes.byref(ts),
             _ptr(Sigma), ld_of(Sigma), _ptr(Syy), ld_of(Syy) if Syy is not None else 1,
             _ptr(Sxy), ld_of(Sxy) if Sxy is not None else 1,
             _ptr(Psi), ld_of(Psi), _ptr(GradL), ld_of(GradL) if GradL is not None else 1,
             _ptr(GradT), ld_of(GradT) if GradT is not None else 1,
-            ctypes.byref(ls) if ls is not None else None, ctypes.byref(ao) if ao is not None else None))
+            ctypes.byref(ls) if ls is not None else None, ctypes.byref(ao) if ao is not None else None)
+        if ao is not None:   # required list sizes, also under CGGM_ERR_CAPACITY (two-call pattern)
+            self.last_active_sizes = (int(ao.m_L), int(ao.m_T))
+        self._check(st)
         res = dict(Psi=Psi, GradL=GradL, GradT=GradT)
         if ao is not None:
             res["active"] = self._active_result(ao, fused)
@@ -276,6 +279,69 @@ class Context:
                     tr_sigma_m=o.tr_sigma_m, pen_L=o.pen_L, pen_T=o.pen_T, is_pd=bool(o.is_pd),
                     fail_col=int(o.fail_col))
 
+
+    # ---------------------------------------------------------------- NEXT-1 / NEXT-2
+    def cggm_gram(self, X, n_total=None, Sxx=None):
+        """S_xx = X^T X / n (p x p), for the Theta sweep."""
+        self._sync_stream()
+        n, p = X.shape
+        n_total = n if n_total is None else n_total
+        if Sxx is None:
+            Sxx = colmajor_empty(p, p, device=X.device, dtype=self.tdtype)
+        self._check(self.lib.cggm_gram(self.h, n, n_total, p, _ptr(X), ld_of(X), _ptr(Sxx), ld_of(Sxx)))
+        return Sxx
+
+    def cggm_lambda_direction(self, Sigma, Psi, GradL, Lam: DeviceCsc, L_row, L_col, lam_L, penalize_diag=True,
+                              passes=1, D=None):
+        """D_Lambda of Eq. (6) on the active list; returns (D, delta = tr(G^T D) + penalty change,
+        ||Lambda||_1)."""
+        self._sync_stream()
+        q = Sigma.shape[0]
+        m = int(L_row.numel())
+        if D is None:
+            D = torch.empty(max(m, 1), dtype=torch.float64, device=Sigma.device)
+        dl = (ctypes.c_double * 2)()
+        l1 = ctypes.c_double()
+        cs = Lam.c_struct()
+        self._check(self.lib.cggm_lambda_direction(
+            self.h, q, _ptr(Sigma), ld_of(Sigma), _ptr(Psi), ld_of(Psi), _ptr(GradL), ld_of(GradL), ctypes.byref(cs),
+            _ptr(L_row), _ptr(L_col), m, float(lam_L), int(bool(penalize_diag)), int(passes), _ptr(D), dl,
+            ctypes.byref(l1)))
+        return D[:m], dl[0] + dl[1], l1.value
+
+    def cggm_lambda_step(self, Lam: DeviceCsc, L_row, L_col, D, alpha, out: DeviceCsc | None = None) -> DeviceCsc:
+        """Lambda + alpha D as a symmetric CSC over the active list (and its mirror)."""
+        self._sync_stream()
+        q = Lam.nrows
+        m = int(L_row.numel())
+        dev = Lam.colptr.device
+        if out is None or out.rowidx.numel() < 2 * m:
+            out = DeviceCsc(q, q, torch.zeros(q + 1, dtype=torch.int64, device=dev),
+                            torch.empty(max(2 * m, 1), dtype=torch.int32, device=dev),
+                            torch.empty(max(2 * m, 1), dtype=torch.float64, device=dev))
+        oc = _abi.cggm_csc(q, q, int(out.rowidx.numel()), out.colptr.data_ptr(), out.rowidx.data_ptr(),
+                           out.val.data_ptr())
+        cs = Lam.c_struct()
+        self._check(self.lib.cggm_lambda_step(self.h, q, ctypes.byref(cs), _ptr(L_row), _ptr(L_col), m, _ptr(D),
+                                              float(alpha), ctypes.byref(oc)))
+        return DeviceCsc(q, q, out.colptr, out.rowidx[:oc.nnz], out.val[:oc.nnz])
+
+    def cggm_theta_cd(self, Sigma, Sxx, Sxy, Theta: DeviceCsc, T_row, T_col, lam_T, passes=1):
+        """One (or `passes`) Theta sweeps of Eq. (7); returns (new Theta CSC, ||Theta||_1)."""
+        self._sync_stream()
+        p, q = Theta.nrows, Theta.ncols
+        m = int(T_row.numel())
+        dev = Sigma.device
+        out = DeviceCsc(p, q, torch.zeros(q + 1, dtype=torch.int64, device=dev),
+                        torch.empty(max(m, 1), dtype=torch.int32, device=dev),
+                        torch.empty(max(m, 1), dtype=torch.float64, device=dev))
+        oc = _abi.cggm_csc(p, q, m, out.colptr.data_ptr(), out.rowidx.data_ptr(), out.val.data_ptr())
+        cs = Theta.c_struct()
+        l1 = ctypes.c_double()
+        self._check(self.lib.cggm_theta_cd(self.h, p, q, _ptr(Sigma), ld_of(Sigma), _ptr(Sxx), ld_of(Sxx), _ptr(Sxy),
+                                           ld_of(Sxy), ctypes.byref(cs), _ptr(T_row), _ptr(T_col), m, float(lam_T),
+                                           int(passes), ctypes.byref(oc), ctypes.byref(l1)))
+        return DeviceCsc(p, q, out.colptr, out.rowidx[:m], out.val[:m]), l1.value
 
     # ---------------------------------------------------------------- composite
     def cggm_newton_eval(self, X, Y, Syy, Lam: DeviceCsc, Theta: DeviceCsc, lam_L, lam_T, penalize_diag=True,

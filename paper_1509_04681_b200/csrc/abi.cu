@@ -353,6 +353,128 @@ cggm_status cggm_covariances(cggm_ctx* ctx, int64_t n_local, int64_t n_total, in
   });
 }
 
+// ================================================================== NEXT-1 / NEXT-2 (cd.cu)
+cggm_status cggm_gram(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64_t p, const void* X, int64_t ldx,
+                      void* Sxx, int64_t ldsxx) {
+  return guard(ctx, [&](Ctx* c) {
+    if (n_local < 0 || p < 0) fail(CGGM_ERR_INVALID_ARG, "negative dimension");
+    if (n_total < 1 || n_total < n_local) fail(CGGM_ERR_INVALID_ARG, "n_total must be >= max(1, n_local)");
+    check_dense("X", X, n_local, p, ldx);
+    check_dense("Sxx", Sxx, p, p, ldsxx);
+    Phase ph(c, TAG_COV);
+    dispatch(c, [&](auto tag) {
+      using T = decltype(tag);
+      EpilogueT<T> e; e.out1 = static_cast<T*>(Sxx); e.ld1 = ldsxx; e.a1 = 1.0 / (double)n_total;
+      gemm(c, true, false, p, p, n_local, static_cast<const T*>(X), ldx, static_cast<const T*>(X), ldx, e,
+           SYM_LOWER | SYM_MIRROR);
+    });
+  });
+}
+
+static void check_list(const char* name, const int32_t* r, const int32_t* cidx, int64_t m) {
+  if (m < 0) fail(CGGM_ERR_INVALID_ARG, std::string(name) + ": negative list length");
+  if (m > 0 && (!r || !cidx)) fail(CGGM_ERR_INVALID_ARG, std::string(name) + ": null list");
+}
+
+cggm_status cggm_lambda_direction(cggm_ctx* ctx, int64_t q, const void* Sigma, int64_t ldsigma, const void* Psi,
+                                  int64_t ldpsi, const void* GradL, int64_t ldgl, const cggm_csc* Lambda,
+                                  const int32_t* L_row, const int32_t* L_col, int64_t m_L, double lam_L,
+                                  int penalize_diag, int passes, void* D, double* delta, double* l1_lambda) {
+  return guard(ctx, [&](Ctx* c) {
+    check_ctx_dtype(c);
+    if (q < 1 || passes < 0) fail(CGGM_ERR_INVALID_ARG, "need q >= 1, passes >= 0");
+    if (!(lam_L >= 0.0)) fail(CGGM_ERR_INVALID_ARG, "lam_L must be >= 0");
+    check_dense("Sigma", Sigma, q, q, ldsigma);
+    check_dense("Psi", Psi, q, q, ldpsi);
+    check_dense("GradL", GradL, q, q, ldgl);
+    check_csc_host("Lambda", Lambda, q, q);
+    check_list("L", L_row, L_col, m_L);
+    if (m_L > 0 && !D) fail(CGGM_ERR_INVALID_ARG, "null D");
+    const int64_t ldu = pad_ld<double>(q);
+    double* U = static_cast<double*>(ws_get(c, WS_CD_U, (size_t)ldu * q * 8));
+    double* out = static_cast<double*>(ws_get(c, WS_CD_OUT, 64));
+    // a fresh direction: D = 0 (zeroed by the kernel), so U = D Sigma = 0
+    CGGM_CUDA_CHECK(cudaMemsetAsync(U, 0, (size_t)ldu * q * 8, c->stream));
+    lambda_cd(c, (int)q, static_cast<const double*>(Sigma), ldsigma, static_cast<const double*>(Psi), ldpsi,
+              static_cast<const double*>(GradL), ldgl, Lambda, L_row, L_col, m_L, lam_L, penalize_diag, passes,
+              static_cast<double*>(D), U, ldu, out);
+    if (delta || l1_lambda) {
+      double h[3];
+      CGGM_CUDA_CHECK(cudaMemcpyAsync(h, out, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+      CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+      if (delta) {
+        delta[0] = h[0];
+        delta[1] = h[1];
+      }
+      if (l1_lambda) *l1_lambda = h[2];
+    }
+  });
+}
+
+cggm_status cggm_lambda_step(cggm_ctx* ctx, int64_t q, const cggm_csc* Lambda, const int32_t* L_row,
+                             const int32_t* L_col, int64_t m_L, const void* D, double alpha, cggm_csc* out) {
+  return guard(ctx, [&](Ctx* c) {
+    check_ctx_dtype(c);
+    if (q < 1) fail(CGGM_ERR_INVALID_ARG, "need q >= 1");
+    check_csc_host("Lambda", Lambda, q, q);
+    check_list("L", L_row, L_col, m_L);
+    if (!out || out->nrows != q || out->ncols != q || !out->colptr) fail(CGGM_ERR_INVALID_ARG, "bad out CSC");
+    if (m_L > 0 && (!D || !out->rowidx || !out->val)) fail(CGGM_ERR_INVALID_ARG, "null D / out arrays");
+    if (out->nnz < 2 * m_L) {
+      out->nnz = 2 * m_L;
+      fail(CGGM_ERR_CAPACITY, "out capacity < 2 m_L (required size written to out->nnz)");
+    }
+    int* cnt = static_cast<int*>(ws_get(c, WS_CD_IDX, (size_t)3 * q * 4 + (size_t)2 * (q + 1) * 8 + 64));
+    int64_t* scan = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(cnt) + ((size_t)3 * q * 4 + 63) / 64 * 64);
+    list_to_csc(c, (int)q, L_row, L_col, m_L, true, Lambda, static_cast<const double*>(D), alpha, nullptr,
+                const_cast<int64_t*>(out->colptr), const_cast<int32_t*>(out->rowidx),
+                static_cast<double*>(const_cast<void*>(out->val)), cnt, scan);
+    int64_t nnz = 0;
+    CGGM_CUDA_CHECK(cudaMemcpyAsync(&nnz, out->colptr + q, 8, cudaMemcpyDeviceToHost, c->stream));
+    CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    out->nnz = nnz;
+  });
+}
+
+cggm_status cggm_theta_cd(cggm_ctx* ctx, int64_t p, int64_t q, const void* Sigma, int64_t ldsigma, const void* Sxx,
+                          int64_t ldsxx, const void* Sxy, int64_t ldsxy, const cggm_csc* Theta, const int32_t* T_row,
+                          const int32_t* T_col, int64_t m_T, double lam_T, int passes, cggm_csc* out,
+                          double* l1_theta) {
+  return guard(ctx, [&](Ctx* c) {
+    check_ctx_dtype(c);
+    if (q < 1 || p < 1 || passes < 0) fail(CGGM_ERR_INVALID_ARG, "need p, q >= 1, passes >= 0");
+    if (!(lam_T >= 0.0)) fail(CGGM_ERR_INVALID_ARG, "lam_T must be >= 0");
+    check_dense("Sigma", Sigma, q, q, ldsigma);
+    check_dense("Sxx", Sxx, p, p, ldsxx);
+    check_dense("Sxy", Sxy, p, q, ldsxy);
+    check_csc_host("Theta", Theta, p, q);
+    check_list("T", T_row, T_col, m_T);
+    if (!out || out->nrows != p || out->ncols != q || !out->colptr) fail(CGGM_ERR_INVALID_ARG, "bad out CSC");
+    if (m_T > 0 && (!out->rowidx || !out->val)) fail(CGGM_ERR_INVALID_ARG, "null out arrays");
+    if (out->nnz < m_T) {
+      out->nnz = m_T;
+      fail(CGGM_ERR_CAPACITY, "out capacity < m_T (required size written to out->nnz)");
+    }
+    const int64_t ldv = pad_ld<double>(p);
+    double* V = static_cast<double*>(ws_get(c, WS_CD_V, (size_t)ldv * q * 8));
+    double* sc = static_cast<double*>(ws_get(c, WS_CD_OUT, 64));
+    int* cnt = static_cast<int*>(ws_get(c, WS_CD_IDX, (size_t)3 * q * 4 + (size_t)2 * (q + 1) * 8 + 64));
+    int64_t* scan = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(cnt) + ((size_t)3 * q * 4 + 63) / 64 * 64);
+    CGGM_CUDA_CHECK(cudaMemsetAsync(V, 0, (size_t)ldv * q * 8, c->stream));
+    theta_sigma(c, (int)q, Theta, static_cast<const double*>(Sigma), ldsigma, V, ldv);
+    double* T = static_cast<double*>(const_cast<void*>(out->val));   // the sweep runs on the output values
+    theta_cd(c, (int)p, (int)q, static_cast<const double*>(Sigma), ldsigma, static_cast<const double*>(Sxx), ldsxx,
+             static_cast<const double*>(Sxy), ldsxy, Theta, T_row, T_col, m_T, lam_T, passes, T, V, ldv, sc);
+    list_to_csc(c, (int)q, T_row, T_col, m_T, false, nullptr, nullptr, 0.0, T, const_cast<int64_t*>(out->colptr),
+                const_cast<int32_t*>(out->rowidx), T, cnt, scan);
+    double h = 0.0;
+    CGGM_CUDA_CHECK(cudaMemcpyAsync(&h, sc, 8, cudaMemcpyDeviceToHost, c->stream));
+    CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    out->nnz = m_T;
+    if (l1_theta) *l1_theta = h;
+  });
+}
+
 int cggm::stream_priority(int which) {
   static int off[8] = {0, 5, 0, 1, 2, 3, 4, 5};
   static bool init = false;

@@ -1,0 +1,351 @@
+// Coordinate-descent consumers of the hot path: the Lambda
+// Newton-direction sweep of Eq. (6) with U = D Sigma, the direct Theta sweep of
+// Eq. (7) with V = Theta Sigma, and the sparse bookkeeping of Algorithm 1
+// (P:407-435): the line-search candidate Lambda + alpha D as a symmetric CSC, the new Theta as
+// a CSC.  Coefficients per the appendix with reading A15.
+//
+// A coordinate sweep is sequential by definition (each update changes U / V, which the next
+// update reads), so one CTA of 1024 threads walks the active list in order: per update three
+// (Lambda) or one (Theta) length-q / length-p dot products as a block reduction, then the two /
+// one row updates of U / V, each thread owning a stride of the vector.  Reduction order is fixed,
+// so sweeps are bitwise reproducible.
+#include "kernels.cuh"
+
+namespace cggm {
+namespace {
+
+constexpr int CD_NT = 1024;
+constexpr int CD_NW = CD_NT / 32;
+
+__device__ __forceinline__ double soft(double w, double r) {
+  const double m = fabs(w) - r;
+  return m > 0.0 ? copysign(m, w) : 0.0;
+}
+
+// value of A_ij in a CSC with sorted rows (0 if not stored)
+__device__ __forceinline__ double csc_at(const int64_t* colptr, const int32_t* rowidx, const double* val, int i,
+                                         int j) {
+  int64_t lo = colptr[j], hi = colptr[j + 1];
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    const int r = rowidx[mid];
+    if (r == i) return val[mid];
+    if (r < i) lo = mid + 1;
+    else hi = mid;
+  }
+  return 0.0;
+}
+
+// sum over the block of NV values per thread; result valid in every thread
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double (*red)[NV]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) red[w][k] = v[k];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double s = lane < CD_NW ? red[lane][k] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    v[k] = s;
+  }
+  __syncthreads();   // red reusable
+}
+
+// One CTA: D (values on the active list, zeroed here) by `passes` sweeps from D = 0; U (q x q, ldu,
+// zero on entry) = D Sigma throughout.  Afterwards out[0] = tr(GradL^T D) (both triangles), out[1] = ||Lambda + D||_1
+// - ||Lambda||_1 weighted by the penalty rule (lam = 0 on an unpenalised diagonal), out[2] =
+// ||Lambda||_1 (all entries, from the CSC).
+__global__ void __launch_bounds__(CD_NT) k_lambda_cd(int q, const double* __restrict__ S, int64_t lds,
+                                                     const double* __restrict__ P, int64_t ldp,
+                                                     const double* __restrict__ G, int64_t ldg, const int64_t* colptr,
+                                                     const int32_t* rowidx, const double* lval, const int32_t* Lr,
+                                                     const int32_t* Lc, int64_t m, double lam, int penalize_diag,
+                                                     int passes, double* D, double* U, int64_t ldu, double* out) {
+  __shared__ double red[CD_NW][3];
+  __shared__ double mu_sh;
+  for (int64_t k = threadIdx.x; k < m; k += CD_NT) D[k] = 0.0;   // a fresh direction (U = 0 on entry)
+  __syncthreads();
+  for (int pass = 0; pass < passes; ++pass) {
+    for (int64_t k = 0; k < m; ++k) {
+      const int i = Lr[k], j = Lc[k];
+      const double* Si = S + (int64_t)i * lds;   // row i of Sigma = column i (symmetric)
+      const double* Pi = P + (int64_t)i * ldp;
+      const double* Pj = P + (int64_t)j * ldp;
+      const double* Uj = U + (int64_t)j * ldu;
+      const double* Ui = U + (int64_t)i * ldu;
+      double v[3] = {0.0, 0.0, 0.0};
+      for (int t = threadIdx.x; t < q; t += CD_NT) {
+        const double uj = Uj[t];
+        v[0] = fma(Si[t], uj, v[0]);
+        v[1] = fma(Pi[t], uj, v[1]);
+        v[2] = fma(Pj[t], Ui[t], v[2]);
+      }
+      block_sum<3>(v, red);
+      if (threadIdx.x == 0) {
+        const double Sii = S[i + (int64_t)i * lds], Sjj = S[j + (int64_t)j * lds], Sij = S[i + (int64_t)j * lds];
+        const double Pii = P[i + (int64_t)i * ldp], Pjj = P[j + (int64_t)j * ldp], Pij = P[i + (int64_t)j * ldp];
+        const double a = (i == j) ? Sii * Sii + 2.0 * Sii * Pii
+                                  : Sij * Sij + Sii * Sjj + Sii * Pjj + Sjj * Pii + 2.0 * Sij * Pij;
+        const double b = G[i + (int64_t)j * ldg] + v[0] + v[1] + v[2];
+        const double c = csc_at(colptr, rowidx, lval, i, j) + D[k];
+        const double lm = (i == j && !penalize_diag) ? 0.0 : lam;
+        double mu = 0.0;
+        if (a > 0.0) mu = -c + soft(c - b / a, lm / a);
+        D[k] += mu;
+        mu_sh = mu;
+      }
+      __syncthreads();
+      const double mu = mu_sh;
+      if (mu != 0.0) {
+        const double* Sj = S + (int64_t)j * lds;
+        for (int t = threadIdx.x; t < q; t += CD_NT) {
+          const int64_t o = (int64_t)t * ldu;
+          if (i != j) {
+            U[i + o] += mu * Sj[t];
+            U[j + o] += mu * Si[t];
+          } else {
+            U[i + o] += mu * Si[t];
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // line-search decrease measure and ||Lambda||_1, fixed-order block reduction
+  double v[3] = {0.0, 0.0, 0.0};
+  for (int64_t k = threadIdx.x; k < m; k += CD_NT) {
+    const int i = Lr[k], j = Lc[k];
+    const double w = (i == j) ? 1.0 : 2.0;
+    const double lm = (i == j && !penalize_diag) ? 0.0 : lam;
+    const double l = csc_at(colptr, rowidx, lval, i, j);
+    v[0] += w * G[i + (int64_t)j * ldg] * D[k];
+    v[1] += w * lm * (fabs(l + D[k]) - fabs(l));
+  }
+  for (int j = threadIdx.x; j < q; j += CD_NT)
+    for (int64_t t = colptr[j]; t < colptr[j + 1]; ++t) v[2] += fabs(lval[t]);
+  block_sum<3>(v, red);
+  if (threadIdx.x == 0) {
+    out[0] = v[0];
+    out[1] = v[1];
+    out[2] = v[2];
+  }
+}
+
+// V = Theta Sigma (p x q, ldv, zeroed): one warp per output column t walks Theta's columns in
+// order (distinct rows inside a column: no write conflicts), deterministic summation order.
+__global__ void k_theta_sigma(int q, const int64_t* colptr, const int32_t* rowidx, const double* val,
+                              const double* __restrict__ S, int64_t lds, double* V, int64_t ldv) {
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (t >= q) return;
+  double* Vt = V + (int64_t)t * ldv;
+  for (int j = 0; j < q; ++j) {
+    const int64_t a = colptr[j], b = colptr[j + 1];
+    if (a == b) continue;
+    const double s = S[j + (int64_t)t * lds];
+    for (int64_t e = a + lane; e < b; e += 32) Vt[rowidx[e]] += val[e] * s;
+    __syncwarp();
+  }
+}
+
+// One CTA: Theta values on the active list (in: current Theta, gathered here; out: after the
+// sweeps); V = Theta Sigma maintained.  out[0] = ||Theta_new||_1.
+__global__ void __launch_bounds__(CD_NT) k_theta_cd(int p, int q, const double* __restrict__ S, int64_t lds,
+                                                    const double* __restrict__ Sxx, int64_t ldx,
+                                                    const double* __restrict__ Sxy, int64_t ldxy,
+                                                    const int64_t* colptr, const int32_t* rowidx, const double* tval,
+                                                    const int32_t* Tr, const int32_t* Tc, int64_t m, double lam,
+                                                    int passes, double* T, double* V, int64_t ldv, double* out) {
+  __shared__ double red[CD_NW][1];
+  __shared__ double mu_sh;
+  for (int64_t k = threadIdx.x; k < m; k += CD_NT) T[k] = csc_at(colptr, rowidx, tval, Tr[k], Tc[k]);
+  __syncthreads();
+  for (int pass = 0; pass < passes; ++pass) {
+    for (int64_t k = 0; k < m; ++k) {
+      const int i = Tr[k], j = Tc[k];
+      const double* Xi = Sxx + (int64_t)i * ldx;   // row i of S_xx = column i
+      const double* Vj = V + (int64_t)j * ldv;
+      double v[1] = {0.0};
+      for (int t = threadIdx.x; t < p; t += CD_NT) v[0] = fma(Xi[t], Vj[t], v[0]);
+      block_sum<1>(v, red);
+      if (threadIdx.x == 0) {
+        const double a = 2.0 * S[j + (int64_t)j * lds] * Sxx[i + (int64_t)i * ldx];
+        const double b = 2.0 * Sxy[i + (int64_t)j * ldxy] + 2.0 * v[0];
+        const double c = T[k];
+        double mu = 0.0;
+        if (a > 0.0) mu = -c + soft(c - b / a, lam / a);
+        T[k] += mu;
+        mu_sh = mu;
+      }
+      __syncthreads();
+      const double mu = mu_sh;
+      if (mu != 0.0) {
+        const double* Sj = S + (int64_t)j * lds;
+        for (int t = threadIdx.x; t < q; t += CD_NT) V[i + (int64_t)t * ldv] += mu * Sj[t];
+      }
+      __syncthreads();
+    }
+  }
+  double v[1] = {0.0};
+  for (int64_t k = threadIdx.x; k < m; k += CD_NT) v[0] += fabs(T[k]);
+  block_sum<1>(v, red);
+  if (threadIdx.x == 0) out[0] = v[0];
+}
+
+// ---------------------------------------------------------------- sparse bookkeeping
+// count list entries per column (cl) and mirrored entries per column (cm: entry (i, j), i < j,
+// mirrors into column i)
+__global__ void k_list_counts(int64_t m, const int32_t* r, const int32_t* cidx, int mirror, int* cl, int* cm) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+    const int i = r[k], j = cidx[k];
+    atomicAdd(&cl[j], 1);
+    if (mirror && i < j) atomicAdd(&cm[i], 1);
+  }
+}
+
+// exclusive scans (one block): lp = scan(cl), cp = scan(cl + cm) with cp[n] = total; mb = cp + cl
+__global__ void __launch_bounds__(1024) k_list_scan(int n, const int* cl, const int* cm, int64_t* lp, int64_t* cp,
+                                                    int64_t* mb) {
+  __shared__ int64_t carry_l, carry_c;
+  __shared__ int64_t sl[1024], sc[1024];
+  if (threadIdx.x == 0) carry_l = carry_c = 0;
+  __syncthreads();
+  for (int base = 0; base < n; base += 1024) {
+    const int c = base + threadIdx.x;
+    const int64_t a = c < n ? cl[c] : 0, b = c < n ? (int64_t)cl[c] + (cm ? cm[c] : 0) : 0;
+    sl[threadIdx.x] = a;
+    sc[threadIdx.x] = b;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {   // Hillis-Steele inclusive scan
+      const int64_t xa = threadIdx.x >= o ? sl[threadIdx.x - o] : 0, xb = threadIdx.x >= o ? sc[threadIdx.x - o] : 0;
+      __syncthreads();
+      sl[threadIdx.x] += xa;
+      sc[threadIdx.x] += xb;
+      __syncthreads();
+    }
+    if (c < n) {
+      lp[c] = carry_l + sl[threadIdx.x] - a;
+      cp[c] = carry_c + sc[threadIdx.x] - b;
+      if (mb) mb[c] = cp[c] + a;
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) {
+      carry_l += sl[1023];
+      carry_c += sc[1023];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    lp[n] = carry_l;
+    cp[n] = carry_c;
+  }
+}
+
+// Lambda + alpha D as a symmetric CSC: list entries at their column-major rank, mirrored entries
+// appended per column (sorted afterwards by k_sort_segments)
+__global__ void k_lambda_trial_scatter(int64_t m, const int32_t* Lr, const int32_t* Lc, const double* D, double alpha,
+                                       const int64_t* colptr, const int32_t* rowidx, const double* lval,
+                                       const int64_t* lp, const int64_t* cp, const int64_t* mb, int* mfill,
+                                       int32_t* orow, double* oval) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+    const int i = Lr[k], j = Lc[k];
+    const double v = csc_at(colptr, rowidx, lval, i, j) + alpha * D[k];
+    const int64_t pos = cp[j] + (k - lp[j]);
+    orow[pos] = i;
+    oval[pos] = v;
+    if (i < j) {
+      const int64_t mp = mb[i] + atomicAdd(&mfill[i], 1);
+      orow[mp] = j;
+      oval[mp] = v;
+    }
+  }
+}
+
+// insertion sort of each column's mirrored segment [mb[c], cp[c+1]) by row (deterministic order)
+__global__ void k_sort_segments(int n, const int64_t* mb, const int64_t* cp, int32_t* row, double* val) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const int64_t a = mb[c], b = cp[c + 1];
+  for (int64_t x = a + 1; x < b; ++x) {
+    const int32_t r = row[x];
+    const double v = val[x];
+    int64_t y = x - 1;
+    while (y >= a && row[y] > r) {
+      row[y + 1] = row[y];
+      val[y + 1] = val[y];
+      --y;
+    }
+    row[y + 1] = r;
+    val[y + 1] = v;
+  }
+}
+
+__global__ void k_copy_list(int64_t m, const int32_t* r, const double* v, int32_t* orow, double* oval) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+    orow[k] = r[k];
+    oval[k] = v[k];
+  }
+}
+
+int grid_for(int64_t m) { return (int)std::min<int64_t>(std::max<int64_t>((m + 255) / 256, 1), 148 * 16); }
+
+}  // namespace
+
+void lambda_cd(Ctx* c, int q, const double* S, int64_t lds, const double* P, int64_t ldp, const double* G, int64_t ldg,
+               const cggm_csc* Lam, const int32_t* Lr, const int32_t* Lc, int64_t m, double lam, int penalize_diag,
+               int passes, double* D, double* U, int64_t ldu, double* out) {
+  Prof pr(c, TAG_MISC);
+  k_lambda_cd<<<1, CD_NT, 0, c->stream>>>(q, S, lds, P, ldp, G, ldg, Lam->colptr, Lam->rowidx,
+                                          static_cast<const double*>(Lam->val), Lr, Lc, m, lam, penalize_diag, passes, D,
+                                          U, ldu, out);
+  post_launch(c, "k_lambda_cd");
+}
+
+void theta_sigma(Ctx* c, int q, const cggm_csc* Th, const double* S, int64_t lds, double* V, int64_t ldv) {
+  Prof pr(c, TAG_MISC);
+  k_theta_sigma<<<(q + 7) / 8, 256, 0, c->stream>>>(q, Th->colptr, Th->rowidx, static_cast<const double*>(Th->val), S,
+                                                    lds, V, ldv);
+  post_launch(c, "k_theta_sigma");
+}
+
+void theta_cd(Ctx* c, int p, int q, const double* S, int64_t lds, const double* Sxx, int64_t ldx, const double* Sxy,
+              int64_t ldxy, const cggm_csc* Th, const int32_t* Tr, const int32_t* Tc, int64_t m, double lam, int passes,
+              double* T, double* V, int64_t ldv, double* out) {
+  Prof pr(c, TAG_MISC);
+  k_theta_cd<<<1, CD_NT, 0, c->stream>>>(p, q, S, lds, Sxx, ldx, Sxy, ldxy, Th->colptr, Th->rowidx,
+                                         static_cast<const double*>(Th->val), Tr, Tc, m, lam, passes, T, V, ldv, out);
+  post_launch(c, "k_theta_cd");
+}
+
+// workspace: ints[2n] counts, int64[3(n+1)] scans
+void list_to_csc(Ctx* c, int n, const int32_t* r, const int32_t* cidx, int64_t m, bool mirror, const cggm_csc* base,
+                 const double* D, double alpha, const double* vals, int64_t* out_colptr, int32_t* out_row,
+                 double* out_val, int* cnt_ws, int64_t* scan_ws) {
+  int* cl = cnt_ws;
+  int* cm = cnt_ws + n;
+  int* mfill = cnt_ws + 2 * n;
+  int64_t* lp = scan_ws;
+  int64_t* mb = scan_ws + (n + 1);
+  CGGM_CUDA_CHECK(cudaMemsetAsync(cnt_ws, 0, sizeof(int) * 3 * (size_t)n, c->stream));
+  Prof pr(c, TAG_MISC);
+  k_list_counts<<<grid_for(m), 256, 0, c->stream>>>(m, r, cidx, mirror ? 1 : 0, cl, cm);
+  k_list_scan<<<1, 1024, 0, c->stream>>>(n, cl, mirror ? cm : nullptr, lp, out_colptr, mirror ? mb : nullptr);
+  if (mirror) {
+    k_lambda_trial_scatter<<<grid_for(m), 256, 0, c->stream>>>(m, r, cidx, D, alpha, base->colptr, base->rowidx,
+                                                              static_cast<const double*>(base->val), lp, out_colptr, mb,
+                                                              mfill, out_row, out_val);
+    k_sort_segments<<<(n + 255) / 256, 256, 0, c->stream>>>(n, mb, out_colptr, out_row, out_val);
+  } else {
+    k_copy_list<<<grid_for(m), 256, 0, c->stream>>>(m, r, vals, out_row, out_val);
+  }
+  c->launches += mirror ? 3 : 2;
+  post_launch(c, "list_to_csc");
+}
+
+}  // namespace cggm

@@ -158,6 +158,10 @@ enum Slot {
   WS_TMP_OBJ,       // objective: recursion temporaries (full-inverse subtrees + block products)
   WS_GTCHUNK,       // streamed grad_Theta column chunk (fused active sets without a stored p x q gradient)
   WS_SCAL2,         // scalar block of the auxiliary lane
+  WS_CD_U,          // Lambda sweep: U = D Sigma (q x q)
+  WS_CD_V,          // Theta sweep: V = Theta Sigma (p x q)
+  WS_CD_IDX,        // list -> CSC counts / scans
+  WS_CD_OUT,        // sweep scalars
   WS_NUM
 };
 

@@ -49,4 +49,19 @@ void active_compact(Ctx* c, int64_t p, int64_t q, const T* GradL, int64_t ldgl, 
                     double tie_eps, const ActWs& ws, int32_t* L_row, int32_t* L_col, int32_t* T_row, int32_t* T_col,
                     long long capL, long long capT);
 
+// Coordinate-descent consumers (cd.cu), fp64
+void lambda_cd(Ctx* c, int q, const double* S, int64_t lds, const double* P, int64_t ldp, const double* G, int64_t ldg,
+               const cggm_csc* Lam, const int32_t* Lr, const int32_t* Lc, int64_t m, double lam, int penalize_diag,
+               int passes, double* D, double* U, int64_t ldu, double* out);
+void theta_sigma(Ctx* c, int q, const cggm_csc* Th, const double* S, int64_t lds, double* V, int64_t ldv);
+void theta_cd(Ctx* c, int p, int q, const double* S, int64_t lds, const double* Sxx, int64_t ldx, const double* Sxy,
+              int64_t ldxy, const cggm_csc* Th, const int32_t* Tr, const int32_t* Tc, int64_t m, double lam, int passes,
+              double* T, double* V, int64_t ldv, double* out);
+// sorted list (column-major) -> CSC: mirror = symmetric Lambda + alpha D from the upper-triangle list
+// (values base_ij + alpha D[k]); otherwise the list itself with `vals`.  cnt_ws: 3n ints, scan_ws:
+// 2(n+1) int64.
+void list_to_csc(Ctx* c, int n, const int32_t* r, const int32_t* cidx, int64_t m, bool mirror, const cggm_csc* base,
+                 const double* D, double alpha, const double* vals, int64_t* out_colptr, int32_t* out_row,
+                 double* out_val, int* cnt_ws, int64_t* scan_ws);
+
 }  // namespace cggm
