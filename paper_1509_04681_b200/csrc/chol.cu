@@ -240,6 +240,262 @@ __global__ void __launch_bounds__(LEAF_THREADS, CGGM_LEAF_MINB) leaf_potrf_trtri
 #undef LT
 }
 
+// ---------------------------------------------------------------------------------------------
+// Full-inverse leaf by the same recursion as node() below, carried out inside one CTA in shared
+// memory: node(64) = node(32), T = A21 X11^T, {A22 -= T T^T, A21 := T X11}, node(32),
+// X21 = -X22 A21, down to 8x8 base blocks that one warp factors and inverts in registers.  The
+// dependency chain is 8 base blocks (8 pivots each: rsqrt + two FP64 latencies) plus three levels
+// of short products, instead of 64 shuffle-driven pivot steps and a 64-step inverse sweep
+// (profiles: 50k -> ~18k cycles per 64-column leaf).
+template <typename T>
+struct LeafRec {
+  T (*L)[NB + 1];   // [col][row]: the block being factored (A11 regions become T)
+  T (*X)[NB + 1];   // [col][row]: L^{-1}
+  T* diag;
+  T* invd;
+  int* fail_sm;
+};
+
+// 8x8 base block at offset s: warp 0 (every lane redundantly holds the block), lane c < 8 then
+// computes column c of the inverse
+template <typename T>
+__device__ __forceinline__ void leaf_base8(const LeafRec<T>& R, int s) {
+  const int lane = threadIdx.x & 31;
+  if ((threadIdx.x >> 5) == 0) {
+    T a[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j <= i; ++j) a[i][j] = R.L[s + j][s + i];
+    T inv[8];
+    int bad = -1;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const T d = a[j][j];
+      if ((!(d > T(0)) || !isfinite(d)) && bad < 0) bad = j;
+      inv[j] = rsqrt_t(d);
+      a[j][j] = d * inv[j];
+#pragma unroll
+      for (int i = j + 1; i < 8; ++i) a[i][j] *= inv[j];
+#pragma unroll
+      for (int k = j + 1; k < 8; ++k)
+#pragma unroll
+        for (int i = k; i < 8; ++i) a[i][k] = fma_t(-a[i][j], a[k][j], a[i][k]);
+    }
+    if (lane < 8) {
+      const int c = lane;
+      T x[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        T acc = T(0);
+#pragma unroll
+        for (int m = 0; m < r; ++m) acc = fma_t(-a[r][m], x[m], acc);
+        x[r] = (r < c) ? T(0) : ((r == c) ? inv[r] : acc * inv[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (r >= c) R.X[s + c][s + r] = x[r];
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        R.diag[s + j] = a[j][j];
+        R.invd[s + j] = inv[j];
+      }
+      if (bad >= 0) atomicMin(R.fail_sm, s + bad);
+    }
+  }
+  __syncthreads();
+}
+
+// One product phase on 8x8 DMMA fragments of an H x H output (fp64): warp w takes fragments
+// w, w + 8, ...; a(i, m) and b(m, k) read the operands from shared memory, c0 / c1 the lane's two
+// initial accumulators (C[g][2t], C[g][2t+1]), st writes them back.
+template <int H, bool LOWER, class FA, class FB, class FC, class FS>
+__device__ __forceinline__ void frag_phase(FA a, FB b, FC cinit, FS st) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  constexpr int NF = H / 8;
+  for (int f = warp; f < NF * NF; f += LEAF_THREADS / 32) {
+    const int fi = f % NF, fk = f / NF;
+    if (LOWER && fi < fk) continue;
+    const int i = fi * 8 + g, k0 = fk * 8 + 2 * t;
+    double c0, c1;
+    cinit(i, k0, c0, c1);
+#pragma unroll
+    for (int kk = 0; kk < H / 4; ++kk) ptx::dmma_8x8x4(c0, c1, a(i, 4 * kk + t), b(4 * kk + t, fk * 8 + g));
+    st(i, k0, c0, c1);
+  }
+}
+
+// the products of one recursion level: block [s, s + 2H), halves of width H.  X blocks hold zeros
+// above their diagonal and the loads put zeros above A's, so every dot product runs over the full
+// length H (no triangular bounds).
+template <typename T, int H>
+__device__ __forceinline__ void leaf_products_down(const LeafRec<T>& R, int s) {
+  const int a = s + H;   // first row/col of the second half
+  if constexpr (sizeof(T) == 8) {
+    auto L = R.L;
+    auto X = R.X;
+    auto zero = [](int, int, double& c0, double& c1) { c0 = 0.0; c1 = 0.0; };
+    // T = A21 X11^T  (T[i][k] = sum_m A21[i][m] X11[k][m]) -> over the A11 block (not read here)
+    frag_phase<H, false>([&](int i, int m) { return (double)L[s + m][a + i]; },
+                         [&](int m, int k) { return (double)X[s + m][s + k]; }, zero,
+                         [&](int i, int k, double c0, double c1) {
+                           L[s + k][s + i] = c0;
+                           L[s + k + 1][s + i] = c1;
+                         });
+    __syncthreads();
+    // A22 -= T T^T (lower fragments) and A21 := T X11 (A21[i][k] = sum_m T[i][m] X11[m][k])
+    frag_phase<H, true>([&](int i, int k) { return -(double)L[s + k][s + i]; },
+                        [&](int k, int j) { return (double)L[s + k][s + j]; },
+                        [&](int i, int j, double& c0, double& c1) {
+                          c0 = L[a + j][a + i];
+                          c1 = L[a + j + 1][a + i];
+                        },
+                        [&](int i, int j, double c0, double c1) {
+                          L[a + j][a + i] = c0;
+                          L[a + j + 1][a + i] = c1;
+                        });
+    frag_phase<H, false>([&](int i, int m) { return (double)L[s + m][s + i]; },
+                         [&](int m, int k) { return (double)X[s + k][s + m]; }, zero,
+                         [&](int i, int k, double c0, double c1) {
+                           L[s + k][a + i] = c0;
+                           L[s + k + 1][a + i] = c1;
+                         });
+    __syncthreads();
+  } else {
+    T tv[(H * H + LEAF_THREADS - 1) / LEAF_THREADS];
+#pragma unroll
+    for (int u = 0; u * LEAF_THREADS < H * H; ++u) {
+      const int idx = threadIdx.x + u * LEAF_THREADS;
+      T acc = T(0);
+      if (idx < H * H) {
+        const int i = idx % H, k = idx / H;
+#pragma unroll 8
+        for (int m = 0; m < H; ++m) acc = fma_t(R.L[s + m][a + i], R.X[s + m][s + k], acc);
+      }
+      tv[u] = acc;
+    }
+#pragma unroll
+    for (int u = 0; u * LEAF_THREADS < H * H; ++u) {
+      const int idx = threadIdx.x + u * LEAF_THREADS;
+      if (idx < H * H) R.L[s + idx / H][s + idx % H] = tv[u];
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < 2 * H * H; idx += LEAF_THREADS) {
+      const int w = idx / (H * H), e = idx - w * H * H, i = e % H, j = e / H;
+      if (w == 0) {
+        if (i < j) continue;
+        T acc = R.L[a + j][a + i];
+#pragma unroll 8
+        for (int k = 0; k < H; ++k) acc = fma_t(-R.L[s + k][s + i], R.L[s + k][s + j], acc);
+        R.L[a + j][a + i] = acc;
+      } else {
+        T acc = T(0);
+#pragma unroll 8
+        for (int m = 0; m < H; ++m) acc = fma_t(R.L[s + m][s + i], R.X[s + j][s + m], acc);
+        R.L[s + j][a + i] = acc;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// X21 = -X22 A21  (X21[i][k] = -sum_m X22[i][m] A21[m][k])
+template <typename T, int H>
+__device__ __forceinline__ void leaf_products_up(const LeafRec<T>& R, int s) {
+  const int a = s + H;
+  if constexpr (sizeof(T) == 8) {
+    auto L = R.L;
+    auto X = R.X;
+    frag_phase<H, false>([&](int i, int m) { return -(double)X[a + m][a + i]; },
+                         [&](int m, int k) { return (double)L[s + k][a + m]; },
+                         [](int, int, double& c0, double& c1) { c0 = 0.0; c1 = 0.0; },
+                         [&](int i, int k, double c0, double c1) {
+                           X[s + k][a + i] = c0;
+                           X[s + k + 1][a + i] = c1;
+                         });
+  } else {
+    for (int idx = threadIdx.x; idx < H * H; idx += LEAF_THREADS) {
+      const int i = idx % H, k = idx / H;
+      T acc = T(0);
+#pragma unroll 8
+      for (int m = 0; m < H; ++m) acc = fma_t(-R.X[a + m][a + i], R.L[s + k][a + m], acc);
+      R.X[s + k][a + i] = acc;
+    }
+  }
+  __syncthreads();
+}
+
+template <typename T, int N>
+struct LeafNode {
+  __device__ __forceinline__ static void run(const LeafRec<T>& R, int s) {
+    LeafNode<T, N / 2>::run(R, s);
+    leaf_products_down<T, N / 2>(R, s);
+    LeafNode<T, N / 2>::run(R, s + N / 2);
+    leaf_products_up<T, N / 2>(R, s);
+  }
+};
+template <typename T>
+struct LeafNode<T, 8> {
+  __device__ __forceinline__ static void run(const LeafRec<T>& R, int s) { leaf_base8<T>(R, s); }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(LEAF_THREADS, CGGM_LEAF_MINB) leaf_rec_inverse(const T* A, int64_t lda, int nb, T* Xo,
+                                                                                  int64_t ldx, double* logdet_slot,
+                                                                                  int* fail_col, int col0) {
+  extern __shared__ __align__(16) unsigned char leaf_raw[];
+  T(*Ls)[NB + 1] = reinterpret_cast<T(*)[NB + 1]>(leaf_raw);
+  T(*Xs)[NB + 1] = reinterpret_cast<T(*)[NB + 1]>(leaf_raw + NB * (NB + 1) * sizeof(T));
+  __shared__ T diag[NB], invd[NB];
+  __shared__ int fail_sm;
+  const int t = threadIdx.x;
+  {
+    constexpr int PER = NB * NB / LEAF_THREADS, HALF = PER / 2;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      T v[HALF];
+#pragma unroll
+      for (int u = 0; u < HALF; ++u) {
+        const int idx = t + LEAF_THREADS * (u + h * HALF), i = idx & (NB - 1), j = idx >> 6;
+        v[u] = (i < nb && j < nb && i >= j) ? A[i + (int64_t)j * lda] : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < HALF; ++u) {
+        const int idx = t + LEAF_THREADS * (u + h * HALF), i = idx & (NB - 1), j = idx >> 6;
+        Ls[j][i] = (i < nb && j < nb) ? v[u] : ((i == j) ? T(1) : T(0));
+        Xs[j][i] = T(0);
+      }
+    }
+  }
+  if (t == 0) fail_sm = INT_MAX;
+  __syncthreads();
+#ifdef CGGM_LEAF_TIMING
+  const long long c0 = clock64();
+#endif
+  LeafRec<T> R{Ls, Xs, diag, invd, &fail_sm};
+  LeafNode<T, NB>::run(R, 0);
+#ifdef CGGM_LEAF_TIMING
+  if (t == 0 && col0 == 0) printf("leaf_rec clocks: recursion %lld\n", clock64() - c0);
+#endif
+#pragma unroll 4
+  for (int idx = t; idx < NB * NB; idx += LEAF_THREADS) {
+    const int i = idx & (NB - 1), j = idx >> 6;
+    if (i >= nb || j >= nb) continue;
+    Xo[i + (int64_t)j * ldx] = (i >= j) ? Xs[j][i] : T(0);
+  }
+  if (t < 32) {  // 2 sum ln L_jj, fixed order
+    double sacc = log((double)diag[t]) + log((double)diag[t + 32]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_down_sync(0xffffffffu, sacc, o);
+    if (t == 0) {
+      *logdet_slot = 2.0 * sacc;
+      if (fail_sm != INT_MAX && fail_sm < nb) atomicMin(fail_col, col0 + fail_sm);
+    }
+  }
+}
+
 int split_point(int64_t n) {
   const int64_t gran = n > 4 * 128 ? 128 : NB;
   int64_t n1 = (n / 2) / gran * gran;
@@ -353,6 +609,19 @@ void leaf(Rec<T>& R, ViewT<T> A, ViewT<T> X, int64_t col0) {
     attr = true;
   }
   Prof pr(R.c, TAG_CHOL_LEAF);
+  if (R.full_inverse && !R.c->leaf_sweep) {
+    static bool attr2 = false;
+    if (!attr2) {
+      CGGM_CUDA_CHECK(cudaFuncSetAttribute(leaf_rec_inverse<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           leaf_smem_bytes<T>()));
+      attr2 = true;
+    }
+    leaf_rec_inverse<T><<<1, LEAF_THREADS, leaf_smem_bytes<T>(), R.c->stream>>>(A.p, A.ld, nb, xp, ldx,
+                                                                               R.logdet_slots + col0 / NB, R.fail_col,
+                                                                               (int)col0);
+    post_launch(R.c, "leaf_rec_inverse");
+    return;
+  }
   leaf_potrf_trtri<T><<<1, LEAF_THREADS, leaf_smem_bytes<T>(), R.c->stream>>>(A.p, A.ld, nb, xp, ldx, R.full_inverse ? 0 : 1,
                                                         R.logdet_slots + col0 / NB, R.fail_col, (int)col0);
   post_launch(R.c, "leaf_potrf_trtri");

@@ -79,6 +79,8 @@ struct Ctx {
   ActTotals* graph_tot = nullptr;
   int force_tile = 0;
   int small_kmax = 1024;    // mid-size GEMMs (64-tile grid < #SMs) with K <= this use the 32x32 cp.async kernel (CGGM_SMALL_KMAX)
+  int leaf_sweep = 0;       // CGGM_LEAF_SWEEP=1: full-inverse leaves by the panel/sweep kernel (A/B)
+  int mid_tile = 0;         // CGGM_MID_TILE=1: 128x64 tiles (2 CTAs/SM) for the large non-symmetric GEMMs
   int no_small_async = 0;
   int no_active_vec = 0;    // test hook (CGGM_NO_ACTIVE_VEC=1): scalar active-set kernel only   // test hook (CGGM_NO_SMALL_ASYNC=1): direct-load small kernel only
   int no_tma3d = 0;   // test hook: 1 = always use 16-wide 2-D boxes for MN-inner operands  // test hook: 0 auto, 1 = 128x128 tiles, 2 = 64x64 tiles

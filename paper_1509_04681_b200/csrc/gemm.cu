@@ -50,12 +50,14 @@ struct Cfg {
   // register cap: a 128x128 CTA (8 warps x 192) leaves 16384 registers and ~95 KB of shared memory
   // on its SM, exactly one 64x64 CTA (4 warps x 128), so latency-bound kernels of a concurrent
   // stream co-reside with the big tiles instead of waiting for a whole SM
-  static constexpr int MAXREG = NTHREADS >= 256 ? CGGM_BIG_MAXNREG : 128;
+  static constexpr int MAXREG = (WTM >= 64 && WTN >= 32) ? CGGM_BIG_MAXNREG : 128;
   static_assert(FM % 2 == 0 && FN % 2 == 0, "MN-inner fragments come in pairs");
   static_assert(BM % 16 == 0 && BN % 16 == 0, "16-wide TMA boxes");
 };
 using CfgBig = Cfg<128, 128, 2, 4>;    // 8 warps, warp tile 64 x 32
 using CfgSmall = Cfg<64, 64, 2, 2>;    // 4 warps, warp tile 32 x 32
+using CfgMid = Cfg<128, 64, 2, 2>;     // 4 warps, warp tile 64 x 32: two CTAs per SM, so one's
+                                       // prologue / epilogue overlaps the other's main loop
 
 struct KParams {
   int M, N, K;
@@ -597,6 +599,9 @@ void launch(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensor
   if (!attr_set) {
     CGGM_CUDA_CHECK(cudaFuncSetAttribute(gemm_dmma_kernel<AK, BKI, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::SMEM_BYTES));
+    // the largest shared-memory carveout, so that configurations sized for 2-3 CTAs per SM get them
+    CGGM_CUDA_CHECK(cudaFuncSetAttribute(gemm_dmma_kernel<AK, BKI, C>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         (int)cudaSharedmemCarveoutMaxShared));
     attr_set = true;
   }
   Prof pr(c, c->cur_tag);
@@ -727,7 +732,8 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
   const double big_eff = (double)big_tiles / (double)(waves * c->num_sms);
   const bool auto_big = big_tiles >= 3 * c->num_sms || big_eff >= 0.9;
   const bool use_big = c->force_tile ? (c->force_tile == 1) : auto_big;
-  if (use_big) run_cfg<CfgBig>(c, transA, transB, M, N, Keff, A, lda, B, ldb, P);
+  if (use_big && c->mid_tile && !(flags & SYM_LOWER)) run_cfg<CfgMid>(c, transA, transB, M, N, Keff, A, lda, B, ldb, P);
+  else if (use_big) run_cfg<CfgBig>(c, transA, transB, M, N, Keff, A, lda, B, ldb, P);
   else run_cfg<CfgSmall>(c, transA, transB, M, N, Keff, A, lda, B, ldb, P);
 }
 

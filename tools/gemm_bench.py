@@ -37,7 +37,9 @@ def bench(tA, tB, M, N, K, flags=0, alg=None, reps=3, beta=0.0, tile=0):
           f"{ms:9.3f} ms  {fl / ms / 1e9:7.2f} TFLOP/s", flush=True)
 
 
-if len(sys.argv) > 1 and sys.argv[1] == "tiles":
+if __name__ != "__main__":
+    pass
+elif len(sys.argv) > 1 and sys.argv[1] == "tiles":
     for s_ in (1536, 2048, 3072, 4096, 6144):
         for tile in (1, 2):
             bench(False, True, s_, s_, s_, tile=tile, reps=5)
@@ -47,23 +49,24 @@ if len(sys.argv) > 1 and sys.argv[1] == "tiles":
         bench(True, False, 10000, 4000, 500, tile=tile)
         bench(False, False, 500, 4000, 4000, tile=tile)
     sys.exit(0)
-n = 8192
-for tA in (False, True):
-    for tB in (False, True):
-        bench(tA, tB, n, n, n)
-bench(False, True, n, n, n, beta=1.0)
-bench(False, True, 10016, 10016, 9984, flags=SYM_LOWER, alg=10016 * 10017 * 9984.0, beta=1.0)
-bench(True, False, 10016, 10016, 9984, flags=SYM_LOWER, alg=10016 * 10017 * 9984.0)
-bench(False, True, 10016, 9984, 9984, flags=B_KLE_N, alg=10016 * 9984.0 * 9984)
-bench(False, False, 10016, 9984, 9984, flags=B_KGE_N, alg=10016 * 9984.0 * 9984)
-bench(False, False, 10016, 9984, 10016, flags=A_KLE_M, alg=10016 * 10016.0 * 9984)
-bench(True, False, 20000, 20000, 20000, flags=A_KGE_M | B_KGE_N | SYM_LOWER | SYM_MIRROR, alg=20000 ** 3 / 3.0, reps=1)
-bench(False, False, 1000, 20000, 20000)
-bench(True, False, 20000, 20000, 1000, flags=SYM_LOWER | SYM_MIRROR, alg=20000 * 20001 * 1000.0)
-bench(True, False, 40000, 20000, 1000)
-for s in (256, 512, 1024, 2048):
+if __name__ == "__main__":
+    n = 8192
+    for tA in (False, True):
+        for tB in (False, True):
+            bench(tA, tB, n, n, n)
+    bench(False, True, n, n, n, beta=1.0)
+    bench(False, True, 10016, 10016, 9984, flags=SYM_LOWER, alg=10016 * 10017 * 9984.0, beta=1.0)
+    bench(True, False, 10016, 10016, 9984, flags=SYM_LOWER, alg=10016 * 10017 * 9984.0)
+    bench(False, True, 10016, 9984, 9984, flags=B_KLE_N, alg=10016 * 9984.0 * 9984)
+    bench(False, False, 10016, 9984, 9984, flags=B_KGE_N, alg=10016 * 9984.0 * 9984)
+    bench(False, False, 10016, 9984, 10016, flags=A_KLE_M, alg=10016 * 10016.0 * 9984)
+    bench(True, False, 20000, 20000, 20000, flags=A_KGE_M | B_KGE_N | SYM_LOWER | SYM_MIRROR, alg=20000 ** 3 / 3.0, reps=1)
+    bench(False, False, 1000, 20000, 20000)
+    bench(True, False, 20000, 20000, 1000, flags=SYM_LOWER | SYM_MIRROR, alg=20000 * 20001 * 1000.0)
+    bench(True, False, 40000, 20000, 1000)
+    for s in (256, 512, 1024, 2048):
+        for tile in (1, 2):
+            bench(False, True, s, s, s, tile=tile, reps=10)
     for tile in (1, 2):
-        bench(False, True, s, s, s, tile=tile, reps=10)
-for tile in (1, 2):
-    bench(False, True, 1064, 64, 64, tile=tile, reps=20)
-    bench(False, True, 1064 + 500, 500, 512, flags=SYM_LOWER, tile=tile, reps=20, alg=(500 * 501 / 2 + 1064 * 500) * 512 * 2.0)
+        bench(False, True, 1064, 64, 64, tile=tile, reps=20)
+        bench(False, True, 1064 + 500, 500, 512, flags=SYM_LOWER, tile=tile, reps=20, alg=(500 * 501 / 2 + 1064 * 500) * 512 * 2.0)
