@@ -397,9 +397,10 @@ cggm_status cggm_lambda_direction(cggm_ctx* ctx, int64_t q, const void* Sigma, i
     double* out = static_cast<double*>(ws_get(c, WS_CD_OUT, 64));
     // a fresh direction: D = 0 (zeroed by the kernel), so U = D Sigma = 0
     CGGM_CUDA_CHECK(cudaMemsetAsync(U, 0, (size_t)ldu * q * 8, c->stream));
+    double* coef = static_cast<double*>(ws_get(c, WS_CD_COEF, (size_t)std::max<int64_t>(m_L, 1) * 4 * 8));
     lambda_cd(c, (int)q, static_cast<const double*>(Sigma), ldsigma, static_cast<const double*>(Psi), ldpsi,
               static_cast<const double*>(GradL), ldgl, Lambda, L_row, L_col, m_L, lam_L, penalize_diag, passes,
-              static_cast<double*>(D), U, ldu, out);
+              static_cast<double*>(D), U, ldu, coef, out);
     if (delta || l1_lambda) {
       double h[3];
       CGGM_CUDA_CHECK(cudaMemcpyAsync(h, out, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
@@ -465,8 +466,9 @@ cggm_status cggm_theta_cd(cggm_ctx* ctx, int64_t p, int64_t q, const void* Sigma
     CGGM_CUDA_CHECK(cudaMemsetAsync(V, 0, (size_t)ldv * q * 8, c->stream));
     theta_sigma(c, (int)q, Theta, static_cast<const double*>(Sigma), ldsigma, V, ldv);
     double* T = static_cast<double*>(const_cast<void*>(out->val));   // the sweep runs on the output values
+    double* coef = static_cast<double*>(ws_get(c, WS_CD_COEF, (size_t)std::max<int64_t>(m_T, 1) * 2 * 8));
     theta_cd(c, (int)p, (int)q, static_cast<const double*>(Sigma), ldsigma, static_cast<const double*>(Sxx), ldsxx,
-             static_cast<const double*>(Sxy), ldsxy, Theta, T_row, T_col, m_T, lam_T, passes, T, V, ldv, sc);
+             static_cast<const double*>(Sxy), ldsxy, Theta, T_row, T_col, m_T, lam_T, passes, T, V, ldv, coef, sc);
     list_to_csc(c, (int)q, T_row, T_col, m_T, false, nullptr, nullptr, 0.0, T, const_cast<int64_t*>(out->colptr),
                 const_cast<int32_t*>(out->rowidx), T, cnt, scan);
     double h = 0.0;

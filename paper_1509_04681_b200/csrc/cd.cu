@@ -16,6 +16,7 @@ namespace {
 
 constexpr int CD_NT = 1024;
 constexpr int CD_NW = CD_NT / 32;
+constexpr int CD_UNR = 4;   // vector elements per thread whose loads are issued together
 
 __device__ __forceinline__ double soft(double w, double r) {
   const double m = fabs(w) - r;
@@ -58,60 +59,131 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double (*red)[NV]) {
   __syncthreads();   // red reusable
 }
 
-// One CTA: D (values on the active list, zeroed here) by `passes` sweeps from D = 0; U (q x q, ldu,
-// zero on entry) = D Sigma throughout.  Afterwards out[0] = tr(GradL^T D) (both triangles), out[1] = ||Lambda + D||_1
-// - ||Lambda||_1 weighted by the penalty rule (lam = 0 on an unpenalised diagonal), out[2] =
-// ||Lambda||_1 (all entries, from the CSC).
+// Per-entry constants of the Lambda sweep (they do not change during it): a, Lambda_ij, GradL_ij and
+// the entry's lambda, computed for the whole list in parallel before the sequential walk.
+__global__ void k_lambda_coefs(int64_t m, const double* __restrict__ S, int64_t lds, const double* __restrict__ P,
+                               int64_t ldp, const double* __restrict__ G, int64_t ldg, const int64_t* colptr,
+                               const int32_t* rowidx, const double* lval, const int32_t* Lr, const int32_t* Lc,
+                               double lam, int penalize_diag, double4* coef) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+    const int i = Lr[k], j = Lc[k];
+    const double Sii = S[i + (int64_t)i * lds], Sjj = S[j + (int64_t)j * lds], Sij = S[i + (int64_t)j * lds];
+    const double Pii = P[i + (int64_t)i * ldp], Pjj = P[j + (int64_t)j * ldp], Pij = P[i + (int64_t)j * ldp];
+    const double a = (i == j) ? Sii * Sii + 2.0 * Sii * Pii
+                              : Sij * Sij + Sii * Sjj + Sii * Pjj + Sjj * Pii + 2.0 * Sij * Pij;
+    coef[k] = make_double4(a, csc_at(colptr, rowidx, lval, i, j), G[i + (int64_t)j * ldg],
+                           (i == j && !penalize_diag) ? 0.0 : lam);
+  }
+}
+
+// One CTA: D (values on the active list, zeroed here) by `passes` sweeps from D = 0; U (q x q,
+// row-major with row stride ldu, zero on entry) = D Sigma throughout.  Per update: the three dot
+// products, ONE barrier, every thread sums the 32 warp partials in the same order and forms the
+// same mu (no broadcast barrier), the two contiguous row updates, ONE barrier.  The next entry's
+// indices and constants are loaded while the current one is processed.  Afterwards out[0] =
+// tr(GradL^T D) (both triangles), out[1] = ||Lambda + D||_1 - ||Lambda||_1 weighted by the penalty
+// rule, out[2] = ||Lambda||_1 (all entries, from the CSC).
 __global__ void __launch_bounds__(CD_NT) k_lambda_cd(int q, const double* __restrict__ S, int64_t lds,
                                                      const double* __restrict__ P, int64_t ldp,
                                                      const double* __restrict__ G, int64_t ldg, const int64_t* colptr,
                                                      const int32_t* rowidx, const double* lval, const int32_t* Lr,
-                                                     const int32_t* Lc, int64_t m, double lam, int penalize_diag,
-                                                     int passes, double* D, double* U, int64_t ldu, double* out) {
-  __shared__ double red[CD_NW][3];
-  __shared__ double mu_sh;
+                                                     const int32_t* Lc, const double4* coef, int64_t m,
+                                                     int penalize_diag, double lam, int passes, double* D, double* U,
+                                                     int64_t ldu, double* out) {
+  __shared__ double red[2][CD_NW][3];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t k = threadIdx.x; k < m; k += CD_NT) D[k] = 0.0;   // a fresh direction (U = 0 on entry)
   __syncthreads();
+  int par = 0;
   for (int pass = 0; pass < passes; ++pass) {
+    int ni = m > 0 ? Lr[0] : 0, nj = m > 0 ? Lc[0] : 0;
+    double4 nc = m > 0 ? coef[0] : make_double4(0, 0, 0, 0);
+    double nd = m > 0 ? D[0] : 0.0;
     for (int64_t k = 0; k < m; ++k) {
-      const int i = Lr[k], j = Lc[k];
+      const int i = ni, j = nj;
+      const double4 cf = nc;
+      const double dk = nd;
+      if (k + 1 < m) {   // prefetch: the list and the constants are not modified by the sweep
+        ni = Lr[k + 1];
+        nj = Lc[k + 1];
+        nc = coef[k + 1];
+        nd = D[k + 1];
+      }
       const double* Si = S + (int64_t)i * lds;   // row i of Sigma = column i (symmetric)
       const double* Pi = P + (int64_t)i * ldp;
       const double* Pj = P + (int64_t)j * ldp;
-      const double* Uj = U + (int64_t)j * ldu;
-      const double* Ui = U + (int64_t)i * ldu;
-      double v[3] = {0.0, 0.0, 0.0};
-      for (int t = threadIdx.x; t < q; t += CD_NT) {
-        const double uj = Uj[t];
-        v[0] = fma(Si[t], uj, v[0]);
-        v[1] = fma(Pi[t], uj, v[1]);
-        v[2] = fma(Pj[t], Ui[t], v[2]);
+      // U is row-major (U[t][c] at t * ldu + c): its columns j, i are strided reads, while the two
+      // row updates below -- the larger traffic -- are contiguous
+      // all of a thread's loads in flight together (CD_UNR elements per batch), then the FMAs
+      double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+      for (int t0 = threadIdx.x; t0 < q; t0 += CD_UNR * CD_NT) {
+        double uj[CD_UNR], ui[CD_UNR], si[CD_UNR], pi[CD_UNR], pj[CD_UNR];
+#pragma unroll
+        for (int u = 0; u < CD_UNR; ++u) {
+          const int t = t0 + u * CD_NT;
+          const bool in = t < q;
+          uj[u] = in ? U[(int64_t)t * ldu + j] : 0.0;
+          ui[u] = in ? U[(int64_t)t * ldu + i] : 0.0;
+          si[u] = in ? Si[t] : 0.0;
+          pi[u] = in ? Pi[t] : 0.0;
+          pj[u] = in ? Pj[t] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < CD_UNR; ++u) {
+          v0 = fma(si[u], uj[u], v0);
+          v1 = fma(pi[u], uj[u], v1);
+          v2 = fma(pj[u], ui[u], v2);
+        }
       }
-      block_sum<3>(v, red);
-      if (threadIdx.x == 0) {
-        const double Sii = S[i + (int64_t)i * lds], Sjj = S[j + (int64_t)j * lds], Sij = S[i + (int64_t)j * lds];
-        const double Pii = P[i + (int64_t)i * ldp], Pjj = P[j + (int64_t)j * ldp], Pij = P[i + (int64_t)j * ldp];
-        const double a = (i == j) ? Sii * Sii + 2.0 * Sii * Pii
-                                  : Sij * Sij + Sii * Sjj + Sii * Pjj + Sjj * Pii + 2.0 * Sij * Pij;
-        const double b = G[i + (int64_t)j * ldg] + v[0] + v[1] + v[2];
-        const double c = csc_at(colptr, rowidx, lval, i, j) + D[k];
-        const double lm = (i == j && !penalize_diag) ? 0.0 : lam;
-        double mu = 0.0;
-        if (a > 0.0) mu = -c + soft(c - b / a, lm / a);
-        D[k] += mu;
-        mu_sh = mu;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+        v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+        v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+      }
+      if (lane == 0) {
+        red[par][w][0] = v0;
+        red[par][w][1] = v1;
+        red[par][w][2] = v2;
       }
       __syncthreads();
-      const double mu = mu_sh;
+      // every warp reduces the 32 warp partials by the same shfl_down tree and takes lane 0's value:
+      // bitwise the same b in every thread, so every thread forms the same mu without a broadcast
+      double b = (red[par][lane][0] + red[par][lane][1]) + red[par][lane][2];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) b += __shfl_down_sync(0xffffffffu, b, o);
+      b = __shfl_sync(0xffffffffu, b, 0);
+      par ^= 1;   // the other buffer was last read before this barrier
+      b += cf.z;
+      const double a = cf.x, c = cf.y + dk;
+      const double mu = (a > 0.0) ? -c + soft(c - b / a, cf.w / a) : 0.0;
+      if (threadIdx.x == 0) D[k] = dk + mu;
       if (mu != 0.0) {
         const double* Sj = S + (int64_t)j * lds;
-        for (int t = threadIdx.x; t < q; t += CD_NT) {
-          const int64_t o = (int64_t)t * ldu;
-          if (i != j) {
-            U[i + o] += mu * Sj[t];
-            U[j + o] += mu * Si[t];
-          } else {
-            U[i + o] += mu * Si[t];
+        double* Ur_i = U + (int64_t)i * ldu;
+        double* Ur_j = U + (int64_t)j * ldu;
+        for (int t0 = threadIdx.x; t0 < q; t0 += CD_UNR * CD_NT) {
+          double a0[CD_UNR], a1[CD_UNR], s0[CD_UNR], s1[CD_UNR];
+#pragma unroll
+          for (int u = 0; u < CD_UNR; ++u) {
+            const int t = t0 + u * CD_NT;
+            const bool in = t < q;
+            a0[u] = in ? Ur_i[t] : 0.0;
+            s0[u] = in ? Sj[t] : 0.0;
+            a1[u] = (in && i != j) ? Ur_j[t] : 0.0;
+            s1[u] = (in && i != j) ? Si[t] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < CD_UNR; ++u) {
+            const int t = t0 + u * CD_NT;
+            if (t < q) {
+              if (i != j) {
+                Ur_i[t] = a0[u] + mu * s0[u];
+                Ur_j[t] = a1[u] + mu * s1[u];
+              } else {
+                Ur_i[t] = a0[u] + mu * s0[u];
+              }
+            }
           }
         }
       }
@@ -119,18 +191,18 @@ __global__ void __launch_bounds__(CD_NT) k_lambda_cd(int q, const double* __rest
     }
   }
   // line-search decrease measure and ||Lambda||_1, fixed-order block reduction
+  __shared__ double red3[CD_NW][3];
   double v[3] = {0.0, 0.0, 0.0};
   for (int64_t k = threadIdx.x; k < m; k += CD_NT) {
     const int i = Lr[k], j = Lc[k];
-    const double w = (i == j) ? 1.0 : 2.0;
-    const double lm = (i == j && !penalize_diag) ? 0.0 : lam;
-    const double l = csc_at(colptr, rowidx, lval, i, j);
-    v[0] += w * G[i + (int64_t)j * ldg] * D[k];
-    v[1] += w * lm * (fabs(l + D[k]) - fabs(l));
+    const double wgt = (i == j) ? 1.0 : 2.0;
+    const double4 cf = coef[k];
+    v[0] += wgt * cf.z * D[k];
+    v[1] += wgt * cf.w * (fabs(cf.y + D[k]) - fabs(cf.y));
   }
   for (int j = threadIdx.x; j < q; j += CD_NT)
     for (int64_t t = colptr[j]; t < colptr[j + 1]; ++t) v[2] += fabs(lval[t]);
-  block_sum<3>(v, red);
+  block_sum<3>(v, red3);
   if (threadIdx.x == 0) {
     out[0] = v[0];
     out[1] = v[1];
@@ -154,48 +226,95 @@ __global__ void k_theta_sigma(int q, const int64_t* colptr, const int32_t* rowid
   }
 }
 
-// One CTA: Theta values on the active list (in: current Theta, gathered here; out: after the
-// sweeps); V = Theta Sigma maintained.  out[0] = ||Theta_new||_1.
+// Per-entry constants of the Theta sweep: a = 2 Sigma_jj (S_xx)_ii, 2 (S_xy)_ij, the current Theta_ij
+// (gathered from the CSC into T, the sweep's state) -- before the sequential walk.
+__global__ void k_theta_coefs(int64_t m, const double* __restrict__ S, int64_t lds, const double* __restrict__ Sxx,
+                              int64_t ldx, const double* __restrict__ Sxy, int64_t ldxy, const int64_t* colptr,
+                              const int32_t* rowidx, const double* tval, const int32_t* Tr, const int32_t* Tc,
+                              double2* coef, double* T) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+    const int i = Tr[k], j = Tc[k];
+    coef[k] = make_double2(2.0 * S[j + (int64_t)j * lds] * Sxx[i + (int64_t)i * ldx], 2.0 * Sxy[i + (int64_t)j * ldxy]);
+    T[k] = csc_at(colptr, rowidx, tval, i, j);
+  }
+}
+
+// One CTA: Theta values on the active list (T: the gathered current values on entry, the new ones
+// on exit); V = Theta Sigma maintained (column-major: the length-p dot reads a contiguous column,
+// the length-q row update is strided -- p > q on the paper's problems).  Same one-barrier-per-step
+// structure as the Lambda sweep.  out[0] = ||Theta_new||_1.
 __global__ void __launch_bounds__(CD_NT) k_theta_cd(int p, int q, const double* __restrict__ S, int64_t lds,
-                                                    const double* __restrict__ Sxx, int64_t ldx,
-                                                    const double* __restrict__ Sxy, int64_t ldxy,
-                                                    const int64_t* colptr, const int32_t* rowidx, const double* tval,
-                                                    const int32_t* Tr, const int32_t* Tc, int64_t m, double lam,
+                                                    const double* __restrict__ Sxx, int64_t ldx, const int32_t* Tr,
+                                                    const int32_t* Tc, const double2* coef, int64_t m, double lam,
                                                     int passes, double* T, double* V, int64_t ldv, double* out) {
-  __shared__ double red[CD_NW][1];
-  __shared__ double mu_sh;
-  for (int64_t k = threadIdx.x; k < m; k += CD_NT) T[k] = csc_at(colptr, rowidx, tval, Tr[k], Tc[k]);
-  __syncthreads();
+  __shared__ double red[2][CD_NW];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int par = 0;
   for (int pass = 0; pass < passes; ++pass) {
+    int ni = m > 0 ? Tr[0] : 0, nj = m > 0 ? Tc[0] : 0;
+    double2 nc = m > 0 ? coef[0] : make_double2(0, 0);
+    double nt = m > 0 ? T[0] : 0.0;
     for (int64_t k = 0; k < m; ++k) {
-      const int i = Tr[k], j = Tc[k];
+      const int i = ni, j = nj;
+      const double2 cf = nc;
+      const double c = nt;
+      if (k + 1 < m) {
+        ni = Tr[k + 1];
+        nj = Tc[k + 1];
+        nc = coef[k + 1];
+        nt = T[k + 1];
+      }
       const double* Xi = Sxx + (int64_t)i * ldx;   // row i of S_xx = column i
       const double* Vj = V + (int64_t)j * ldv;
-      double v[1] = {0.0};
-      for (int t = threadIdx.x; t < p; t += CD_NT) v[0] = fma(Xi[t], Vj[t], v[0]);
-      block_sum<1>(v, red);
-      if (threadIdx.x == 0) {
-        const double a = 2.0 * S[j + (int64_t)j * lds] * Sxx[i + (int64_t)i * ldx];
-        const double b = 2.0 * Sxy[i + (int64_t)j * ldxy] + 2.0 * v[0];
-        const double c = T[k];
-        double mu = 0.0;
-        if (a > 0.0) mu = -c + soft(c - b / a, lam / a);
-        T[k] += mu;
-        mu_sh = mu;
+      double v = 0.0;
+      for (int t0 = threadIdx.x; t0 < p; t0 += CD_UNR * CD_NT) {
+        double xa[CD_UNR], va[CD_UNR];
+#pragma unroll
+        for (int u = 0; u < CD_UNR; ++u) {
+          const int t = t0 + u * CD_NT;
+          xa[u] = t < p ? Xi[t] : 0.0;
+          va[u] = t < p ? Vj[t] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < CD_UNR; ++u) v = fma(xa[u], va[u], v);
       }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) red[par][w] = v;
       __syncthreads();
-      const double mu = mu_sh;
+      double dot = red[par][lane];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dot += __shfl_down_sync(0xffffffffu, dot, o);
+      dot = __shfl_sync(0xffffffffu, dot, 0);
+      par ^= 1;
+      const double a = cf.x, b = cf.y + 2.0 * dot;
+      const double mu = (a > 0.0) ? -c + soft(c - b / a, lam / a) : 0.0;
+      if (threadIdx.x == 0) T[k] = c + mu;
       if (mu != 0.0) {
         const double* Sj = S + (int64_t)j * lds;
-        for (int t = threadIdx.x; t < q; t += CD_NT) V[i + (int64_t)t * ldv] += mu * Sj[t];
+        for (int t0 = threadIdx.x; t0 < q; t0 += CD_UNR * CD_NT) {
+          double va[CD_UNR], sa[CD_UNR];
+#pragma unroll
+          for (int u = 0; u < CD_UNR; ++u) {
+            const int t = t0 + u * CD_NT;
+            va[u] = t < q ? V[i + (int64_t)t * ldv] : 0.0;
+            sa[u] = t < q ? Sj[t] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < CD_UNR; ++u) {
+            const int t = t0 + u * CD_NT;
+            if (t < q) V[i + (int64_t)t * ldv] = va[u] + mu * sa[u];
+          }
+        }
       }
       __syncthreads();
     }
   }
-  double v[1] = {0.0};
-  for (int64_t k = threadIdx.x; k < m; k += CD_NT) v[0] += fabs(T[k]);
-  block_sum<1>(v, red);
-  if (threadIdx.x == 0) out[0] = v[0];
+  __shared__ double red1[CD_NW][1];
+  double vv[1] = {0.0};
+  for (int64_t k = threadIdx.x; k < m; k += CD_NT) vv[0] += fabs(T[k]);
+  block_sum<1>(vv, red1);
+  if (threadIdx.x == 0) out[0] = vv[0];
 }
 
 // ---------------------------------------------------------------- sparse bookkeeping
@@ -299,11 +418,16 @@ int grid_for(int64_t m) { return (int)std::min<int64_t>(std::max<int64_t>((m + 2
 
 void lambda_cd(Ctx* c, int q, const double* S, int64_t lds, const double* P, int64_t ldp, const double* G, int64_t ldg,
                const cggm_csc* Lam, const int32_t* Lr, const int32_t* Lc, int64_t m, double lam, int penalize_diag,
-               int passes, double* D, double* U, int64_t ldu, double* out) {
+               int passes, double* D, double* U, int64_t ldu, double* coef_ws, double* out) {
   Prof pr(c, TAG_MISC);
-  k_lambda_cd<<<1, CD_NT, 0, c->stream>>>(q, S, lds, P, ldp, G, ldg, Lam->colptr, Lam->rowidx,
-                                          static_cast<const double*>(Lam->val), Lr, Lc, m, lam, penalize_diag, passes, D,
-                                          U, ldu, out);
+  double4* coef = reinterpret_cast<double4*>(coef_ws);
+  const double* lv = static_cast<const double*>(Lam->val);
+  if (m > 0)
+    k_lambda_coefs<<<grid_for(m), 256, 0, c->stream>>>(m, S, lds, P, ldp, G, ldg, Lam->colptr, Lam->rowidx, lv, Lr, Lc,
+                                                       lam, penalize_diag, coef);
+  k_lambda_cd<<<1, CD_NT, 0, c->stream>>>(q, S, lds, P, ldp, G, ldg, Lam->colptr, Lam->rowidx, lv, Lr, Lc, coef, m,
+                                          penalize_diag, lam, passes, D, U, ldu, out);
+  c->launches += m > 0 ? 1 : 0;
   post_launch(c, "k_lambda_cd");
 }
 
@@ -316,10 +440,14 @@ void theta_sigma(Ctx* c, int q, const cggm_csc* Th, const double* S, int64_t lds
 
 void theta_cd(Ctx* c, int p, int q, const double* S, int64_t lds, const double* Sxx, int64_t ldx, const double* Sxy,
               int64_t ldxy, const cggm_csc* Th, const int32_t* Tr, const int32_t* Tc, int64_t m, double lam, int passes,
-              double* T, double* V, int64_t ldv, double* out) {
+              double* T, double* V, int64_t ldv, double* coef_ws, double* out) {
   Prof pr(c, TAG_MISC);
-  k_theta_cd<<<1, CD_NT, 0, c->stream>>>(p, q, S, lds, Sxx, ldx, Sxy, ldxy, Th->colptr, Th->rowidx,
-                                         static_cast<const double*>(Th->val), Tr, Tc, m, lam, passes, T, V, ldv, out);
+  double2* coef = reinterpret_cast<double2*>(coef_ws);
+  if (m > 0)
+    k_theta_coefs<<<grid_for(m), 256, 0, c->stream>>>(m, S, lds, Sxx, ldx, Sxy, ldxy, Th->colptr, Th->rowidx,
+                                                      static_cast<const double*>(Th->val), Tr, Tc, coef, T);
+  k_theta_cd<<<1, CD_NT, 0, c->stream>>>(p, q, S, lds, Sxx, ldx, Tr, Tc, coef, m, lam, passes, T, V, ldv, out);
+  c->launches += m > 0 ? 1 : 0;
   post_launch(c, "k_theta_cd");
 }
 

@@ -164,6 +164,7 @@ enum Slot {
   WS_CD_V,          // Theta sweep: V = Theta Sigma (p x q)
   WS_CD_IDX,        // list -> CSC counts / scans
   WS_CD_OUT,        // sweep scalars
+  WS_CD_COEF,       // per-entry sweep constants
   WS_NUM
 };
 

@@ -52,11 +52,11 @@ void active_compact(Ctx* c, int64_t p, int64_t q, const T* GradL, int64_t ldgl, 
 // Coordinate-descent consumers (cd.cu), fp64
 void lambda_cd(Ctx* c, int q, const double* S, int64_t lds, const double* P, int64_t ldp, const double* G, int64_t ldg,
                const cggm_csc* Lam, const int32_t* Lr, const int32_t* Lc, int64_t m, double lam, int penalize_diag,
-               int passes, double* D, double* U, int64_t ldu, double* out);
+               int passes, double* D, double* U, int64_t ldu, double* coef_ws /* 4m doubles */, double* out);
 void theta_sigma(Ctx* c, int q, const cggm_csc* Th, const double* S, int64_t lds, double* V, int64_t ldv);
 void theta_cd(Ctx* c, int p, int q, const double* S, int64_t lds, const double* Sxx, int64_t ldx, const double* Sxy,
               int64_t ldxy, const cggm_csc* Th, const int32_t* Tr, const int32_t* Tc, int64_t m, double lam, int passes,
-              double* T, double* V, int64_t ldv, double* out);
+              double* T, double* V, int64_t ldv, double* coef_ws /* 2m doubles */, double* out);
 // sorted list (column-major) -> CSC: mirror = symmetric Lambda + alpha D from the upper-triangle list
 // (values base_ij + alpha D[k]); otherwise the list itself with `vals`.  cnt_ws: 3n ints, scan_ws:
 // 2(n+1) int64.
