@@ -167,6 +167,7 @@ cggm_status cggm_ctx_create(cggm_ctx** out, int device, cggm_dtype dtype, void* 
   if (const char* e = std::getenv("CGGM_NO_ACTIVE_VEC")) c->no_active_vec = std::atoi(e);
   if (const char* e = std::getenv("CGGM_MID_TILE")) c->mid_tile = std::atoi(e);
   if (const char* e = std::getenv("CGGM_LEAF_SWEEP")) c->leaf_sweep = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_CD_COOP")) c->cd_coop = std::atoi(e);
   if (const char* e = std::getenv("CGGM_GRAPH_PROF")) c->graph_prof = std::atoi(e);
   cudaDriverEntryPointQueryResult q;
   void* fn = nullptr;
@@ -398,9 +399,25 @@ cggm_status cggm_lambda_direction(cggm_ctx* ctx, int64_t q, const void* Sigma, i
     // a fresh direction: D = 0 (zeroed by the kernel), so U = D Sigma = 0
     CGGM_CUDA_CHECK(cudaMemsetAsync(U, 0, (size_t)ldu * q * 8, c->stream));
     double* coef = static_cast<double*>(ws_get(c, WS_CD_COEF, (size_t)std::max<int64_t>(m_L, 1) * 4 * 8));
-    lambda_cd(c, (int)q, static_cast<const double*>(Sigma), ldsigma, static_cast<const double*>(Psi), ldpsi,
-              static_cast<const double*>(GradL), ldgl, Lambda, L_row, L_col, m_L, lam_L, penalize_diag, passes,
-              static_cast<double*>(D), U, ldu, coef, out);
+    if (coop_ok(c)) {
+      double* Z = static_cast<double*>(ws_get(c, WS_CD_Z, (size_t)ldu * q * 8));
+      CGGM_CUDA_CHECK(cudaMemsetAsync(Z, 0, (size_t)ldu * q * 8, c->stream));
+      const size_t aux = (size_t)q * 4 + 2 * (size_t)(q + 1) * 8 + (size_t)std::max<int64_t>(m_L, 1) * 8 +
+                         (size_t)2 * q * 8 + 4 * 64;
+      char* w = static_cast<char*>(ws_get(c, WS_CD_AUX, aux));
+      int* cnt = reinterpret_cast<int*>(w);
+      int64_t* scr = reinterpret_cast<int64_t*>(w + ((size_t)q * 4 + 63) / 64 * 64);
+      int64_t* lp = scr + (q + 1);
+      double* dmu = reinterpret_cast<double*>(lp + (q + 1));
+      double* colbuf = dmu + std::max<int64_t>(m_L, 1);
+      lambda_cd_coop(c, (int)q, static_cast<const double*>(Sigma), ldsigma, static_cast<const double*>(Psi), ldpsi,
+                     static_cast<const double*>(GradL), ldgl, Lambda, L_row, L_col, m_L, lam_L, penalize_diag, passes,
+                     static_cast<double*>(D), U, Z, ldu, coef, cnt, scr, lp, dmu, colbuf, out);
+    } else {
+      lambda_cd(c, (int)q, static_cast<const double*>(Sigma), ldsigma, static_cast<const double*>(Psi), ldpsi,
+                static_cast<const double*>(GradL), ldgl, Lambda, L_row, L_col, m_L, lam_L, penalize_diag, passes,
+                static_cast<double*>(D), U, ldu, coef, out);
+    }
     if (delta || l1_lambda) {
       double h[3];
       CGGM_CUDA_CHECK(cudaMemcpyAsync(h, out, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
@@ -463,12 +480,29 @@ cggm_status cggm_theta_cd(cggm_ctx* ctx, int64_t p, int64_t q, const void* Sigma
     double* sc = static_cast<double*>(ws_get(c, WS_CD_OUT, 64));
     int* cnt = static_cast<int*>(ws_get(c, WS_CD_IDX, (size_t)3 * q * 4 + (size_t)2 * (q + 1) * 8 + 64));
     int64_t* scan = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(cnt) + ((size_t)3 * q * 4 + 63) / 64 * 64);
-    CGGM_CUDA_CHECK(cudaMemsetAsync(V, 0, (size_t)ldv * q * 8, c->stream));
-    theta_sigma(c, (int)q, Theta, static_cast<const double*>(Sigma), ldsigma, V, ldv);
     double* T = static_cast<double*>(const_cast<void*>(out->val));   // the sweep runs on the output values
     double* coef = static_cast<double*>(ws_get(c, WS_CD_COEF, (size_t)std::max<int64_t>(m_T, 1) * 2 * 8));
-    theta_cd(c, (int)p, (int)q, static_cast<const double*>(Sigma), ldsigma, static_cast<const double*>(Sxx), ldsxx,
-             static_cast<const double*>(Sxy), ldsxy, Theta, T_row, T_col, m_T, lam_T, passes, T, V, ldv, coef, sc);
+    if (coop_ok(c)) {
+      const int64_t ldvr = pad_ld<double>(q);   // row-major V: p rows of stride ldvr
+      V = static_cast<double*>(ws_get(c, WS_CD_V, (size_t)ldvr * p * 8));
+      CGGM_CUDA_CHECK(cudaMemsetAsync(V, 0, (size_t)ldvr * p * 8, c->stream));
+      const size_t aux = (size_t)q * 4 + 2 * (size_t)(q + 1) * 8 + (size_t)std::max<int64_t>(m_T, 1) * 8 +
+                         (size_t)p * 8 + 4 * 64;
+      char* w = static_cast<char*>(ws_get(c, WS_CD_AUX, aux));
+      int* cnt2 = reinterpret_cast<int*>(w);
+      int64_t* scr = reinterpret_cast<int64_t*>(w + ((size_t)q * 4 + 63) / 64 * 64);
+      int64_t* lp = scr + (q + 1);
+      double* dmu = reinterpret_cast<double*>(lp + (q + 1));
+      double* colbuf = dmu + std::max<int64_t>(m_T, 1);
+      theta_cd_coop(c, (int)p, (int)q, static_cast<const double*>(Sigma), ldsigma, static_cast<const double*>(Sxx),
+                    ldsxx, static_cast<const double*>(Sxy), ldsxy, Theta, T_row, T_col, m_T, lam_T, passes, T, V, ldvr,
+                    coef, cnt2, scr, lp, dmu, colbuf, sc);
+    } else {
+      CGGM_CUDA_CHECK(cudaMemsetAsync(V, 0, (size_t)ldv * q * 8, c->stream));
+      theta_sigma(c, (int)q, Theta, static_cast<const double*>(Sigma), ldsigma, V, ldv);
+      theta_cd(c, (int)p, (int)q, static_cast<const double*>(Sigma), ldsigma, static_cast<const double*>(Sxx), ldsxx,
+               static_cast<const double*>(Sxy), ldsxy, Theta, T_row, T_col, m_T, lam_T, passes, T, V, ldv, coef, sc);
+    }
     list_to_csc(c, (int)q, T_row, T_col, m_T, false, nullptr, nullptr, 0.0, T, const_cast<int64_t*>(out->colptr),
                 const_cast<int32_t*>(out->rowidx), T, cnt, scan);
     double h = 0.0;

@@ -9,6 +9,8 @@
 // (Lambda) or one (Theta) length-q / length-p dot products as a block reduction, then the two /
 // one row updates of U / V, each thread owning a stride of the vector.  Reduction order is fixed,
 // so sweeps are bitwise reproducible.
+#include <cooperative_groups.h>
+
 #include "kernels.cuh"
 
 namespace cggm {
@@ -317,6 +319,242 @@ __global__ void __launch_bounds__(CD_NT) k_theta_cd(int p, int q, const double* 
   if (threadIdx.x == 0) out[0] = vv[0];
 }
 
+// ---------------------------------------------------------------- column-batched cooperative sweeps
+// The active lists are column-major, so consecutive updates share the column j.  With
+// Z = D Psi (so that (Psi D Sigma)_ji = (Sigma D Psi)_ij = Sigma_i . Z_{:,j}) every dot product of
+// the Lambda update reads only column j of U = D Sigma and of Z:
+//     b = GradL_ij + (Sigma_i + Psi_i) . U_{:,j} + Sigma_i . Z_{:,j}
+// and an update changes column j in two entries only (rows i and j).  So per column: CTA 0 walks
+// the column's entries with U_{:,j}, Z_{:,j} in shared memory (O(1) column updates), then the whole
+// grid applies the column's deferred row updates U[i, t] += mu Sigma[j, t], U[j, t] += mu Sigma[i, t]
+// (and Z with Psi) to every other column t -- off the sequential chain, coalesced (U, Z row-major).
+// Two grid barriers per non-empty column.  The Theta sweep is the same with V = Theta Sigma.
+constexpr int CO_NT = 512;
+constexpr int CO_NW = CO_NT / 32;
+constexpr int CO_UNR = 8;
+
+__device__ __forceinline__ double co_block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double b = lane < CO_NW ? red[lane] : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) b += __shfl_down_sync(0xffffffffu, b, o);
+  b = __shfl_sync(0xffffffffu, b, 0);   // the same value in every thread
+  __syncthreads();
+  return b;
+}
+
+__global__ void __launch_bounds__(CO_NT) k_lambda_sweep_coop(int q, const double* __restrict__ S, int64_t lds,
+                                                             const double* __restrict__ P, int64_t ldp,
+                                                             const int32_t* Lr, const double4* coef, const int64_t* lp,
+                                                             int passes, double* D, double* dmu, double* U, double* Z,
+                                                             int64_t ldu, double* colbuf, int use_smem) {
+  namespace cgx = cooperative_groups;
+  cgx::grid_group grid = cgx::this_grid();
+  extern __shared__ double co_sm[];
+  __shared__ double red[CO_NW];
+  double* Uj = use_smem ? co_sm : colbuf;
+  double* Zj = Uj + q;
+  const int64_t gtid = blockIdx.x * (int64_t)CO_NT + threadIdx.x, gsz = (int64_t)gridDim.x * CO_NT;
+  for (int pass = 0; pass < passes; ++pass) {
+    for (int j = 0; j < q; ++j) {
+      const int64_t k0 = lp[j], k1 = lp[j + 1];
+      if (k0 == k1) continue;
+      if (blockIdx.x == 0) {
+        for (int t = threadIdx.x; t < q; t += CO_NT) {
+          Uj[t] = U[(int64_t)t * ldu + j];
+          Zj[t] = Z[(int64_t)t * ldu + j];
+        }
+        __syncthreads();
+        const double Sjj = S[j + (int64_t)j * lds], Pjj = P[j + (int64_t)j * ldp];
+        for (int64_t k = k0; k < k1; ++k) {
+          const int i = Lr[k];
+          const double4 cf = coef[k];
+          const double* Si = S + (int64_t)i * lds;
+          const double* Pi = P + (int64_t)i * ldp;
+          // CO_UNR elements per thread in flight at once (the columns come from DRAM / L2)
+          double v = 0.0;
+          for (int t0 = threadIdx.x; t0 < q; t0 += CO_UNR * CO_NT) {
+            double sv[CO_UNR], pv[CO_UNR];
+#pragma unroll
+            for (int u = 0; u < CO_UNR; ++u) {
+              const int t = t0 + u * CO_NT;
+              sv[u] = t < q ? Si[t] : 0.0;
+              pv[u] = t < q ? Pi[t] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < CO_UNR; ++u) {
+              const int t = t0 + u * CO_NT;
+              if (t < q) v = fma(sv[u] + pv[u], Uj[t], fma(sv[u], Zj[t], v));
+            }
+          }
+          const double b = cf.z + co_block_sum(v, red);
+          const double a = cf.x, c = cf.y + D[k];
+          const double mu = (a > 0.0) ? -c + soft(c - b / a, cf.w / a) : 0.0;
+          if (threadIdx.x == 0) {
+            D[k] = c - cf.y + mu;
+            dmu[k] = mu;
+            Uj[i] += mu * Sjj;
+            Zj[i] += mu * Pjj;
+            if (i != j) {
+              Uj[j] += mu * Si[j];
+              Zj[j] += mu * Pi[j];
+            }
+          }
+          __syncthreads();
+        }
+        for (int t = threadIdx.x; t < q; t += CO_NT) {
+          U[(int64_t)t * ldu + j] = Uj[t];
+          Z[(int64_t)t * ldu + j] = Zj[t];
+        }
+      }
+      grid.sync();
+      // the column's deferred row updates, t != j (column j is current in memory already):
+      //   rows i_k != j: U[i_k, t] += mu_k Sigma[j, t], Z[i_k, t] += mu_k Psi[j, t]  -- parallel over (k, t)
+      //   row j:         U[j, t] += sum_k mu_k Sigma[i_k, t] (Z with Psi)          -- parallel over t
+      // (disjoint elements: no ordering between the two loops)
+      {
+        const int64_t nk = k1 - k0, work = nk * (int64_t)q;
+        for (int64_t w = gtid; w < work; w += gsz) {
+          const int64_t k = k0 + w / q;
+          const int t = (int)(w - (k - k0) * q);
+          const int i = Lr[k];
+          const double mu = dmu[k];
+          if (t == j || i == j || mu == 0.0) continue;
+          U[(int64_t)i * ldu + t] += mu * S[t + (int64_t)j * lds];
+          Z[(int64_t)i * ldu + t] += mu * P[t + (int64_t)j * ldp];
+        }
+        for (int64_t t = gtid; t < q; t += gsz) {
+          if (t == j) continue;
+          double ua = 0.0, za = 0.0;
+          for (int64_t k = k0; k < k1; ++k) {
+            const double mu = dmu[k];
+            const int i = Lr[k];
+            ua = fma(mu, S[t + (int64_t)i * lds], ua);
+            za = fma(mu, P[t + (int64_t)i * ldp], za);
+          }
+          U[(int64_t)j * ldu + t] += ua;
+          Z[(int64_t)j * ldu + t] += za;
+        }
+      }
+      grid.sync();
+    }
+  }
+}
+
+// the Lambda sweep's scalars after the walk: out[0] = tr(GradL^T D), out[1] = the penalty change,
+// out[2] = ||Lambda||_1
+__global__ void __launch_bounds__(CD_NT) k_lambda_tail(int q, const int64_t* colptr, const double* lval,
+                                                       const int32_t* Lr, const int32_t* Lc, const double4* coef,
+                                                       int64_t m, const double* D, double* out) {
+  __shared__ double red3[CD_NW][3];
+  double v[3] = {0.0, 0.0, 0.0};
+  for (int64_t k = threadIdx.x; k < m; k += CD_NT) {
+    const double wgt = (Lr[k] == Lc[k]) ? 1.0 : 2.0;
+    const double4 cf = coef[k];
+    v[0] += wgt * cf.z * D[k];
+    v[1] += wgt * cf.w * (fabs(cf.y + D[k]) - fabs(cf.y));
+  }
+  for (int j = threadIdx.x; j < q; j += CD_NT)
+    for (int64_t t = colptr[j]; t < colptr[j + 1]; ++t) v[2] += fabs(lval[t]);
+  block_sum<3>(v, red3);
+  if (threadIdx.x == 0) {
+    out[0] = v[0];
+    out[1] = v[1];
+    out[2] = v[2];
+  }
+}
+
+__global__ void __launch_bounds__(CD_NT) k_theta_l1(const double* T, int64_t m, double* out) {
+  __shared__ double red1[CD_NW][1];
+  double v[1] = {0.0};
+  for (int64_t k = threadIdx.x; k < m; k += CD_NT) v[0] += fabs(T[k]);
+  block_sum<1>(v, red1);
+  if (threadIdx.x == 0) out[0] = v[0];
+}
+
+// V = Theta Sigma, ROW-major (row stride ldv): one warp per output column t
+__global__ void k_theta_sigma_rm(int q, const int64_t* colptr, const int32_t* rowidx, const double* val,
+                                 const double* __restrict__ S, int64_t lds, double* V, int64_t ldv) {
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (t >= q) return;
+  for (int j = 0; j < q; ++j) {
+    const int64_t a = colptr[j], b = colptr[j + 1];
+    if (a == b) continue;
+    const double s = S[j + (int64_t)t * lds];
+    for (int64_t e = a + lane; e < b; e += 32) V[(int64_t)rowidx[e] * ldv + t] += val[e] * s;
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(CO_NT) k_theta_sweep_coop(int p, int q, const double* __restrict__ S, int64_t lds,
+                                                            const double* __restrict__ Sxx, int64_t ldx,
+                                                            const int32_t* Tr, const double2* coef, const int64_t* lp,
+                                                            double lam, int passes, double* T, double* dmu, double* V,
+                                                            int64_t ldv, double* colbuf, int use_smem) {
+  namespace cgx = cooperative_groups;
+  cgx::grid_group grid = cgx::this_grid();
+  extern __shared__ double co_sm[];
+  __shared__ double red[CO_NW];
+  double* Vj = use_smem ? co_sm : colbuf;
+  const int64_t gtid = blockIdx.x * (int64_t)CO_NT + threadIdx.x, gsz = (int64_t)gridDim.x * CO_NT;
+  for (int pass = 0; pass < passes; ++pass) {
+    for (int j = 0; j < q; ++j) {
+      const int64_t k0 = lp[j], k1 = lp[j + 1];
+      if (k0 == k1) continue;
+      if (blockIdx.x == 0) {
+        for (int t = threadIdx.x; t < p; t += CO_NT) Vj[t] = V[(int64_t)t * ldv + j];
+        __syncthreads();
+        const double Sjj = S[j + (int64_t)j * lds];
+        for (int64_t k = k0; k < k1; ++k) {
+          const int i = Tr[k];
+          const double2 cf = coef[k];
+          const double* Xi = Sxx + (int64_t)i * ldx;
+          double v = 0.0;
+          for (int t0 = threadIdx.x; t0 < p; t0 += CO_UNR * CO_NT) {
+            double xv[CO_UNR];
+#pragma unroll
+            for (int u = 0; u < CO_UNR; ++u) {
+              const int t = t0 + u * CO_NT;
+              xv[u] = t < p ? Xi[t] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < CO_UNR; ++u) {
+              const int t = t0 + u * CO_NT;
+              if (t < p) v = fma(xv[u], Vj[t], v);
+            }
+          }
+          const double b = cf.y + 2.0 * co_block_sum(v, red);
+          const double a = cf.x, c = T[k];
+          const double mu = (a > 0.0) ? -c + soft(c - b / a, lam / a) : 0.0;
+          if (threadIdx.x == 0) {
+            T[k] = c + mu;
+            dmu[k] = mu;
+            Vj[i] += mu * Sjj;
+          }
+          __syncthreads();
+        }
+        for (int t = threadIdx.x; t < p; t += CO_NT) V[(int64_t)t * ldv + j] = Vj[t];
+      }
+      grid.sync();
+      {   // deferred row updates V[i_k, t] += mu_k Sigma[j, t], t != j: parallel over (k, t)
+        const int64_t nk = k1 - k0, work = nk * (int64_t)q;
+        for (int64_t w = gtid; w < work; w += gsz) {
+          const int64_t k = k0 + w / q;
+          const int t = (int)(w - (k - k0) * q);
+          const double mu = dmu[k];
+          if (t == j || mu == 0.0) continue;
+          V[(int64_t)Tr[k] * ldv + t] += mu * S[t + (int64_t)j * lds];
+        }
+      }
+      grid.sync();
+    }
+  }
+}
+
 // ---------------------------------------------------------------- sparse bookkeeping
 // count list entries per column (cl) and mirrored entries per column (cm: entry (i, j), i < j,
 // mirrors into column i)
@@ -449,6 +687,91 @@ void theta_cd(Ctx* c, int p, int q, const double* S, int64_t lds, const double* 
   k_theta_cd<<<1, CD_NT, 0, c->stream>>>(p, q, S, lds, Sxx, ldx, Tr, Tc, coef, m, lam, passes, T, V, ldv, out);
   c->launches += m > 0 ? 1 : 0;
   post_launch(c, "k_theta_cd");
+}
+
+// list column pointers lp (n+1) of a column-major list: counts + scan (cnt: n ints, scr: n+1 int64)
+static void list_colptr(Ctx* c, int n, const int32_t* r, const int32_t* cidx, int64_t m, int* cnt, int64_t* scr,
+                        int64_t* lp) {
+  CGGM_CUDA_CHECK(cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)n, c->stream));
+  k_list_counts<<<grid_for(m), 256, 0, c->stream>>>(m, r, cidx, 0, cnt, nullptr);
+  k_list_scan<<<1, 1024, 0, c->stream>>>(n, cnt, nullptr, lp, scr, nullptr);
+  c->launches += 2;
+}
+
+bool coop_ok(Ctx* c) {
+  static int ok = -1;
+  if (ok < 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrCooperativeLaunch, c->device);
+    ok = v;
+  }
+  return ok && c->cd_coop;
+}
+
+// ws: cnt (q ints), scr (q+1 int64), lp (q+1 int64), dmu (m), colbuf (2q or p doubles)
+void lambda_cd_coop(Ctx* c, int q, const double* S, int64_t lds, const double* P, int64_t ldp, const double* G,
+                    int64_t ldg, const cggm_csc* Lam, const int32_t* Lr, const int32_t* Lc, int64_t m, double lam,
+                    int penalize_diag, int passes, double* D, double* U, double* Z, int64_t ldu, double* coef_ws,
+                    int* cnt, int64_t* scr, int64_t* lp, double* dmu, double* colbuf, double* out) {
+  Prof pr(c, TAG_MISC);
+  double4* coef = reinterpret_cast<double4*>(coef_ws);
+  const double* lv = static_cast<const double*>(Lam->val);
+  CGGM_CUDA_CHECK(cudaMemsetAsync(D, 0, sizeof(double) * (size_t)std::max<int64_t>(m, 1), c->stream));
+  if (m > 0) {
+    k_lambda_coefs<<<grid_for(m), 256, 0, c->stream>>>(m, S, lds, P, ldp, G, ldg, Lam->colptr, Lam->rowidx, lv, Lr, Lc,
+                                                       lam, penalize_diag, coef);
+    list_colptr(c, q, Lr, Lc, m, cnt, scr, lp);
+    const size_t smem = (size_t)2 * q * 8;
+    const int use_smem = smem <= 200 * 1024 ? 1 : 0;
+    static bool attr = false;
+    if (!attr) {
+      CGGM_CUDA_CHECK(cudaFuncSetAttribute(k_lambda_sweep_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+    int grid = c->num_sms;
+    void* args[] = {&q, &S, &lds, &P, &ldp, &Lr, &coef, &lp, &passes, &D, &dmu, &U, &Z, &ldu, &colbuf,
+                    const_cast<int*>(&use_smem)};
+    CGGM_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_lambda_sweep_coop, dim3(grid), dim3(CO_NT), args,
+                                                use_smem ? smem : 0, c->stream));
+    c->launches += 2;
+  }
+  k_lambda_tail<<<1, CD_NT, 0, c->stream>>>(q, Lam->colptr, lv, Lr, Lc, coef, m, D, out);
+  post_launch(c, "k_lambda_sweep_coop");
+}
+
+void theta_cd_coop(Ctx* c, int p, int q, const double* S, int64_t lds, const double* Sxx, int64_t ldx,
+                   const double* Sxy, int64_t ldxy, const cggm_csc* Th, const int32_t* Tr, const int32_t* Tc, int64_t m,
+                   double lam, int passes, double* T, double* V, int64_t ldv, double* coef_ws, int* cnt, int64_t* scr,
+                   int64_t* lp, double* dmu, double* colbuf, double* out) {
+  Prof pr(c, TAG_MISC);
+  double2* coef = reinterpret_cast<double2*>(coef_ws);
+  // V = Theta Sigma, row-major
+  k_theta_sigma_rm<<<(q + 7) / 8, 256, 0, c->stream>>>(q, Th->colptr, Th->rowidx, static_cast<const double*>(Th->val),
+                                                       S, lds, V, ldv);
+  if (m > 0) {
+    k_theta_coefs<<<grid_for(m), 256, 0, c->stream>>>(m, S, lds, Sxx, ldx, Sxy, ldxy, Th->colptr, Th->rowidx,
+                                                      static_cast<const double*>(Th->val), Tr, Tc, coef, T);
+    list_colptr(c, q, Tr, Tc, m, cnt, scr, lp);
+    const size_t smem = (size_t)p * 8;
+    const int use_smem = smem <= 200 * 1024 ? 1 : 0;
+    static bool attr = false;
+    if (!attr) {
+      CGGM_CUDA_CHECK(cudaFuncSetAttribute(k_theta_sweep_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+    int grid = c->num_sms;
+    void* args[] = {&p, &q, &S, &lds, &Sxx, &ldx, &Tr, &coef, &lp, &lam, &passes, &T, &dmu, &V, &ldv, &colbuf,
+                    const_cast<int*>(&use_smem)};
+    CGGM_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_theta_sweep_coop, dim3(grid), dim3(CO_NT), args,
+                                                use_smem ? smem : 0, c->stream));
+    c->launches += 2;
+  }
+  {
+    double* o = out;
+    // ||Theta_new||_1 by the single-CTA tail of the Theta kernel family
+    k_theta_l1<<<1, CD_NT, 0, c->stream>>>(T, m, o);
+  }
+  post_launch(c, "k_theta_sweep_coop");
 }
 
 // workspace: ints[2n] counts, int64[3(n+1)] scans

@@ -80,6 +80,7 @@ struct Ctx {
   int force_tile = 0;
   int small_kmax = 1024;    // mid-size GEMMs (64-tile grid < #SMs) with K <= this use the 32x32 cp.async kernel (CGGM_SMALL_KMAX)
   int leaf_sweep = 0;       // CGGM_LEAF_SWEEP=1: full-inverse leaves by the panel/sweep kernel (A/B)
+  int cd_coop = 1;          // CGGM_CD_COOP=0: single-CTA coordinate sweeps (no column batching)
   int mid_tile = 0;         // CGGM_MID_TILE=1: 128x64 tiles (2 CTAs/SM) for the large non-symmetric GEMMs
   int no_small_async = 0;
   int no_active_vec = 0;    // test hook (CGGM_NO_ACTIVE_VEC=1): scalar active-set kernel only   // test hook (CGGM_NO_SMALL_ASYNC=1): direct-load small kernel only
@@ -165,6 +166,8 @@ enum Slot {
   WS_CD_IDX,        // list -> CSC counts / scans
   WS_CD_OUT,        // sweep scalars
   WS_CD_COEF,       // per-entry sweep constants
+  WS_CD_Z,          // Lambda sweep: Z = D Psi (q x q, row-major)
+  WS_CD_AUX,        // cooperative sweeps: list column pointers, per-entry changes, column buffer
   WS_NUM
 };
 

@@ -57,6 +57,15 @@ void theta_sigma(Ctx* c, int q, const cggm_csc* Th, const double* S, int64_t lds
 void theta_cd(Ctx* c, int p, int q, const double* S, int64_t lds, const double* Sxx, int64_t ldx, const double* Sxy,
               int64_t ldxy, const cggm_csc* Th, const int32_t* Tr, const int32_t* Tc, int64_t m, double lam, int passes,
               double* T, double* V, int64_t ldv, double* coef_ws /* 2m doubles */, double* out);
+bool coop_ok(Ctx* c);
+void lambda_cd_coop(Ctx* c, int q, const double* S, int64_t lds, const double* P, int64_t ldp, const double* G,
+                    int64_t ldg, const cggm_csc* Lam, const int32_t* Lr, const int32_t* Lc, int64_t m, double lam,
+                    int penalize_diag, int passes, double* D, double* U, double* Z, int64_t ldu, double* coef_ws,
+                    int* cnt, int64_t* scr, int64_t* lp, double* dmu, double* colbuf, double* out);
+void theta_cd_coop(Ctx* c, int p, int q, const double* S, int64_t lds, const double* Sxx, int64_t ldx,
+                   const double* Sxy, int64_t ldxy, const cggm_csc* Th, const int32_t* Tr, const int32_t* Tc, int64_t m,
+                   double lam, int passes, double* T, double* V, int64_t ldv, double* coef_ws, int* cnt, int64_t* scr,
+                   int64_t* lp, double* dmu, double* colbuf, double* out);
 // sorted list (column-major) -> CSC: mirror = symmetric Lambda + alpha D from the upper-triangle list
 // (values base_ij + alpha D[k]); otherwise the list itself with `vals`.  cnt_ws: 3n ints, scan_ws:
 // 2(n+1) int64.
