@@ -168,6 +168,7 @@ cggm_status cggm_ctx_create(cggm_ctx** out, int device, cggm_dtype dtype, void* 
   if (const char* e = std::getenv("CGGM_MID_TILE")) c->mid_tile = std::atoi(e);
   if (const char* e = std::getenv("CGGM_LEAF_SWEEP")) c->leaf_sweep = std::atoi(e);
   if (const char* e = std::getenv("CGGM_CD_COOP")) c->cd_coop = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_CD_PREFETCH")) c->cd_prefetch = std::atoi(e);
   if (const char* e = std::getenv("CGGM_GRAPH_PROF")) c->graph_prof = std::atoi(e);
   cudaDriverEntryPointQueryResult q;
   void* fn = nullptr;

@@ -555,6 +555,229 @@ __global__ void __launch_bounds__(CO_NT) k_theta_sweep_coop(int p, int q, const 
   }
 }
 
+// Lambda sweep, register/prefetch variant (q <= CO_QMAX): columns j of U and Z live in registers, the
+// Sigma and Psi columns of the NEXT entry are fetched by cp.async while the current update runs.
+constexpr int CO_LU = 12;
+constexpr int CO_QMAX = CO_NT * CO_LU;
+
+__global__ void __launch_bounds__(CO_NT) k_lambda_sweep_pf(int q, const double* __restrict__ S, int64_t lds,
+                                                           const double* __restrict__ P, int64_t ldp,
+                                                           const int32_t* Lr, const double4* coef, const int64_t* lp,
+                                                           int passes, double* D, double* dmu, double* U, double* Z,
+                                                           int64_t ldu) {
+  namespace cgx = cooperative_groups;
+  cgx::grid_group grid = cgx::this_grid();
+  extern __shared__ double co_sm[];
+  __shared__ double red[CO_NW];
+  const int64_t qs = (q + 1) & ~1;
+  double* sb[2] = {co_sm, co_sm + 2 * qs};   // [Sigma_i | Psi_i] per buffer
+  const int64_t gtid = blockIdx.x * (int64_t)CO_NT + threadIdx.x, gsz = (int64_t)gridDim.x * CO_NT;
+  const int x = threadIdx.x;
+  auto fetch = [&](int i, int b) {
+    const double* s1 = S + (int64_t)i * lds;
+    const double* p1 = P + (int64_t)i * ldp;
+    for (int c2 = x; 2 * c2 < q; c2 += CO_NT) {
+      const int r = 2 * c2;
+      const uint32_t by = (r + 1 < q) ? 16u : 8u;
+      ptx::cp_async16(sb[b] + r, s1 + r, by);
+      ptx::cp_async16(sb[b] + qs + r, p1 + r, by);
+    }
+    ptx::cp_async_commit();
+  };
+  for (int pass = 0; pass < passes; ++pass) {
+    for (int j = 0; j < q; ++j) {
+      const int64_t k0 = lp[j], k1 = lp[j + 1];
+      if (k0 == k1) continue;
+      if (blockIdx.x == 0) {
+        double ur[CO_LU], zr[CO_LU];
+#pragma unroll
+        for (int u = 0; u < CO_LU; ++u) {
+          const int t = x + u * CO_NT;
+          ur[u] = t < q ? U[(int64_t)t * ldu + j] : 0.0;
+          zr[u] = t < q ? Z[(int64_t)t * ldu + j] : 0.0;
+        }
+        const double Sjj = S[j + (int64_t)j * lds], Pjj = P[j + (int64_t)j * ldp];
+        int cur = 0;
+        fetch(Lr[k0], 0);
+        for (int64_t k = k0; k < k1; ++k) {
+          const int i = Lr[k];
+          const double4 cf = coef[k];
+          if (k + 1 < k1) {
+            fetch(Lr[k + 1], cur ^ 1);
+            ptx::cp_async_wait<1>();
+          } else {
+            ptx::cp_async_wait<0>();
+          }
+          __syncthreads();
+          const double* Si = sb[cur];
+          const double* Pi = sb[cur] + qs;
+          double v = 0.0;
+#pragma unroll
+          for (int u = 0; u < CO_LU; ++u) {
+            const int t = x + u * CO_NT;
+            if (t < q) v = fma(Si[t] + Pi[t], ur[u], fma(Si[t], zr[u], v));
+          }
+          const double b = cf.z + co_block_sum(v, red);
+          const double a = cf.x, c = cf.y + D[k];
+          const double mu = (a > 0.0) ? -c + soft(c - b / a, cf.w / a) : 0.0;
+          if (x == 0) {
+            D[k] = c - cf.y + mu;
+            dmu[k] = mu;
+          }
+          if (mu != 0.0) {
+            const double sij = Si[j], pij = Pi[j];   // Sigma_ji, Psi_ji from the staged column i
+            const int ui = i / CO_NT, uj = j / CO_NT;
+            const bool own_i = x == (i % CO_NT), own_j = (i != j) && x == (j % CO_NT);
+#pragma unroll
+            for (int u = 0; u < CO_LU; ++u) {
+              if (own_i && u == ui) {
+                ur[u] += mu * Sjj;
+                zr[u] += mu * Pjj;
+              }
+              if (own_j && u == uj) {
+                ur[u] += mu * sij;
+                zr[u] += mu * pij;
+              }
+            }
+          }
+          cur ^= 1;
+        }
+#pragma unroll
+        for (int u = 0; u < CO_LU; ++u) {
+          const int t = x + u * CO_NT;
+          if (t < q) {
+            U[(int64_t)t * ldu + j] = ur[u];
+            Z[(int64_t)t * ldu + j] = zr[u];
+          }
+        }
+      }
+      grid.sync();
+      {
+        const int64_t nk = k1 - k0, work = nk * (int64_t)q;
+        for (int64_t w = gtid; w < work; w += gsz) {
+          const int64_t k = k0 + w / q;
+          const int t = (int)(w - (k - k0) * q);
+          const int i = Lr[k];
+          const double mu = dmu[k];
+          if (t == j || i == j || mu == 0.0) continue;
+          U[(int64_t)i * ldu + t] += mu * S[t + (int64_t)j * lds];
+          Z[(int64_t)i * ldu + t] += mu * P[t + (int64_t)j * ldp];
+        }
+        for (int64_t t = gtid; t < q; t += gsz) {
+          if (t == j) continue;
+          double ua = 0.0, za = 0.0;
+          for (int64_t k = k0; k < k1; ++k) {
+            const double mu = dmu[k];
+            const int i = Lr[k];
+            ua = fma(mu, S[t + (int64_t)i * lds], ua);
+            za = fma(mu, P[t + (int64_t)i * ldp], za);
+          }
+          U[(int64_t)j * ldu + t] += ua;
+          Z[(int64_t)j * ldu + t] += za;
+        }
+      }
+      grid.sync();
+    }
+  }
+}
+
+// Theta sweep, register/prefetch variant (p <= CO_PMAX): column j of V lives in registers (thread
+// x owns rows x, x + 512, ...), and the S_xx column of the NEXT entry is fetched by cp.async into
+// the other half of a shared double buffer while the current dot product runs -- the sequential
+// walk no longer waits on DRAM for each update's length-p column.
+constexpr int CO_VU = 24;                 // register slots per thread: p <= 512 * 24
+constexpr int CO_PMAX = CO_NT * CO_VU;
+
+__global__ void __launch_bounds__(CO_NT) k_theta_sweep_pf(int p, int q, const double* __restrict__ S, int64_t lds,
+                                                          const double* __restrict__ Sxx, int64_t ldx,
+                                                          const int32_t* Tr, const double2* coef, const int64_t* lp,
+                                                          double lam, int passes, double* T, double* dmu, double* V,
+                                                          int64_t ldv) {
+  namespace cgx = cooperative_groups;
+  cgx::grid_group grid = cgx::this_grid();
+  extern __shared__ double co_sm[];
+  __shared__ double red[CO_NW];
+  const int64_t pst = (p + 1) & ~1;        // buffer stride (16-byte aligned halves)
+  double* buf[2] = {co_sm, co_sm + pst};
+  const int64_t gtid = blockIdx.x * (int64_t)CO_NT + threadIdx.x, gsz = (int64_t)gridDim.x * CO_NT;
+  const int x = threadIdx.x;
+  // S_xx column i -> shared buffer b, 16-byte cp.async chunks (ldx even, so columns are aligned)
+  auto fetch = [&](int i, int b) {
+    const double* src = Sxx + (int64_t)i * ldx;
+    for (int c2 = x; 2 * c2 < p; c2 += CO_NT) {
+      const int r = 2 * c2;
+      ptx::cp_async16(buf[b] + r, src + r, (r + 1 < p) ? 16u : 8u);
+    }
+    ptx::cp_async_commit();
+  };
+  for (int pass = 0; pass < passes; ++pass) {
+    for (int j = 0; j < q; ++j) {
+      const int64_t k0 = lp[j], k1 = lp[j + 1];
+      if (k0 == k1) continue;
+      if (blockIdx.x == 0) {
+        double vr[CO_VU];
+#pragma unroll
+        for (int u = 0; u < CO_VU; ++u) {
+          const int t = x + u * CO_NT;
+          vr[u] = t < p ? V[(int64_t)t * ldv + j] : 0.0;
+        }
+        const double Sjj = S[j + (int64_t)j * lds];
+        int cur = 0;
+        fetch(Tr[k0], 0);
+        for (int64_t k = k0; k < k1; ++k) {
+          const int i = Tr[k];
+          const double2 cf = coef[k];
+          if (k + 1 < k1) {
+            fetch(Tr[k + 1], cur ^ 1);
+            ptx::cp_async_wait<1>();    // the current column has landed (the next may be in flight)
+          } else {
+            ptx::cp_async_wait<0>();
+          }
+          __syncthreads();
+          const double* Xs = buf[cur];
+          double v = 0.0;
+#pragma unroll
+          for (int u = 0; u < CO_VU; ++u) {
+            const int t = x + u * CO_NT;
+            if (t < p) v = fma(Xs[t], vr[u], v);
+          }
+          const double b = cf.y + 2.0 * co_block_sum(v, red);   // (its barriers also retire buf[cur])
+          const double a = cf.x, c = T[k];
+          const double mu = (a > 0.0) ? -c + soft(c - b / a, lam / a) : 0.0;
+          if (x == 0) {
+            T[k] = c + mu;
+            dmu[k] = mu;
+          }
+          if (mu != 0.0 && x == (i % CO_NT)) {
+            const int ui = i / CO_NT;
+#pragma unroll
+            for (int u = 0; u < CO_VU; ++u)
+              if (u == ui) vr[u] += mu * Sjj;
+          }
+          cur ^= 1;
+        }
+#pragma unroll
+        for (int u = 0; u < CO_VU; ++u) {
+          const int t = x + u * CO_NT;
+          if (t < p) V[(int64_t)t * ldv + j] = vr[u];
+        }
+      }
+      grid.sync();
+      {
+        const int64_t nk = k1 - k0, work = nk * (int64_t)q;
+        for (int64_t w = gtid; w < work; w += gsz) {
+          const int64_t k = k0 + w / q;
+          const int t = (int)(w - (k - k0) * q);
+          const double mu = dmu[k];
+          if (t == j || mu == 0.0) continue;
+          V[(int64_t)Tr[k] * ldv + t] += mu * S[t + (int64_t)j * lds];
+        }
+      }
+      grid.sync();
+    }
+  }
+}
+
 // ---------------------------------------------------------------- sparse bookkeeping
 // count list entries per column (cl) and mirrored entries per column (cm: entry (i, j), i < j,
 // mirrors into column i)
@@ -721,6 +944,22 @@ void lambda_cd_coop(Ctx* c, int q, const double* S, int64_t lds, const double* P
     k_lambda_coefs<<<grid_for(m), 256, 0, c->stream>>>(m, S, lds, P, ldp, G, ldg, Lam->colptr, Lam->rowidx, lv, Lr, Lc,
                                                        lam, penalize_diag, coef);
     list_colptr(c, q, Lr, Lc, m, cnt, scr, lp);
+    const size_t smem_pf = (size_t)4 * ((q + 1) & ~1) * 8;
+    if (q >= 2048 && q <= CO_QMAX && smem_pf <= 200 * 1024 && lds % 2 == 0 && ldp % 2 == 0 && c->cd_prefetch) {
+      static bool attr_pf = false;
+      if (!attr_pf) {
+        CGGM_CUDA_CHECK(cudaFuncSetAttribute(k_lambda_sweep_pf, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr_pf = true;
+      }
+      int grid = c->num_sms;
+      void* args[] = {&q, &S, &lds, &P, &ldp, &Lr, &coef, &lp, &passes, &D, &dmu, &U, &Z, &ldu};
+      CGGM_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_lambda_sweep_pf, dim3(grid), dim3(CO_NT), args, smem_pf,
+                                                  c->stream));
+      c->launches += 2;
+      k_lambda_tail<<<1, CD_NT, 0, c->stream>>>(q, Lam->colptr, lv, Lr, Lc, coef, m, D, out);
+      post_launch(c, "k_lambda_sweep_pf");
+      return;
+    }
     const size_t smem = (size_t)2 * q * 8;
     const int use_smem = smem <= 200 * 1024 ? 1 : 0;
     static bool attr = false;
@@ -752,6 +991,22 @@ void theta_cd_coop(Ctx* c, int p, int q, const double* S, int64_t lds, const dou
     k_theta_coefs<<<grid_for(m), 256, 0, c->stream>>>(m, S, lds, Sxx, ldx, Sxy, ldxy, Th->colptr, Th->rowidx,
                                                       static_cast<const double*>(Th->val), Tr, Tc, coef, T);
     list_colptr(c, q, Tr, Tc, m, cnt, scr, lp);
+    int grid = c->num_sms;
+    const size_t smem_pf = (size_t)2 * ((p + 1) & ~1) * 8;
+    if (p >= 2048 && p <= CO_PMAX && smem_pf <= 200 * 1024 && ldx % 2 == 0 && c->cd_prefetch) {
+      static bool attr_pf = false;
+      if (!attr_pf) {
+        CGGM_CUDA_CHECK(cudaFuncSetAttribute(k_theta_sweep_pf, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr_pf = true;
+      }
+      void* args[] = {&p, &q, &S, &lds, &Sxx, &ldx, &Tr, &coef, &lp, &lam, &passes, &T, &dmu, &V, &ldv};
+      CGGM_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_theta_sweep_pf, dim3(grid), dim3(CO_NT), args, smem_pf,
+                                                  c->stream));
+      c->launches += 2;
+      k_theta_l1<<<1, CD_NT, 0, c->stream>>>(T, m, out);
+      post_launch(c, "k_theta_sweep_pf");
+      return;
+    }
     const size_t smem = (size_t)p * 8;
     const int use_smem = smem <= 200 * 1024 ? 1 : 0;
     static bool attr = false;
@@ -759,7 +1014,6 @@ void theta_cd_coop(Ctx* c, int p, int q, const double* S, int64_t lds, const dou
       CGGM_CUDA_CHECK(cudaFuncSetAttribute(k_theta_sweep_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       attr = true;
     }
-    int grid = c->num_sms;
     void* args[] = {&p, &q, &S, &lds, &Sxx, &ldx, &Tr, &coef, &lp, &lam, &passes, &T, &dmu, &V, &ldv, &colbuf,
                     const_cast<int*>(&use_smem)};
     CGGM_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_theta_sweep_coop, dim3(grid), dim3(CO_NT), args,

@@ -80,6 +80,7 @@ struct Ctx {
   int force_tile = 0;
   int small_kmax = 1024;    // mid-size GEMMs (64-tile grid < #SMs) with K <= this use the 32x32 cp.async kernel (CGGM_SMALL_KMAX)
   int leaf_sweep = 0;       // CGGM_LEAF_SWEEP=1: full-inverse leaves by the panel/sweep kernel (A/B)
+  int cd_prefetch = 1;      // CGGM_CD_PREFETCH=0: cooperative Theta sweep without the register/prefetch variant
   int cd_coop = 1;          // CGGM_CD_COOP=0: single-CTA coordinate sweeps (no column batching)
   int mid_tile = 0;         // CGGM_MID_TILE=1: 128x64 tiles (2 CTAs/SM) for the large non-symmetric GEMMs
   int no_small_async = 0;

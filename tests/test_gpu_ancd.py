@@ -169,3 +169,32 @@ def test_algorithm1_small_tight_tolerance_matches_prox_grad(ctx):
     ref = A.prox_grad_fit(Xh, Yh, 0.1, 0.1)
     assert g.converged
     assert g.f == pytest.approx(ref["f"], rel=1e-7)
+
+
+@pytest.mark.parametrize("variant", [{"CGGM_CD_COOP": "0"}, {"CGGM_CD_PREFETCH": "0"}, {}])
+def test_sweep_variants_agree_medium(variant):
+    """The single-CTA sweeps, the column-batched cooperative sweeps and their register / prefetch
+    variants (taken at medium sizes) give the same direction and Theta to summation-order rounding."""
+    import os
+    from paper_1509_04681_b200 import Context
+    P = problem("medium")
+    for k_, v_ in variant.items():
+        os.environ[k_] = v_
+    try:
+        c = Context(0)
+    finally:
+        for k_ in variant:
+            os.environ.pop(k_, None)
+    s = _gpu_state(c, P, 0)
+    act = s["active"]
+    D, delta, _ = c.cggm_lambda_direction(s["Sigma"], s["Psi"], s["GradL"], s["Lg"], act["L_row"], act["L_col"],
+                                          P.lam_L, True, 1)
+    Sxx = c.cggm_gram(s["X"])
+    Tn, l1 = c.cggm_theta_cd(s["Sigma"], Sxx, s["Sxy"], s["Tg"], act["T_row"], act["T_col"], P.lam_T, 1)
+    key = "medium_sweeps"
+    if key not in _P:
+        _P[key] = (D.cpu().numpy(), Tn.val.cpu().numpy(), delta, l1)
+    D0, T0, d0, l0 = _P[key]
+    assert np.linalg.norm(D.cpu().numpy() - D0) <= 1e-10 * np.linalg.norm(D0)
+    assert np.linalg.norm(Tn.val.cpu().numpy() - T0) <= 1e-10 * np.linalg.norm(T0)
+    assert delta == pytest.approx(d0, rel=1e-9) and l1 == pytest.approx(l0, rel=1e-10)
