@@ -10,6 +10,13 @@ unsharded quantity: S_yy = sum_r Y_r^T Y_r / n, Psi = sum_r R_r^T R_r, grad_Thet
 The evaluator is written against a small backend interface so that the same host logic runs
 with the CUDA backend (`CudaBackend`, libcggm via the binding; NCCL process group) and, in the
 CPU tests only, with a test backend over the gloo process group.
+
+Split factorisations (world >= 2, the default): the line-search objective needs a Cholesky of its
+own (a trial Lambda), independent of the inverse's.  Rank 1 keeps a full copy of X and Y
+(gathered once in setup(); the data do not change across evaluations) and evaluates the
+objective on all n rows while rank 0 computes Sigma = Lambda^{-1} -- the two O(q^3) chains run on
+different GPUs instead of one after the other (with split_objective=False every rank factors the
+trial Lambda for its partial traces, as in a plain data-parallel reading).
 """
 from __future__ import annotations
 
@@ -53,6 +60,10 @@ class CudaBackend:
         from .api import colmajor_empty
         return colmajor_empty(q, q, device=like.device)
 
+    def empty_matrix(self, rows, cols, like):
+        from .api import colmajor_empty
+        return colmajor_empty(rows, cols, device=like.device, dtype=like.dtype)
+
     def psi_grad_partial(self, X, Y, Theta, Sigma, n_total):
         r = self.ctx.cggm_psi_grad(X, Y, Theta, Sigma, n_total=n_total, want_gradL=False)
         return r["Psi"], r["GradT"]
@@ -70,12 +81,15 @@ class CudaBackend:
 class ShardedEvaluator:
     """One Newton-iteration evaluation with the rows of X, Y split over the process group."""
 
-    def __init__(self, backend, group=None, replicate_inverse: bool = False):
+    def __init__(self, backend, group=None, replicate_inverse: bool = False, split_objective: bool = True):
         self.b = backend
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.replicate_inverse = replicate_inverse
+        self.split = split_objective and self.world > 1 and not replicate_inverse
+        self.obj_rank = 1 if self.split else None
+        self.X_full = self.Y_full = None
 
     def _allreduce(self, t):
         if self.world > 1:
@@ -83,10 +97,48 @@ class ShardedEvaluator:
         return t
 
     def setup(self, X_r, Y_r, n_total):
-        """Per-dataset S_yy (excluded from the evaluation's timing)."""
+        """Per-dataset S_yy (excluded from the evaluation's timing); with split factorisations the
+        objective rank also assembles the full X, Y from the row blocks (point-to-point)."""
         self.n_total = n_total
         self.Syy = self._allreduce(self.b.covariances_partial(X_r, Y_r, n_total))
+        if self.split:
+            self._gather_full(X_r, Y_r)
         return self.Syy
+
+    def _gather_full(self, X_r, Y_r):
+        n = self.n_total
+        p, q = X_r.shape[1], Y_r.shape[1]
+        if self.rank == self.obj_rank:
+            self.X_full = self.b.empty_matrix(n, p, X_r)
+            self.Y_full = self.b.empty_matrix(n, q, Y_r)
+            for r in range(self.world):
+                a, b = shard_rows(n, self.world, r)
+                for full, local in ((self.X_full, X_r), (self.Y_full, Y_r)):
+                    if r == self.rank:
+                        full[a:b].copy_(local)
+                    else:
+                        buf = torch.empty((b - a) * full.shape[1], dtype=full.dtype, device=full.device)
+                        dist.recv(buf, src=r, group=self.group)
+                        full[a:b].copy_(buf.view(full.shape[1], b - a).t())
+        else:
+            for local in (X_r, Y_r):
+                dist.send(local.t().contiguous().view(-1), dst=self.obj_rank, group=self.group)
+
+    _OB_KEYS = ("f", "g", "logdet", "tr_syy_lam", "tr_sxy_theta", "tr_sigma_m", "pen_L", "pen_T", "is_pd", "fail_col")
+
+    def _objective_split(self, Lam, Theta, lam_L, lam_T, penalize_diag, like):
+        """The objective on all rows at the objective rank (concurrently with rank 0's inverse),
+        its scalars broadcast to every rank."""
+        vals = torch.zeros(len(self._OB_KEYS), dtype=torch.float64, device=like.device)
+        if self.rank == self.obj_rank:
+            ob = self.b.objective_partial(self.X_full, self.Y_full, Lam, Theta, lam_L, lam_T, penalize_diag,
+                                          self.n_total)
+            vals = torch.tensor([float(ob[k]) for k in self._OB_KEYS], dtype=torch.float64, device=like.device)
+        dist.broadcast(vals, src=self.obj_rank, group=self.group)
+        ob = {k: float(v) for k, v in zip(self._OB_KEYS, vals.tolist())}
+        ob["is_pd"] = ob["is_pd"] > 0.5
+        ob["fail_col"] = int(ob["fail_col"])
+        return ob
 
     def evaluate(self, X_r, Y_r, Lam, Theta, lam_L, lam_T, penalize_diag=True, tie_eps=1e-9):
         n = self.n_total
@@ -96,6 +148,8 @@ class ShardedEvaluator:
             Sigma, logdet, pd, fc = self.b.invert_logdet(Lam)
         else:
             Sigma, logdet, pd, fc = self.b.empty_sigma(q, Y_r), None, None, None
+        if self.split:
+            self._ob_split = self._objective_split(Lam, Theta, lam_L, lam_T, penalize_diag, Sigma)
         if self.world > 1 and not self.replicate_inverse:
             dist.broadcast(flat(Sigma), src=0, group=self.group)
             meta = torch.tensor([logdet if logdet is not None else 0.0, float(bool(pd)), float(fc or 0)],
@@ -107,11 +161,16 @@ class ShardedEvaluator:
         self._allreduce(GradT)
         GradL = self.b.grad_lambda(self.Syy, Sigma, Psi)
         act = self.b.active_set(GradL, GradT, Lam, Theta, lam_L, lam_T, penalize_diag, tie_eps)
-        ob = self.b.objective_partial(X_r, Y_r, Lam, Theta, lam_L, lam_T, penalize_diag, n)
-        parts = torch.tensor([ob["tr_syy_lam"], ob["tr_sxy_theta"], ob["tr_sigma_m"]], dtype=torch.float64,
-                             device=Psi.device)
-        if self.world > 1:
-            dist.all_reduce(parts, group=self.group)
+        if self.split:
+            # the objective rank evaluated the whole objective on all rows (see _objective_split)
+            ob = self._ob_split
+            parts = torch.tensor([ob["tr_syy_lam"], ob["tr_sxy_theta"], ob["tr_sigma_m"]], dtype=torch.float64)
+        else:
+            ob = self.b.objective_partial(X_r, Y_r, Lam, Theta, lam_L, lam_T, penalize_diag, n)
+            parts = torch.tensor([ob["tr_syy_lam"], ob["tr_sxy_theta"], ob["tr_sigma_m"]], dtype=torch.float64,
+                                 device=Psi.device)
+            if self.world > 1:
+                dist.all_reduce(parts, group=self.group)
         tr_syy, tr_sxy, tr_sm = (float(v) for v in parts.tolist())
         if ob["is_pd"]:
             g = -ob["logdet"] + tr_syy + 2.0 * tr_sxy + tr_sm

@@ -33,6 +33,9 @@ class OracleBackend:
     def empty_sigma(self, q, like):
         return col(np.zeros((q, q)))
 
+    def empty_matrix(self, rows, cols, like):
+        return col(np.zeros((rows, cols)))
+
     def psi_grad_partial(self, X, Y, Theta, Sigma, n_total):
         Xn, Yn, S = X.numpy(), Y.numpy(), Sigma.numpy()
         W = O.spmm_x_theta(Xn, Theta)
@@ -50,7 +53,7 @@ class OracleBackend:
         return O.objective(X.numpy(), Y.numpy(), Lam, Theta, lam_L, lam_T, penalize_diag, n_total=n_total)
 
 
-def _worker(rank, world, port, name, k, q_out):
+def _worker(rank, world, port, name, k, q_out, split=True):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -60,7 +63,7 @@ def _worker(rank, world, port, name, k, q_out):
         _, lam, th = P.points[k]
         a, b = shard_rows(P.n, world, rank)
         X, Y = col(P.X[a:b]), col(P.Y[a:b])
-        ev = ShardedEvaluator(OracleBackend())
+        ev = ShardedEvaluator(OracleBackend(), split_objective=split)
         ev.setup(X, Y, P.n)
         r = ev.evaluate(X, Y, lam, th, P.lam_L, P.lam_T, True)
         if rank == 0:
@@ -79,13 +82,15 @@ def free_port():
     return p
 
 
-@pytest.mark.parametrize("name,k", [("tiny", 1), ("small", 1)])
-def test_sharded_matches_unsharded_oracle(name, k):
+@pytest.mark.parametrize("name,k,world,split", [("tiny", 1, 2, True), ("small", 1, 2, True), ("tiny", 1, 2, False),
+                                                ("tiny", 1, 3, True)])
+def test_sharded_matches_unsharded_oracle(name, k, world, split):
+    """split: rank 1 evaluates the objective on the gathered full data while rank 0 inverts;
+    otherwise every rank contributes partial traces of its own rows."""
     ctx = mp.get_context("spawn")
     qo = ctx.Queue()
-    world = 2
     port = free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, name, k, qo)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, k, qo, split)) for r in range(world)]
     for p in procs:
         p.start()
     res = qo.get(timeout=300)
