@@ -225,9 +225,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # (CGGM_BENCH_DEVICE / CGGM_BENCH_BACKEND: functional smoke test of the multi-rank path on a
+    # one-GPU box -- every rank on one device over gloo; such a run's numbers are not measurements)
+    local = int(os.environ.get("CGGM_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("CGGM_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     from paper_1509_04681_b200 import Context, DeviceCsc, colmajor_empty
     from paper_1509_04681_b200.sharded import CudaBackend, ShardedEvaluator, shard_rows

@@ -108,6 +108,8 @@ class ShardedEvaluator:
     def _gather_full(self, X_r, Y_r):
         n = self.n_total
         p, q = X_r.shape[1], Y_r.shape[1]
+        # gloo's point-to-point needs host memory (the CPU tests, or a gloo smoke run on a GPU)
+        host = dist.get_backend(self.group) == "gloo"
         if self.rank == self.obj_rank:
             self.X_full = self.b.empty_matrix(n, p, X_r)
             self.Y_full = self.b.empty_matrix(n, q, Y_r)
@@ -117,12 +119,14 @@ class ShardedEvaluator:
                     if r == self.rank:
                         full[a:b].copy_(local)
                     else:
-                        buf = torch.empty((b - a) * full.shape[1], dtype=full.dtype, device=full.device)
+                        buf = torch.empty((b - a) * full.shape[1], dtype=full.dtype,
+                                          device="cpu" if host else full.device)
                         dist.recv(buf, src=r, group=self.group)
                         full[a:b].copy_(buf.view(full.shape[1], b - a).t())
         else:
             for local in (X_r, Y_r):
-                dist.send(local.t().contiguous().view(-1), dst=self.obj_rank, group=self.group)
+                buf = local.t().contiguous().view(-1)
+                dist.send(buf.cpu() if host else buf, dst=self.obj_rank, group=self.group)
 
     _OB_KEYS = ("f", "g", "logdet", "tr_syy_lam", "tr_sxy_theta", "tr_sigma_m", "pen_L", "pen_T", "is_pd", "fail_col")
 
