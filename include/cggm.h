@@ -117,8 +117,15 @@ cggm_status cggm_ctx_set_validate(cggm_ctx* ctx, int level);
  *     256; 0 = everything on one stream, each kernel's duration its own);
  *   CGGM_OPT_GRAPHS: 1 = cggm_newton_eval captures its launches into a CUDA graph on the second
  *     call with the same arguments and replays it afterwards (default), 0 = plain stream launches.
+ *   CGGM_OPT_FACTOR_REUSE: 1 = cggm_newton_eval runs the objective's trial factorisation in
+ *     full-inverse mode and keeps L_trial^{-1}; the NEXT cggm_newton_eval on this ctx takes
+ *     Sigma = L^{-T} L^{-1} from it (one symmetric product, no factorisation) and the log-det / PD
+ *     flag from the kept trial -- the secondary "factor-reuse" evaluation of SURVEY.md §8(d),
+ *     (4/3) q^3 -> q^3 flop.  The CALLER guarantees that the next Lambda equals the previous call's
+ *     Lambda (the accepted line-search trial); q must match, else the call falls back to a full
+ *     inverse.  Setting the option (either value) forgets the kept factor.
  * Unknown option -> CGGM_ERR_INVALID_ARG. */
-typedef enum cggm_option { CGGM_OPT_LOOKAHEAD_MIN = 0, CGGM_OPT_GRAPHS = 1 } cggm_option;
+typedef enum cggm_option { CGGM_OPT_LOOKAHEAD_MIN = 0, CGGM_OPT_GRAPHS = 1, CGGM_OPT_FACTOR_REUSE = 2 } cggm_option;
 cggm_status cggm_ctx_set_option(cggm_ctx* ctx, int option, int64_t value);
 /* Number of library kernels launched on this ctx so far (for launch accounting). */
 cggm_status cggm_ctx_launch_count(cggm_ctx* ctx, int64_t* count);

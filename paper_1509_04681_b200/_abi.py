@@ -26,6 +26,7 @@ CGGM_F64 = 0
 CGGM_F32 = 1
 CGGM_OPT_LOOKAHEAD_MIN = 0
 CGGM_OPT_GRAPHS = 1
+CGGM_OPT_FACTOR_REUSE = 2
 PROF_NTAGS = 14
 
 

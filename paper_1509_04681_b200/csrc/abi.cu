@@ -243,6 +243,11 @@ cggm_status cggm_ctx_set_option(cggm_ctx* ctx, int option, int64_t value) {
       if (value != 0 && value != 1) return CGGM_ERR_INVALID_ARG;
       c->use_graphs = (int)value;
       return CGGM_OK;
+    case CGGM_OPT_FACTOR_REUSE:
+      if (value != 0 && value != 1) return CGGM_ERR_INVALID_ARG;
+      c->factor_reuse = (int)value;
+      c->reuse_valid = 0;
+      return CGGM_OK;
     default:
       return CGGM_ERR_INVALID_ARG;
   }
@@ -553,7 +558,8 @@ static int64_t n_leaves(int64_t q) { return (q + leaf_nb() - 1) / leaf_nb(); }
 // ------------------------------------------------------------------ a3
 // Scal layout: dbl[0] = logdet sum, dbl[8..] leaf slots
 template <typename T>
-static void invert_enqueue(Ctx* c, int lane, const cggm_csc* Lambda, T* Sigma, int64_t ldsigma) {
+static void invert_enqueue(Ctx* c, int lane, const cggm_csc* Lambda, T* Sigma, int64_t ldsigma,
+                           int xslot = WS_LINV) {
   const int64_t q = Lambda->nrows;
   const int64_t lda = pad_ld<T>(q);
   const int nb = leaf_nb();
@@ -565,7 +571,7 @@ static void invert_enqueue(Ctx* c, int lane, const cggm_csc* Lambda, T* Sigma, i
   densify_csc(c, Lambda, Av);
   init_scalars(c, s.fail, s.flag);
   if (Sigma) {
-    T* X = static_cast<T*>(ws_get(c, WS_LINV, (size_t)lda * q * sizeof(T)));
+    T* X = static_cast<T*>(ws_get(c, xslot, (size_t)lda * q * sizeof(T)));
     CGGM_CUDA_CHECK(cudaMemsetAsync(X, 0, (size_t)lda * q * sizeof(T), c->stream));
     const size_t tmp_elems = chol_tmp_elems(q);
     T* tmp = static_cast<T*>(ws_get(c, WS_TMP, tmp_elems * sizeof(T)));
@@ -576,6 +582,19 @@ static void invert_enqueue(Ctx* c, int lane, const cggm_csc* Lambda, T* Sigma, i
     potrf_recursive<T>(c, Av, ViewT<T>{nullptr, lda, q, q}, false, leafinv, slots, s.fail, nullptr, 0);
   }
   sum_arrays_1(c, slots, nleaves, s.dbl);
+}
+
+// factor reuse: Sigma from the kept L^{-1} (one symmetric product), the kept trial's (fail_col,
+// log-det) into this lane's scalar block
+template <typename T>
+static void invert_from_kept(Ctx* c, int lane, int64_t q, T* Sigma, int64_t ldsigma, int xslot) {
+  const int64_t lda = pad_ld<T>(q);
+  T* X = static_cast<T*>(ws_get(c, xslot, (size_t)lda * q * sizeof(T)));
+  Scal s = scal_lane(c, lane, 8 + n_leaves(q));
+  const char* kept = static_cast<const char*>(ws_get(c, WS_REUSE_SCAL, 64 + 8));
+  CGGM_CUDA_CHECK(cudaMemcpyAsync(s.fail, kept, 4, cudaMemcpyDeviceToDevice, c->stream));
+  CGGM_CUDA_CHECK(cudaMemcpyAsync(s.dbl, kept + 64, 8, cudaMemcpyDeviceToDevice, c->stream));
+  lauum<T>(c, ViewT<T>{X, lda, q, q}, ViewT<T>{Sigma, ldsigma, q, q});
 }
 
 // D2H of (fail_col, logdet) from a lane's scalar block; caller synchronises
@@ -878,6 +897,52 @@ static void objective_enqueue(Ctx* c, int lane, int64_t n_local, int64_t q, cons
   sum_arrays_1(c, penTp, q, res + 5);
 }
 
+// factor reuse: the objective with its trial factorisation in full-inverse mode, keeping
+// X = L^{-1} in `xslot`; tr(Sigma M) = ||W X^T||^2 / n by one triangular GEMM.  Same scalar block
+// layout as objective_enqueue.
+template <typename T>
+static void objective_fullinv_enqueue(Ctx* c, int lane, int64_t n_local, int64_t q, const T* Yd, int64_t ldy,
+                                      const T* Wd, int64_t ldwd, const cggm_csc* Lambda, const cggm_csc* Theta,
+                                      int32_t penalize_diag, int xslot) {
+  const int64_t nleaves = n_leaves(q);
+  const int64_t lda = pad_ld<T>(q);
+  T* A = static_cast<T*>(ws_get(c, kLane[lane].dense, (size_t)lda * q * sizeof(T)));
+  T* X = static_cast<T*>(ws_get(c, xslot, (size_t)lda * q * sizeof(T)));
+  const size_t tmp_elems = chol_tmp_elems(q);
+  T* tmp = static_cast<T*>(ws_get(c, WS_TMP2, tmp_elems * sizeof(T)));
+  const int64_t ldz = pad_ld<T>(n_local);
+  T* Z = static_cast<T*>(ws_get(c, WS_Z, (size_t)ldz * q * sizeof(T)));
+  Scal s = scal_lane(c, lane, 16 + 5 * q + nleaves);
+  double* res = s.dbl;
+  double* partY = s.dbl + 16;
+  double* partWY = partY + q;
+  double* partZ = partWY + q;
+  double* penLp = partZ + q;
+  double* penTp = penLp + q;
+  double* slots = penTp + q;
+  CGGM_CUDA_CHECK(cudaMemsetAsync(X, 0, (size_t)lda * q * sizeof(T), c->stream));
+  densify_csc(c, Lambda, ViewT<T>{A, lda, q, q});
+  init_scalars(c, s.fail, s.flag);
+  potrf_recursive<T>(c, ViewT<T>{A, lda, q, q}, ViewT<T>{X, lda, q, q}, true, nullptr, slots, s.fail, tmp, tmp_elems);
+  {  // Z = W X^T (X lower triangular: op(B)[k][j] = X[j][k] vanishes for k > j)
+    Phase ph(c, TAG_TRSM);
+    EpilogueT<T> e; e.out1 = Z; e.ld1 = ldz;
+    gemm(c, false, true, n_local, q, q, Wd, ldwd, X, lda, e, B_KLE_N);
+  }
+  Phase ph(c, TAG_OBJRED);
+  col_partials<T>(c, 0, n_local, q, Yd, ldy, nullptr, 0, Lambda, partY);
+  col_partials<T>(c, 1, n_local, q, Wd, ldwd, Yd, ldy, nullptr, partWY);
+  col_partials<T>(c, 2, n_local, q, Z, ldz, nullptr, 0, nullptr, partZ);
+  csc_abs_partials<T>(c, Lambda, penalize_diag == 0, penLp);
+  csc_abs_partials<T>(c, Theta, false, penTp);
+  sum_arrays_1(c, slots, nleaves, res + 0);
+  sum_arrays_1(c, partY, q, res + 1);
+  sum_arrays_1(c, partWY, q, res + 2);
+  sum_arrays_1(c, partZ, q, res + 3);
+  sum_arrays_1(c, penLp, q, res + 4);
+  sum_arrays_1(c, penTp, q, res + 5);
+}
+
 static void objective_readback_async(Ctx* c, int lane, char* h) {
   Scal s = scal_lane(c, lane, 0);
   CGGM_CUDA_CHECK(cudaMemcpyAsync(h, s.fail, 4, cudaMemcpyDeviceToHost, c->stream));
@@ -1018,7 +1083,17 @@ cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, con
       ws_get(c, WS_E, (size_t)ldn * q * es);
       if (!GradT) ws_get(c, WS_GTCHUNK, (size_t)pad_ld<T>(p) * std::min<int64_t>(GT_CHUNK, q) * es);
       ws_get(c, WS_W, (size_t)ldn * q * es);
+      if (c->factor_reuse) {
+        ws_get(c, WS_LINV2, (size_t)pad_ld<T>(q) * q * es);
+        ws_get(c, WS_TMP2, chol_tmp_elems(q) * es);
+        ws_get(c, WS_Z, (size_t)ldn * q * es);
+        ws_get(c, WS_REUSE_SCAL, 64 + 8);
+      }
     });
+    // factor reuse: Sigma from the kept trial inverse of the previous call (buffer xs_prev); this
+    // call's trial inverse goes to the other buffer
+    const bool reuse_now = c->factor_reuse && c->reuse_valid && c->reuse_q == q;
+    const int xs_prev = c->reuse_buf ? WS_LINV2 : WS_LINV, xs_next = c->reuse_buf ? WS_LINV : WS_LINV2;
     ActTotals* tot = nullptr;
     char* h = static_cast<char*>(c->host_scratch);
     // the whole evaluation, enqueue only: fork onto the chain / objective streams, join back into
@@ -1046,7 +1121,10 @@ cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, con
           // a7 on the auxiliary stream (lane 1)
           c->stream = c->aux;
           c->lane = 1;
-          objective_enqueue<T>(c, 1, n, q, Yd, ldy, W, ldn, Lambda, Theta, active->penalize_diag);
+          if (c->factor_reuse)
+            objective_fullinv_enqueue<T>(c, 1, n, q, Yd, ldy, W, ldn, Lambda, Theta, active->penalize_diag, xs_next);
+          else
+            objective_enqueue<T>(c, 1, n, q, Yd, ldy, W, ldn, Lambda, Theta, active->penalize_diag);
           CGGM_CUDA_CHECK(cudaEventRecord(c->ev_join, c->aux));
           c->stream = s0;
           c->lane = 0;
@@ -1056,7 +1134,10 @@ cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, con
           throw;
         }
         // a3, a4/a5, a6 on the chain stream (lane 0)
-        invert_enqueue<T>(c, 0, Lambda, static_cast<T*>(Sigma), ldsigma);
+        if (reuse_now)
+          invert_from_kept<T>(c, 0, q, static_cast<T*>(Sigma), ldsigma, xs_prev);
+        else
+          invert_enqueue<T>(c, 0, Lambda, static_cast<T*>(Sigma), ldsigma, c->factor_reuse ? xs_prev : (int)WS_LINV);
         Fuse fz{Lambda, Theta, active, active_ws(c, q)};
         psi_enqueue<T>(c, n, n, p, q, Xd, ldx, Yd, ldy, W, ldn, static_cast<const T*>(Sigma), ldsigma,
                        static_cast<const T*>(Syy), ldsyy, nullptr, 0, static_cast<T*>(Psi), ldpsi,
@@ -1069,6 +1150,12 @@ cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, con
         CGGM_CUDA_CHECK(cudaStreamWaitEvent(so, c->ev_join_hi, 0));
       }
       CGGM_CUDA_CHECK(cudaStreamWaitEvent(so, c->ev_join, 0));
+      if (c->factor_reuse) {   // keep the trial's (fail_col, log-det) with its inverse
+        Scal s1 = scal_lane(c, 1, 0);
+        char* kept = static_cast<char*>(ws_get(c, WS_REUSE_SCAL, 64 + 8));
+        CGGM_CUDA_CHECK(cudaMemcpyAsync(kept, s1.fail, 4, cudaMemcpyDeviceToDevice, so));
+        CGGM_CUDA_CHECK(cudaMemcpyAsync(kept + 64, s1.dbl, 8, cudaMemcpyDeviceToDevice, so));
+      }
       chol_readback_async(c, 0, h);
       objective_readback_async(c, 1, h + 64);
       CGGM_CUDA_CHECK(cudaMemcpyAsync(h + 256, tot, sizeof(ActTotals), cudaMemcpyDeviceToHost, so));
@@ -1094,7 +1181,7 @@ cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, con
       key.insert(key.end(), {lb, tb, eb, a->penalize_diag, a->cap_L, a->cap_T, (int64_t)a->L_row, (int64_t)a->L_col,
                              (int64_t)a->T_row, (int64_t)a->T_col});
     }
-    const bool graphs = c->use_graphs && (!c->prof || c->graph_prof);
+    const bool graphs = c->use_graphs && !c->factor_reuse && (!c->prof || c->graph_prof);
     key.push_back(c->prof ? 1 : 0);
     if (graphs && !c->gorigin) {
       // capture origin: an internal stream (the caller's may be the legacy default stream, which
@@ -1156,6 +1243,11 @@ cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, con
       c->graph_key_seen = key;
     }
     CGGM_CUDA_CHECK(cudaStreamSynchronize(s_caller));
+    if (c->factor_reuse) {
+      c->reuse_buf ^= 1;   // this call's trial inverse is the next call's Sigma source
+      c->reuse_valid = 1;
+      c->reuse_q = q;
+    }
     CholResult cr = chol_decode(h);
     out->logdet = cr.logdet;
     out->is_pd = cr.is_pd;

@@ -67,6 +67,13 @@ struct Ctx {
   int la_min = 256;              // defer only when the deferred block is at least this wide (CGGM_LA_MIN; 0 = off)
   int prio_mode = 1;             // composite: 1 = chain on `hi` (greatest priority), objective on `aux`
                                  // (least priority); 0 = chain on the caller's stream (CGGM_PRIO=0)
+  // factor reuse (CGGM_OPT_FACTOR_REUSE): the objective's trial factorisation runs in full-inverse
+  // mode and keeps L^{-1} (buffer reuse_buf ^ 1 of {WS_LINV, WS_LINV2}); the next evaluation's
+  // Sigma is lauum of it.  The caller guarantees the next Lambda is that trial Lambda.
+  int factor_reuse = 0;
+  int reuse_valid = 0;
+  int reuse_buf = 0;
+  int64_t reuse_q = -1;
   // CUDA graph of the composite evaluation (cggm_newton_eval), keyed by its full argument set
   int use_graphs = 1;            // CGGM_GRAPH=0 disables
   int graph_prof = 0;            // CGGM_GRAPH_PROF=1: capture the profiling events too (timelines)
@@ -168,6 +175,9 @@ enum Slot {
   WS_CD_OUT,        // sweep scalars
   WS_CD_COEF,       // per-entry sweep constants
   WS_CD_Z,          // Lambda sweep: Z = D Psi (q x q, row-major)
+  WS_LINV2,         // factor reuse: the second L^{-1} buffer (the objective's, kept for the next call)
+  WS_TMP2,          // factor reuse: the objective lane's full-inverse recursion temporaries
+  WS_REUSE_SCAL,    // factor reuse: the kept factor's (fail_col, log-det) scalars
   WS_CD_AUX,        // cooperative sweeps: list column pointers, per-entry changes, column buffer
   WS_NUM
 };

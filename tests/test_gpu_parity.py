@@ -348,3 +348,37 @@ def test_active_vector_kernel_matches_scalar(ctx, name, k):
         assert torch.equal(a[key], b[key]), key
     assert a["subgrad_l1"] == pytest.approx(b["subgrad_l1"], rel=1e-13)
     assert a["subgrad_l1"] == pytest.approx(ref["sub"], rel=1e-9)
+
+
+@pytest.mark.parametrize("name,k", [("small", 1), ("medium", 0)])
+def test_factor_reuse_evaluation(ctx, name, k):
+    """CGGM_OPT_FACTOR_REUSE: the objective keeps its trial L^{-1} and the next evaluation's Sigma is
+    its symmetric product (no factorisation).  Same Lambda on consecutive calls: Sigma, Psi, the
+    gradients and the lists equal the plain evaluation's, log-det and the PD flag are the kept
+    trial's, the objective matches the oracle (its trace now by a triangular GEMM)."""
+    from paper_1509_04681_b200 import Context, DeviceCsc, _abi, to_device_colmajor
+    from paper_1509_04681_b200.api import newton_evaluation
+    P = problem(name)
+    label, lam, th = P.points[k]
+    X, Y = to_device_colmajor(P.X), to_device_colmajor(P.Y)
+    Lg, Tg = DeviceCsc.from_host(lam), DeviceCsc.from_host(th)
+    cap = 4_000_000
+
+    def bufs():
+        return {k2: torch.empty(cap, dtype=torch.int32, device="cuda") for k2 in ("L_row", "L_col", "T_row", "T_col")}
+
+    c2 = Context(0)
+    Syy, _ = c2.cggm_covariances(X, Y, want_sxy=False)
+    plain = newton_evaluation(c2, X, Y, Syy, Lg, Tg, P.lam_L, P.lam_T, True, bufs())
+    plain = {kk: (v.clone() if torch.is_tensor(v) else v) for kk, v in plain.items()}
+    c2.set_option(_abi.CGGM_OPT_FACTOR_REUSE, 1)
+    runs = [newton_evaluation(c2, X, Y, Syy, Lg, Tg, P.lam_L, P.lam_T, True, bufs()) for _ in range(3)]
+    c2.set_option(_abi.CGGM_OPT_FACTOR_REUSE, 0)
+    ref = oracle_point(name, k)
+    for r in runs:   # the first call factors, the next two reuse the kept trial inverse
+        for key in ("Sigma", "Psi", "GradL", "GradT"):
+            assert relf(to_np(r[key]), to_np(plain[key])) <= 1e-13, key
+        assert r["logdet"] == pytest.approx(plain["logdet"], rel=1e-13) and r["is_pd"] and r["fail_col"] == -1
+        assert r["objective"]["f"] == pytest.approx(ref["obj"]["f"], rel=REL_OBJ)
+        assert r["active"]["m_L"] == plain["active"]["m_L"] and r["active"]["m_T"] == plain["active"]["m_T"]
+        assert relf(to_np(r["Sigma"]), ref["Sigma"]) <= REL_F
