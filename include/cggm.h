@@ -267,6 +267,19 @@ cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q,
                              void* Sigma, int64_t ldsigma, void* Psi, int64_t ldpsi, void* GradL, int64_t ldgl,
                              void* GradT, int64_t ldgt, cggm_active_out* active, cggm_eval_out* out);
 
+/* One Newton-iteration evaluation from HOST buffers (the end-to-end form of cggm_newton_eval):
+ * X (n x p, ldx >= n) and Y (n x q, ldy >= n) column-major fp64 host arrays, Lambda and Theta CSCs
+ * whose colptr / rowidx / val point to HOST memory (page-locked memory makes the uploads
+ * asynchronous).  The library uploads into its workspace on an internal copy stream -- Lambda
+ * first, so the factorisation starts while X and Y are still in flight -- forms S_yy = Y^T Y / n
+ * into Syy (device, q x q, written), and evaluates exactly as cggm_newton_eval; the other
+ * outputs (device) and the host scalars are those of cggm_newton_eval.  fp64 ctx only. */
+cggm_status cggm_newton_eval_host(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, const double* X, int64_t ldx,
+                                  const double* Y, int64_t ldy, const cggm_csc* Lambda, const cggm_csc* Theta,
+                                  void* Syy, int64_t ldsyy, void* Sigma, int64_t ldsigma, void* Psi, int64_t ldpsi,
+                                  void* GradL, int64_t ldgl, void* GradT, int64_t ldgt, cggm_active_out* active,
+                                  cggm_eval_out* out);
+
 #ifdef __cplusplus
 }
 #endif

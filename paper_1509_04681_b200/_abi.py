@@ -81,6 +81,9 @@ SIGNATURES = {
                                  ctypes.POINTER(cggm_csc), ctypes.POINTER(cggm_csc), c_vp, c_i64, c_vp, c_i64,
                                  c_vp, c_i64, c_vp, c_i64, ctypes.POINTER(cggm_active_out),
                                  ctypes.POINTER(cggm_eval_out)]),
+    "cggm_newton_eval_host": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, ctypes.POINTER(cggm_csc),
+                                      ctypes.POINTER(cggm_csc), c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
+                                      c_vp, c_i64, ctypes.POINTER(cggm_active_out), ctypes.POINTER(cggm_eval_out)]),
     "cggm_test_gemm": (c_i32, [c_vp, c_i32, c_i32, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
                                c_d, c_d, c_i32]),
     "cggm_test_gemm_f32": (c_i32, [c_vp, c_i32, c_i32, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,

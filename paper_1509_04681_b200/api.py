@@ -15,7 +15,8 @@ import torch
 
 from . import _abi
 
-__all__ = ["Context", "DeviceCsc", "CggmError", "colmajor_empty", "to_device_colmajor", "ld_of"]
+__all__ = ["Context", "DeviceCsc", "HostCsc", "CggmError", "colmajor_empty", "to_device_colmajor", "ld_of",
+           "host_colmajor"]
 
 
 class CggmError(RuntimeError):
@@ -76,6 +77,40 @@ class DeviceCsc:
         return _abi.cggm_csc(self.nrows, self.ncols, self.nnz, self.colptr.data_ptr(),
                              self.rowidx.data_ptr() if self.nnz else None,
                              self.val.data_ptr() if self.nnz else None)
+
+
+@dataclasses.dataclass
+class HostCsc:
+    """A CSC in (page-locked) host memory, for cggm_newton_eval_host."""
+    nrows: int
+    ncols: int
+    colptr: torch.Tensor  # int64, CPU
+    rowidx: torch.Tensor  # int32, CPU
+    val: torch.Tensor     # float64, CPU
+
+    @classmethod
+    def from_host(cls, csc, pin=True) -> "HostCsc":
+        def t(a, dt):
+            x = torch.as_tensor(np.ascontiguousarray(a, dtype=dt))
+            return x.pin_memory() if pin else x
+        return cls(int(csc.nrows), int(csc.ncols), t(csc.colptr, np.int64), t(csc.rowidx, np.int32),
+                   t(csc.val, np.float64))
+
+    @property
+    def nnz(self) -> int:
+        return int(self.rowidx.numel())
+
+    def c_struct(self) -> _abi.cggm_csc:
+        return _abi.cggm_csc(self.nrows, self.ncols, self.nnz, self.colptr.data_ptr(),
+                             self.rowidx.data_ptr() if self.nnz else None, self.val.data_ptr() if self.nnz else None)
+
+
+def host_colmajor(a: np.ndarray, pin=True) -> torch.Tensor:
+    """(rows, cols) column-major fp64 host tensor (stride (1, rows)), page-locked by default."""
+    a = np.asarray(a, dtype=np.float64)
+    base = torch.empty((a.shape[1], a.shape[0]), dtype=torch.float64, pin_memory=pin)
+    base.copy_(torch.from_numpy(np.ascontiguousarray(a.T)))
+    return base.t()
 
 
 class Context:
@@ -380,6 +415,41 @@ class Context:
         return dict(Sigma=bufs["Sigma"], logdet=eo.logdet, is_pd=bool(eo.is_pd), fail_col=int(eo.fail_col),
                     Psi=bufs["Psi"], GradL=bufs["GradL"], GradT=bufs["GradT"], active=self._active_result(ao, spec),
                     objective=ob)
+
+
+
+
+    def cggm_newton_eval_host(self, Xh, Yh, Lam: HostCsc, Theta: HostCsc, lam_L, lam_T, penalize_diag=True,
+                              tie_eps=1e-9, bufs=None, Syy=None):
+        """cggm_newton_eval from host buffers (column-major CPU tensors, HostCsc): uploads overlap the
+        factorisation; S_yy is formed on the device into `Syy`.  Returns the cggm_newton_eval dict."""
+        self._sync_stream()
+        n, p = Xh.shape
+        q = Yh.shape[1]
+        bufs = bufs if bufs is not None else {}
+        for k, shape in (("Sigma", (q, q)), ("Psi", (q, q)), ("GradL", (q, q)), ("GradT", (p, q))):
+            if bufs.get(k) is None:
+                bufs[k] = colmajor_empty(*shape, device="cuda", dtype=self.tdtype)
+        if Syy is None:
+            Syy = colmajor_empty(q, q, device="cuda", dtype=self.tdtype)
+        spec = dict(lam_L=lam_L, lam_T=lam_T, penalize_diag=int(bool(penalize_diag)), tie_eps=tie_eps,
+                    L_row=bufs.get("L_row"), L_col=bufs.get("L_col"), T_row=bufs.get("T_row"), T_col=bufs.get("T_col"))
+        ao = self._active_struct(spec)
+        eo = _abi.cggm_eval_out()
+        ls, ts = Lam.c_struct(), Theta.c_struct()
+        st = self.lib.cggm_newton_eval_host(
+            self.h, n, p, q, _ptr(Xh), ld_of(Xh), _ptr(Yh), ld_of(Yh), ctypes.byref(ls), ctypes.byref(ts),
+            _ptr(Syy), ld_of(Syy), _ptr(bufs["Sigma"]), ld_of(bufs["Sigma"]), _ptr(bufs["Psi"]), ld_of(bufs["Psi"]),
+            _ptr(bufs["GradL"]), ld_of(bufs["GradL"]), _ptr(bufs["GradT"]), ld_of(bufs["GradT"]), ctypes.byref(ao),
+            ctypes.byref(eo))
+        self.last_active_sizes = (int(ao.m_L), int(ao.m_T))
+        self._check(st)
+        o = eo.obj
+        ob = dict(f=o.f, g=o.g, logdet=o.logdet, tr_syy_lam=o.tr_syy_lam, tr_sxy_theta=o.tr_sxy_theta,
+                  tr_sigma_m=o.tr_sigma_m, pen_L=o.pen_L, pen_T=o.pen_T, is_pd=bool(o.is_pd), fail_col=int(o.fail_col))
+        return dict(Sigma=bufs["Sigma"], logdet=eo.logdet, is_pd=bool(eo.is_pd), fail_col=int(eo.fail_col),
+                    Psi=bufs["Psi"], GradL=bufs["GradL"], GradT=bufs["GradT"], Syy=Syy,
+                    active=self._active_result(ao, spec), objective=ob)
 
 
 def newton_evaluation(ctx: Context, X, Y, Syy, Lam: DeviceCsc, Theta: DeviceCsc, lam_L, lam_T, penalize_diag=True,

@@ -207,6 +207,17 @@ cggm_status cggm_ctx_destroy(cggm_ctx* ctx) {
         cudaStreamDestroy(st);
       }
   for (auto e : c->la_events) cudaEventDestroy(e);
+  if (c->copy) {
+    cudaStreamSynchronize(c->copy);
+    cudaStreamDestroy(c->copy);
+    cudaStreamSynchronize(c->syys);
+    cudaStreamDestroy(c->syys);
+    cudaEventDestroy(c->ev_h_lam);
+    cudaEventDestroy(c->ev_h_xt);
+    cudaEventDestroy(c->ev_h_y);
+  }
+  if (c->ev_w) cudaEventDestroy(c->ev_w);
+  if (c->ev_syy) cudaEventDestroy(c->ev_syy);
   if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
   if (c->gorigin) {
     cudaStreamSynchronize(c->gorigin);
@@ -1022,240 +1033,334 @@ cggm_status cggm_objective(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int6
 // One Newton-iteration evaluation (the bench's unit): the objective's fresh trial Cholesky runs on
 // the auxiliary stream, overlapped with Sigma = Lambda^{-1} and the Psi / gradient / active-set
 // work on the caller's stream; one host synchronisation at the end.
+// Inputs uploaded from host memory by cggm_newton_eval_host: events after each upload
+struct HostIn {
+  cudaEvent_t ev_lam, ev_xt, ev_y;   // Lambda; X and Theta; Y (S_yy is formed from it here)
+};
+
+static void newton_eval_core(Ctx* c, int64_t n, int64_t p, int64_t q, const void* X, int64_t ldx, const void* Y,
+                             int64_t ldy, const void* Syy, int64_t ldsyy, const cggm_csc* Lambda, const cggm_csc* Theta,
+                             void* Sigma, int64_t ldsigma, void* Psi, int64_t ldpsi, void* GradL, int64_t ldgl,
+                             void* GradT, int64_t ldgt, cggm_active_out* active, cggm_eval_out* out,
+                             const HostIn* hin) {
+  if (!out) fail(CGGM_ERR_INVALID_ARG, "null cggm_eval_out");
+  if (n < 1 || p < 0 || q < 1) fail(CGGM_ERR_INVALID_ARG, "need n >= 1, q >= 1, p >= 0");
+  check_dense("X", X, n, p, ldx);
+  check_dense("Y", Y, n, q, ldy);
+  check_dense("Syy", Syy, q, q, ldsyy);
+  check_dense("Sigma", Sigma, q, q, ldsigma);
+  check_dense("Psi", Psi, q, q, ldpsi);
+  check_dense("GradL", GradL, q, q, ldgl);
+  check_dense("GradT", GradT, p, q, ldgt, false);
+  check_csc_host("Lambda", Lambda, q, q);
+  check_csc_host("Theta", Theta, p, q);
+  check_active_args(active);
+  std::memset(out, 0, sizeof(*out));
+  if (!hin) {
+    validate_csc_dev(c, Lambda, true, "Lambda");
+    validate_csc_dev(c, Theta, false, "Theta");
+  }
+  if (!c->aux) {
+    // the objective's trial factorisation is filler work: least priority, so its CTAs take the SMs
+    // the critical chain (a3 -> a4/a5 -> a6, greatest priority) leaves idle in its latency-bound
+    // recursion levels
+    int least = 0, greatest = 0;
+    CGGM_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, stream_priority(1)));
+    CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->hi, cudaStreamNonBlocking, stream_priority(0)));
+    CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_join_hi, cudaEventDisableTiming));
+    CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_w, cudaEventDisableTiming));
+    CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_syy, cudaEventDisableTiming));
+  }
+  cudaStream_t s_caller = c->stream;
+  struct Restore {
+    Ctx* c;
+    cudaStream_t s;
+    ~Restore() { c->stream = s; c->lane = 0; }
+  } restore{c, s_caller};
+  // allocate every workspace slot up front (allocation may synchronise the device; nothing in the
+  // enqueue below may, so that it can be captured into a CUDA graph)
+  dispatch(c, [&](auto tag) {
+    using T = decltype(tag);
+    const size_t es = sizeof(T);
+    const int64_t ldn = pad_ld<T>(n);
+    const int64_t nleaves = n_leaves(q);
+    ws_get(c, WS_DENSE_A, (size_t)pad_ld<T>(q) * q * es);
+    ws_get(c, WS_DENSE_B, (size_t)pad_ld<T>(q + n) * q * es);
+    ws_get(c, WS_LINV, (size_t)pad_ld<T>(q) * q * es);
+    ws_get(c, WS_TMP, chol_tmp_elems(q) * es);
+    ws_get(c, WS_LEAFINV, (size_t)nleaves * leaf_nb() * leaf_nb() * es);
+    ws_get(c, WS_XDIAG, (size_t)pad_ld<T>(q) * block_inverse_size() * es);
+    ws_get(c, WS_TMP_OBJ, ((size_t)(block_inverse_size() + 4) * (block_inverse_size() + 4) +
+                           (size_t)pad_ld<T>(q + n) * block_inverse_size()) * es);
+    ws_get(c, WS_SCAL, 64 + (8 + nleaves) * 8);
+    ws_get(c, WS_SCAL2, 64 + (16 + 5 * q + nleaves) * 8);
+    active_ws(c, q);
+    ws_get(c, WS_R, (size_t)ldn * q * es);
+    ws_get(c, WS_E, (size_t)ldn * q * es);
+    if (!GradT) ws_get(c, WS_GTCHUNK, (size_t)pad_ld<T>(p) * std::min<int64_t>(GT_CHUNK, q) * es);
+    ws_get(c, WS_W, (size_t)ldn * q * es);
+    if (c->factor_reuse) {
+      ws_get(c, WS_LINV2, (size_t)pad_ld<T>(q) * q * es);
+      ws_get(c, WS_TMP2, chol_tmp_elems(q) * es);
+      ws_get(c, WS_Z, (size_t)ldn * q * es);
+      ws_get(c, WS_REUSE_SCAL, 64 + 8);
+    }
+  });
+  // factor reuse: Sigma from the kept trial inverse of the previous call (buffer xs_prev); this
+  // call's trial inverse goes to the other buffer
+  const bool reuse_now = c->factor_reuse && c->reuse_valid && c->reuse_q == q;
+  const int xs_prev = c->reuse_buf ? WS_LINV2 : WS_LINV, xs_next = c->reuse_buf ? WS_LINV : WS_LINV2;
+  ActTotals* tot = nullptr;
+  char* h = static_cast<char*>(c->host_scratch);
+  // the whole evaluation, enqueue only: fork onto the chain / objective streams, join back into
+  // the caller's stream, D2H of the scalars into pinned host memory
+  auto enqueue = [&](cudaStream_t so) {
+    c->stream = so;
+    if (c->prio_mode) {
+      CGGM_CUDA_CHECK(cudaEventRecord(c->ev_fork, so));
+      CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->hi, c->ev_fork, 0));
+      c->stream = c->hi;
+    }
+    cudaStream_t s0 = c->stream;
+    dispatch(c, [&](auto tag) {
+      using T = decltype(tag);
+      const size_t es = sizeof(T);
+      const int64_t ldn = pad_ld<T>(n);
+      T* W = static_cast<T*>(ws_get(c, WS_W, (size_t)ldn * q * es));
+      const T* Xd = static_cast<const T*>(X);
+      const T* Yd = static_cast<const T*>(Y);
+      // fork; a2 (W = X Theta) and a7 on the auxiliary stream (lane 1), the chain a3 -> a4/a5 -> a6
+      // on s0 waits for W only when a4 needs it.  Host inputs (cggm_newton_eval_host): each step
+      // waits for the upload of what it reads, so the factorisation starts while X, Y stream in.
+      CGGM_CUDA_CHECK(cudaEventRecord(c->ev_fork, s0));
+      CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
+      try {
+        c->stream = c->aux;
+        c->lane = 1;
+        if (hin) CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->aux, hin->ev_xt, 0));
+        spmm_x_theta<T>(c, Xd, ldx, n, Theta, ViewT<T>{W, ldn, n, q});
+        CGGM_CUDA_CHECK(cudaEventRecord(c->ev_w, c->aux));
+        if (hin) {   // S_yy on its own stream, above the objective's priority: off the chain's critical path
+          CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->syys, hin->ev_y, 0));
+          c->stream = c->syys;
+          Phase ph(c, TAG_COV);
+          EpilogueT<T> e; e.out1 = static_cast<T*>(const_cast<void*>(Syy)); e.ld1 = ldsyy; e.a1 = 1.0 / (double)n;
+          gemm(c, true, false, q, q, n, Yd, ldy, Yd, ldy, e, SYM_LOWER | SYM_MIRROR);
+          CGGM_CUDA_CHECK(cudaEventRecord(c->ev_syy, c->syys));
+          c->stream = c->aux;
+        }
+        if (c->factor_reuse)
+          objective_fullinv_enqueue<T>(c, 1, n, q, Yd, ldy, W, ldn, Lambda, Theta, active->penalize_diag, xs_next);
+        else
+          objective_enqueue<T>(c, 1, n, q, Yd, ldy, W, ldn, Lambda, Theta, active->penalize_diag);
+        CGGM_CUDA_CHECK(cudaEventRecord(c->ev_join, c->aux));
+        c->stream = s0;
+        c->lane = 0;
+      } catch (...) {
+        c->stream = s0;
+        c->lane = 0;
+        throw;
+      }
+      // a3, a4/a5, a6 on the chain stream (lane 0)
+      if (hin) CGGM_CUDA_CHECK(cudaStreamWaitEvent(s0, hin->ev_lam, 0));
+      if (reuse_now)
+        invert_from_kept<T>(c, 0, q, static_cast<T*>(Sigma), ldsigma, xs_prev);
+      else
+        invert_enqueue<T>(c, 0, Lambda, static_cast<T*>(Sigma), ldsigma, c->factor_reuse ? xs_prev : (int)WS_LINV);
+      CGGM_CUDA_CHECK(cudaStreamWaitEvent(s0, c->ev_w, 0));
+      if (hin) CGGM_CUDA_CHECK(cudaStreamWaitEvent(s0, c->ev_syy, 0));
+      Fuse fz{Lambda, Theta, active, active_ws(c, q)};
+      psi_enqueue<T>(c, n, n, p, q, Xd, ldx, Yd, ldy, W, ldn, static_cast<const T*>(Sigma), ldsigma,
+                     static_cast<const T*>(Syy), ldsyy, nullptr, 0, static_cast<T*>(Psi), ldpsi,
+                     static_cast<T*>(GradL), ldgl, static_cast<T*>(GradT), ldgt, &fz);
+      tot = fz.ws.tot;
+    });
+    c->stream = so;
+    if (c->prio_mode) {
+      CGGM_CUDA_CHECK(cudaEventRecord(c->ev_join_hi, s0));
+      CGGM_CUDA_CHECK(cudaStreamWaitEvent(so, c->ev_join_hi, 0));
+    }
+    CGGM_CUDA_CHECK(cudaStreamWaitEvent(so, c->ev_join, 0));
+    if (c->factor_reuse) {   // keep the trial's (fail_col, log-det) with its inverse
+      Scal s1 = scal_lane(c, 1, 0);
+      char* kept = static_cast<char*>(ws_get(c, WS_REUSE_SCAL, 64 + 8));
+      CGGM_CUDA_CHECK(cudaMemcpyAsync(kept, s1.fail, 4, cudaMemcpyDeviceToDevice, so));
+      CGGM_CUDA_CHECK(cudaMemcpyAsync(kept + 64, s1.dbl, 8, cudaMemcpyDeviceToDevice, so));
+    }
+    chol_readback_async(c, 0, h);
+    objective_readback_async(c, 1, h + 64);
+    CGGM_CUDA_CHECK(cudaMemcpyAsync(h + 256, tot, sizeof(ActTotals), cudaMemcpyDeviceToHost, so));
+  };
+  // CUDA graph of the evaluation: the ~3000 launches of the two recursive factorisations would
+  // otherwise be throttled by the launch queue (the host blocks enqueueing the first one while the
+  // GPU works through it, so the second could not start alongside).  A new argument set runs
+  // eagerly once (allocating anything missing), the second call with the same arguments captures.
+  std::vector<int64_t> key = {n, p, q, ldx, ldy, ldsyy, ldsigma, ldpsi, ldgl, ldgt, (int64_t)c->ws_generation,
+                              (int64_t)c->dtype, c->prio_mode, c->la_min, (int64_t)s_caller};
+  for (const void* ptr : {X, Y, Syy, (const void*)Sigma, (const void*)Psi, (const void*)GradL, (const void*)GradT})
+    key.push_back((int64_t)ptr);
+  for (const cggm_csc* m : {Lambda, Theta}) {
+    key.insert(key.end(), {m->nrows, m->ncols, m->nnz, (int64_t)m->colptr, (int64_t)m->rowidx, (int64_t)m->val});
+  }
+  {
+    const cggm_active_out* a = active;
+    int64_t lb, tb;
+    std::memcpy(&lb, &a->lam_L, 8);
+    std::memcpy(&tb, &a->lam_T, 8);
+    int64_t eb;
+    std::memcpy(&eb, &a->tie_eps, 8);
+    key.insert(key.end(), {lb, tb, eb, a->penalize_diag, a->cap_L, a->cap_T, (int64_t)a->L_row, (int64_t)a->L_col,
+                           (int64_t)a->T_row, (int64_t)a->T_col});
+  }
+  const bool graphs = c->use_graphs && !c->factor_reuse && !hin && (!c->prof || c->graph_prof);
+  key.push_back(c->prof ? 1 : 0);
+  if (graphs && !c->gorigin) {
+    // capture origin: an internal stream (the caller's may be the legacy default stream, which
+    // cannot be captured); ordered after / before the caller's stream by events outside the graph
+    int least = 0, greatest = 0;
+    CGGM_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->gorigin, cudaStreamNonBlocking, greatest));
+    CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_gpre, cudaEventDisableTiming));
+    CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_gpost, cudaEventDisableTiming));
+  }
+  auto launch_graph = [&]() {
+    CGGM_CUDA_CHECK(cudaEventRecord(c->ev_gpre, s_caller));
+    CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->gorigin, c->ev_gpre, 0));
+    CGGM_CUDA_CHECK(cudaGraphLaunch(c->graph_exec, c->gorigin));
+    CGGM_CUDA_CHECK(cudaEventRecord(c->ev_gpost, c->gorigin));
+    CGGM_CUDA_CHECK(cudaStreamWaitEvent(s_caller, c->ev_gpost, 0));
+  };
+  if (graphs && c->graph_exec && key == c->graph_key) {
+    launch_graph();
+    c->launches += c->graph_launches;
+    tot = c->graph_tot;
+  } else if (graphs && key == c->graph_key_seen) {
+    if (c->graph_exec) {
+      cudaGraphExecDestroy(c->graph_exec);
+      c->graph_exec = nullptr;
+    }
+    const int64_t l0 = c->launches;
+    CGGM_CUDA_CHECK(cudaStreamBeginCapture(c->gorigin, cudaStreamCaptureModeRelaxed));
+    cudaGraph_t g = nullptr;
+    bool captured = true;
+    try {
+      enqueue(c->gorigin);
+    } catch (...) {
+      captured = false;
+    }
+    c->stream = s_caller;
+    c->lane = 0;
+    cudaError_t ce = cudaStreamEndCapture(c->gorigin, &g);
+    cudaError_t ie = cudaErrorUnknown;
+    // node priorities: the chain / objective / side streams' priorities carry into the graph
+    if (captured && ce == cudaSuccess && g)
+      ie = cudaGraphInstantiateWithFlags(&c->graph_exec, g, cudaGraphInstantiateFlagUseNodePriority);
+    if (g) cudaGraphDestroy(g);
+    if (ie != cudaSuccess) {
+      // something in the enqueue is not capturable here: run this and later calls eagerly
+      cudaGetLastError();
+      c->graph_exec = nullptr;
+      c->use_graphs = 0;
+      c->launches = l0;
+      enqueue(s_caller);
+    } else {
+      c->graph_launches = c->launches - l0;
+      c->graph_key = key;
+      c->graph_tot = tot;
+      launch_graph();
+    }
+  } else {
+    enqueue(s_caller);
+    c->graph_key_seen = key;
+  }
+  CGGM_CUDA_CHECK(cudaStreamSynchronize(s_caller));
+  if (c->factor_reuse) {
+    c->reuse_buf ^= 1;   // this call's trial inverse is the next call's Sigma source
+    c->reuse_valid = 1;
+    c->reuse_q = q;
+  }
+  CholResult cr = chol_decode(h);
+  out->logdet = cr.logdet;
+  out->is_pd = cr.is_pd;
+  out->fail_col = cr.fail_col;
+  objective_decode(h + 64, n, active->lam_L, active->lam_T, &out->obj);
+  ActTotals at;
+  std::memcpy(&at, h + 256, sizeof(ActTotals));
+  active_decode(at, active);
+}
+
 cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, const void* X, int64_t ldx,
                              const void* Y, int64_t ldy, const void* Syy, int64_t ldsyy, const cggm_csc* Lambda,
                              const cggm_csc* Theta, void* Sigma, int64_t ldsigma, void* Psi, int64_t ldpsi,
                              void* GradL, int64_t ldgl, void* GradT, int64_t ldgt, cggm_active_out* active,
                              cggm_eval_out* out) {
   return guard(ctx, [&](Ctx* c) {
-    if (!out) fail(CGGM_ERR_INVALID_ARG, "null cggm_eval_out");
+    newton_eval_core(c, n, p, q, X, ldx, Y, ldy, Syy, ldsyy, Lambda, Theta, Sigma, ldsigma, Psi, ldpsi, GradL, ldgl,
+                     GradT, ldgt, active, out, nullptr);
+  });
+}
+
+cggm_status cggm_newton_eval_host(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, const double* X, int64_t ldx,
+                                  const double* Y, int64_t ldy, const cggm_csc* Lambda, const cggm_csc* Theta,
+                                  void* Syy, int64_t ldsyy, void* Sigma, int64_t ldsigma, void* Psi, int64_t ldpsi,
+                                  void* GradL, int64_t ldgl, void* GradT, int64_t ldgt, cggm_active_out* active,
+                                  cggm_eval_out* out) {
+  return guard(ctx, [&](Ctx* c) {
+    check_ctx_dtype(c);
     if (n < 1 || p < 0 || q < 1) fail(CGGM_ERR_INVALID_ARG, "need n >= 1, q >= 1, p >= 0");
-    check_dense("X", X, n, p, ldx);
-    check_dense("Y", Y, n, q, ldy);
-    check_dense("Syy", Syy, q, q, ldsyy);
-    check_dense("Sigma", Sigma, q, q, ldsigma);
-    check_dense("Psi", Psi, q, q, ldpsi);
-    check_dense("GradL", GradL, q, q, ldgl);
-    check_dense("GradT", GradT, p, q, ldgt, false);
+    if (!X && p > 0) fail(CGGM_ERR_INVALID_ARG, "null X");
+    if (!Y) fail(CGGM_ERR_INVALID_ARG, "null Y");
+    if (ldx < n || ldy < n) fail(CGGM_ERR_INVALID_ARG, "leading dimension < n");
     check_csc_host("Lambda", Lambda, q, q);
     check_csc_host("Theta", Theta, p, q);
-    check_active_args(active);
-    std::memset(out, 0, sizeof(*out));
-    validate_csc_dev(c, Lambda, true, "Lambda");
-    validate_csc_dev(c, Theta, false, "Theta");
-    if (!c->aux) {
-      // the objective's trial factorisation is filler work: least priority, so its CTAs take the SMs
-      // the critical chain (a3 -> a4/a5 -> a6, greatest priority) leaves idle in its latency-bound
-      // recursion levels
-      int least = 0, greatest = 0;
-      CGGM_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-      CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, stream_priority(1)));
-      CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->hi, cudaStreamNonBlocking, stream_priority(0)));
-      CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
-      CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
-      CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_join_hi, cudaEventDisableTiming));
+    if (!c->copy) {
+      CGGM_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+      CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->syys, cudaStreamNonBlocking, stream_priority(3)));
+      for (cudaEvent_t* e : {&c->ev_h_lam, &c->ev_h_xt, &c->ev_h_y})
+        CGGM_CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
-    cudaStream_t s_caller = c->stream;
-    struct Restore {
-      Ctx* c;
-      cudaStream_t s;
-      ~Restore() { c->stream = s; c->lane = 0; }
-    } restore{c, s_caller};
-    // allocate every workspace slot up front (allocation may synchronise the device; nothing in the
-    // enqueue below may, so that it can be captured into a CUDA graph)
-    dispatch(c, [&](auto tag) {
-      using T = decltype(tag);
-      const size_t es = sizeof(T);
-      const int64_t ldn = pad_ld<T>(n);
-      const int64_t nleaves = n_leaves(q);
-      ws_get(c, WS_DENSE_A, (size_t)pad_ld<T>(q) * q * es);
-      ws_get(c, WS_DENSE_B, (size_t)pad_ld<T>(q + n) * q * es);
-      ws_get(c, WS_LINV, (size_t)pad_ld<T>(q) * q * es);
-      ws_get(c, WS_TMP, chol_tmp_elems(q) * es);
-      ws_get(c, WS_LEAFINV, (size_t)nleaves * leaf_nb() * leaf_nb() * es);
-      ws_get(c, WS_XDIAG, (size_t)pad_ld<T>(q) * block_inverse_size() * es);
-      ws_get(c, WS_TMP_OBJ, ((size_t)(block_inverse_size() + 4) * (block_inverse_size() + 4) +
-                             (size_t)pad_ld<T>(q + n) * block_inverse_size()) * es);
-      ws_get(c, WS_SCAL, 64 + (8 + nleaves) * 8);
-      ws_get(c, WS_SCAL2, 64 + (16 + 5 * q + nleaves) * 8);
-      active_ws(c, q);
-      ws_get(c, WS_R, (size_t)ldn * q * es);
-      ws_get(c, WS_E, (size_t)ldn * q * es);
-      if (!GradT) ws_get(c, WS_GTCHUNK, (size_t)pad_ld<T>(p) * std::min<int64_t>(GT_CHUNK, q) * es);
-      ws_get(c, WS_W, (size_t)ldn * q * es);
-      if (c->factor_reuse) {
-        ws_get(c, WS_LINV2, (size_t)pad_ld<T>(q) * q * es);
-        ws_get(c, WS_TMP2, chol_tmp_elems(q) * es);
-        ws_get(c, WS_Z, (size_t)ldn * q * es);
-        ws_get(c, WS_REUSE_SCAL, 64 + 8);
-      }
-    });
-    // factor reuse: Sigma from the kept trial inverse of the previous call (buffer xs_prev); this
-    // call's trial inverse goes to the other buffer
-    const bool reuse_now = c->factor_reuse && c->reuse_valid && c->reuse_q == q;
-    const int xs_prev = c->reuse_buf ? WS_LINV2 : WS_LINV, xs_next = c->reuse_buf ? WS_LINV : WS_LINV2;
-    ActTotals* tot = nullptr;
-    char* h = static_cast<char*>(c->host_scratch);
-    // the whole evaluation, enqueue only: fork onto the chain / objective streams, join back into
-    // the caller's stream, D2H of the scalars into pinned host memory
-    auto enqueue = [&](cudaStream_t so) {
-      c->stream = so;
-      if (c->prio_mode) {
-        CGGM_CUDA_CHECK(cudaEventRecord(c->ev_fork, so));
-        CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->hi, c->ev_fork, 0));
-        c->stream = c->hi;
-      }
-      cudaStream_t s0 = c->stream;
-      dispatch(c, [&](auto tag) {
-        using T = decltype(tag);
-        const size_t es = sizeof(T);
-        const int64_t ldn = pad_ld<T>(n);
-        T* W = static_cast<T*>(ws_get(c, WS_W, (size_t)ldn * q * es));
-        const T* Xd = static_cast<const T*>(X);
-        const T* Yd = static_cast<const T*>(Y);
-        // a2 on the chain stream, then fork
-        spmm_x_theta<T>(c, Xd, ldx, n, Theta, ViewT<T>{W, ldn, n, q});
-        CGGM_CUDA_CHECK(cudaEventRecord(c->ev_fork, s0));
-        CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
-        try {
-          // a7 on the auxiliary stream (lane 1)
-          c->stream = c->aux;
-          c->lane = 1;
-          if (c->factor_reuse)
-            objective_fullinv_enqueue<T>(c, 1, n, q, Yd, ldy, W, ldn, Lambda, Theta, active->penalize_diag, xs_next);
-          else
-            objective_enqueue<T>(c, 1, n, q, Yd, ldy, W, ldn, Lambda, Theta, active->penalize_diag);
-          CGGM_CUDA_CHECK(cudaEventRecord(c->ev_join, c->aux));
-          c->stream = s0;
-          c->lane = 0;
-        } catch (...) {
-          c->stream = s0;
-          c->lane = 0;
-          throw;
-        }
-        // a3, a4/a5, a6 on the chain stream (lane 0)
-        if (reuse_now)
-          invert_from_kept<T>(c, 0, q, static_cast<T*>(Sigma), ldsigma, xs_prev);
-        else
-          invert_enqueue<T>(c, 0, Lambda, static_cast<T*>(Sigma), ldsigma, c->factor_reuse ? xs_prev : (int)WS_LINV);
-        Fuse fz{Lambda, Theta, active, active_ws(c, q)};
-        psi_enqueue<T>(c, n, n, p, q, Xd, ldx, Yd, ldy, W, ldn, static_cast<const T*>(Sigma), ldsigma,
-                       static_cast<const T*>(Syy), ldsyy, nullptr, 0, static_cast<T*>(Psi), ldpsi,
-                       static_cast<T*>(GradL), ldgl, static_cast<T*>(GradT), ldgt, &fz);
-        tot = fz.ws.tot;
-      });
-      c->stream = so;
-      if (c->prio_mode) {
-        CGGM_CUDA_CHECK(cudaEventRecord(c->ev_join_hi, s0));
-        CGGM_CUDA_CHECK(cudaStreamWaitEvent(so, c->ev_join_hi, 0));
-      }
-      CGGM_CUDA_CHECK(cudaStreamWaitEvent(so, c->ev_join, 0));
-      if (c->factor_reuse) {   // keep the trial's (fail_col, log-det) with its inverse
-        Scal s1 = scal_lane(c, 1, 0);
-        char* kept = static_cast<char*>(ws_get(c, WS_REUSE_SCAL, 64 + 8));
-        CGGM_CUDA_CHECK(cudaMemcpyAsync(kept, s1.fail, 4, cudaMemcpyDeviceToDevice, so));
-        CGGM_CUDA_CHECK(cudaMemcpyAsync(kept + 64, s1.dbl, 8, cudaMemcpyDeviceToDevice, so));
-      }
-      chol_readback_async(c, 0, h);
-      objective_readback_async(c, 1, h + 64);
-      CGGM_CUDA_CHECK(cudaMemcpyAsync(h + 256, tot, sizeof(ActTotals), cudaMemcpyDeviceToHost, so));
+    // device copies (workspace), ordered Lambda, Theta + X, Y so that the factorisation can start first
+    const int64_t ldxd = pad_ld<double>(n);
+    auto up = [&](int slot, const void* src, size_t bytes) -> void* {
+      void* d = ws_get(c, slot, std::max<size_t>(bytes, 16));
+      if (bytes) CGGM_CUDA_CHECK(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, c->copy));
+      return d;
     };
-    // CUDA graph of the evaluation: the ~3000 launches of the two recursive factorisations would
-    // otherwise be throttled by the launch queue (the host blocks enqueueing the first one while the
-    // GPU works through it, so the second could not start alongside).  A new argument set runs
-    // eagerly once (allocating anything missing), the second call with the same arguments captures.
-    std::vector<int64_t> key = {n, p, q, ldx, ldy, ldsyy, ldsigma, ldpsi, ldgl, ldgt, (int64_t)c->ws_generation,
-                                (int64_t)c->dtype, c->prio_mode, c->la_min, (int64_t)s_caller};
-    for (const void* ptr : {X, Y, Syy, (const void*)Sigma, (const void*)Psi, (const void*)GradL, (const void*)GradT})
-      key.push_back((int64_t)ptr);
-    for (const cggm_csc* m : {Lambda, Theta}) {
-      key.insert(key.end(), {m->nrows, m->ncols, m->nnz, (int64_t)m->colptr, (int64_t)m->rowidx, (int64_t)m->val});
-    }
+    CGGM_CUDA_CHECK(cudaEventRecord(c->ev_h_lam, c->stream));   // after the caller's prior work
+    CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->copy, c->ev_h_lam, 0));
+    cggm_csc Ld = *Lambda, Td = *Theta;
+    Ld.colptr = static_cast<const int64_t*>(up(WS_H_LCP, Lambda->colptr, (size_t)(q + 1) * 8));
+    Ld.rowidx = static_cast<const int32_t*>(up(WS_H_LRI, Lambda->rowidx, (size_t)Lambda->nnz * 4));
+    Ld.val = up(WS_H_LVA, Lambda->val, (size_t)Lambda->nnz * 8);
+    CGGM_CUDA_CHECK(cudaEventRecord(c->ev_h_lam, c->copy));
+    Td.colptr = static_cast<const int64_t*>(up(WS_H_TCP, Theta->colptr, (size_t)(q + 1) * 8));
+    Td.rowidx = static_cast<const int32_t*>(up(WS_H_TRI, Theta->rowidx, (size_t)Theta->nnz * 4));
+    Td.val = up(WS_H_TVA, Theta->val, (size_t)Theta->nnz * 8);
+    double* Xd = static_cast<double*>(ws_get(c, WS_H_X, (size_t)ldxd * std::max<int64_t>(p, 1) * 8));
+    double* Yd = static_cast<double*>(ws_get(c, WS_H_Y, (size_t)ldxd * q * 8));
+    // structure checks of the uploaded CSCs on the copy stream (they synchronise it: before the large
+    // X, Y uploads are enqueued, so only the small CSC copies are waited for)
     {
-      const cggm_active_out* a = active;
-      int64_t lb, tb;
-      std::memcpy(&lb, &a->lam_L, 8);
-      std::memcpy(&tb, &a->lam_T, 8);
-      int64_t eb;
-      std::memcpy(&eb, &a->tie_eps, 8);
-      key.insert(key.end(), {lb, tb, eb, a->penalize_diag, a->cap_L, a->cap_T, (int64_t)a->L_row, (int64_t)a->L_col,
-                             (int64_t)a->T_row, (int64_t)a->T_col});
+      struct S {
+        Ctx* c;
+        cudaStream_t prev;
+        ~S() { c->stream = prev; }
+      } s_{c, c->stream};
+      c->stream = c->copy;
+      validate_csc_dev(c, &Ld, true, "Lambda");
+      validate_csc_dev(c, &Td, false, "Theta");
     }
-    const bool graphs = c->use_graphs && !c->factor_reuse && (!c->prof || c->graph_prof);
-    key.push_back(c->prof ? 1 : 0);
-    if (graphs && !c->gorigin) {
-      // capture origin: an internal stream (the caller's may be the legacy default stream, which
-      // cannot be captured); ordered after / before the caller's stream by events outside the graph
-      int least = 0, greatest = 0;
-      CGGM_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-      CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->gorigin, cudaStreamNonBlocking, greatest));
-      CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_gpre, cudaEventDisableTiming));
-      CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_gpost, cudaEventDisableTiming));
-    }
-    auto launch_graph = [&]() {
-      CGGM_CUDA_CHECK(cudaEventRecord(c->ev_gpre, s_caller));
-      CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->gorigin, c->ev_gpre, 0));
-      CGGM_CUDA_CHECK(cudaGraphLaunch(c->graph_exec, c->gorigin));
-      CGGM_CUDA_CHECK(cudaEventRecord(c->ev_gpost, c->gorigin));
-      CGGM_CUDA_CHECK(cudaStreamWaitEvent(s_caller, c->ev_gpost, 0));
-    };
-    if (graphs && c->graph_exec && key == c->graph_key) {
-      launch_graph();
-      c->launches += c->graph_launches;
-      tot = c->graph_tot;
-    } else if (graphs && key == c->graph_key_seen) {
-      if (c->graph_exec) {
-        cudaGraphExecDestroy(c->graph_exec);
-        c->graph_exec = nullptr;
-      }
-      const int64_t l0 = c->launches;
-      CGGM_CUDA_CHECK(cudaStreamBeginCapture(c->gorigin, cudaStreamCaptureModeRelaxed));
-      cudaGraph_t g = nullptr;
-      bool captured = true;
-      try {
-        enqueue(c->gorigin);
-      } catch (...) {
-        captured = false;
-      }
-      c->stream = s_caller;
-      c->lane = 0;
-      cudaError_t ce = cudaStreamEndCapture(c->gorigin, &g);
-      cudaError_t ie = cudaErrorUnknown;
-      // node priorities: the chain / objective / side streams' priorities carry into the graph
-      if (captured && ce == cudaSuccess && g)
-        ie = cudaGraphInstantiateWithFlags(&c->graph_exec, g, cudaGraphInstantiateFlagUseNodePriority);
-      if (g) cudaGraphDestroy(g);
-      if (ie != cudaSuccess) {
-        // something in the enqueue is not capturable here: run this and later calls eagerly
-        cudaGetLastError();
-        c->graph_exec = nullptr;
-        c->use_graphs = 0;
-        c->launches = l0;
-        enqueue(s_caller);
-      } else {
-        c->graph_launches = c->launches - l0;
-        c->graph_key = key;
-        c->graph_tot = tot;
-        launch_graph();
-      }
-    } else {
-      enqueue(s_caller);
-      c->graph_key_seen = key;
-    }
-    CGGM_CUDA_CHECK(cudaStreamSynchronize(s_caller));
-    if (c->factor_reuse) {
-      c->reuse_buf ^= 1;   // this call's trial inverse is the next call's Sigma source
-      c->reuse_valid = 1;
-      c->reuse_q = q;
-    }
-    CholResult cr = chol_decode(h);
-    out->logdet = cr.logdet;
-    out->is_pd = cr.is_pd;
-    out->fail_col = cr.fail_col;
-    objective_decode(h + 64, n, active->lam_L, active->lam_T, &out->obj);
-    ActTotals at;
-    std::memcpy(&at, h + 256, sizeof(ActTotals));
-    active_decode(at, active);
+    if (p > 0)
+      CGGM_CUDA_CHECK(cudaMemcpy2DAsync(Xd, ldxd * 8, X, ldx * 8, n * 8, p, cudaMemcpyHostToDevice, c->copy));
+    CGGM_CUDA_CHECK(cudaEventRecord(c->ev_h_xt, c->copy));
+    CGGM_CUDA_CHECK(cudaMemcpy2DAsync(Yd, ldxd * 8, Y, ldy * 8, n * 8, q, cudaMemcpyHostToDevice, c->copy));
+    CGGM_CUDA_CHECK(cudaEventRecord(c->ev_h_y, c->copy));
+    HostIn hin{c->ev_h_lam, c->ev_h_xt, c->ev_h_y};
+    newton_eval_core(c, n, p, q, Xd, ldxd, Yd, ldxd, Syy, ldsyy, &Ld, &Td, Sigma, ldsigma, Psi, ldpsi, GradL, ldgl,
+                     GradT, ldgt, active, out, &hin);
   });
 }
 

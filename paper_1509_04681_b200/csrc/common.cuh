@@ -58,6 +58,10 @@ struct Ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t hi = nullptr;     // high-priority stream of the composite evaluation's critical chain
   cudaEvent_t ev_join_hi = nullptr;
+  cudaEvent_t ev_w = nullptr, ev_syy = nullptr;      // composite: W ready (lane 1 -> chain); S_yy ready (host inputs)
+  cudaStream_t copy = nullptr;                         // host-input uploads (cggm_newton_eval_host)
+  cudaStream_t syys = nullptr;                         // host-input S_yy (priority between chain and objective)
+  cudaEvent_t ev_h_lam = nullptr, ev_h_xt = nullptr, ev_h_y = nullptr;
   // recursive-factorisation lookahead (chol.cu): per lane a critical-chain stream and two side
   // streams (deferred trailing updates, deferred block products) at decreasing priorities, and a
   // pool of dependency events (reused across calls: every wait is enqueued before a re-record)
@@ -178,6 +182,8 @@ enum Slot {
   WS_LINV2,         // factor reuse: the second L^{-1} buffer (the objective's, kept for the next call)
   WS_TMP2,          // factor reuse: the objective lane's full-inverse recursion temporaries
   WS_REUSE_SCAL,    // factor reuse: the kept factor's (fail_col, log-det) scalars
+  WS_H_X, WS_H_Y,   // host-input evaluation: device copies of X, Y and of the CSC arrays
+  WS_H_LCP, WS_H_LRI, WS_H_LVA, WS_H_TCP, WS_H_TRI, WS_H_TVA,
   WS_CD_AUX,        // cooperative sweeps: list column pointers, per-entry changes, column buffer
   WS_NUM
 };

@@ -382,3 +382,32 @@ def test_factor_reuse_evaluation(ctx, name, k):
         assert r["objective"]["f"] == pytest.approx(ref["obj"]["f"], rel=REL_OBJ)
         assert r["active"]["m_L"] == plain["active"]["m_L"] and r["active"]["m_T"] == plain["active"]["m_T"]
         assert relf(to_np(r["Sigma"]), ref["Sigma"]) <= REL_F
+
+
+@pytest.mark.parametrize("name,k", [("small", 1), ("medium", 0)])
+def test_host_buffer_evaluation_matches_device(ctx, name, k):
+    """cggm_newton_eval_host (uploads from page-locked host memory overlapped with the factorisation,
+    S_yy formed in the call) gives bit-identical results to cggm_newton_eval on device copies."""
+    from paper_1509_04681_b200 import DeviceCsc, HostCsc, host_colmajor, to_device_colmajor
+    from paper_1509_04681_b200.api import newton_evaluation
+    P = problem(name)
+    label, lam, th = P.points[k]
+    X, Y = to_device_colmajor(P.X), to_device_colmajor(P.Y)
+    Lg, Tg = DeviceCsc.from_host(lam), DeviceCsc.from_host(th)
+    Syy, _ = ctx.cggm_covariances(X, Y, want_sxy=False)
+    cap = 4_000_000
+
+    def bufs():
+        return {k2: torch.empty(cap, dtype=torch.int32, device="cuda") for k2 in ("L_row", "L_col", "T_row", "T_col")}
+
+    a = newton_evaluation(ctx, X, Y, Syy, Lg, Tg, P.lam_L, P.lam_T, True, bufs())
+    a = {kk: (v.clone() if torch.is_tensor(v) else v) for kk, v in a.items()}
+    Xh, Yh = host_colmajor(P.X), host_colmajor(P.Y)
+    b = ctx.cggm_newton_eval_host(Xh, Yh, HostCsc.from_host(lam), HostCsc.from_host(th), P.lam_L, P.lam_T, True,
+                                  bufs=bufs())
+    assert torch.equal(b["Syy"], Syy)
+    for key in ("Sigma", "Psi", "GradL", "GradT"):
+        assert torch.equal(a[key], b[key]), key
+    assert a["objective"]["f"] == b["objective"]["f"] and a["logdet"] == b["logdet"]
+    for key in ("L_row", "L_col", "T_row", "T_col"):
+        assert torch.equal(a["active"][key], b["active"][key]), key
