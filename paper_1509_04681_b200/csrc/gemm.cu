@@ -31,7 +31,10 @@ namespace {
 constexpr int BK = 16;
 constexpr int STAGES = 4;
 constexpr int GROUP_N = 8;
-constexpr int SYM_BAND = 8;   // tile rows per band of a SYM_LOWER raster
+#ifndef CGGM_SYM_BAND
+#define CGGM_SYM_BAND 8
+#endif
+constexpr int SYM_BAND = CGGM_SYM_BAND;   // tile rows per band of a SYM_LOWER raster
 
 // CTA tile BM_ x BN_ computed by WM_ x WN_ warps (warp tile (BM_/WM_) x (BN_/WN_), fragments of 8)
 template <int BM_, int BN_, int WM_, int WN_>
