@@ -165,6 +165,7 @@ cggm_status cggm_ctx_create(cggm_ctx** out, int device, cggm_dtype dtype, void* 
   if (const char* e = std::getenv("CGGM_GRAPH")) c->use_graphs = std::atoi(e);
   if (const char* e = std::getenv("CGGM_SMALL_KMAX")) c->small_kmax = std::atoi(e);
   if (const char* e = std::getenv("CGGM_NO_ACTIVE_VEC")) c->no_active_vec = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_ACT_ONEPASS")) c->act_onepass = std::atoi(e);
   if (const char* e = std::getenv("CGGM_MID_TILE")) c->mid_tile = std::atoi(e);
   if (const char* e = std::getenv("CGGM_LEAF_SWEEP")) c->leaf_sweep = std::atoi(e);
   if (const char* e = std::getenv("CGGM_CD_COOP")) c->cd_coop = std::atoi(e);

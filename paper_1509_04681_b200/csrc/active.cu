@@ -20,9 +20,25 @@
 namespace cggm {
 namespace {
 
+#ifndef CGGM_ACT_LAM_MINB
+#define CGGM_ACT_LAM_MINB 6
+#endif
 constexpr int NT = 256;
 constexpr int NW = NT / 32;   // warp segments per column
 constexpr int UNR = 4;        // 32-row chunks in flight per lane
+#ifndef CGGM_LF_UNR
+#define CGGM_LF_UNR 4
+#endif
+#ifndef CGGM_LF_MINB
+#define CGGM_LF_MINB 6
+#endif
+constexpr int LF_UNR = CGGM_LF_UNR;   // 64-row pair chunks in flight per lane (split Lambda flags pass)
+// words of the Lambda flag bitmask before column j (column c: ceil((c + 1) / 64) chunks of 2 words)
+__host__ __device__ inline long long tri_words_before_i(long long j) {
+  const long long m = j / 64, r = j % 64;
+  return 2 * (64 * m * (m + 1) / 2 + r * (m + 1));
+}
+
 constexpr unsigned long long ST_AGG = 1ull << 62, ST_INC = 2ull << 62, ST_VAL = (1ull << 62) - 1;
 
 template <bool LAM, typename T>
@@ -195,7 +211,7 @@ struct PairOf<float> {
 };
 
 template <bool LAM, typename T>
-__global__ void __launch_bounds__(NT, LAM ? 6 : 4) k_active_vec(int64_t nrows, const T* __restrict__ G, int64_t ldg,
+__global__ void __launch_bounds__(NT, LAM ? CGGM_ACT_LAM_MINB : 4) k_active_vec(int64_t nrows, const T* __restrict__ G, int64_t ldg,
                                                    const int64_t* colptr, const int32_t* rowidx, const T* val,
                                                    T lam, int penalize_diag, T tie_eps,
                                                    unsigned long long* state, int32_t* out_row, int32_t* out_col,
@@ -375,6 +391,238 @@ __global__ void __launch_bounds__(NT, LAM ? 6 : 4) k_active_vec(int64_t nrows, c
   }
 }
 
+// ---------------------------------------------------------------- split Lambda compaction
+// The Lambda list is ~half the upper triangle at `large` (1.03e8 entries): its single-pass kernel
+// spent a quarter of its time with seven warps parked at the barrier behind warp 0's look-back.
+// Split instead: (1) the scan writes each column's flag words (2 per 64 rows) to a global bitmask
+// (q^2/64 words, 25 MB at q = 20000) with its count / ties / subgradient partial -- no
+// inter-column dependency at all; (2) one block scans the q counts into column bases; (3) the
+// writer turns each column's words into (row, col) entries at its base.
+template <typename T>
+__device__ __forceinline__ void k_lam_flags_col(const T* __restrict__ G, int64_t ldg, const int64_t* colptr,
+                                                const int32_t* rowidx, const T* val, T lam, int penalize_diag,
+                                                T tie_eps, uint32_t* flags, unsigned long long* cnt_col,
+                                                long long* ties_col, double* sub_col, int64_t j) {
+  using V = typename PairOf<T>::V;
+  extern __shared__ uint32_t sm[];
+  const int scan_rows = (int)(j + 1);
+  const int nch = (scan_rows + 63) >> 6;
+  uint32_t* sup = sm;
+  uint32_t* flg = flags + tri_words_before_i(j);
+  __shared__ int wcnt[NW];
+  __shared__ double wsub[NW];
+  __shared__ long long wtie[NW];
+  for (int w = threadIdx.x; w < 2 * nch; w += NT) sup[w] = 0u;
+  __syncthreads();
+  for (int64_t t = colptr[j] + threadIdx.x; t < colptr[j + 1]; t += NT) {
+    const int32_t r = rowidx[t];
+    if (r < scan_rows && val[t] != T(0)) atomicOr(&sup[r >> 5], 1u << (r & 31));
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int per = (nch + NW - 1) / NW;
+  const int ca = min(nch, w * per), cb = min(nch, (w + 1) * per);
+  const T* gc = G + j * ldg;
+  const V* gv = reinterpret_cast<const V*>(gc);
+  const int full_end = scan_rows >> 6;
+  const int jj = (int)j;
+  const T lam_diag = !penalize_diag ? T(0) : lam;
+  int cnt = 0, tc = 0;
+  double s_all = 0.0, s_diag = 0.0;   // rows i < j count twice (both triangles): 2 s_all - s_diag
+  auto process = [&](int c, T x0, T x1) {
+    const int r = 64 * c + 2 * lane;
+    const bool in0 = r < scan_rows, in1 = r + 1 < scan_rows;
+    const uint32_t sb = sup[2 * c + (lane >> 4)] >> ((2 * lane) & 31);
+    const T l0 = (r == jj) ? lam_diag : lam;
+    const T l1 = (r + 1 == jj) ? lam_diag : lam;
+    const T d0 = fabs(x0) - l0, d1 = fabs(x1) - l1;
+    const bool sp0 = sb & 1u, sp1 = (sb >> 1) & 1u;
+    const bool f0 = in0 && (d0 > T(0) || sp0), f1 = in1 && (d1 > T(0) || sp1);
+    const unsigned m0 = __ballot_sync(0xffffffffu, f0), m1 = __ballot_sync(0xffffffffu, f1);
+    if (lane == 0) *reinterpret_cast<uint2*>(&flg[2 * c]) = make_uint2(m0, m1);
+    cnt += __popc(m0) + __popc(m1);
+    tc += (in0 && !sp0 && fabs(d0) <= tie_eps) + (in1 && !sp1 && fabs(d1) <= tie_eps);
+    const double e0 = (in0 && d0 > T(0)) ? (double)d0 : 0.0, e1 = (in1 && d1 > T(0)) ? (double)d1 : 0.0;
+    s_all += e0 + e1;
+    if (r == jj) s_diag += e0;
+    if (r + 1 == jj) s_diag += e1;
+  };
+  // chunks wholly above the diagonal (64 c + 63 < j): every row in range, off-diagonal weight --
+  // the bulk of the triangle, with a third fewer instructions than the general chunk (the pass is
+  // issue-bound, not DRAM-bound, with the general form)
+  auto process_off = [&](int c, T x0, T x1) {
+    const uint32_t sb = sup[2 * c + (lane >> 4)] >> ((2 * lane) & 31);
+    const T d0 = fabs(x0) - lam, d1 = fabs(x1) - lam;
+    const bool sp0 = sb & 1u, sp1 = sb & 2u;
+    const unsigned m0 = __ballot_sync(0xffffffffu, d0 > T(0) || sp0);
+    const unsigned m1 = __ballot_sync(0xffffffffu, d1 > T(0) || sp1);
+    if (lane == 0) *reinterpret_cast<uint2*>(&flg[2 * c]) = make_uint2(m0, m1);
+    cnt += __popc(m0) + __popc(m1);
+    tc += (!sp0 && fabs(d0) <= tie_eps) + (!sp1 && fabs(d1) <= tie_eps);
+    s_all += (double)fmax(d0, T(0)) + (double)fmax(d1, T(0));
+  };
+  const int oe = min(cb, jj >> 6);
+  int c = ca;
+  for (; c + LF_UNR <= oe; c += LF_UNR) {
+    V v[LF_UNR];
+#pragma unroll
+    for (int u = 0; u < LF_UNR; ++u) v[u] = __ldcs(gv + (int64_t)(c + u) * 32 + lane);
+#pragma unroll
+    for (int u = 0; u < LF_UNR; ++u) process_off(c + u, v[u].x, v[u].y);
+  }
+  for (; c < oe; ++c) {
+    const V v = __ldcs(gv + (int64_t)c * 32 + lane);
+    process_off(c, v.x, v.y);
+  }
+  const int fe = min(cb, full_end);
+  for (; c < fe; ++c) {
+    const V v = __ldcs(gv + (int64_t)c * 32 + lane);
+    process(c, v.x, v.y);
+  }
+  for (; c < cb; ++c) {
+    const int r = 64 * c + 2 * lane;
+    const T x0 = r < scan_rows ? __ldcs(gc + r) : T(0);
+    const T x1 = r + 1 < scan_rows ? __ldcs(gc + r + 1) : T(0);
+    process(c, x0, x1);
+  }
+  double sacc = 2.0 * s_all - s_diag;
+  for (int64_t t = colptr[j] + threadIdx.x; t < colptr[j + 1]; t += NT) {
+    const T x = val[t];
+    if (x == T(0)) continue;
+    const int64_t i = rowidx[t];
+    const T gi = gc[i];
+    const T lm = lam_of<true>(i, j, lam, penalize_diag);
+    sacc += (double)fabs(gi + lm * (x > T(0) ? T(1) : T(-1))) - (double)fmax(fabs(gi) - lm, T(0));
+  }
+  long long tcl = tc;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sacc += __shfl_down_sync(0xffffffffu, sacc, o);
+    tcl += __shfl_down_sync(0xffffffffu, tcl, o);
+  }
+  if (lane == 0) {
+    wcnt[w] = cnt;
+    wsub[w] = sacc;
+    wtie[w] = tcl;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long total = 0, tt = 0;
+    double ss = 0.0;
+    for (int k = 0; k < NW; ++k) {
+      total += wcnt[k];
+      tt += wtie[k];
+      ss += wsub[k];
+    }
+    cnt_col[j] = (unsigned long long)total;
+    ties_col[j] = tt;
+    sub_col[j] = ss;
+  }
+}
+
+// CTA k takes columns k and q - 1 - k: every CTA scans q + 1 rows of the triangle
+template <typename T>
+__global__ void __launch_bounds__(NT, CGGM_LF_MINB) k_lam_flags(const T* __restrict__ G, int64_t ldg,
+                                                                const int64_t* colptr, const int32_t* rowidx,
+                                                                const T* val, T lam, int penalize_diag, T tie_eps,
+                                                                uint32_t* flags, unsigned long long* cnt_col,
+                                                                long long* ties_col, double* sub_col, int64_t q) {
+  for (int side = 0; side < 2; ++side) {
+    const int64_t j = side == 0 ? (int64_t)blockIdx.x : q - 1 - (int64_t)blockIdx.x;
+    if (side == 1 && j <= (int64_t)blockIdx.x) break;
+    k_lam_flags_col<T>(G, ldg, colptr, rowidx, val, lam, penalize_diag, tie_eps, flags, cnt_col, ties_col, sub_col, j);
+    __syncthreads();
+  }
+}
+
+// exclusive scan of the column counts (one block); state[q - 1] gets the inclusive total in the
+// look-back encoding k_active_totals reads
+__global__ void __launch_bounds__(1024) k_lam_scan(int64_t q, unsigned long long* cnt_state, long long* base) {
+  __shared__ long long sh[1024];
+  __shared__ long long carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t b0 = 0; b0 < q; b0 += 1024) {
+    const int64_t c = b0 + threadIdx.x;
+    const long long v = c < q ? (long long)cnt_state[c] : 0;
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+      const long long x = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
+      __syncthreads();
+      sh[threadIdx.x] += x;
+      __syncthreads();
+    }
+    if (c < q) base[c] = carry + sh[threadIdx.x] - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += sh[1023];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && q > 0) {
+    base[q] = carry;
+    cnt_state[q - 1] = ST_INC | (unsigned long long)carry;
+  }
+}
+
+// (row, col) entries of column j from its flag words at base[j]
+__device__ __forceinline__ void k_lam_write_col(const uint32_t* __restrict__ flags, const long long* base,
+                                                int32_t* __restrict__ out_row, int32_t* __restrict__ out_col,
+                                                long long cap, int64_t j) {
+  const int nch = (int)((j + 1 + 63) >> 6);
+  const uint32_t* flg = flags + tri_words_before_i(j);
+  __shared__ int wcnt[NW];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int per = (nch + NW - 1) / NW;
+  const int ca = min(nch, w * per), cb = min(nch, (w + 1) * per);
+  int cnt = 0;
+  for (int c = ca + lane; c < cb; c += 32) {
+    const uint2 m = *reinterpret_cast<const uint2*>(&flg[2 * c]);
+    cnt += __popc(m.x) + __popc(m.y);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if (lane == 0) wcnt[w] = cnt;
+  __syncthreads();
+  long long pos = base[j];
+  for (int k = 0; k < w; ++k) pos += wcnt[k];
+  const unsigned below = (1u << lane) - 1u;
+  // 32 chunks per round: lane l loads chunk c0 + l's words, the warp walks the non-empty ones
+  for (int c0 = ca; c0 < cb; c0 += 32) {
+    uint2 mine = make_uint2(0u, 0u);
+    if (c0 + lane < cb) mine = *reinterpret_cast<const uint2*>(&flg[2 * (c0 + lane)]);
+    unsigned nz = __ballot_sync(0xffffffffu, (mine.x | mine.y) != 0u);
+    while (nz) {
+      const int l = __ffs(nz) - 1;
+      nz &= nz - 1u;
+      const unsigned m0 = __shfl_sync(0xffffffffu, mine.x, l), m1 = __shfl_sync(0xffffffffu, mine.y, l);
+      const long long b = pos + __popc(m0 & below) + __popc(m1 & below);
+      const int r = 64 * (c0 + l) + 2 * lane;
+      const bool s0 = (m0 >> lane) & 1u, s1 = (m1 >> lane) & 1u;
+      if (s0 && b < cap) {
+        out_row[b] = r;
+        out_col[b] = (int32_t)j;
+      }
+      const long long p1 = b + s0;
+      if (s1 && p1 < cap) {
+        out_row[p1] = r + 1;
+        out_col[p1] = (int32_t)j;
+      }
+      pos += __popc(m0) + __popc(m1);
+    }
+  }
+}
+
+// (row, col) entries of columns k and q - 1 - k from their flag words at base[]
+__global__ void __launch_bounds__(NT) k_lam_write(const uint32_t* flags, const long long* base, int32_t* out_row,
+                                                  int32_t* out_col, long long cap, int64_t q) {
+  for (int side = 0; side < 2; ++side) {
+    const int64_t j = side == 0 ? (int64_t)blockIdx.x : q - 1 - (int64_t)blockIdx.x;
+    if (side == 1 && j <= (int64_t)blockIdx.x) break;
+    k_lam_write_col(flags, base, out_row, out_col, cap, j);
+    __syncthreads();
+  }
+}
+
 // totals: m from the last column's inclusive state, ties / subgradient summed in fixed order
 constexpr int TOT_NT = 1024;
 __global__ void __launch_bounds__(TOT_NT) k_active_totals(int64_t ncols, const unsigned long long* state,
@@ -424,7 +672,8 @@ void set_smem(K kernel, size_t bytes) {
 }  // namespace
 
 ActWs active_ws(Ctx* c, int64_t q) {
-  const size_t bytes = (size_t)q * 2 * (8 + 8 + 8) + sizeof(ActTotals) + 256;
+  const size_t fl_words = (size_t)tri_words_before_i(q) + 64;
+  const size_t bytes = (size_t)q * 2 * (8 + 8 + 8) + sizeof(ActTotals) + 256 + (size_t)(q + 1) * 8 + fl_words * 4;
   char* base = static_cast<char*>(ws_get(c, WS_ACT, bytes));
   ActWs w;
   w.stateL = reinterpret_cast<unsigned long long*>(base);
@@ -434,6 +683,9 @@ ActWs active_ws(Ctx* c, int64_t q) {
   w.subL = reinterpret_cast<double*>(w.tieT + q);
   w.subT = w.subL + q;
   w.tot = reinterpret_cast<ActTotals*>(w.subT + q);
+  char* after = reinterpret_cast<char*>(w.tot) + ((sizeof(ActTotals) + 255) / 256) * 256;
+  w.baseL = reinterpret_cast<long long*>(after);
+  w.flagsL = reinterpret_cast<uint32_t*>(w.baseL + (q + 1));
   return w;
 }
 
@@ -447,6 +699,19 @@ void active_lambda(Ctx* c, int64_t q, const T* GradL, int64_t ldgl, const cggm_c
                    long long capL) {
   if (q == 0) return;
   Prof pr(c, TAG_ACTIVE);
+  if (vec_ok(GradL, ldgl, c->no_active_vec) && !c->act_onepass) {   // split: flags -> scan -> write
+    const size_t bf = (size_t)((q + 63) / 64) * 2 * 4;
+    set_smem(k_lam_flags<T>, bf);
+    const unsigned pairs = (unsigned)((q + 1) / 2);
+    k_lam_flags<T><<<pairs, NT, bf, c->stream>>>(GradL, ldgl, Lambda->colptr, Lambda->rowidx,
+                                                 static_cast<const T*>(Lambda->val), (T)lam_L, penalize_diag,
+                                                 (T)tie_eps, ws.flagsL, ws.stateL, ws.tieL, ws.subL, q);
+    k_lam_scan<<<1, 1024, 0, c->stream>>>(q, ws.stateL, ws.baseL);
+    k_lam_write<<<pairs, NT, 0, c->stream>>>(ws.flagsL, ws.baseL, L_row, L_col, capL, q);
+    c->launches += 2;
+    post_launch(c, "k_lam_flags/scan/write");
+    return;
+  }
   if (vec_ok(GradL, ldgl, c->no_active_vec)) {
     const size_t bv = smem_bytes_vec(q);
     set_smem(k_active_vec<true, T>, bv);

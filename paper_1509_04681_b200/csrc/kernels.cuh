@@ -26,6 +26,8 @@ struct ActWs {
   long long *tieL, *tieT;
   double *subL, *subT;
   ActTotals* tot;
+  uint32_t* flagsL;        // Lambda flag bitmask of the upper triangle (split compaction)
+  long long* baseL;        // column bases of the Lambda list
 };
 ActWs active_ws(Ctx* c, int64_t q);
 // Building blocks of the single-pass compaction (one stream, in this order): begin (reset the
