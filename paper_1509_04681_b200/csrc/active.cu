@@ -330,7 +330,9 @@ __global__ void __launch_bounds__(NT, LAM ? CGGM_ACT_LAM_MINB : 4) k_active_vec(
     wtie[w] = tc;
   }
   __syncthreads();
-  if (w == 0) {
+  __shared__ long long s_total, s_add[NW];
+  __shared__ int s_stop;
+  if (threadIdx.x == 0) {
     long long total = 0, tt = 0;
     double ss = 0.0;
     for (int k = 0; k < NW; ++k) {
@@ -338,56 +340,65 @@ __global__ void __launch_bounds__(NT, LAM ? CGGM_ACT_LAM_MINB : 4) k_active_vec(
       tt += wtie[k];
       ss += wsub[k];
     }
-    if (lane == 0) {
-      sub_col[j] = ss;
-      ties_col[j] = tt;
-      st_release(&state[j], (j == 0 ? ST_INC : ST_AGG) | (unsigned long long)total);
-    }
-    long long excl = 0;
-    int64_t k0 = j - 1;
-    while (k0 >= 0) {
-      const int64_t k = k0 - lane;
-      unsigned long long v = (k >= 0) ? ld_acquire(&state[k]) : ST_INC;
-      while (__any_sync(0xffffffffu, (v & ~ST_VAL) == 0)) {
-        if ((v & ~ST_VAL) == 0) v = ld_acquire(&state[k]);
-      }
-      const unsigned inc = __ballot_sync(0xffffffffu, (v & ~ST_VAL) == ST_INC);
-      const int stop = inc ? __ffs(inc) - 1 : 31;
-      long long add = (lane <= stop && k >= 0) ? (long long)(v & ST_VAL) : 0;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
-      excl += add;
-      if (inc) break;
-      k0 -= 32;
-    }
-    if (lane == 0) {
-      if (j > 0) st_release(&state[j], ST_INC | (unsigned long long)(excl + total));
-      col_base = excl;
-    }
+    sub_col[j] = ss;
+    ties_col[j] = tt;
+    st_release(&state[j], (j == 0 ? ST_INC : ST_AGG) | (unsigned long long)total);
+    s_total = total;
+    s_stop = NT;
   }
   __syncthreads();
-  long long pos = col_base;
+  // decoupled look-back with the whole block: thread t inspects predecessor k0 - t, so a window
+  // spans NT columns (the predecessors still scanning are about one wave of CTAs back)
+  long long excl = 0;
+  for (int64_t k0 = j - 1; k0 >= 0; k0 -= NT) {
+    const int64_t k = k0 - threadIdx.x;
+    unsigned long long v = ST_INC;   // before column 0: prefix 0
+    if (k >= 0) {
+      v = ld_acquire(&state[k]);
+      while ((v & ~ST_VAL) == 0) v = ld_acquire(&state[k]);
+    }
+    if ((v & ~ST_VAL) == ST_INC) atomicMin(&s_stop, (int)threadIdx.x);
+    __syncthreads();
+    const int stop = s_stop;   // nearest inclusive predecessor
+    long long add = (threadIdx.x <= stop && k >= 0) ? (long long)(v & ST_VAL) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
+    if (lane == 0) s_add[w] = add;
+    __syncthreads();
+    for (int k2 = 0; k2 < NW; ++k2) excl += s_add[k2];
+    if (stop < NT) break;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && j > 0) st_release(&state[j], ST_INC | (unsigned long long)(excl + s_total));
+  long long pos = excl;
   for (int k = 0; k < w; ++k) pos += wcnt[k];
   const unsigned below = (1u << lane) - 1u;
-  for (int cc = ca; cc < cb; ++cc) {
-    const unsigned m0 = flg[2 * cc], m1 = flg[2 * cc + 1];
-    if ((m0 | m1) == 0u) continue;   // warp-uniform
-    const long long base = pos + __popc(m0 & below) + __popc(m1 & below);
-    const int r = 64 * cc + 2 * lane;
-    if ((m0 >> lane) & 1u) {
-      if (base < cap) {
+  // 32 chunks per round: lane l reads chunk c0 + l's words, the warp walks the non-empty ones
+  for (int c0 = ca; c0 < cb; c0 += 32) {
+    unsigned w0 = 0u, w1 = 0u;
+    if (c0 + lane < cb) {
+      w0 = flg[2 * (c0 + lane)];
+      w1 = flg[2 * (c0 + lane) + 1];
+    }
+    unsigned nz = __ballot_sync(0xffffffffu, (w0 | w1) != 0u);
+    while (nz) {
+      const int l = __ffs(nz) - 1;
+      nz &= nz - 1u;
+      const unsigned m0 = __shfl_sync(0xffffffffu, w0, l), m1 = __shfl_sync(0xffffffffu, w1, l);
+      const long long base = pos + __popc(m0 & below) + __popc(m1 & below);
+      const int r = 64 * (c0 + l) + 2 * lane;
+      const bool s0 = (m0 >> lane) & 1u, s1 = (m1 >> lane) & 1u;
+      if (s0 && base < cap) {
         out_row[base] = r;
         out_col[base] = (int32_t)j;
       }
-    }
-    if ((m1 >> lane) & 1u) {
-      const long long p1 = base + ((m0 >> lane) & 1u);
-      if (p1 < cap) {
+      const long long p1 = base + s0;
+      if (s1 && p1 < cap) {
         out_row[p1] = r + 1;
         out_col[p1] = (int32_t)j;
       }
+      pos += __popc(m0) + __popc(m1);
     }
-    pos += __popc(m0) + __popc(m1);
   }
 }
 
