@@ -53,7 +53,7 @@ typedef enum cggm_status {
   CGGM_ERR_CAPACITY = 6,      /* active-set lists larger than the given capacity */
   CGGM_ERR_OOM = 7,           /* workspace allocation failed */
   CGGM_ERR_CUDA = 8,          /* CUDA runtime / launch error */
-  CGGM_ERR_NCCL = 9,          /* reserved (collectives are done by the caller's process group) */
+  CGGM_ERR_NCCL = 9,          /* NCCL (or external collective callback) failure, see cggm_comm_init */
   CGGM_ERR_UNSUPPORTED = 10   /* dtype or mode not implemented */
 } cggm_status;
 
@@ -143,6 +143,47 @@ const char* cggm_profile_tag_name(int32_t tag);
 const char* cggm_last_error(cggm_ctx* ctx);
 /* Library version string. */
 const char* cggm_version(void);
+
+/* ---- sample sharding: library-owned collectives (north_star) --------------
+ * Rank r of a group of `world` holds rows X_r, Y_r of the data (n_local of the n_total samples;
+ * every 1/n uses n_total, reading A21).  Once a communicator is attached to a ctx, the calls below
+ * become COLLECTIVE (every rank calls them, in the same order, with the same Lambda / Theta / lambda
+ * arguments) and return the unsharded results on every rank:
+ *   cggm_covariances   S_yy and S_xy partials all-reduced (sum);
+ *   cggm_gram          S_xx partial all-reduced;
+ *   cggm_invert_logdet rank 0 factors and inverts; Sigma and (logdet, is_pd, fail_col) are
+ *                      broadcast from rank 0 (other ranks do no compute; "the q x q
+ *                      Cholesky/inverse runs on one GPU and is then broadcast", north_star);
+ *   cggm_psi_grad      Psi = sum_r R_r^T R_r and grad_Theta = sum_r (2/n) X_r^T E_r all-reduced
+ *                      before grad_Lambda and the active sets, which every rank then forms
+ *                      identically (GradL with n_local < n_total is allowed only with a comm);
+ *                      with GradT = NULL and fused active sets, each grad_Theta column chunk is
+ *                      all-reduced before its scan (bounded buffer);
+ *   cggm_objective     every rank factors the trial Lambda (augmented with its own W_r rows); the
+ *                      three data traces are all-reduced, logdet and penalties are replicated.
+ * cggm_newton_eval / _host with world > 1 return CGGM_ERR_UNSUPPORTED (the composite overlaps
+ * its steps on one GPU; sharded callers compose the collective calls above).
+ * Collectives are enqueued on the ctx stream.  Failures return CGGM_ERR_NCCL. */
+/* 128-byte NCCL unique id, created on rank 0 (cggm_comm_unique_id) and sent to the other ranks by
+ * the caller (e.g. a torch.distributed broadcast). */
+cggm_status cggm_comm_unique_id(char id[128]);
+/* Attach an NCCL communicator (rank `rank` of `world`, on the ctx device).  NCCL is loaded at
+ * run time (the libnccl.so.2 already in the process, else the system one); CGGM_ERR_NCCL if it
+ * cannot be loaded or the init fails.  Replaces any communicator attached before. */
+cggm_status cggm_comm_init(cggm_ctx* ctx, const char id[128], int32_t rank, int32_t world);
+/* Attach caller-provided collectives instead of NCCL (another transport, or tests that run several
+ * ranks on one GPU where NCCL refuses duplicate devices).  The library synchronises the ctx stream
+ * before each callback; the callback must complete the operation before returning (result in
+ * `buf`, device memory, `count` elements of `dtype`: 0 = double, 1 = float) and return 0 on
+ * success. */
+typedef int (*cggm_allreduce_fn)(void* user, void* buf, int64_t count, int32_t dtype);
+typedef int (*cggm_broadcast_fn)(void* user, void* buf, int64_t count, int32_t dtype, int32_t root);
+cggm_status cggm_comm_init_external(cggm_ctx* ctx, int32_t rank, int32_t world, cggm_allreduce_fn allreduce,
+                                    cggm_broadcast_fn broadcast, void* user);
+/* Detach (and destroy an NCCL) communicator; the calls become single-rank again. */
+cggm_status cggm_comm_destroy(cggm_ctx* ctx);
+/* rank / world of the attached communicator (0 / 1 when none). */
+cggm_status cggm_comm_info(cggm_ctx* ctx, int32_t* rank, int32_t* world);
 
 /* ---- a1: sample covariances (§2.1) ----------------------------------------- */
 /* Syy (q x q, ldsyy) = Y^T Y / n_total (full symmetric), Sxy (p x q, ldsxy) = X^T Y / n_total.

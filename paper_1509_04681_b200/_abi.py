@@ -52,8 +52,17 @@ class cggm_eval_out(ctypes.Structure):
     _fields_ = [("logdet", c_d), ("is_pd", c_i32), ("fail_col", c_i64), ("obj", cggm_objective_out)]
 
 
+# caller-provided collectives (cggm_comm_init_external)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(c_i32, c_vp, c_vp, c_i64, c_i32)
+BROADCAST_FN = ctypes.CFUNCTYPE(c_i32, c_vp, c_vp, c_i64, c_i32, c_i32)
+
 # name -> (restype, argtypes); every symbol include/cggm.h declares
 SIGNATURES = {
+    "cggm_comm_unique_id": (c_i32, [c_vp]),
+    "cggm_comm_init": (c_i32, [c_vp, c_vp, c_i32, c_i32]),
+    "cggm_comm_init_external": (c_i32, [c_vp, c_i32, c_i32, ALLREDUCE_FN, BROADCAST_FN, c_vp]),
+    "cggm_comm_destroy": (c_i32, [c_vp]),
+    "cggm_comm_info": (c_i32, [c_vp, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)]),
     "cggm_ctx_create": (c_i32, [ctypes.POINTER(c_vp), c_i32, c_i32, c_vp]),
     "cggm_ctx_destroy": (c_i32, [c_vp]),
     "cggm_ctx_set_stream": (c_i32, [c_vp, c_vp]),

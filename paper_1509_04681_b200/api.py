@@ -164,6 +164,82 @@ class Context:
         self._check(self.lib.cggm_ctx_profile_read(self.h, ms, cnt, n))
         return {self.lib.cggm_profile_tag_name(i).decode(): (ms[i], int(cnt[i])) for i in range(n)}
 
+    # ---------------------------------------------------------------- sample sharding
+    def comm_init(self, group=None):
+        """Attach an NCCL communicator inside the library (cggm_comm_init) spanning the ranks of the
+        torch.distributed `group`; rank 0's unique id travels over that group.  Afterwards
+        cggm_covariances / cggm_gram / cggm_invert_logdet / cggm_psi_grad / cggm_objective are
+        collective (include/cggm.h, "sample sharding")."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        buf = (ctypes.c_char * 128)()
+        if rank == 0:
+            st = self.lib.cggm_comm_unique_id(buf)
+            if st != 0:
+                raise CggmError(st, "cggm_comm_unique_id failed (NCCL not loadable?)")
+        dev = torch.device("cuda", self.device) if dist.get_backend(group) == "nccl" else torch.device("cpu")
+        t = torch.frombuffer(bytearray(bytes(buf)), dtype=torch.uint8).to(dev)
+        dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        buf = (ctypes.c_char * 128).from_buffer_copy(bytes(t.cpu().tolist()))
+        self._check(self.lib.cggm_comm_init(self.h, buf, rank, world))
+
+    def comm_init_torch(self, group=None):
+        """Attach the torch.distributed `group` itself as the library's collectives
+        (cggm_comm_init_external): each all-reduce / broadcast the library issues runs as a
+        torch.distributed call on a view of the library's device buffer (staged through host memory
+        for gloo).  For transports NCCL cannot serve, e.g. several ranks sharing one GPU in tests."""
+        import torch.distributed as dist
+        host = dist.get_backend(group) == "gloo"
+        device = torch.device("cuda", self.device)
+
+        def view(ptr, count, dtype):
+            class _Cai:
+                __cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8" if dtype == 0 else "<f4",
+                                            "data": (int(ptr), False), "version": 3, "strides": None}
+            return torch.as_tensor(_Cai(), device=device)
+
+        def allreduce(_user, ptr, count, dtype):
+            try:
+                t = view(ptr, count, dtype)
+                if host:
+                    h = t.cpu()
+                    dist.all_reduce(h, group=group)
+                    t.copy_(h)
+                else:
+                    dist.all_reduce(t, group=group)
+                torch.cuda.synchronize(device)
+                return 0
+            except Exception:   # noqa: BLE001 -- reported to the library as a collective failure
+                return 1
+
+        def broadcast(_user, ptr, count, dtype, root):
+            try:
+                t = view(ptr, count, dtype)
+                src = dist.get_global_rank(group, root) if group is not None else root
+                if host:
+                    h = t.cpu()
+                    dist.broadcast(h, src=src, group=group)
+                    t.copy_(h)
+                else:
+                    dist.broadcast(t, src=src, group=group)
+                torch.cuda.synchronize(device)
+                return 0
+            except Exception:   # noqa: BLE001
+                return 1
+
+        self._comm_cbs = (_abi.ALLREDUCE_FN(allreduce), _abi.BROADCAST_FN(broadcast))   # keep alive
+        self._check(self.lib.cggm_comm_init_external(self.h, dist.get_rank(group), dist.get_world_size(group),
+                                                     self._comm_cbs[0], self._comm_cbs[1], None))
+
+    def comm_destroy(self):
+        self._check(self.lib.cggm_comm_destroy(self.h))
+        self._comm_cbs = None
+
+    def comm_info(self) -> tuple[int, int]:
+        r, w = ctypes.c_int32(), ctypes.c_int32()
+        self._check(self.lib.cggm_comm_info(self.h, ctypes.byref(r), ctypes.byref(w)))
+        return int(r.value), int(w.value)
+
     def launch_count(self) -> int:
         v = ctypes.c_int64()
         self._check(self.lib.cggm_ctx_launch_count(self.h, ctypes.byref(v)))

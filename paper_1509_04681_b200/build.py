@@ -14,7 +14,7 @@ LIB = os.path.join(LIBDIR, "libcggm.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr"]
-SOURCES = ["gemm.cu", "gemm_f32.cu", "chol.cu", "stream.cu", "active.cu", "cd.cu", "abi.cu", "peak.cu"]
+SOURCES = ["gemm.cu", "gemm_f32.cu", "chol.cu", "stream.cu", "active.cu", "cd.cu", "abi.cu", "peak.cu", "comm.cu"]
 
 
 def _deps_mtime() -> float:
@@ -46,7 +46,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB
         for _, err in results:
             sys.stderr.write(err)
     objs = [o for o, _ in results]
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib, *objs]
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib, *objs, "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -233,6 +233,7 @@ cggm_status cggm_ctx_destroy(cggm_ctx* ctx) {
   }
   for (auto e : c->evpool) cudaEventDestroy(e);
   if (c->ts_buf) cudaFree(c->ts_buf);
+  comm_release(c);
   delete ctx;
   return CGGM_OK;
 }
@@ -345,6 +346,56 @@ const char* cggm_last_error(cggm_ctx* ctx) { return ctx ? ctx->impl.last_error.c
 }  // extern "C"  (the definitions below keep the C linkage declared in cggm.h)
 
 // ------------------------------------------------------------------ a1
+// ================================================================== sample sharding: communicator
+cggm_status cggm_comm_unique_id(char id[128]) {
+  if (!id) return CGGM_ERR_INVALID_ARG;
+  try {
+    comm_unique_id(id);
+    return CGGM_OK;
+  } catch (const CudaError& e) {
+    return e.code;
+  }
+}
+
+cggm_status cggm_comm_init(cggm_ctx* ctx, const char id[128], int32_t rank, int32_t world) {
+  return guard(ctx, [&](Ctx* c) {
+    if (!id) fail(CGGM_ERR_INVALID_ARG, "null unique id");
+    if (world < 1 || rank < 0 || rank >= world) fail(CGGM_ERR_INVALID_ARG, "need 0 <= rank < world");
+    comm_init_nccl(c, id, rank, world);
+  });
+}
+
+cggm_status cggm_comm_init_external(cggm_ctx* ctx, int32_t rank, int32_t world, cggm_allreduce_fn allreduce,
+                                    cggm_broadcast_fn broadcast, void* user) {
+  return guard(ctx, [&](Ctx* c) {
+    if (!allreduce || !broadcast) fail(CGGM_ERR_INVALID_ARG, "null collective callback");
+    if (world < 1 || rank < 0 || rank >= world) fail(CGGM_ERR_INVALID_ARG, "need 0 <= rank < world");
+    comm_release(c);
+    c->comm.kind = 2;
+    c->comm.rank = rank;
+    c->comm.world = world;
+    c->comm.ar = allreduce;
+    c->comm.bc = broadcast;
+    c->comm.user = user;
+  });
+}
+
+cggm_status cggm_comm_destroy(cggm_ctx* ctx) {
+  return guard(ctx, [&](Ctx* c) { comm_release(c); });
+}
+
+cggm_status cggm_comm_info(cggm_ctx* ctx, int32_t* rank, int32_t* world) {
+  return guard(ctx, [&](Ctx* c) {
+    if (!rank || !world) fail(CGGM_ERR_INVALID_ARG, "null output pointer");
+    *rank = c->comm.rank;
+    *world = c->comm.world;
+  });
+}
+
+// ld-padded column-major matrix as one flat buffer for a collective (padding included)
+static int64_t flat_count(int64_t rows, int64_t cols, int64_t ld) { return cols > 0 ? ld * (cols - 1) + rows : 0; }
+static int dt_code(Ctx* c) { return c->dtype == CGGM_F32 ? 1 : 0; }
+
 cggm_status cggm_covariances(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64_t p, int64_t q, const void* X,
                              int64_t ldx, const void* Y, int64_t ldy, void* Syy, int64_t ldsyy, void* Sxy,
                              int64_t ldsxy) {
@@ -371,6 +422,8 @@ cggm_status cggm_covariances(cggm_ctx* ctx, int64_t n_local, int64_t n_total, in
         gemm(c, true, false, p, q, n_local, static_cast<const T*>(X), ldx, static_cast<const T*>(Y), ldy, e, 0);
       }
     });
+    if (Syy) comm_allreduce(c, Syy, flat_count(q, q, ldsyy), dt_code(c));   // sum of the shards' partials
+    if (Sxy) comm_allreduce(c, Sxy, flat_count(p, q, ldsxy), dt_code(c));
   });
 }
 
@@ -389,6 +442,7 @@ cggm_status cggm_gram(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64_t p
       gemm(c, true, false, p, p, n_local, static_cast<const T*>(X), ldx, static_cast<const T*>(X), ldx, e,
            SYM_LOWER | SYM_MIRROR);
     });
+    comm_allreduce(c, Sxx, flat_count(p, p, ldsxx), dt_code(c));
   });
 }
 
@@ -641,14 +695,32 @@ cggm_status cggm_invert_logdet(cggm_ctx* ctx, const cggm_csc* Lambda, void* Sigm
       return;
     }
     validate_csc_dev(c, Lambda, true, "Lambda");
-    dispatch(c, [&](auto tag) {
-      using T = decltype(tag);
-      invert_enqueue<T>(c, 0, Lambda, static_cast<T*>(Sigma), ldsigma);
-    });
     char* h = static_cast<char*>(c->host_scratch);
-    chol_readback_async(c, 0, h);
-    CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
-    CholResult r = chol_decode(h);
+    CholResult r{};
+    if (c->comm.rank == 0) {   // with a communicator only rank 0 factors (north_star)
+      dispatch(c, [&](auto tag) {
+        using T = decltype(tag);
+        invert_enqueue<T>(c, 0, Lambda, static_cast<T*>(Sigma), ldsigma);
+      });
+      chol_readback_async(c, 0, h);
+      CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+      r = chol_decode(h);
+    }
+    if (comm_attached(c)) {   // Sigma and (logdet, is_pd, fail_col) from rank 0
+      if (Sigma) comm_bcast(c, Sigma, flat_count(q, q, ldsigma), dt_code(c), 0);
+      double* sc = static_cast<double*>(ws_get(c, WS_COMM, 64));
+      double* hs = reinterpret_cast<double*>(h + 512);
+      hs[0] = r.logdet;
+      hs[1] = (double)r.is_pd;
+      hs[2] = (double)r.fail_col;
+      CGGM_CUDA_CHECK(cudaMemcpyAsync(sc, hs, 3 * 8, cudaMemcpyHostToDevice, c->stream));
+      comm_bcast(c, sc, 3, 0, 0);
+      CGGM_CUDA_CHECK(cudaMemcpyAsync(hs, sc, 3 * 8, cudaMemcpyDeviceToHost, c->stream));
+      CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+      r.logdet = hs[0];
+      r.is_pd = hs[1] > 0.5 ? 1 : 0;
+      r.fail_col = (int64_t)hs[2];
+    }
     *logdet = r.logdet;
     *is_pd = r.is_pd;
     *fail_col = r.fail_col;
@@ -735,8 +807,9 @@ template <typename T>
 static void psi_enqueue(Ctx* c, int64_t n_local, int64_t n_total, int64_t p, int64_t q, const T* Xd, int64_t ldx,
                         const T* Yd, int64_t ldy, const T* W, int64_t ldw, const T* Sg, int64_t ldsigma, const T* Syy,
                         int64_t ldsyy, const T* Sxy, int64_t ldsxy, T* Psi, int64_t ldpsi, T* GradL, int64_t ldgl,
-                        T* GradT, int64_t ldgt, const Fuse* fz) {
+                        T* GradT, int64_t ldgt, const Fuse* fz, bool collective = false) {
   const int64_t ldn = pad_ld<T>(n_local > 0 ? n_local : 1);
+  const int dt = sizeof(T) == 4 ? 1 : 0;
   T* R = static_cast<T*>(ws_get(c, WS_R, (size_t)ldn * q * sizeof(T)));
   T* E = static_cast<T*>(ws_get(c, WS_E, (size_t)ldn * q * sizeof(T)));
   {  // a4: acc = W Sigma -> R = acc / sqrt(n), E = Y + acc
@@ -749,6 +822,7 @@ static void psi_enqueue(Ctx* c, int64_t n_local, int64_t n_total, int64_t p, int
     Phase ph(c, TAG_PSI);
     EpilogueT<T> e; e.out1 = Psi; e.ld1 = ldpsi; e.a1 = 1.0;
     gemm(c, true, false, q, q, n_local, R, ldn, R, ldn, e, SYM_LOWER | SYM_MIRROR);
+    if (collective) comm_allreduce(c, Psi, flat_count(q, q, ldpsi), dt);   // Psi = sum_r R_r^T R_r
     if (GradL) {
       Phase pg(c, TAG_GRADL);
       grad_lambda(c, q, Syy, ldsyy, Sg, ldsigma, Psi, ldpsi, GradL, ldgl);
@@ -773,6 +847,7 @@ static void psi_enqueue(Ctx* c, int64_t n_local, int64_t n_total, int64_t p, int
       e.in1a = Sxy + j0 * ldsxy; e.ld1a = ldsxy; e.b1 = 2.0;
       gemm(c, true, false, p, nc, n_local, Xd, ldx, R + j0 * ldn, ldn, e, 0);
     }
+    if (collective) comm_allreduce(c, out, flat_count(p, nc, ldo), dt);   // sum_r (2/n) X_r^T E_r
   };
   if (GradT) {
     grad_theta(0, q, GradT, ldgt);
@@ -816,7 +891,8 @@ cggm_status cggm_psi_grad(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64
     check_dense("Sxy", Sxy, p, q, ldsxy, false);
     if (GradL) {
       check_dense("Syy", Syy, q, q, ldsyy);
-      if (n_local != n_total) fail(CGGM_ERR_INVALID_ARG, "GradL needs the all-reduced Psi: pass GradL=NULL when sharded");
+      if (n_local != n_total && !comm_attached(c))
+        fail(CGGM_ERR_INVALID_ARG, "GradL needs the all-reduced Psi: pass GradL=NULL when sharded without a comm");
     }
     if (Sxy && n_local != n_total) fail(CGGM_ERR_INVALID_ARG, "the S_xy route is not a per-shard partial sum");
     if (fused) {
@@ -837,7 +913,7 @@ cggm_status cggm_psi_grad(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64
       psi_enqueue<T>(c, n_local, n_total, p, q, static_cast<const T*>(X), ldx, static_cast<const T*>(Y), ldy, W, ldn,
                      static_cast<const T*>(Sigma), ldsigma, static_cast<const T*>(Syy), ldsyy,
                      static_cast<const T*>(Sxy), ldsxy, static_cast<T*>(Psi), ldpsi, static_cast<T*>(GradL), ldgl,
-                     static_cast<T*>(GradT), ldgt, fused ? &fz : nullptr);
+                     static_cast<T*>(GradT), ldgt, fused ? &fz : nullptr, comm_attached(c));
       if (fused) tot = fz.ws.tot;
     });
     if (fused) active_sync(c, tot, fused);
@@ -1023,6 +1099,8 @@ cggm_status cggm_objective(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int6
       }
       objective_enqueue<T>(c, 0, n_local, q, static_cast<const T*>(Y), ldy, Wd, ldwd, Lambda, Theta, penalize_diag);
     });
+    // the three data traces are sums over samples; logdet and penalties are the same on every rank
+    comm_allreduce(c, scal_lane(c, 0, 0).dbl + 1, 3, 0);
     char* h = static_cast<char*>(c->host_scratch);
     objective_readback_async(c, 0, h);
     CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
@@ -1045,6 +1123,8 @@ static void newton_eval_core(Ctx* c, int64_t n, int64_t p, int64_t q, const void
                              void* GradT, int64_t ldgt, cggm_active_out* active, cggm_eval_out* out,
                              const HostIn* hin) {
   if (!out) fail(CGGM_ERR_INVALID_ARG, "null cggm_eval_out");
+  if (c->comm.world > 1)
+    fail(CGGM_ERR_UNSUPPORTED, "cggm_newton_eval is single-GPU; with a communicator use the collective calls");
   if (n < 1 || p < 0 || q < 1) fail(CGGM_ERR_INVALID_ARG, "need n >= 1, q >= 1, p >= 0");
   check_dense("X", X, n, p, ldx);
   check_dense("Y", Y, n, q, ldy);

@@ -40,6 +40,16 @@ enum ProfTag {
 
 struct ActTotals;
 
+// attached communicator (sample sharding; cggm_comm_init / _external)
+struct CommState {
+  int kind = 0;   // 0 none, 1 NCCL, 2 external callbacks
+  int rank = 0, world = 1;
+  void* nccl = nullptr;   // ncclComm_t
+  cggm_allreduce_fn ar = nullptr;
+  cggm_broadcast_fn bc = nullptr;
+  void* user = nullptr;
+};
+
 struct Ctx {
   int device = 0;
   cggm_dtype dtype = CGGM_F64;
@@ -110,6 +120,7 @@ struct Ctx {
     cudaStream_t stream;
   };
   std::vector<ProfRec> prof_recs;
+  CommState comm;
 };
 
 // RAII event pair around one launch (no-op unless profiling is enabled)
@@ -165,6 +176,7 @@ enum Slot {
   WS_Z,             // trsm result (n x q)
   WS_SCAL,          // small device scalars / partial-sum arrays
   WS_ACT,           // active-set per-column arrays
+  WS_COMM,          // broadcast scalars (sample sharding)
   WS_PACK0,         // packing for TMA-incompatible operands (lane 0: 0/1, lane 1: 2/3)
   WS_PACK1,
   WS_PACK2,
@@ -190,6 +202,14 @@ enum Slot {
 };
 
 void* ws_get(Ctx* c, int slot, size_t bytes);  // throws CudaError on OOM
+// collectives on the ctx stream over the attached communicator (comm.cu); no-ops without one.
+// dtype 0 = double, 1 = float; buffers in device memory, in place.
+inline bool comm_attached(const Ctx* c) { return c->comm.kind != 0; }
+void comm_allreduce(Ctx* c, void* buf, int64_t count, int dtype);
+void comm_bcast(Ctx* c, void* buf, int64_t count, int dtype, int root);
+void comm_release(Ctx* c);
+void comm_unique_id(char id[128]);
+void comm_init_nccl(Ctx* c, const char id[128], int rank, int world);
 
 struct CudaError {
   cggm_status code;

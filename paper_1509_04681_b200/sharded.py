@@ -23,7 +23,7 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-__all__ = ["shard_rows", "flat", "ShardedEvaluator", "CudaBackend"]
+__all__ = ["shard_rows", "flat", "ShardedEvaluator", "CudaBackend", "CollectiveEvaluator"]
 
 
 def shard_rows(n: int, world: int, rank: int) -> tuple[int, int]:
@@ -184,3 +184,31 @@ class ShardedEvaluator:
         return dict(Sigma=Sigma, logdet=logdet, is_pd=pd, fail_col=fc, Psi=Psi, GradL=GradL, GradT=GradT,
                     active=act, f=f, g=g, obj_logdet=ob["logdet"], tr_syy_lam=tr_syy, tr_sxy_theta=tr_sxy,
                     tr_sigma_m=tr_sm)
+
+
+class CollectiveEvaluator:
+    """The same sample-sharded evaluation with the collectives inside libcggm: the ctx carries a
+    communicator (`Context.comm_init` for NCCL, `Context.comm_init_torch` for a torch.distributed
+    group) and the library calls are collective (include/cggm.h, "sample sharding"):
+    cggm_invert_logdet (rank 0 factors, Sigma broadcast), cggm_psi_grad (Psi and grad_Theta
+    all-reduced before grad_Lambda), cggm_objective (each rank's trial Cholesky on its rows, the
+    three traces all-reduced).  The active sets are then formed identically on every rank."""
+
+    def __init__(self, ctx):
+        self.ctx = ctx
+        self.rank, self.world = ctx.comm_info()
+
+    def setup(self, X_r, Y_r, n_total):
+        self.n_total = n_total
+        self.Syy, _ = self.ctx.cggm_covariances(X_r, Y_r, n_total=n_total, want_sxy=False)
+        return self.Syy
+
+    def evaluate(self, X_r, Y_r, Lam, Theta, lam_L, lam_T, penalize_diag=True, tie_eps=1e-9):
+        n = self.n_total
+        Sigma, logdet, pd, fc = self.ctx.cggm_invert_logdet(Lam)
+        r = self.ctx.cggm_psi_grad(X_r, Y_r, Theta, Sigma, Syy=self.Syy, n_total=n)
+        act = self.ctx.cggm_active_set(r["GradL"], r["GradT"], Lam, Theta, lam_L, lam_T, penalize_diag, tie_eps)
+        ob = self.ctx.cggm_objective(X_r, Y_r, Lam, Theta, lam_L, lam_T, penalize_diag, n_total=n)
+        return dict(Sigma=Sigma, logdet=logdet, is_pd=pd, fail_col=fc, Psi=r["Psi"], GradL=r["GradL"],
+                    GradT=r["GradT"], active=act, f=ob["f"], g=ob["g"], obj_logdet=ob["logdet"],
+                    tr_syy_lam=ob["tr_syy_lam"], tr_sxy_theta=ob["tr_sxy_theta"], tr_sigma_m=ob["tr_sigma_m"])

@@ -79,3 +79,116 @@ def test_two_ranks_match_oracle(name, split):
     assert res["logdet"] == pytest.approx(ld, rel=1e-12)
     if a["ties_L"] == 0 and a["ties_T"] == 0:
         assert (res["m_L"], res["m_T"]) == (a["m_L"], a["m_T"])
+
+
+def _worker_lib(rank, world, port, name, q_out):
+    """Collectives inside libcggm (cggm_comm_init_external over this gloo group)."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_1509_04681_b200 import Context, DeviceCsc, to_device_colmajor
+        from paper_1509_04681_b200.sharded import CollectiveEvaluator, shard_rows
+        from synth.cggm_inputs import make_problem
+        P = make_problem(name)
+        _, lam, th = P.points[1]
+        a, b = shard_rows(P.n, world, rank)
+        X, Y = to_device_colmajor(P.X[a:b]), to_device_colmajor(P.Y[a:b])
+        ctx = Context(0)
+        ctx.comm_init_torch()
+        assert ctx.comm_info() == (rank, world)
+        ev = CollectiveEvaluator(ctx)
+        Syy = ev.setup(X, Y, P.n)
+        r = ev.evaluate(X, Y, DeviceCsc.from_host(lam), DeviceCsc.from_host(th), P.lam_L, P.lam_T, True)
+        # the one-GPU composite must refuse a multi-rank communicator
+        from paper_1509_04681_b200.api import CggmError
+        try:
+            ctx.cggm_newton_eval(X, Y, Syy, DeviceCsc.from_host(lam), DeviceCsc.from_host(th), P.lam_L, P.lam_T)
+            refused = False
+        except CggmError as e:
+            refused = e.status == 10
+        torch.cuda.synchronize()
+        q_out.put({"rank": rank, "Psi": r["Psi"].cpu().numpy(), "GradL": r["GradL"].cpu().numpy(),
+                   "GradT": r["GradT"].cpu().numpy(), "Sigma": r["Sigma"].cpu().numpy(), "Syy": Syy.cpu().numpy(),
+                   "f": r["f"], "logdet": r["logdet"], "is_pd": r["is_pd"], "m_L": r["active"]["m_L"],
+                   "m_T": r["active"]["m_T"], "refused": refused})
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_library_collectives_match_oracle(world):
+    """Every rank of the library-internal collective path ends with the unsharded results."""
+    import torch.multiprocessing as mp
+    from oracle import cggm_oracle as O
+    from synth.cggm_inputs import make_problem
+    ctx = mp.get_context("spawn")
+    qo = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_lib, args=(r, world, port, "small", qo)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [qo.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=600)
+        assert p.exitcode == 0
+    P = make_problem("small")
+    _, lam, th = P.points[1]
+    Syy, Sxy = O.covariances(P.X, P.Y)
+    S, ld, _, _ = O.invert_logdet(lam.to_dense())
+    ref = O.psi_grad(P.X, P.Y, th, S, Syy, Sxy)
+    ob = O.objective(P.X, P.Y, lam, th, P.lam_L, P.lam_T)
+    a = O.active_set(ref["GradL"], ref["GradT"], lam, th, P.lam_L, P.lam_T)
+    rel = lambda x, y: np.linalg.norm(x - y) / np.linalg.norm(y)  # noqa: E731
+    for r in res:
+        assert r["refused"]
+        assert r["is_pd"]
+        assert rel(r["Syy"], Syy) <= 1e-12
+        assert rel(r["Sigma"], S) <= 1e-9
+        assert rel(r["Psi"], ref["Psi"]) <= 1e-9
+        assert rel(r["GradL"], ref["GradL"]) <= 1e-9
+        assert rel(r["GradT"], ref["GradT"]) <= 1e-9
+        assert r["f"] == pytest.approx(ob["f"], rel=1e-10)
+        assert r["logdet"] == pytest.approx(ld, rel=1e-12)
+        if a["ties_L"] == 0 and a["ties_T"] == 0:
+            assert (r["m_L"], r["m_T"]) == (a["m_L"], a["m_T"])
+    # every rank holds bit-identical results (one all-reduce / broadcast result)
+    for r in res[1:]:
+        for k in ("Sigma", "Psi", "GradL", "GradT"):
+            assert np.array_equal(r[k], res[0][k]), k
+
+
+def test_nccl_comm_single_rank_is_identity():
+    """cggm_comm_init (NCCL, loaded at run time) with one rank: the collective calls run their NCCL
+    all-reduce / broadcast and return exactly the single-GPU results."""
+    import torch.distributed as dist
+    from paper_1509_04681_b200 import Context, DeviceCsc, to_device_colmajor
+    from paper_1509_04681_b200.sharded import CollectiveEvaluator
+    from synth.cggm_inputs import make_problem
+    P = make_problem("small")
+    _, lam, th = P.points[1]
+    X, Y = to_device_colmajor(P.X), to_device_colmajor(P.Y)
+    L, T = DeviceCsc.from_host(lam), DeviceCsc.from_host(th)
+    plain = Context(0)
+    ev0 = CollectiveEvaluator(plain)
+    ev0.setup(X, Y, P.n)
+    r0 = ev0.evaluate(X, Y, L, T, P.lam_L, P.lam_T)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        c = Context(0)
+        c.comm_init()
+        assert c.comm_info() == (0, 1)
+        ev = CollectiveEvaluator(c)
+        ev.setup(X, Y, P.n)
+        r = ev.evaluate(X, Y, L, T, P.lam_L, P.lam_T)
+        for k in ("Sigma", "Psi", "GradL", "GradT"):
+            assert torch.equal(r[k], r0[k]), k
+        assert r["f"] == r0["f"] and r["logdet"] == r0["logdet"]
+        c.comm_destroy()
+        assert c.comm_info() == (0, 1)
+    finally:
+        dist.destroy_process_group()
