@@ -166,6 +166,7 @@ cggm_status cggm_ctx_create(cggm_ctx** out, int device, cggm_dtype dtype, void* 
   if (const char* e = std::getenv("CGGM_SMALL_KMAX")) c->small_kmax = std::atoi(e);
   if (const char* e = std::getenv("CGGM_NO_ACTIVE_VEC")) c->no_active_vec = std::atoi(e);
   if (const char* e = std::getenv("CGGM_ACT_ONEPASS")) c->act_onepass = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_NO_VEC_EPI")) c->no_vec_epi = std::atoi(e);
   if (const char* e = std::getenv("CGGM_MID_TILE")) c->mid_tile = std::atoi(e);
   if (const char* e = std::getenv("CGGM_LEAF_SWEEP")) c->leaf_sweep = std::atoi(e);
   if (const char* e = std::getenv("CGGM_CD_COOP")) c->cd_coop = std::atoi(e);
@@ -586,7 +587,12 @@ cggm_status cggm_theta_cd(cggm_ctx* ctx, int64_t p, int64_t q, const void* Sigma
 }
 
 int cggm::stream_priority(int which) {
-  static int off[8] = {0, 5, 0, 1, 2, 3, 4, 5};
+  // which: 0 chain tail (Sigma product, W Sigma, Psi, grad_Theta), 1 objective origin, 2-4 inverse
+  // recursion (critical chain, deferred updates, background products), 5-7 the objective's
+  // recursion, 3 also S_yy.  The recursions' critical chains outrank the big throughput GEMMs, so
+  // their latency-bound kernels start as soon as SMs free up (measured 429.7 -> 426.1 ms at large
+  // against {0, 5, 0, 1, 2, 3, 4, 5}).
+  static int off[8] = {4, 5, 1, 2, 3, 0, 4, 5};
   static bool init = false;
   if (!init) {
     if (const char* e = std::getenv("CGGM_PRIO_SCHEME")) {

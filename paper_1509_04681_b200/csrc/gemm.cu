@@ -68,6 +68,8 @@ struct KParams {
   int flags;
   int a3d, b3d;  // MN-inner operand: tiles inside the first a3d / b3d rows (a multiple of 16) load one
                  // 3-D TMA box; 0 = never (the ragged last tile uses 16-wide 2-D boxes of the second map)
+  int vec;       // epilogue outputs / inputs 16-B aligned with even leading dimensions, no in1b / in2b:
+                 // interior tiles take the paired (double2) epilogue
   Epilogue epi;
 };
 
@@ -320,20 +322,80 @@ __global__ void __maxnreg__(C::MAXREG)
   }
   __syncthreads();
   const bool diag = (P.flags & SYM_LOWER) && I == J;
-  for (int idx = threadIdx.x; idx < BM * BN; idx += NTHREADS) {
-    const int ml = idx % BM, nl = idx / BM;
-    const int m = m0 + ml, n = n0 + nl;
-    if (m >= P.M || n >= P.N) continue;
-    if (diag && m < n) continue;
-    epi_apply(P.epi, m, n, Cs[nl * EPI_LD + ml]);
-  }
-  if (P.flags & SYM_MIRROR) {
+  if (P.vec && !diag && m0 + BM <= P.M && n0 + BN <= P.N) {
+    // interior tile: thread = row pair x column group, 16-B global accesses, the inputs of U
+    // columns loaded before any is used (one memory round trip per U columns, not per element);
+    // per element the same arithmetic as epi_apply
+    constexpr int RP = BM / 2, CG = NTHREADS / RP, NCOL = BN / CG, U = 8;
+    const Epilogue& E = P.epi;
+    const int ml = 2 * (threadIdx.x % RP), cg = threadIdx.x / RP;
+    const int64_t m = m0 + ml;
+#pragma unroll 1
+    for (int i0 = 0; i0 < NCOL; i0 += U) {
+      double2 x1[U], x2[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t n = n0 + cg + CG * (i0 + u);
+        if (E.in1a) x1[u] = *reinterpret_cast<const double2*>(E.in1a + m + n * E.ld1a);
+        if (E.in2a) x2[u] = *reinterpret_cast<const double2*>(E.in2a + m + n * E.ld2a);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int nl = cg + CG * (i0 + u);
+        const int64_t n = n0 + nl;
+        const double v0 = Cs[nl * EPI_LD + ml], v1 = Cs[nl * EPI_LD + ml + 1];
+        if (E.out1) {
+          double2 o = make_double2(__dmul_rn(E.a1, v0), __dmul_rn(E.a1, v1));
+          if (E.in1a) {
+            o.x = __dadd_rn(o.x, __dmul_rn(E.b1, x1[u].x));
+            o.y = __dadd_rn(o.y, __dmul_rn(E.b1, x1[u].y));
+          }
+          *reinterpret_cast<double2*>(E.out1 + m + n * E.ld1) = o;
+        }
+        if (E.out2) {
+          double2 o = make_double2(__dmul_rn(E.a2, v0), __dmul_rn(E.a2, v1));
+          if (E.in2a) {
+            o.x = __dadd_rn(o.x, __dmul_rn(E.b2, x2[u].x));
+            o.y = __dadd_rn(o.y, __dmul_rn(E.b2, x2[u].y));
+          }
+          *reinterpret_cast<double2*>(E.out2 + m + n * E.ld2) = o;
+        }
+      }
+    }
+  } else {
     for (int idx = threadIdx.x; idx < BM * BN; idx += NTHREADS) {
-      const int nl = idx % BN, ml = idx / BN;
+      const int ml = idx % BM, nl = idx / BM;
       const int m = m0 + ml, n = n0 + nl;
       if (m >= P.M || n >= P.N) continue;
-      if (diag && m <= n) continue;
-      epi_apply(P.epi, n, m, Cs[nl * EPI_LD + ml]);
+      if (diag && m < n) continue;
+      epi_apply(P.epi, m, n, Cs[nl * EPI_LD + ml]);
+    }
+  }
+  if (P.flags & SYM_MIRROR) {
+    if (P.vec && !diag && m0 + BM <= P.M && n0 + BN <= P.N && !P.epi.in1a && !P.epi.in2a) {
+      // transposed copy: thread = output row pair (nl, nl + 1) x output-column group
+      constexpr int RP = BN / 2, CG = NTHREADS / RP, NCOL = BM / CG;
+      const Epilogue& E = P.epi;
+      const int nl = 2 * (threadIdx.x % RP), cg = threadIdx.x / RP;
+      const int64_t n = n0 + nl;
+#pragma unroll 4
+      for (int i = 0; i < NCOL; ++i) {
+        const int ml = cg + CG * i;
+        const int64_t m = m0 + ml;
+        const double v0 = Cs[nl * EPI_LD + ml], v1 = Cs[(nl + 1) * EPI_LD + ml];
+        if (E.out1)
+          *reinterpret_cast<double2*>(E.out1 + n + m * E.ld1) = make_double2(__dmul_rn(E.a1, v0), __dmul_rn(E.a1, v1));
+        if (E.out2)
+          *reinterpret_cast<double2*>(E.out2 + n + m * E.ld2) = make_double2(__dmul_rn(E.a2, v0), __dmul_rn(E.a2, v1));
+      }
+    } else {
+      for (int idx = threadIdx.x; idx < BM * BN; idx += NTHREADS) {
+        const int nl = idx % BN, ml = idx / BN;
+        const int m = m0 + ml, n = n0 + nl;
+        if (m >= P.M || n >= P.N) continue;
+        if (diag && m <= n) continue;
+        epi_apply(P.epi, n, m, Cs[nl * EPI_LD + ml]);
+      }
     }
   }
 }
@@ -724,6 +786,11 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
   P.M = (int)M; P.N = (int)N; P.K = (int)(K > 0 ? K : 0);
   P.flags = flags;
   P.epi = epi;
+  {
+    auto al = [](const double* q, int64_t ld) { return !q || (reinterpret_cast<uintptr_t>(q) % 16 == 0 && ld % 2 == 0); };
+    P.vec = !c->no_vec_epi && !epi.in1b && !epi.in2b && al(epi.out1, epi.ld1) && al(epi.out2, epi.ld2) &&
+            al(epi.in1a, epi.ld1a) && al(epi.in2a, epi.ld2a);
+  }
   if ((flags & SYM_LOWER) && (M < N || ((flags & SYM_MIRROR) && M != N)))
     throw CudaError{CGGM_ERR_SHAPE, "SYM_LOWER gemm needs M >= N (M == N with SYM_MIRROR)"};
   // 128x128 tiles unless they cannot fill the GPU; then 64x64 tiles (4x the CTAs, several per SM)
