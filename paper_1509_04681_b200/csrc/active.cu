@@ -546,32 +546,43 @@ __global__ void __launch_bounds__(NT, CGGM_LF_MINB) k_lam_flags(const T* __restr
   }
 }
 
-// exclusive scan of the column counts (one block); state[q - 1] gets the inclusive total in the
+// exclusive scan of the column counts (one block): thread t owns a contiguous run of columns,
+// the 1024 run totals are scanned with warp shuffles; state[q - 1] gets the inclusive total in the
 // look-back encoding k_active_totals reads
 __global__ void __launch_bounds__(1024) k_lam_scan(int64_t q, unsigned long long* cnt_state, long long* base) {
-  __shared__ long long sh[1024];
-  __shared__ long long carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int64_t b0 = 0; b0 < q; b0 += 1024) {
-    const int64_t c = b0 + threadIdx.x;
-    const long long v = c < q ? (long long)cnt_state[c] : 0;
-    sh[threadIdx.x] = v;
-    __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {
-      const long long x = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
-      __syncthreads();
-      sh[threadIdx.x] += x;
-      __syncthreads();
-    }
-    if (c < q) base[c] = carry + sh[threadIdx.x] - v;
-    __syncthreads();
-    if (threadIdx.x == 1023) carry += sh[1023];
-    __syncthreads();
+  __shared__ long long wsum[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t per = (q + 1023) / 1024;
+  const int64_t c0 = min(q, (int64_t)threadIdx.x * per), c1 = min(q, c0 + per);
+  long long run = 0;
+  for (int64_t c = c0; c < c1; ++c) run += (long long)cnt_state[c];
+  long long incl = run;   // inclusive scan over the block
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long x = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += x;
   }
-  if (threadIdx.x == 0 && q > 0) {
-    base[q] = carry;
-    cnt_state[q - 1] = ST_INC | (unsigned long long)carry;
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    long long v = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long x = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += x;
+    }
+    wsum[lane] = v;   // inclusive over warps
+  }
+  __syncthreads();
+  long long pos = incl - run + (w > 0 ? wsum[w - 1] : 0);
+  for (int64_t c = c0; c < c1; ++c) {
+    const long long v = (long long)cnt_state[c];
+    base[c] = pos;
+    pos += v;
+  }
+  if (threadIdx.x == 1023 && q > 0) {
+    base[q] = wsum[31];
+    cnt_state[q - 1] = ST_INC | (unsigned long long)wsum[31];
   }
 }
 
@@ -634,13 +645,21 @@ __global__ void __launch_bounds__(NT) k_lam_write(const uint32_t* flags, const l
   }
 }
 
-// totals: m from the last column's inclusive state, ties / subgradient summed in fixed order
+// totals: m from the last column's inclusive state, ties / subgradient summed in a fixed order
+// (contiguous runs per thread, then a fixed shuffle tree): bitwise reproducible
 constexpr int TOT_NT = 1024;
-__global__ void __launch_bounds__(TOT_NT) k_active_totals(int64_t ncols, const unsigned long long* state,
-                                                          const long long* ties_col, const double* sub_col,
-                                                          long long* tot_m, long long* tot_ties, double* tot_sub) {
-  __shared__ long long st[TOT_NT];
-  __shared__ double sd[TOT_NT];
+// block 0: the Lambda list, block 1: the Theta list
+__global__ void __launch_bounds__(TOT_NT) k_active_totals(int64_t ncols, ActWs ws) {
+  const bool th = blockIdx.x == 1;
+  const unsigned long long* state = th ? ws.stateT : ws.stateL;
+  const long long* ties_col = th ? ws.tieT : ws.tieL;
+  const double* sub_col = th ? ws.subT : ws.subL;
+  long long* tot_m = th ? &ws.tot->m_T : &ws.tot->m_L;
+  long long* tot_ties = th ? &ws.tot->ties_T : &ws.tot->ties_L;
+  double* tot_sub = th ? &ws.tot->sub_T : &ws.tot->sub_L;
+  __shared__ long long st[32];
+  __shared__ double sd[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t per = (ncols + TOT_NT - 1) / TOT_NT;
   const int64_t b = threadIdx.x * per, e = min(ncols, b + per);
   long long t = 0;
@@ -649,19 +668,29 @@ __global__ void __launch_bounds__(TOT_NT) k_active_totals(int64_t ncols, const u
     t += ties_col[i];
     d += sub_col[i];
   }
-  st[threadIdx.x] = t;
-  sd[threadIdx.x] = d;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    t += __shfl_down_sync(0xffffffffu, t, o);
+    d += __shfl_down_sync(0xffffffffu, d, o);
+  }
+  if (lane == 0) {
+    st[w] = t;
+    sd[w] = d;
+  }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    long long tt = 0;
-    double dd = 0.0;
-    for (int k = 0; k < TOT_NT; ++k) {
-      tt += st[k];
-      dd += sd[k];
+  if (w == 0) {
+    t = st[lane];
+    d = sd[lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      t += __shfl_down_sync(0xffffffffu, t, o);
+      d += __shfl_down_sync(0xffffffffu, d, o);
     }
-    *tot_m = ncols > 0 ? (long long)(state[ncols - 1] & ST_VAL) : 0;
-    *tot_ties = tt;
-    *tot_sub = dd;
+    if (lane == 0) {
+      *tot_m = ncols > 0 ? (long long)(state[ncols - 1] & ST_VAL) : 0;
+      *tot_ties = t;
+      *tot_sub = d;
+    }
   }
 }
 
@@ -765,18 +794,9 @@ void active_theta_chunk(Ctx* c, int64_t p, int64_t col0, int64_t ncols, const T*
 
 void active_end(Ctx* c, int64_t q, const ActWs& ws) {
   if (q == 0) return;
-  {
-    Prof pr(c, TAG_ACTIVE);
-    k_active_totals<<<1, TOT_NT, 0, c->stream>>>(q, ws.stateL, ws.tieL, ws.subL, &ws.tot->m_L, &ws.tot->ties_L,
-                                                 &ws.tot->sub_L);
-    post_launch(c, "k_active_totals<L>");
-  }
-  {
-    Prof pr(c, TAG_ACTIVE);
-    k_active_totals<<<1, TOT_NT, 0, c->stream>>>(q, ws.stateT, ws.tieT, ws.subT, &ws.tot->m_T, &ws.tot->ties_T,
-                                                 &ws.tot->sub_T);
-    post_launch(c, "k_active_totals<T>");
-  }
+  Prof pr(c, TAG_ACTIVE);
+  k_active_totals<<<2, TOT_NT, 0, c->stream>>>(q, ws);
+  post_launch(c, "k_active_totals");
 }
 
 template <typename T>
