@@ -1204,6 +1204,7 @@ static void newton_eval_core(Ctx* c, int64_t n, int64_t p, int64_t q, const void
   char* h = static_cast<char*>(c->host_scratch);
   // the whole evaluation, enqueue only: fork onto the chain / objective streams, join back into
   // the caller's stream, D2H of the scalars into pinned host memory
+  unsigned hin_wait = 0;   // cudaEventWaitExternal while capturing (events recorded outside the graph)
   auto enqueue = [&](cudaStream_t so) {
     c->stream = so;
     if (c->prio_mode) {
@@ -1227,11 +1228,11 @@ static void newton_eval_core(Ctx* c, int64_t n, int64_t p, int64_t q, const void
       try {
         c->stream = c->aux;
         c->lane = 1;
-        if (hin) CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->aux, hin->ev_xt, 0));
+        if (hin) CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->aux, hin->ev_xt, hin_wait));
         spmm_x_theta<T>(c, Xd, ldx, n, Theta, ViewT<T>{W, ldn, n, q});
         CGGM_CUDA_CHECK(cudaEventRecord(c->ev_w, c->aux));
         if (hin) {   // S_yy on its own stream, above the objective's priority: off the chain's critical path
-          CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->syys, hin->ev_y, 0));
+          CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->syys, hin->ev_y, hin_wait));
           c->stream = c->syys;
           Phase ph(c, TAG_COV);
           EpilogueT<T> e; e.out1 = static_cast<T*>(const_cast<void*>(Syy)); e.ld1 = ldsyy; e.a1 = 1.0 / (double)n;
@@ -1252,7 +1253,7 @@ static void newton_eval_core(Ctx* c, int64_t n, int64_t p, int64_t q, const void
         throw;
       }
       // a3, a4/a5, a6 on the chain stream (lane 0)
-      if (hin) CGGM_CUDA_CHECK(cudaStreamWaitEvent(s0, hin->ev_lam, 0));
+      if (hin) CGGM_CUDA_CHECK(cudaStreamWaitEvent(s0, hin->ev_lam, hin_wait));
       if (reuse_now)
         invert_from_kept<T>(c, 0, q, static_cast<T*>(Sigma), ldsigma, xs_prev);
       else
@@ -1302,7 +1303,10 @@ static void newton_eval_core(Ctx* c, int64_t n, int64_t p, int64_t q, const void
     key.insert(key.end(), {lb, tb, eb, a->penalize_diag, a->cap_L, a->cap_T, (int64_t)a->L_row, (int64_t)a->L_col,
                            (int64_t)a->T_row, (int64_t)a->T_col});
   }
-  const bool graphs = c->use_graphs && !c->factor_reuse && !hin && (!c->prof || c->graph_prof);
+  // host inputs: the uploads run eagerly on the copy stream before the (captured) evaluation, which
+  // waits for them through external event-wait nodes
+  const bool graphs = c->use_graphs && !c->factor_reuse && (!c->prof || c->graph_prof);
+  key.push_back(hin ? 1 : 0);
   key.push_back(c->prof ? 1 : 0);
   if (graphs && !c->gorigin) {
     // capture origin: an internal stream (the caller's may be the legacy default stream, which
@@ -1334,10 +1338,13 @@ static void newton_eval_core(Ctx* c, int64_t n, int64_t p, int64_t q, const void
     cudaGraph_t g = nullptr;
     bool captured = true;
     try {
+      hin_wait = cudaEventWaitExternal;
       enqueue(c->gorigin);
+      hin_wait = 0;
     } catch (...) {
       captured = false;
     }
+    hin_wait = 0;
     c->stream = s_caller;
     c->lane = 0;
     cudaError_t ce = cudaStreamEndCapture(c->gorigin, &g);

@@ -411,3 +411,43 @@ def test_host_buffer_evaluation_matches_device(ctx, name, k):
     assert a["objective"]["f"] == b["objective"]["f"] and a["logdet"] == b["logdet"]
     for key in ("L_row", "L_col", "T_row", "T_col"):
         assert torch.equal(a["active"][key], b["active"][key]), key
+
+
+def test_host_buffer_graph_replay_sees_new_host_data(ctx):
+    """cggm_newton_eval_host with the same arguments runs eagerly, then captures a CUDA graph, then
+    replays it; the uploads stay outside the graph (external event waits), so a replay must see host
+    data changed in place between calls: results equal a fresh device-path evaluation of the new
+    data, bit for bit."""
+    from paper_1509_04681_b200 import Context, DeviceCsc, HostCsc, host_colmajor, to_device_colmajor
+    from paper_1509_04681_b200.api import newton_evaluation
+    P = problem("small")
+    label, lam, th = P.points[1]
+    Xh, Yh = host_colmajor(P.X), host_colmajor(P.Y)
+    Lh, Th = HostCsc.from_host(lam), HostCsc.from_host(th)
+    cap = 400_000
+    bufs = {k2: torch.empty(cap, dtype=torch.int32, device="cuda") for k2 in ("L_row", "L_col", "T_row", "T_col")}
+    c = Context(0)
+    outs = []
+    for it in range(5):
+        if it == 3:   # new data in the same pinned buffers: the replayed graph must upload it
+            Yh.mul_(0.5)
+            Xh.add_(0.25)
+        r = c.cggm_newton_eval_host(Xh, Yh, Lh, Th, P.lam_L, P.lam_T, True, bufs=bufs)
+        outs.append({k: (v.clone() if torch.is_tensor(v) else v) for k, v in r.items() if k != "active"}
+                    | {"active": {k: (v.clone() if torch.is_tensor(v) else v) for k, v in r["active"].items()}})
+    for key in ("Sigma", "Psi", "GradL", "GradT", "Syy"):
+        assert torch.equal(outs[0][key], outs[1][key]) and torch.equal(outs[1][key], outs[2][key]), key
+        assert torch.equal(outs[3][key], outs[4][key]), key
+    # reference for the modified data through the device path on a fresh context
+    d = Context(0)
+    X, Y = to_device_colmajor(Xh.numpy()), to_device_colmajor(Yh.numpy())
+    Syy, _ = d.cggm_covariances(X, Y, want_sxy=False)
+    bufs2 = {k2: torch.empty(cap, dtype=torch.int32, device="cuda") for k2 in ("L_row", "L_col", "T_row", "T_col")}
+    ref = newton_evaluation(d, X, Y, Syy, DeviceCsc.from_host(lam), DeviceCsc.from_host(th), P.lam_L, P.lam_T, True,
+                            bufs2)
+    assert torch.equal(outs[4]["Syy"], Syy)
+    for key in ("Sigma", "Psi", "GradL", "GradT"):
+        assert torch.equal(outs[4][key], ref[key]), key
+    assert outs[4]["objective"]["f"] == ref["objective"]["f"]
+    assert outs[4]["active"]["m_L"] == ref["active"]["m_L"] and outs[4]["active"]["m_T"] == ref["active"]["m_T"]
+    assert not torch.equal(outs[4]["GradT"], outs[0]["GradT"])
