@@ -1232,6 +1232,7 @@ static void newton_eval_core(Ctx* c, int64_t n, int64_t p, int64_t q, const void
         spmm_x_theta<T>(c, Xd, ldx, n, Theta, ViewT<T>{W, ldn, n, q});
         CGGM_CUDA_CHECK(cudaEventRecord(c->ev_w, c->aux));
         if (hin) {   // S_yy on its own stream, above the objective's priority: off the chain's critical path
+          CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->syys, c->ev_fork, 0));   // joins the capture, if any
           CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->syys, hin->ev_y, hin_wait));
           c->stream = c->syys;
           Phase ph(c, TAG_COV);
@@ -1341,6 +1342,9 @@ static void newton_eval_core(Ctx* c, int64_t n, int64_t p, int64_t q, const void
       hin_wait = cudaEventWaitExternal;
       enqueue(c->gorigin);
       hin_wait = 0;
+    } catch (const CudaError& e) {
+      captured = false;
+      if (std::getenv("CGGM_GRAPH_DEBUG")) std::fprintf(stderr, "cggm: capture enqueue threw: %s\n", e.msg.c_str());
     } catch (...) {
       captured = false;
     }
@@ -1355,6 +1359,9 @@ static void newton_eval_core(Ctx* c, int64_t n, int64_t p, int64_t q, const void
     if (g) cudaGraphDestroy(g);
     if (ie != cudaSuccess) {
       // something in the enqueue is not capturable here: run this and later calls eagerly
+      if (std::getenv("CGGM_GRAPH_DEBUG"))
+        std::fprintf(stderr, "cggm: graph capture failed (captured=%d end=%s instantiate=%s); eager from now on\n",
+                     (int)captured, cudaGetErrorString(ce), cudaGetErrorString(ie));
       cudaGetLastError();
       c->graph_exec = nullptr;
       c->use_graphs = 0;
