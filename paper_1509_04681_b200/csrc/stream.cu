@@ -72,10 +72,83 @@ __global__ void __launch_bounds__(SPMM_ROWS) k_spmm_x_theta(const T* __restrict_
 }
 
 template <typename T>
+struct SpPair;
+template <>
+struct SpPair<double> {
+  using V = double2;
+};
+template <>
+struct SpPair<float> {
+  using V = float2;
+};
+
+// Paired variant (16-byte aligned X and W, even leading dimensions): each thread owns two adjacent
+// rows, so one 16-byte gather serves both and the per-gather address / issue work halves (the
+// kernel is bound by L2 gather throughput and SM issue, not by HBM: X is read from HBM about once)
+template <typename T>
+__global__ void __launch_bounds__(SPMM_ROWS / 2) k_spmm_x_theta2(const T* __restrict__ X, int64_t ldx, int64_t n,
+                                                                const int64_t* __restrict__ colptr,
+                                                                const int32_t* __restrict__ rowidx,
+                                                                const T* __restrict__ val, T* __restrict__ W,
+                                                                int64_t ldw) {
+  using V = typename SpPair<T>::V;
+  constexpr int NT = SPMM_ROWS / 2;
+  __shared__ int64_t offs[SPMM_ROWS];
+  __shared__ T vals[SPMM_ROWS];
+  const int64_t j = blockIdx.x;
+  const int64_t k = (int64_t)blockIdx.y * SPMM_ROWS + 2 * threadIdx.x;
+  const int64_t a = colptr[j], b = colptr[j + 1];
+  T acc0 = T(0), acc1 = T(0);
+  const bool full = k + 1 < n;
+  for (int64_t t0 = a; t0 < b; t0 += SPMM_ROWS) {
+    const int cnt = (int)((b - t0) < SPMM_ROWS ? (b - t0) : SPMM_ROWS);
+    __syncthreads();
+    for (int e = threadIdx.x; e < cnt; e += NT) {
+      offs[e] = (int64_t)rowidx[t0 + e] * ldx;
+      vals[e] = val[t0 + e];
+    }
+    __syncthreads();
+    if (full) {
+      int e = 0;
+      for (; e + 8 <= cnt; e += 8) {  // 8 independent 16-byte gathers in flight
+        V xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xv[u] = __ldg(reinterpret_cast<const V*>(X + k + offs[e + u]));
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          acc0 = fma(vals[e + u], xv[u].x, acc0);
+          acc1 = fma(vals[e + u], xv[u].y, acc1);
+        }
+      }
+      for (; e < cnt; ++e) {
+        const V xv = __ldg(reinterpret_cast<const V*>(X + k + offs[e]));
+        acc0 = fma(vals[e], xv.x, acc0);
+        acc1 = fma(vals[e], xv.y, acc1);
+      }
+    } else if (k < n) {
+      for (int e = 0; e < cnt; ++e) acc0 = fma(vals[e], __ldg(X + k + offs[e]), acc0);
+    }
+  }
+  if (full) {
+    *reinterpret_cast<V*>(W + k + j * ldw) = V{acc0, acc1};
+  } else if (k < n) {
+    W[k + j * ldw] = acc0;
+  }
+}
+
+template <typename T>
 void spmm_x_theta(Ctx* c, const T* X, int64_t ldx, int64_t n, const cggm_csc* Theta, ViewT<T> W) {
   if (Theta->ncols == 0 || n == 0) return;
   Prof pr(c, TAG_SPMM);
   dim3 grid((unsigned)Theta->ncols, (unsigned)((n + SPMM_ROWS - 1) / SPMM_ROWS));
+  const bool paired = reinterpret_cast<uintptr_t>(X) % (2 * sizeof(T)) == 0 && ldx % 2 == 0 &&
+                      reinterpret_cast<uintptr_t>(W.p) % (2 * sizeof(T)) == 0 && W.ld % 2 == 0;
+  if (paired) {
+    k_spmm_x_theta2<T><<<grid, SPMM_ROWS / 2, 0, c->stream>>>(X, ldx, n, Theta->colptr, Theta->rowidx,
+                                                              static_cast<const T*>(Theta->val), W.p, W.ld);
+    post_launch(c, "k_spmm_x_theta2");
+    return;
+  }
   k_spmm_x_theta<T><<<grid, SPMM_ROWS, 0, c->stream>>>(X, ldx, n, Theta->colptr, Theta->rowidx,
                                                       static_cast<const T*>(Theta->val), W.p, W.ld);
   post_launch(c, "k_spmm_x_theta");
