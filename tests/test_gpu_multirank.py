@@ -192,3 +192,68 @@ def test_nccl_comm_single_rank_is_identity():
         assert c.comm_info() == (0, 1)
     finally:
         dist.destroy_process_group()
+
+
+def _worker_stream(rank, world, port, q_out):
+    """cggm_psi_grad with the streamed grad_Theta (GradT = NULL, fused active sets) under the library
+    collectives: each column chunk is all-reduced before its scan (medium: q = 4000, two chunks)."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_1509_04681_b200 import Context, DeviceCsc, to_device_colmajor
+        from paper_1509_04681_b200.sharded import shard_rows
+        from synth.cggm_inputs import make_problem
+        P = make_problem("medium")
+        _, lam, th = P.points[0]
+        a, b = shard_rows(P.n, world, rank)
+        X, Y = to_device_colmajor(P.X[a:b]), to_device_colmajor(P.Y[a:b])
+        ctx = Context(0)
+        ctx.comm_init_torch()
+        Syy, _ = ctx.cggm_covariances(X, Y, n_total=P.n, want_sxy=False)
+        L, T = DeviceCsc.from_host(lam), DeviceCsc.from_host(th)
+        Sigma, _, _, _ = ctx.cggm_invert_logdet(L)
+        cap = 2_000_000
+        spec = dict(lam_L=P.lam_L, lam_T=P.lam_T, penalize_diag=1,
+                    **{k: torch.empty(cap, dtype=torch.int32, device="cuda") for k in ("L_row", "L_col", "T_row", "T_col")})
+        r = ctx.cggm_psi_grad(X, Y, T, Sigma, Syy=Syy, n_total=P.n, want_gradT=False, Lam=L, fused=spec)
+        act = r["active"]
+        torch.cuda.synchronize()
+        q_out.put({"rank": rank, "m_L": act["m_L"], "m_T": act["m_T"], "ties": (act["ties_L"], act["ties_T"]),
+                   "sub": act["subgrad_l1"], "T_row": act["T_row"].cpu().numpy(), "T_col": act["T_col"].cpu().numpy(),
+                   "GradL": r["GradL"].cpu().numpy()})
+    finally:
+        dist.destroy_process_group()
+
+
+def test_library_collectives_streamed_grad_theta():
+    import torch.multiprocessing as mp
+    from oracle import cggm_oracle as O
+    from synth.cggm_inputs import make_problem
+    ctx = mp.get_context("spawn")
+    qo = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_stream, args=(r, 2, port, qo)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [qo.get(timeout=900) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=900)
+        assert p.exitcode == 0
+    P = make_problem("medium")
+    _, lam, th = P.points[0]
+    Syy, Sxy = O.covariances(P.X, P.Y)
+    S, _, _, _ = O.invert_logdet(lam.to_dense())
+    ref = O.psi_grad(P.X, P.Y, th, S, Syy, Sxy)
+    a = O.active_set(ref["GradL"], ref["GradT"], lam, th, P.lam_L, P.lam_T)
+    sub = O.min_norm_subgradient(ref["GradL"], ref["GradT"], lam, th, P.lam_L, P.lam_T)
+    for r in res:
+        assert np.linalg.norm(r["GradL"] - ref["GradL"]) <= 1e-9 * np.linalg.norm(ref["GradL"])
+        assert r["sub"] == pytest.approx(sub, rel=1e-9)
+        if a["ties_L"] == 0 and a["ties_T"] == 0:
+            assert (r["m_L"], r["m_T"]) == (a["m_L"], a["m_T"])
+            assert np.array_equal(r["T_row"], a["T_row"]) and np.array_equal(r["T_col"], a["T_col"])
+    assert (res[0]["m_L"], res[0]["m_T"], res[0]["ties"]) == (res[1]["m_L"], res[1]["m_T"], res[1]["ties"])
+    assert np.array_equal(res[0]["T_row"], res[1]["T_row"])
