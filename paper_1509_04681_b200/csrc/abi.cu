@@ -166,6 +166,7 @@ cggm_status cggm_ctx_create(cggm_ctx** out, int device, cggm_dtype dtype, void* 
   if (const char* e = std::getenv("CGGM_SMALL_KMAX")) c->small_kmax = std::atoi(e);
   if (const char* e = std::getenv("CGGM_NO_ACTIVE_VEC")) c->no_active_vec = std::atoi(e);
   if (const char* e = std::getenv("CGGM_ACT_ONEPASS")) c->act_onepass = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_NO_SPLIT_K")) c->no_split_k = std::atoi(e);
   if (const char* e = std::getenv("CGGM_NO_VEC_EPI")) c->no_vec_epi = std::atoi(e);
   if (const char* e = std::getenv("CGGM_MID_TILE")) c->mid_tile = std::atoi(e);
   if (const char* e = std::getenv("CGGM_LEAF_SWEEP")) c->leaf_sweep = std::atoi(e);
@@ -809,6 +810,16 @@ struct Fuse {
 };
 constexpr int64_t GT_CHUNK = 2048;
 
+// split-k for W Sigma when the 128x128 grid fills its last wave poorly and K is long (the halves
+// keep 2500+ k-steps each): wave efficiency of tiles vs 2 x tiles on num_sms SMs
+static bool split_wsigma(Ctx* c, int64_t n, int64_t q) {
+  if (c->no_split_k || q < 4096) return false;
+  const int64_t tiles = ((n + 127) / 128) * ((q + 127) / 128), S = c->num_sms;
+  if (tiles < S || tiles >= 16 * S) return false;
+  auto eff = [&](int64_t t) { return (double)t / (double)(((t + S - 1) / S) * S); };
+  return eff(2 * tiles) > eff(tiles) + 0.02;
+}
+
 template <typename T>
 static void psi_enqueue(Ctx* c, int64_t n_local, int64_t n_total, int64_t p, int64_t q, const T* Xd, int64_t ldx,
                         const T* Yd, int64_t ldy, const T* W, int64_t ldw, const T* Sg, int64_t ldsigma, const T* Syy,
@@ -820,9 +831,21 @@ static void psi_enqueue(Ctx* c, int64_t n_local, int64_t n_total, int64_t p, int
   T* E = static_cast<T*>(ws_get(c, WS_E, (size_t)ldn * q * sizeof(T)));
   {  // a4: acc = W Sigma -> R = acc / sqrt(n), E = Y + acc
     Phase ph(c, TAG_WSIGMA);
-    EpilogueT<T> e; e.out1 = R; e.ld1 = ldn; e.a1 = 1.0 / std::sqrt((double)n_total);
-    if ((GradT || fz) && !Sxy) { e.out2 = E; e.ld2 = ldn; e.a2 = 1.0; e.in2a = Yd; e.ld2a = ldy; e.b2 = 1.0; }
-    gemm(c, false, false, n_local, q, q, W, ldw, Sg, ldsigma, e, 0);
+    const bool want_e = (GradT || fz) && !Sxy;
+    if (sizeof(T) == 8 && split_wsigma(c, n_local, q)) {
+      // too few 128x128 tiles for whole waves (n = 1000, q = 20000: 8.5 waves): both k-halves of
+      // each tile as separate CTAs, partials added into a zeroed accumulator, then R and E
+      T* Acc = static_cast<T*>(ws_get(c, WS_ACC, (size_t)ldn * q * sizeof(T)));
+      CGGM_CUDA_CHECK(cudaMemsetAsync(Acc, 0, (size_t)ldn * q * sizeof(T), c->stream));
+      EpilogueT<T> e; e.out1 = Acc; e.ld1 = ldn; e.a1 = 1.0;
+      gemm(c, false, false, n_local, q, q, W, ldw, Sg, ldsigma, e, SPLIT_K2);
+      r_e_from_acc(c, n_local, q, Acc, ldn, Yd, ldy, R, ldn, want_e ? E : nullptr, ldn,
+                   1.0 / std::sqrt((double)n_total));
+    } else {
+      EpilogueT<T> e; e.out1 = R; e.ld1 = ldn; e.a1 = 1.0 / std::sqrt((double)n_total);
+      if (want_e) { e.out2 = E; e.ld2 = ldn; e.a2 = 1.0; e.in2a = Yd; e.ld2a = ldy; e.b2 = 1.0; }
+      gemm(c, false, false, n_local, q, q, W, ldw, Sg, ldsigma, e, 0);
+    }
   }
   {  // a4/a5: Psi = R^T R (mirrored), then grad_Lambda = (S_yy - Sigma) - Psi as one streaming pass
     Phase ph(c, TAG_PSI);
@@ -1189,6 +1212,7 @@ static void newton_eval_core(Ctx* c, int64_t n, int64_t p, int64_t q, const void
     ws_get(c, WS_E, (size_t)ldn * q * es);
     if (!GradT) ws_get(c, WS_GTCHUNK, (size_t)pad_ld<T>(p) * std::min<int64_t>(GT_CHUNK, q) * es);
     ws_get(c, WS_W, (size_t)ldn * q * es);
+    if (es == 8 && split_wsigma(c, n, q)) ws_get(c, WS_ACC, (size_t)ldn * q * es);
     if (c->factor_reuse) {
       ws_get(c, WS_LINV2, (size_t)pad_ld<T>(q) * q * es);
       ws_get(c, WS_TMP2, chol_tmp_elems(q) * es);

@@ -107,6 +107,7 @@ struct Ctx {
   int no_small_async = 0;
   int no_active_vec = 0;
   int act_onepass = 0;
+  int no_split_k = 0;   // CGGM_NO_SPLIT_K=1: W Sigma without the split-k grid (A/B)
   int no_vec_epi = 0;   // CGGM_NO_VEC_EPI=1: scalar GEMM epilogue everywhere (A/B)      // CGGM_ACT_ONEPASS=1: Lambda list by the single-pass look-back kernel (not the split one)    // test hook (CGGM_NO_ACTIVE_VEC=1): scalar active-set kernel only   // test hook (CGGM_NO_SMALL_ASYNC=1): direct-load small kernel only
   int no_tma3d = 0;   // test hook: 1 = always use 16-wide 2-D boxes for MN-inner operands  // test hook: 0 auto, 1 = 128x128 tiles, 2 = 64x64 tiles
   // phase profiling (CUDA events around every launch while enabled)
@@ -177,6 +178,7 @@ enum Slot {
   WS_Z,             // trsm result (n x q)
   WS_SCAL,          // small device scalars / partial-sum arrays
   WS_ACT,           // active-set per-column arrays
+  WS_ACC,           // split-k W Sigma accumulator (n x q)
   WS_COMM,          // broadcast scalars (sample sharding)
   WS_PACK0,         // packing for TMA-incompatible operands (lane 0: 0/1, lane 1: 2/3)
   WS_PACK1,
@@ -250,6 +252,9 @@ enum GemmFlags : int {
   B_KGE_N = 8,          // op(B)[k][n] == 0 for k < n
   SYM_LOWER = 16,       // M == N: compute only tiles I >= J; diagonal tiles write m >= n only
   SYM_MIRROR = 32,      // with SYM_LOWER: also write every value at its transposed position
+  SPLIT_K2 = 64,        // two CTAs per tile, each half of the k-range, out1 += a1 * partial by atomic
+                        // add (out1 must hold zeros; out2 / inputs unsupported).  Two partials added
+                        // to zero give a + b in either order: the result is deterministic
 };
 
 template <typename T>

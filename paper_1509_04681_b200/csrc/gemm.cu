@@ -70,6 +70,7 @@ struct KParams {
                  // 3-D TMA box; 0 = never (the ragged last tile uses 16-wide 2-D boxes of the second map)
   int vec;       // epilogue outputs / inputs 16-B aligned with even leading dimensions, no in1b / in2b:
                  // interior tiles take the paired (double2) epilogue
+  int ksplit;    // 1, or 2 (SPLIT_K2): CTA 2t + h computes k-half h of tile t
   Epilogue epi;
 };
 
@@ -163,7 +164,8 @@ __global__ void __maxnreg__(C::MAXREG)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int I, J;
-  tile_coords(P, blockIdx.x, I, J);
+  const int part = P.ksplit > 1 ? (int)(blockIdx.x % P.ksplit) : 0;
+  tile_coords(P, P.ksplit > 1 ? (int)(blockIdx.x / P.ksplit) : (int)blockIdx.x, I, J);
   const int m0 = I * BM, n0 = J * BN;
 
   int kbeg = 0, kend = P.K;
@@ -171,8 +173,13 @@ __global__ void __maxnreg__(C::MAXREG)
   if (P.flags & B_KGE_N) kbeg = max(kbeg, n0);
   if (P.flags & A_KLE_M) kend = min(kend, m0 + BM);
   if (P.flags & B_KLE_N) kend = min(kend, n0 + BN);
-  const int kt0 = kbeg / BK;
-  const int nkt = kend > kbeg ? (kend - kt0 * BK + BK - 1) / BK : 0;
+  int kt0 = kbeg / BK;
+  int nkt = kend > kbeg ? (kend - kt0 * BK + BK - 1) / BK : 0;
+  if (P.ksplit > 1) {   // this CTA's share of the k-tiles
+    const int per = (nkt + P.ksplit - 1) / P.ksplit;
+    kt0 += part * per;
+    nkt = max(0, min(per, nkt - part * per));
+  }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -322,6 +329,15 @@ __global__ void __maxnreg__(C::MAXREG)
   }
   __syncthreads();
   const bool diag = (P.flags & SYM_LOWER) && I == J;
+  if (P.ksplit > 1) {   // partial sum of this k-half into out1 (zeros + two partials: order-free)
+    for (int idx = threadIdx.x; idx < BM * BN; idx += NTHREADS) {
+      const int ml = idx % BM, nl = idx / BM;
+      const int m = m0 + ml, n = n0 + nl;
+      if (m >= P.M || n >= P.N) continue;
+      atomicAdd(P.epi.out1 + m + (int64_t)n * P.epi.ld1, __dmul_rn(P.epi.a1, Cs[nl * EPI_LD + ml]));
+    }
+    return;
+  }
   if (P.vec && !diag && m0 + BM <= P.M && n0 + BN <= P.N) {
     // interior tile: thread = row pair x column group, 16-B global accesses, the inputs of U
     // columns loaded before any is used (one memory round trip per U columns, not per element);
@@ -708,6 +724,7 @@ void run_cfg(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t Kef
   int grid;
   if (P.flags & SYM_LOWER) grid = P.tilesN * (P.tilesN + 1) / 2 + (P.tilesM - P.tilesN) * P.tilesN;
   else grid = P.tilesM * P.tilesN;
+  grid *= P.ksplit;
   // K-inner operand: dims {K, X}, box {16, BX}; MN-inner: dims {X, K}, box {16, 16}
   // MN-inner operand: the 3-D single-box map covers the leading multiple of 16 rows (so a box
   // never reads past the extent); a 16-wide 2-D map serves the ragged last tile
@@ -752,7 +769,7 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
   const bool mid_shape = K <= c->small_kmax && tiles64 < c->num_sms && !c->no_small_async &&
                          (reinterpret_cast<uintptr_t>(A) % 16 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0) &&
                          lda % 2 == 0 && ldb % 2 == 0;
-  if ((small_shape || mid_shape) && !aliased && c->force_tile != 1 && c->force_tile != 2) {
+  if ((small_shape || mid_shape) && !aliased && !(flags & SPLIT_K2) && c->force_tile != 1 && c->force_tile != 2) {
     KParamsS S;
     S.M = (int)M; S.N = (int)N; S.K = (int)(K > 0 ? K : 0); S.flags = flags; S.epi = epi;
     if (transA && transB) launch_small<true, true>(c, A, lda, B, ldb, S);
@@ -786,6 +803,9 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
   P.M = (int)M; P.N = (int)N; P.K = (int)(K > 0 ? K : 0);
   P.flags = flags;
   P.epi = epi;
+  P.ksplit = (flags & SPLIT_K2) ? 2 : 1;
+  if (P.ksplit > 1 && ((flags & (SYM_LOWER | SYM_MIRROR)) || epi.out2 || epi.in1a || epi.in1b || !epi.out1))
+    throw CudaError{CGGM_ERR_UNSUPPORTED, "SPLIT_K2: plain out1 only"};
   {
     auto al = [](const double* q, int64_t ld) { return !q || (reinterpret_cast<uintptr_t>(q) % 16 == 0 && ld % 2 == 0); };
     P.vec = !c->no_vec_epi && !epi.in1b && !epi.in2b && al(epi.out1, epi.ld1) && al(epi.out2, epi.ld2) &&
@@ -802,7 +822,7 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
   const double big_eff = (double)big_tiles / (double)(waves * c->num_sms);
   const bool auto_big = big_tiles >= 3 * c->num_sms || big_eff >= 0.9;
   const bool use_big = c->force_tile ? (c->force_tile == 1) : auto_big;
-  if (use_big && c->mid_tile && !(flags & SYM_LOWER)) run_cfg<CfgMid>(c, transA, transB, M, N, Keff, A, lda, B, ldb, P);
+  if (use_big && c->mid_tile && !(flags & (SYM_LOWER | SPLIT_K2))) run_cfg<CfgMid>(c, transA, transB, M, N, Keff, A, lda, B, ldb, P);
   else if (use_big) run_cfg<CfgBig>(c, transA, transB, M, N, Keff, A, lda, B, ldb, P);
   else run_cfg<CfgSmall>(c, transA, transB, M, N, Keff, A, lda, B, ldb, P);
 }

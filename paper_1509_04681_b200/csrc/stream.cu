@@ -154,6 +154,33 @@ void spmm_x_theta(Ctx* c, const T* X, int64_t ldx, int64_t n, const cggm_csc* Th
   post_launch(c, "k_spmm_x_theta");
 }
 
+// R = s * Acc, E = Y + Acc (the split-k W Sigma: Acc holds the sum of the two k-halves)
+template <typename T>
+__global__ void k_r_e_from_acc(int64_t n, int64_t q, const T* __restrict__ acc, int64_t lda,
+                               const T* __restrict__ Y, int64_t ldy, T* __restrict__ R, int64_t ldr,
+                               T* __restrict__ E, int64_t lde, double s) {
+  const int64_t j = blockIdx.y;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const T a = acc[i + j * lda];
+    R[i + j * ldr] = (T)((double)a * s);
+    if (E) E[i + j * lde] = Y[i + j * ldy] + a;
+  }
+}
+
+template <typename T>
+void r_e_from_acc(Ctx* c, int64_t n, int64_t q, const T* acc, int64_t lda, const T* Y, int64_t ldy, T* R, int64_t ldr,
+                  T* E, int64_t lde, double s) {
+  if (n == 0 || q == 0) return;
+  Prof pr(c, TAG_WSIGMA);
+  dim3 grid((unsigned)((n + 255) / 256 < 8 ? (n + 255) / 256 : 8), (unsigned)q);
+  k_r_e_from_acc<T><<<grid, 256, 0, c->stream>>>(n, q, acc, lda, Y, ldy, R, ldr, E, lde, s);
+  post_launch(c, "k_r_e_from_acc");
+}
+template void r_e_from_acc<double>(Ctx*, int64_t, int64_t, const double*, int64_t, const double*, int64_t, double*,
+                                   int64_t, double*, int64_t, double);
+template void r_e_from_acc<float>(Ctx*, int64_t, int64_t, const float*, int64_t, const float*, int64_t, float*,
+                                  int64_t, float*, int64_t, double);
+
 // ------------------------------------------------------------------ CSC checks
 // flag bits: 1 = colptr not monotone / bad ends, 2 = row out of range or not strictly increasing,
 //            4 = not symmetric (symmetric mode)
