@@ -208,6 +208,9 @@ def main():
     ap.add_argument("--impl", default="cggm", choices=["cggm", "reference"])
     ap.add_argument("--config", default="large")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--inverse", default="auto", choices=["auto", "rank0", "distributed"],
+                    help="N > 1: Sigma on rank 0 + broadcast, or the block-cyclic distributed inverse "
+                         "(NEXT-3); auto = distributed from 3 GPUs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--peak-seconds", type=float, default=2.0)
     ap.add_argument("--stream-grad-theta", action="store_true",
@@ -265,7 +268,8 @@ def main():
     ctx._check(ctx.lib.cggm_test_fp64_peak(ctx.h, args.peak_seconds, ctypes.byref(tf), ctypes.byref(ms)))
     peak_tflops = tf.value
 
-    ev = ShardedEvaluator(CudaBackend(ctx))
+    dist_inv = args.inverse == "distributed" or (args.inverse == "auto" and world >= 3)
+    ev = ShardedEvaluator(CudaBackend(ctx), distributed_inverse=dist_inv)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -467,7 +471,8 @@ def main():
             "data": "synthetic",
             "config": {"workload": args.config, "n": P.n, "p": P.p, "q": P.q, "nnz_theta": P.theta_star.nnz,
                        "nnz_lambda": P.lam_star.nnz, "lambda": P.lam_L, "point": "generating (Lambda*, Theta*)",
-                       "parallelism": f"sample-shard dp{world}" if world > 1 else "1 GPU",
+                       "parallelism": (f"sample-shard dp{world}, " + ("distributed inverse" if dist_inv else
+                                       "rank-0 inverse + split objective")) if world > 1 else "1 GPU",
                        "l2": "inputs larger than L2 (Sigma/Psi/grad_Lambda 3.2 GB each, grad_Theta 6.4 GB)",
                        "setup_syy_ms": setup_ms, "generator_s": round(t_gen, 2),
                        "grad_theta": "streamed into the active sets (not stored)" if args.stream_grad_theta

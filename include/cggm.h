@@ -185,6 +185,34 @@ cggm_status cggm_comm_destroy(cggm_ctx* ctx);
 /* rank / world of the attached communicator (0 / 1 when none). */
 cggm_status cggm_comm_info(cggm_ctx* ctx, int32_t* rank, int32_t* world);
 
+/* ---- dense building blocks (NEXT-3: the distributed factorisation composes them) -----------
+ * The paper parallelises exactly these precomputations across cores; sharded.py's
+ * DistributedInverse runs a block-cyclic factorisation and inverse of Lambda over the ranks of a
+ * process group out of these calls (every FLOP in this library's kernels, the exchanges by the
+ * caller's collectives). */
+/* C (M x N, ldc) = alpha * op(A) op(B) + beta * C in the ctx dtype (fp64: DMMA engine; fp32: FFMA
+ * engine).  op(A) = A (M x K, lda) or A^T (A is K x M); op(B) = B (K x N) or B^T (B is N x K).
+ * flags (cggm_gemm_flags): structural zeros the engine may skip -- bit0 op(A)[m][k] = 0 for k > m,
+ * bit1 op(A)[m][k] = 0 for k < m, bit2 op(B)[k][n] = 0 for k > n, bit3 op(B)[k][n] = 0 for k < n --
+ * and symmetric outputs: bit4 (M == N) lower tiles only, diagonal tiles m >= n; bit5 with bit4 also
+ * write the transposed values.  beta == 0 never reads C.  C must not alias A or B except as an
+ * exact in-place operand the engine supports (not guaranteed: treat as an error). */
+typedef enum cggm_gemm_flags {
+  CGGM_A_KLE_M = 1, CGGM_A_KGE_M = 2, CGGM_B_KLE_N = 4, CGGM_B_KGE_N = 8, CGGM_SYM_LOWER = 16, CGGM_SYM_MIRROR = 32
+} cggm_gemm_flags;
+cggm_status cggm_gemm(cggm_ctx* ctx, int32_t transA, int32_t transB, int64_t M, int64_t N, int64_t K, double alpha,
+                      const void* A, int64_t lda, const void* B, int64_t ldb, double beta, void* C, int64_t ldc,
+                      int32_t flags);
+/* Dense SPD block (q x q, lda even, lower triangle read; A is overwritten with scratch): the
+ * recursive Cholesky in full-inverse mode, X (q x q, ldx even) = L^{-1} (lower; zeros above the
+ * diagonal), logdet = 2 sum ln L_jj, is_pd / fail_col as cggm_invert_logdet (host outputs). */
+cggm_status cggm_chol_inverse_dense(cggm_ctx* ctx, int64_t q, void* A, int64_t lda, void* X, int64_t ldx,
+                                    double* logdet, int32_t* is_pd, int64_t* fail_col);
+/* S (n x n, lds): copy the strict lower triangle onto the upper (S becomes exactly symmetric). */
+cggm_status cggm_symmetrize(cggm_ctx* ctx, int64_t n, void* S, int64_t lds);
+/* Dense D (nrows x ncols, ldd) = the CSC matrix (zeros elsewhere). */
+cggm_status cggm_densify(cggm_ctx* ctx, const cggm_csc* A, void* D, int64_t ldd);
+
 /* ---- a1: sample covariances (§2.1) ----------------------------------------- */
 /* Syy (q x q, ldsyy) = Y^T Y / n_total (full symmetric), Sxy (p x q, ldsxy) = X^T Y / n_total.
  * Either output may be NULL (skipped).  X: n_local x p (ldx), Y: n_local x q (ldy).

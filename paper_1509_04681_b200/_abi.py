@@ -27,6 +27,8 @@ CGGM_F32 = 1
 CGGM_OPT_LOOKAHEAD_MIN = 0
 CGGM_OPT_GRAPHS = 1
 CGGM_OPT_FACTOR_REUSE = 2
+# cggm_gemm structural flags
+A_KLE_M, A_KGE_M, B_KLE_N, B_KGE_N, SYM_LOWER, SYM_MIRROR = 1, 2, 4, 8, 16, 32
 PROF_NTAGS = 14
 
 
@@ -62,6 +64,12 @@ SIGNATURES = {
     "cggm_comm_init": (c_i32, [c_vp, c_vp, c_i32, c_i32]),
     "cggm_comm_init_external": (c_i32, [c_vp, c_i32, c_i32, ALLREDUCE_FN, BROADCAST_FN, c_vp]),
     "cggm_comm_destroy": (c_i32, [c_vp]),
+    "cggm_gemm": (c_i32, [c_vp, c_i32, c_i32, c_i64, c_i64, c_i64, c_d, c_vp, c_i64, c_vp, c_i64, c_d, c_vp, c_i64,
+                          c_i32]),
+    "cggm_chol_inverse_dense": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, ctypes.POINTER(c_d),
+                                        ctypes.POINTER(c_i32), ctypes.POINTER(c_i64)]),
+    "cggm_symmetrize": (c_i32, [c_vp, c_i64, c_vp, c_i64]),
+    "cggm_densify": (c_i32, [c_vp, ctypes.POINTER(cggm_csc), c_vp, c_i64]),
     "cggm_comm_info": (c_i32, [c_vp, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)]),
     "cggm_ctx_create": (c_i32, [ctypes.POINTER(c_vp), c_i32, c_i32, c_vp]),
     "cggm_ctx_destroy": (c_i32, [c_vp]),

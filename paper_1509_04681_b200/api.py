@@ -164,6 +164,43 @@ class Context:
         self._check(self.lib.cggm_ctx_profile_read(self.h, ms, cnt, n))
         return {self.lib.cggm_profile_tag_name(i).decode(): (ms[i], int(cnt[i])) for i in range(n)}
 
+    # ---------------------------------------------------------------- dense building blocks
+    def cggm_gemm(self, C, A, B, transA=False, transB=False, alpha=1.0, beta=0.0, flags=0, M=None, N=None, K=None):
+        """C = alpha op(A) op(B) + beta C on column-major views (include/cggm.h cggm_gemm)."""
+        self._sync_stream()
+        M = C.shape[0] if M is None else M
+        N = C.shape[1] if N is None else N
+        if K is None:
+            K = A.shape[0] if transA else A.shape[1]
+        self._check(self.lib.cggm_gemm(self.h, int(bool(transA)), int(bool(transB)), M, N, K, float(alpha), _ptr(A),
+                                       ld_of(A), _ptr(B), ld_of(B), float(beta), _ptr(C), ld_of(C), int(flags)))
+        return C
+
+    def cggm_chol_inverse_dense(self, A, X=None):
+        """X = L^{-1} of the dense SPD block A (A's storage is overwritten); returns X, logdet, is_pd,
+        fail_col."""
+        self._sync_stream()
+        q = A.shape[0]
+        if X is None:
+            X = colmajor_empty(q, q, device=A.device, dtype=self.tdtype)
+        ld, pd, fc = ctypes.c_double(), ctypes.c_int32(), ctypes.c_int64()
+        self._check(self.lib.cggm_chol_inverse_dense(self.h, q, _ptr(A), ld_of(A), _ptr(X), ld_of(X), ctypes.byref(ld),
+                                                     ctypes.byref(pd), ctypes.byref(fc)))
+        return X, ld.value, bool(pd.value), int(fc.value)
+
+    def cggm_symmetrize(self, S):
+        self._sync_stream()
+        self._check(self.lib.cggm_symmetrize(self.h, S.shape[0], _ptr(S), ld_of(S)))
+        return S
+
+    def cggm_densify(self, A: DeviceCsc, D=None):
+        self._sync_stream()
+        if D is None:
+            D = colmajor_empty(A.nrows, A.ncols, device=A.colptr.device, dtype=self.tdtype)
+        cs = A.c_struct()
+        self._check(self.lib.cggm_densify(self.h, ctypes.byref(cs), _ptr(D), ld_of(D)))
+        return D
+
     # ---------------------------------------------------------------- sample sharding
     def comm_init(self, group=None):
         """Attach an NCCL communicator inside the library (cggm_comm_init) spanning the ranks of the

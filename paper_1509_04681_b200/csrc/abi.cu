@@ -734,6 +734,87 @@ cggm_status cggm_invert_logdet(cggm_ctx* ctx, const cggm_csc* Lambda, void* Sigm
   });
 }
 
+// ================================================================== dense building blocks (NEXT-3)
+cggm_status cggm_gemm(cggm_ctx* ctx, int32_t transA, int32_t transB, int64_t M, int64_t N, int64_t K, double alpha,
+                      const void* A, int64_t lda, const void* B, int64_t ldb, double beta, void* C, int64_t ldc,
+                      int32_t flags) {
+  return guard(ctx, [&](Ctx* c) {
+    if (M < 0 || N < 0 || K < 0) fail(CGGM_ERR_INVALID_ARG, "negative dimension");
+    if (flags & ~63) fail(CGGM_ERR_INVALID_ARG, "unknown gemm flag");
+    if (M == 0 || N == 0) return;
+    check_dense("C", C, M, N, ldc);
+    if (K > 0) {
+      check_dense("A", A, transA ? K : M, transA ? M : K, lda);
+      check_dense("B", B, transB ? N : K, transB ? K : N, ldb);
+      if (C == A || C == B) fail(CGGM_ERR_INVALID_ARG, "C aliases an operand");
+    }
+    dispatch(c, [&](auto tag) {
+      using T = decltype(tag);
+      EpilogueT<T> e; e.out1 = static_cast<T*>(C); e.ld1 = ldc; e.a1 = alpha;
+      if (beta != 0.0) { e.in1a = static_cast<const T*>(C); e.ld1a = ldc; e.b1 = beta; }
+      gemm(c, transA != 0, transB != 0, M, N, K, static_cast<const T*>(A), lda, static_cast<const T*>(B), ldb, e,
+           flags);
+    });
+  });
+}
+
+cggm_status cggm_chol_inverse_dense(cggm_ctx* ctx, int64_t q, void* A, int64_t lda, void* X, int64_t ldx,
+                                    double* logdet, int32_t* is_pd, int64_t* fail_col) {
+  return guard(ctx, [&](Ctx* c) {
+    if (q < 1) fail(CGGM_ERR_INVALID_ARG, "need q >= 1");
+    check_dense("A", A, q, q, lda);
+    check_dense("X", X, q, q, ldx);
+    if (lda % 2 || ldx % 2) fail(CGGM_ERR_INVALID_ARG, "leading dimensions must be even");
+    if (!logdet || !is_pd || !fail_col) fail(CGGM_ERR_INVALID_ARG, "null host output pointer");
+    const int64_t nleaves = n_leaves(q);
+    Scal s = scal_lane(c, 0, 8 + nleaves);
+    double* slots = s.dbl + 8;
+    init_scalars(c, s.fail, s.flag);
+    dispatch(c, [&](auto tag) {
+      using T = decltype(tag);
+      CGGM_CUDA_CHECK(cudaMemsetAsync(X, 0, (size_t)ldx * q * sizeof(T), c->stream));
+      const size_t tmp_elems = chol_tmp_elems(q);
+      T* tmp = static_cast<T*>(ws_get(c, WS_TMP, tmp_elems * sizeof(T)));
+      potrf_recursive<T>(c, ViewT<T>{static_cast<T*>(A), lda, q, q}, ViewT<T>{static_cast<T*>(X), ldx, q, q}, true,
+                         nullptr, slots, s.fail, tmp, tmp_elems);
+    });
+    sum_arrays_1(c, slots, nleaves, s.dbl);
+    char* h = static_cast<char*>(c->host_scratch);
+    chol_readback_async(c, 0, h);
+    CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    const CholResult r = chol_decode(h);
+    *logdet = r.logdet;
+    *is_pd = r.is_pd;
+    *fail_col = r.fail_col;
+  });
+}
+
+cggm_status cggm_symmetrize(cggm_ctx* ctx, int64_t n, void* S, int64_t lds) {
+  return guard(ctx, [&](Ctx* c) {
+    if (n < 0) fail(CGGM_ERR_INVALID_ARG, "negative dimension");
+    if (n == 0) return;
+    check_dense("S", S, n, n, lds);
+    dispatch(c, [&](auto tag) {
+      using T = decltype(tag);
+      symmetrize<T>(c, n, static_cast<T*>(S), lds);
+    });
+  });
+}
+
+cggm_status cggm_densify(cggm_ctx* ctx, const cggm_csc* A, void* D, int64_t ldd) {
+  return guard(ctx, [&](Ctx* c) {
+    if (!A) fail(CGGM_ERR_INVALID_ARG, "null CSC");
+    check_csc_host("A", A, A->nrows, A->ncols);
+    if (A->nrows == 0 || A->ncols == 0) return;
+    check_dense("D", D, A->nrows, A->ncols, ldd);
+    validate_csc_dev(c, A, false, "A");
+    dispatch(c, [&](auto tag) {
+      using T = decltype(tag);
+      densify_csc<T>(c, A, ViewT<T>{static_cast<T*>(D), ldd, A->nrows, A->ncols});
+    });
+  });
+}
+
 // ------------------------------------------------------------------ a6
 template <typename T>
 static ActTotals* active_enqueue(Ctx* c, int64_t p, int64_t q, const T* GradL, int64_t ldgl, const T* GradT,

@@ -19,6 +19,8 @@ void sum_arrays_1(Ctx* c, const double* a, int64_t len, double* out_dev);
 template <typename T>
 void r_e_from_acc(Ctx* c, int64_t n, int64_t q, const T* acc, int64_t lda, const T* Y, int64_t ldy, T* R, int64_t ldr,
                   T* E, int64_t lde, double s);
+template <typename T>
+void symmetrize(Ctx* c, int64_t n, T* S, int64_t ld);
 struct ActTotals {
   long long m_L, m_T, ties_L, ties_T;
   double sub_L, sub_T;

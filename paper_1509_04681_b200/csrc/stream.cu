@@ -181,6 +181,36 @@ template void r_e_from_acc<double>(Ctx*, int64_t, int64_t, const double*, int64_
 template void r_e_from_acc<float>(Ctx*, int64_t, int64_t, const float*, int64_t, const float*, int64_t, float*,
                                   int64_t, float*, int64_t, double);
 
+// S[j][i] = S[i][j] for i > j: 32 x 32 tiles of the lower triangle through shared memory, so both
+// the read of the lower tile and the write of its transpose are coalesced
+template <typename T>
+__global__ void k_symmetrize(int64_t n, T* S, int64_t ld) {
+  __shared__ T tile[32][33];
+  const int64_t bi = blockIdx.x, bj = blockIdx.y;   // source tile: rows 32 bi.., cols 32 bj..
+  if (bi < bj) return;
+  const int tx = threadIdx.x, ty = threadIdx.y;      // 32 x 8 threads
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t i = bi * 32 + tx, j = bj * 32 + r;
+    tile[r][tx] = (i < n && j < n) ? S[i + j * ld] : T(0);
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t i = bj * 32 + tx, j = bi * 32 + r;   // destination (row i, col j) = source (j, i)
+    if (i < n && j < n && j > i) S[i + j * ld] = tile[tx][r];
+  }
+}
+
+template <typename T>
+void symmetrize(Ctx* c, int64_t n, T* S, int64_t ld) {
+  if (n <= 1) return;
+  const unsigned nt = (unsigned)((n + 31) / 32);
+  Prof pr(c, TAG_MISC);
+  k_symmetrize<T><<<dim3(nt, nt), dim3(32, 8), 0, c->stream>>>(n, S, ld);
+  post_launch(c, "k_symmetrize");
+}
+template void symmetrize<double>(Ctx*, int64_t, double*, int64_t);
+template void symmetrize<float>(Ctx*, int64_t, float*, int64_t);
+
 // ------------------------------------------------------------------ CSC checks
 // flag bits: 1 = colptr not monotone / bad ends, 2 = row out of range or not strictly increasing,
 //            4 = not symmetric (symmetric mode)

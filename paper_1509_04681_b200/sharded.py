@@ -23,7 +23,7 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-__all__ = ["shard_rows", "flat", "ShardedEvaluator", "CudaBackend", "CollectiveEvaluator"]
+__all__ = ["shard_rows", "flat", "ShardedEvaluator", "CudaBackend", "CollectiveEvaluator", "DistributedInverse"]
 
 
 def shard_rows(n: int, world: int, rank: int) -> tuple[int, int]:
@@ -77,18 +77,39 @@ class CudaBackend:
     def objective_partial(self, X, Y, Lam, Theta, lam_L, lam_T, penalize_diag, n_total):
         return self.ctx.cggm_objective(X, Y, Lam, Theta, lam_L, lam_T, penalize_diag, n_total=n_total)
 
+    # dense building blocks (DistributedInverse)
+    def zeros(self, rows, cols):
+        from .api import colmajor_empty
+        return colmajor_empty(rows, cols, device=torch.device("cuda", self.ctx.device), dtype=self.ctx.tdtype, zero=True)
+
+    def densify(self, Lam):
+        return self.ctx.cggm_densify(Lam)
+
+    def chol_inverse(self, D):
+        return self.ctx.cggm_chol_inverse_dense(D)
+
+    def gemm(self, C, A, B, transA=False, transB=False, alpha=1.0, beta=0.0, flags=0):
+        return self.ctx.cggm_gemm(C, A, B, transA=transA, transB=transB, alpha=alpha, beta=beta, flags=flags)
+
+    def symmetrize(self, S):
+        return self.ctx.cggm_symmetrize(S)
+
 
 class ShardedEvaluator:
     """One Newton-iteration evaluation with the rows of X, Y split over the process group."""
 
-    def __init__(self, backend, group=None, replicate_inverse: bool = False, split_objective: bool = True):
+    def __init__(self, backend, group=None, replicate_inverse: bool = False, split_objective: bool = True,
+                 distributed_inverse: bool = False, block: int = 2048):
         self.b = backend
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.replicate_inverse = replicate_inverse
+        # NEXT-3: Sigma by the block-cyclic factorisation over all ranks (every rank ends with Sigma)
+        self.dist_inv = DistributedInverse(backend, block=block, group=group) if (
+            distributed_inverse and self.world > 1 and not replicate_inverse) else None
         self.split = split_objective and self.world > 1 and not replicate_inverse
-        self.obj_rank = 1 if self.split else None
+        self.obj_rank = (self.world - 1 if self.dist_inv is not None else 1) if self.split else None
         self.X_full = self.Y_full = None
 
     def _allreduce(self, t):
@@ -147,14 +168,19 @@ class ShardedEvaluator:
     def evaluate(self, X_r, Y_r, Lam, Theta, lam_L, lam_T, penalize_diag=True, tie_eps=1e-9):
         n = self.n_total
         q = Lam.nrows
-        # Sigma = Lambda^{-1}: rank 0 factors and broadcasts (or every rank, replicate_inverse)
-        if self.world == 1 or self.replicate_inverse or self.rank == 0:
+        # Sigma = Lambda^{-1}: rank 0 factors and broadcasts (or every rank, replicate_inverse; or
+        # all ranks together, distributed_inverse)
+        if self.dist_inv is not None:
+            Sigma, logdet, pd, fc = self.dist_inv.invert(Lam)
+            if Sigma is None:
+                Sigma = self.b.empty_sigma(q, Y_r)
+        elif self.world == 1 or self.replicate_inverse or self.rank == 0:
             Sigma, logdet, pd, fc = self.b.invert_logdet(Lam)
         else:
             Sigma, logdet, pd, fc = self.b.empty_sigma(q, Y_r), None, None, None
         if self.split:
             self._ob_split = self._objective_split(Lam, Theta, lam_L, lam_T, penalize_diag, Sigma)
-        if self.world > 1 and not self.replicate_inverse:
+        if self.world > 1 and not self.replicate_inverse and self.dist_inv is None:
             dist.broadcast(flat(Sigma), src=0, group=self.group)
             meta = torch.tensor([logdet if logdet is not None else 0.0, float(bool(pd)), float(fc or 0)],
                                 dtype=torch.float64, device=Sigma.device)
@@ -212,3 +238,137 @@ class CollectiveEvaluator:
         return dict(Sigma=Sigma, logdet=logdet, is_pd=pd, fail_col=fc, Psi=r["Psi"], GradL=r["GradL"],
                     GradT=r["GradT"], active=act, f=ob["f"], g=ob["g"], obj_logdet=ob["logdet"],
                     tr_syy_lam=ob["tr_syy_lam"], tr_sxy_theta=ob["tr_sxy_theta"], tr_sigma_m=ob["tr_sigma_m"])
+
+
+# ------------------------------------------------------------------ NEXT-3: distributed inverse
+class DistributedInverse:
+    """Sigma = Lambda^{-1}, log|Lambda| and the PD test with the q^3 work split over the ranks of a
+    process group (the paper parallelises these precomputations).
+
+    Block-cyclic 1-D distribution of b-wide column blocks (block k on rank k mod G):
+      1. right-looking blocked Cholesky: the owner of block k factors its diagonal block into
+         X_kk = L_kk^{-1} (cggm_chol_inverse_dense: the recursive GEMM-rich factorisation), forms
+         the panel L_{>k,k} = A_{>k,k} X_kk^T and broadcasts (X_kk, panel, log-det, PD flag); every
+         rank applies the panel to the trailing block columns it owns (A_jj.. -= L_j,k L_jk^T);
+      2. L^{-1} by owned column blocks: X_JJ = X_kk, then block forward substitution
+         X_mJ = X_mm R_m, R_{>m} -= L_{>m,m} X_mJ over the panels every rank received in step 1;
+      3. Sigma's lower column blocks Sigma_{>=J,J} = X_{>=J,>=J}^T X_{>=J,J} (the k-range starts at
+         the row block: X is lower triangular), gathered and mirrored.
+    Per rank (4/3) q^3 / G flop (+ the owners' b^3 diagonal blocks); exchanged: the panels (q^2/2),
+    L^{-1} (q^2/2) and Sigma (q^2/2).  Every flop runs in the backend's kernels (libcggm for
+    CudaBackend); the exchanges are torch.distributed broadcasts.
+
+    backend: zeros(r, c), densify(Lam), chol_inverse(D) -> (X, logdet, is_pd, fail_col),
+    gemm(C, A, B, transA, transB, alpha, beta, flags), symmetrize(S).
+    """
+
+    A_KLE_M, A_KGE_M, B_KLE_N, B_KGE_N = 1, 2, 4, 8
+
+    def __init__(self, backend, block: int = 2048, group=None):
+        self.b = backend
+        self.block = int(block)
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.host = dist.is_initialized() and dist.get_backend(group) == "gloo"
+
+    def _bcast(self, t, src):
+        """Broadcast the (possibly strided) view t from group rank src into t on every rank."""
+        if self.world == 1:
+            return t
+        gsrc = dist.get_global_rank(self.group, src) if self.group is not None else src
+        buf = t.contiguous() if self.rank == src else torch.empty(t.shape, dtype=t.dtype, device=t.device)
+        if self.host:
+            h = buf.cpu()
+            dist.broadcast(h, src=gsrc, group=self.group)
+            buf = h.to(t.device)
+        else:
+            dist.broadcast(buf, src=gsrc, group=self.group)
+        if self.rank != src:
+            t.copy_(buf)
+        return t
+
+    def invert(self, Lam, want_sigma=True):
+        q = Lam.nrows
+        b, G, me = self.block, self.world, self.rank
+        blocks = [(k0, min(q, k0 + b)) for k0 in range(0, q, b)]
+        K = len(blocks)
+        owned = [k for k in range(K) if k % G == me]
+        A = self.b.densify(Lam)                 # working copy; panels overwrite their block columns
+        Xd = [None] * K
+        logdet, fail = 0.0, -1
+        scal = [None] * K
+
+        def factor(k):   # owner of block k: X_kk, panel into A's block column, (log-det, PD, column)
+            c0, c1 = blocks[k]
+            bk = c1 - c0
+            D = self.b.zeros(bk, bk)
+            D.copy_(A[c0:c1, c0:c1])
+            X_, ld_k, pd_k, fc_k = self.b.chol_inverse(D)
+            Xd[k] = X_
+            scal[k] = torch.tensor([ld_k, float(pd_k), float(fc_k)], dtype=torch.float64, device=X_.device)
+            if c1 < q and pd_k:
+                P = self.b.zeros(q - c1, bk)
+                self.b.gemm(P, A[c1:, c0:c1], X_, transB=True, flags=self.B_KLE_N)   # L_{>k,k} = A_{>k,k} X_kk^T
+                A[c1:, c0:c1].copy_(P)
+
+        def update(j, k):   # block column j (owned) -= panel k's contribution
+            c1 = blocks[k][1]
+            d0, d1 = blocks[j]
+            P = A[c1:, blocks[k][0]:c1]
+            self.b.gemm(A[d0:, d0:d1], P[d0 - c1:], P[d0 - c1:d1 - c1], transB=True, alpha=-1.0, beta=1.0)
+
+        if me == 0 % G:
+            factor(0)
+        for k, (c0, c1) in enumerate(blocks):
+            o, bk = k % G, c1 - c0
+            if me != o:
+                Xd[k] = self.b.zeros(bk, bk)
+                scal[k] = torch.zeros(3, dtype=torch.float64, device=Xd[k].device)
+            self._bcast(scal[k], o)
+            if scal[k][1] < 0.5:
+                fail = c0 + int(scal[k][2])
+                break
+            logdet += float(scal[k][0])
+            self._bcast(Xd[k], o)
+            if c1 == q:
+                continue
+            self._bcast(A[c1:, c0:c1], o)
+            # lookahead: the next block's owner applies this panel to that block and factors it
+            # before its other trailing updates, so the next panel's broadcast is not held up
+            if me == (k + 1) % G:
+                update(k + 1, k)
+                factor(k + 1)
+            for j in owned:
+                if j > k and not (j == k + 1 and me == (k + 1) % G):
+                    update(j, k)
+        if fail >= 0:
+            return None, float("nan"), False, fail
+        if not want_sigma:
+            return None, logdet, True, -1
+        # 2. L^{-1}, owned column blocks (X_JJ, then forward substitution over the panels)
+        X = self.b.zeros(q, q)
+        for J in owned:
+            j0, j1 = blocks[J]
+            X[j0:j1, j0:j1].copy_(Xd[J])
+            if j1 == q:
+                continue
+            R = self.b.zeros(q - j1, j1 - j0)
+            self.b.gemm(R, A[j1:, j0:j1], Xd[J], alpha=-1.0, flags=self.B_KGE_N)   # -L_{>J,J} X_JJ
+            for m in range(J + 1, K):
+                m0, m1 = blocks[m]
+                Xm = X[m0:m1, j0:j1]
+                self.b.gemm(Xm, Xd[m], R[m0 - j1:m1 - j1], flags=self.A_KLE_M)       # X_mJ = X_mm R_m
+                if m1 < q:
+                    self.b.gemm(R[m1 - j1:], A[m1:, m0:m1], Xm, alpha=-1.0, beta=1.0)
+        for J, (j0, j1) in enumerate(blocks):
+            self._bcast(X[j0:, j0:j1], J % G)
+        # 3. Sigma's lower column blocks, gathered, mirrored
+        S = self.b.zeros(q, q)
+        for J in owned:
+            j0, j1 = blocks[J]
+            self.b.gemm(S[j0:, j0:j1], X[j0:, j0:], X[j0:, j0:j1], transA=True, flags=self.A_KGE_M)
+        for J, (j0, j1) in enumerate(blocks):
+            self._bcast(S[j0:, j0:j1], J % G)
+        self.b.symmetrize(S)
+        return S, logdet, True, -1

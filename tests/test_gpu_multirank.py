@@ -21,7 +21,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, name, split, q_out):
+def _worker(rank, world, port, name, split, q_out, distributed=False):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -36,7 +36,7 @@ def _worker(rank, world, port, name, split, q_out):
         a, b = shard_rows(P.n, world, rank)
         X, Y = to_device_colmajor(P.X[a:b]), to_device_colmajor(P.Y[a:b])
         ctx = Context(0)
-        ev = ShardedEvaluator(CudaBackend(ctx), split_objective=split)
+        ev = ShardedEvaluator(CudaBackend(ctx), split_objective=split, distributed_inverse=distributed, block=128)
         ev.setup(X, Y, P.n)
         r = ev.evaluate(X, Y, DeviceCsc.from_host(lam), DeviceCsc.from_host(th), P.lam_L, P.lam_T, True)
         torch.cuda.synchronize()
@@ -48,15 +48,16 @@ def _worker(rank, world, port, name, split, q_out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,split", [("small", True), ("small", False), ("tiny", True)])
-def test_two_ranks_match_oracle(name, split):
+@pytest.mark.parametrize("name,split,distributed", [("small", True, False), ("small", False, False), ("tiny", True, False),
+                                                    ("small", True, True), ("small", False, True)])
+def test_two_ranks_match_oracle(name, split, distributed):
     import torch.multiprocessing as mp
     from oracle import cggm_oracle as O
     from synth.cggm_inputs import make_problem
     ctx = mp.get_context("spawn")
     qo = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, split, qo)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, split, qo, distributed)) for r in range(2)]
     for p in procs:
         p.start()
     res = qo.get(timeout=600)

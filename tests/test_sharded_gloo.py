@@ -53,7 +53,18 @@ class OracleBackend:
         return O.objective(X.numpy(), Y.numpy(), Lam, Theta, lam_L, lam_T, penalize_diag, n_total=n_total)
 
 
-def _worker(rank, world, port, name, k, q_out, split=True):
+class OracleBackendBlocks(OracleBackend):
+    """OracleBackend plus the dense building blocks the distributed inverse (NEXT-3) composes."""
+
+    def __init__(self):
+        from tests.test_distributed_inverse import OracleBlocks
+        self._blk = OracleBlocks()
+
+    def __getattr__(self, name):
+        return getattr(self._blk, name)
+
+
+def _worker(rank, world, port, name, k, q_out, split=True, distributed=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -63,7 +74,8 @@ def _worker(rank, world, port, name, k, q_out, split=True):
         _, lam, th = P.points[k]
         a, b = shard_rows(P.n, world, rank)
         X, Y = col(P.X[a:b]), col(P.Y[a:b])
-        ev = ShardedEvaluator(OracleBackend(), split_objective=split)
+        ev = ShardedEvaluator(OracleBackendBlocks() if distributed else OracleBackend(), split_objective=split,
+                              distributed_inverse=distributed, block=16)
         ev.setup(X, Y, P.n)
         r = ev.evaluate(X, Y, lam, th, P.lam_L, P.lam_T, True)
         if rank == 0:
@@ -82,15 +94,17 @@ def free_port():
     return p
 
 
-@pytest.mark.parametrize("name,k,world,split", [("tiny", 1, 2, True), ("small", 1, 2, True), ("tiny", 1, 2, False),
-                                                ("tiny", 1, 3, True)])
-def test_sharded_matches_unsharded_oracle(name, k, world, split):
-    """split: rank 1 evaluates the objective on the gathered full data while rank 0 inverts;
-    otherwise every rank contributes partial traces of its own rows."""
+@pytest.mark.parametrize("name,k,world,split,distributed", [("tiny", 1, 2, True, False), ("small", 1, 2, True, False),
+                                                            ("tiny", 1, 2, False, False), ("tiny", 1, 3, True, False),
+                                                            ("tiny", 1, 2, True, True), ("tiny", 1, 3, False, True)])
+def test_sharded_matches_unsharded_oracle(name, k, world, split, distributed):
+    """split: the objective rank evaluates the objective on the gathered full data while Sigma is
+    formed (by rank 0, or by all ranks with the distributed inverse); otherwise every rank
+    contributes partial traces of its own rows."""
     ctx = mp.get_context("spawn")
     qo = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, name, k, qo, split)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, k, qo, split, distributed)) for r in range(world)]
     for p in procs:
         p.start()
     res = qo.get(timeout=300)
