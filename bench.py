@@ -269,7 +269,7 @@ def main():
     peak_tflops = tf.value
 
     dist_inv = args.inverse == "distributed" or (args.inverse == "auto" and world >= 3)
-    ev = ShardedEvaluator(CudaBackend(ctx), distributed_inverse=dist_inv)
+    ev = ShardedEvaluator(CudaBackend(ctx), distributed_inverse=dist_inv, split_objective=not dist_inv)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -471,7 +471,7 @@ def main():
             "data": "synthetic",
             "config": {"workload": args.config, "n": P.n, "p": P.p, "q": P.q, "nnz_theta": P.theta_star.nnz,
                        "nnz_lambda": P.lam_star.nnz, "lambda": P.lam_L, "point": "generating (Lambda*, Theta*)",
-                       "parallelism": (f"sample-shard dp{world}, " + ("distributed inverse" if dist_inv else
+                       "parallelism": (f"sample-shard dp{world}, " + ("distributed inverse and trial factorisation" if dist_inv else
                                        "rank-0 inverse + split objective")) if world > 1 else "1 GPU",
                        "l2": "inputs larger than L2 (Sigma/Psi/grad_Lambda 3.2 GB each, grad_Theta 6.4 GB)",
                        "setup_syy_ms": setup_ms, "generator_s": round(t_gen, 2),

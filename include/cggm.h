@@ -213,6 +213,18 @@ cggm_status cggm_symmetrize(cggm_ctx* ctx, int64_t n, void* S, int64_t lds);
 /* Dense D (nrows x ncols, ldd) = the CSC matrix (zeros elsewhere). */
 cggm_status cggm_densify(cggm_ctx* ctx, const cggm_csc* A, void* D, int64_t ldd);
 
+/* The line-search objective (as cggm_objective) at a Lambda whose inverse Cholesky factor the caller
+ * already holds: Linv (q x q, lower) = L^{-1} with Lambda = L L^T and logdet = log|Lambda| (e.g. from
+ * DistributedInverse's factorisation of the trial Lambda).  tr(Sigma Theta^T S_xx Theta) is
+ * ||W Linv^T||_F^2 / n_total (one triangular GEMM), the other terms as cggm_objective; is_pd = 1,
+ * fail_col = -1 (the caller's factorisation is the PD test).  With n_local < n_total the three data
+ * traces are this shard's partial sums (all-reduced when a communicator is attached). */
+cggm_status cggm_objective_given_inverse(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64_t p, int64_t q,
+                                         const void* X, int64_t ldx, const void* Y, int64_t ldy,
+                                         const cggm_csc* Lambda, const cggm_csc* Theta, double lam_L, double lam_T,
+                                         int32_t penalize_diag, const void* W, int64_t ldw, const void* Linv,
+                                         int64_t ldlinv, double logdet, cggm_objective_out* out);
+
 /* ---- a1: sample covariances (§2.1) ----------------------------------------- */
 /* Syy (q x q, ldsyy) = Y^T Y / n_total (full symmetric), Sxy (p x q, ldsxy) = X^T Y / n_total.
  * Either output may be NULL (skipped).  X: n_local x p (ldx), Y: n_local x q (ldy).

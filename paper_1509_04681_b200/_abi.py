@@ -69,6 +69,9 @@ SIGNATURES = {
     "cggm_chol_inverse_dense": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, ctypes.POINTER(c_d),
                                         ctypes.POINTER(c_i32), ctypes.POINTER(c_i64)]),
     "cggm_symmetrize": (c_i32, [c_vp, c_i64, c_vp, c_i64]),
+    "cggm_objective_given_inverse": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64,
+                                             ctypes.POINTER(cggm_csc), ctypes.POINTER(cggm_csc), c_d, c_d, c_i32,
+                                             c_vp, c_i64, c_vp, c_i64, c_d, ctypes.POINTER(cggm_objective_out)]),
     "cggm_densify": (c_i32, [c_vp, ctypes.POINTER(cggm_csc), c_vp, c_i64]),
     "cggm_comm_info": (c_i32, [c_vp, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)]),
     "cggm_ctx_create": (c_i32, [ctypes.POINTER(c_vp), c_i32, c_i32, c_vp]),

@@ -429,6 +429,22 @@ class Context:
 
 
     # ---------------------------------------------------------------- NEXT-1 / NEXT-2
+    def cggm_objective_given_inverse(self, X, Y, Lam: DeviceCsc, Theta: DeviceCsc, lam_L, lam_T, Linv, logdet,
+                                     penalize_diag=True, W=None, n_total=None):
+        """The objective with the caller's L^{-1} and log-det (include/cggm.h)."""
+        self._sync_stream()
+        n, q = Y.shape
+        p = Theta.nrows
+        n_total = n if n_total is None else n_total
+        o = _abi.cggm_objective_out()
+        ls, ts = Lam.c_struct(), Theta.c_struct()
+        self._check(self.lib.cggm_objective_given_inverse(
+            self.h, n, n_total, p, q, _ptr(X), ld_of(X) if X is not None else 1, _ptr(Y), ld_of(Y), ctypes.byref(ls),
+            ctypes.byref(ts), float(lam_L), float(lam_T), int(bool(penalize_diag)), _ptr(W),
+            ld_of(W) if W is not None else 1, _ptr(Linv), ld_of(Linv), float(logdet), ctypes.byref(o)))
+        return dict(f=o.f, g=o.g, logdet=o.logdet, tr_syy_lam=o.tr_syy_lam, tr_sxy_theta=o.tr_sxy_theta,
+                    tr_sigma_m=o.tr_sigma_m, pen_L=o.pen_L, pen_T=o.pen_T, is_pd=bool(o.is_pd), fail_col=int(o.fail_col))
+
     def cggm_gram(self, X, n_total=None, Sxx=None):
         """S_xx = X^T X / n (p x p), for the Theta sweep."""
         self._sync_stream()

@@ -1218,6 +1218,87 @@ cggm_status cggm_objective(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int6
   });
 }
 
+cggm_status cggm_objective_given_inverse(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64_t p, int64_t q,
+                                         const void* X, int64_t ldx, const void* Y, int64_t ldy,
+                                         const cggm_csc* Lambda, const cggm_csc* Theta, double lam_L, double lam_T,
+                                         int32_t penalize_diag, const void* W, int64_t ldw, const void* Linv,
+                                         int64_t ldlinv, double logdet, cggm_objective_out* out) {
+  return guard(ctx, [&](Ctx* c) {
+    if (!out) fail(CGGM_ERR_INVALID_ARG, "null cggm_objective_out");
+    if (n_local < 0 || p < 0 || q < 0) fail(CGGM_ERR_INVALID_ARG, "negative dimension");
+    if (n_total < 1 || n_total < n_local) fail(CGGM_ERR_INVALID_ARG, "n_total must be >= max(1, n_local)");
+    if (!(lam_L >= 0.0) || !(lam_T >= 0.0)) fail(CGGM_ERR_INVALID_ARG, "negative lambda");
+    check_dense("Y", Y, n_local, q, ldy);
+    check_csc_host("Lambda", Lambda, q, q);
+    check_csc_host("Theta", Theta, p, q);
+    check_dense("Linv", Linv, q, q, ldlinv);
+    if (W) check_dense("W", W, n_local, q, ldw);
+    else check_dense("X", X, n_local, p, ldx);
+    std::memset(out, 0, sizeof(*out));
+    if (q == 0) {
+      out->is_pd = 1; out->fail_col = -1;
+      return;
+    }
+    validate_csc_dev(c, Lambda, true, "Lambda");
+    validate_csc_dev(c, Theta, false, "Theta");
+    Scal s = scal_lane(c, 0, 16 + 5 * q);
+    double* res = s.dbl;
+    double* partY = s.dbl + 16;
+    double* partWY = partY + q;
+    double* partZ = partWY + q;
+    double* penLp = partZ + q;
+    double* penTp = penLp + q;
+    dispatch(c, [&](auto tag) {
+      using T = decltype(tag);
+      const int64_t ldn = pad_ld<T>(n_local > 0 ? n_local : 1);
+      const T* Wd;
+      int64_t ldwd;
+      if (W) {
+        Wd = static_cast<const T*>(W);
+        ldwd = ldw;
+      } else {
+        T* Wb = static_cast<T*>(ws_get(c, WS_W, (size_t)ldn * q * sizeof(T)));
+        spmm_x_theta<T>(c, static_cast<const T*>(X), ldx, n_local, Theta, ViewT<T>{Wb, ldn, n_local, q});
+        Wd = Wb;
+        ldwd = ldn;
+      }
+      T* Z = static_cast<T*>(ws_get(c, WS_Z, (size_t)ldn * q * sizeof(T)));
+      {  // Z = W Linv^T (Linv lower: op(B)[k][j] = Linv[j][k] vanishes for k > j)
+        Phase ph(c, TAG_TRSM);
+        EpilogueT<T> e; e.out1 = Z; e.ld1 = ldn;
+        if (n_local > 0) gemm(c, false, true, n_local, q, q, Wd, ldwd, static_cast<const T*>(Linv), ldlinv, e, B_KLE_N);
+      }
+      Phase ph(c, TAG_OBJRED);
+      const T* Yd = static_cast<const T*>(Y);
+      col_partials<T>(c, 0, n_local, q, Yd, ldy, nullptr, 0, Lambda, partY);
+      col_partials<T>(c, 1, n_local, q, Wd, ldwd, Yd, ldy, nullptr, partWY);
+      col_partials<T>(c, 2, n_local, q, Z, ldn, nullptr, 0, nullptr, partZ);
+      csc_abs_partials<T>(c, Lambda, penalize_diag == 0, penLp);
+      csc_abs_partials<T>(c, Theta, false, penTp);
+      sum_arrays_1(c, partY, q, res + 1);
+      sum_arrays_1(c, partWY, q, res + 2);
+      sum_arrays_1(c, partZ, q, res + 3);
+      sum_arrays_1(c, penLp, q, res + 4);
+      sum_arrays_1(c, penTp, q, res + 5);
+    });
+    comm_allreduce(c, res + 1, 3, 0);
+    double v[6];
+    CGGM_CUDA_CHECK(cudaMemcpyAsync(v, res, 6 * 8, cudaMemcpyDeviceToHost, c->stream));
+    CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    const double nt = (double)n_total;
+    out->pen_L = lam_L * v[4];
+    out->pen_T = lam_T * v[5];
+    out->is_pd = 1;
+    out->fail_col = -1;
+    out->logdet = logdet;
+    out->tr_syy_lam = v[1] / nt;
+    out->tr_sxy_theta = v[2] / nt;
+    out->tr_sigma_m = v[3] / nt;
+    out->g = -logdet + out->tr_syy_lam + 2.0 * out->tr_sxy_theta + out->tr_sigma_m;
+    out->f = out->g + out->pen_L + out->pen_T;
+  });
+}
+
 // ------------------------------------------------------------------ composite evaluation
 // One Newton-iteration evaluation (the bench's unit): the objective's fresh trial Cholesky runs on
 // the auxiliary stream, overlapped with Sigma = Lambda^{-1} and the Psi / gradient / active-set

@@ -77,6 +77,10 @@ class CudaBackend:
     def objective_partial(self, X, Y, Lam, Theta, lam_L, lam_T, penalize_diag, n_total):
         return self.ctx.cggm_objective(X, Y, Lam, Theta, lam_L, lam_T, penalize_diag, n_total=n_total)
 
+    def objective_given_inverse_partial(self, X, Y, Lam, Theta, lam_L, lam_T, penalize_diag, n_total, Linv, logdet):
+        return self.ctx.cggm_objective_given_inverse(X, Y, Lam, Theta, lam_L, lam_T, Linv, logdet,
+                                                     penalize_diag=penalize_diag, n_total=n_total)
+
     # dense building blocks (DistributedInverse)
     def zeros(self, rows, cols):
         from .api import colmajor_empty
@@ -195,6 +199,24 @@ class ShardedEvaluator:
             # the objective rank evaluated the whole objective on all rows (see _objective_split)
             ob = self._ob_split
             parts = torch.tensor([ob["tr_syy_lam"], ob["tr_sxy_theta"], ob["tr_sigma_m"]], dtype=torch.float64)
+        elif self.dist_inv is not None:
+            # the trial factorisation distributed too: L^{-1} gathered, each rank's partial traces
+            Linv, ld_t, pd_t, fc_t = self.dist_inv.invert(Lam, want_sigma=False, want_linv=True)
+            if pd_t:
+                ob = self.b.objective_given_inverse_partial(X_r, Y_r, Lam, Theta, lam_L, lam_T, penalize_diag, n,
+                                                            Linv, ld_t)
+            else:
+                ob = dict(is_pd=False, fail_col=fc_t, logdet=float("nan"), tr_syy_lam=0.0, tr_sxy_theta=0.0,
+                          tr_sigma_m=0.0, pen_L=0.0, pen_T=0.0)
+            parts = torch.tensor([ob["tr_syy_lam"], ob["tr_sxy_theta"], ob["tr_sigma_m"]], dtype=torch.float64,
+                                 device=Psi.device)
+            if self.world > 1:
+                if dist.get_backend(self.group) == "gloo":
+                    h = parts.cpu()
+                    dist.all_reduce(h, group=self.group)
+                    parts = h
+                else:
+                    dist.all_reduce(parts, group=self.group)
         else:
             ob = self.b.objective_partial(X_r, Y_r, Lam, Theta, lam_L, lam_T, penalize_diag, n)
             parts = torch.tensor([ob["tr_syy_lam"], ob["tr_sxy_theta"], ob["tr_sigma_m"]], dtype=torch.float64,
@@ -288,7 +310,8 @@ class DistributedInverse:
             t.copy_(buf)
         return t
 
-    def invert(self, Lam, want_sigma=True):
+    def invert(self, Lam, want_sigma=True, want_linv=False):
+        """(Sigma, logdet, is_pd, fail_col); want_linv: return the gathered L^{-1} instead of Sigma."""
         q = Lam.nrows
         b, G, me = self.block, self.world, self.rank
         blocks = [(k0, min(q, k0 + b)) for k0 in range(0, q, b)]
@@ -344,7 +367,7 @@ class DistributedInverse:
                     update(j, k)
         if fail >= 0:
             return None, float("nan"), False, fail
-        if not want_sigma:
+        if not want_sigma and not want_linv:
             return None, logdet, True, -1
         # 2. L^{-1}, owned column blocks (X_JJ, then forward substitution over the panels)
         X = self.b.zeros(q, q)
@@ -363,6 +386,8 @@ class DistributedInverse:
                     self.b.gemm(R[m1 - j1:], A[m1:, m0:m1], Xm, alpha=-1.0, beta=1.0)
         for J, (j0, j1) in enumerate(blocks):
             self._bcast(X[j0:, j0:j1], J % G)
+        if want_linv:
+            return X, logdet, True, -1
         # 3. Sigma's lower column blocks, gathered, mirrored
         S = self.b.zeros(q, q)
         for J in owned:

@@ -132,3 +132,23 @@ def test_distributed_inverse_cuda_non_pd():
         assert p.exitcode == 0
     for _, S, ld, pd, fc in res:
         assert not pd and fc == fail_at and S is None
+
+
+def test_objective_given_inverse_matches_objective(ctx):
+    """cggm_objective_given_inverse with L^{-1} and log|Lambda| from cggm_chol_inverse_dense equals
+    cggm_objective (its own factorisation) and the oracle."""
+    from paper_1509_04681_b200 import DeviceCsc, to_device_colmajor
+    from synth.cggm_inputs import make_problem
+    P = make_problem("small")
+    _, lam, th = P.points[1]
+    X, Y = to_device_colmajor(P.X), to_device_colmajor(P.Y)
+    L, T = DeviceCsc.from_host(lam), DeviceCsc.from_host(th)
+    a = ctx.cggm_objective(X, Y, L, T, P.lam_L, P.lam_T)
+    D = ctx.cggm_densify(L)
+    Linv, ld, pd, _ = ctx.cggm_chol_inverse_dense(D)
+    assert pd
+    b = ctx.cggm_objective_given_inverse(X, Y, L, T, P.lam_L, P.lam_T, Linv, ld)
+    ref = O.objective(P.X, P.Y, lam, th, P.lam_L, P.lam_T)
+    for k in ("f", "g", "tr_syy_lam", "tr_sxy_theta", "tr_sigma_m", "pen_L", "pen_T", "logdet"):
+        assert b[k] == pytest.approx(a[k], rel=1e-12), k
+        assert b[k] == pytest.approx(ref[k], rel=1e-10), k

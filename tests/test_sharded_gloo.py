@@ -63,6 +63,14 @@ class OracleBackendBlocks(OracleBackend):
     def __getattr__(self, name):
         return getattr(self._blk, name)
 
+    def objective_given_inverse_partial(self, X, Y, Lam, Theta, lam_L, lam_T, penalize_diag, n_total, Linv, logdet):
+        """The shard's objective terms with tr(Sigma M) from the caller's (gathered) L^{-1}."""
+        ob = dict(O.objective(X.numpy(), Y.numpy(), Lam, Theta, lam_L, lam_T, penalize_diag, n_total=n_total))
+        Z = O.spmm_x_theta(X.numpy(), Theta) @ Linv.numpy().T
+        ob["tr_sigma_m"] = float(np.sum(Z * Z)) / n_total
+        ob["logdet"] = logdet
+        return ob
+
 
 def _worker(rank, world, port, name, k, q_out, split=True, distributed=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
