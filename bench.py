@@ -98,7 +98,7 @@ class ClockSampler:
         except subprocess.TimeoutExpired:
             self.proc.kill()
             out, _ = self.proc.communicate()
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, pw = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
             parts = [x.strip() for x in line.split(",")]
@@ -109,6 +109,10 @@ class ClockSampler:
                 mx = float(parts[2])
             except ValueError:
                 continue
+            try:
+                pw.append(float(parts[3]))
+            except ValueError:
+                pass
             for nm, v in zip(names, parts[5:9]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
@@ -116,7 +120,26 @@ class ClockSampler:
             return None
         loaded = [s for s in sm if mx is None or s > 0.5 * mx] or sm
         return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "power_w_median": statistics.median(pw) if pw else None}
+
+
+def run_env():
+    """GPU / driver / CUDA / host description for the JSON line (SURVEY.md §8(d) timing protocol)."""
+    import torch
+    env = {"gpu": torch.cuda.get_device_name(0), "torch": torch.__version__, "cuda_runtime": torch.version.cuda}
+    try:
+        out = subprocess.run(["nvidia-smi", "--query-gpu=driver_version", "--format=csv,noheader"],
+                             capture_output=True, text=True, timeout=20).stdout.strip().splitlines()
+        env["driver"] = out[0] if out else None
+    except (OSError, subprocess.TimeoutExpired):
+        env["driver"] = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            env["cpu_model"] = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), None)
+    except OSError:
+        env["cpu_model"] = None
+    env["host_cores"] = os.cpu_count()
+    return env
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) leg
@@ -333,6 +356,25 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed = float(t.item())
 
+    # ---------------- per-step distribution (after region A, which it does not perturb): each step
+    # bracketed by its own events, at least 10 steps (median with p10 / p90)
+    n_dist = max(10, args.steps)
+    ev_pairs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_dist)]
+    for a_, b_ in ev_pairs:
+        a_.record(stream)
+        step()
+        b_.record(stream)
+    torch.cuda.synchronize()
+    per_step = sorted(a_.elapsed_time(b_) for a_, b_ in ev_pairs)
+    q10 = per_step[max(0, int(round(0.1 * (n_dist - 1))))]
+    q90 = per_step[min(n_dist - 1, int(round(0.9 * (n_dist - 1))))]
+    step_dist = {"n": n_dist, "median_ms": statistics.median(per_step), "p10_ms": q10, "p90_ms": q90,
+                 "min_ms": per_step[0], "max_ms": per_step[-1]}
+    if world > 1:
+        t = torch.tensor([step_dist["median_ms"]], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_dist["median_ms_max_over_ranks"] = float(t.item())
+
     # ---------------- secondary: the factor-reuse evaluation: the accepted trial's
     # inverse factor seeds the next Sigma (CGGM_OPT_FACTOR_REUSE; here the trial Lambda is the
     # evaluation's Lambda, as for the accepted unit step of a converging line search)
@@ -478,6 +520,8 @@ def main():
                        "grad_theta": "streamed into the active sets (not stored)" if args.stream_grad_theta
                        else "stored (p x q)"},
             "clocks": clk,
+            "step_ms_distribution": step_dist,
+            "env": run_env(),
             "gpu_launches": launches,
             "roofline": {"bound": "tensor", "kernel": "gemm_dmma_kernel (FP64 DMMA.8x8x4, all dense contractions)",
                          "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
