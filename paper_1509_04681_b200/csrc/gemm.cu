@@ -389,20 +389,28 @@ __global__ void __maxnreg__(C::MAXREG)
   }
   if (P.flags & SYM_MIRROR) {
     if (P.vec && !diag && m0 + BM <= P.M && n0 + BN <= P.N && !P.epi.in1a && !P.epi.in2a) {
-      // transposed copy: thread = output row pair (nl, nl + 1) x output-column group
-      constexpr int RP = BN / 2, CG = NTHREADS / RP, NCOL = BM / CG;
+      // transposed copy: lane l of a warp reads row nl = nb + l of the staged tile at columns ml and
+      // ml + 1 (consecutive lanes 129 doubles apart: conflict-free), then lane pairs swap one value
+      // so that the even lane stores (nl, nl + 1) of output column ml and the odd lane those of
+      // column ml + 1, 16 bytes each, contiguous along the output rows
+      constexpr int NWARPS = NTHREADS / 32, NBLK = BN / 32, GROUPS = NWARPS / NBLK, PAIRS = BM / 2 / GROUPS;
+      static_assert(NWARPS % NBLK == 0 && (BM / 2) % GROUPS == 0, "mirror epilogue warp layout");
       const Epilogue& E = P.epi;
-      const int nl = 2 * (threadIdx.x % RP), cg = threadIdx.x / RP;
-      const int64_t n = n0 + nl;
+      const int wv = threadIdx.x >> 5, ln = threadIdx.x & 31;
+      const int nl = 32 * (wv % NBLK) + ln, grp = wv / NBLK;
+      const bool odd = ln & 1;
+      const int64_t n = n0 + nl - (odd ? 1 : 0);
 #pragma unroll 4
-      for (int i = 0; i < NCOL; ++i) {
-        const int ml = cg + CG * i;
-        const int64_t m = m0 + ml;
-        const double v0 = Cs[nl * EPI_LD + ml], v1 = Cs[(nl + 1) * EPI_LD + ml];
+      for (int i = 0; i < PAIRS; ++i) {
+        const int ml = 2 * (grp + GROUPS * i);
+        const double a = Cs[nl * EPI_LD + ml], b = Cs[nl * EPI_LD + ml + 1];
+        const double pa = __shfl_xor_sync(0xffffffffu, a, 1), pb = __shfl_xor_sync(0xffffffffu, b, 1);
+        const double lo = odd ? pb : a, hi = odd ? b : pa;   // rows (n, n + 1) of output column m
+        const int64_t m = m0 + ml + (odd ? 1 : 0);
         if (E.out1)
-          *reinterpret_cast<double2*>(E.out1 + n + m * E.ld1) = make_double2(__dmul_rn(E.a1, v0), __dmul_rn(E.a1, v1));
+          *reinterpret_cast<double2*>(E.out1 + n + m * E.ld1) = make_double2(__dmul_rn(E.a1, lo), __dmul_rn(E.a1, hi));
         if (E.out2)
-          *reinterpret_cast<double2*>(E.out2 + n + m * E.ld2) = make_double2(__dmul_rn(E.a2, v0), __dmul_rn(E.a2, v1));
+          *reinterpret_cast<double2*>(E.out2 + n + m * E.ld2) = make_double2(__dmul_rn(E.a2, lo), __dmul_rn(E.a2, hi));
       }
     } else {
       for (int idx = threadIdx.x; idx < BM * BN; idx += NTHREADS) {
