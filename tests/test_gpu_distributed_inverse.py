@@ -152,3 +152,26 @@ def test_objective_given_inverse_matches_objective(ctx):
     for k in ("f", "g", "tr_syy_lam", "tr_sxy_theta", "tr_sigma_m", "pen_L", "pen_T", "logdet"):
         assert b[k] == pytest.approx(a[k], rel=1e-12), k
         assert b[k] == pytest.approx(ref[k], rel=1e-10), k
+
+
+def test_building_block_errors_and_non_pd(ctx):
+    """Argument errors of the building blocks are reported before any launch; a non-PD block is not
+    an error (is_pd = 0 and the first failing column, reading A10)."""
+    from paper_1509_04681_b200 import to_device_colmajor
+    from paper_1509_04681_b200.api import CggmError, colmajor_empty
+    C = colmajor_empty(64, 64)
+    with pytest.raises(CggmError) as e:
+        ctx.cggm_gemm(C, C, C)                      # output aliases an operand
+    assert e.value.status == 1
+    with pytest.raises(CggmError) as e:
+        ctx.cggm_gemm(C, C, C, flags=1 << 7)        # unknown flag
+    assert e.value.status == 1
+    A = random_spd(97, 4)
+    L, _, _ = O.cholesky(A)
+    A[50, 50] = float(np.dot(L[50, :50], L[50, :50])) - 1.0
+    X, ld, pd, fc = ctx.cggm_chol_inverse_dense(to_device_colmajor(A))
+    assert not pd and fc == 50
+    odd = torch.zeros((97, 97), dtype=torch.float64, device="cuda").t()   # ld 97: odd
+    with pytest.raises(CggmError) as e:
+        ctx.cggm_chol_inverse_dense(odd)
+    assert e.value.status == 1
