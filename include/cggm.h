@@ -361,6 +361,21 @@ cggm_status cggm_newton_eval_host(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q
                                   void* GradL, int64_t ldgl, void* GradT, int64_t ldgt, cggm_active_out* active,
                                   cggm_eval_out* out);
 
+/* ---- NEXT-4: memory-bounded evaluation ------------------------------------------------------
+ * One Newton-iteration evaluation at (Lambda, Theta) without storing Sigma, Psi or grad_Lambda
+ * (the paper's block mode, P:555-595 / P:671-825, with triangular products of the GPU factor in
+ * place of CG): the q x q memory is the factorisation's (dense Lambda, freed after, and L^{-1});
+ * Sigma, Psi and the gradients exist only as b-wide column blocks (block = 0: 2048) consumed by the
+ * active-set compaction.  Outputs as cggm_newton_eval without the dense matrices: log-det / PD,
+ * the active lists and counts (active, two-call CGGM_ERR_CAPACITY pattern), the subgradient
+ * statistic, and the objective at the same Lambda from the same factor (out->obj; a line-search
+ * trial is a separate cggm_objective).  X (n x p), Y (n x q) device, n_total = n.  Flops:
+ * factorisation (2/3) q^3 + Sigma blocks q^3 (two passes) + 3 n q^2 + 2 n p q. */
+cggm_status cggm_newton_eval_blocked(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, const void* X, int64_t ldx,
+                                     const void* Y, int64_t ldy, const cggm_csc* Lambda, const cggm_csc* Theta,
+                                     int64_t block, cggm_active_out* active, cggm_eval_out* out);
+
+
 #ifdef __cplusplus
 }
 #endif

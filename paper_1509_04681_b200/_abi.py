@@ -101,6 +101,9 @@ SIGNATURES = {
                                  ctypes.POINTER(cggm_csc), ctypes.POINTER(cggm_csc), c_vp, c_i64, c_vp, c_i64,
                                  c_vp, c_i64, c_vp, c_i64, ctypes.POINTER(cggm_active_out),
                                  ctypes.POINTER(cggm_eval_out)]),
+    "cggm_newton_eval_blocked": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, ctypes.POINTER(cggm_csc),
+                                         ctypes.POINTER(cggm_csc), c_i64, ctypes.POINTER(cggm_active_out),
+                                         ctypes.POINTER(cggm_eval_out)]),
     "cggm_newton_eval_host": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, ctypes.POINTER(cggm_csc),
                                       ctypes.POINTER(cggm_csc), c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
                                       c_vp, c_i64, ctypes.POINTER(cggm_active_out), ctypes.POINTER(cggm_eval_out)]),

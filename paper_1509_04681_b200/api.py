@@ -548,6 +548,31 @@ class Context:
 
 
 
+    def cggm_newton_eval_blocked(self, X, Y, Lam: DeviceCsc, Theta: DeviceCsc, lam_L, lam_T, penalize_diag=True,
+                                 tie_eps=1e-9, block=0, bufs=None):
+        """NEXT-4: the evaluation without dense Sigma / Psi / gradients (include/cggm.h); bufs holds the
+        active-list buffers (L_row, L_col, T_row, T_col; two-call pattern: last_active_sizes)."""
+        self._sync_stream()
+        n, p = X.shape
+        q = Y.shape[1]
+        bufs = bufs if bufs is not None else {}
+        spec = dict(lam_L=lam_L, lam_T=lam_T, penalize_diag=int(bool(penalize_diag)), tie_eps=tie_eps,
+                    L_row=bufs.get("L_row"), L_col=bufs.get("L_col"), T_row=bufs.get("T_row"), T_col=bufs.get("T_col"))
+        ao = self._active_struct(spec)
+        eo = _abi.cggm_eval_out()
+        ls, ts = Lam.c_struct(), Theta.c_struct()
+        self.last_active_sizes = None
+        st = self.lib.cggm_newton_eval_blocked(self.h, n, p, q, _ptr(X), ld_of(X), _ptr(Y), ld_of(Y),
+                                               ctypes.byref(ls), ctypes.byref(ts), int(block), ctypes.byref(ao),
+                                               ctypes.byref(eo))
+        self.last_active_sizes = (int(ao.m_L), int(ao.m_T))
+        self._check(st)
+        o = eo.obj
+        ob = dict(f=o.f, g=o.g, logdet=o.logdet, tr_syy_lam=o.tr_syy_lam, tr_sxy_theta=o.tr_sxy_theta,
+                  tr_sigma_m=o.tr_sigma_m, pen_L=o.pen_L, pen_T=o.pen_T, is_pd=bool(o.is_pd), fail_col=int(o.fail_col))
+        return dict(logdet=eo.logdet, is_pd=bool(eo.is_pd), fail_col=int(eo.fail_col),
+                    active=self._active_result(ao, spec), objective=ob)
+
     def cggm_newton_eval_host(self, Xh, Yh, Lam: HostCsc, Theta: HostCsc, lam_L, lam_T, penalize_diag=True,
                               tie_eps=1e-9, bufs=None, Syy=None):
         """cggm_newton_eval from host buffers (column-major CPU tensors, HostCsc): uploads overlap the

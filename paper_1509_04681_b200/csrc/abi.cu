@@ -1579,6 +1579,190 @@ static void newton_eval_core(Ctx* c, int64_t n, int64_t p, int64_t q, const void
   active_decode(at, active);
 }
 
+// ------------------------------------------------------------------ NEXT-4: memory-bounded evaluation
+// The evaluation without any q x q matrix besides the factorisation's (the
+// paper's block mode P:555-595, with triangular products of the GPU factor in place of
+// CG): L^{-1} from the recursive full-inverse factorisation, then column blocks C of width b --
+// pass 1: Sigma_C = L^{-T} L^{-1}_C (two GEMMs: the rows above C dense, the rows from C with the
+// triangular k-range), R_C = W Sigma_C / sqrt n and E_C = Y_C + W Sigma_C (one GEMM, two
+// epilogues), grad_Theta_C = (2/n) X^T E_C into its active-set chunk; pass 2 (R complete):
+// grad_Lambda rows 0..j of each column j of C = Y^T Y_C / n - R^T R_C - Sigma[0:j1, C] into its
+// active-set chunk.  The objective reuses L^{-1}: tr(Sigma M) = ||W L^{-T}||^2 / n.
+template <typename T>
+static void newton_eval_blocked_impl(Ctx* c, int64_t n, int64_t p, int64_t q, const T* Xd, int64_t ldx, const T* Yd,
+                                     int64_t ldy, const cggm_csc* Lambda, const cggm_csc* Theta, int64_t b,
+                                     cggm_active_out* active, cggm_eval_out* out) {
+  const int64_t ldq = pad_ld<T>(q), ldn = pad_ld<T>(n), ldp = pad_ld<T>(std::max<int64_t>(p, 1));
+  const int64_t nleaves = n_leaves(q);
+  // 1. L^{-1}, log-det, PD
+  T* Xl = static_cast<T*>(ws_get(c, WS_LINV, (size_t)ldq * q * sizeof(T)));
+  {
+    T* A = static_cast<T*>(ws_get(c, WS_DENSE_A, (size_t)ldq * q * sizeof(T)));
+    Scal s = scal_lane(c, 0, 8 + nleaves);
+    double* slots = s.dbl + 8;
+    densify_csc(c, Lambda, ViewT<T>{A, ldq, q, q});
+    init_scalars(c, s.fail, s.flag);
+    CGGM_CUDA_CHECK(cudaMemsetAsync(Xl, 0, (size_t)ldq * q * sizeof(T), c->stream));
+    const size_t tmp_elems = chol_tmp_elems(q);
+    T* tmp = static_cast<T*>(ws_get(c, WS_TMP, tmp_elems * sizeof(T)));
+    potrf_recursive<T>(c, ViewT<T>{A, ldq, q, q}, ViewT<T>{Xl, ldq, q, q}, true, nullptr, slots, s.fail, tmp,
+                       tmp_elems);
+    sum_arrays_1(c, slots, nleaves, s.dbl);
+  }
+  char* h = static_cast<char*>(c->host_scratch);
+  chol_readback_async(c, 0, h);
+  CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  const CholResult cr = chol_decode(h);
+  out->logdet = cr.logdet;
+  out->is_pd = cr.is_pd;
+  out->fail_col = cr.fail_col;
+  // the dense copy of Lambda is no longer needed: give its memory back before the block passes
+  {
+    Buffer& bA = c->slots[WS_DENSE_A];
+    if (bA.ptr) {
+      CGGM_CUDA_CHECK(cudaFree(bA.ptr));
+      bA = Buffer{};
+      c->ws_generation++;
+    }
+  }
+  if (!cr.is_pd) {
+    out->obj.is_pd = 0;
+    out->obj.fail_col = cr.fail_col;
+    out->obj.f = out->obj.g = INFINITY;
+    active->m_L = active->m_T = active->ties_L = active->ties_T = 0;
+    active->subgrad_l1 = 0.0;
+    return;
+  }
+  // 2. W = X Theta; R, E (n x q)
+  T* W = static_cast<T*>(ws_get(c, WS_W, (size_t)ldn * q * sizeof(T)));
+  T* R = static_cast<T*>(ws_get(c, WS_R, (size_t)ldn * q * sizeof(T)));
+  T* E = static_cast<T*>(ws_get(c, WS_E, (size_t)ldn * q * sizeof(T)));
+  spmm_x_theta<T>(c, Xd, ldx, n, Theta, ViewT<T>{W, ldn, n, q});
+  T* SigC = static_cast<T*>(ws_get(c, WS_BLK_S, (size_t)ldq * b * sizeof(T)));
+  T* GLC = static_cast<T*>(ws_get(c, WS_BLK_G, (size_t)ldq * b * sizeof(T)));
+  T* GTC = static_cast<T*>(ws_get(c, WS_GTCHUNK, (size_t)ldp * b * sizeof(T)));
+  ActWs aws = active_ws(c, q);
+  active_begin(c, q, aws);
+  const double rs = 1.0 / std::sqrt((double)n);
+  // pass 1
+  for (int64_t j0 = 0; j0 < q; j0 += b) {
+    const int64_t bc = std::min<int64_t>(b, q - j0);
+    {  // Sigma_C: rows [0, j0) dense, rows [j0, q) with the k-range starting at the row block
+      Phase ph(c, TAG_LAUUM);
+      EpilogueT<T> e; e.out1 = SigC; e.ld1 = ldq;
+      if (j0 > 0) gemm(c, true, false, j0, bc, q - j0, Xl + j0, ldq, Xl + j0 + j0 * ldq, ldq, e, 0);
+      EpilogueT<T> e2; e2.out1 = SigC + j0; e2.ld1 = ldq;
+      gemm(c, true, false, q - j0, bc, q - j0, Xl + j0 + j0 * ldq, ldq, Xl + j0 + j0 * ldq, ldq, e2, A_KGE_M);
+    }
+    {  // R_C = W Sigma_C / sqrt n, E_C = Y_C + W Sigma_C
+      Phase ph(c, TAG_WSIGMA);
+      EpilogueT<T> e; e.out1 = R + j0 * ldn; e.ld1 = ldn; e.a1 = rs;
+      e.out2 = E + j0 * ldn; e.ld2 = ldn; e.a2 = 1.0; e.in2a = Yd + j0 * ldy; e.ld2a = ldy; e.b2 = 1.0;
+      gemm(c, false, false, n, bc, q, W, ldn, SigC, ldq, e, 0);
+    }
+    if (p > 0) {  // grad_Theta_C = (2/n) X^T E_C and its active-set chunk
+      Phase ph(c, TAG_GRADT);
+      EpilogueT<T> e; e.out1 = GTC; e.ld1 = ldp; e.a1 = 2.0 / (double)n;
+      gemm(c, true, false, p, bc, n, Xd, ldx, E + j0 * ldn, ldn, e, 0);
+      active_theta_chunk<T>(c, p, j0, bc, GTC, ldp, Theta, active->lam_T, active->tie_eps, aws, active->T_row,
+                            active->T_col, active->cap_T);
+    }
+  }
+  // pass 2: grad_Lambda rows 0..j1 of block C = S_yy - Sigma - Psi, its active-set chunk
+  for (int64_t j0 = 0; j0 < q; j0 += b) {
+    const int64_t bc = std::min<int64_t>(b, q - j0), j1 = j0 + bc;
+    Phase ph(c, TAG_GRADL);
+    {
+      EpilogueT<T> e; e.out1 = GLC; e.ld1 = ldq; e.a1 = 1.0 / (double)n;
+      gemm(c, true, false, j1, bc, n, Yd, ldy, Yd + j0 * ldy, ldy, e, 0);                 // S_yy[0:j1, C]
+    }
+    {
+      EpilogueT<T> e; e.out1 = GLC; e.ld1 = ldq; e.a1 = -1.0; e.in1a = GLC; e.ld1a = ldq; e.b1 = 1.0;
+      gemm(c, true, false, j1, bc, q - j0, Xl + j0, ldq, Xl + j0 + j0 * ldq, ldq, e, 0);  // - Sigma[0:j1, C]
+    }
+    {
+      EpilogueT<T> e; e.out1 = GLC; e.ld1 = ldq; e.a1 = -1.0; e.in1a = GLC; e.ld1a = ldq; e.b1 = 1.0;
+      gemm(c, true, false, j1, bc, n, R, ldn, R + j0 * ldn, ldn, e, 0);                     // - Psi[0:j1, C]
+    }
+    active_lambda_chunk<T>(c, q, j0, bc, GLC, ldq, Lambda, active->lam_L, active->penalize_diag, active->tie_eps,
+                           aws, active->L_row, active->L_col, active->cap_L);
+  }
+  active_end(c, q, aws);
+  // 4. objective at Lambda with the same factor: tr(Sigma M) = ||W L^{-T}||^2 / n
+  T* Z = static_cast<T*>(ws_get(c, WS_Z, (size_t)ldn * q * sizeof(T)));
+  {
+    Phase ph(c, TAG_TRSM);
+    EpilogueT<T> e; e.out1 = Z; e.ld1 = ldn;
+    gemm(c, false, true, n, q, q, W, ldn, Xl, ldq, e, B_KLE_N);
+  }
+  Scal s2 = scal_lane(c, 1, 16 + 5 * q);
+  double* res = s2.dbl;
+  double* partY = res + 16;
+  double* partWY = partY + q;
+  double* partZ = partWY + q;
+  double* penLp = partZ + q;
+  double* penTp = penLp + q;
+  {
+    Phase ph(c, TAG_OBJRED);
+    col_partials<T>(c, 0, n, q, Yd, ldy, nullptr, 0, Lambda, partY);
+    col_partials<T>(c, 1, n, q, W, ldn, Yd, ldy, nullptr, partWY);
+    col_partials<T>(c, 2, n, q, Z, ldn, nullptr, 0, nullptr, partZ);
+    csc_abs_partials<T>(c, Lambda, active->penalize_diag == 0, penLp);
+    csc_abs_partials<T>(c, Theta, false, penTp);
+    sum_arrays_1(c, partY, q, res + 1);
+    sum_arrays_1(c, partWY, q, res + 2);
+    sum_arrays_1(c, partZ, q, res + 3);
+    sum_arrays_1(c, penLp, q, res + 4);
+    sum_arrays_1(c, penTp, q, res + 5);
+  }
+  CGGM_CUDA_CHECK(cudaMemcpyAsync(h + 256, aws.tot, sizeof(ActTotals), cudaMemcpyDeviceToHost, c->stream));
+  CGGM_CUDA_CHECK(cudaMemcpyAsync(h + 512, res, 6 * 8, cudaMemcpyDeviceToHost, c->stream));
+  CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  double v[6];
+  std::memcpy(v, h + 512, 6 * 8);
+  const double nt = (double)n;
+  cggm_objective_out& o = out->obj;
+  o.is_pd = 1;
+  o.fail_col = -1;
+  o.logdet = cr.logdet;
+  o.pen_L = active->lam_L * v[4];
+  o.pen_T = active->lam_T * v[5];
+  o.tr_syy_lam = v[1] / nt;
+  o.tr_sxy_theta = v[2] / nt;
+  o.tr_sigma_m = v[3] / nt;
+  o.g = -o.logdet + o.tr_syy_lam + 2.0 * o.tr_sxy_theta + o.tr_sigma_m;
+  o.f = o.g + o.pen_L + o.pen_T;
+  ActTotals at;
+  std::memcpy(&at, h + 256, sizeof(ActTotals));
+  active_decode(at, active);
+}
+
+cggm_status cggm_newton_eval_blocked(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, const void* X, int64_t ldx,
+                                     const void* Y, int64_t ldy, const cggm_csc* Lambda, const cggm_csc* Theta,
+                                     int64_t block, cggm_active_out* active, cggm_eval_out* out) {
+  return guard(ctx, [&](Ctx* c) {
+    if (!out) fail(CGGM_ERR_INVALID_ARG, "null cggm_eval_out");
+    if (c->comm.world > 1) fail(CGGM_ERR_UNSUPPORTED, "the memory-bounded evaluation is single-GPU");
+    if (n < 1 || p < 0 || q < 1) fail(CGGM_ERR_INVALID_ARG, "need n >= 1, q >= 1, p >= 0");
+    if (block < 0) fail(CGGM_ERR_INVALID_ARG, "negative block width");
+    check_dense("X", X, n, p, ldx);
+    check_dense("Y", Y, n, q, ldy);
+    check_csc_host("Lambda", Lambda, q, q);
+    check_csc_host("Theta", Theta, p, q);
+    check_active_args(active);
+    std::memset(out, 0, sizeof(*out));
+    validate_csc_dev(c, Lambda, true, "Lambda");
+    validate_csc_dev(c, Theta, false, "Theta");
+    int64_t b = block > 0 ? block : 2048;
+    b = std::min<int64_t>((b + 1) & ~int64_t(1), q);
+    dispatch(c, [&](auto tag) {
+      using T = decltype(tag);
+      newton_eval_blocked_impl<T>(c, n, p, q, static_cast<const T*>(X), ldx, static_cast<const T*>(Y), ldy, Lambda,
+                                  Theta, b, active, out);
+    });
+  });
+}
+
 cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, const void* X, int64_t ldx,
                              const void* Y, int64_t ldy, const void* Syy, int64_t ldsyy, const cggm_csc* Lambda,
                              const cggm_csc* Theta, void* Sigma, int64_t ldsigma, void* Psi, int64_t ldpsi,

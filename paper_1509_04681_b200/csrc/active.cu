@@ -126,9 +126,11 @@ __global__ void __launch_bounds__(NT) k_active_onepass(int64_t nrows, const T* _
     const T x = val[t];
     if (x == T(0)) continue;
     const int64_t i = rowidx[t];
+    if (LAM && i > j) continue;   // lower entries: counted twice from their mirror (symmetric Lambda, gradient)
     const T gv = gc[i];
     const T lm = lam_of<LAM>(i, j, lam, penalize_diag);
-    s += (double)fabs(gv + lm * (x > T(0) ? T(1) : T(-1))) - (double)fmax(fabs(gv) - lm, T(0));
+    const double wt = (LAM && i < j) ? 2.0 : 1.0;
+    s += wt * ((double)fabs(gv + lm * (x > T(0) ? T(1) : T(-1))) - (double)fmax(fabs(gv) - lm, T(0)));
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -314,10 +316,14 @@ __global__ void __launch_bounds__(NT, LAM ? CGGM_ACT_LAM_MINB : 4) k_active_vec(
   for (int64_t t = colptr[j] + threadIdx.x; t < colptr[j + 1]; t += NT) {
     const T x = val[t];
     if (x == T(0)) continue;
-    const int64_t i = rowidx[t];   // every stored entry of the column, both triangles for Lambda
+    const int64_t i = rowidx[t];
+    // Lambda: entries below the diagonal are counted twice from their mirror in the upper triangle
+    // (Lambda and its gradient are exactly symmetric), so only rows <= j of the gradient are read
+    if (LAM && i > j) continue;
     const T gi = gc[i];
     const T lm = lam_of<LAM>(i, j, lam, penalize_diag);
-    sacc += (double)fabs(gi + lm * (x > T(0) ? T(1) : T(-1))) - (double)fmax(fabs(gi) - lm, T(0));
+    const double wt = (LAM && i < j) ? 2.0 : 1.0;
+    sacc += wt * ((double)fabs(gi + lm * (x > T(0) ? T(1) : T(-1))) - (double)fmax(fabs(gi) - lm, T(0)));
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -501,9 +507,11 @@ __device__ __forceinline__ void k_lam_flags_col(const T* __restrict__ G, int64_t
     const T x = val[t];
     if (x == T(0)) continue;
     const int64_t i = rowidx[t];
+    if (i > j) continue;   // counted twice from the mirror (symmetric)
     const T gi = gc[i];
     const T lm = lam_of<true>(i, j, lam, penalize_diag);
-    sacc += (double)fabs(gi + lm * (x > T(0) ? T(1) : T(-1))) - (double)fmax(fabs(gi) - lm, T(0));
+    const double wt = i < j ? 2.0 : 1.0;
+    sacc += wt * ((double)fabs(gi + lm * (x > T(0) ? T(1) : T(-1))) - (double)fmax(fabs(gi) - lm, T(0)));
   }
   long long tcl = tc;
 #pragma unroll
@@ -769,6 +777,32 @@ void active_lambda(Ctx* c, int64_t q, const T* GradL, int64_t ldgl, const cggm_c
   post_launch(c, "k_active_onepass<L>");
 }
 
+// Lambda list for columns [col0, col0 + ncols) from a gradient block G whose column j - col0 holds
+// rows 0..j of column j (the memory-bounded evaluation forms grad_Lambda block by block); chunks in
+// ascending column order, chained by the same decoupled look-back as the whole-matrix kernel
+template <typename T>
+void active_lambda_chunk(Ctx* c, int64_t q, int64_t col0, int64_t ncols, const T* G, int64_t ldg,
+                         const cggm_csc* Lambda, double lam_L, int penalize_diag, double tie_eps, const ActWs& ws,
+                         int32_t* L_row, int32_t* L_col, long long capL) {
+  if (ncols == 0) return;
+  Prof pr(c, TAG_ACTIVE);
+  if (vec_ok(G, ldg, c->no_active_vec)) {
+    const size_t bv = smem_bytes_vec(q);
+    set_smem(k_active_vec<true, T>, bv);
+    k_active_vec<true, T><<<(unsigned)ncols, NT, bv, c->stream>>>(
+        q, G, ldg, Lambda->colptr, Lambda->rowidx, static_cast<const T*>(Lambda->val), (T)lam_L, penalize_diag,
+        (T)tie_eps, ws.stateL, L_row, L_col, capL, ws.tieL, ws.subL, col0);
+    post_launch(c, "k_active_vec<L> chunk");
+    return;
+  }
+  const size_t bl = smem_bytes(q);
+  set_smem(k_active_onepass<true, T>, bl);
+  k_active_onepass<true, T><<<(unsigned)ncols, NT, bl, c->stream>>>(
+      q, G, ldg, Lambda->colptr, Lambda->rowidx, static_cast<const T*>(Lambda->val), (T)lam_L, penalize_diag,
+      (T)tie_eps, ws.stateL, L_row, L_col, capL, ws.tieL, ws.subL, col0);
+  post_launch(c, "k_active_onepass<L> chunk");
+}
+
 template <typename T>
 void active_theta_chunk(Ctx* c, int64_t p, int64_t col0, int64_t ncols, const T* G, int64_t ldg,
                         const cggm_csc* Theta, double lam_T, double tie_eps, const ActWs& ws, int32_t* T_row,
@@ -820,6 +854,8 @@ template void active_compact<float>(Ctx*, int64_t, int64_t, const float*, int64_
 #define CGGM_INST(T)                                                                                          \
   template void active_lambda<T>(Ctx*, int64_t, const T*, int64_t, const cggm_csc*, double, int, double,      \
                                  const ActWs&, int32_t*, int32_t*, long long);                                 \
+  template void active_lambda_chunk<T>(Ctx*, int64_t, int64_t, int64_t, const T*, int64_t, const cggm_csc*,    \
+                                       double, int, double, const ActWs&, int32_t*, int32_t*, long long);      \
   template void active_theta_chunk<T>(Ctx*, int64_t, int64_t, int64_t, const T*, int64_t, const cggm_csc*,     \
                                       double, double, const ActWs&, int32_t*, int32_t*, long long);
 CGGM_INST(double)

@@ -179,6 +179,8 @@ enum Slot {
   WS_SCAL,          // small device scalars / partial-sum arrays
   WS_ACT,           // active-set per-column arrays
   WS_ACC,           // split-k W Sigma accumulator (n x q)
+  WS_BLK_S,         // memory-bounded evaluation: a Sigma column block (q x b)
+  WS_BLK_G,         // memory-bounded evaluation: a grad_Lambda column block (q x b)
   WS_COMM,          // broadcast scalars (sample sharding)
   WS_PACK0,         // packing for TMA-incompatible operands (lane 0: 0/1, lane 1: 2/3)
   WS_PACK1,

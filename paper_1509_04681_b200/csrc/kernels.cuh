@@ -44,6 +44,10 @@ void active_lambda(Ctx* c, int64_t q, const T* GradL, int64_t ldgl, const cggm_c
                    int penalize_diag, double tie_eps, const ActWs& ws, int32_t* L_row, int32_t* L_col,
                    long long capL);
 template <typename T>
+void active_lambda_chunk(Ctx* c, int64_t q, int64_t col0, int64_t ncols, const T* G, int64_t ldg,
+                         const cggm_csc* Lambda, double lam_L, int penalize_diag, double tie_eps, const ActWs& ws,
+                         int32_t* L_row, int32_t* L_col, long long capL);
+template <typename T>
 void active_theta_chunk(Ctx* c, int64_t p, int64_t col0, int64_t ncols, const T* G, int64_t ldg,
                         const cggm_csc* Theta, double lam_T, double tie_eps, const ActWs& ws, int32_t* T_row,
                         int32_t* T_col, long long capT);

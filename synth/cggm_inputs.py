@@ -92,6 +92,9 @@ CONFIGS = {
     "large": dict(n=1000, p=40000, q=20000, lam_kind="chain", theta_k=20, lam=0.2),
     # configs[4]: "~3 off-diagonals per row" -> 1.5q pairs (reading A17)
     "sharded": dict(n=4000, p=200000, q=40000, lam_kind="random", pairs_per_row=1.5, theta_k=25, lam=0.2),
+    # NEXT-4 demonstration (not a BASELINE config): q beyond one GPU's dense capacity (the dense
+    # evaluation's q x q matrices alone are 8 x 28.8 GB); `large`'s recipe with a sparser target
+    "block": dict(n=1000, p=20000, q=60000, lam_kind="chain", theta_k=10, lam=1.0),
 }
 
 
