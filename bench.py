@@ -183,7 +183,7 @@ def blas_threads():
         return os.cpu_count() or 1
 
 
-def cpu_baseline(P, qs=2000, ps=4000):
+def cpu_baseline(P, qs=5000, ps=10000):
     X, Y, lam_s, th_s = oracle_sample(P, qs, ps)
     secs, _ = oracle_eval_seconds(X, Y, lam_s, th_s, P.lam_L, P.lam_T)
     _, full = alg_flops(P.n, P.p, P.q, P.theta_star.nnz)
@@ -201,7 +201,7 @@ def run_reference(args):
         return
     from synth.cggm_inputs import make_problem
     P = make_problem(args.config)
-    qs, ps = 1500, 3000
+    qs, ps = 3000, 6000
     X, Y, lam_s, th_s = oracle_sample(P, qs, ps)
     _, full = alg_flops(P.n, P.p, P.q, P.theta_star.nnz)
     _, samp = alg_flops(P.n, ps, qs, th_s.nnz)
