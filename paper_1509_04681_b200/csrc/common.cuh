@@ -10,6 +10,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/cggm.h"
 
 namespace cggm {
@@ -160,11 +162,19 @@ struct Prof {
 };
 
 // scoped phase tag
+// a phase of the hot path: the tag the profiler attributes launches to, and an NVTX range of the
+// same name (visible in nsys / ncu --nvtx; a no-op without an attached tool)
 struct Phase {
   Ctx* c;
   int prev;
-  Phase(Ctx* c_, int tag) : c(c_), prev(c_->cur_tag) { c->cur_tag = tag; }
-  ~Phase() { c->cur_tag = prev; }
+  Phase(Ctx* c_, int tag) : c(c_), prev(c_->cur_tag) {
+    c->cur_tag = tag;
+    nvtxRangePushA(cggm_profile_tag_name(tag));
+  }
+  ~Phase() {
+    nvtxRangePop();
+    c->cur_tag = prev;
+  }
 };
 
 enum Slot {
