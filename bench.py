@@ -189,10 +189,23 @@ def cpu_baseline(P, qs=5000, ps=10000):
     _, full = alg_flops(P.n, P.p, P.q, P.theta_star.nnz)
     _, samp = alg_flops(P.n, ps, qs, th_s.nnz)
     est = secs * full / samp
-    return {"value": 1.0 / est, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
-            "sample": f"one oracle evaluation on the leading {qs} outputs x {ps} inputs x all {P.n} samples of "
-                      f"`large` ({secs:.2f} s), extrapolated by algorithmic flops x{full / samp:.0f}",
-            "sample_seconds": secs}
+    out = {"value": 1.0 / est, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+           "sample": f"one oracle evaluation on the leading {qs} outputs x {ps} inputs x all {P.n} samples of "
+                     f"`large` ({secs:.2f} s), extrapolated by algorithmic flops x{full / samp:.0f}",
+           "sample_seconds": secs}
+    try:   # the same oracle on one core (one thread and all cores), a smaller block
+        from threadpoolctl import threadpool_limits
+        q1, p1 = 1500, 3000
+        X1, Y1, lam1, th1 = oracle_sample(P, q1, p1)
+        with threadpool_limits(limits=1):
+            s1, _ = oracle_eval_seconds(X1, Y1, lam1, th1, P.lam_L, P.lam_T)
+        _, samp1 = alg_flops(P.n, p1, q1, th1.nnz)
+        out["single_thread"] = {"value": samp1 / full / s1, "unit": UNIT, "cores": 1, "sample_seconds": s1,
+                                "sample": f"leading {q1} outputs x {p1} inputs x all {P.n} samples, "
+                                          f"extrapolated x{full / samp1:.0f}"}
+    except ImportError:
+        pass
+    return out
 
 
 def run_reference(args):
