@@ -71,3 +71,27 @@ def test_blocked_non_pd(ctx):
                                        block=128, bufs=lists(1_000_000))
     assert not out["is_pd"] and out["fail_col"] == j
     assert out["objective"]["f"] == float("inf")
+
+
+def test_blocked_fp32_matches_dense_fp32():
+    """The FP32 variant of the memory-bounded evaluation against the FP32 dense composite (same
+    arithmetic type, reading A18): active counts and lists (outside the fp32 tie band), objective."""
+    from paper_1509_04681_b200 import Context, DeviceCsc, to_device_colmajor
+    from paper_1509_04681_b200.api import newton_evaluation
+    c32 = Context(0, dtype="f32")
+    P = make_problem("medium")
+    _, lam, th = P.points[0]
+    f32 = torch.float32
+    X, Y = to_device_colmajor(P.X, dtype=f32), to_device_colmajor(P.Y, dtype=f32)
+    L, T = DeviceCsc.from_host(lam, dtype=f32), DeviceCsc.from_host(th, dtype=f32)
+    cap = 2_000_000
+    b = c32.cggm_newton_eval_blocked(X, Y, L, T, P.lam_L, P.lam_T, tie_eps=1e-5, block=512, bufs=lists(cap))
+    Syy, _ = c32.cggm_covariances(X, Y, want_sxy=False)
+    d = newton_evaluation(c32, X, Y, Syy, L, T, P.lam_L, P.lam_T, True, lists(cap), tie_eps=1e-5)
+    assert b["is_pd"] and d["is_pd"]
+    ab, ad = b["active"], d["active"]
+    if ab["ties_L"] + ab["ties_T"] + ad["ties_L"] + ad["ties_T"] == 0:
+        assert (ab["m_L"], ab["m_T"]) == (ad["m_L"], ad["m_T"])
+        assert torch.equal(ab["T_row"], ad["T_row"]) and torch.equal(ab["T_col"], ad["T_col"])
+    assert abs(ab["m_L"] - ad["m_L"]) <= ab["ties_L"] + ad["ties_L"]
+    assert b["objective"]["f"] == pytest.approx(d["objective"]["f"], rel=1e-5)
