@@ -244,6 +244,8 @@ def main():
     ap.add_argument("--impl", default="cggm", choices=["cggm", "reference"])
     ap.add_argument("--config", default="large")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--allreduce", default="nccl", choices=["nccl", "peer"],
+                    help="N > 1: Psi / grad_Theta partials summed by NCCL or over CUDA IPC peer memory")
     ap.add_argument("--inverse", default="auto", choices=["auto", "rank0", "distributed"],
                     help="N > 1: Sigma on rank 0 + broadcast, or the block-cyclic distributed inverse "
                          "(NEXT-3); auto = distributed from 3 GPUs")
@@ -305,7 +307,8 @@ def main():
     peak_tflops = tf.value
 
     dist_inv = args.inverse == "distributed" or (args.inverse == "auto" and world >= 3)
-    ev = ShardedEvaluator(CudaBackend(ctx), distributed_inverse=dist_inv, split_objective=not dist_inv)
+    ev = ShardedEvaluator(CudaBackend(ctx), distributed_inverse=dist_inv, split_objective=not dist_inv,
+                          peer_allreduce=args.allreduce == "peer")
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -527,7 +530,7 @@ def main():
             "config": {"workload": args.config, "n": P.n, "p": P.p, "q": P.q, "nnz_theta": P.theta_star.nnz,
                        "nnz_lambda": P.lam_star.nnz, "lambda": P.lam_L, "point": "generating (Lambda*, Theta*)",
                        "parallelism": (f"sample-shard dp{world}, " + ("distributed inverse and trial factorisation" if dist_inv else
-                                       "rank-0 inverse + split objective")) if world > 1 else "1 GPU",
+                                       "rank-0 inverse + split objective") + f", {args.allreduce} all-reduce") if world > 1 else "1 GPU",
                        "l2": "inputs larger than L2 (Sigma/Psi/grad_Lambda 3.2 GB each, grad_Theta 6.4 GB)",
                        "setup_syy_ms": setup_ms, "generator_s": round(t_gen, 2),
                        "grad_theta": "streamed into the active sets (not stored)" if args.stream_grad_theta

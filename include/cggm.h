@@ -164,6 +164,22 @@ const char* cggm_version(void);
  * cggm_newton_eval / _host with world > 1 return CGGM_ERR_UNSUPPORTED (the composite overlaps
  * its steps on one GPU; sharded callers compose the collective calls above).
  * Collectives are enqueued on the ctx stream.  Failures return CGGM_ERR_NCCL. */
+/* All-reduce over peer memory (CUDA IPC; NVLink peer loads / stores between the GPUs of a node),
+ * the alternative to NCCL for the partial sums: every rank registers one symmetric buffer of the
+ * same size (cggm_ipc_get_handle on its own, cggm_ipc_open_handle on the others' handles, exchanged
+ * by the caller), its GEMM writes its partial straight into it, and after a barrier rank r sums
+ * slice r of all ranks' buffers in rank order and writes the sum into slice r of every rank's
+ * buffer (cggm_peer_allreduce; in place: each slice is read and written by its owner only); after
+ * a second barrier every buffer holds the bit-identical total.  bufs: host array of `world`
+ * device pointers (rank k's buffer at bufs[k]), count elements of the ctx dtype. */
+/* A device allocation of its own (cudaMalloc on the ctx device), so that its IPC handle covers
+ * exactly the buffer (pool sub-allocations would need an offset); freed by cggm_device_free. */
+cggm_status cggm_device_alloc(cggm_ctx* ctx, int64_t bytes, void** dev_ptr);
+cggm_status cggm_device_free(cggm_ctx* ctx, void* dev_ptr);
+cggm_status cggm_ipc_get_handle(cggm_ctx* ctx, const void* dev_ptr, char handle[64]);
+cggm_status cggm_ipc_open_handle(cggm_ctx* ctx, const char handle[64], void** dev_ptr);
+cggm_status cggm_ipc_close_handle(cggm_ctx* ctx, void* dev_ptr);
+cggm_status cggm_peer_allreduce(cggm_ctx* ctx, int32_t world, int32_t rank, void* const* bufs, int64_t count);
 /* 128-byte NCCL unique id, created on rank 0 (cggm_comm_unique_id) and sent to the other ranks by
  * the caller (e.g. a torch.distributed broadcast). */
 cggm_status cggm_comm_unique_id(char id[128]);

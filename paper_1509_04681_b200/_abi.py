@@ -64,6 +64,12 @@ SIGNATURES = {
     "cggm_comm_init": (c_i32, [c_vp, c_vp, c_i32, c_i32]),
     "cggm_comm_init_external": (c_i32, [c_vp, c_i32, c_i32, ALLREDUCE_FN, BROADCAST_FN, c_vp]),
     "cggm_comm_destroy": (c_i32, [c_vp]),
+    "cggm_device_alloc": (c_i32, [c_vp, c_i64, ctypes.POINTER(c_vp)]),
+    "cggm_device_free": (c_i32, [c_vp, c_vp]),
+    "cggm_ipc_get_handle": (c_i32, [c_vp, c_vp, c_vp]),
+    "cggm_ipc_open_handle": (c_i32, [c_vp, c_vp, ctypes.POINTER(c_vp)]),
+    "cggm_ipc_close_handle": (c_i32, [c_vp, c_vp]),
+    "cggm_peer_allreduce": (c_i32, [c_vp, c_i32, c_i32, ctypes.POINTER(c_vp), c_i64]),
     "cggm_gemm": (c_i32, [c_vp, c_i32, c_i32, c_i64, c_i64, c_i64, c_d, c_vp, c_i64, c_vp, c_i64, c_d, c_vp, c_i64,
                           c_i32]),
     "cggm_chol_inverse_dense": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, ctypes.POINTER(c_d),

@@ -382,6 +382,68 @@ cggm_status cggm_comm_init_external(cggm_ctx* ctx, int32_t rank, int32_t world, 
   });
 }
 
+cggm_status cggm_device_alloc(cggm_ctx* ctx, int64_t bytes, void** dev_ptr) {
+  return guard(ctx, [&](Ctx* c) {
+    if (!dev_ptr || bytes <= 0) fail(CGGM_ERR_INVALID_ARG, "need bytes > 0 and an output pointer");
+    if (cudaMalloc(dev_ptr, (size_t)bytes) != cudaSuccess) {
+      cudaGetLastError();
+      *dev_ptr = nullptr;
+      fail(CGGM_ERR_OOM, "cggm_device_alloc failed");
+    }
+    (void)c;
+  });
+}
+
+cggm_status cggm_device_free(cggm_ctx* ctx, void* dev_ptr) {
+  return guard(ctx, [&](Ctx* c) {
+    if (dev_ptr) CGGM_CUDA_CHECK(cudaFree(dev_ptr));
+    (void)c;
+  });
+}
+
+cggm_status cggm_ipc_get_handle(cggm_ctx* ctx, const void* dev_ptr, char handle[64]) {
+  return guard(ctx, [&](Ctx* c) {
+    if (!dev_ptr || !handle) fail(CGGM_ERR_INVALID_ARG, "null pointer");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    cudaIpcMemHandle_t h;
+    CGGM_CUDA_CHECK(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+    std::memcpy(handle, &h, 64);
+    (void)c;
+  });
+}
+
+cggm_status cggm_ipc_open_handle(cggm_ctx* ctx, const char handle[64], void** dev_ptr) {
+  return guard(ctx, [&](Ctx* c) {
+    if (!dev_ptr || !handle) fail(CGGM_ERR_INVALID_ARG, "null pointer");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    CGGM_CUDA_CHECK(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    (void)c;
+  });
+}
+
+cggm_status cggm_ipc_close_handle(cggm_ctx* ctx, void* dev_ptr) {
+  return guard(ctx, [&](Ctx* c) {
+    if (!dev_ptr) fail(CGGM_ERR_INVALID_ARG, "null pointer");
+    CGGM_CUDA_CHECK(cudaIpcCloseMemHandle(dev_ptr));
+    (void)c;
+  });
+}
+
+cggm_status cggm_peer_allreduce(cggm_ctx* ctx, int32_t world, int32_t rank, void* const* bufs, int64_t count) {
+  return guard(ctx, [&](Ctx* c) {
+    if (world < 1 || world > 8 || rank < 0 || rank >= world) fail(CGGM_ERR_INVALID_ARG, "need 0 <= rank < world <= 8");
+    if (count < 0) fail(CGGM_ERR_INVALID_ARG, "negative count");
+    if (!bufs) fail(CGGM_ERR_INVALID_ARG, "null buffer array");
+    for (int k = 0; k < world; ++k)
+      if (!bufs[k] && count > 0) fail(CGGM_ERR_INVALID_ARG, "null peer buffer");
+    dispatch(c, [&](auto tag) {
+      using T = decltype(tag);
+      peer_allreduce<T>(c, world, rank, bufs, count);
+    });
+  });
+}
+
 cggm_status cggm_comm_destroy(cggm_ctx* ctx) {
   return guard(ctx, [&](Ctx* c) { comm_release(c); });
 }

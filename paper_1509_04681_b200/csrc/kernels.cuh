@@ -21,6 +21,8 @@ void r_e_from_acc(Ctx* c, int64_t n, int64_t q, const T* acc, int64_t lda, const
                   T* E, int64_t lde, double s);
 template <typename T>
 void symmetrize(Ctx* c, int64_t n, T* S, int64_t ld);
+template <typename T>
+void peer_allreduce(Ctx* c, int world, int rank, void* const* bufs, int64_t count);
 struct ActTotals {
   long long m_L, m_T, ties_L, ties_T;
   double sub_L, sub_T;

@@ -211,6 +211,35 @@ void symmetrize(Ctx* c, int64_t n, T* S, int64_t ld) {
 template void symmetrize<double>(Ctx*, int64_t, double*, int64_t);
 template void symmetrize<float>(Ctx*, int64_t, float*, int64_t);
 
+// slice [lo, hi) of the sum over `world` peer buffers, in rank order, written back to every buffer
+constexpr int PEER_MAX = 8;
+struct PeerPtrs {
+  void* p[PEER_MAX];
+};
+template <typename T>
+__global__ void k_peer_allreduce(PeerPtrs bufs, int world, int64_t lo, int64_t hi) {
+  for (int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
+    T s = static_cast<const T*>(bufs.p[0])[i];
+    for (int k = 1; k < world; ++k) s += static_cast<const T*>(bufs.p[k])[i];
+    for (int k = 0; k < world; ++k) static_cast<T*>(bufs.p[k])[i] = s;
+  }
+}
+
+template <typename T>
+void peer_allreduce(Ctx* c, int world, int rank, void* const* bufs, int64_t count) {
+  if (world < 1 || world > PEER_MAX) throw CudaError{CGGM_ERR_INVALID_ARG, "peer all-reduce: 1..8 ranks"};
+  const int64_t per = (count + world - 1) / world;
+  const int64_t lo = std::min<int64_t>(count, (int64_t)rank * per), hi = std::min<int64_t>(count, lo + per);
+  if (hi <= lo) return;
+  PeerPtrs P{};
+  for (int k = 0; k < world; ++k) P.p[k] = bufs[k];
+  Prof pr(c, TAG_MISC);
+  k_peer_allreduce<T><<<(unsigned)(2 * c->num_sms), 256, 0, c->stream>>>(P, world, lo, hi);
+  post_launch(c, "k_peer_allreduce");
+}
+template void peer_allreduce<double>(Ctx*, int, int, void* const*, int64_t);
+template void peer_allreduce<float>(Ctx*, int, int, void* const*, int64_t);
+
 // ------------------------------------------------------------------ CSC checks
 // flag bits: 1 = colptr not monotone / bad ends, 2 = row out of range or not strictly increasing,
 //            4 = not symmetric (symmetric mode)

@@ -23,7 +23,8 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-__all__ = ["shard_rows", "flat", "ShardedEvaluator", "CudaBackend", "CollectiveEvaluator", "DistributedInverse"]
+__all__ = ["shard_rows", "flat", "ShardedEvaluator", "CudaBackend", "CollectiveEvaluator", "DistributedInverse",
+           "PeerAllReduce"]
 
 
 def shard_rows(n: int, world: int, rank: int) -> tuple[int, int]:
@@ -64,8 +65,8 @@ class CudaBackend:
         from .api import colmajor_empty
         return colmajor_empty(rows, cols, device=like.device, dtype=like.dtype)
 
-    def psi_grad_partial(self, X, Y, Theta, Sigma, n_total):
-        r = self.ctx.cggm_psi_grad(X, Y, Theta, Sigma, n_total=n_total, want_gradL=False)
+    def psi_grad_partial(self, X, Y, Theta, Sigma, n_total, out=None):
+        r = self.ctx.cggm_psi_grad(X, Y, Theta, Sigma, n_total=n_total, want_gradL=False, out=out)
         return r["Psi"], r["GradT"]
 
     def grad_lambda(self, Syy, Sigma, Psi):
@@ -103,7 +104,7 @@ class ShardedEvaluator:
     """One Newton-iteration evaluation with the rows of X, Y split over the process group."""
 
     def __init__(self, backend, group=None, replicate_inverse: bool = False, split_objective: bool = True,
-                 distributed_inverse: bool = False, block: int = 2048):
+                 distributed_inverse: bool = False, block: int = 2048, peer_allreduce: bool = False):
         self.b = backend
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -115,9 +116,14 @@ class ShardedEvaluator:
         self.split = split_objective and self.world > 1 and not replicate_inverse
         self.obj_rank = (self.world - 1 if self.dist_inv is not None else 1) if self.split else None
         self.X_full = self.Y_full = None
+        # Psi / grad_Theta partials summed over CUDA IPC peer memory instead of NCCL (CudaBackend)
+        self.peer = PeerAllReduce(backend.ctx, group) if (peer_allreduce and self.world > 1) else None
+        self._peer_out = None
 
     def _allreduce(self, t):
         if self.world > 1:
+            if self.peer is not None and hasattr(t, "_peer_index"):
+                return self.peer.allreduce(t)
             dist.all_reduce(flat(t), group=self.group)
         return t
 
@@ -190,7 +196,13 @@ class ShardedEvaluator:
                                 dtype=torch.float64, device=Sigma.device)
             dist.broadcast(meta, src=0, group=self.group)
             logdet, pd, fc = float(meta[0]), bool(meta[1] > 0.5), int(meta[2])
-        Psi, GradT = self.b.psi_grad_partial(X_r, Y_r, Theta, Sigma, n)
+        if self.peer is not None:
+            if self._peer_out is None:   # symmetric buffers, allocated once (same shapes every call)
+                p = X_r.shape[1]
+                self._peer_out = {"Psi": self.peer.empty(q, q, Sigma.dtype), "GradT": self.peer.empty(p, q, Sigma.dtype)}
+            Psi, GradT = self.b.psi_grad_partial(X_r, Y_r, Theta, Sigma, n, out=self._peer_out)
+        else:
+            Psi, GradT = self.b.psi_grad_partial(X_r, Y_r, Theta, Sigma, n)
         self._allreduce(Psi)
         self._allreduce(GradT)
         GradL = self.b.grad_lambda(self.Syy, Sigma, Psi)
@@ -397,3 +409,75 @@ class DistributedInverse:
             self._bcast(S[j0:, j0:j1], J % G)
         self.b.symmetrize(S)
         return S, logdet, True, -1
+
+
+# ------------------------------------------------------------------ all-reduce over peer memory
+class PeerAllReduce:
+    """Sum of same-shaped partials over the ranks of a node through CUDA IPC peer memory
+    (cggm_peer_allreduce): every rank's partial lives in a symmetric buffer (a cggm_device_alloc
+    allocation whose IPC handle every other rank opened), the GEMM writes into it directly, and
+    rank r reduces slice r of all buffers in rank order into all buffers -- NVLink loads / stores
+    between GPUs instead of an NCCL call, bit-identical on every rank.  Host barriers order the
+    phases (no kernel waits on another rank's kernel)."""
+
+    def __init__(self, ctx, group=None):
+        import ctypes
+        self.ctypes = ctypes
+        self.ctx = ctx
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self._bufs = []   # (own pointer, ctypes pointer array, opened peer pointers)
+
+    def empty(self, rows, cols, dtype=torch.float64):
+        """A (rows, cols) column-major symmetric buffer (identical layout on every rank)."""
+        ct = self.ctypes
+        ld = rows + (rows & 1)
+        nbytes = ld * max(cols, 1) * torch.empty(0, dtype=dtype).element_size()
+        p = ct.c_void_p()
+        self.ctx._check(self.ctx.lib.cggm_device_alloc(self.ctx.h, nbytes, ct.byref(p)))
+        h = (ct.c_char * 64)()
+        self.ctx._check(self.ctx.lib.cggm_ipc_get_handle(self.ctx.h, p, h))
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(h), group=self.group)
+        ptrs, opened = [], []
+        for k, hb in enumerate(handles):
+            if k == self.rank:
+                ptrs.append(p.value)
+                continue
+            q = ct.c_void_p()
+            self.ctx._check(self.ctx.lib.cggm_ipc_open_handle(self.ctx.h, (ct.c_char * 64).from_buffer_copy(hb),
+                                                              ct.byref(q)))
+            ptrs.append(q.value)
+            opened.append(q.value)
+        arr = (ct.c_void_p * self.world)(*ptrs)
+        count = ld * (max(cols, 1) - 1) + rows
+        self._bufs.append((p.value, arr, opened, count))
+        typestr = {torch.float64: "<f8", torch.float32: "<f4"}[dtype]
+        es = torch.empty(0, dtype=dtype).element_size()
+
+        class _Cai:
+            __cuda_array_interface__ = {"shape": (rows, cols), "typestr": typestr, "data": (p.value, False),
+                                        "version": 3, "strides": (es, ld * es)}
+        t = torch.as_tensor(_Cai(), device=torch.device("cuda", self.ctx.device))
+        t._peer_index = len(self._bufs) - 1
+        return t
+
+    def allreduce(self, t):
+        own, arr, _, count = self._bufs[t._peer_index]
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)          # every partial is complete
+        self.ctx._sync_stream()
+        self.ctx._check(self.ctx.lib.cggm_peer_allreduce(self.ctx.h, self.world, self.rank, arr, count))
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)          # every slice is written everywhere
+        return t
+
+    def close(self):
+        for own, _, opened, _ in self._bufs:
+            for q in opened:
+                self.ctx.lib.cggm_ipc_close_handle(self.ctx.h, self.ctypes.c_void_p(q))
+        dist.barrier(group=self.group)
+        for own, _, _, _ in self._bufs:
+            self.ctx.lib.cggm_device_free(self.ctx.h, self.ctypes.c_void_p(own))
+        self._bufs = []

@@ -258,3 +258,73 @@ def test_library_collectives_streamed_grad_theta():
             assert np.array_equal(r["T_row"], a["T_row"]) and np.array_equal(r["T_col"], a["T_col"])
     assert (res[0]["m_L"], res[0]["m_T"], res[0]["ties"]) == (res[1]["m_L"], res[1]["m_T"], res[1]["ties"])
     assert np.array_equal(res[0]["T_row"], res[1]["T_row"])
+
+
+def _worker_peer(rank, world, port, q_out):
+    """Psi / grad_Theta partials summed over CUDA IPC peer memory (cggm_peer_allreduce)."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_1509_04681_b200 import Context, DeviceCsc, to_device_colmajor
+        from paper_1509_04681_b200.sharded import CudaBackend, PeerAllReduce, ShardedEvaluator, shard_rows
+        from synth.cggm_inputs import make_problem
+        ctx = Context(0)
+        # the primitive: random symmetric buffers, sum = the sum of every rank's seeded values
+        pr = PeerAllReduce(ctx)
+        buf = pr.empty(37, 5)
+        g = torch.Generator().manual_seed(rank)
+        buf.copy_(torch.randn(37, 5, generator=g, dtype=torch.float64))
+        pr.allreduce(buf)
+        ref = sum(torch.randn(37, 5, generator=torch.Generator().manual_seed(k), dtype=torch.float64)
+                  for k in range(world))
+        prim_ok = bool(torch.allclose(buf.cpu(), ref, rtol=1e-14, atol=1e-14))
+        P = make_problem("small")
+        _, lam, th = P.points[1]
+        a, b = shard_rows(P.n, world, rank)
+        X, Y = to_device_colmajor(P.X[a:b]), to_device_colmajor(P.Y[a:b])
+        ev = ShardedEvaluator(CudaBackend(ctx), split_objective=False, peer_allreduce=True)
+        ev.setup(X, Y, P.n)
+        r = ev.evaluate(X, Y, DeviceCsc.from_host(lam), DeviceCsc.from_host(th), P.lam_L, P.lam_T, True)
+        torch.cuda.synchronize()
+        q_out.put({"rank": rank, "prim_ok": prim_ok, "Psi": r["Psi"].cpu().numpy().copy(),
+                   "GradT": r["GradT"].cpu().numpy().copy(), "GradL": r["GradL"].cpu().numpy().copy(),
+                   "f": r["f"]})
+        pr.close()
+        ev.peer.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_allreduce_matches_oracle(world):
+    import torch.multiprocessing as mp
+    from oracle import cggm_oracle as O
+    from synth.cggm_inputs import make_problem
+    ctx = mp.get_context("spawn")
+    qo = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_peer, args=(r, world, port, qo)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [qo.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=600)
+        assert p.exitcode == 0
+    P = make_problem("small")
+    _, lam, th = P.points[1]
+    Syy, Sxy = O.covariances(P.X, P.Y)
+    S, _, _, _ = O.invert_logdet(lam.to_dense())
+    ref = O.psi_grad(P.X, P.Y, th, S, Syy, Sxy)
+    ob = O.objective(P.X, P.Y, lam, th, P.lam_L, P.lam_T)
+    rel = lambda x, y: np.linalg.norm(x - y) / np.linalg.norm(y)  # noqa: E731
+    for r in res:
+        assert r["prim_ok"]
+        assert rel(r["Psi"], ref["Psi"]) <= 1e-9
+        assert rel(r["GradT"], ref["GradT"]) <= 1e-9
+        assert rel(r["GradL"], ref["GradL"]) <= 1e-9
+        assert r["f"] == pytest.approx(ob["f"], rel=1e-10)
+    for r in res[1:]:
+        assert np.array_equal(r["Psi"], res[0]["Psi"]) and np.array_equal(r["GradT"], res[0]["GradT"])
