@@ -101,7 +101,14 @@ class CudaBackend:
 
 
 class ShardedEvaluator:
-    """One Newton-iteration evaluation with the rows of X, Y split over the process group."""
+    """One Newton-iteration evaluation with the rows of X, Y split over the process group.
+
+    Sigma: rank 0 factors and broadcasts (default), every rank factors (replicate_inverse), or all
+    ranks factor together (distributed_inverse, NEXT-3, block-cyclic with `block`-wide columns).
+    Objective: on one rank with the gathered full data while Sigma is formed (split_objective),
+    else each rank's partial traces are all-reduced (with distributed_inverse its trial
+    factorisation is distributed too).  Psi / grad_Theta partials: NCCL all-reduce, or CUDA IPC peer
+    memory (peer_allreduce, CudaBackend only)."""
 
     def __init__(self, backend, group=None, replicate_inverse: bool = False, split_objective: bool = True,
                  distributed_inverse: bool = False, block: int = 2048, peer_allreduce: bool = False):
