@@ -181,25 +181,6 @@ __global__ void __maxnreg__(C::MAXREG)
     nkt = max(0, min(per, nkt - part * per));
   }
 
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], NCW);
-    }
-    ptx::fence_barrier_init();
-  }
-  __syncthreads();
-
-  double acc[FM][FN][2];
-#pragma unroll
-  for (int a = 0; a < FM; ++a)
-#pragma unroll
-    for (int b = 0; b < FN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-
-  const int g = lane >> 2, t = lane & 3;
-  const int wm = warp / C::WN, wn = warp % C::WN;
-  const int xa0 = wm * C::WTM, xb0 = wn * C::WTN;
-
   // ------------------------------------------------ TMA producer: thread 0, STAGES-1 tiles ahead
   uint32_t tx_bytes = 0;
   if (threadIdx.x == 0 && nkt > 0) {
@@ -242,8 +223,28 @@ __global__ void __maxnreg__(C::MAXREG)
       for (int xb = 0; xb < b_boxes; ++xb) ptx::tma_load_2d(sb + xb * 2048, &tmB2, &full[s], n0 + xb * 16, k);
     }
   };
-  if (threadIdx.x == 0)
+  // thread 0 initialises the ring barriers and issues the first STAGES-1 k-tiles before the block
+  // barrier, so the loads are in flight while the other threads reach it
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], NCW);
+    }
+    ptx::fence_barrier_init();
     for (int i = 0; i < STAGES - 1 && i < nkt; ++i) issue(i);
+  }
+  __syncthreads();
+
+  double acc[FM][FN][2];
+#pragma unroll
+  for (int a = 0; a < FM; ++a)
+#pragma unroll
+    for (int b = 0; b < FN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp / C::WN, wn = warp % C::WN;
+  const int xa0 = wm * C::WTM, xb0 = wn * C::WTN;
+
   {
     // ------------------------------------------------ DMMA consumers
     for (int i = 0; i < nkt; ++i) {
