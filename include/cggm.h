@@ -171,7 +171,10 @@ const char* cggm_version(void);
  * slice r of all ranks' buffers in rank order and writes the sum into slice r of every rank's
  * buffer (cggm_peer_allreduce; in place: each slice is read and written by its owner only); after
  * a second barrier every buffer holds the bit-identical total.  bufs: host array of `world`
- * device pointers (rank k's buffer at bufs[k]), count elements of the ctx dtype. */
+ * device pointers (rank k's buffer at bufs[k]), count elements of the ctx dtype.  The same exchange
+ * north_star assigns to an NCCL all-reduce (the partial X^T(X Theta) and R^T R sums).  Errors:
+ * CGGM_ERR_INVALID_ARG (world outside 1..8, rank out of range, null pointers), CGGM_ERR_CUDA (an
+ * IPC call failed, e.g. no peer access between the devices), CGGM_ERR_OOM (cggm_device_alloc). */
 /* A device allocation of its own (cudaMalloc on the ctx device), so that its IPC handle covers
  * exactly the buffer (pool sub-allocations would need an offset); freed by cggm_device_free. */
 cggm_status cggm_device_alloc(cggm_ctx* ctx, int64_t bytes, void** dev_ptr);
