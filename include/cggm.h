@@ -384,7 +384,7 @@ cggm_status cggm_newton_eval_host(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q
  * One Newton-iteration evaluation at (Lambda, Theta) without storing Sigma, Psi or grad_Lambda
  * (the paper's block mode, P:555-595 / P:671-825, with triangular products of the GPU factor in
  * place of CG): the q x q memory is the factorisation's (dense Lambda, freed after, and L^{-1});
- * Sigma, Psi and the gradients exist only as b-wide column blocks (block = 0: 2048) consumed by the
+ * Sigma, Psi and the gradients exist only as b-wide column blocks (block = 0: 1024) consumed by the
  * active-set compaction.  Outputs as cggm_newton_eval without the dense matrices: log-det / PD,
  * the active lists and counts (active, two-call CGGM_ERR_CAPACITY pattern), the subgradient
  * statistic, and the objective at the same Lambda from the same factor (out->obj; a line-search

@@ -1649,7 +1649,8 @@ static void newton_eval_core(Ctx* c, int64_t n, int64_t p, int64_t q, const void
 // triangular k-range), R_C = W Sigma_C / sqrt n and E_C = Y_C + W Sigma_C (one GEMM, two
 // epilogues), grad_Theta_C = (2/n) X^T E_C into its active-set chunk; pass 2 (R complete):
 // grad_Lambda rows 0..j of each column j of C = Y^T Y_C / n - R^T R_C - Sigma[0:j1, C] into its
-// active-set chunk.  The objective reuses L^{-1}: tr(Sigma M) = ||W L^{-T}||^2 / n.
+// active-set chunk.  The objective reuses L^{-1}: tr(Sigma M) = ||W L^{-T}||^2 / n.  The passes'
+// buffers live in the dense-Lambda workspace the factorisation has finished with.
 template <typename T>
 static void newton_eval_blocked_impl(Ctx* c, int64_t n, int64_t p, int64_t q, const T* Xd, int64_t ldx, const T* Yd,
                                      int64_t ldy, const cggm_csc* Lambda, const cggm_csc* Theta, int64_t b,
@@ -1678,15 +1679,6 @@ static void newton_eval_blocked_impl(Ctx* c, int64_t n, int64_t p, int64_t q, co
   out->logdet = cr.logdet;
   out->is_pd = cr.is_pd;
   out->fail_col = cr.fail_col;
-  // the dense copy of Lambda is no longer needed: give its memory back before the block passes
-  {
-    Buffer& bA = c->slots[WS_DENSE_A];
-    if (bA.ptr) {
-      CGGM_CUDA_CHECK(cudaFree(bA.ptr));
-      bA = Buffer{};
-      c->ws_generation++;
-    }
-  }
   if (!cr.is_pd) {
     out->obj.is_pd = 0;
     out->obj.fail_col = cr.fail_col;
@@ -1695,14 +1687,34 @@ static void newton_eval_blocked_impl(Ctx* c, int64_t n, int64_t p, int64_t q, co
     active->subgrad_l1 = 0.0;
     return;
   }
-  // 2. W = X Theta; R, E (n x q)
-  T* W = static_cast<T*>(ws_get(c, WS_W, (size_t)ldn * q * sizeof(T)));
-  T* R = static_cast<T*>(ws_get(c, WS_R, (size_t)ldn * q * sizeof(T)));
-  T* E = static_cast<T*>(ws_get(c, WS_E, (size_t)ldn * q * sizeof(T)));
+  // 2. the block passes' buffers, carved out of the dense copy of Lambda (free after the
+  // factorisation: the passes add no memory beyond the factorisation's peak, and nothing is
+  // allocated per call); separate workspace slots only if they do not fit
+  T *W, *R, *E, *SigC, *GLC, *GTC, *Z;
+  {
+    const size_t nq = (size_t)ldn * q, qb = (size_t)ldq * b, pb = (size_t)ldp * b;
+    auto up = [](size_t e) { return (e + 31) & ~size_t(31); };   // 256-byte aligned carving
+    const size_t need = 4 * up(nq) + 2 * up(qb) + up(pb);
+    if (need <= (size_t)ldq * q) {
+      T* pool = static_cast<T*>(ws_get(c, WS_DENSE_A, (size_t)ldq * q * sizeof(T)));
+      W = pool;
+      R = W + up(nq);
+      E = R + up(nq);
+      Z = E + up(nq);
+      SigC = Z + up(nq);
+      GLC = SigC + up(qb);
+      GTC = GLC + up(qb);
+    } else {
+      W = static_cast<T*>(ws_get(c, WS_W, nq * sizeof(T)));
+      R = static_cast<T*>(ws_get(c, WS_R, nq * sizeof(T)));
+      E = static_cast<T*>(ws_get(c, WS_E, nq * sizeof(T)));
+      Z = static_cast<T*>(ws_get(c, WS_Z, nq * sizeof(T)));
+      SigC = static_cast<T*>(ws_get(c, WS_BLK_S, qb * sizeof(T)));
+      GLC = static_cast<T*>(ws_get(c, WS_BLK_G, qb * sizeof(T)));
+      GTC = static_cast<T*>(ws_get(c, WS_GTCHUNK, pb * sizeof(T)));
+    }
+  }
   spmm_x_theta<T>(c, Xd, ldx, n, Theta, ViewT<T>{W, ldn, n, q});
-  T* SigC = static_cast<T*>(ws_get(c, WS_BLK_S, (size_t)ldq * b * sizeof(T)));
-  T* GLC = static_cast<T*>(ws_get(c, WS_BLK_G, (size_t)ldq * b * sizeof(T)));
-  T* GTC = static_cast<T*>(ws_get(c, WS_GTCHUNK, (size_t)ldp * b * sizeof(T)));
   ActWs aws = active_ws(c, q);
   active_begin(c, q, aws);
   const double rs = 1.0 / std::sqrt((double)n);
@@ -1751,7 +1763,6 @@ static void newton_eval_blocked_impl(Ctx* c, int64_t n, int64_t p, int64_t q, co
   }
   active_end(c, q, aws);
   // 4. objective at Lambda with the same factor: tr(Sigma M) = ||W L^{-T}||^2 / n
-  T* Z = static_cast<T*>(ws_get(c, WS_Z, (size_t)ldn * q * sizeof(T)));
   {
     Phase ph(c, TAG_TRSM);
     EpilogueT<T> e; e.out1 = Z; e.ld1 = ldn;
@@ -1815,7 +1826,7 @@ cggm_status cggm_newton_eval_blocked(cggm_ctx* ctx, int64_t n, int64_t p, int64_
     std::memset(out, 0, sizeof(*out));
     validate_csc_dev(c, Lambda, true, "Lambda");
     validate_csc_dev(c, Theta, false, "Theta");
-    int64_t b = block > 0 ? block : 2048;
+    int64_t b = block > 0 ? block : 1024;   // measured best at large (1024: 544 ms, 2048: 558, 4096: 577)
     b = std::min<int64_t>((b + 1) & ~int64_t(1), q);
     dispatch(c, [&](auto tag) {
       using T = decltype(tag);
