@@ -29,6 +29,9 @@ namespace {
 #define CGGM_BIG_MAXNREG 192
 #endif
 constexpr int BK = 16;
+#ifndef CGGM_WS
+#define CGGM_WS 1
+#endif
 constexpr int STAGES = 4;
 constexpr int GROUP_N = 8;
 #ifndef CGGM_SYM_BAND
@@ -54,6 +57,12 @@ struct Cfg {
   // on its SM, exactly one 64x64 CTA (4 warps x 128), so latency-bound kernels of a concurrent
   // stream co-reside with the big tiles instead of waiting for a whole SM
   static constexpr int MAXREG = (WTM >= 64 && WTN >= 32) ? CGGM_BIG_MAXNREG : 128;
+  // warp specialisation (the big-warp-tile configurations): a producer warpgroup streams the TMA
+  // k-tiles and donates its registers (setmaxnreg 40), the consumer warpgroups run the DMMA main
+  // loop and the epilogue at up to 232 registers; no consumer warp ever waits on a ring slot
+  static constexpr bool WSP = CGGM_WS && (WTM >= 64 && WTN >= 32);
+  static constexpr int LB_THREADS = NTHREADS + (WSP ? 128 : 0);
+  static constexpr int LB_MINB = WSP ? 1 : 65536 / (NTHREADS * MAXREG);
   static_assert(FM % 2 == 0 && FN % 2 == 0, "MN-inner fragments come in pairs");
   static_assert(BM % 16 == 0 && BN % 16 == 0, "16-wide TMA boxes");
 };
@@ -150,19 +159,25 @@ __device__ __forceinline__ int frag_x(int f, int r) {
 }
 
 template <bool AK, bool BKI, class C>
-__global__ void __maxnreg__(C::MAXREG)
+__global__ void __launch_bounds__(C::LB_THREADS, C::LB_MINB)
     gemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
                      const KParams P) {
   constexpr int BM = C::BM, BN = C::BN, NCW = C::WM * C::WN, FM = C::FM, FN = C::FN;
   constexpr int OP_BYTES = C::A_BYTES, STAGE_BYTES = C::STAGE_BYTES, DATA_BYTES = C::DATA_BYTES;
   constexpr int EPI_LD = C::EPI_LD, NTHREADS = C::NTHREADS;
+  constexpr bool WS = C::WSP;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + DATA_BYTES);
   uint64_t* empty = full + STAGES;
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tid = (int)threadIdx.x - (WS ? 128 : 0);   // consumer thread index
+  const int warp = tid >> 5, lane = threadIdx.x & 31;
+  auto cbar = [&]() {   // barrier of the consumer threads
+    if (WS) asm volatile("bar.sync 1, %0;\n" ::"n"(NTHREADS) : "memory");
+    else __syncthreads();
+  };
   int I, J;
   const int part = P.ksplit > 1 ? (int)(blockIdx.x % P.ksplit) : 0;
   tile_coords(P, P.ksplit > 1 ? (int)(blockIdx.x / P.ksplit) : (int)blockIdx.x, I, J);
@@ -234,6 +249,18 @@ __global__ void __maxnreg__(C::MAXREG)
     for (int i = 0; i < STAGES - 1 && i < nkt; ++i) issue(i);
   }
   __syncthreads();
+  if (WS) {
+    if (threadIdx.x < 128) {   // producer warpgroup: 40 registers, thread 0 streams the k-tiles
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+      if (threadIdx.x == 0)
+        for (int j = STAGES - 1; j < nkt; ++j) {
+          if (j >= STAGES) ptx::mbar_wait(&empty[j % STAGES], ((j / STAGES) & 1) ^ 1);
+          issue(j);
+        }
+      return;
+    }
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+  }
 
   double acc[FM][FN][2];
 #pragma unroll
@@ -302,7 +329,7 @@ __global__ void __maxnreg__(C::MAXREG)
       }
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&empty[s]);
-      if (threadIdx.x == 0) {
+      if (!WS && threadIdx.x == 0) {
         const int j = i + STAGES - 1;
         if (j < nkt) {
           if (j >= STAGES) ptx::mbar_wait(&empty[j % STAGES], ((j / STAGES) & 1) ^ 1);
@@ -313,7 +340,7 @@ __global__ void __maxnreg__(C::MAXREG)
   }
 
   // ------------------------------------------------ epilogue through shared memory
-  __syncthreads();
+  cbar();
   double* Cs = reinterpret_cast<double*>(smem);
   {
 #pragma unroll
@@ -328,10 +355,10 @@ __global__ void __maxnreg__(C::MAXREG)
         }
     }
   }
-  __syncthreads();
+  cbar();
   const bool diag = (P.flags & SYM_LOWER) && I == J;
   if (P.ksplit > 1) {   // partial sum of this k-half into out1 (zeros + two partials: order-free)
-    for (int idx = threadIdx.x; idx < BM * BN; idx += NTHREADS) {
+    for (int idx = tid; idx < BM * BN; idx += NTHREADS) {
       const int ml = idx % BM, nl = idx / BM;
       const int m = m0 + ml, n = n0 + nl;
       if (m >= P.M || n >= P.N) continue;
@@ -345,7 +372,7 @@ __global__ void __maxnreg__(C::MAXREG)
     // per element the same arithmetic as epi_apply
     constexpr int RP = BM / 2, CG = NTHREADS / RP, NCOL = BN / CG, U = 8;
     const Epilogue& E = P.epi;
-    const int ml = 2 * (threadIdx.x % RP), cg = threadIdx.x / RP;
+    const int ml = 2 * (tid % RP), cg = tid / RP;
     const int64_t m = m0 + ml;
 #pragma unroll 1
     for (int i0 = 0; i0 < NCOL; i0 += U) {
@@ -380,7 +407,7 @@ __global__ void __maxnreg__(C::MAXREG)
       }
     }
   } else {
-    for (int idx = threadIdx.x; idx < BM * BN; idx += NTHREADS) {
+    for (int idx = tid; idx < BM * BN; idx += NTHREADS) {
       const int ml = idx % BM, nl = idx / BM;
       const int m = m0 + ml, n = n0 + nl;
       if (m >= P.M || n >= P.N) continue;
@@ -397,7 +424,7 @@ __global__ void __maxnreg__(C::MAXREG)
       constexpr int NWARPS = NTHREADS / 32, NBLK = BN / 32, GROUPS = NWARPS / NBLK, PAIRS = BM / 2 / GROUPS;
       static_assert(NWARPS % NBLK == 0 && (BM / 2) % GROUPS == 0, "mirror epilogue warp layout");
       const Epilogue& E = P.epi;
-      const int wv = threadIdx.x >> 5, ln = threadIdx.x & 31;
+      const int wv = tid >> 5, ln = tid & 31;
       const int nl = 32 * (wv % NBLK) + ln, grp = wv / NBLK;
       const bool odd = ln & 1;
       const int64_t n = n0 + nl - (odd ? 1 : 0);
@@ -414,7 +441,7 @@ __global__ void __maxnreg__(C::MAXREG)
           *reinterpret_cast<double2*>(E.out2 + n + m * E.ld2) = make_double2(__dmul_rn(E.a2, lo), __dmul_rn(E.a2, hi));
       }
     } else {
-      for (int idx = threadIdx.x; idx < BM * BN; idx += NTHREADS) {
+      for (int idx = tid; idx < BM * BN; idx += NTHREADS) {
         const int nl = idx % BN, ml = idx / BN;
         const int m = m0 + ml, n = n0 + nl;
         if (m >= P.M || n >= P.N) continue;
@@ -695,7 +722,7 @@ void launch(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensor
     attr_set = true;
   }
   Prof pr(c, c->cur_tag);
-  gemm_dmma_kernel<AK, BKI, C><<<grid, C::NTHREADS, C::SMEM_BYTES, c->stream>>>(ma, mb, ma2, mb2, P);
+  gemm_dmma_kernel<AK, BKI, C><<<grid, C::LB_THREADS, C::SMEM_BYTES, c->stream>>>(ma, mb, ma2, mb2, P);
   post_launch(c, "gemm_dmma_kernel");
 }
 
