@@ -110,7 +110,8 @@ struct Ctx {
   int no_active_vec = 0;
   int act_onepass = 0;
   int no_split_k = 0;   // CGGM_NO_SPLIT_K=1: W Sigma without the split-k grid (A/B)
-  int no_vec_epi = 0;   // CGGM_NO_VEC_EPI=1: scalar GEMM epilogue everywhere (A/B)      // CGGM_ACT_ONEPASS=1: Lambda list by the single-pass look-back kernel (not the split one)    // test hook (CGGM_NO_ACTIVE_VEC=1): scalar active-set kernel only   // test hook (CGGM_NO_SMALL_ASYNC=1): direct-load small kernel only
+  int no_vec_epi = 0;
+  int persist_tpc = 0;   // CGGM_PERSIST_TPC: tiles per CTA of the persistent warp-specialised GEMM (0: off)   // CGGM_NO_VEC_EPI=1: scalar GEMM epilogue everywhere (A/B)      // CGGM_ACT_ONEPASS=1: Lambda list by the single-pass look-back kernel (not the split one)    // test hook (CGGM_NO_ACTIVE_VEC=1): scalar active-set kernel only   // test hook (CGGM_NO_SMALL_ASYNC=1): direct-load small kernel only
   int no_tma3d = 0;   // test hook: 1 = always use 16-wide 2-D boxes for MN-inner operands  // test hook: 0 auto, 1 = 128x128 tiles, 2 = 64x64 tiles
   // phase profiling (CUDA events around every launch while enabled)
   int cur_tag = TAG_MISC;

@@ -726,6 +726,289 @@ void launch(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensor
   post_launch(c, "gemm_dmma_kernel");
 }
 
+// ------------------------------------------------------------------ persistent warp-specialised
+// One CTA per SM walks tiles tbase, tbase + rw, ... (windows of `resident` CTAs, so the tiles in
+// flight at any moment are consecutive in the tile order).  The producer warpgroup streams the
+// k-tiles of all of its tiles through the ring without a break, so while the consumers run a
+// tile's epilogue (through a staging buffer of its own, half a tile per round) the ring already
+// fills with the next tile's operands: the per-tile pipeline fill and CTA launch vanish.
+template <class C>
+constexpr int pws_smem_bytes() {
+  return STAGES * C::STAGE_BYTES + (C::BN / 2) * C::EPI_LD * 8 + 2 * STAGES * 8 + 1024;
+}
+
+template <bool AK, bool BKI, class C>
+__device__ __forceinline__ void pws_tile(const KParams& P, int tile, int& I, int& J, int& kt0, int& nkt) {
+  tile_coords(P, tile, I, J);
+  const int m0 = I * C::BM, n0 = J * C::BN;
+  int kbeg = 0, kend = P.K;
+  if (P.flags & A_KGE_M) kbeg = max(kbeg, m0);
+  if (P.flags & B_KGE_N) kbeg = max(kbeg, n0);
+  if (P.flags & A_KLE_M) kend = min(kend, m0 + C::BM);
+  if (P.flags & B_KLE_N) kend = min(kend, n0 + C::BN);
+  kt0 = kbeg / BK;
+  nkt = kend > kbeg ? (kend - kt0 * BK + BK - 1) / BK : 0;
+}
+
+template <bool AK, bool BKI, class C>
+__global__ void __launch_bounds__(C::NTHREADS + 128, 1)
+    gemm_dmma_pws(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
+                  const KParams P, int ntiles, int tpc, int resident) {
+  constexpr int BM = C::BM, BN = C::BN, NCW = C::WM * C::WN, FM = C::FM, FN = C::FN;
+  constexpr int OP_BYTES = C::A_BYTES, STAGE_BYTES = C::STAGE_BYTES;
+  constexpr int EPI_LD = C::EPI_LD, NTHREADS = C::NTHREADS, SW = BN / 2;
+  constexpr int RING = STAGES * STAGE_BYTES, SLAB = SW * EPI_LD * 8;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  double* Cs = reinterpret_cast<double*>(smem + RING);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + RING + SLAB);
+  uint64_t* empty = full + STAGES;
+  const int win = blockIdx.x / resident, r_in = blockIdx.x % resident;
+  const int rw = min(resident, (int)gridDim.x - win * resident);
+  const int tbase = win * resident * tpc + r_in;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], NCW);
+    }
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x < 128) {   // ------------------------------ producer warpgroup
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    if (threadIdx.x == 0) {
+      int slot = 0, g = 0;
+      uint32_t ph = 0;   // parity to wait for on the slot's release (used from the second pass on)
+      for (int kt = 0; kt < tpc; ++kt) {
+        const int tile = tbase + kt * rw;
+        if (tile >= ntiles) break;
+        int I, J, kt0, nkt;
+        pws_tile<AK, BKI, C>(P, tile, I, J, kt0, nkt);
+        const int m0 = I * BM, n0 = J * BN;
+        const bool a_one = !AK && P.a3d && (m0 + BM <= P.a3d || P.a3d == P.M);
+        const bool b_one = !BKI && P.b3d && (n0 + BN <= P.b3d || P.b3d == P.N);
+        int a_boxes = 0, b_boxes = 0;
+        if (!AK && !a_one)
+          for (int xb = 0; xb < BM / 16; ++xb) a_boxes += (m0 + xb * 16 < P.M);
+        if (!BKI && !b_one)
+          for (int xb = 0; xb < BN / 16; ++xb) b_boxes += (n0 + xb * 16 < P.N);
+        const uint32_t tx = ((AK || a_one) ? C::A_BYTES : a_boxes * 2048) + ((BKI || b_one) ? C::B_BYTES : b_boxes * 2048);
+        for (int i = 0; i < nkt; ++i, ++g) {
+          if (g >= STAGES) ptx::mbar_wait(&empty[slot], ph ^ 1);
+          uint8_t* sa = smem + slot * STAGE_BYTES;
+          uint8_t* sb = sa + OP_BYTES;
+          ptx::mbar_arrive_expect_tx(&full[slot], tx);
+          const int k = (kt0 + i) * BK;
+          if (AK) ptx::tma_load_2d(sa, &tmA, &full[slot], k, m0);
+          else if (a_one) ptx::tma_load_3d(sa, &tmA, &full[slot], 0, k, m0 / 16);
+          else for (int xb = 0; xb < a_boxes; ++xb) ptx::tma_load_2d(sa + xb * 2048, &tmA2, &full[slot], m0 + xb * 16, k);
+          if (BKI) ptx::tma_load_2d(sb, &tmB, &full[slot], k, n0);
+          else if (b_one) ptx::tma_load_3d(sb, &tmB, &full[slot], 0, k, n0 / 16);
+          else for (int xb = 0; xb < b_boxes; ++xb) ptx::tma_load_2d(sb + xb * 2048, &tmB2, &full[slot], n0 + xb * 16, k);
+          if (++slot == STAGES) {
+            slot = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+    return;
+  }
+  // -------------------------------------------------------------- consumer warpgroups
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+  const int tid = threadIdx.x - 128, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp / C::WN, wn = warp % C::WN;
+  const int xa0 = wm * C::WTM, xb0 = wn * C::WTN;
+  auto cbar = [&]() { asm volatile("bar.sync 1, %0;\n" ::"n"(NTHREADS) : "memory"); };
+  int slot = 0;
+  uint32_t ph = 0;
+  for (int kt = 0; kt < tpc; ++kt) {
+    const int tile = tbase + kt * rw;
+    if (tile >= ntiles) break;
+    int I, J, kt0, nkt;
+    pws_tile<AK, BKI, C>(P, tile, I, J, kt0, nkt);
+    double acc[FM][FN][2];
+#pragma unroll
+    for (int a = 0; a < FM; ++a)
+#pragma unroll
+      for (int b = 0; b < FN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int i = 0; i < nkt; ++i) {
+      ptx::mbar_wait(&full[slot], ph);
+      const uint32_t sa = ptx::smem_u32(smem + slot * STAGE_BYTES);
+      const uint32_t sb = sa + OP_BYTES;
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        double a[FM][2], b[FN][2];
+        if (AK) {
+#pragma unroll
+          for (int f = 0; f < FM; ++f) {
+            const int x = xa0 + frag_x<true>(f, g);
+            const int chunk = (4 * kk + t) ^ (x & 7);
+            ptx::lds128(a[f][0], a[f][1], sa + x * 128 + chunk * 16);
+          }
+        } else {
+#pragma unroll
+          for (int pr = 0; pr < FM / 2; ++pr) {
+            const int xb = xa0 / 16 + pr;
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+              const int k = 8 * kk + 2 * t + s2;
+              const int chunk = g ^ (k & 7);
+              ptx::lds128(a[2 * pr][s2], a[2 * pr + 1][s2], sa + xb * 2048 + k * 128 + chunk * 16);
+            }
+          }
+        }
+        if (BKI) {
+#pragma unroll
+          for (int f = 0; f < FN; ++f) {
+            const int x = xb0 + frag_x<true>(f, g);
+            const int chunk = (4 * kk + t) ^ (x & 7);
+            ptx::lds128(b[f][0], b[f][1], sb + x * 128 + chunk * 16);
+          }
+        } else {
+#pragma unroll
+          for (int pr = 0; pr < FN / 2; ++pr) {
+            const int xb = xb0 / 16 + pr;
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+              const int k = 8 * kk + 2 * t + s2;
+              const int chunk = g ^ (k & 7);
+              ptx::lds128(b[2 * pr][s2], b[2 * pr + 1][s2], sb + xb * 2048 + k * 128 + chunk * 16);
+            }
+          }
+        }
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+          for (int fm = 0; fm < FM; ++fm)
+#pragma unroll
+            for (int fn = 0; fn < FN; ++fn) ptx::dmma_8x8x4(acc[fm][fn][0], acc[fm][fn][1], a[fm][s2], b[fn][s2]);
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&empty[slot]);
+      if (++slot == STAGES) {
+        slot = 0;
+        ph ^= 1;
+      }
+    }
+    // ---------------------------------------------------------- epilogue, half a tile per round
+    const int m0 = I * BM, n0 = J * BN;
+    const bool diag = (P.flags & SYM_LOWER) && I == J;
+    const bool interior = P.vec && !diag && m0 + BM <= P.M && n0 + BN <= P.N;
+    const Epilogue& E = P.epi;
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      const int nbase = n0 + h * SW;
+      if (wn / (C::WN / 2) == h) {
+#pragma unroll
+        for (int fm = 0; fm < FM; ++fm) {
+          const int ml = xa0 + frag_x<AK>(fm, g);
+#pragma unroll
+          for (int fn = 0; fn < FN; ++fn)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) Cs[(xb0 - h * SW + frag_x<BKI>(fn, 2 * t + j)) * EPI_LD + ml] = acc[fm][fn][j];
+        }
+      }
+      cbar();
+      if (interior) {
+        constexpr int RP = BM / 2, CG = NTHREADS / RP, NCOL = SW / CG, U = NCOL < 8 ? NCOL : 8;
+        const int ml = 2 * (tid % RP), cg = tid / RP;
+        const int64_t m = m0 + ml;
+#pragma unroll 1
+        for (int i0 = 0; i0 < NCOL; i0 += U) {
+          double2 x1[U], x2[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int64_t n = nbase + cg + CG * (i0 + u);
+            if (E.in1a) x1[u] = *reinterpret_cast<const double2*>(E.in1a + m + n * E.ld1a);
+            if (E.in2a) x2[u] = *reinterpret_cast<const double2*>(E.in2a + m + n * E.ld2a);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int nl = cg + CG * (i0 + u);
+            const int64_t n = nbase + nl;
+            const double v0 = Cs[nl * EPI_LD + ml], v1 = Cs[nl * EPI_LD + ml + 1];
+            if (E.out1) {
+              double2 o = make_double2(__dmul_rn(E.a1, v0), __dmul_rn(E.a1, v1));
+              if (E.in1a) {
+                o.x = __dadd_rn(o.x, __dmul_rn(E.b1, x1[u].x));
+                o.y = __dadd_rn(o.y, __dmul_rn(E.b1, x1[u].y));
+              }
+              *reinterpret_cast<double2*>(E.out1 + m + n * E.ld1) = o;
+            }
+            if (E.out2) {
+              double2 o = make_double2(__dmul_rn(E.a2, v0), __dmul_rn(E.a2, v1));
+              if (E.in2a) {
+                o.x = __dadd_rn(o.x, __dmul_rn(E.b2, x2[u].x));
+                o.y = __dadd_rn(o.y, __dmul_rn(E.b2, x2[u].y));
+              }
+              *reinterpret_cast<double2*>(E.out2 + m + n * E.ld2) = o;
+            }
+          }
+        }
+      } else {
+        for (int idx = tid; idx < BM * SW; idx += NTHREADS) {
+          const int ml = idx % BM, nl = idx / BM;
+          const int m = m0 + ml, n = nbase + nl;
+          if (m >= P.M || n >= P.N) continue;
+          if (diag && m < n) continue;
+          epi_apply(E, m, n, Cs[nl * EPI_LD + ml]);
+        }
+      }
+      if (P.flags & SYM_MIRROR) {
+        if (interior && !E.in1a && !E.in2a) {
+          constexpr int NWARPS = NTHREADS / 32, NBLK = SW / 32, GROUPS = NWARPS / NBLK, PAIRS = BM / 2 / GROUPS;
+          const int nl = 32 * (warp % NBLK) + lane, grp = warp / NBLK;
+          const bool odd = lane & 1;
+          const int64_t n = nbase + nl - (odd ? 1 : 0);
+#pragma unroll 4
+          for (int i = 0; i < PAIRS; ++i) {
+            const int ml = 2 * (grp + GROUPS * i);
+            const double a = Cs[nl * EPI_LD + ml], b = Cs[nl * EPI_LD + ml + 1];
+            const double pa = __shfl_xor_sync(0xffffffffu, a, 1), pb = __shfl_xor_sync(0xffffffffu, b, 1);
+            const double lo = odd ? pb : a, hi = odd ? b : pa;
+            const int64_t m = m0 + ml + (odd ? 1 : 0);
+            if (E.out1)
+              *reinterpret_cast<double2*>(E.out1 + n + m * E.ld1) = make_double2(__dmul_rn(E.a1, lo), __dmul_rn(E.a1, hi));
+            if (E.out2)
+              *reinterpret_cast<double2*>(E.out2 + n + m * E.ld2) = make_double2(__dmul_rn(E.a2, lo), __dmul_rn(E.a2, hi));
+          }
+        } else {
+          for (int idx = tid; idx < BM * SW; idx += NTHREADS) {
+            const int nl = idx % SW, ml = idx / SW;
+            const int m = m0 + ml, n = nbase + nl;
+            if (m >= P.M || n >= P.N) continue;
+            if (diag && m <= n) continue;
+            epi_apply(E, n, m, Cs[nl * EPI_LD + ml]);
+          }
+        }
+      }
+      cbar();
+    }
+  }
+}
+
+template <bool AK, bool BKI, class C>
+void launch_pws(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& ma2, const CUtensorMap& mb2,
+                const KParams& P, int ntiles) {
+  constexpr int smem = pws_smem_bytes<C>();
+  static bool attr_set = false;
+  if (!attr_set) {
+    CGGM_CUDA_CHECK(cudaFuncSetAttribute(gemm_dmma_pws<AK, BKI, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CGGM_CUDA_CHECK(cudaFuncSetAttribute(gemm_dmma_pws<AK, BKI, C>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         (int)cudaSharedmemCarveoutMaxShared));
+    attr_set = true;
+  }
+  const int tpc = c->persist_tpc, R = c->num_sms;
+  const int full = ntiles / (R * tpc), rem = ntiles - full * R * tpc;
+  const int grid = full * R + (rem + tpc - 1) / tpc;
+  Prof pr(c, c->cur_tag);
+  gemm_dmma_pws<AK, BKI, C><<<grid, C::NTHREADS + 128, smem, c->stream>>>(ma, mb, ma2, mb2, P, ntiles, tpc, R);
+  post_launch(c, "gemm_dmma_pws");
+}
+
 // CGGM_GEMM_LOG=1: one stderr line per launch with the MMA flops the tiles execute (triangular
 // k-ranges applied per tile), for joining with an ncu launch list (per-launch efficiency)
 void gemm_log(Ctx* c, int BM, int BN, int M, int N, int K, int flags, int grid, bool tA, bool tB) {
@@ -776,6 +1059,15 @@ void run_cfg(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t Kef
   CUtensorMap mb2 = b_tail ? make_map(c, B, ldb, N, Keff, 16, 16) : mb;
   const bool AK = transA, BKI = !transB;
   gemm_log(c, C::BM, C::BN, P.M, P.N, P.K, P.flags, grid, transA, transB);
+  if constexpr (C::WSP) {
+    if (C::BN == 128 && c->persist_tpc > 0 && P.ksplit == 1 && grid >= 2 * c->num_sms) {
+      if (AK && BKI) launch_pws<true, true, C>(c, ma, mb, ma2, mb2, P, grid);
+      else if (AK && !BKI) launch_pws<true, false, C>(c, ma, mb, ma2, mb2, P, grid);
+      else if (!AK && BKI) launch_pws<false, true, C>(c, ma, mb, ma2, mb2, P, grid);
+      else launch_pws<false, false, C>(c, ma, mb, ma2, mb2, P, grid);
+      return;
+    }
+  }
   if (AK && BKI) launch<true, true, C>(c, ma, mb, ma2, mb2, P, grid);
   else if (AK && !BKI) launch<true, false, C>(c, ma, mb, ma2, mb2, P, grid);
   else if (!AK && BKI) launch<false, true, C>(c, ma, mb, ma2, mb2, P, grid);
