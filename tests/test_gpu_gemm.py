@@ -168,3 +168,52 @@ def test_gemm_small_trapezoid_inplace_update(ctx):
     ref = C0 - A @ A[:N].T
     np.testing.assert_allclose(out[mask], ref[mask], rtol=1e-12, atol=1e-12)
     np.testing.assert_array_equal(out[~mask], C0[~mask])
+
+
+@pytest.fixture(scope="module", params=[2, 3], ids=["persist2", "persist3"])
+def pctx(request):
+    """The persistent warp-specialised 128x128 kernel (CGGM_PERSIST_TPC): engaged for grids of at
+    least two tiles per SM, so the shapes below span >= 296 tiles with ragged edges."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import os
+    from paper_1509_04681_b200 import Context
+    os.environ["CGGM_PERSIST_TPC"] = str(request.param)
+    try:
+        c = Context(0)
+    finally:
+        os.environ.pop("CGGM_PERSIST_TPC", None)
+    c._check(c.lib.cggm_test_set_tile(c.h, 1))
+    return c
+
+
+@pytest.mark.parametrize("tA", [False, True])
+@pytest.mark.parametrize("tB", [False, True])
+@pytest.mark.parametrize("M,N,K", [(2600, 2410, 100), (4100, 1290, 37)])
+def test_gemm_persistent(pctx, tA, tB, M, N, K):
+    rng = np.random.default_rng(M + N + K)
+    A = rng.standard_normal((K, M) if tA else (M, K))
+    B = rng.standard_normal((N, K) if tB else (K, N))
+    C0 = rng.standard_normal((M, N))
+    ref = 1.5 * ((A.T if tA else A) @ (B.T if tB else B)) + 0.25 * C0
+    out = run(pctx, tA, tB, A, B, C0, 1.5, 0.25, 0, M, N, K)
+    assert np.linalg.norm(out - ref) / np.linalg.norm(ref) < 1e-14
+
+
+@pytest.mark.parametrize("flags", [SYM_LOWER | SYM_MIRROR, SYM_LOWER, B_KLE_N])
+def test_gemm_persistent_structured(pctx, flags):
+    q, K = 2500, 2500 if flags == B_KLE_N else 90
+    rng = np.random.default_rng(flags)
+    A = rng.standard_normal((q, K))
+    if flags == B_KLE_N:
+        B = np.triu(rng.standard_normal((K, q)))   # B[k][n] = 0 for k > n: B_KLE_N shortens the k-range
+        ref = A @ B
+        out = run(pctx, False, False, A, B, np.zeros((q, q)), 1.0, 0.0, flags, q, q, K)
+        assert np.linalg.norm(out - ref) / np.linalg.norm(ref) < 1e-14
+        return
+    ref = A @ A.T
+    out = run(pctx, False, True, A, A, np.zeros((q, q)), 1.0, 0.0, flags, q, q, K)
+    lo = np.tril_indices(q)
+    assert np.linalg.norm(out[lo] - ref[lo]) / np.linalg.norm(ref[lo]) < 1e-14
+    if flags & SYM_MIRROR:
+        np.testing.assert_array_equal(out, out.T)
