@@ -946,11 +946,9 @@ void lambda_cd_coop(Ctx* c, int q, const double* S, int64_t lds, const double* P
     list_colptr(c, q, Lr, Lc, m, cnt, scr, lp);
     const size_t smem_pf = (size_t)4 * ((q + 1) & ~1) * 8;
     if (q >= 2048 && q <= CO_QMAX && smem_pf <= 200 * 1024 && lds % 2 == 0 && ldp % 2 == 0 && c->cd_prefetch) {
-      static bool attr_pf = false;
-      if (!attr_pf) {
+      CGGM_ONCE_PER_DEVICE({
         CGGM_CUDA_CHECK(cudaFuncSetAttribute(k_lambda_sweep_pf, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr_pf = true;
-      }
+      });
       int grid = c->num_sms;
       void* args[] = {&q, &S, &lds, &P, &ldp, &Lr, &coef, &lp, &passes, &D, &dmu, &U, &Z, &ldu};
       CGGM_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_lambda_sweep_pf, dim3(grid), dim3(CO_NT), args, smem_pf,
@@ -962,11 +960,9 @@ void lambda_cd_coop(Ctx* c, int q, const double* S, int64_t lds, const double* P
     }
     const size_t smem = (size_t)2 * q * 8;
     const int use_smem = smem <= 200 * 1024 ? 1 : 0;
-    static bool attr = false;
-    if (!attr) {
+    CGGM_ONCE_PER_DEVICE({
       CGGM_CUDA_CHECK(cudaFuncSetAttribute(k_lambda_sweep_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr = true;
-    }
+    });
     int grid = c->num_sms;
     void* args[] = {&q, &S, &lds, &P, &ldp, &Lr, &coef, &lp, &passes, &D, &dmu, &U, &Z, &ldu, &colbuf,
                     const_cast<int*>(&use_smem)};
@@ -994,11 +990,9 @@ void theta_cd_coop(Ctx* c, int p, int q, const double* S, int64_t lds, const dou
     int grid = c->num_sms;
     const size_t smem_pf = (size_t)2 * ((p + 1) & ~1) * 8;
     if (p >= 2048 && p <= CO_PMAX && smem_pf <= 200 * 1024 && ldx % 2 == 0 && c->cd_prefetch) {
-      static bool attr_pf = false;
-      if (!attr_pf) {
+      CGGM_ONCE_PER_DEVICE({
         CGGM_CUDA_CHECK(cudaFuncSetAttribute(k_theta_sweep_pf, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr_pf = true;
-      }
+      });
       void* args[] = {&p, &q, &S, &lds, &Sxx, &ldx, &Tr, &coef, &lp, &lam, &passes, &T, &dmu, &V, &ldv};
       CGGM_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_theta_sweep_pf, dim3(grid), dim3(CO_NT), args, smem_pf,
                                                   c->stream));
@@ -1009,11 +1003,9 @@ void theta_cd_coop(Ctx* c, int p, int q, const double* S, int64_t lds, const dou
     }
     const size_t smem = (size_t)p * 8;
     const int use_smem = smem <= 200 * 1024 ? 1 : 0;
-    static bool attr = false;
-    if (!attr) {
+    CGGM_ONCE_PER_DEVICE({
       CGGM_CUDA_CHECK(cudaFuncSetAttribute(k_theta_sweep_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr = true;
-    }
+    });
     void* args[] = {&p, &q, &S, &lds, &Sxx, &ldx, &Tr, &coef, &lp, &lam, &passes, &T, &dmu, &V, &ldv, &colbuf,
                     const_cast<int*>(&use_smem)};
     CGGM_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_theta_sweep_coop, dim3(grid), dim3(CO_NT), args,

@@ -603,19 +603,15 @@ void leaf(Rec<T>& R, ViewT<T> A, ViewT<T> X, int64_t col0) {
     xp = R.leafinv + (col0 / NB) * NB * NB;
     ldx = NB;
   }
-  static bool attr = false;
-  if (!attr) {
+  CGGM_ONCE_PER_DEVICE({
     CGGM_CUDA_CHECK(cudaFuncSetAttribute(leaf_potrf_trtri<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, leaf_smem_bytes<T>()));
-    attr = true;
-  }
+  });
   Prof pr(R.c, TAG_CHOL_LEAF);
   if (R.full_inverse && !R.c->leaf_sweep) {
-    static bool attr2 = false;
-    if (!attr2) {
+    CGGM_ONCE_PER_DEVICE({
       CGGM_CUDA_CHECK(cudaFuncSetAttribute(leaf_rec_inverse<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            leaf_smem_bytes<T>()));
-      attr2 = true;
-    }
+    });
     leaf_rec_inverse<T><<<1, LEAF_THREADS, leaf_smem_bytes<T>(), R.c->stream>>>(A.p, A.ld, nb, xp, ldx,
                                                                                R.logdet_slots + col0 / NB, R.fail_col,
                                                                                (int)col0);

@@ -5,6 +5,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <string>
@@ -237,6 +238,20 @@ struct CudaError {
     cudaError_t _e = (expr);                                                                   \
     if (_e != cudaSuccess)                                                                     \
       throw ::cggm::CudaError{CGGM_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)}; \
+  } while (0)
+
+// Kernel attributes (cudaFuncSetAttribute) apply to the CURRENT device only: run the setup once per
+// device (one bit per ordinal), so contexts on several GPUs in one process each get them.
+#define CGGM_ONCE_PER_DEVICE(...)                                       \
+  do {                                                                  \
+    static std::atomic<uint64_t> _done{0};                              \
+    int _dev = 0;                                                       \
+    CGGM_CUDA_CHECK(cudaGetDevice(&_dev));                              \
+    const uint64_t _bit = uint64_t(1) << (_dev & 63);                   \
+    if (!(_done.load(std::memory_order_acquire) & _bit)) {              \
+      __VA_ARGS__;                                                      \
+      _done.fetch_or(_bit, std::memory_order_acq_rel);                  \
+    }                                                                   \
   } while (0)
 
 // After every launch: count it and surface launch errors.

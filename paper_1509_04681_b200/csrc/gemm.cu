@@ -666,12 +666,10 @@ void launch_small(Ctx* c, const double* A, int64_t lda, const double* B, int64_t
   const bool aligned = (reinterpret_cast<uintptr_t>(A) % 16 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0) &&
                        lda % 2 == 0 && ldb % 2 == 0 && !c->no_small_async;
   if (aligned) {
-    static bool attr = false;
-    if (!attr) {
+    CGGM_ONCE_PER_DEVICE({
       CGGM_CUDA_CHECK(cudaFuncSetAttribute(gemm_small_async_kernel<TA, TB>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, SA_SMEM));
-      attr = true;
-    }
+    });
     gemm_small_async_kernel<TA, TB><<<grid, 128, SA_SMEM, c->stream>>>(A, lda, B, ldb, P);
     post_launch(c, "gemm_small_async_kernel");
   } else {
@@ -712,15 +710,13 @@ CUtensorMap make_map(Ctx* c, const double* ptr, int64_t ld, int64_t inner, int64
 template <bool AK, bool BKI, class C>
 void launch(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& ma2, const CUtensorMap& mb2,
             const KParams& P, int grid) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  CGGM_ONCE_PER_DEVICE({
     CGGM_CUDA_CHECK(cudaFuncSetAttribute(gemm_dmma_kernel<AK, BKI, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::SMEM_BYTES));
     // the largest shared-memory carveout, so that configurations sized for 2-3 CTAs per SM get them
     CGGM_CUDA_CHECK(cudaFuncSetAttribute(gemm_dmma_kernel<AK, BKI, C>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          (int)cudaSharedmemCarveoutMaxShared));
-    attr_set = true;
-  }
+  });
   Prof pr(c, c->cur_tag);
   gemm_dmma_kernel<AK, BKI, C><<<grid, C::LB_THREADS, C::SMEM_BYTES, c->stream>>>(ma, mb, ma2, mb2, P);
   post_launch(c, "gemm_dmma_kernel");
@@ -994,13 +990,11 @@ template <bool AK, bool BKI, class C>
 void launch_pws(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& ma2, const CUtensorMap& mb2,
                 const KParams& P, int ntiles) {
   constexpr int smem = pws_smem_bytes<C>();
-  static bool attr_set = false;
-  if (!attr_set) {
+  CGGM_ONCE_PER_DEVICE({
     CGGM_CUDA_CHECK(cudaFuncSetAttribute(gemm_dmma_pws<AK, BKI, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     CGGM_CUDA_CHECK(cudaFuncSetAttribute(gemm_dmma_pws<AK, BKI, C>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          (int)cudaSharedmemCarveoutMaxShared));
-    attr_set = true;
-  }
+  });
   const int tpc = c->persist_tpc, R = c->num_sms;
   const int full = ntiles / (R * tpc), rem = ntiles - full * R * tpc;
   const int grid = full * R + (rem + tpc - 1) / tpc;

@@ -260,11 +260,9 @@ CUtensorMap make_map_f_mn3d(Ctx* c, const float* ptr, int64_t ld, int64_t X, int
 
 template <bool AK, bool BKI>
 void launch_f(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KParamsF& P, int grid) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  CGGM_ONCE_PER_DEVICE({
     CGGM_CUDA_CHECK(cudaFuncSetAttribute(gemm_ffma_kernel<AK, BKI>, cudaFuncAttributeMaxDynamicSharedMemorySize, F_SMEM));
-    attr_set = true;
-  }
+  });
   Prof pr(c, c->cur_tag);
   gemm_ffma_kernel<AK, BKI><<<grid, FNT, F_SMEM, c->stream>>>(ma, mb, P);
   post_launch(c, "gemm_ffma_kernel");
