@@ -32,6 +32,9 @@ constexpr int BK = 16;
 #ifndef CGGM_WS
 #define CGGM_WS 1
 #endif
+#ifndef CGGM_MID_CTAS
+#define CGGM_MID_CTAS 2
+#endif
 constexpr int STAGES = 4;
 constexpr int GROUP_N = 8;
 #ifndef CGGM_SYM_BAND
@@ -62,7 +65,10 @@ struct Cfg {
   // loop and the epilogue at up to 232 registers; no consumer warp ever waits on a ring slot
   static constexpr bool WSP = CGGM_WS && (WTM >= 64 && WTN >= 32);
   static constexpr int LB_THREADS = NTHREADS + (WSP ? 128 : 0);
-  static constexpr int LB_MINB = WSP ? 1 : 65536 / (NTHREADS * MAXREG);
+  // a warp-specialised 4-consumer-warp tile (128x64) runs two CTAs per SM: 2 x 256 threads x 128
+  // registers at launch; the consumers raise to 216 with what the producer warpgroup donates
+  static constexpr int LB_MINB = WSP ? (NTHREADS == 128 ? CGGM_MID_CTAS : 1) : 65536 / (NTHREADS * MAXREG);
+  static constexpr int CONS_REG = (WSP && NTHREADS == 128 && CGGM_MID_CTAS == 2) ? 216 : 232;
   static_assert(FM % 2 == 0 && FN % 2 == 0, "MN-inner fragments come in pairs");
   static_assert(BM % 16 == 0 && BN % 16 == 0, "16-wide TMA boxes");
 };
@@ -259,7 +265,7 @@ __global__ void __launch_bounds__(C::LB_THREADS, C::LB_MINB)
         }
       return;
     }
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(C::CONS_REG) : "memory");
   }
 
   double acc[FM][FN][2];
