@@ -482,7 +482,14 @@ def main():
 
     # ---------------------------------------------------------------- e2e through the public API
     e2e = None
-    if not args.no_e2e and world == 1:
+    need_gt = 8.0 * P.p * P.q if args.stream_grad_theta else 0.0
+    if not args.no_e2e and world == 1 and need_gt > 0.95 * torch.cuda.mem_get_info()[0]:
+        # the host-buffer entry point returns the dense grad_Theta; beside the streamed path's
+        # buffers it does not fit at this size
+        e2e = {"value": None, "unit": UNIT, "skipped": f"cggm_newton_eval_host stores the dense p x q grad_Theta "
+                                                       f"({need_gt / 2**30:.1f} GiB), more than the free device memory "
+                                                       f"beside the streamed evaluation's buffers"}
+    elif not args.no_e2e and world == 1:
         # the public host-buffer entry point: X, Y and the CSCs from page-locked host memory, uploaded
         # by the library (Lambda first, the factorisation overlapping the X / Y transfers), S_yy formed
         # in the call, the scalar results read back
