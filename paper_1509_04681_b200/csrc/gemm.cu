@@ -1150,7 +1150,7 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
   const double big_eff = (double)big_tiles / (double)(waves * c->num_sms);
   const bool auto_big = big_tiles >= 3 * c->num_sms || big_eff >= 0.9;
   const bool use_big = c->force_tile ? (c->force_tile == 1) : auto_big;
-  if (use_big && c->mid_tile && !(flags & (SYM_LOWER | SPLIT_K2))) run_cfg<CfgMid>(c, transA, transB, M, N, Keff, A, lda, B, ldb, P);
+  if (use_big && c->mid_tile && !(flags & SYM_LOWER) && (c->mid_tile > 1 || !(flags & SPLIT_K2))) run_cfg<CfgMid>(c, transA, transB, M, N, Keff, A, lda, B, ldb, P);
   else if (use_big) run_cfg<CfgBig>(c, transA, transB, M, N, Keff, A, lda, B, ldb, P);
   else run_cfg<CfgSmall>(c, transA, transB, M, N, Keff, A, lda, B, ldb, P);
 }
