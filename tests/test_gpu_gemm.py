@@ -12,21 +12,27 @@ pytestmark = pytest.mark.gpu
 A_KLE_M, A_KGE_M, B_KLE_N, B_KGE_N, SYM_LOWER, SYM_MIRROR = 1, 2, 4, 8, 16, 32
 
 
-@pytest.fixture(scope="module", params=[0, 1, 2, 5, 6, "direct"],
-                ids=["auto_small", "tile128", "tile64", "tile128_2d", "tile64_2d", "auto_small_direct"])
+@pytest.fixture(scope="module", params=[0, 1, "big", 2, 5, 6, "direct"],
+                ids=["auto_small", "tile128", "tile128_square", "tile64", "tile128_2d", "tile64_2d", "auto_small_direct"])
 def ctx(request):
-    """auto_small: small shapes on the cp.async kernel; auto_small_direct: on the direct-load one."""
+    """auto_small: small shapes on the cp.async kernel; auto_small_direct: on the direct-load one;
+    tile128: non-symmetric products on the two-CTA 128x64 tiles (the default), symmetric ones on
+    128x128; tile128_square: everything on 128x128 (CGGM_MID_TILE=0)."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import os
     from paper_1509_04681_b200 import Context
     direct = request.param == "direct"
     os.environ["CGGM_NO_SMALL_ASYNC"] = "1" if direct else "0"
+    if request.param == "big":
+        os.environ["CGGM_MID_TILE"] = "0"
     try:
         c = Context(0)
     finally:
         os.environ.pop("CGGM_NO_SMALL_ASYNC", None)
-    c._check(c.lib.cggm_test_set_tile(c.h, 0 if direct else request.param))
+        os.environ.pop("CGGM_MID_TILE", None)
+    tile = {"direct": 0, "big": 1}.get(request.param, request.param)
+    c._check(c.lib.cggm_test_set_tile(c.h, tile))
     return c
 
 
@@ -179,10 +185,12 @@ def pctx(request):
     import os
     from paper_1509_04681_b200 import Context
     os.environ["CGGM_PERSIST_TPC"] = str(request.param)
+    os.environ["CGGM_MID_TILE"] = "0"   # the persistent kernel is the 128x128 configuration
     try:
         c = Context(0)
     finally:
         os.environ.pop("CGGM_PERSIST_TPC", None)
+        os.environ.pop("CGGM_MID_TILE", None)
     c._check(c.lib.cggm_test_set_tile(c.h, 1))
     return c
 
