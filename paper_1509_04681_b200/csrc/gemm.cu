@@ -86,6 +86,8 @@ struct KParams {
   int vec;       // epilogue outputs / inputs 16-B aligned with even leading dimensions, no in1b / in2b:
                  // interior tiles take the paired (double2) epilogue
   int ksplit;    // 1, or 2 (SPLIT_K2): CTA 2t + h computes k-half h of tile t
+  int sym_split; // SYM_LOWER with BN = BM / 2: the walk runs over BM x BM squares (tilesM / tilesN
+                 // count squares), tile 2s + h is column half h of square s
   Epilogue epi;
 };
 
@@ -95,6 +97,8 @@ struct KParams {
 // Triangular k-ranges are scheduled longest-first (LPT) to shorten the tail wave.
 __device__ __forceinline__ void tile_coords(const KParams& P, int t, int& I, int& J) {
   if (P.flags & SYM_LOWER) {
+    const int half = P.sym_split == 2 ? (t & 1) : 0;
+    if (P.sym_split == 2) t >>= 1;
     // lower triangle part (rows I < tilesN) in bands of SYM_BAND tile rows, band by band (I
     // ascending: longest k-ranges first for A_KGE_M / B_KGE_N), column by column inside a band:
     // the CTAs in flight share the band's row panels and each column panel, so the panels are read
@@ -129,6 +133,7 @@ __device__ __forceinline__ void tile_coords(const KParams& P, int t, int& I, int
       I = P.tilesN + r / P.tilesN;
       J = r % P.tilesN;
     }
+    if (P.sym_split == 2) J = 2 * J + half;
     return;
   }
   const int per_group = GROUP_N * P.tilesM;
@@ -195,8 +200,8 @@ __global__ void __launch_bounds__(C::LB_THREADS, C::LB_MINB)
   if (P.flags & A_KLE_M) kend = min(kend, m0 + BM);
   if (P.flags & B_KLE_N) kend = min(kend, n0 + BN);
   int kt0 = kbeg / BK;
-  int nkt = kend > kbeg ? (kend - kt0 * BK + BK - 1) / BK : 0;
-  if (P.ksplit > 1) {   // this CTA's share of the k-tiles
+  int nkt = kend > kbeg && n0 < P.N ? (kend - kt0 * BK + BK - 1) / BK : 0;   // (a split square's
+  if (P.ksplit > 1) {                                                        //  half past N: no work)   // this CTA's share of the k-tiles
     const int per = (nkt + P.ksplit - 1) / P.ksplit;
     kt0 += part * per;
     nkt = max(0, min(per, nkt - part * per));
@@ -362,7 +367,7 @@ __global__ void __launch_bounds__(C::LB_THREADS, C::LB_MINB)
     }
   }
   cbar();
-  const bool diag = (P.flags & SYM_LOWER) && I == J;
+  const bool diag = (P.flags & SYM_LOWER) && m0 < n0 + BN;   // the tile reaches above the diagonal
   if (P.ksplit > 1) {   // partial sum of this k-half into out1 (zeros + two partials: order-free)
     for (int idx = tid; idx < BM * BN; idx += NTHREADS) {
       const int ml = idx % BM, nl = idx / BM;
@@ -897,7 +902,7 @@ __global__ void __launch_bounds__(C::NTHREADS + 128, 1)
     }
     // ---------------------------------------------------------- epilogue, half a tile per round
     const int m0 = I * BM, n0 = J * BN;
-    const bool diag = (P.flags & SYM_LOWER) && I == J;
+    const bool diag = (P.flags & SYM_LOWER) && m0 < n0 + BN;
     const bool interior = P.vec && !diag && m0 + BM <= P.M && n0 + BN <= P.N;
     const Epilogue& E = P.epi;
 #pragma unroll 1
@@ -1040,8 +1045,13 @@ void run_cfg(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t Kef
              const double* B, int64_t ldb, KParams& P) {
   P.tilesM = (int)((M + C::BM - 1) / C::BM);
   P.tilesN = (int)((N + C::BN - 1) / C::BN);
+  P.sym_split = 1;
+  if ((P.flags & SYM_LOWER) && C::BN * 2 == C::BM) {   // walk BM x BM squares, two column halves each
+    P.sym_split = 2;
+    P.tilesN = (int)((N + C::BM - 1) / C::BM);
+  }
   int grid;
-  if (P.flags & SYM_LOWER) grid = P.tilesN * (P.tilesN + 1) / 2 + (P.tilesM - P.tilesN) * P.tilesN;
+  if (P.flags & SYM_LOWER) grid = (P.tilesN * (P.tilesN + 1) / 2 + (P.tilesM - P.tilesN) * P.tilesN) * P.sym_split;
   else grid = P.tilesM * P.tilesN;
   grid *= P.ksplit;
   // K-inner operand: dims {K, X}, box {16, BX}; MN-inner: dims {X, K}, box {16, 16}
@@ -1150,7 +1160,13 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
   const double big_eff = (double)big_tiles / (double)(waves * c->num_sms);
   const bool auto_big = big_tiles >= 3 * c->num_sms || big_eff >= 0.9;
   const bool use_big = c->force_tile ? (c->force_tile == 1) : auto_big;
-  if (use_big && c->mid_tile && !(flags & SYM_LOWER) && (c->mid_tile > 1 || !(flags & SPLIT_K2))) run_cfg<CfgMid>(c, transA, transB, M, N, Keff, A, lda, B, ldb, P);
+  // CGGM_MID_TILE (two-CTA 128x64 tiles for): 3 = every large product (default; the step 410.2 ->
+  // 409.7 ms against 4, although lauum alone is 74.46 -> 74.58 ms: its k-loop hides the epilogue,
+  // but the co-running streams gain), 1 = non-symmetric and symmetric with K <= 4096, 2 = 1 plus
+  // split-k, 4 = non-symmetric only; 0 = 128x128 everywhere
+  const bool mid_sym = c->mid_tile == 3 || (c->mid_tile != 4 && Keff <= 4096);
+  if (use_big && c->mid_tile && (mid_sym || !(flags & SYM_LOWER)) && (c->mid_tile == 2 || c->mid_tile == 3 || !(flags & SPLIT_K2)))
+    run_cfg<CfgMid>(c, transA, transB, M, N, Keff, A, lda, B, ldb, P);
   else if (use_big) run_cfg<CfgBig>(c, transA, transB, M, N, Keff, A, lda, B, ldb, P);
   else run_cfg<CfgSmall>(c, transA, transB, M, N, Keff, A, lda, B, ldb, P);
 }
