@@ -14,7 +14,8 @@ Pins (tests/test_oracle_pins.py, `-m "not gpu"`): P1 scalar worked example (SPEC
 S:161), P2 (I,0) closed form, P3/P4/P5 chain closed forms (logdet, Sigma, PD boundary),
 P6 SPEC logdet examples, P7 Sigma Lambda = I, P8 central finite differences, P9 Psi PSD and
 explicit-S_xx route, P10 trace identities, P11 two gradient routes, P12 active-set examples,
-P13 1x1 optimum, P14 convexity, P15 eigenvalue logdet / library inverse, P16 generating-point
+P13 1x1 optimum and a hand-worked q = 3 ||grad^S||_1 (both triangles, unpenalised
+diagonal), P14 convexity, P15 eigenvalue logdet / library inverse, P16 generating-point
 identity I7, P17 shard partial sums, plus a density-based pin of g (multivariate normal
 log-likelihood, reading A1).  Tie-band entries of the active sets are "parity unpinned" by
 design (excluded from comparisons and counted).

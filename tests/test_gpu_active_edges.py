@@ -35,10 +35,14 @@ def ctx_for(variant):
     return _CTX[variant]
 
 
-def case(p, q, seed):
+def case(p, q, seed, drop_diag=False):
     rng = np.random.default_rng(seed)
     G = rng.standard_normal((q, q))
     GL = (G + G.T) / 2.0
+    if drop_diag:   # unpenalised-diagonal case: exact zeros and tiny values on the diagonal
+        d = np.arange(q)
+        GL[d[::3], d[::3]] = 0.0
+        GL[d[1::5], d[1::5]] = 1e-300
     GT = rng.standard_normal((p, q))
     # symmetric Lambda support: diagonal, random off-diagonal pairs (some with small gradients), and
     # one explicit stored zero (reading A7: value test)
@@ -47,6 +51,8 @@ def case(p, q, seed):
         i, j = rng.integers(0, q, 2)
         pairs.add((int(i), int(j)))
         pairs.add((int(j), int(i)))
+    if drop_diag:   # the diagonal is then decided by the gradient alone (lam_ii = 0)
+        pairs = {(i, j) for (i, j) in pairs if i != j} or {(0, 0)}
     rows, cols = zip(*sorted(pairs))
     vals = rng.uniform(0.1, 0.5, len(rows)) * rng.choice([-1.0, 1.0], len(rows))
     for k, (r, c) in enumerate(zip(rows, cols)):
@@ -69,20 +75,25 @@ def case(p, q, seed):
     return GL, GT, lam, th
 
 
+@pytest.mark.parametrize("diag", ["penalised", "unpenalised", "unpenalised_nodiag"])
 @pytest.mark.parametrize("variant", list(VARIANTS))
 @pytest.mark.parametrize("p,q", [(1, 1), (3, 2), (64, 63), (65, 64), (130, 65), (200, 127), (129, 128),
                                  (2049, 129), (300, 257), (70, 1000), (4100, 33)])
-def test_active_lists_edge_sizes(variant, p, q):
+def test_active_lists_edge_sizes(variant, p, q, diag):
+    """penalize_diag = 0 (reading A3: lam_ii = 0) on every kernel path: with the diagonal stored in
+    Lambda (forced active, the subgradient uses |g_ii|) and with it absent from the support (the
+    diagonal then enters iff |g_ii| > 0, exact zeros do not, 1e-300 does)."""
     from paper_1509_04681_b200 import DeviceCsc, to_device_colmajor
     c = ctx_for(variant)
-    GL, GT, lam, th = case(p, q, seed=1000 * p + q)
+    pen = diag == "penalised"
+    GL, GT, lam, th = case(p, q, seed=1000 * p + q, drop_diag=diag == "unpenalised_nodiag")
     lam_L, lam_T = 0.6, 1.2
-    ref = O.active_set(GL, GT, lam, th, lam_L, lam_T)
+    ref = O.active_set(GL, GT, lam, th, lam_L, lam_T, penalize_diag=pen)
     got = c.cggm_active_set(to_device_colmajor(GL), to_device_colmajor(GT), DeviceCsc.from_host(lam),
-                            DeviceCsc.from_host(th), lam_L, lam_T)
+                            DeviceCsc.from_host(th), lam_L, lam_T, penalize_diag=pen)
     assert (got["m_L"], got["m_T"]) == (ref["m_L"], ref["m_T"])
     assert (got["ties_L"], got["ties_T"]) == (ref["ties_L"], ref["ties_T"])
     for key in ("L_row", "L_col", "T_row", "T_col"):
         assert np.array_equal(got[key].cpu().numpy(), ref[key]), key
-    sub = O.min_norm_subgradient(GL, GT, lam, th, lam_L, lam_T)
+    sub = O.min_norm_subgradient(GL, GT, lam, th, lam_L, lam_T, penalize_diag=pen)
     assert got["subgrad_l1"] == pytest.approx(sub, rel=1e-12, abs=1e-12)

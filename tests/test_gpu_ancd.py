@@ -171,10 +171,33 @@ def test_algorithm1_small_tight_tolerance_matches_prox_grad(ctx):
     assert g.f == pytest.approx(ref["f"], rel=1e-7)
 
 
+def _medium_oracle_sweeps(s, P, penalize_diag):
+    """The oracle's Lambda direction and Theta sweep on the GPU state's lists at `medium` (q = 4000,
+    p = 10000: the register / cp.async prefetch sweep path, q, p >= 2048), computed once."""
+    key = ("medium_oracle", penalize_diag)
+    if key not in _P:
+        act = s["active"]
+        Sig, Psi, G = (s[x].cpu().numpy() for x in ("Sigma", "Psi", "GradL"))
+        rows, cols = act["L_row"].cpu().numpy(), act["L_col"].cpu().numpy()
+        Lam = s["lam"].to_dense()
+        Dref, _, vals = A.lambda_newton_direction(Sig, Psi, G, Lam, rows, cols, P.lam_L, penalize_diag, 1)
+        lamM = np.full(Lam.shape, P.lam_L)
+        if not penalize_diag:
+            np.fill_diagonal(lamM, 0.0)
+        d_ref = float(np.sum(G * Dref)) + float(np.sum(lamM * (np.abs(Lam + Dref) - np.abs(Lam))))
+        trows, tcols = act["T_row"].cpu().numpy(), act["T_col"].cpu().numpy()
+        n = P.X.shape[0]
+        Tref, _ = A.theta_cd_sweep(Sig, P.X.T @ P.X / n, P.X.T @ P.Y / n, s["th"].to_dense(), trows, tcols,
+                                   P.lam_T, 1)
+        _P[key] = (vals, d_ref, Tref[trows, tcols], float(np.abs(Tref).sum()))
+    return _P[key]
+
+
 @pytest.mark.parametrize("variant", [{"CGGM_CD_COOP": "0"}, {"CGGM_CD_PREFETCH": "0"}, {}])
 def test_sweep_variants_agree_medium(variant):
     """The single-CTA sweeps, the column-batched cooperative sweeps and their register / prefetch
-    variants (taken at medium sizes) give the same direction and Theta to summation-order rounding."""
+    variants (taken at medium sizes, q, p >= 2048) give the same direction and Theta to summation-order
+    rounding, and each matches the oracle's sweeps on the same lists."""
     import os
     from paper_1509_04681_b200 import Context
     P = problem("medium")
@@ -198,3 +221,20 @@ def test_sweep_variants_agree_medium(variant):
     assert np.linalg.norm(D.cpu().numpy() - D0) <= 1e-10 * np.linalg.norm(D0)
     assert np.linalg.norm(Tn.val.cpu().numpy() - T0) <= 1e-10 * np.linalg.norm(T0)
     assert delta == pytest.approx(d0, rel=1e-9) and l1 == pytest.approx(l0, rel=1e-10)
+    vals, d_ref, tvals, tl1 = _medium_oracle_sweeps(s, P, True)
+    assert np.linalg.norm(D.cpu().numpy() - vals) <= 1e-10 * np.linalg.norm(vals)
+    assert delta == pytest.approx(d_ref, rel=1e-9)
+    assert np.linalg.norm(Tn.val.cpu().numpy() - tvals) <= 1e-9 * np.linalg.norm(tvals)
+    assert l1 == pytest.approx(tl1, rel=1e-9)
+
+
+def test_lambda_direction_medium_unpenalised_matches_oracle(ctx):
+    """penalize_diag = 0 on the q >= 2048 sweep path against the oracle (reading A3)."""
+    P = problem("medium")
+    s = _gpu_state(ctx, P, 0)
+    act = s["active"]
+    D, delta, _ = ctx.cggm_lambda_direction(s["Sigma"], s["Psi"], s["GradL"], s["Lg"], act["L_row"], act["L_col"],
+                                            P.lam_L, False, 1)
+    vals, d_ref, _, _ = _medium_oracle_sweeps(s, P, False)
+    assert np.linalg.norm(D.cpu().numpy() - vals) <= 1e-10 * np.linalg.norm(vals)
+    assert delta == pytest.approx(d_ref, rel=1e-9)

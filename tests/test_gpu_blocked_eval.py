@@ -53,6 +53,33 @@ def test_blocked_matches_dense_and_oracle(ctx, name, k, block):
         assert ob[key] == pytest.approx(od[key], rel=1e-11), key
     ref = O.objective(P.X, P.Y, lam, th, P.lam_L, P.lam_T)
     assert ob["f"] == pytest.approx(ref["f"], rel=1e-10)
+    # the lists directly against the oracle's definition, bit-exact outside the tie band
+    ora = _oracle_active(name, k)
+    for rk, ck, tm in (("L_row", "L_col", ora["tie_mask_L"]), ("T_row", "T_col", ora["tie_mask_T"])):
+        gr, gc = ab[rk].cpu().numpy().astype(np.int64), ab[ck].cpu().numpy().astype(np.int64)
+        for (i, j) in set(zip(gr.tolist(), gc.tolist())) ^ set(zip(ora[rk].tolist(), ora[ck].tolist())):
+            assert tm[i, j], (rk, i, j)
+        assert np.all(np.diff(gc * (1 << 31) + gr) > 0)
+    if ora["ties_L"] + ora["ties_T"] == 0:
+        assert (ab["m_L"], ab["m_T"]) == (ora["m_L"], ora["m_T"])
+    assert (ab["ties_L"], ab["ties_T"]) == (ora["ties_L"], ora["ties_T"])
+    assert ab["subgrad_l1"] == pytest.approx(ora["sub"], rel=1e-9)
+
+
+_ORA = {}
+
+
+def _oracle_active(name, k):
+    if (name, k) not in _ORA:
+        P = make_problem(name)
+        _, lam, th = P.points[k]
+        Syy, Sxy = O.covariances(P.X, P.Y)
+        Sig, _, _, _ = O.invert_logdet(lam.to_dense())
+        r = O.psi_grad(P.X, P.Y, th, Sig, Syy, Sxy)
+        a = O.active_set(r["GradL"], r["GradT"], lam, th, P.lam_L, P.lam_T)
+        a["sub"] = O.min_norm_subgradient(r["GradL"], r["GradT"], lam, th, P.lam_L, P.lam_T)
+        _ORA[(name, k)] = a
+    return _ORA[(name, k)]
 
 
 def test_blocked_non_pd(ctx):

@@ -13,6 +13,8 @@ mathematics fix, independent of the oracle's own formulas:
   P24  Armijo: the accepted Lambda is PD and decreases f; Lambda = I, D = -2I backtracks below 1/2
   P25  Algorithm 1 meets its stopping rule and its objective matches an independent joint
        proximal-gradient solver of Eq. (1) to 1e-6 relative (convexity)
+  P26  the quadratic model of Eq. (6) (lambda_surrogate) is the second-order Taylor expansion of the
+       oracle's g (Eq. 1 / Eq. 4) by central first and second differences
 """
 import math
 
@@ -103,6 +105,45 @@ def test_p19_p20_sweep_keeps_u_and_decreases_model():
     D2, U2, _ = A.lambda_newton_direction(Sigma, Psi, GradL, Lam, rows, cols, 0.05, passes=3)
     np.testing.assert_allclose(U2, D2 @ Sigma, atol=1e-12)
     np.testing.assert_array_equal(D2, D2.T)
+
+
+@pytest.mark.parametrize("seed", [21, 22, 23])
+def test_p26_lambda_surrogate_matches_g_by_finite_differences(seed):
+    """The quadratic model of Eq. (6) is the second-order Taylor expansion of g of Eq. (1) (P:270-282,
+    Eq. 4), checked against the oracle's g itself (O.objective with lam = 0) along random symmetric
+    directions D, with Theta != 0 so that Psi matters:
+      linear:    (g(L+tD) - g(L-tD)) / 2t            -> tr(GradL D)             (error O(t^2))
+      quadratic: (g(L+tD) + g(L-tD) - 2 g(L)) / 2t^2 -> 1/2 tr(DSDS) + tr(DSDP)  (error O(t^2))
+    The surrogate's quadratic part is read off lambda_surrogate at lam = 0 as
+    (m(tD) + m(-tD)) / 2t^2 (exact for a quadratic).  A wrong Hessian term (a dropped Psi term, a
+    factor 2, Sigma for Psi) changes the quadratic by O(1) relative and fails."""
+    from synth.cggm_inputs import csc_from_dense
+    X, Y, Lam, Theta = _instance(6, seed, p=8)
+    Sxx, Syy, Sxy, Sigma, Psi, GradL = _model_pieces(X, Y, Lam, Theta)
+    rng = np.random.default_rng(seed + 100)
+    tc = csc_from_dense(Theta)
+
+    def g(L):
+        return O.objective(X, Y, csc_from_dense(L), tc, 0.0, 0.0)["g"]
+
+    g0 = g(Lam)
+    for _ in range(3):
+        D = rng.standard_normal((6, 6))
+        D = 0.5 * (D + D.T)
+        t = 2e-4
+        gp, gm = g(Lam + t * D), g(Lam - t * D)
+        lin_fd = (gp - gm) / (2 * t)
+        quad_fd = (gp + gm - 2 * g0) / (2 * t * t)
+        mp = A.lambda_surrogate(t * D, GradL, Sigma, Psi, Lam, 0.0)
+        mm = A.lambda_surrogate(-t * D, GradL, Sigma, Psi, Lam, 0.0)
+        quad_model = (mp + mm) / (2 * t * t)
+        lin_model = (mp - mm) / (2 * t)
+        assert lin_model == pytest.approx(float(np.sum(GradL * D)), rel=1e-12)
+        assert lin_fd == pytest.approx(lin_model, rel=1e-6)
+        assert quad_fd == pytest.approx(quad_model, rel=1e-5)
+        # and the Psi term is not negligible here (the check would not see a Psi mistake otherwise)
+        DS = D @ Sigma
+        assert abs(np.trace(DS @ D @ Psi)) > 0.05 * abs(quad_model)
 
 
 @pytest.mark.parametrize("s", [0.3, 1.0, 2.5])

@@ -301,6 +301,72 @@ def test_p13_one_by_one_optimum():
     assert abs(stat) < 1e-12
 
 
+def _p13_hand_example():
+    """q = 3, p = 2 hand example for ||grad^S||_1 (SPEC S:183 per-coordinate rule,
+    reading A9: both triangles of Lambda, all of Theta).  lam_L = 0.5, lam_T = 0.25."""
+    Lam = np.array([[2.0, -0.4, 0.0],
+                    [-0.4, 1.0, 0.0],
+                    [0.0, 0.0, 1.5]])
+    GL = np.array([[0.3, -0.2, 0.8],
+                   [-0.2, 0.9, 0.1],
+                   [0.8, 0.1, -0.6]])
+    Th = np.array([[0.0, 1.0, 0.0],
+                   [-0.5, 0.0, 0.0]])
+    GT = np.array([[0.1, -0.3, 0.4],
+                   [0.2, 0.7, -0.25]])
+    return Lam, GL, Th, GT
+
+
+def test_p13_min_norm_subgradient_hand_example():
+    """Worked by hand, entry by entry (x != 0: |g + lam sign x|; x == 0: max(|g| - lam, 0)):
+      Lambda, diagonal penalised:   (0,0) |0.3+0.5| = 0.8   (1,1) |0.9+0.5| = 1.4   (2,2) |-0.6+0.5| = 0.1
+                                    (0,1),(1,0): x = -0.4 -> |-0.2-0.5| = 0.7 each  -> 1.4
+                                    (0,2),(2,0): x = 0    -> 0.8-0.5 = 0.3 each     -> 0.6
+                                    (1,2),(2,1): x = 0    -> max(0.1-0.5, 0) = 0    -> 0
+                                    sum 4.3   (one triangle only would give 3.3)
+      Lambda, diagonal unpenalised (lam_ii = 0): diagonal |0.3| + |0.9| + |-0.6| = 1.8, off-diagonal 2.0
+                                    sum 3.8   (keeping lam_ii would give 4.3)
+      Theta: (0,0) max(0.1-0.25,0)=0  (0,1) |-0.3+0.25| = 0.05  (0,2) 0.4-0.25 = 0.15
+             (1,0) |0.2-0.25| = 0.05  (1,1) 0.7-0.25 = 0.45   (1,2) |-0.25|-0.25 = 0 (exact tie)
+             sum 0.70
+    Totals: 5.0 (penalised diagonal), 4.5 (unpenalised)."""
+    Lam, GL, Th, GT = _p13_hand_example()
+    lc, tc = csc_from_dense(Lam), csc_from_dense(Th)
+    assert O.min_norm_subgradient(GL, GT, lc, tc, 0.5, 0.25, True) == pytest.approx(5.0, abs=1e-14)
+    assert O.min_norm_subgradient(GL, GT, lc, tc, 0.5, 0.25, False) == pytest.approx(4.5, abs=1e-14)
+    # the Theta part alone (Lambda = gradient-free identity with lam_L = 0 contributes 0)
+    z = np.zeros((3, 3))
+    assert O.min_norm_subgradient(z, GT, csc_from_dense(np.eye(3)), tc, 0.0, 0.25) == pytest.approx(0.70, abs=1e-14)
+
+
+def test_p12_active_set_unpenalised_diagonal():
+    """Reading A3 with penalize_diag = 0 (lam_ii = 0, strict '>'): every diagonal entry with
+    a nonzero gradient enters S_Lambda, an exactly-zero diagonal gradient does not; off-diagonal
+    entries still use lam_L.  Hand example, lam_L = 1.0: GL diagonal (0.3, 0, -0.6), (0,2) = 1.2,
+    (0,1) = 0.9, (1,2) = -1.0 (a tie with lam: not active), Lambda = I except Lambda_01 = 0.1."""
+    GL = np.array([[0.3, 0.9, 1.2],
+                   [0.9, 0.0, -1.0],
+                   [1.2, -1.0, -0.6]])
+    Lam = np.eye(3)
+    Lam[0, 1] = Lam[1, 0] = 0.1
+    GT = np.array([[0.5, -2.0, 0.0]])
+    th = csc_from_dense(np.array([[0.0, 0.0, 3.0]]))
+    lc = csc_from_dense(Lam)
+    a = O.active_set(GL, GT, lc, th, 1.0, 1.0, penalize_diag=True)
+    # penalised: (0,0), (1,1), (2,2) forced by Lambda = I; (0,1) forced by Lambda_01; (0,2) |1.2| > 1
+    assert list(zip(a["L_row"].tolist(), a["L_col"].tolist())) == [(0, 0), (0, 1), (1, 1), (0, 2), (2, 2)]
+    # unpenalised with a zero diagonal in Lambda: only the gradient decides the diagonal
+    Lam0 = Lam - np.diag(np.diag(Lam))
+    a0 = O.active_set(GL, GT, csc_from_dense(Lam0), th, 1.0, 1.0, penalize_diag=False)
+    assert list(zip(a0["L_row"].tolist(), a0["L_col"].tolist())) == [(0, 0), (0, 1), (0, 2), (2, 2)]
+    a1 = O.active_set(GL, GT, csc_from_dense(Lam0), th, 1.0, 1.0, penalize_diag=True)
+    assert list(zip(a1["L_row"].tolist(), a1["L_col"].tolist())) == [(0, 1), (0, 2)]
+    # Theta: |-2| > 1 and the stored 3.0; the diagonal flag does not touch Theta
+    assert list(zip(a0["T_row"].tolist(), a0["T_col"].tolist())) == [(0, 1), (0, 2)]
+    # the tie (1,2) is flagged in the tie band, the exact-zero diagonal (1,1) only when lam_ii = 0
+    assert a0["tie_mask_L"][1, 2] and a0["tie_mask_L"][1, 1] and not a1["tie_mask_L"][1, 1]
+
+
 # ------------------------------------------------------------------ P14 convexity
 def test_p14_convexity(tiny):
     P = tiny
