@@ -235,6 +235,45 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- launch
+def _free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def maybe_self_launch(args):
+    """`python bench.py --gpus N` without torchrun: re-launch as N ranks through
+    torch.distributed.run (one process per GPU, 127.0.0.1 rendezvous).  Under torchrun, WORLD_SIZE
+    must equal --gpus."""
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None:
+        if args.gpus > 1 and args.impl == "cggm":
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+                   "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__),
+                   *sys.argv[1:]]
+            sys.exit(subprocess.call(cmd))
+        return
+    if int(env_world) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_world}")
+
+
+def l2_note(P):
+    q2, pq = 8.0 * P.q * P.q, 8.0 * P.p * P.q
+    return (f"inputs larger than L2 (126 MB): Sigma/Psi/grad_Lambda {q2 / 1e9:.1f} GB each, "
+            f"grad_Theta {pq / 1e9:.1f} GB, X {8.0 * P.n * P.p / 1e9:.2f} GB")
+
+
+def gather_objects(obj, world):
+    import torch.distributed as dist
+    if world == 1:
+        return [obj]
+    out = [None] * world
+    dist.all_gather_object(out, obj)
+    return out
+
+
 # ----------------------------------------------------------------------------- GPU leg
 def main():
     ap = argparse.ArgumentParser()
@@ -250,12 +289,14 @@ def main():
                     help="N > 1: Sigma on rank 0 + broadcast, or the block-cyclic distributed inverse "
                          "(NEXT-3); auto = distributed from 3 GPUs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the eager / changing-Lambda step timings")
     ap.add_argument("--peak-seconds", type=float, default=2.0)
     ap.add_argument("--stream-grad-theta", action="store_true",
                     help="do not store the p x q grad_Theta (streamed into the active sets); default for `sharded`")
     args = ap.parse_args()
     if args.config == "sharded":
         args.stream_grad_theta = True
+    maybe_self_launch(args)
     if args.impl == "reference":
         run_reference(args)
         return
@@ -266,16 +307,23 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    # (CGGM_BENCH_DEVICE / CGGM_BENCH_BACKEND: functional smoke test of the multi-rank path on a
-    # one-GPU box -- every rank on one device over gloo; such a run's numbers are not measurements)
+    # (CGGM_BENCH_DEVICE / CGGM_BENCH_BACKEND: functional check of the multi-rank path on a one-GPU
+    # box -- every rank on one device over gloo; such a run's numbers are not measurements)
+    functional = "CGGM_BENCH_DEVICE" in os.environ
     local = int(os.environ.get("CGGM_BENCH_DEVICE", local))
+    if not functional and world > torch.cuda.device_count():
+        raise SystemExit(f"bench.py: {world} ranks but {torch.cuda.device_count()} visible GPU(s)")
     torch.cuda.set_device(local)
+    backend = os.environ.get("CGGM_BENCH_BACKEND", "nccl")
     if world > 1:
-        backend = os.environ.get("CGGM_BENCH_BACKEND", "nccl")
         if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")          # communicator rank / nranks in the log
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
+        print(f"[bench] rank {dist.get_rank()} of world {dist.get_world_size()} on cuda:{local} "
+              f"({backend})", file=sys.stderr, flush=True)
 
     from paper_1509_04681_b200 import Context, DeviceCsc, colmajor_empty
     from paper_1509_04681_b200.sharded import CudaBackend, ShardedEvaluator, shard_rows
@@ -317,9 +365,9 @@ def main():
     torch.cuda.synchronize()
     setup_ms = e0.elapsed_time(e1)
 
+    q, p = P.q, P.p
     if world == 1:
         # single GPU: fused active sets in the Psi/grad call, preallocated outputs
-        q, p = P.q, P.p
         bufs = {"Sigma": colmajor_empty(q, q), "Psi": colmajor_empty(q, q), "GradL": colmajor_empty(q, q)}
         if not args.stream_grad_theta:
             bufs["GradT"] = colmajor_empty(p, q)
@@ -334,7 +382,7 @@ def main():
             if getattr(exc, "status", None) != 6:
                 raise
         m = ctx.last_active_sizes
-        capL, capT = int(m[0] * 1.05) + 1024, int(m[1] * 1.05) + 1024
+        capL, capT = int(m[0] * 1.10) + 1024, int(m[1] * 1.10) + 1024
         for k, cap in (("L_row", capL), ("L_col", capL), ("T_row", capT), ("T_col", capT)):
             bufs[k] = torch.empty(cap, dtype=torch.int32, device="cuda")
 
@@ -345,32 +393,57 @@ def main():
         def step():
             return ev.evaluate(X, Y, Lam, Th, P.lam_L, P.lam_T, True)
 
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(fn, k, pre=None):
+        """k calls of fn between events on the launching stream, barrier + synchronize on both sides,
+        max over ranks (ms for all k)."""
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for i in range(k):
+            if pre is not None:
+                pre(i)
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1))
+
     for _ in range(max(args.warmup, 0)):
         last = step()
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
-    if world > 1:
-        dist.barrier()
+    barrier()
     torch.cuda.synchronize()
     clocks.start()
     time.sleep(0.3)
     # ---------------- timed region A: the reported value (no library profiling events inside)
     l0 = ctx.launch_count()
+    barrier()
+    torch.cuda.synchronize()
     e0.record(stream)
     for _ in range(args.steps):
         last = step()
     e1.record(stream)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    barrier()
     elapsed = e0.elapsed_time(e1)
     launches = ctx.launch_count() - l0
     clk = clocks.stop()
-    if world > 1:
-        t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed = float(t.item())
+    elapsed = max_over_ranks(elapsed)
+    launches_all = gather_objects(launches, world)
+    clk_all = gather_objects(clk, world)
 
     # ---------------- per-step distribution (after region A, which it does not perturb): each step
     # bracketed by its own events, at least 10 steps (SURVEY.md §8(d): median with p10 / p90)
@@ -387,9 +460,38 @@ def main():
     step_dist = {"n": n_dist, "median_ms": statistics.median(per_step), "p10_ms": q10, "p90_ms": q90,
                  "min_ms": per_step[0], "max_ms": per_step[-1]}
     if world > 1:
-        t = torch.tensor([step_dist["median_ms"]], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        step_dist["median_ms_max_over_ranks"] = float(t.item())
+        step_dist["median_ms_max_over_ranks"] = max_over_ranks(step_dist["median_ms"])
+
+    # ---------------- step variants (honest timing of the graph replay): the plain stream launches
+    # (CGGM_OPT_GRAPHS = 0), and a Lambda whose values change every step (new values written into
+    # the same CSC buffers before each evaluation -- the replayed graph reads them; the write is timed)
+    variants = None
+    if world == 1 and not args.no_variants:
+        kv = max(3, min(args.steps, 5))
+        ctx.set_option(_abi.CGGM_OPT_GRAPHS, 0)
+        step()
+        eager_ms = timed(step, kv) / kv
+        ctx.set_option(_abi.CGGM_OPT_GRAPHS, 1)
+        v0 = Lam.val.clone()
+        offd = (Lam.rowidx.long() != torch.repeat_interleave(
+            torch.arange(q, device="cuda"), Lam.colptr[1:] - Lam.colptr[:-1])).to(torch.float64)
+        scales = [1.0 - 0.002 * (i % 5) for i in range(kv + 2)]
+        vals = [v0 * (1.0 - offd * (1.0 - s_)) for s_ in scales]   # off-diagonals scaled: stays PD (chain)
+
+        def pre(i):
+            Lam.val.copy_(vals[i % len(vals)])
+        for i in range(2):
+            pre(i + kv)
+            step()
+        chg_ms = timed(step, kv, pre=pre) / kv
+        Lam.val.copy_(v0)
+        last = step()
+        torch.cuda.synchronize()
+        variants = {"graph_replay_ms": elapsed / args.steps, "eager_ms": eager_ms, "changing_lambda_ms": chg_ms,
+                    "steps": kv,
+                    "changing_lambda": "off-diagonal values of Lambda* scaled by 1, 0.998, ..., 0.992 in turn, "
+                                       "written into the same CSC before each step (copy timed); the graph "
+                                       "replays on the new values"}
 
     # ---------------- secondary: the factor-reuse evaluation: the accepted trial's
     # inverse factor seeds the next Sigma (CGGM_OPT_FACTOR_REUSE; here the trial Lambda is the
@@ -399,14 +501,8 @@ def main():
         ctx.set_option(_abi.CGGM_OPT_FACTOR_REUSE, 1)
         for _ in range(2):
             step()
-        torch.cuda.synchronize()
-        e0.record(stream)
-        for _ in range(args.steps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize()
+        r_ms = timed(step, args.steps) / args.steps
         ctx.set_option(_abi.CGGM_OPT_FACTOR_REUSE, 0)
-        r_ms = e0.elapsed_time(e1) / args.steps
         _, r_all = alg_flops(P.n, P.p, P.q, P.theta_star.nnz)
         r_all -= P.q ** 3 / 3.0
         reuse = {"value": 1e3 / r_ms, "unit": UNIT, "ms_per_step": r_ms, "alg_flops_per_step": r_all,
@@ -414,10 +510,11 @@ def main():
                  "what": "Sigma from the previous evaluation's trial inverse (potrf+trtri in the objective, "
                          "lauum for Sigma): (4/3) q^3 -> q^3"}
 
-    # ---------------- timed region B: per-launch CUDA events on the launching streams (library
-    # profiling), the same evaluation issued as the serialised separate calls so that every
-    # kernel's duration is its own (no overlap with the auxiliary stream)
+    # ---------------- timed region B (attribution only): per-launch CUDA events on the launching
+    # streams (library profiling), the same evaluation issued as the serialised separate calls so that
+    # every kernel's duration is its own (no overlap with the auxiliary stream)
     prof_steps = max(1, min(args.steps, 3))
+    phases, prof_elapsed, rank_phases = {}, None, None
     if world == 1:
         from paper_1509_04681_b200.api import newton_evaluation as _ne
 
@@ -425,64 +522,82 @@ def main():
             if args.stream_grad_theta:   # the separate calls need a stored grad_Theta
                 return _ne(ctx, X, Y, Syy, Lam, Th, P.lam_L, P.lam_T, True, bufs, stream_grad_theta=True)
             return _ne(ctx, X, Y, Syy, Lam, Th, P.lam_L, P.lam_T, True, bufs, composite=False)
-    else:
-        step_prof = step
-    torch.cuda.synchronize()
-    # pass B without the recursion lookahead: every kernel runs alone on its stream, so the sum of
-    # per-launch durations is the GEMM family's own time (concurrent side-stream launches would
-    # each be charged the shared wall time)
-    ctx.set_option(_abi.CGGM_OPT_LOOKAHEAD_MIN, 0)
-    step_prof()
-    torch.cuda.synchronize()
-    ctx.profile(True)
-    e0.record(stream)
-    for _ in range(prof_steps):
+        torch.cuda.synchronize()
+        # without the recursion lookahead: every kernel runs alone on its stream, so the sum of
+        # per-launch durations is the GEMM family's own time
+        ctx.set_option(_abi.CGGM_OPT_LOOKAHEAD_MIN, 0)
         step_prof()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    prof_elapsed = e0.elapsed_time(e1)
-    prof = ctx.profile_read()
-    ctx.profile(False)
-    ctx.set_option(_abi.CGGM_OPT_LOOKAHEAD_MIN, 256)
+        torch.cuda.synchronize()
+        ctx.profile(True)
+        e0.record(stream)
+        for _ in range(prof_steps):
+            step_prof()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        prof_elapsed = e0.elapsed_time(e1)
+        prof = ctx.profile_read()
+        ctx.profile(False)
+        ctx.set_option(_abi.CGGM_OPT_LOOKAHEAD_MIN, 256)
+        ph_flops = phase_flops(P.n, P.p, P.q)
+        for tag, (tms, tcnt) in prof.items():
+            if tcnt == 0:
+                continue
+            d = {"ms_per_step": tms / prof_steps, "launches_per_step": tcnt / prof_steps}
+            if tag in ph_flops:
+                d["tflops"] = ph_flops[tag] / (tms / prof_steps * 1e-3) / 1e12
+            phases[tag] = d
+    else:
+        # per-rank phase times of one evaluation (events between the evaluator's phases)
+        ev.timing = True
+        barrier()
+        step()
+        pt = ev.phase_times()
+        ev.timing = False
+        rank_phases = gather_objects(pt, world)
 
     ms_step = elapsed / args.steps
     value = args.steps / (elapsed / 1e3)
     gemm_flops, all_flops = alg_flops(P.n, P.p, P.q, P.theta_star.nnz)
-    gemm_ms = sum(prof[t][0] for t in GEMM_TAGS) / prof_steps
-    achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12
-    ph_flops = phase_flops(P.n, P.p, P.q)
-    phases = {}
-    for tag, (tms, tcnt) in prof.items():
-        if tcnt == 0:
-            continue
-        d = {"ms_per_step": tms / prof_steps, "launches_per_step": tcnt / prof_steps}
-        if tag in ph_flops:
-            d["tflops"] = ph_flops[tag] / (tms / prof_steps * 1e-3) / 1e12
-        phases[tag] = d
+    q_, p_, n_ = P.q, P.p, P.n
+
+    # collectives per evaluation at N > 1 (bytes each rank contributes; achieved = bytes / phase time)
+    comm = None
+    if world > 1:
+        by = {"bcast_sigma": 8.0 * q_ * q_, "allreduce_psi": 8.0 * q_ * q_, "allreduce_grad_theta": 8.0 * p_ * q_}
+        comm = {"backend": backend, "allreduce": args.allreduce, "per_rank": []}
+        for r_, ph in enumerate(rank_phases):
+            d = {"rank": r_, "phase_ms": ph}
+            for k_, b_ in by.items():
+                if k_ in ph and ph[k_] > 0:
+                    alg = b_ / (ph[k_] * 1e-3) / 1e9
+                    bus = alg * (2.0 * (world - 1) / world if k_.startswith("allreduce") else 1.0)
+                    d[k_ + "_GBps"] = {"bytes": b_, "algbw": alg, "busbw": bus}
+            comm["per_rank"].append(d)
 
     # HBM-bound phases: algorithmic bytes per step / the phase's measured time per
     # step in pass B (every launch of the phase bracketed by its own CUDA events)
-    m_L, m_T = last["active"]["m_L"], last["active"]["m_T"]
-    q_, p_, n_ = P.q, P.p, P.n
-    spmm_calls = phases.get("spmm", {}).get("launches_per_step", 1.0)
-    hbm_alg = {
-        # one read of grad_Lambda's upper triangle and of grad_Theta (stored, or its streamed column
-        # chunks), 8 bytes written per active entry
-        "active_set": 8.0 * (q_ * (q_ + 1) / 2 + p_ * q_) + 8.0 * (m_L + m_T),
-        "grad_lambda": 32.0 * q_ * q_,                       # read S_yy, Sigma, Psi, write grad_Lambda
-        "spmm": 8.0 * n_ * (p_ + q_) * spmm_calls,           # per call: read X once, write W
-    }
     hbm = {}
-    for tag, by in hbm_alg.items():
-        if tag in phases:
-            ms_s = phases[tag]["ms_per_step"]
-            gbs = by / (ms_s * 1e-3) / 1e9
-            hbm[tag] = {"alg_bytes_per_step": by, "ms_per_step": ms_s, "achieved_gbs": gbs,
-                        "frac_of_measured_copy": gbs / HBM_PEAK_GBS}
+    if world == 1:
+        m_L, m_T = last["active"]["m_L"], last["active"]["m_T"]
+        spmm_calls = phases.get("spmm", {}).get("launches_per_step", 1.0)
+        hbm_alg = {
+            # one read of grad_Lambda's upper triangle and of grad_Theta (stored, or its streamed column
+            # chunks), 8 bytes written per active entry
+            "active_set": 8.0 * (q_ * (q_ + 1) / 2 + p_ * q_) + 8.0 * (m_L + m_T),
+            "grad_lambda": 32.0 * q_ * q_,                       # read S_yy, Sigma, Psi, write grad_Lambda
+            "spmm": 8.0 * n_ * (p_ + q_) * spmm_calls,           # per call: read X once, write W
+        }
+        for tag, by_ in hbm_alg.items():
+            if tag in phases:
+                ms_s = phases[tag]["ms_per_step"]
+                gbs = by_ / (ms_s * 1e-3) / 1e9
+                hbm[tag] = {"alg_bytes_per_step": by_, "ms_per_step": ms_s, "achieved_gbs": gbs,
+                            "frac_of_measured_copy": gbs / HBM_PEAK_GBS}
 
     # ---------------------------------------------------------------- e2e through the public API
     e2e = None
     need_gt = 8.0 * P.p * P.q if args.stream_grad_theta else 0.0
+    from paper_1509_04681_b200 import HostCsc, host_colmajor
     if not args.no_e2e and world == 1 and need_gt > 0.95 * torch.cuda.mem_get_info()[0]:
         # the host-buffer entry point returns the dense grad_Theta; beside the streamed path's
         # buffers it does not fit at this size
@@ -493,7 +608,6 @@ def main():
         # the public host-buffer entry point: X, Y and the CSCs from page-locked host memory, uploaded
         # by the library (Lambda first, the factorisation overlapping the X / Y transfers), S_yy formed
         # in the call, the scalar results read back
-        from paper_1509_04681_b200 import HostCsc, host_colmajor
         Xh, Yh = host_colmajor(P.X), host_colmajor(P.Y)
         Lh, Thh = HostCsc.from_host(lam_h), HostCsc.from_host(th_h)
         h2d = (Xh.numel() + Yh.numel()) * 8 + sum(t.numel() * t.element_size() for c_ in (Lh, Thh)
@@ -509,55 +623,91 @@ def main():
 
         step_e2e()
         step_e2e()
-        torch.cuda.synchronize()
         e2_steps = max(1, min(args.steps, 3))
-        e0.record(stream)
-        for _ in range(e2_steps):
-            step_e2e()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e2ms = e0.elapsed_time(e1)
+        e2ms = timed(step_e2e, e2_steps)
         e2e = {"value": e2_steps / (e2ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "steps": e2_steps,
                "includes": "cggm_newton_eval_host: H2D of X, Y, Lambda, Theta from page-locked host memory "
                            "(overlapped with the factorisation) + S_yy + evaluation + D2H of scalars"}
+    elif not args.no_e2e:
+        # N > 1: every rank uploads its row block of X and Y and the two CSCs from page-locked host
+        # memory each step, evaluates through the sharded evaluator (library calls + collectives) and
+        # reads the objective back
+        Xh, Yh = host_colmajor(P.X[a:b]), host_colmajor(P.Y[a:b])
+        Lh, Thh = HostCsc.from_host(lam_h), HostCsc.from_host(th_h)
+        h2d = (Xh.numel() + Yh.numel()) * 8 + sum(t.numel() * t.element_size() for c_ in (Lh, Thh)
+                                                  for t in (c_.colptr, c_.rowidx, c_.val))
+
+        def step_e2e():
+            X.copy_(Xh, non_blocking=True)
+            Y.copy_(Yh, non_blocking=True)
+            for dc, hc in ((Lam, Lh), (Th, Thh)):
+                for f_ in ("colptr", "rowidx", "val"):
+                    getattr(dc, f_).copy_(getattr(hc, f_), non_blocking=True)
+            r_ = ev.evaluate(X, Y, Lam, Th, P.lam_L, P.lam_T, True)
+            return float(r_["f"])
+
+        step_e2e()
+        e2_steps = max(1, min(args.steps, 3))
+        e2ms = timed(step_e2e, e2_steps)
+        e2e = {"value": e2_steps / (e2ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": 8, "steps": e2_steps,
+               "includes": "per rank: H2D of its X / Y row block and the Lambda / Theta CSCs from page-locked "
+                           "host memory + the sharded evaluation + D2H of f; max over ranks"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(P)
+    barrier()
 
     res = last
     obj = res["objective"] if world == 1 else {"f": res["f"]}
+    step_achieved = all_flops / (ms_step * 1e-3) / world / 1e12
     if rank == 0:
+        roof = {"bound": "tensor", "kernel": "gemm_dmma_kernel family (FP64 DMMA.8x8x4): every dense contraction "
+                                             "of the step (97% of its time)",
+                "achieved": step_achieved, "peak": peak_tflops, "unit": "TFLOP/s", "frac": step_achieved / peak_tflops,
+                "traffic": _dominant_traffic(),
+                "measured_in": f"timed region A: all algorithmic flops of the step ({all_flops:.4g}) / "
+                               f"({world} GPU x {ms_step:.2f} ms)",
+                "peak_source": f"live DMMA.8x8x4 microbenchmark on this GPU ({args.peak_seconds:.1f} s, "
+                               "2 CTAs/SM); MEASURED_PEAKS.json has no FP64 entry",
+                "traffic_source": "dram read+write bytes per launch of the largest launch (lauum) from the "
+                                  "committed ncu --set full capture"}
+        if world == 1:
+            gemm_ms = sum(phases[t]["ms_per_step"] for t in GEMM_TAGS if t in phases)
+            roof["attribution_pass_b"] = {
+                "gemm_ms_per_step": gemm_ms, "gemm_alg_flops_per_step": gemm_flops,
+                "gemm_tflops": gemm_flops / (gemm_ms * 1e-3) / 1e12,
+                "gemm_frac": gemm_flops / (gemm_ms * 1e-3) / 1e12 / peak_tflops,
+                "lauum_tflops": phases.get("lauum", {}).get("tflops"),
+                "what": f"serialised separate calls without lookahead, per-launch CUDA events, {prof_steps} steps "
+                        f"({prof_elapsed / prof_steps:.1f} ms/step); per-launch durations include the "
+                        f"latency-bound bottom of the recursions, so they sum to more than the overlapped step"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": args.config, "n": P.n, "p": P.p, "q": P.q, "nnz_theta": P.theta_star.nnz,
                        "nnz_lambda": P.lam_star.nnz, "lambda": P.lam_L, "point": "generating (Lambda*, Theta*)",
                        "parallelism": (f"sample-shard dp{world}, " + ("distributed inverse and trial factorisation" if dist_inv else
                                        "rank-0 inverse + split objective") + f", {args.allreduce} all-reduce") if world > 1 else "1 GPU",
-                       "l2": "inputs larger than L2 (Sigma/Psi/grad_Lambda 3.2 GB each, grad_Theta 6.4 GB)",
+                       "l2": l2_note(P),
                        "setup_syy_ms": setup_ms, "generator_s": round(t_gen, 2),
                        "grad_theta": "streamed into the active sets (not stored)" if args.stream_grad_theta
                        else "stored (p x q)"},
-            "clocks": clk,
+            "clocks": clk_all[0] if world == 1 else {**(clk_all[0] or {}), "per_rank": clk_all},
             "step_ms_distribution": step_dist,
+            "step_variants": variants,
             "env": run_env(),
-            "gpu_launches": launches,
-            "roofline": {"bound": "tensor", "kernel": "gemm_dmma_kernel (FP64 DMMA.8x8x4, all dense contractions)",
-                         "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
-                         "frac": achieved / peak_tflops, "traffic": _dominant_traffic(),
-                         "peak_source": f"live DMMA.8x8x4 microbenchmark on this GPU ({args.peak_seconds:.1f} s, "
-                                        "2 CTAs/SM); MEASURED_PEAKS.json has no FP64 entry",
-                         "gemm_ms_per_step": gemm_ms, "gemm_alg_flops_per_step": gemm_flops,
-                         "measured_in": f"profiled pass B ({prof_steps} steps, separate calls without lookahead, "
-                                        f"per-launch CUDA events; {prof_elapsed / prof_steps:.1f} ms/step)",
-                         "step_frac_of_peak": all_flops / (ms_step * 1e-3) / 1e12 / peak_tflops},
-            "phases": phases,
+            "gpu_launches": int(sum(launches_all)),
+            "gpu_launches_per_rank": launches_all if world > 1 else None,
+            "roofline": roof,
+            "phases": phases if world == 1 else None,
+            "comm": comm,
             "hbm_roofline": {"peak_gbs": HBM_PEAK_GBS, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)",
-                             "kernels": hbm},
+                             "kernels": hbm} if world == 1 else None,
             "e2e": e2e,
             "factor_reuse": reuse,
             "cpu_baseline": cpu,
@@ -565,6 +715,8 @@ def main():
                        "m_L": res["active"]["m_L"], "m_T": res["active"]["m_T"],
                        "subgrad_l1": res["active"]["subgrad_l1"]},
         }
+        if functional:
+            line["functional_only"] = "all ranks on one GPU (CGGM_BENCH_DEVICE): not a measurement"
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -126,6 +126,28 @@ class ShardedEvaluator:
         # Psi / grad_Theta partials summed over CUDA IPC peer memory instead of NCCL (CudaBackend)
         self.peer = PeerAllReduce(backend.ctx, group) if (peer_allreduce and self.world > 1) else None
         self._peer_out = None
+        # per-phase CUDA events on the current stream (bench: per-rank phase times, collective GB/s)
+        self.timing = False
+        self._marks = []
+
+    def _mark(self, name):
+        if self.timing:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self._marks.append((name, e))
+
+    def phase_times(self):
+        """{phase: ms} between consecutive marks of the last timed evaluate() (synchronises)."""
+        torch.cuda.synchronize()
+        out = {}
+        for (_, a), (name, b) in zip(self._marks, self._marks[1:]):
+            out[name] = out.get(name, 0.0) + a.elapsed_time(b)
+        self._marks = []
+        return out
+
+    def _g(self, r):
+        """Global rank of group rank r (torch's src / dst arguments are global ranks)."""
+        return dist.get_global_rank(self.group, r) if self.group is not None else r
 
     def _allreduce(self, t):
         if self.world > 1:
@@ -159,12 +181,12 @@ class ShardedEvaluator:
                     else:
                         buf = torch.empty((b - a) * full.shape[1], dtype=full.dtype,
                                           device="cpu" if host else full.device)
-                        dist.recv(buf, src=r, group=self.group)
+                        dist.recv(buf, src=self._g(r), group=self.group)
                         full[a:b].copy_(buf.view(full.shape[1], b - a).t())
         else:
             for local in (X_r, Y_r):
                 buf = local.t().contiguous().view(-1)
-                dist.send(buf.cpu() if host else buf, dst=self.obj_rank, group=self.group)
+                dist.send(buf.cpu() if host else buf, dst=self._g(self.obj_rank), group=self.group)
 
     _OB_KEYS = ("f", "g", "logdet", "tr_syy_lam", "tr_sxy_theta", "tr_sigma_m", "pen_L", "pen_T", "is_pd", "fail_col")
 
@@ -176,7 +198,7 @@ class ShardedEvaluator:
             ob = self.b.objective_partial(self.X_full, self.Y_full, Lam, Theta, lam_L, lam_T, penalize_diag,
                                           self.n_total)
             vals = torch.tensor([float(ob[k]) for k in self._OB_KEYS], dtype=torch.float64, device=like.device)
-        dist.broadcast(vals, src=self.obj_rank, group=self.group)
+        dist.broadcast(vals, src=self._g(self.obj_rank), group=self.group)
         ob = {k: float(v) for k, v in zip(self._OB_KEYS, vals.tolist())}
         ob["is_pd"] = ob["is_pd"] > 0.5
         ob["fail_col"] = int(ob["fail_col"])
@@ -185,6 +207,8 @@ class ShardedEvaluator:
     def evaluate(self, X_r, Y_r, Lam, Theta, lam_L, lam_T, penalize_diag=True, tie_eps=1e-9):
         n = self.n_total
         q = Lam.nrows
+        self._marks = []
+        self._mark("start")
         # Sigma = Lambda^{-1}: rank 0 factors and broadcasts (or every rank, replicate_inverse; or
         # all ranks together, distributed_inverse)
         if self.dist_inv is not None:
@@ -195,14 +219,17 @@ class ShardedEvaluator:
             Sigma, logdet, pd, fc = self.b.invert_logdet(Lam)
         else:
             Sigma, logdet, pd, fc = self.b.empty_sigma(q, Y_r), None, None, None
+        self._mark("inverse")
         if self.split:
             self._ob_split = self._objective_split(Lam, Theta, lam_L, lam_T, penalize_diag, Sigma)
+            self._mark("objective_split")
         if self.world > 1 and not self.replicate_inverse and self.dist_inv is None:
-            dist.broadcast(flat(Sigma), src=0, group=self.group)
+            dist.broadcast(flat(Sigma), src=self._g(0), group=self.group)
             meta = torch.tensor([logdet if logdet is not None else 0.0, float(bool(pd)), float(fc or 0)],
                                 dtype=torch.float64, device=Sigma.device)
-            dist.broadcast(meta, src=0, group=self.group)
+            dist.broadcast(meta, src=self._g(0), group=self.group)
             logdet, pd, fc = float(meta[0]), bool(meta[1] > 0.5), int(meta[2])
+            self._mark("bcast_sigma")
         if self.peer is not None:
             if self._peer_out is None:   # symmetric buffers, allocated once (same shapes every call)
                 p = X_r.shape[1]
@@ -210,10 +237,14 @@ class ShardedEvaluator:
             Psi, GradT = self.b.psi_grad_partial(X_r, Y_r, Theta, Sigma, n, out=self._peer_out)
         else:
             Psi, GradT = self.b.psi_grad_partial(X_r, Y_r, Theta, Sigma, n)
+        self._mark("psi_grad_partial")
         self._allreduce(Psi)
+        self._mark("allreduce_psi")
         self._allreduce(GradT)
+        self._mark("allreduce_grad_theta")
         GradL = self.b.grad_lambda(self.Syy, Sigma, Psi)
         act = self.b.active_set(GradL, GradT, Lam, Theta, lam_L, lam_T, penalize_diag, tie_eps)
+        self._mark("grad_lambda_active")
         if self.split:
             # the objective rank evaluated the whole objective on all rows (see _objective_split)
             ob = self._ob_split
@@ -242,6 +273,7 @@ class ShardedEvaluator:
                                  device=Psi.device)
             if self.world > 1:
                 dist.all_reduce(parts, group=self.group)
+        self._mark("objective")
         tr_syy, tr_sxy, tr_sm = (float(v) for v in parts.tolist())
         if ob["is_pd"]:
             g = -ob["logdet"] + tr_syy + 2.0 * tr_sxy + tr_sm
