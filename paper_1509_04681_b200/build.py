@@ -14,7 +14,7 @@ LIB = os.path.join(LIBDIR, "libcggm.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr"]
-SOURCES = ["gemm.cu", "gemm_f32.cu", "chol.cu", "stream.cu", "active.cu", "cd.cu", "abi.cu", "peak.cu", "comm.cu"]
+SOURCES = ["gemm.cu", "gemm_f32.cu", "gemm_tf32.cu", "chol.cu", "stream.cu", "active.cu", "cd.cu", "abi.cu", "peak.cu", "comm.cu"]
 
 
 def _deps_mtime() -> float:

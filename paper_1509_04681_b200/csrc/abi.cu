@@ -174,6 +174,9 @@ cggm_status cggm_ctx_create(cggm_ctx** out, int device, cggm_dtype dtype, void* 
   if (const char* e = std::getenv("CGGM_CD_COOP")) c->cd_coop = std::atoi(e);
   if (const char* e = std::getenv("CGGM_CD_PREFETCH")) c->cd_prefetch = std::atoi(e);
   if (const char* e = std::getenv("CGGM_GRAPH_PROF")) c->graph_prof = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_TF32_CHUNK")) c->tf32_chunk = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_TF32_DEBUG")) c->tf32_dbg = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_F32_ENGINE")) c->f32_engine = std::string(e) == "ffma" ? 1 : 0;
   cudaDriverEntryPointQueryResult q;
   void* fn = nullptr;
   if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
@@ -2007,5 +2010,11 @@ extern "C" cggm_status cggm_test_set_tile(cggm_ctx* ctx, int mode) {
   if (!ctx || mode < 0 || mode > 6) return CGGM_ERR_INVALID_ARG;
   ctx->impl.force_tile = mode & 3;
   ctx->impl.no_tma3d = (mode & 4) ? 1 : 0;
+  return CGGM_OK;
+}
+
+extern "C" cggm_status cggm_test_set_f32_engine(cggm_ctx* ctx, int engine) {
+  if (!ctx || engine < 0 || engine > 1) return CGGM_ERR_INVALID_ARG;
+  ctx->impl.f32_engine = engine;
   return CGGM_OK;
 }

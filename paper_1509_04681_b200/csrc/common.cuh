@@ -113,6 +113,9 @@ struct Ctx {
   int no_split_k = 0;   // CGGM_NO_SPLIT_K=1: W Sigma without the split-k grid (A/B)
   int no_vec_epi = 0;
   int persist_tpc = 0;   // CGGM_PERSIST_TPC: tiles per CTA of the persistent warp-specialised GEMM (0: off)   // CGGM_NO_VEC_EPI=1: scalar GEMM epilogue everywhere (A/B)      // CGGM_ACT_ONEPASS=1: Lambda list by the single-pass look-back kernel (not the split one)    // test hook (CGGM_NO_ACTIVE_VEC=1): scalar active-set kernel only   // test hook (CGGM_NO_SMALL_ASYNC=1): direct-load small kernel only
+  int tf32_dbg = 0;     // CGGM_TF32_DEBUG (gemm_tf32.cu measurement aid)
+  int tf32_chunk = 4;   // 3xTF32: k-tiles per drained TMEM partial (gemm_tf32.cu; CGGM_TF32_CHUNK, 0 = none)
+  int f32_engine = 0;   // FP32 contractions: 0 = 3xTF32 on tcgen05 (gemm_tf32.cu), 1 = SIMT FFMA (CGGM_F32_ENGINE=ffma)
   int no_tma3d = 0;   // test hook: 1 = always use 16-wide 2-D boxes for MN-inner operands  // test hook: 0 auto, 1 = 128x128 tiles, 2 = 64x64 tiles
   // phase profiling (CUDA events around every launch while enabled)
   int cur_tag = TAG_MISC;
@@ -301,9 +304,12 @@ using Epilogue = EpilogueT<double>;
 // op(B) = B (transB=false, B is K x N) or B^T (B is N x K).  Column-major, FP64 DMMA.
 void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K,
           const double* A, int64_t lda, const double* B, int64_t ldb, const Epilogue& epi, int flags);
-// FP32 variant (gemm_f32.cu): same contract, SIMT FFMA with fp32 accumulation (reading A18).
+// FP32 variant (gemm_f32.cu): same contract, fp32 accumulation (reading A18): 3xTF32 on the
+// tcgen05 tensor cores (gemm_tf32.cu) or the SIMT FFMA engine (Ctx::f32_engine).
 void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K,
           const float* A, int64_t lda, const float* B, int64_t ldb, const EpilogueT<float>& epi, int flags);
+void gemm_tf32x3(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                 const float* B, int64_t ldb, const EpilogueT<float>& epi, int flags);
 
 // ------------------------------------------------------------------ Cholesky family (chol.cu)
 // In-place blocked recursive Cholesky of the lower triangle of A (q x q).

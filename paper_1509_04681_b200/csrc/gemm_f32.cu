@@ -299,6 +299,10 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
   }
   if ((flags & SYM_LOWER) && (M < N || ((flags & SYM_MIRROR) && M != N)))
     throw CudaError{CGGM_ERR_SHAPE, "SYM_LOWER gemm needs M >= N (M == N with SYM_MIRROR)"};
+  if (c->f32_engine == 0) {
+    gemm_tf32x3(c, transA, transB, M, N, K, A, lda, B, ldb, epi, flags);
+    return;
+  }
   KParamsF P;
   P.M = (int)M; P.N = (int)N; P.K = (int)(K > 0 ? K : 0);
   P.flags = flags;

@@ -1,0 +1,440 @@
+// FP32 variant of the GEMM engine on the 5th-generation tensor cores (reading A18: fp32 inputs,
+// fp32 accumulation; north_star "an FP32 variant" of the dense contractions).
+//
+// TF32 alone (10-bit mantissa) is too inexact for the 1e-4 contract, so every product is the
+// 3xTF32 split: x = hi(x) + lo(x), hi = rna_tf32(x), lo = rna_tf32(x - hi) (both exact tf32
+// values, |lo| <= 2^-11 |x|), and
+//     A B  ~  A_lo B_hi + A_hi B_lo + A_hi B_hi        (the dropped A_lo B_lo is ~2^-22 |A||B|)
+// accumulated in one fp32 TMEM accumulator by tcgen05.mma.kind::tf32 (M = 128, N = 128, K = 8).
+//
+// CTA = 4 producer warps + 4 drain warps (256 threads), one 128 x 128 output tile:
+//  * producers (warps 0-3) stream k-tiles of 32: 16-byte global loads of the raw fp32 operands into
+//    registers one k-tile ahead, split into hi / lo, and store both into the stage's shared-memory
+//    buffers in the canonical layouts the UMMA descriptors name (K-major: SWIZZLE_128B, one 128-byte
+//    row per m / n; MN-major: SWIZZLE_128B with 32-byte atoms -- the only MN-major layout of 32-bit
+//    operands -- 128-byte rows along m / n, one row per k, 4 KB per 32-wide chunk), then
+//    fence.proxy.async and arrive on the stage's full barrier; thread 0 then issues the PREVIOUS
+//    k-tile's 4 k-steps x 3 products (its barrier has completed by then, so the issue never stalls
+//    the producer) and tcgen05.commit's that stage's empty barrier;
+//  * hi*hi accumulates in TMEM over chunks of CH k-tiles (two buffers), the corrections in a third
+//    accumulator; the drain warps (tcgen05.ld 32x32b, warp w owns TMEM lanes 32(w%4).. = rows) add
+//    each finished chunk into fp32 registers (the tensor core's own accumulation rounds toward zero),
+//    then the corrections, stage the tile in shared memory and run the engine's common epilogue
+//    (alpha / beta / second output, lower trapezoid, mirrored symmetric writes).
+// Same flags, tile order and epilogue contract as the FFMA kernel (gemm_f32.cu), which stays as the
+// A/B alternative (CGGM_F32_ENGINE=ffma, cggm_test_set_f32_engine).
+#include "common.cuh"
+
+namespace cggm {
+namespace {
+
+constexpr int TBM = 128, TBN = 128, TBK = 32;
+constexpr int TSTAGES = 3;
+constexpr int T_OP = TBM * TBK * 4;          // 16 KB per operand half (hi or lo)
+constexpr int T_STAGE = 4 * T_OP;            // A_hi, A_lo, B_hi, B_lo
+constexpr int T_DATA = TSTAGES * T_STAGE;    // 192 KB
+constexpr int T_EPI_LD = TBM + 1;
+static_assert(TBN * T_EPI_LD * 4 <= T_DATA, "epilogue tile must fit in the stage buffers");
+constexpr int T_SMEM = T_DATA + 1024 + 128;
+constexpr int T_PROD = 128;                  // producer threads (warps 0-3); thread 0 also issues the MMAs
+constexpr int T_DRAIN = 128;                 // accumulator-drain / epilogue threads (warps 4-7)
+constexpr int T_NT = T_PROD + T_DRAIN;
+constexpr int T_GROUP_N = 8;
+constexpr uint32_t T_TMEM_COLS = 512;   // accumulators: X0 (cols 0-127), D2 (128-255), X1 (256-383)
+
+struct KParamsT {
+  int M, N, K;
+  int tilesM, tilesN;
+  int flags;
+  const float* A;
+  int64_t lda;
+  const float* B;
+  int64_t ldb;
+  int chunk;      // k-tiles per drained partial sum (0: one TMEM accumulator over the whole k-range)
+  int dbg;        // measurement aid (CGGM_TF32_DEBUG): bit 0 = hi*hi products only
+  EpilogueT<float> epi;
+};
+
+__device__ __forceinline__ void tile_coords_t(const KParamsT& P, int t, int& I, int& J) {
+  if (P.flags & SYM_LOWER) {
+    const long long tri = (long long)P.tilesN * (P.tilesN + 1) / 2;
+    if (t < tri) {
+      int i = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+      while ((long long)(i + 1) * (i + 2) / 2 <= t) ++i;
+      while ((long long)i * (i + 1) / 2 > t) --i;
+      I = i;
+      J = t - (int)((long long)i * (i + 1) / 2);
+    } else {
+      const int r = t - (int)tri;
+      I = P.tilesN + r / P.tilesN;
+      J = r % P.tilesN;
+    }
+    return;
+  }
+  const int per_group = T_GROUP_N * P.tilesM;
+  const int gi = t / per_group;
+  const int local = t - gi * per_group;
+  const int nb0 = gi * T_GROUP_N;
+  const int width = min(T_GROUP_N, P.tilesN - nb0);
+  I = local / width;
+  J = nb0 + local % width;
+  if (P.flags & B_KLE_N) J = P.tilesN - 1 - J;
+  if (P.flags & A_KLE_M) I = P.tilesM - 1 - I;
+}
+
+__device__ __forceinline__ void epi_apply_t(const EpilogueT<float>& E, int64_t r, int64_t c, float v) {
+  if (E.out1) {
+    float o = __fmul_rn((float)E.a1, v);
+    if (E.in1a) o = __fadd_rn(o, __fmul_rn((float)E.b1, E.in1a[r + c * E.ld1a]));
+    if (E.in1b) o = __fadd_rn(o, __fmul_rn((float)E.c1, E.in1b[r + c * E.ld1b]));
+    E.out1[r + c * E.ld1] = o;
+  }
+  if (E.out2) {
+    float o = __fmul_rn((float)E.a2, v);
+    if (E.in2a) o = __fadd_rn(o, __fmul_rn((float)E.b2, E.in2a[r + c * E.ld2a]));
+    if (E.in2b) o = __fadd_rn(o, __fmul_rn((float)E.c2, E.in2b[r + c * E.ld2b]));
+    E.out2[r + c * E.ld2] = o;
+  }
+}
+
+// ---------------------------------------------------------------- tcgen05 / TMEM PTX
+// round-to-nearest (ties away) to tf32 on the bit pattern: +half an ulp of the 10-bit mantissa, clear
+// the 13 low bits (a mantissa carry moves into the exponent, as it should); two integer ops instead
+// of the conversion unit's cvt.rna.tf32 (the split runs on every operand element of every k-tile)
+__device__ __forceinline__ uint32_t rna_tf32(float x) { return (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u; }
+
+// shared-memory matrix descriptor (tcgen05): start >> 4 [0,14), LBO >> 4 [16,30), SBO >> 4 [32,46),
+// version 1 [46,48), base offset 0, layout at [61,64): SWIZZLE_128B = 2 (K-major), SWIZZLE_128B with
+// 32-byte atoms = 1 (the only MN-major layout of 32-bit operands)
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint64_t layout) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (layout << 61);
+}
+
+// instruction descriptor: D fp32 [4,6) = 1, A / B tf32 [7,10) / [10,13) = 2, A / B major [15] / [16]
+// (0 K-major, 1 MN-major), N >> 3 at [17,23), M >> 4 at [24,29)
+__host__ __device__ constexpr uint32_t idesc_tf32(bool a_mn, bool b_mn, int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   ptx::smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+// ---------------------------------------------------------------- producer: loads and the split
+// Operand tile of 128 (m or n) x 32 (k), 1024 float4 = 8 per producer thread.
+//  K-inner (element (x, k) at base[k + x ld]):  f -> row x = f >> 3, 16-byte chunk c = f & 7
+//  MN-inner (element (x, k) at base[x + k ld]): f -> k = f >> 5, x = 4 (f & 31)
+template <bool KIN>
+__device__ __forceinline__ void load_tile(float4 (&r)[8], const float* __restrict__ base, int64_t ld, int x0, int X,
+                                          int k0, int K, int tid) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int f = tid + T_PROD * i;
+    int x, k;
+    if (KIN) {
+      x = x0 + (f >> 3);
+      k = k0 + 4 * (f & 7);
+    } else {
+      k = k0 + (f >> 5);
+      x = x0 + 4 * (f & 31);
+    }
+    const float* p = KIN ? base + (int64_t)x * ld + k : base + (int64_t)k * ld + x;
+    const bool full = KIN ? (x < X && k + 3 < K) : (k < K && x + 3 < X);
+    if (full) {
+      r[i] = __ldg(reinterpret_cast<const float4*>(p));
+    } else {
+      float v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const bool ok = KIN ? (x < X && k + e < K) : (k < K && x + e < X);
+        v[e] = ok ? __ldg(p + e) : 0.f;
+      }
+      r[i] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+  }
+}
+
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+template <bool KIN>
+__device__ __forceinline__ void store_split(const float4 (&r)[8], uint32_t hi, uint32_t lo, int tid) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int f = tid + T_PROD * i;
+    uint32_t off;
+    if (KIN) {
+      const int row = f >> 3, c = f & 7;
+      off = row * 128 + ((c ^ (row & 7)) << 4);
+    } else {
+      // MN-major, 128-byte rows along m / n, 32-byte swizzle atoms: 32-byte unit u of row k sits at
+      // u ^ (k & 3) (byte-address bits [5,7) ^= [7,9))
+      const int k = f >> 5, mc = f & 31, c = mc & 7;
+      off = (mc >> 3) * 4096 + k * 128 + (((((c >> 1) ^ (k & 3)) << 1) | (c & 1)) << 4);
+    }
+    const float v[4] = {r[i].x, r[i].y, r[i].z, r[i].w};
+    uint32_t h[4], l[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      h[e] = rna_tf32(v[e]);
+      l[e] = rna_tf32(v[e] - __uint_as_float(h[e]));
+    }
+    sts128(hi + off, h[0], h[1], h[2], h[3]);
+    sts128(lo + off, l[0], l[1], l[2], l[3]);
+  }
+}
+
+template <bool AK, bool BKI>
+__global__ void __launch_bounds__(T_NT, 1) gemm_tf32x3_kernel(const __grid_constant__ KParamsT P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + T_DATA);
+  uint64_t* empty = full + TSTAGES;
+  uint64_t* cfull = empty + TSTAGES;    // chunk partial in X[b] complete
+  uint64_t* cempty = cfull + 2;          // X[b] drained
+  uint64_t* accf = cempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  int I, J;
+  tile_coords_t(P, blockIdx.x, I, J);
+  const int m0 = I * TBM, n0 = J * TBN;
+  int kbeg = 0, kend = P.K;
+  if (P.flags & A_KGE_M) kbeg = max(kbeg, m0);
+  if (P.flags & B_KGE_N) kbeg = max(kbeg, n0);
+  if (P.flags & A_KLE_M) kend = min(kend, m0 + TBM);
+  if (P.flags & B_KLE_N) kend = min(kend, n0 + TBN);
+  const int kt0 = kbeg / TBK;
+  const int nkt = kend > kbeg ? (kend - kt0 * TBK + TBK - 1) / TBK : 0;
+  const int CH = P.chunk;
+  const bool drain = CH > 0;
+  if (tid == 0) {
+    for (int s = 0; s < TSTAGES; ++s) {
+      ptx::mbar_init(&full[s], T_PROD);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&cfull[b], 1);
+      ptx::mbar_init(&cempty[b], T_DRAIN);
+    }
+    ptx::mbar_init(accf, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(ptx::smem_u32(tmem_slot)),
+                 "n"(T_TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sbase = ptx::smem_u32(smem);
+
+  if (warp < 4) {
+    // ---- producers: operand k-tiles, one ahead in registers; after each stage's stores a producer
+    // barrier, then thread 0 issues that stage's MMAs.  With draining, the hi*hi products of chunk c
+    // (CH k-tiles) go to X[c & 1], which the drain warps add into fp32 registers (round-to-nearest)
+    // while the next chunk fills the other buffer; the two corrections (~2^-11 of the result)
+    // accumulate in D2 over the whole k-range.  The tensor core's accumulation rounds toward zero, so
+    // a long k-range in one accumulator is biased by ~k/8 x 2^-24 relative (measured,
+    // tools/debug/tf32_acc_probe.py); bounded chunks keep fp32-class accuracy.
+    const float* A = P.A;
+    const float* B = P.B;
+    float4 ra[8], rb[8];
+    if (nkt > 0) {
+      load_tile<AK>(ra, A, P.lda, m0, P.M, kt0 * TBK, P.K, tid);
+      load_tile<BKI>(rb, B, P.ldb, n0, P.N, kt0 * TBK, P.K, tid);
+    }
+    constexpr uint32_t idesc = idesc_tf32(!AK, !BKI, TBM, TBN);
+    // MMAs of k-tile j (thread 0, after every producer stored it: full[j % TSTAGES])
+    auto issue = [&](int j) {
+      const int s = j % TSTAGES;
+      ptx::mbar_wait(&full[s], (j / TSTAGES) & 1);
+      tc_fence_after();
+      const int c = drain ? j / CH : 0;
+      const bool first = drain && (j % CH == 0);
+      if (first && c >= 2) {
+        ptx::mbar_wait(&cempty[c & 1], ((c >> 1) - 1) & 1);
+        tc_fence_after();
+      }
+      const uint32_t st = sbase + s * T_STAGE;
+      const uint32_t a_hi = st, a_lo = st + T_OP, b_hi = st + 2 * T_OP, b_lo = st + 3 * T_OP;
+      const uint32_t X = tmem + ((c & 1) ? 256u : 0u);
+#pragma unroll
+      for (int kk = 0; kk < TBK / 8; ++kk) {
+        // K-major: the k-step advances 32 bytes inside the 128-byte swizzled row (SBO = 8 rows = 1 KB);
+        // MN-major: it advances two 4-row k groups (SBO = 512 B; LBO = 4 KB between 32-wide chunks)
+        const uint32_t oa = kk * (AK ? 32 : 1024), ob = kk * (BKI ? 32 : 1024);
+        const uint32_t la = AK ? 16 : 4096, lb = BKI ? 16 : 4096;
+        const uint32_t sa = AK ? 1024 : 512, sb = BKI ? 1024 : 512;
+        const uint64_t ya = AK ? 2 : 1, yb = BKI ? 2 : 1;
+        const uint64_t dah = sdesc(a_hi + oa, la, sa, ya), dal = sdesc(a_lo + oa, la, sa, ya);
+        const uint64_t dbh = sdesc(b_hi + ob, lb, sb, yb), dbl = sdesc(b_lo + ob, lb, sb, yb);
+        if (P.dbg & 1) {
+          umma_tf32(X, dah, dbh, idesc, (first && kk == 0) || (!drain && (j | kk) == 0) ? 0u : 1u);
+        } else if (drain) {
+          umma_tf32(tmem + 128u, dal, dbh, idesc, (j | kk) != 0);
+          umma_tf32(tmem + 128u, dah, dbl, idesc, 1u);
+          umma_tf32(X, dah, dbh, idesc, (first && kk == 0) ? 0u : 1u);
+        } else {
+          umma_tf32(tmem, dal, dbh, idesc, (j | kk) != 0);
+          umma_tf32(tmem, dah, dbl, idesc, 1u);
+          umma_tf32(tmem, dah, dbh, idesc, 1u);
+        }
+      }
+      umma_commit(&empty[s]);   // the slot is free once these MMAs have read it
+      if (drain && (j % CH == CH - 1 || j == nkt - 1)) umma_commit(&cfull[c & 1]);
+      if (j == nkt - 1) umma_commit(accf);
+    };
+    for (int it = 0; it < nkt; ++it) {
+      const int s = it % TSTAGES;
+      float4 na[8], nb[8];
+      if (it + 1 < nkt) {
+        load_tile<AK>(na, A, P.lda, m0, P.M, (kt0 + it + 1) * TBK, P.K, tid);
+        load_tile<BKI>(nb, B, P.ldb, n0, P.N, (kt0 + it + 1) * TBK, P.K, tid);
+      }
+      if (it >= TSTAGES) ptx::mbar_wait(&empty[s], ((it / TSTAGES) - 1) & 1);
+      const uint32_t st = sbase + s * T_STAGE;
+      store_split<AK>(ra, st, st + T_OP, tid);
+      store_split<BKI>(rb, st + 2 * T_OP, st + 3 * T_OP, tid);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      ptx::mbar_arrive(&full[s]);
+      // thread 0 issues the previous k-tile's MMAs (its full barrier has long completed: no stall)
+      if (tid == 0 && it > 0) issue(it - 1);
+      if (it + 1 < nkt) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          ra[i] = na[i];
+          rb[i] = nb[i];
+        }
+      }
+    }
+    if (tid == 0 && nkt > 0) issue(nkt - 1);
+  } else {
+    // ---- drain warps 4-7 (warp w reads TMEM lanes 32 (w % 4)..: one accumulator row per thread):
+    // fp32 sums of the chunk partials, then D2, then the epilogue
+    const int dt = tid - T_PROD;
+    const int row = (warp - 4) * 32 + lane;
+    const uint32_t lanebase = tmem + ((uint32_t)((warp - 4) * 32) << 16);
+    float acc[TBN];
+#pragma unroll
+    for (int j = 0; j < TBN; ++j) acc[j] = 0.f;
+    if (nkt > 0) {
+      const int nch = drain ? (nkt + CH - 1) / CH : 0;
+      for (int c = 0; c < nch; ++c) {
+        ptx::mbar_wait(&cfull[c & 1], (c >> 1) & 1);
+        tc_fence_after();
+        const uint32_t xa = lanebase + ((c & 1) ? 256u : 0u);
+#pragma unroll
+        for (int g = 0; g < TBN / 32; ++g) {
+          uint32_t v[32];
+          tmem_ld32(xa + 32u * g, v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[32 * g + j] += __uint_as_float(v[j]);
+        }
+        tc_fence_before();
+        ptx::mbar_arrive(&cempty[c & 1]);
+      }
+      ptx::mbar_wait(accf, 0);
+      tc_fence_after();
+      const uint32_t xa = lanebase + (drain ? 128u : 0u);   // D2 (draining) or the single accumulator
+#pragma unroll
+      for (int g = 0; g < TBN / 32; ++g) {
+        uint32_t v[32];
+        tmem_ld32(xa + 32u * g, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[32 * g + j] += __uint_as_float(v[j]);
+      }
+    }
+    float* Cs = reinterpret_cast<float*>(smem);   // stage buffers: every MMA has completed (accf)
+#pragma unroll
+    for (int j = 0; j < TBN; ++j) Cs[j * T_EPI_LD + row] = acc[j];
+    tc_fence_before();
+    asm volatile("bar.sync 1, %0;\n" ::"n"(T_DRAIN) : "memory");
+    const bool diag = (P.flags & SYM_LOWER) && I == J;
+    for (int idx = dt; idx < TBM * TBN; idx += T_DRAIN) {
+      const int mm = idx % TBM, nl = idx / TBM;
+      const int m = m0 + mm, n = n0 + nl;
+      if (m >= P.M || n >= P.N) continue;
+      if (diag && m < n) continue;
+      epi_apply_t(P.epi, m, n, Cs[nl * T_EPI_LD + mm]);
+    }
+    if (P.flags & SYM_MIRROR) {
+      for (int idx = dt; idx < TBM * TBN; idx += T_DRAIN) {
+        const int nl = idx % TBN, mm = idx / TBN;
+        const int m = m0 + mm, n = n0 + nl;
+        if (m >= P.M || n >= P.N) continue;
+        if (diag && m <= n) continue;
+        epi_apply_t(P.epi, n, m, Cs[nl * T_EPI_LD + mm]);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(T_TMEM_COLS) : "memory");
+  }
+}
+
+template <bool AK, bool BKI>
+void launch_t(Ctx* c, const KParamsT& P, int grid) {
+  CGGM_ONCE_PER_DEVICE({
+    CGGM_CUDA_CHECK(cudaFuncSetAttribute(gemm_tf32x3_kernel<AK, BKI>, cudaFuncAttributeMaxDynamicSharedMemorySize, T_SMEM));
+  });
+  Prof pr(c, c->cur_tag);
+  gemm_tf32x3_kernel<AK, BKI><<<grid, T_NT, T_SMEM, c->stream>>>(P);
+  post_launch(c, "gemm_tf32x3_kernel");
+}
+
+}  // namespace
+
+// Operands 16-byte aligned with ld % 4 == 0 (gemm_f32.cu packs others first); same contract as gemm().
+void gemm_tf32x3(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                 const float* B, int64_t ldb, const EpilogueT<float>& epi, int flags) {
+  KParamsT P;
+  P.M = (int)M; P.N = (int)N; P.K = (int)(K > 0 ? K : 0);
+  P.flags = flags;
+  P.A = A; P.lda = lda; P.B = B; P.ldb = ldb;
+  P.chunk = c->tf32_chunk;
+  P.dbg = c->tf32_dbg;
+  P.epi = epi;
+  P.tilesM = (int)((M + TBM - 1) / TBM);
+  P.tilesN = (int)((N + TBN - 1) / TBN);
+  const int grid = (flags & SYM_LOWER) ? P.tilesN * (P.tilesN + 1) / 2 + (P.tilesM - P.tilesN) * P.tilesN
+                                       : P.tilesM * P.tilesN;
+  const bool AK = transA, BKI = !transB;
+  if (AK && BKI) launch_t<true, true>(c, P, grid);
+  else if (AK && !BKI) launch_t<true, false>(c, P, grid);
+  else if (!AK && BKI) launch_t<false, true>(c, P, grid);
+  else launch_t<false, false>(c, P, grid);
+}
+
+}  // namespace cggm

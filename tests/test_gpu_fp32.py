@@ -32,6 +32,19 @@ def ctx32():
     return Context(0, dtype="f32")
 
 
+ENGINES = {"tf32x3": 0, "ffma": 1}
+# 3xTF32: each product carries ~2^-22 relative error (the split's rounding and the dropped lo*lo);
+# FFMA: fp32 rounding only
+GEMM_TOL = {"tf32x3": 5e-6, "ffma": 2e-6}
+
+
+@pytest.fixture(params=list(ENGINES))
+def engine(request, ctx32):
+    ctx32._check(ctx32.lib.cggm_test_set_f32_engine(ctx32.h, ENGINES[request.param]))
+    yield request.param
+    ctx32._check(ctx32.lib.cggm_test_set_f32_engine(ctx32.h, 0))
+
+
 def run_f32(ctx, tA, tB, A, B, C0, alpha, beta, flags, M, N, K):
     from paper_1509_04681_b200.api import colmajor_empty, ld_of
     ts = []
@@ -50,8 +63,8 @@ def run_f32(ctx, tA, tB, A, B, C0, alpha, beta, flags, M, N, K):
 @pytest.mark.parametrize("tA", [False, True])
 @pytest.mark.parametrize("tB", [False, True])
 @pytest.mark.parametrize("M,N,K", [(1, 1, 1), (37, 45, 29), (300, 260, 171), (256, 64, 300), (513, 129, 1000)])
-@pytest.mark.parametrize("mode", [1, 5])   # 3-D / 2-D TMA boxes for MN-inner operands
-def test_ffma_gemm_variants(ctx32, tA, tB, M, N, K, mode):
+@pytest.mark.parametrize("mode", [1, 5])   # 3-D / 2-D TMA boxes for MN-inner operands (FFMA engine)
+def test_f32_gemm_variants(ctx32, engine, tA, tB, M, N, K, mode):
     ctx32._check(ctx32.lib.cggm_test_set_tile(ctx32.h, mode))
     rng = np.random.default_rng(M + 3 * N + 7 * K)
     A = rng.standard_normal((K, M) if tA else (M, K)).astype(np.float32).astype(np.float64)
@@ -59,12 +72,12 @@ def test_ffma_gemm_variants(ctx32, tA, tB, M, N, K, mode):
     C0 = rng.standard_normal((M, N)).astype(np.float32).astype(np.float64)
     ref = 0.75 * ((A.T if tA else A) @ (B.T if tB else B)) - 0.5 * C0
     out = run_f32(ctx32, tA, tB, A, B, C0, 0.75, -0.5, 0, M, N, K)
-    assert relf(out, ref) < 2e-6
+    assert relf(out, ref) < GEMM_TOL[engine]
     ctx32._check(ctx32.lib.cggm_test_set_tile(ctx32.h, 0))
 
 
 @pytest.mark.parametrize("flags", [A_KLE_M, A_KGE_M, B_KLE_N, B_KGE_N])
-def test_ffma_gemm_triangular(ctx32, flags):
+def test_f32_gemm_triangular(ctx32, engine, flags):
     rng = np.random.default_rng(flags)
     n = 333
     A = rng.standard_normal((n, n)).astype(np.float32).astype(np.float64)
@@ -72,16 +85,16 @@ def test_ffma_gemm_triangular(ctx32, flags):
     A = np.tril(A) if flags & A_KLE_M else np.triu(A) if flags & A_KGE_M else A
     B = np.triu(B) if flags & B_KLE_N else np.tril(B) if flags & B_KGE_N else B
     out = run_f32(ctx32, False, False, A, B, np.zeros((n, n)), 1.0, 0.0, flags, n, n, n)
-    assert relf(out, A @ B) < 2e-6
+    assert relf(out, A @ B) < GEMM_TOL[engine]
 
 
-def test_ffma_gemm_sym_and_trapezoid(ctx32):
+def test_f32_gemm_sym_and_trapezoid(ctx32, engine):
     rng = np.random.default_rng(3)
     q, K = 385, 300
     A = rng.standard_normal((K, q)).astype(np.float32).astype(np.float64)
     out = run_f32(ctx32, True, False, A, A, np.zeros((q, q)), 1.0, 0.0, SYM_LOWER | SYM_MIRROR, q, q, K)
     np.testing.assert_array_equal(out, out.T)
-    assert relf(out, A.T @ A) < 2e-6
+    assert relf(out, A.T @ A) < GEMM_TOL[engine]
     N, extra = 300, 257
     Bm = rng.standard_normal((N + extra, K)).astype(np.float32).astype(np.float64)
     C0 = rng.standard_normal((N + extra, N)).astype(np.float32).astype(np.float64)
@@ -108,7 +121,7 @@ def oracle_point(name, k):
 
 
 @pytest.mark.parametrize("name,k", [("tiny", 1), ("small", 0), ("small", 1), ("medium", 0)])
-def test_fp32_parity(ctx32, name, k):
+def test_fp32_parity(ctx32, engine, name, k):
     from paper_1509_04681_b200 import DeviceCsc, to_device_colmajor
     from paper_1509_04681_b200.api import newton_evaluation
     P, ref = oracle_point(name, k)
@@ -146,7 +159,7 @@ def test_fp32_parity(ctx32, name, k):
     aT = O.active_set(ref["GradL"], ref["GradT"], lam, th, P.lam_L, P.lam_T, True, bT)
     ties_L, ties_T = int(aL["tie_mask_L"].sum()), int(aT["tie_mask_T"].sum())
     n_entries = P.q * (P.q + 1) // 2 + P.p * P.q
-    print(f"fp32 {name}/{k}: err_L={err_L:.3e} err_T={err_T:.3e} excluded L={ties_L} T={ties_T} "
+    print(f"fp32 [{engine}] {name}/{k}: err_L={err_L:.3e} err_T={err_T:.3e} excluded L={ties_L} T={ties_T} "
           f"of m_L={aL['m_L']} m_T={aT['m_T']}")
     assert ties_L + ties_T <= max(16, 1e-4 * n_entries), (ties_L, ties_T)
     for rk, ck, tm in (("L_row", "L_col", aL["tie_mask_L"]), ("T_row", "T_col", aT["tie_mask_T"])):

@@ -1,4 +1,4 @@
-"""FP32 SIMT GEMM engine (cggm_test_gemm_f32) on hot-path shapes: TFLOP/s."""
+"""FP32 GEMM engines (cggm_test_gemm_f32: 3xTF32 tcgen05 and SIMT FFMA) on hot-path shapes: TFLOP/s."""
 import ctypes
 import os
 import sys
@@ -10,8 +10,10 @@ from paper_1509_04681_b200 import Context  # noqa
 from paper_1509_04681_b200.api import colmajor_empty, ld_of  # noqa
 
 ctx = Context(0, dtype="f32")
-for (tA, tB, M, N, K) in [(1, 0, 8192, 8192, 8192), (0, 1, 8192, 8192, 8192), (0, 0, 8192, 8192, 8192),
-                          (1, 0, 40000, 20000, 1000), (0, 0, 1000, 20000, 20000)]:
+for eng, (tA, tB, M, N, K) in [(e, s) for e in (0, 1) for s in [
+        (1, 0, 8192, 8192, 8192), (0, 1, 8192, 8192, 8192), (0, 0, 8192, 8192, 8192), (1, 1, 8192, 8192, 8192),
+        (1, 0, 40000, 20000, 1000), (0, 0, 1000, 20000, 20000)]]:
+    ctx._check(ctx.lib.cggm_test_set_f32_engine(ctx.h, eng))
     A = colmajor_empty(K, M, dtype=torch.float32) if tA else colmajor_empty(M, K, dtype=torch.float32)
     B = colmajor_empty(N, K, dtype=torch.float32) if tB else colmajor_empty(K, N, dtype=torch.float32)
     C = colmajor_empty(M, N, dtype=torch.float32)
@@ -28,4 +30,4 @@ for (tA, tB, M, N, K) in [(1, 0, 8192, 8192, 8192), (0, 1, 8192, 8192, 8192), (0
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 3
-    print(f"tA={tA} tB={tB} {M}x{N}x{K}: {ms:.3f} ms {2.0 * M * N * K / ms / 1e9:.2f} TFLOP/s", flush=True)
+    print(f"{('tf32x3', 'ffma')[eng]} tA={tA} tB={tB} {M}x{N}x{K}: {ms:.3f} ms {2.0 * M * N * K / ms / 1e9:.2f} TFLOP/s", flush=True)
