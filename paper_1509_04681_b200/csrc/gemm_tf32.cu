@@ -7,20 +7,20 @@
 //     A B  ~  A_lo B_hi + A_hi B_lo + A_hi B_hi        (the dropped A_lo B_lo is ~2^-22 |A||B|)
 // accumulated in one fp32 TMEM accumulator by tcgen05.mma.kind::tf32 (M = 128, N = 128, K = 8).
 //
-// CTA = 4 producer warps + 4 drain warps (256 threads), one 128 x 128 output tile:
-//  * producers (warps 0-3) stream k-tiles of 32: 16-byte global loads of the raw fp32 operands into
+// CTA = 8 producer warps + 4 drain warps + 1 MMA warp (416 threads), one 128 x 128 output tile:
+//  * producers (warps 0-7) stream k-tiles of 32: 16-byte global loads of the raw fp32 operands into
 //    registers one k-tile ahead, split into hi / lo, and store both into the stage's shared-memory
 //    buffers in the canonical layouts the UMMA descriptors name (K-major: SWIZZLE_128B, one 128-byte
 //    row per m / n; MN-major: SWIZZLE_128B with 32-byte atoms -- the only MN-major layout of 32-bit
 //    operands -- 128-byte rows along m / n, one row per k, 4 KB per 32-wide chunk), then
-//    fence.proxy.async and arrive on the stage's full barrier; thread 0 then issues the PREVIOUS
-//    k-tile's 4 k-steps x 3 products (its barrier has completed by then, so the issue never stalls
-//    the producer) and tcgen05.commit's that stage's empty barrier;
+//    fence.proxy.async and arrive on the stage's full barrier;
+//  * the MMA warp's lane 0 waits on the full barrier, issues 4 k-steps x 3 products and
+//    tcgen05.commit's the stage's empty barrier (the slot is reusable when those MMAs completed);
 //  * hi*hi accumulates in TMEM over chunks of CH k-tiles (two buffers), the corrections in a third
-//    accumulator; the drain warps (tcgen05.ld 32x32b, warp w owns TMEM lanes 32(w%4).. = rows) add
-//    each finished chunk into fp32 registers (the tensor core's own accumulation rounds toward zero),
-//    then the corrections, stage the tile in shared memory and run the engine's common epilogue
-//    (alpha / beta / second output, lower trapezoid, mirrored symmetric writes).
+//    accumulator; the drain warps (tcgen05.ld/st 32x32b, warp w owns TMEM lanes 32(w%4).. = rows)
+//    add each finished chunk into a running fp32 sum kept in TMEM (the tensor core's own accumulation
+//    rounds toward zero), then the corrections, stage the tile in shared memory and run the engine's
+//    common epilogue (alpha / beta / second output, lower trapezoid, mirrored symmetric writes).
 // Same flags, tile order and epilogue contract as the FFMA kernel (gemm_f32.cu), which stays as the
 // A/B alternative (CGGM_F32_ENGINE=ffma, cggm_test_set_f32_engine).
 #include "common.cuh"
@@ -36,11 +36,14 @@ constexpr int T_DATA = TSTAGES * T_STAGE;    // 192 KB
 constexpr int T_EPI_LD = TBM + 1;
 static_assert(TBN * T_EPI_LD * 4 <= T_DATA, "epilogue tile must fit in the stage buffers");
 constexpr int T_SMEM = T_DATA + 1024 + 128;
-constexpr int T_PROD = 128;                  // producer threads (warps 0-3); thread 0 also issues the MMAs
-constexpr int T_DRAIN = 128;                 // accumulator-drain / epilogue threads (warps 4-7)
-constexpr int T_NT = T_PROD + T_DRAIN;
+constexpr int T_PROD = 256;                  // producer threads (warps 0-7)
+constexpr int T_PER = TBM * TBK / 4 / T_PROD;   // float4 per operand per producer thread per k-tile (4)
+constexpr int T_DRAIN = 128;                 // accumulator-drain / epilogue threads (warps 8-11)
+constexpr int T_DW0 = T_PROD / 32;           // first drain warp
+constexpr int T_MMA_WARP = T_DW0 + 4;        // the MMA-issuing warp (12)
+constexpr int T_NT = T_PROD + T_DRAIN + 32;
 constexpr int T_GROUP_N = 8;
-constexpr uint32_t T_TMEM_COLS = 512;   // accumulators: X0 (cols 0-127), D2 (128-255), X1 (256-383)
+constexpr uint32_t T_TMEM_COLS = 512;   // X0 (cols 0-127), D2 (128-255), X1 (256-383), running sum S (384-511)
 
 struct KParamsT {
   int M, N, K;
@@ -146,15 +149,27 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+}
+
 // ---------------------------------------------------------------- producer: loads and the split
-// Operand tile of 128 (m or n) x 32 (k), 1024 float4 = 8 per producer thread.
+// Operand tile of 128 (m or n) x 32 (k), 1024 float4 = 4 per producer thread.
 //  K-inner (element (x, k) at base[k + x ld]):  f -> row x = f >> 3, 16-byte chunk c = f & 7
 //  MN-inner (element (x, k) at base[x + k ld]): f -> k = f >> 5, x = 4 (f & 31)
 template <bool KIN>
-__device__ __forceinline__ void load_tile(float4 (&r)[8], const float* __restrict__ base, int64_t ld, int x0, int X,
+__device__ __forceinline__ void load_tile(float4 (&r)[T_PER], const float* __restrict__ base, int64_t ld, int x0, int X,
                                           int k0, int K, int tid) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < T_PER; ++i) {
     const int f = tid + T_PROD * i;
     int x, k;
     if (KIN) {
@@ -185,9 +200,9 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
 }
 
 template <bool KIN>
-__device__ __forceinline__ void store_split(const float4 (&r)[8], uint32_t hi, uint32_t lo, int tid) {
+__device__ __forceinline__ void store_split(const float4 (&r)[T_PER], uint32_t hi, uint32_t lo, int tid) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < T_PER; ++i) {
     const int f = tid + T_PROD * i;
     uint32_t off;
     if (KIN) {
@@ -246,7 +261,7 @@ __global__ void __launch_bounds__(T_NT, 1) gemm_tf32x3_kernel(const __grid_const
     ptx::mbar_init(accf, 1);
     ptx::fence_barrier_init();
   }
-  if (warp == 4) {
+  if (warp == T_MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(ptx::smem_u32(tmem_slot)),
                  "n"(T_TMEM_COLS)
                  : "memory");
@@ -258,65 +273,68 @@ __global__ void __launch_bounds__(T_NT, 1) gemm_tf32x3_kernel(const __grid_const
   const uint32_t tmem = *tmem_slot;
   const uint32_t sbase = ptx::smem_u32(smem);
 
-  if (warp < 4) {
-    // ---- producers: operand k-tiles, one ahead in registers; after each stage's stores a producer
-    // barrier, then thread 0 issues that stage's MMAs.  With draining, the hi*hi products of chunk c
-    // (CH k-tiles) go to X[c & 1], which the drain warps add into fp32 registers (round-to-nearest)
-    // while the next chunk fills the other buffer; the two corrections (~2^-11 of the result)
-    // accumulate in D2 over the whole k-range.  The tensor core's accumulation rounds toward zero, so
-    // a long k-range in one accumulator is biased by ~k/8 x 2^-24 relative (measured,
-    // tools/debug/tf32_acc_probe.py); bounded chunks keep fp32-class accuracy.
+  if (warp == T_MMA_WARP) {
+    // ---- MMA issue (one thread).  With draining, the hi*hi products of chunk c (CH k-tiles) go to
+    // X[c & 1], which the drain warps add into a running fp32 sum (round-to-nearest) while the next
+    // chunk fills the other buffer; the two corrections (~2^-11 of the result) accumulate in D2 over
+    // the whole k-range.  The tensor core's accumulation rounds toward zero, so a long k-range in one
+    // accumulator is biased by ~k/8 x 2^-24 relative (measured, tools/debug/tf32_acc_probe.py);
+    // bounded chunks keep fp32-class accuracy.
+    if (lane == 0 && nkt > 0) {
+      constexpr uint32_t idesc = idesc_tf32(!AK, !BKI, TBM, TBN);
+      for (int j = 0; j < nkt; ++j) {
+        const int s = j % TSTAGES;
+        const int c = drain ? j / CH : 0;
+        const bool first = drain && (j % CH == 0);
+        if (first && c >= 2) {
+          ptx::mbar_wait(&cempty[c & 1], ((c >> 1) - 1) & 1);
+          tc_fence_after();
+        }
+        ptx::mbar_wait(&full[s], (j / TSTAGES) & 1);
+        tc_fence_after();
+        const uint32_t st = sbase + s * T_STAGE;
+        const uint32_t a_hi = st, a_lo = st + T_OP, b_hi = st + 2 * T_OP, b_lo = st + 3 * T_OP;
+        const uint32_t X = tmem + ((c & 1) ? 256u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < TBK / 8; ++kk) {
+          // K-major: the k-step advances 32 bytes inside the 128-byte swizzled row (SBO = 8 rows = 1 KB);
+          // MN-major: it advances two 4-row k groups (SBO = 512 B; LBO = 4 KB between 32-wide chunks)
+          const uint32_t oa = kk * (AK ? 32 : 1024), ob = kk * (BKI ? 32 : 1024);
+          const uint32_t la = AK ? 16 : 4096, lb = BKI ? 16 : 4096;
+          const uint32_t sa = AK ? 1024 : 512, sb = BKI ? 1024 : 512;
+          const uint64_t ya = AK ? 2 : 1, yb = BKI ? 2 : 1;
+          const uint64_t dah = sdesc(a_hi + oa, la, sa, ya), dal = sdesc(a_lo + oa, la, sa, ya);
+          const uint64_t dbh = sdesc(b_hi + ob, lb, sb, yb), dbl = sdesc(b_lo + ob, lb, sb, yb);
+          if (P.dbg & 1) {
+            umma_tf32(X, dah, dbh, idesc, (first && kk == 0) || (!drain && (j | kk) == 0) ? 0u : 1u);
+          } else if (drain) {
+            umma_tf32(tmem + 128u, dal, dbh, idesc, (j | kk) != 0);
+            umma_tf32(tmem + 128u, dah, dbl, idesc, 1u);
+            umma_tf32(X, dah, dbh, idesc, (first && kk == 0) ? 0u : 1u);
+          } else {
+            umma_tf32(tmem, dal, dbh, idesc, (j | kk) != 0);
+            umma_tf32(tmem, dah, dbl, idesc, 1u);
+            umma_tf32(tmem, dah, dbh, idesc, 1u);
+          }
+        }
+        umma_commit(&empty[s]);   // the slot is free once these MMAs have read it
+        if (drain && (j % CH == CH - 1 || j == nkt - 1)) umma_commit(&cfull[c & 1]);
+      }
+      umma_commit(accf);
+    }
+    __syncwarp();
+  } else if (warp < T_DW0) {
+    // ---- producers (warps 0-7): operand k-tiles, one ahead in registers
     const float* A = P.A;
     const float* B = P.B;
-    float4 ra[8], rb[8];
+    float4 ra[T_PER], rb[T_PER];
     if (nkt > 0) {
       load_tile<AK>(ra, A, P.lda, m0, P.M, kt0 * TBK, P.K, tid);
       load_tile<BKI>(rb, B, P.ldb, n0, P.N, kt0 * TBK, P.K, tid);
     }
-    constexpr uint32_t idesc = idesc_tf32(!AK, !BKI, TBM, TBN);
-    // MMAs of k-tile j (thread 0, after every producer stored it: full[j % TSTAGES])
-    auto issue = [&](int j) {
-      const int s = j % TSTAGES;
-      ptx::mbar_wait(&full[s], (j / TSTAGES) & 1);
-      tc_fence_after();
-      const int c = drain ? j / CH : 0;
-      const bool first = drain && (j % CH == 0);
-      if (first && c >= 2) {
-        ptx::mbar_wait(&cempty[c & 1], ((c >> 1) - 1) & 1);
-        tc_fence_after();
-      }
-      const uint32_t st = sbase + s * T_STAGE;
-      const uint32_t a_hi = st, a_lo = st + T_OP, b_hi = st + 2 * T_OP, b_lo = st + 3 * T_OP;
-      const uint32_t X = tmem + ((c & 1) ? 256u : 0u);
-#pragma unroll
-      for (int kk = 0; kk < TBK / 8; ++kk) {
-        // K-major: the k-step advances 32 bytes inside the 128-byte swizzled row (SBO = 8 rows = 1 KB);
-        // MN-major: it advances two 4-row k groups (SBO = 512 B; LBO = 4 KB between 32-wide chunks)
-        const uint32_t oa = kk * (AK ? 32 : 1024), ob = kk * (BKI ? 32 : 1024);
-        const uint32_t la = AK ? 16 : 4096, lb = BKI ? 16 : 4096;
-        const uint32_t sa = AK ? 1024 : 512, sb = BKI ? 1024 : 512;
-        const uint64_t ya = AK ? 2 : 1, yb = BKI ? 2 : 1;
-        const uint64_t dah = sdesc(a_hi + oa, la, sa, ya), dal = sdesc(a_lo + oa, la, sa, ya);
-        const uint64_t dbh = sdesc(b_hi + ob, lb, sb, yb), dbl = sdesc(b_lo + ob, lb, sb, yb);
-        if (P.dbg & 1) {
-          umma_tf32(X, dah, dbh, idesc, (first && kk == 0) || (!drain && (j | kk) == 0) ? 0u : 1u);
-        } else if (drain) {
-          umma_tf32(tmem + 128u, dal, dbh, idesc, (j | kk) != 0);
-          umma_tf32(tmem + 128u, dah, dbl, idesc, 1u);
-          umma_tf32(X, dah, dbh, idesc, (first && kk == 0) ? 0u : 1u);
-        } else {
-          umma_tf32(tmem, dal, dbh, idesc, (j | kk) != 0);
-          umma_tf32(tmem, dah, dbl, idesc, 1u);
-          umma_tf32(tmem, dah, dbh, idesc, 1u);
-        }
-      }
-      umma_commit(&empty[s]);   // the slot is free once these MMAs have read it
-      if (drain && (j % CH == CH - 1 || j == nkt - 1)) umma_commit(&cfull[c & 1]);
-      if (j == nkt - 1) umma_commit(accf);
-    };
     for (int it = 0; it < nkt; ++it) {
       const int s = it % TSTAGES;
-      float4 na[8], nb[8];
+      float4 na[T_PER], nb[T_PER];
       if (it + 1 < nkt) {
         load_tile<AK>(na, A, P.lda, m0, P.M, (kt0 + it + 1) * TBK, P.K, tid);
         load_tile<BKI>(nb, B, P.ldb, n0, P.N, (kt0 + it + 1) * TBK, P.K, tid);
@@ -327,56 +345,62 @@ __global__ void __launch_bounds__(T_NT, 1) gemm_tf32x3_kernel(const __grid_const
       store_split<BKI>(rb, st + 2 * T_OP, st + 3 * T_OP, tid);
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       ptx::mbar_arrive(&full[s]);
-      // thread 0 issues the previous k-tile's MMAs (its full barrier has long completed: no stall)
-      if (tid == 0 && it > 0) issue(it - 1);
       if (it + 1 < nkt) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < T_PER; ++i) {
           ra[i] = na[i];
           rb[i] = nb[i];
         }
       }
     }
-    if (tid == 0 && nkt > 0) issue(nkt - 1);
   } else {
-    // ---- drain warps 4-7 (warp w reads TMEM lanes 32 (w % 4)..: one accumulator row per thread):
-    // fp32 sums of the chunk partials, then D2, then the epilogue
+    // ---- drain warps 8-11 (warp w reads TMEM lanes 32 (w % 4)..: one accumulator row per thread):
+    // the running fp32 sum S (TMEM cols 384-511) += each finished chunk, then + D2, then the epilogue
     const int dt = tid - T_PROD;
-    const int row = (warp - 4) * 32 + lane;
-    const uint32_t lanebase = tmem + ((uint32_t)((warp - 4) * 32) << 16);
-    float acc[TBN];
+    const int row = (warp - T_DW0) * 32 + lane;
+    const uint32_t lanebase = tmem + ((uint32_t)((warp - T_DW0) * 32) << 16);
+    const int nch = nkt > 0 ? (drain ? (nkt + CH - 1) / CH : 1) : 0;
+    for (int c = 0; c < nch; ++c) {
+      if (drain) ptx::mbar_wait(&cfull[c & 1], (c >> 1) & 1);
+      else ptx::mbar_wait(accf, 0);
+      tc_fence_after();
+      const uint32_t xa = lanebase + ((c & 1) ? 256u : 0u);
+#pragma unroll 1
+      for (int g = 0; g < TBN / 32; ++g) {
+        uint32_t v[32], w[32];
+        tmem_ld32(xa + 32u * g, v);
+        if (c > 0) {
+          tmem_ld32(lanebase + 384u + 32u * g, w);
 #pragma unroll
-    for (int j = 0; j < TBN; ++j) acc[j] = 0.f;
-    if (nkt > 0) {
-      const int nch = drain ? (nkt + CH - 1) / CH : 0;
-      for (int c = 0; c < nch; ++c) {
-        ptx::mbar_wait(&cfull[c & 1], (c >> 1) & 1);
-        tc_fence_after();
-        const uint32_t xa = lanebase + ((c & 1) ? 256u : 0u);
-#pragma unroll
-        for (int g = 0; g < TBN / 32; ++g) {
-          uint32_t v[32];
-          tmem_ld32(xa + 32u * g, v);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) acc[32 * g + j] += __uint_as_float(v[j]);
+          for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(w[j]) + __uint_as_float(v[j]));
         }
-        tc_fence_before();
-        ptx::mbar_arrive(&cempty[c & 1]);
+        tmem_st32(lanebase + 384u + 32u * g, v);
       }
+      tc_fence_before();
+      if (drain) ptx::mbar_arrive(&cempty[c & 1]);
+    }
+    if (nkt > 0 && drain) {
       ptx::mbar_wait(accf, 0);
       tc_fence_after();
-      const uint32_t xa = lanebase + (drain ? 128u : 0u);   // D2 (draining) or the single accumulator
-#pragma unroll
-      for (int g = 0; g < TBN / 32; ++g) {
-        uint32_t v[32];
-        tmem_ld32(xa + 32u * g, v);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) acc[32 * g + j] += __uint_as_float(v[j]);
-      }
     }
     float* Cs = reinterpret_cast<float*>(smem);   // stage buffers: every MMA has completed (accf)
+#pragma unroll 1
+    for (int g = 0; g < TBN / 32; ++g) {
+      uint32_t v[32], w[32];
+      if (nkt > 0) {
+        tmem_ld32(lanebase + 384u + 32u * g, v);
+        if (drain) {
+          tmem_ld32(lanebase + 128u + 32u * g, w);
 #pragma unroll
-    for (int j = 0; j < TBN; ++j) Cs[j * T_EPI_LD + row] = acc[j];
+          for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(w[j]));
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) Cs[(32 * g + j) * T_EPI_LD + row] = __uint_as_float(v[j]);
+    }
     tc_fence_before();
     asm volatile("bar.sync 1, %0;\n" ::"n"(T_DRAIN) : "memory");
     const bool diag = (P.flags & SYM_LOWER) && I == J;
@@ -398,7 +422,7 @@ __global__ void __launch_bounds__(T_NT, 1) gemm_tf32x3_kernel(const __grid_const
     }
   }
   __syncthreads();
-  if (warp == 4) {
+  if (warp == T_MMA_WARP) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(T_TMEM_COLS) : "memory");
   }
