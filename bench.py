@@ -235,6 +235,63 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- FP32 variant
+def _bf16_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"])
+    except Exception:
+        return 1628.6   # B200_PROFILING.md fallback
+
+
+def fp32_variant(configs, steps, P_large=None):
+    """The FP32 variant (reading A18; north_star "with an FP32 variant", `medium fp64+fp32`): one
+    Newton-iteration evaluation in a CGGM_F32 context (3xTF32 on the tcgen05 tensor cores), timed like
+    region A at each config.  Roofline: algorithmic flops (the same count as FP64) / step / the 3xTF32
+    peak = MEASURED_PEAKS bf16 x 1/2 (the guide's nominal tf32 : bf16 ratio) / 3 products."""
+    import torch
+    from paper_1509_04681_b200 import Context, DeviceCsc, newton_evaluation, to_device_colmajor
+    from synth.cggm_inputs import make_problem
+    peak = _bf16_peak() * 0.5 / 3.0
+    out = {"engine": "3xTF32 tcgen05.mma.kind::tf32 (hi/lo split, TMEM accumulators, chunked fp32 drain)",
+           "peak_tflops_3xtf32": peak, "peak_source": "MEASURED_PEAKS.json bf16_tflops x 0.5 (tf32 : bf16) / 3"}
+    for name in configs:
+        P = P_large if (name == "large" and P_large is not None) else make_problem(name)
+        _, lam, th = [pt for pt in P.points if pt[0] == "truth"][0]
+        ctx = Context(0, dtype="f32")
+        f32 = torch.float32
+        X, Y = to_device_colmajor(P.X, dtype=f32), to_device_colmajor(P.Y, dtype=f32)
+        L, T = DeviceCsc.from_host(lam, dtype=f32), DeviceCsc.from_host(th, dtype=f32)
+        Syy, _ = ctx.cggm_covariances(X, Y, want_sxy=False)
+        bufs = {k: torch.empty(0, dtype=torch.int32, device="cuda") for k in ("L_row", "L_col", "T_row", "T_col")}
+        try:
+            newton_evaluation(ctx, X, Y, Syy, L, T, P.lam_L, P.lam_T, True, bufs)
+        except Exception as exc:
+            if getattr(exc, "status", None) != 6:
+                raise
+        mL, mT = ctx.last_active_sizes
+        for k, c_ in (("L_row", mL), ("L_col", mL), ("T_row", mT), ("T_col", mT)):
+            bufs[k] = torch.empty(int(c_ * 1.1) + 1024, dtype=torch.int32, device="cuda")
+        for _ in range(3):
+            r = newton_evaluation(ctx, X, Y, Syy, L, T, P.lam_L, P.lam_T, True, bufs)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            r = newton_evaluation(ctx, X, Y, Syy, L, T, P.lam_L, P.lam_T, True, bufs)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        _, fl = alg_flops(P.n, P.p, P.q, P.theta_star.nnz)
+        ach = fl / (ms * 1e-3) / 1e12
+        out[name] = {"value": 1e3 / ms, "unit": UNIT, "ms_per_step": ms, "steps": steps, "dtype": "f32",
+                     "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                                  "frac": ach / peak},
+                     "f": r["objective"]["f"], "m_L": r["active"]["m_L"], "m_T": r["active"]["m_T"]}
+        del ctx, X, Y, L, T, Syy, bufs, r
+        torch.cuda.empty_cache()
+    return out
+
+
 # ----------------------------------------------------------------------------- launch
 def _free_port() -> int:
     import socket
@@ -289,6 +346,7 @@ def main():
                     help="N > 1: Sigma on rank 0 + broadcast, or the block-cyclic distributed inverse "
                          "(NEXT-3); auto = distributed from 3 GPUs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the FP32-variant timings (medium, large)")
     ap.add_argument("--no-variants", action="store_true", help="skip the eager / changing-Lambda step timings")
     ap.add_argument("--peak-seconds", type=float, default=2.0)
     ap.add_argument("--stream-grad-theta", action="store_true",
@@ -659,6 +717,12 @@ def main():
     if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(P)
     barrier()
+    fp32 = None
+    if world == 1 and not args.no_fp32 and args.config == "large":
+        del bufs
+        ctx.lib.cggm_ctx_release_workspace(ctx.h)
+        torch.cuda.empty_cache()
+        fp32 = fp32_variant(["medium", "large"], max(3, min(args.steps, 5)), P_large=P)
 
     res = last
     obj = res["objective"] if world == 1 else {"f": res["f"]}
@@ -710,6 +774,7 @@ def main():
                              "kernels": hbm} if world == 1 else None,
             "e2e": e2e,
             "factor_reuse": reuse,
+            "fp32": fp32,
             "cpu_baseline": cpu,
             "result": {"f": obj.get("f"), "logdet": res.get("logdet"),
                        "m_L": res["active"]["m_L"], "m_T": res["active"]["m_T"],
