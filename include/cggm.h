@@ -163,7 +163,11 @@ const char* cggm_version(void);
  *                      three data traces are all-reduced, logdet and penalties are replicated.
  * cggm_newton_eval / _host with world > 1 return CGGM_ERR_UNSUPPORTED (the composite overlaps
  * its steps on one GPU; sharded callers compose the collective calls above).
- * Collectives are enqueued on the ctx stream.  Failures return CGGM_ERR_NCCL. */
+ * Collectives are enqueued on the ctx stream.  Failures return CGGM_ERR_NCCL.  After each NCCL
+ * collective the call waits for it on the host while polling ncclCommGetAsyncError, with a deadline
+ * of CGGM_NCCL_TIMEOUT_S seconds (environment, default 600; 0 = no wait): a peer failure or a hung
+ * rank then returns CGGM_ERR_NCCL (the communicator is aborted and detached) instead of blocking
+ * the caller forever. */
 /* All-reduce over peer memory (CUDA IPC; NVLink peer loads / stores between the GPUs of a node),
  * the alternative to NCCL for the partial sums: every rank registers one symmetric buffer of the
  * same size (cggm_ipc_get_handle on its own, cggm_ipc_open_handle on the others' handles, exchanged
@@ -283,6 +287,25 @@ cggm_status cggm_psi_grad(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64
 cggm_status cggm_grad_lambda(cggm_ctx* ctx, int64_t q, const void* Syy, int64_t ldsyy,
                              const void* Sigma, int64_t ldsigma, const void* Psi, int64_t ldpsi,
                              void* GradL, int64_t ldgl);
+
+/* ---- sample-sharded grad_Theta by column ranges (SURVEY.md §8(e) "Better": reduce-scatter over
+ * column blocks, local compaction, all-gather of the compact lists; sharded.ShardedEvaluator with
+ * grad_theta="reduce_scatter").  No rank ever holds a p x q buffer. */
+/* Psi (q x q, ldpsi; this shard's partial R_r^T R_r, all-reduced when a communicator is attached) and
+ * E (n_local x q, lde) = Y_r + X_r Theta Sigma, the residual whose (2/n_total) X_r^T E_r is the
+ * shard's grad_Theta partial (identity I3); W = X Theta as in cggm_psi_grad. */
+cggm_status cggm_psi_residual(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64_t p, int64_t q, const void* X,
+                              int64_t ldx, const void* Y, int64_t ldy, const cggm_csc* Theta, const void* Sigma,
+                              int64_t ldsigma, void* Psi, int64_t ldpsi, void* E, int64_t lde);
+/* S_Theta = {(i,j) : |GradT_ij| > lam_T or Theta_ij != 0} restricted to the columns
+ * [col0, col0 + ncols): GradT is that column block (p x ncols, ldgt; device), Theta the full p x q
+ * CSC.  Entries are written in column-major order with GLOBAL column indices into T_row / T_col
+ * (device, capacity cap).  Host outputs: m = the block's |S_Theta| (CGGM_ERR_CAPACITY when m > cap;
+ * m then holds the required size), ties (nullable) = entries within tie_eps of lam_T not forced by the
+ * support, subgrad (nullable) = the block's Theta part of ||grad^S||_1. */
+cggm_status cggm_active_theta_block(cggm_ctx* ctx, int64_t p, int64_t col0, int64_t ncols, const void* GradT,
+                                   int64_t ldgt, const cggm_csc* Theta, double lam_T, double tie_eps, int32_t* T_row,
+                                   int32_t* T_col, int64_t cap, int64_t* m, int64_t* ties, double* subgrad);
 
 /* ---- a6: active sets + stopping statistic (§2.2, §5.1) -------------
  * S_Lambda = {(i,j), i <= j : |GradL_ij| > lam_ij or Lambda_ij != 0}, lam_ii = 0 if !penalize_diag

@@ -79,6 +79,11 @@ SIGNATURES = {
                                              ctypes.POINTER(cggm_csc), ctypes.POINTER(cggm_csc), c_d, c_d, c_i32,
                                              c_vp, c_i64, c_vp, c_i64, c_d, ctypes.POINTER(cggm_objective_out)]),
     "cggm_densify": (c_i32, [c_vp, ctypes.POINTER(cggm_csc), c_vp, c_i64]),
+    "cggm_psi_residual": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, ctypes.POINTER(cggm_csc),
+                                  c_vp, c_i64, c_vp, c_i64, c_vp, c_i64]),
+    "cggm_active_theta_block": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, ctypes.POINTER(cggm_csc), c_d, c_d,
+                                        c_vp, c_vp, c_i64, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64),
+                                        ctypes.POINTER(c_d)]),
     "cggm_comm_info": (c_i32, [c_vp, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)]),
     "cggm_ctx_create": (c_i32, [ctypes.POINTER(c_vp), c_i32, c_i32, c_vp]),
     "cggm_ctx_destroy": (c_i32, [c_vp]),

@@ -359,6 +359,42 @@ class Context:
                                               _ptr(Psi), ld_of(Psi), _ptr(GradL), ld_of(GradL)))
         return GradL
 
+    def cggm_psi_residual(self, X, Y, Theta: DeviceCsc, Sigma, n_total=None, Psi=None, E=None):
+        """Psi partial (all-reduced with a communicator) and the residual E = Y + X Theta Sigma
+        (include/cggm.h, sample-sharded grad_Theta by column ranges)."""
+        self._sync_stream()
+        n, p = X.shape
+        q = Y.shape[1]
+        n_total = n if n_total is None else n_total
+        if Psi is None:
+            Psi = colmajor_empty(q, q, device=X.device, dtype=self.tdtype)
+        if E is None:
+            E = colmajor_empty(n, q, device=X.device, dtype=self.tdtype)
+        ts = Theta.c_struct()
+        self._check(self.lib.cggm_psi_residual(self.h, n, n_total, p, q, _ptr(X), ld_of(X), _ptr(Y), ld_of(Y),
+                                               ctypes.byref(ts), _ptr(Sigma), ld_of(Sigma), _ptr(Psi), ld_of(Psi),
+                                               _ptr(E), ld_of(E)))
+        return Psi, E
+
+    def cggm_active_theta_block(self, GradT_block, Theta: DeviceCsc, col0, lam_T, tie_eps, T_row, T_col):
+        """S_Theta entries of the column block [col0, col0 + ncols) (global column indices) written
+        into T_row / T_col from offset 0; returns (m, ties, subgrad_theta_part).  CGGM_ERR_CAPACITY
+        carries the required size in the exception's `m`."""
+        self._sync_stream()
+        p, nc = GradT_block.shape
+        ts = Theta.c_struct()
+        m, ties, sub = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_double()
+        st = self.lib.cggm_active_theta_block(self.h, p, int(col0), nc, _ptr(GradT_block), ld_of(GradT_block),
+                                              ctypes.byref(ts), float(lam_T), float(tie_eps), _ptr(T_row), _ptr(T_col),
+                                              int(T_row.numel()), ctypes.byref(m), ctypes.byref(ties),
+                                              ctypes.byref(sub))
+        if st == 6:
+            err = CggmError(st, self.lib.cggm_last_error(self.h).decode())
+            err.m = int(m.value)
+            raise err
+        self._check(st)
+        return int(m.value), int(ties.value), float(sub.value)
+
     # ---------------------------------------------------------------- a6
     @staticmethod
     def _active_struct(spec: dict) -> _abi.cggm_active_out:

@@ -132,6 +132,12 @@ cggm_status guard(cggm_ctx* ctx, F f) {
   }
 }
 
+// column indices of a block's S_Theta entries, local -> global (cggm_active_theta_block)
+__global__ void k_col_offset(int32_t* col, const ActTotals* tot, long long cap, int32_t off) {
+  const long long m = min((long long)tot->m_T, cap);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x)
+    col[i] += off;
+}
 }  // namespace
 }  // namespace cggm
 
@@ -971,14 +977,17 @@ template <typename T>
 static void psi_enqueue(Ctx* c, int64_t n_local, int64_t n_total, int64_t p, int64_t q, const T* Xd, int64_t ldx,
                         const T* Yd, int64_t ldy, const T* W, int64_t ldw, const T* Sg, int64_t ldsigma, const T* Syy,
                         int64_t ldsyy, const T* Sxy, int64_t ldsxy, T* Psi, int64_t ldpsi, T* GradL, int64_t ldgl,
-                        T* GradT, int64_t ldgt, const Fuse* fz, bool collective = false) {
+                        T* GradT, int64_t ldgt, const Fuse* fz, bool collective = false, T* E_out = nullptr,
+                        int64_t lde_out = 0) {
   const int64_t ldn = pad_ld<T>(n_local > 0 ? n_local : 1);
   const int dt = sizeof(T) == 4 ? 1 : 0;
   T* R = static_cast<T*>(ws_get(c, WS_R, (size_t)ldn * q * sizeof(T)));
-  T* E = static_cast<T*>(ws_get(c, WS_E, (size_t)ldn * q * sizeof(T)));
+  // E = Y + W Sigma: library workspace, or the caller's buffer (cggm_psi_residual)
+  T* E = E_out ? E_out : static_cast<T*>(ws_get(c, WS_E, (size_t)ldn * q * sizeof(T)));
+  const int64_t lde = E_out ? lde_out : ldn;
   {  // a4: acc = W Sigma -> R = acc / sqrt(n), E = Y + acc
     Phase ph(c, TAG_WSIGMA);
-    const bool want_e = (GradT || fz) && !Sxy;
+    const bool want_e = ((GradT || fz) && !Sxy) || E_out;
     if (sizeof(T) == 8 && split_wsigma(c, n_local, q)) {
       // too few 128x128 tiles for whole waves (n = 1000, q = 20000: 8.5 waves): both k-halves of
       // each tile as separate CTAs, partials added into a zeroed accumulator, then R and E
@@ -986,11 +995,11 @@ static void psi_enqueue(Ctx* c, int64_t n_local, int64_t n_total, int64_t p, int
       CGGM_CUDA_CHECK(cudaMemsetAsync(Acc, 0, (size_t)ldn * q * sizeof(T), c->stream));
       EpilogueT<T> e; e.out1 = Acc; e.ld1 = ldn; e.a1 = 1.0;
       gemm(c, false, false, n_local, q, q, W, ldw, Sg, ldsigma, e, SPLIT_K2);
-      r_e_from_acc(c, n_local, q, Acc, ldn, Yd, ldy, R, ldn, want_e ? E : nullptr, ldn,
+      r_e_from_acc(c, n_local, q, Acc, ldn, Yd, ldy, R, ldn, want_e ? E : nullptr, lde,
                    1.0 / std::sqrt((double)n_total));
     } else {
       EpilogueT<T> e; e.out1 = R; e.ld1 = ldn; e.a1 = 1.0 / std::sqrt((double)n_total);
-      if (want_e) { e.out2 = E; e.ld2 = ldn; e.a2 = 1.0; e.in2a = Yd; e.ld2a = ldy; e.b2 = 1.0; }
+      if (want_e) { e.out2 = E; e.ld2 = lde; e.a2 = 1.0; e.in2a = Yd; e.ld2a = ldy; e.b2 = 1.0; }
       gemm(c, false, false, n_local, q, q, W, ldw, Sg, ldsigma, e, 0);
     }
   }
@@ -1017,7 +1026,7 @@ static void psi_enqueue(Ctx* c, int64_t n_local, int64_t n_total, int64_t p, int
     EpilogueT<T> e; e.out1 = out; e.ld1 = ldo;
     if (!Sxy) {
       e.a1 = 2.0 / (double)n_total;
-      gemm(c, true, false, p, nc, n_local, Xd, ldx, E + j0 * ldn, ldn, e, 0);
+      gemm(c, true, false, p, nc, n_local, Xd, ldx, E + j0 * lde, lde, e, 0);
     } else {
       e.a1 = 2.0 / std::sqrt((double)n_total);
       e.in1a = Sxy + j0 * ldsxy; e.ld1a = ldsxy; e.b1 = 2.0;
@@ -1109,6 +1118,86 @@ cggm_status cggm_grad_lambda(cggm_ctx* ctx, int64_t q, const void* Syy, int64_t 
       grad_lambda<T>(c, q, static_cast<const T*>(Syy), ldsyy, static_cast<const T*>(Sigma), ldsigma,
                      static_cast<const T*>(Psi), ldpsi, static_cast<T*>(GradL), ldgl);
     });
+  });
+}
+
+// Psi partial (all-reduced with a communicator) and the residual E = Y + X Theta Sigma of this
+// shard's rows into the caller's buffer: the sharded evaluation's grad_Theta is then formed column
+// block by column block ((2/n) X_r^T E_r, cggm_gemm) and reduce-scattered by the caller.
+cggm_status cggm_psi_residual(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64_t p, int64_t q, const void* X,
+                              int64_t ldx, const void* Y, int64_t ldy, const cggm_csc* Theta, const void* Sigma,
+                              int64_t ldsigma, void* Psi, int64_t ldpsi, void* E, int64_t lde) {
+  return guard(ctx, [&](Ctx* c) {
+    if (n_local < 0 || p < 0 || q < 0) fail(CGGM_ERR_INVALID_ARG, "negative dimension");
+    if (n_total < 1 || n_total < n_local) fail(CGGM_ERR_INVALID_ARG, "n_total must be >= max(1, n_local)");
+    check_dense("X", X, n_local, p, ldx);
+    check_dense("Y", Y, n_local, q, ldy);
+    check_csc_host("Theta", Theta, p, q);
+    check_dense("Sigma", Sigma, q, q, ldsigma);
+    check_dense("Psi", Psi, q, q, ldpsi);
+    check_dense("E", E, n_local, q, lde);
+    if (q == 0) return;
+    validate_csc_dev(c, Theta, false, "Theta");
+    dispatch(c, [&](auto tag) {
+      using T = decltype(tag);
+      const int64_t ldn = pad_ld<T>(n_local > 0 ? n_local : 1);
+      T* W = static_cast<T*>(ws_get(c, WS_W, (size_t)ldn * q * sizeof(T)));
+      spmm_x_theta<T>(c, static_cast<const T*>(X), ldx, n_local, Theta, ViewT<T>{W, ldn, n_local, q});
+      psi_enqueue<T>(c, n_local, n_total, p, q, static_cast<const T*>(X), ldx, static_cast<const T*>(Y), ldy, W, ldn,
+                     static_cast<const T*>(Sigma), ldsigma, nullptr, 0, nullptr, 0, static_cast<T*>(Psi), ldpsi,
+                     nullptr, 0, nullptr, 0, nullptr, comm_attached(c), static_cast<T*>(E), lde);
+    });
+  });
+}
+
+// S_Theta entries of columns [col0, col0 + ncols) from a gradient block (P:296-303 for that block,
+// reading A5-A7), with global column indices, in column-major order; host totals.  The block of a
+// column-range owner in the sharded evaluation (its reduce-scattered grad_Theta columns).
+cggm_status cggm_active_theta_block(cggm_ctx* ctx, int64_t p, int64_t col0, int64_t ncols, const void* GradT,
+                                   int64_t ldgt, const cggm_csc* Theta, double lam_T, double tie_eps, int32_t* T_row,
+                                   int32_t* T_col, int64_t cap, int64_t* m, int64_t* ties, double* subgrad) {
+  return guard(ctx, [&](Ctx* c) {
+    if (p < 0 || ncols < 0 || col0 < 0) fail(CGGM_ERR_INVALID_ARG, "negative dimension or column");
+    if (!Theta) fail(CGGM_ERR_INVALID_ARG, "null Theta");
+    if (col0 + ncols > Theta->ncols) fail(CGGM_ERR_SHAPE, "column block beyond Theta's columns");
+    check_csc_host("Theta", Theta, p, Theta->ncols);
+    check_dense("GradT", GradT, p, ncols, ldgt);
+    if (!(lam_T >= 0.0) || !(tie_eps >= 0.0)) fail(CGGM_ERR_INVALID_ARG, "negative lambda or tie_eps");
+    if (cap < 0 || (cap > 0 && (!T_row || !T_col))) fail(CGGM_ERR_INVALID_ARG, "bad output list");
+    if (!m) fail(CGGM_ERR_INVALID_ARG, "null m");
+    *m = 0;
+    if (ties) *ties = 0;
+    if (subgrad) *subgrad = 0.0;
+    if (ncols == 0) return;
+    validate_csc_dev(c, Theta, false, "Theta");
+    // the block as a CSC of its own: the column pointers of columns col0.. (absolute offsets into the
+    // same row / value arrays)
+    cggm_csc sub = *Theta;
+    sub.ncols = ncols;
+    sub.colptr = Theta->colptr + col0;
+    ActTotals* tot = nullptr;
+    dispatch(c, [&](auto tag) {
+      using T = decltype(tag);
+      ActWs ws = active_ws(c, ncols);
+      Phase ph(c, TAG_ACTIVE);
+      active_begin(c, ncols, ws);
+      active_theta_chunk<T>(c, p, 0, ncols, static_cast<const T*>(GradT), ldgt, &sub, lam_T, tie_eps, ws, T_row, T_col,
+                            cap);
+      active_end(c, ncols, ws);
+      if (col0 > 0 && cap > 0) {
+        k_col_offset<<<c->num_sms, 256, 0, c->stream>>>(T_col, ws.tot, cap, (int32_t)col0);
+        post_launch(c, "k_col_offset");
+      }
+      tot = ws.tot;
+    });
+    ActTotals h;
+    CGGM_CUDA_CHECK(cudaMemcpyAsync(c->host_scratch, tot, sizeof(ActTotals), cudaMemcpyDeviceToHost, c->stream));
+    CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    std::memcpy(&h, c->host_scratch, sizeof(ActTotals));
+    *m = h.m_T;
+    if (ties) *ties = h.ties_T;
+    if (subgrad) *subgrad = h.sub_T;
+    if (h.m_T > cap) fail(CGGM_ERR_CAPACITY, "S_Theta block larger than capacity (m=" + std::to_string(h.m_T) + ")");
   });
 }
 

@@ -5,8 +5,11 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <thread>
 
 #include "common.cuh"
 
@@ -25,6 +28,8 @@ struct NcclApi {
                             cudaStream_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
 };
 
 const NcclApi& nccl() {
@@ -46,8 +51,10 @@ const NcclApi& nccl() {
     api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
     api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(sym("ncclBroadcast"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+    api.CommGetAsyncError = reinterpret_cast<decltype(api.CommGetAsyncError)>(sym("ncclCommGetAsyncError"));
+    api.CommAbort = reinterpret_cast<decltype(api.CommAbort)>(sym("ncclCommAbort"));
     api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.Broadcast &&
-             api.GetErrorString;
+             api.GetErrorString && api.CommGetAsyncError && api.CommAbort;
     if (!api.ok) api.why = "libnccl.so.2 lacks an expected symbol";
   });
   return api;
@@ -59,6 +66,52 @@ const NcclApi& nccl() {
 
 ncclDataType_t nccl_type(int dtype) { return dtype == 1 ? ncclFloat32 : ncclFloat64; }
 
+// A collective that never completes (a peer died, a hung rank) would otherwise block the caller's
+// next synchronisation forever: after each NCCL call, wait for it on the host while polling the
+// communicator's asynchronous error state, with a deadline (CGGM_NCCL_TIMEOUT_S, default 600 s;
+// 0 disables the wait).  On an error or the deadline the communicator is aborted (so no later call
+// can hang on it) and CGGM_ERR_NCCL is returned.
+double nccl_timeout_s() {
+  static double t = [] {
+    const char* e = std::getenv("CGGM_NCCL_TIMEOUT_S");
+    return e ? std::atof(e) : 600.0;
+  }();
+  return t;
+}
+
+void nccl_wait(Ctx* c, const char* what) {
+  const double limit = nccl_timeout_s();
+  if (limit <= 0) return;
+  cudaEvent_t ev;
+  CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CGGM_CUDA_CHECK(cudaEventRecord(ev, c->stream));
+  const auto t0 = std::chrono::steady_clock::now();
+  ncclComm_t comm = static_cast<ncclComm_t>(c->comm.nccl);
+  for (;;) {
+    const cudaError_t q = cudaEventQuery(ev);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) {
+      cudaEventDestroy(ev);
+      CGGM_CUDA_CHECK(q);
+    }
+    ncclResult_t ae = ncclSuccess;
+    nccl().CommGetAsyncError(comm, &ae);
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if ((ae != ncclSuccess && ae != ncclInProgress) || el > limit) {
+      cudaEventDestroy(ev);
+      nccl().CommAbort(comm);
+      c->comm = CommState{};   // detached: the calls are single-rank again
+      throw CudaError{CGGM_ERR_NCCL, std::string(what) + (ae != ncclSuccess && ae != ncclInProgress
+                                                              ? std::string(": asynchronous error ") +
+                                                                    nccl().GetErrorString(ae)
+                                                              : ": not complete after " + std::to_string(limit) +
+                                                                    " s (CGGM_NCCL_TIMEOUT_S); communicator aborted")};
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+  cudaEventDestroy(ev);
+}
+
 }  // namespace
 
 void comm_allreduce(Ctx* c, void* buf, int64_t count, int dtype) {
@@ -67,6 +120,7 @@ void comm_allreduce(Ctx* c, void* buf, int64_t count, int dtype) {
     const ncclResult_t r = nccl().AllReduce(buf, buf, (size_t)count, nccl_type(dtype), ncclSum,
                                             static_cast<ncclComm_t>(c->comm.nccl), c->stream);
     if (r != ncclSuccess) nccl_fail("ncclAllReduce", r);
+    nccl_wait(c, "ncclAllReduce");
   } else {
     CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
     if (c->comm.ar(c->comm.user, buf, count, dtype) != 0)
@@ -80,6 +134,7 @@ void comm_bcast(Ctx* c, void* buf, int64_t count, int dtype, int root) {
     const ncclResult_t r = nccl().Broadcast(buf, buf, (size_t)count, nccl_type(dtype), root,
                                             static_cast<ncclComm_t>(c->comm.nccl), c->stream);
     if (r != ncclSuccess) nccl_fail("ncclBroadcast", r);
+    nccl_wait(c, "ncclBroadcast");
   } else {
     CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
     if (c->comm.bc(c->comm.user, buf, count, dtype, root) != 0)

@@ -72,6 +72,38 @@ class CudaBackend:
     def grad_lambda(self, Syy, Sigma, Psi):
         return self.ctx.cggm_grad_lambda(Syy, Sigma, Psi)
 
+    # sample-sharded grad_Theta by column ranges (reduce-scatter, local compaction, list all-gather)
+    def psi_residual_partial(self, X, Y, Theta, Sigma, n_total):
+        return self.ctx.cggm_psi_residual(X, Y, Theta, Sigma, n_total=n_total)
+
+    def grad_theta_block(self, X, E, c0, c1, n_total, out):
+        """out (p x (c1 - c0)) = (2/n) X_r^T E_r[:, c0:c1], this shard's grad_Theta partial (I3)."""
+        self.ctx.cggm_gemm(out, X, E[:, c0:c1], transA=True, alpha=2.0 / n_total)
+
+    def active_lambda_only(self, GradL, Lam, lam_L, penalize_diag, tie_eps):
+        """S_Lambda and the Lambda part of the statistic (the Theta side empty: a 1 x q zero gradient
+        with an empty Theta and lam_T = 1 contributes no entry and 0)."""
+        from .api import DeviceCsc, colmajor_empty
+        q = GradL.shape[0]
+        key = ("lam_only", q)
+        if getattr(self, "_lam_only_key", None) != key:
+            self._zero_gt = colmajor_empty(1, q, device=GradL.device, dtype=GradL.dtype, zero=True)
+            self._empty_th = DeviceCsc(1, q, torch.zeros(q + 1, dtype=torch.int64, device=GradL.device),
+                                       torch.zeros(0, dtype=torch.int32, device=GradL.device),
+                                       torch.zeros(0, dtype=GradL.dtype, device=GradL.device))
+            self._lam_only_key = key
+        return self.ctx.cggm_active_set(GradL, self._zero_gt, Lam, self._empty_th, lam_L, 1.0, penalize_diag, tie_eps)
+
+    def active_theta_block(self, G, Theta, c0, lam_T, tie_eps, T_row, T_col):
+        return self.ctx.cggm_active_theta_block(G, Theta, c0, lam_T, tie_eps, T_row, T_col)
+
+    def flat_zeros(self, count, like):
+        return torch.zeros(count, dtype=like.dtype, device=like.device)
+
+    def int_lists(self, cap, like):
+        return (torch.empty(cap, dtype=torch.int32, device=like.device),
+                torch.empty(cap, dtype=torch.int32, device=like.device))
+
     def active_set(self, GradL, GradT, Lam, Theta, lam_L, lam_T, penalize_diag, tie_eps):
         return self.ctx.cggm_active_set(GradL, GradT, Lam, Theta, lam_L, lam_T, penalize_diag, tie_eps)
 
@@ -81,6 +113,29 @@ class CudaBackend:
     def objective_given_inverse_partial(self, X, Y, Lam, Theta, lam_L, lam_T, penalize_diag, n_total, Linv, logdet):
         return self.ctx.cggm_objective_given_inverse(X, Y, Lam, Theta, lam_L, lam_T, Linv, logdet,
                                                      penalize_diag=penalize_diag, n_total=n_total)
+
+    def _obj_ctx(self, group):
+        """A second context on the device with a library-owned communicator over `group` (NCCL, or the
+        torch group's own collectives for gloo): its cggm_objective / cggm_objective_given_inverse are
+        collective -- the shards' trace partials are all-reduced and f assembled inside libcggm."""
+        if getattr(self, "_octx", None) is None:
+            from .api import Context
+            c = Context(self.ctx.device, dtype="f64" if self.ctx.tdtype == torch.float64 else "f32")
+            if dist.get_backend(group) == "nccl":
+                c.comm_init(group)
+            else:
+                c.comm_init_torch(group)
+            self._octx = c
+        return self._octx
+
+    def objective_sharded(self, X, Y, Lam, Theta, lam_L, lam_T, penalize_diag, n_total, group, Linv=None,
+                          logdet=None):
+        """The whole objective of the sharded data, assembled by the library's collective calls."""
+        c = self._obj_ctx(group)
+        if Linv is None:
+            return c.cggm_objective(X, Y, Lam, Theta, lam_L, lam_T, penalize_diag, n_total=n_total)
+        return c.cggm_objective_given_inverse(X, Y, Lam, Theta, lam_L, lam_T, Linv, logdet,
+                                              penalize_diag=penalize_diag, n_total=n_total)
 
     # dense building blocks (DistributedInverse)
     def zeros(self, rows, cols):
@@ -111,8 +166,18 @@ class ShardedEvaluator:
     memory (peer_allreduce, CudaBackend only)."""
 
     def __init__(self, backend, group=None, replicate_inverse: bool = False, split_objective: bool = True,
-                 distributed_inverse: bool = False, block: int = 2048, peer_allreduce: bool = False):
+                 distributed_inverse: bool = False, block: int = 2048, peer_allreduce: bool = False,
+                 grad_theta: str = "allreduce", rs_width: int = 256):
         self.b = backend
+        # grad_Theta: "allreduce" = every rank holds the summed p x q gradient (north_star's all-reduce);
+        # "reduce_scatter" = column ranges owned by the ranks, each column block's partials
+        # reduce-scattered (rs_width columns per owner per round), compacted by the owner, the compact
+        # S_Theta lists all-gathered (SURVEY.md §8(e) "Better"): no rank holds a p x q buffer
+        if grad_theta not in ("allreduce", "reduce_scatter"):
+            raise ValueError(f"grad_theta must be allreduce or reduce_scatter, not {grad_theta!r}")
+        self.grad_theta = grad_theta
+        self.rs_width = int(rs_width)
+        self._rs = {}
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -204,6 +269,102 @@ class ShardedEvaluator:
         ob["fail_col"] = int(ob["fail_col"])
         return ob
 
+    def _reduce_scatter(self, flat_in, flat_out):
+        """flat_out = block `rank` of the element-wise sum over ranks of flat_in (world equal blocks)."""
+        if self.world == 1:
+            flat_out.copy_(flat_in[:flat_out.numel()])
+            return
+        if dist.get_backend(self.group) == "nccl":
+            dist.reduce_scatter_tensor(flat_out, flat_in, group=self.group)
+        else:   # gloo has no reduce-scatter: all-reduce, keep this rank's block (same sums)
+            h = flat_in.cpu()
+            dist.all_reduce(h, group=self.group)
+            k = flat_out.numel()
+            flat_out.copy_(h[self.rank * k:(self.rank + 1) * k].to(flat_out.device))
+
+    def _all_gather_lists(self, rows, cols, m):
+        """Concatenation in rank order of every rank's first m entries (rank r owns an ascending column
+        range, so the result is the global column-major list, identical on every rank)."""
+        if self.world == 1:
+            return rows[:m].clone(), cols[:m].clone()
+        host = dist.get_backend(self.group) == "gloo"
+        dev = rows.device
+        cnt = torch.tensor([m], dtype=torch.int64, device="cpu" if host else dev)
+        cnts = [torch.zeros_like(cnt) for _ in range(self.world)]
+        dist.all_gather(cnts, cnt, group=self.group)
+        cnts = [int(c.item()) for c in cnts]
+        mx = max(max(cnts), 1)
+        out = []
+        for src in (rows, cols):
+            loc = torch.zeros(mx, dtype=src.dtype, device="cpu" if host else dev)
+            loc[:m].copy_(src[:m])
+            parts = [torch.empty_like(loc) for _ in range(self.world)]
+            dist.all_gather(parts, loc, group=self.group)
+            out.append(torch.cat([pt[:c] for pt, c in zip(parts, cnts)]).to(dev))
+        return out[0], out[1]
+
+    def _grad_theta_reduce_scatter(self, X_r, E, Theta, lam_T, tie_eps, actL):
+        """S_Theta without a stored p x q gradient: ranks own balanced column ranges; round t forms,
+        for every owner r, the partial (2/n) X^T E[:, a_r + t w : a_r + (t + 1) w] into block r of a
+        p x (world w) buffer, reduce-scatters it (block r, summed, to rank r) and the owner compacts
+        its block (global column indices).  The compact lists are all-gathered at the end."""
+        n = self.n_total
+        p, q = X_r.shape[1], Theta.ncols
+        G, me = self.world, self.rank
+        ranges = [shard_rows(q, G, r) for r in range(G)]
+        span = max(b - a for a, b in ranges)
+        w = max(1, min(self.rs_width, span))
+        ld = p + (p & 1)
+        key = (p, q, G, w)
+        if self._rs.get("key") != key:
+            self._rs = {"key": key, "buf": self.b.flat_zeros(G * ld * w, E), "out": self.b.flat_zeros(ld * w, E)}
+            self._rs["T_row"], self._rs["T_col"] = self.b.int_lists(max(4096, 2 * Theta.nnz // G + p), E)
+        buf, outf = self._rs["buf"], self._rs["out"]
+
+        def block(flat, r):   # p x w column-major view of block r (leading dimension ld)
+            return torch.as_strided(flat, (p, w), (1, ld), r * ld * w)
+
+        a_me, b_me = ranges[me]
+        m_tot, ties, sub = 0, 0, 0.0
+        for t in range((span + w - 1) // w):
+            for r, (a, b) in enumerate(ranges):
+                c0, c1 = a + t * w, min(b, a + (t + 1) * w)
+                if c1 > c0:
+                    self.b.grad_theta_block(X_r, E, c0, c1, n, block(buf, r)[:, :c1 - c0])
+            self._reduce_scatter(buf, outf)
+            c0, c1 = a_me + t * w, min(b_me, a_me + (t + 1) * w)
+            if c1 <= c0:
+                continue
+            G_blk = block(outf, 0)[:, :c1 - c0]
+            while True:
+                T_row, T_col = self._rs["T_row"], self._rs["T_col"]
+                try:
+                    mb, tb, sb = self.b.active_theta_block(G_blk, Theta, c0, lam_T, tie_eps, T_row[m_tot:],
+                                                           T_col[m_tot:])
+                    break
+                except Exception as exc:   # CGGM_ERR_CAPACITY: grow the lists, keep what is written
+                    need = getattr(exc, "m", None)
+                    if need is None:
+                        raise
+                    nr, nc = self.b.int_lists(2 * (m_tot + need) + 4096, E)
+                    nr[:m_tot].copy_(T_row[:m_tot])
+                    nc[:m_tot].copy_(T_col[:m_tot])
+                    self._rs["T_row"], self._rs["T_col"] = nr, nc
+            m_tot += mb
+            ties += tb
+            sub += sb
+        T_row, T_col = self._all_gather_lists(self._rs["T_row"], self._rs["T_col"], m_tot)
+        tot = torch.tensor([float(ties), sub], dtype=torch.float64)
+        if G > 1:
+            host = dist.get_backend(self.group) == "gloo"
+            tot = tot if host else tot.to(E.device)
+            dist.all_reduce(tot, group=self.group)
+        ties_T, sub_T = float(tot[0]), float(tot[1])
+        act = dict(actL)
+        act.update(T_row=T_row, T_col=T_col, m_T=int(T_row.numel()), ties_T=int(round(ties_T)),
+                   subgrad_l1=float(actL["subgrad_l1"]) + sub_T)
+        return act
+
     def evaluate(self, X_r, Y_r, Lam, Theta, lam_L, lam_T, penalize_diag=True, tie_eps=1e-9):
         n = self.n_total
         q = Lam.nrows
@@ -230,6 +391,19 @@ class ShardedEvaluator:
             dist.broadcast(meta, src=self._g(0), group=self.group)
             logdet, pd, fc = float(meta[0]), bool(meta[1] > 0.5), int(meta[2])
             self._mark("bcast_sigma")
+        if self.grad_theta == "reduce_scatter":
+            Psi, E = self.b.psi_residual_partial(X_r, Y_r, Theta, Sigma, n)
+            self._mark("psi_residual")
+            self._allreduce(Psi)
+            self._mark("allreduce_psi")
+            GradL = self.b.grad_lambda(self.Syy, Sigma, Psi)
+            actL = self.b.active_lambda_only(GradL, Lam, lam_L, penalize_diag, tie_eps)
+            self._mark("grad_lambda_active")
+            act = self._grad_theta_reduce_scatter(X_r, E, Theta, lam_T, tie_eps, actL)
+            self._mark("reduce_scatter_grad_theta")
+            GradT = None
+            return self._finish(Sigma, logdet, pd, fc, Psi, GradL, GradT, act, X_r, Y_r, Lam, Theta, lam_L, lam_T,
+                                penalize_diag, n)
         if self.peer is not None:
             if self._peer_out is None:   # symmetric buffers, allocated once (same shapes every call)
                 p = X_r.shape[1]
@@ -245,44 +419,36 @@ class ShardedEvaluator:
         GradL = self.b.grad_lambda(self.Syy, Sigma, Psi)
         act = self.b.active_set(GradL, GradT, Lam, Theta, lam_L, lam_T, penalize_diag, tie_eps)
         self._mark("grad_lambda_active")
+        return self._finish(Sigma, logdet, pd, fc, Psi, GradL, GradT, act, X_r, Y_r, Lam, Theta, lam_L, lam_T,
+                            penalize_diag, n)
+
+    def _finish(self, Sigma, logdet, pd, fc, Psi, GradL, GradT, act, X_r, Y_r, Lam, Theta, lam_L, lam_T,
+                penalize_diag, n):
+        """The line-search objective and the result.  f comes from libcggm in every mode: the split
+        objective rank's cggm_objective on all rows (scalars broadcast); otherwise the library's
+        collective cggm_objective / cggm_objective_given_inverse (trace partials all-reduced inside the
+        library) through the backend's objective_sharded."""
         if self.split:
             # the objective rank evaluated the whole objective on all rows (see _objective_split)
             ob = self._ob_split
-            parts = torch.tensor([ob["tr_syy_lam"], ob["tr_sxy_theta"], ob["tr_sigma_m"]], dtype=torch.float64)
         elif self.dist_inv is not None:
-            # the trial factorisation distributed too: L^{-1} gathered, each rank's partial traces
+            # the trial factorisation distributed too: L^{-1} gathered, the shards' traces combined by
+            # the library's collective objective
             Linv, ld_t, pd_t, fc_t = self.dist_inv.invert(Lam, want_sigma=False, want_linv=True)
             if pd_t:
-                ob = self.b.objective_given_inverse_partial(X_r, Y_r, Lam, Theta, lam_L, lam_T, penalize_diag, n,
-                                                            Linv, ld_t)
+                ob = self.b.objective_sharded(X_r, Y_r, Lam, Theta, lam_L, lam_T, penalize_diag, n, self.group,
+                                              Linv=Linv, logdet=ld_t)
             else:
-                ob = dict(is_pd=False, fail_col=fc_t, logdet=float("nan"), tr_syy_lam=0.0, tr_sxy_theta=0.0,
-                          tr_sigma_m=0.0, pen_L=0.0, pen_T=0.0)
-            parts = torch.tensor([ob["tr_syy_lam"], ob["tr_sxy_theta"], ob["tr_sigma_m"]], dtype=torch.float64,
-                                 device=Psi.device)
-            if self.world > 1:
-                if dist.get_backend(self.group) == "gloo":
-                    h = parts.cpu()
-                    dist.all_reduce(h, group=self.group)
-                    parts = h
-                else:
-                    dist.all_reduce(parts, group=self.group)
+                ob = dict(f=float("inf"), g=float("inf"), is_pd=False, fail_col=fc_t, logdet=float("nan"),
+                          tr_syy_lam=float("nan"), tr_sxy_theta=float("nan"), tr_sigma_m=float("nan"))
+        elif self.world > 1:
+            ob = self.b.objective_sharded(X_r, Y_r, Lam, Theta, lam_L, lam_T, penalize_diag, n, self.group)
         else:
             ob = self.b.objective_partial(X_r, Y_r, Lam, Theta, lam_L, lam_T, penalize_diag, n)
-            parts = torch.tensor([ob["tr_syy_lam"], ob["tr_sxy_theta"], ob["tr_sigma_m"]], dtype=torch.float64,
-                                 device=Psi.device)
-            if self.world > 1:
-                dist.all_reduce(parts, group=self.group)
         self._mark("objective")
-        tr_syy, tr_sxy, tr_sm = (float(v) for v in parts.tolist())
-        if ob["is_pd"]:
-            g = -ob["logdet"] + tr_syy + 2.0 * tr_sxy + tr_sm
-            f = g + ob["pen_L"] + ob["pen_T"]
-        else:
-            g = f = float("inf")
         return dict(Sigma=Sigma, logdet=logdet, is_pd=pd, fail_col=fc, Psi=Psi, GradL=GradL, GradT=GradT,
-                    active=act, f=f, g=g, obj_logdet=ob["logdet"], tr_syy_lam=tr_syy, tr_sxy_theta=tr_sxy,
-                    tr_sigma_m=tr_sm)
+                    active=act, f=ob["f"], g=ob["g"], obj_logdet=ob["logdet"], tr_syy_lam=ob["tr_syy_lam"],
+                    tr_sxy_theta=ob["tr_sxy_theta"], tr_sigma_m=ob["tr_sigma_m"])
 
 
 class CollectiveEvaluator:
@@ -301,6 +467,102 @@ class CollectiveEvaluator:
         self.n_total = n_total
         self.Syy, _ = self.ctx.cggm_covariances(X_r, Y_r, n_total=n_total, want_sxy=False)
         return self.Syy
+
+    def _reduce_scatter(self, flat_in, flat_out):
+        """flat_out = block `rank` of the element-wise sum over ranks of flat_in (world equal blocks)."""
+        if self.world == 1:
+            flat_out.copy_(flat_in[:flat_out.numel()])
+            return
+        if dist.get_backend(self.group) == "nccl":
+            dist.reduce_scatter_tensor(flat_out, flat_in, group=self.group)
+        else:   # gloo has no reduce-scatter: all-reduce, keep this rank's block (same sums)
+            h = flat_in.cpu()
+            dist.all_reduce(h, group=self.group)
+            k = flat_out.numel()
+            flat_out.copy_(h[self.rank * k:(self.rank + 1) * k].to(flat_out.device))
+
+    def _all_gather_lists(self, rows, cols, m):
+        """Concatenation in rank order of every rank's first m entries (rank r owns an ascending column
+        range, so the result is the global column-major list, identical on every rank)."""
+        if self.world == 1:
+            return rows[:m].clone(), cols[:m].clone()
+        host = dist.get_backend(self.group) == "gloo"
+        dev = rows.device
+        cnt = torch.tensor([m], dtype=torch.int64, device="cpu" if host else dev)
+        cnts = [torch.zeros_like(cnt) for _ in range(self.world)]
+        dist.all_gather(cnts, cnt, group=self.group)
+        cnts = [int(c.item()) for c in cnts]
+        mx = max(max(cnts), 1)
+        out = []
+        for src in (rows, cols):
+            loc = torch.zeros(mx, dtype=src.dtype, device="cpu" if host else dev)
+            loc[:m].copy_(src[:m])
+            parts = [torch.empty_like(loc) for _ in range(self.world)]
+            dist.all_gather(parts, loc, group=self.group)
+            out.append(torch.cat([pt[:c] for pt, c in zip(parts, cnts)]).to(dev))
+        return out[0], out[1]
+
+    def _grad_theta_reduce_scatter(self, X_r, E, Theta, lam_T, tie_eps, actL):
+        """S_Theta without a stored p x q gradient: ranks own balanced column ranges; round t forms,
+        for every owner r, the partial (2/n) X^T E[:, a_r + t w : a_r + (t + 1) w] into block r of a
+        p x (world w) buffer, reduce-scatters it (block r, summed, to rank r) and the owner compacts
+        its block (global column indices).  The compact lists are all-gathered at the end."""
+        n = self.n_total
+        p, q = X_r.shape[1], Theta.ncols
+        G, me = self.world, self.rank
+        ranges = [shard_rows(q, G, r) for r in range(G)]
+        span = max(b - a for a, b in ranges)
+        w = max(1, min(self.rs_width, span))
+        ld = p + (p & 1)
+        key = (p, q, G, w)
+        if self._rs.get("key") != key:
+            self._rs = {"key": key, "buf": self.b.flat_zeros(G * ld * w, E), "out": self.b.flat_zeros(ld * w, E)}
+            self._rs["T_row"], self._rs["T_col"] = self.b.int_lists(max(4096, 2 * Theta.nnz // G + p), E)
+        buf, outf = self._rs["buf"], self._rs["out"]
+
+        def block(flat, r):   # p x w column-major view of block r (leading dimension ld)
+            return torch.as_strided(flat, (p, w), (1, ld), r * ld * w)
+
+        a_me, b_me = ranges[me]
+        m_tot, ties, sub = 0, 0, 0.0
+        for t in range((span + w - 1) // w):
+            for r, (a, b) in enumerate(ranges):
+                c0, c1 = a + t * w, min(b, a + (t + 1) * w)
+                if c1 > c0:
+                    self.b.grad_theta_block(X_r, E, c0, c1, n, block(buf, r)[:, :c1 - c0])
+            self._reduce_scatter(buf, outf)
+            c0, c1 = a_me + t * w, min(b_me, a_me + (t + 1) * w)
+            if c1 <= c0:
+                continue
+            G_blk = block(outf, 0)[:, :c1 - c0]
+            while True:
+                T_row, T_col = self._rs["T_row"], self._rs["T_col"]
+                try:
+                    mb, tb, sb = self.b.active_theta_block(G_blk, Theta, c0, lam_T, tie_eps, T_row[m_tot:],
+                                                           T_col[m_tot:])
+                    break
+                except Exception as exc:   # CGGM_ERR_CAPACITY: grow the lists, keep what is written
+                    need = getattr(exc, "m", None)
+                    if need is None:
+                        raise
+                    nr, nc = self.b.int_lists(2 * (m_tot + need) + 4096, E)
+                    nr[:m_tot].copy_(T_row[:m_tot])
+                    nc[:m_tot].copy_(T_col[:m_tot])
+                    self._rs["T_row"], self._rs["T_col"] = nr, nc
+            m_tot += mb
+            ties += tb
+            sub += sb
+        T_row, T_col = self._all_gather_lists(self._rs["T_row"], self._rs["T_col"], m_tot)
+        tot = torch.tensor([float(ties), sub], dtype=torch.float64)
+        if G > 1:
+            host = dist.get_backend(self.group) == "gloo"
+            tot = tot if host else tot.to(E.device)
+            dist.all_reduce(tot, group=self.group)
+        ties_T, sub_T = float(tot[0]), float(tot[1])
+        act = dict(actL)
+        act.update(T_row=T_row, T_col=T_col, m_T=int(T_row.numel()), ties_T=int(round(ties_T)),
+                   subgrad_l1=float(actL["subgrad_l1"]) + sub_T)
+        return act
 
     def evaluate(self, X_r, Y_r, Lam, Theta, lam_L, lam_T, penalize_diag=True, tie_eps=1e-9):
         n = self.n_total

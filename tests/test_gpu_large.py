@@ -18,7 +18,7 @@ TIE = 1e-9
 
 
 @pytest.fixture(scope="module")
-def run_large():
+def run_large():  # noqa: C901
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_1509_04681_b200 import Context, DeviceCsc, colmajor_empty, newton_evaluation, to_device_colmajor
@@ -35,7 +35,10 @@ def run_large():
             "T_col": torch.empty(6_000_000, dtype=torch.int32, device="cuda")}
     res = newton_evaluation(ctx, X, Y, Syy, Lam, Th, P.lam_L, P.lam_T, True, bufs, tie_eps=TIE)
     torch.cuda.synchronize()
-    return P, res, Syy
+    yield P, res, Syy
+    del res, Syy, bufs, X, Y
+    ctx.lib.cggm_ctx_release_workspace(ctx.h)
+    torch.cuda.empty_cache()
 
 
 def chain_sigma_cols(q, cols, phi=0.5):
@@ -112,3 +115,81 @@ def test_large_objective(run_large):
     assert ob["is_pd"]
     assert ob["tr_sigma_m"] == pytest.approx(tr_sm, rel=1e-10)
     assert ob["f"] == pytest.approx(f, rel=1e-10)
+
+
+# ------------------------------------------------------------------ full-matrix parity (all columns)
+BLK = 2000
+
+
+def _list_block(a, rk, ck, c0, c1):
+    """Entries of the (row, col) list with c0 <= col < c1 (the list is column-major sorted)."""
+    cols = a[ck]
+    lo = int(torch.searchsorted(cols, torch.tensor(c0, dtype=cols.dtype, device=cols.device)))
+    hi = int(torch.searchsorted(cols, torch.tensor(c1, dtype=cols.dtype, device=cols.device)))
+    return a[rk][lo:hi].cpu().numpy().astype(np.int64), cols[lo:hi].cpu().numpy().astype(np.int64) - c0
+
+
+def _check_list_block(rows, cols, G, lam, supp, upper_c0=None):
+    """The GPU list's entries in this column block equal the definition evaluated on the
+    host reference gradient block G, except entries within the tie band of the threshold."""
+    want = np.abs(G) > lam
+    want |= supp
+    if upper_c0 is not None:   # S_Lambda: i <= j
+        i = np.arange(G.shape[0])[:, None]
+        j = upper_c0 + np.arange(G.shape[1])[None, :]
+        want &= i <= j
+    got = np.zeros_like(want)
+    got[rows, cols] = True
+    assert got.sum() == rows.size, "duplicate list entries"
+    diff = np.nonzero(got ^ want)
+    band = np.abs(np.abs(G[diff]) - lam) <= TIE + 1e-12 * np.maximum(1.0, np.abs(G[diff]))
+    assert np.all(band), f"{int((~band).sum())} list entries differ outside the tie band"
+    return int(diff[0].size)
+
+
+def _support_block(csc, nrows, c0, c1):
+    S = np.zeros((nrows, c1 - c0), dtype=bool)
+    for j in range(c0, c1):
+        a, b = csc.colptr[j], csc.colptr[j + 1]
+        r = csc.rowidx[a:b]
+        S[r[csc.val[a:b] != 0], j - c0] = True
+    return S
+
+
+def test_large_full_matrices_and_lists(run_large):
+    """Every entry at full `large` size: Sigma against the P4 closed form, Psi* = D^T D / n,
+    grad_Theta* = (2/n) X^T E_noise and grad_Lambda* = S_yy - Sigma* - Psi* (identity I7, P:264-269,
+    P:283-284) as full-matrix rel-F <= 1e-9 (Sigma 1e-12), both triangles bit-identical, and the
+    complete S_Lambda / S_Theta lists against the definition on those host matrices."""
+    P, res, _ = run_large
+    q, p, n = P.q, P.p, P.n
+    D = P.Y - P.E_noise
+    err = {k: 0.0 for k in ("Sigma", "Psi", "GradL", "GradT")}
+    nrm = dict(err)
+    flips = 0
+    a = res["active"]
+    assert np.all(np.diff(a["L_col"].cpu().numpy().astype(np.int64) * (1 << 31) + a["L_row"].cpu().numpy()) > 0)
+    assert np.all(np.diff(a["T_col"].cpu().numpy().astype(np.int64) * (1 << 31) + a["T_row"].cpu().numpy()) > 0)
+    for c0 in range(0, q, BLK):
+        c1 = min(q, c0 + BLK)
+        cols = list(range(c0, c1))
+        S_ref = chain_sigma_cols(q, cols)
+        psi_ref = D.T @ D[:, c0:c1] / n
+        syy = P.Y.T @ P.Y[:, c0:c1] / n
+        gl_ref = syy - S_ref - psi_ref
+        gt_ref = (2.0 / n) * (P.X.T @ P.E_noise[:, c0:c1])
+        for key, ref in (("Sigma", S_ref), ("Psi", psi_ref), ("GradL", gl_ref), ("GradT", gt_ref)):
+            g = res[key][:, c0:c1].cpu().numpy()
+            err[key] += float(np.sum((g - ref) ** 2))
+            nrm[key] += float(np.sum(ref ** 2))
+            if key != "GradT":   # both triangles bit-identical (reading A19): rows c0:c1 == columns c0:c1
+                np.testing.assert_array_equal(g, res[key][c0:c1, :].cpu().numpy().T)
+        r_, c_ = _list_block(a, "L_row", "L_col", c0, c1)
+        flips += _check_list_block(r_, c_, gl_ref, P.lam_L, _support_block(P.lam_star, q, c0, c1), upper_c0=c0)
+        r_, c_ = _list_block(a, "T_row", "T_col", c0, c1)
+        flips += _check_list_block(r_, c_, gt_ref, P.lam_T, _support_block(P.theta_star, p, c0, c1))
+    rel = {k: (err[k] / nrm[k]) ** 0.5 for k in err}
+    print("large full rel-F:", rel, "tie-band differences:", flips)
+    assert rel["Sigma"] <= 1e-12
+    for k in ("Psi", "GradL", "GradT"):
+        assert rel[k] <= REL_F, (k, rel[k])

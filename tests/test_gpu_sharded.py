@@ -10,7 +10,12 @@ pinned by what holds at any size:
       outside the tie band);
   I2  tr(Sigma Theta^T S_xx Theta) from the objective's augmented factorisation = <Lambda, Psi>;
   the inverse's and the objective's factorisations give the same log-det.
-Generation of the inputs takes ~1-2 minutes of host time.  Set CGGM_TEST_SHARDED=0 to skip."""
+Every entry is checked too (test_sharded_full_*): Lambda Sigma = I over all columns, Psi* and
+grad_Lambda* as full-matrix rel-F, the complete S_Lambda / S_Theta lists against the definition on
+host gradients (grad_Theta* = (2/n) X^T E_noise by host BLAS, column block by column block), and the
+log-determinant and objective against an independent LAPACK Cholesky of Lambda* on the host.
+Generation of the inputs takes ~1-2 minutes of host time, the host references ~3 minutes.
+Set CGGM_TEST_SHARDED=0 to skip."""
 import math
 import os
 
@@ -59,10 +64,12 @@ def run_sharded():
     cols = torch.as_tensor(np.repeat(np.arange(P.q), np.diff(P.lam_star.colptr)), device="cuda")
     out["Psi_at_lambda"] = res["Psi"][rows, cols].cpu().numpy()
     out["lists"] = {k: res["active"][k].cpu().numpy() for k in ("L_row", "L_col", "T_row", "T_col")}
-    del res, X, Y, Syy, bufs
+    out["dev"] = res                 # the full device matrices / lists, for the all-entries tests
+    del X, Y, Syy
     ctx.lib.cggm_ctx_release_workspace(ctx.h)
+    yield P, out
+    del out["dev"], res, bufs
     torch.cuda.empty_cache()
-    return P, out
 
 
 def test_sharded_sigma_lambda_identity(run_sharded):
@@ -113,3 +120,108 @@ def test_sharded_objective_trace_identity(run_sharded):
     tr_syy = float(np.sum(P.Y * (P.Y @ lamd))) / P.n
     assert ob["tr_syy_lam"] == pytest.approx(tr_syy, rel=1e-11)
     assert math.isfinite(ob["f"])
+
+
+# ------------------------------------------------------------------ every entry
+BLK = 2000
+
+
+def _list_block(rows, cols, c0, c1):
+    lo, hi = np.searchsorted(cols, c0), np.searchsorted(cols, c1)
+    return rows[lo:hi].astype(np.int64), cols[lo:hi].astype(np.int64) - c0
+
+
+def _support_block(csc, nrows, c0, c1):
+    S = np.zeros((nrows, c1 - c0), dtype=bool)
+    for j in range(c0, c1):
+        a, b = csc.colptr[j], csc.colptr[j + 1]
+        r = csc.rowidx[a:b]
+        S[r[csc.val[a:b] != 0], j - c0] = True
+    return S
+
+
+def _check_list_block(rows, cols, G, lam, supp, upper_c0=None):
+    want = (np.abs(G) > lam) | supp
+    if upper_c0 is not None:
+        want &= np.arange(G.shape[0])[:, None] <= upper_c0 + np.arange(G.shape[1])[None, :]
+    got = np.zeros_like(want)
+    got[rows, cols] = True
+    assert got.sum() == rows.size, "duplicate list entries"
+    diff = np.nonzero(got ^ want)
+    band = np.abs(np.abs(G[diff]) - lam) <= TIE + 1e-12 * np.maximum(1.0, np.abs(G[diff]))
+    assert np.all(band), f"{int((~band).sum())} entries differ outside the tie band"
+    return int(diff[0].size)
+
+
+def test_sharded_full_matrices_and_lists(run_sharded):
+    """All columns: Lambda Sigma = I (P7, the random-SPD Sigma has no closed form), Psi* = D^T D / n and
+    grad_Lambda* = S_yy - Sigma - Psi* (I7) as full rel-F <= 1e-9, both triangles bit-identical, and the
+    complete S_Lambda (upper, against grad_Lambda*) and S_Theta (against grad_Theta* = (2/n) X^T E_noise)
+    lists against the definition P:296-303."""
+    import scipy.sparse as sp
+    P, r = run_sharded
+    res = r["dev"]
+    q, p, n = P.q, P.p, P.n
+    D = P.Y - P.E_noise
+    lam_sp = P.lam_star.to_scipy()
+    lists = r["lists"]
+    for rk, ck in (("L_row", "L_col"), ("T_row", "T_col")):
+        assert np.all(np.diff(lists[ck].astype(np.int64) * (1 << 31) + lists[rk]) > 0)
+    err = {"Psi": 0.0, "GradL": 0.0}
+    nrm = dict(err)
+    resid = 0.0
+    flips = 0
+    for c0 in range(0, q, BLK):
+        c1 = min(q, c0 + BLK)
+        S = res["Sigma"][:, c0:c1].cpu().numpy()
+        np.testing.assert_array_equal(S, res["Sigma"][c0:c1, :].cpu().numpy().T)
+        E = np.asarray(lam_sp @ S)                      # (Lambda Sigma)[:, block] = I[:, block]
+        E[np.arange(c0, c1), np.arange(c1 - c0)] -= 1.0
+        resid += float(np.sum(E * E))
+        psi_ref = D.T @ D[:, c0:c1] / n
+        gl_ref = P.Y.T @ P.Y[:, c0:c1] / n - S - psi_ref
+        for key, ref in (("Psi", psi_ref), ("GradL", gl_ref)):
+            g = res[key][:, c0:c1].cpu().numpy()
+            np.testing.assert_array_equal(g, res[key][c0:c1, :].cpu().numpy().T)
+            err[key] += float(np.sum((g - ref) ** 2))
+            nrm[key] += float(np.sum(ref ** 2))
+        rr, cc = _list_block(lists["L_row"], lists["L_col"], c0, c1)
+        flips += _check_list_block(rr, cc, gl_ref, P.lam_L, _support_block(P.lam_star, q, c0, c1), upper_c0=c0)
+        gt_ref = (2.0 / n) * (P.X.T @ P.E_noise[:, c0:c1])
+        rr, cc = _list_block(lists["T_row"], lists["T_col"], c0, c1)
+        flips += _check_list_block(rr, cc, gt_ref, P.lam_T, _support_block(P.theta_star, p, c0, c1))
+        del gt_ref
+    rel = {k: (err[k] / nrm[k]) ** 0.5 for k in err}
+    print("sharded full: ||Lambda Sigma - I||_F / sqrt(q) =", (resid / q) ** 0.5, "rel-F:", rel, "tie flips:", flips)
+    assert (resid / q) ** 0.5 <= 1e-12
+    for k, v in rel.items():
+        assert v <= 1e-9, (k, v)
+    assert sp.issparse(lam_sp)
+
+
+def test_sharded_logdet_and_objective_vs_lapack(run_sharded):
+    """Independent reference for the `sharded` log-determinant and objective: a dense LAPACK Cholesky
+    of Lambda* on the host (potrf, not this library's factorisation), log|Lambda| = 2 sum ln L_jj, and
+    tr(Sigma Theta^T S_xx Theta) = ||L^{-1} W^T||_F^2 / n by a LAPACK triangular solve with W = X Theta
+    (reading A14); f of Eq. 1 assembled from them."""
+    import scipy.linalg
+    P, r = run_sharded
+    n = P.n
+    A = P.lam_star.to_dense()
+    L = scipy.linalg.cholesky(A, lower=True, overwrite_a=True, check_finite=False)
+    del A
+    logdet = 2.0 * float(np.sum(np.log(np.diag(L))))
+    W = np.asarray(P.X @ P.theta_star.to_scipy())
+    Z = scipy.linalg.solve_triangular(L, W.T, lower=True, check_finite=False)
+    tr_sm = float(np.sum(Z * Z)) / n
+    del Z, L
+    lamd = P.lam_star.to_scipy()
+    tr_syy = float(np.sum(P.Y * (P.Y @ lamd))) / n
+    tr_sxy = float(np.sum(W * P.Y)) / n
+    f = -logdet + tr_syy + 2 * tr_sxy + tr_sm + P.lam_L * np.abs(P.lam_star.val).sum() \
+        + P.lam_T * np.abs(P.theta_star.val).sum()
+    ob = r["objective"]
+    assert r["logdet"] == pytest.approx(logdet, rel=1e-12)
+    assert ob["logdet"] == pytest.approx(logdet, rel=1e-12)
+    assert ob["tr_sigma_m"] == pytest.approx(tr_sm, rel=1e-10)
+    assert ob["f"] == pytest.approx(f, rel=1e-10)
