@@ -345,6 +345,9 @@ def main():
     ap.add_argument("--inverse", default="auto", choices=["auto", "rank0", "distributed"],
                     help="N > 1: Sigma on rank 0 + broadcast, or the block-cyclic distributed inverse "
                          "(NEXT-3); auto = distributed from 3 GPUs")
+    ap.add_argument("--grad-theta", default="reduce_scatter", choices=["reduce_scatter", "allreduce"],
+                    help="N > 1: grad_Theta by reduce-scattered column ranges with compact-list all-gather "
+                         "(no p x q buffer), or the full p x q all-reduce")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fp32", action="store_true", help="skip the FP32-variant timings (medium, large)")
     ap.add_argument("--no-variants", action="store_true", help="skip the eager / changing-Lambda step timings")
@@ -411,10 +414,14 @@ def main():
     tf, ms = ctypes.c_double(), ctypes.c_double()
     ctx._check(ctx.lib.cggm_test_fp64_peak(ctx.h, args.peak_seconds, ctypes.byref(tf), ctypes.byref(ms)))
     peak_tflops = tf.value
+    # L2 -> SM read bandwidth, measured live (the SpMM gathers from L2: its roofline denominator)
+    l2g, l2ms = ctypes.c_double(), ctypes.c_double()
+    ctx._check(ctx.lib.cggm_test_l2_peak(ctx.h, 1.0, ctypes.byref(l2g), ctypes.byref(l2ms)))
+    l2_peak_gbs = l2g.value
 
     dist_inv = args.inverse == "distributed" or (args.inverse == "auto" and world >= 3)
     ev = ShardedEvaluator(CudaBackend(ctx), distributed_inverse=dist_inv, split_objective=not dist_inv,
-                          peer_allreduce=args.allreduce == "peer")
+                          peer_allreduce=args.allreduce == "peer", grad_theta=args.grad_theta)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -621,14 +628,16 @@ def main():
     # collectives per evaluation at N > 1 (bytes each rank contributes; achieved = bytes / phase time)
     comm = None
     if world > 1:
-        by = {"bcast_sigma": 8.0 * q_ * q_, "allreduce_psi": 8.0 * q_ * q_, "allreduce_grad_theta": 8.0 * p_ * q_}
-        comm = {"backend": backend, "allreduce": args.allreduce, "per_rank": []}
+        by = {"bcast_sigma": 8.0 * q_ * q_, "allreduce_psi": 8.0 * q_ * q_, "allreduce_grad_theta": 8.0 * p_ * q_,
+              "reduce_scatter_grad_theta": 8.0 * p_ * q_}
+        comm = {"backend": backend, "allreduce": args.allreduce, "grad_theta": args.grad_theta, "per_rank": []}
         for r_, ph in enumerate(rank_phases):
             d = {"rank": r_, "phase_ms": ph}
             for k_, b_ in by.items():
                 if k_ in ph and ph[k_] > 0:
                     alg = b_ / (ph[k_] * 1e-3) / 1e9
-                    bus = alg * (2.0 * (world - 1) / world if k_.startswith("allreduce") else 1.0)
+                    bus = alg * (2.0 * (world - 1) / world if k_.startswith("allreduce") else
+                                 (world - 1) / world if k_.startswith("reduce_scatter") else 1.0)
                     d[k_ + "_GBps"] = {"bytes": b_, "algbw": alg, "busbw": bus}
             comm["per_rank"].append(d)
 
@@ -651,6 +660,15 @@ def main():
                 gbs = by_ / (ms_s * 1e-3) / 1e9
                 hbm[tag] = {"alg_bytes_per_step": by_, "ms_per_step": ms_s, "achieved_gbs": gbs,
                             "frac_of_measured_copy": gbs / HBM_PEAK_GBS}
+        if "spmm" in hbm:
+            # W = X Theta gathers n values of X per stored Theta entry (X is read from DRAM once and
+            # then re-read from L2): bound by L2 -> SM bandwidth, measured live beside it
+            l2_by = 8.0 * n_ * P.theta_star.nnz * spmm_calls
+            l2_gbs = l2_by / (hbm["spmm"]["ms_per_step"] * 1e-3) / 1e9
+            hbm["spmm"].update({"bound": "l2", "l2_gathered_bytes_per_step": l2_by, "l2_achieved_gbs": l2_gbs,
+                                "l2_peak_gbs": l2_peak_gbs, "l2_frac": l2_gbs / l2_peak_gbs,
+                                "l2_peak_source": "live cggm_test_l2_peak (16-byte loads over a 48 MB L2-resident "
+                                                  "buffer, every SM)"})
 
     # ---------------------------------------------------------------- e2e through the public API
     e2e = None
@@ -756,7 +774,8 @@ def main():
             "config": {"workload": args.config, "n": P.n, "p": P.p, "q": P.q, "nnz_theta": P.theta_star.nnz,
                        "nnz_lambda": P.lam_star.nnz, "lambda": P.lam_L, "point": "generating (Lambda*, Theta*)",
                        "parallelism": (f"sample-shard dp{world}, " + ("distributed inverse and trial factorisation" if dist_inv else
-                                       "rank-0 inverse + split objective") + f", {args.allreduce} all-reduce") if world > 1 else "1 GPU",
+                                       "rank-0 inverse + split objective") + f", {args.allreduce} all-reduce, grad_Theta "
+                                       f"{args.grad_theta}") if world > 1 else "1 GPU",
                        "l2": l2_note(P),
                        "setup_syy_ms": setup_ms, "generator_s": round(t_gen, 2),
                        "grad_theta": "streamed into the active sets (not stored)" if args.stream_grad_theta

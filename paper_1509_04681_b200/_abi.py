@@ -125,6 +125,7 @@ SIGNATURES = {
     "cggm_test_set_tile": (c_i32, [c_vp, c_i32]),
     "cggm_test_set_f32_engine": (c_i32, [c_vp, c_i32]),
     "cggm_test_fp64_peak": (c_i32, [c_vp, c_d, ctypes.POINTER(c_d), ctypes.POINTER(c_d)]),
+    "cggm_test_l2_peak": (c_i32, [c_vp, c_d, ctypes.POINTER(c_d), ctypes.POINTER(c_d)]),
     "cggm_test_profile_dump": (c_i32, [c_vp, ctypes.c_char_p]),
     "cggm_test_chol_dense": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_i32, ctypes.POINTER(c_d),
                                      ctypes.POINTER(c_i64)]),

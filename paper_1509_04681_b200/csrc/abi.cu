@@ -181,6 +181,7 @@ cggm_status cggm_ctx_create(cggm_ctx** out, int device, cggm_dtype dtype, void* 
   if (const char* e = std::getenv("CGGM_CD_PREFETCH")) c->cd_prefetch = std::atoi(e);
   if (const char* e = std::getenv("CGGM_GRAPH_PROF")) c->graph_prof = std::atoi(e);
   if (const char* e = std::getenv("CGGM_TF32_CHUNK")) c->tf32_chunk = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_NO_FUSE_GRADL")) c->no_fuse_gradl = std::atoi(e);
   if (const char* e = std::getenv("CGGM_TF32_DEBUG")) c->tf32_dbg = std::atoi(e);
   if (const char* e = std::getenv("CGGM_F32_ENGINE")) c->f32_engine = std::string(e) == "ffma" ? 1 : 0;
   cudaDriverEntryPointQueryResult q;
@@ -1003,12 +1004,20 @@ static void psi_enqueue(Ctx* c, int64_t n_local, int64_t n_total, int64_t p, int
       gemm(c, false, false, n_local, q, q, W, ldw, Sg, ldsigma, e, 0);
     }
   }
-  {  // a4/a5: Psi = R^T R (mirrored), then grad_Lambda = (S_yy - Sigma) - Psi as one streaming pass
+  {  // a4/a5: Psi = R^T R (mirrored); grad_Lambda = S_yy - Sigma - Psi as the same GEMM's second
+     // epilogue output (-Psi + S_yy - Sigma per element, both triangles from one value;
+     // no separate 32 B/element streaming pass), unless Psi must first be all-reduced over the shards
     Phase ph(c, TAG_PSI);
     EpilogueT<T> e; e.out1 = Psi; e.ld1 = ldpsi; e.a1 = 1.0;
+    const bool fuse_gl = GradL && !collective && !c->no_fuse_gradl;
+    if (fuse_gl) {
+      e.out2 = GradL; e.ld2 = ldgl; e.a2 = -1.0;
+      e.in2a = Syy; e.ld2a = ldsyy; e.b2 = 1.0;
+      e.in2b = Sg; e.ld2b = ldsigma; e.c2 = -1.0;
+    }
     gemm(c, true, false, q, q, n_local, R, ldn, R, ldn, e, SYM_LOWER | SYM_MIRROR);
     if (collective) comm_allreduce(c, Psi, flat_count(q, q, ldpsi), dt);   // Psi = sum_r R_r^T R_r
-    if (GradL) {
+    if (GradL && !fuse_gl) {
       Phase pg(c, TAG_GRADL);
       grad_lambda(c, q, Syy, ldsyy, Sg, ldsigma, Psi, ldpsi, GradL, ldgl);
     }

@@ -413,6 +413,11 @@ __global__ void __launch_bounds__(C::LB_THREADS, C::LB_MINB)
             o.x = __dadd_rn(o.x, __dmul_rn(E.b2, x2[u].x));
             o.y = __dadd_rn(o.y, __dmul_rn(E.b2, x2[u].y));
           }
+          if (E.in2b) {   // (only the Psi GEMM's grad_Lambda output has a second input: loaded here)
+            const double2 x4 = *reinterpret_cast<const double2*>(E.in2b + m + n * E.ld2b);
+            o.x = __dadd_rn(o.x, __dmul_rn(E.c2, x4.x));
+            o.y = __dadd_rn(o.y, __dmul_rn(E.c2, x4.y));
+          }
           *reinterpret_cast<double2*>(E.out2 + m + n * E.ld2) = o;
         }
       }
@@ -427,7 +432,7 @@ __global__ void __launch_bounds__(C::LB_THREADS, C::LB_MINB)
     }
   }
   if (P.flags & SYM_MIRROR) {
-    if (P.vec && !diag && m0 + BM <= P.M && n0 + BN <= P.N && !P.epi.in1a && !P.epi.in2a) {
+    if (P.vec && !diag && m0 + BM <= P.M && n0 + BN <= P.N && !P.epi.in1a) {
       // transposed copy: lane l of a warp reads row nl = nb + l of the staged tile at columns ml and
       // ml + 1 (consecutive lanes 129 doubles apart: conflict-free), then lane pairs swap one value
       // so that the even lane stores (nl, nl + 1) of output column ml and the odd lane those of
@@ -448,8 +453,20 @@ __global__ void __launch_bounds__(C::LB_THREADS, C::LB_MINB)
         const int64_t m = m0 + ml + (odd ? 1 : 0);
         if (E.out1)
           *reinterpret_cast<double2*>(E.out1 + n + m * E.ld1) = make_double2(__dmul_rn(E.a1, lo), __dmul_rn(E.a1, hi));
-        if (E.out2)
-          *reinterpret_cast<double2*>(E.out2 + n + m * E.ld2) = make_double2(__dmul_rn(E.a2, lo), __dmul_rn(E.a2, hi));
+        if (E.out2) {
+          double2 o = make_double2(__dmul_rn(E.a2, lo), __dmul_rn(E.a2, hi));
+          if (E.in2a) {   // the inputs at the written (transposed) position: contiguous along n
+            const double2 x = *reinterpret_cast<const double2*>(E.in2a + n + m * E.ld2a);
+            o.x = __dadd_rn(o.x, __dmul_rn(E.b2, x.x));
+            o.y = __dadd_rn(o.y, __dmul_rn(E.b2, x.y));
+          }
+          if (E.in2b) {
+            const double2 x = *reinterpret_cast<const double2*>(E.in2b + n + m * E.ld2b);
+            o.x = __dadd_rn(o.x, __dmul_rn(E.c2, x.x));
+            o.y = __dadd_rn(o.y, __dmul_rn(E.c2, x.y));
+          }
+          *reinterpret_cast<double2*>(E.out2 + n + m * E.ld2) = o;
+        }
       }
     } else {
       for (int idx = tid; idx < BM * BN; idx += NTHREADS) {
@@ -951,6 +968,11 @@ __global__ void __launch_bounds__(C::NTHREADS + 128, 1)
                 o.x = __dadd_rn(o.x, __dmul_rn(E.b2, x2[u].x));
                 o.y = __dadd_rn(o.y, __dmul_rn(E.b2, x2[u].y));
               }
+              if (E.in2b) {   // (only the Psi GEMM's grad_Lambda output has a second input: loaded here)
+                const double2 x4 = *reinterpret_cast<const double2*>(E.in2b + m + n * E.ld2b);
+                o.x = __dadd_rn(o.x, __dmul_rn(E.c2, x4.x));
+                o.y = __dadd_rn(o.y, __dmul_rn(E.c2, x4.y));
+              }
               *reinterpret_cast<double2*>(E.out2 + m + n * E.ld2) = o;
             }
           }
@@ -965,7 +987,7 @@ __global__ void __launch_bounds__(C::NTHREADS + 128, 1)
         }
       }
       if (P.flags & SYM_MIRROR) {
-        if (interior && !E.in1a && !E.in2a) {
+        if (interior && !E.in1a) {
           constexpr int NWARPS = NTHREADS / 32, NBLK = SW / 32, GROUPS = NWARPS / NBLK, PAIRS = BM / 2 / GROUPS;
           const int nl = 32 * (warp % NBLK) + lane, grp = warp / NBLK;
           const bool odd = lane & 1;
@@ -979,8 +1001,20 @@ __global__ void __launch_bounds__(C::NTHREADS + 128, 1)
             const int64_t m = m0 + ml + (odd ? 1 : 0);
             if (E.out1)
               *reinterpret_cast<double2*>(E.out1 + n + m * E.ld1) = make_double2(__dmul_rn(E.a1, lo), __dmul_rn(E.a1, hi));
-            if (E.out2)
-              *reinterpret_cast<double2*>(E.out2 + n + m * E.ld2) = make_double2(__dmul_rn(E.a2, lo), __dmul_rn(E.a2, hi));
+            if (E.out2) {
+              double2 o = make_double2(__dmul_rn(E.a2, lo), __dmul_rn(E.a2, hi));
+              if (E.in2a) {   // the inputs at the written (transposed) position: contiguous along n
+                const double2 x = *reinterpret_cast<const double2*>(E.in2a + n + m * E.ld2a);
+                o.x = __dadd_rn(o.x, __dmul_rn(E.b2, x.x));
+                o.y = __dadd_rn(o.y, __dmul_rn(E.b2, x.y));
+              }
+              if (E.in2b) {
+                const double2 x = *reinterpret_cast<const double2*>(E.in2b + n + m * E.ld2b);
+                o.x = __dadd_rn(o.x, __dmul_rn(E.c2, x.x));
+                o.y = __dadd_rn(o.y, __dmul_rn(E.c2, x.y));
+              }
+              *reinterpret_cast<double2*>(E.out2 + n + m * E.ld2) = o;
+            }
           }
         } else {
           for (int idx = tid; idx < BM * SW; idx += NTHREADS) {
@@ -1146,8 +1180,8 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
     throw CudaError{CGGM_ERR_UNSUPPORTED, "SPLIT_K2: plain out1 only"};
   {
     auto al = [](const double* q, int64_t ld) { return !q || (reinterpret_cast<uintptr_t>(q) % 16 == 0 && ld % 2 == 0); };
-    P.vec = !c->no_vec_epi && !epi.in1b && !epi.in2b && al(epi.out1, epi.ld1) && al(epi.out2, epi.ld2) &&
-            al(epi.in1a, epi.ld1a) && al(epi.in2a, epi.ld2a);
+    P.vec = !c->no_vec_epi && !epi.in1b && al(epi.out1, epi.ld1) && al(epi.out2, epi.ld2) &&
+            al(epi.in1a, epi.ld1a) && al(epi.in2a, epi.ld2a) && al(epi.in2b, epi.ld2b);
   }
   if ((flags & SYM_LOWER) && (M < N || ((flags & SYM_MIRROR) && M != N)))
     throw CudaError{CGGM_ERR_SHAPE, "SYM_LOWER gemm needs M >= N (M == N with SYM_MIRROR)"};

@@ -60,3 +60,64 @@ extern "C" cggm_status cggm_test_fp64_peak(cggm_ctx* ctx_, double seconds, doubl
   cudaFree(out);
   return cudaGetLastError() == cudaSuccess ? CGGM_OK : CGGM_ERR_CUDA;
 }
+
+// L2 -> SM read bandwidth (test/bench-only export): every SM streams 16-byte loads over a buffer that
+// fits in L2 (after a warm-up pass), as the SpMM's gathers do; the denominator of the SpMM's L2
+// roofline (its algorithmic HBM bytes are far below its gathered bytes: it is L2-bound).
+namespace cggm {
+namespace {
+__global__ void __launch_bounds__(512) k_l2_read(const double2* __restrict__ buf, int64_t n16, int passes,
+                                                 double* out) {
+  double s0 = 0.0, s1 = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int p = 0; p < passes; ++p) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + (int64_t)p * 4096; i < n16 + (int64_t)p * 4096;
+         i += stride) {
+      const double2 v = __ldcg(buf + (i % n16));
+      s0 += v.x;
+      s1 += v.y;
+    }
+  }
+  if (s0 + s1 == 1234.5678) out[0] = s0;
+}
+}  // namespace
+}  // namespace cggm
+
+extern "C" cggm_status cggm_test_l2_peak(cggm_ctx* ctx_, double seconds, double* gbs, double* elapsed_ms) {
+  if (!ctx_ || !gbs || !elapsed_ms || !(seconds > 0)) return CGGM_ERR_INVALID_ARG;
+  Ctx* c = reinterpret_cast<Ctx*>(ctx_);
+  const int64_t bytes = 48ll << 20;   // 48 MB: resident in the 126 MB L2
+  void* buf = nullptr;
+  double* out = nullptr;
+  if (cudaMalloc(&buf, bytes) != cudaSuccess) return CGGM_ERR_OOM;
+  if (cudaMalloc(&out, 64) != cudaSuccess) {
+    cudaFree(buf);
+    return CGGM_ERR_OOM;
+  }
+  cudaMemsetAsync(buf, 0, bytes, c->stream);
+  const int64_t n16 = bytes / 16;
+  const int blocks = c->num_sms * 4, threads = 512;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  k_l2_read<<<blocks, threads, 0, c->stream>>>(static_cast<const double2*>(buf), n16, 1, out);   // warm L2
+  int passes = 4;
+  float ms = 0.f;
+  for (int rep = 0; rep < 6; ++rep) {
+    cudaEventRecord(e0, c->stream);
+    k_l2_read<<<blocks, threads, 0, c->stream>>>(static_cast<const double2*>(buf), n16, passes, out);
+    cudaEventRecord(e1, c->stream);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms >= 0.9 * seconds * 1e3) break;
+    const double scale = (seconds * 1e3) / (ms > 0.01 ? ms : 0.01);
+    passes = (int)std::min<double>(1e6, passes * scale) + 1;
+  }
+  *gbs = (double)bytes * passes / (ms * 1e-3) / 1e9;
+  *elapsed_ms = ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(buf);
+  cudaFree(out);
+  return cudaGetLastError() == cudaSuccess ? CGGM_OK : CGGM_ERR_CUDA;
+}

@@ -21,7 +21,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, name, split, q_out, distributed=False):
+def _worker(rank, world, port, name, split, q_out, distributed=False, grad_theta="allreduce", rs_width=256):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -36,14 +36,19 @@ def _worker(rank, world, port, name, split, q_out, distributed=False):
         a, b = shard_rows(P.n, world, rank)
         X, Y = to_device_colmajor(P.X[a:b]), to_device_colmajor(P.Y[a:b])
         ctx = Context(0)
-        ev = ShardedEvaluator(CudaBackend(ctx), split_objective=split, distributed_inverse=distributed, block=128)
+        ev = ShardedEvaluator(CudaBackend(ctx), split_objective=split, distributed_inverse=distributed, block=128,
+                              grad_theta=grad_theta, rs_width=rs_width)
         ev.setup(X, Y, P.n)
         r = ev.evaluate(X, Y, DeviceCsc.from_host(lam), DeviceCsc.from_host(th), P.lam_L, P.lam_T, True)
         torch.cuda.synchronize()
         if rank == 0:
+            act = r["active"]
             q_out.put({"Psi": r["Psi"].cpu().numpy(), "GradL": r["GradL"].cpu().numpy(),
-                       "GradT": r["GradT"].cpu().numpy(), "Sigma": r["Sigma"].cpu().numpy(), "f": r["f"],
-                       "logdet": r["logdet"], "m_L": r["active"]["m_L"], "m_T": r["active"]["m_T"]})
+                       "GradT": None if r["GradT"] is None else r["GradT"].cpu().numpy(),
+                       "Sigma": r["Sigma"].cpu().numpy(), "f": r["f"],
+                       "logdet": r["logdet"], "m_L": act["m_L"], "m_T": act["m_T"],
+                       "lists": {k: act[k].cpu().numpy() for k in ("L_row", "L_col", "T_row", "T_col")},
+                       "subgrad_l1": act["subgrad_l1"]})
     finally:
         dist.destroy_process_group()
 
@@ -328,3 +333,45 @@ def test_peer_allreduce_matches_oracle(world):
         assert r["f"] == pytest.approx(ob["f"], rel=1e-10)
     for r in res[1:]:
         assert np.array_equal(r["Psi"], res[0]["Psi"]) and np.array_equal(r["GradT"], res[0]["GradT"])
+
+
+@pytest.mark.parametrize("name,world,rs_width", [("small", 2, 128), ("small", 3, 100), ("medium", 2, 512),
+                                                 ("medium", 3, 256)])
+def test_reduce_scatter_grad_theta_matches_oracle(name, world, rs_width):
+    """grad_theta="reduce_scatter" with the CUDA backend: column ranges of grad_Theta reduce-scattered
+    round by round (cggm_psi_residual, cggm_gemm blocks, cggm_active_theta_block compaction with global
+    column indices), compact S_Theta lists all-gathered -- no rank holds a p x q buffer.  Lists equal
+    the oracle's exactly outside the tie band, statistic and f to rounding; ranks share
+    cuda:0 over gloo (functional check)."""
+    import torch.multiprocessing as mp
+    from oracle import cggm_oracle as O
+    from synth.cggm_inputs import make_problem
+    ctx = mp.get_context("spawn")
+    qo = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, True, qo, False, "reduce_scatter", rs_width))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = qo.get(timeout=900)
+    for p in procs:
+        p.join(timeout=900)
+        assert p.exitcode == 0
+    P = make_problem(name)
+    _, lam, th = P.points[1 if name in ("tiny", "small") else 0]
+    Syy, Sxy = O.covariances(P.X, P.Y)
+    S, ld, _, _ = O.invert_logdet(lam.to_dense())
+    ref = O.psi_grad(P.X, P.Y, th, S, Syy, Sxy)
+    ob = O.objective(P.X, P.Y, lam, th, P.lam_L, P.lam_T)
+    a = O.active_set(ref["GradL"], ref["GradT"], lam, th, P.lam_L, P.lam_T)
+    sub = O.min_norm_subgradient(ref["GradL"], ref["GradT"], lam, th, P.lam_L, P.lam_T)
+    assert res["GradT"] is None
+    for rk, ck, tm in (("L_row", "L_col", a["tie_mask_L"]), ("T_row", "T_col", a["tie_mask_T"])):
+        g = set(zip(res["lists"][rk].tolist(), res["lists"][ck].tolist()))
+        o = set(zip(a[rk].tolist(), a[ck].tolist()))
+        for (i, j) in g ^ o:
+            assert tm[i, j], (rk, i, j)
+        key = res["lists"][ck].astype(np.int64) * (1 << 31) + res["lists"][rk]
+        assert np.all(np.diff(key) > 0)
+    assert res["subgrad_l1"] == pytest.approx(sub, rel=1e-9)
+    assert res["f"] == pytest.approx(ob["f"], rel=1e-10)
