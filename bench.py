@@ -667,7 +667,7 @@ def main():
             l2_gbs = l2_by / (hbm["spmm"]["ms_per_step"] * 1e-3) / 1e9
             hbm["spmm"].update({"bound": "l2", "l2_gathered_bytes_per_step": l2_by, "l2_achieved_gbs": l2_gbs,
                                 "l2_peak_gbs": l2_peak_gbs, "l2_frac": l2_gbs / l2_peak_gbs,
-                                "l2_peak_source": "live cggm_test_l2_peak (16-byte loads over a 48 MB L2-resident "
+                                "l2_peak_source": "live cggm_test_l2_peak (16-byte loads over a 24 MB L2-resident "
                                                   "buffer, every SM)"})
 
     # ---------------------------------------------------------------- e2e through the public API

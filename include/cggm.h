@@ -368,6 +368,22 @@ cggm_status cggm_theta_cd(cggm_ctx* ctx, int64_t p, int64_t q, const void* Sigma
                           const int32_t* T_col, int64_t m_T, double lam_T, int passes, cggm_csc* out,
                           double* l1_theta);
 
+/* On-demand S_xx for the Theta sweep (the paper's (S_xx)_i rows): only
+ * the rows of S_xx the active list touches are formed, as columns (S_xx symmetric) of a p x n_cols
+ * block.  cggm_gram_rows: xmap (device, p int32, written) = position of row i among the distinct
+ * rows of T_row[0..m_T) in ascending order, -1 when absent; Sxx_cols (device, p x cap, ldsxx) column
+ * c = X^T X_{rows[c]} / n_total (all-reduced with a communicator); host n_cols = the number of
+ * distinct rows (CGGM_ERR_CAPACITY when > cap, n_cols then holds the required count).
+ * cggm_theta_cd_rows: cggm_theta_cd with S_xx given as those columns (xmap, n_cols).  fp64 ctx. */
+cggm_status cggm_gram_rows(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64_t p, const void* X, int64_t ldx,
+                           const int32_t* T_row, int64_t m_T, void* Sxx_cols, int64_t ldsxx, int64_t cap,
+                           int32_t* xmap, int64_t* n_cols);
+cggm_status cggm_theta_cd_rows(cggm_ctx* ctx, int64_t p, int64_t q, const void* Sigma, int64_t ldsigma,
+                               const void* Sxx_cols, int64_t ldsxx, const int32_t* xmap, int64_t n_cols,
+                               const void* Sxy, int64_t ldsxy, const cggm_csc* Theta, const int32_t* T_row,
+                               const int32_t* T_col, int64_t m_T, double lam_T, int passes, cggm_csc* out,
+                               double* l1_theta);
+
 /* ---- composite: one Newton-iteration evaluation -------------------
  * Same results as cggm_invert_logdet(Lambda) + cggm_psi_grad(residual route, fused active sets)
  * + cggm_objective(Lambda_trial = Lambda, Theta) on one GPU (n samples, no sharding), with the

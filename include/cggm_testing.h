@@ -29,7 +29,7 @@ cggm_status cggm_test_set_tile(cggm_ctx* ctx, int mode);
 /* FP64 tensor-pipe peak: independent DMMA.8x8x4 chains on 2 CTAs/SM for ~`seconds`; returns the
  * achieved TFLOP/s and the timed milliseconds (the roofline denominator bench.py reports). */
 cggm_status cggm_test_fp64_peak(cggm_ctx* ctx, double seconds, double* tflops, double* elapsed_ms);
-/* L2 -> SM read bandwidth: every SM streams 16-byte loads over a 48 MB L2-resident buffer for
+/* L2 -> SM read bandwidth: every SM streams 16-byte loads over a 24 MB L2-resident buffer for
  * ~`seconds`; returns GB/s and the timed milliseconds (the SpMM's L2 roofline denominator). */
 cggm_status cggm_test_l2_peak(cggm_ctx* ctx, double seconds, double* gbs, double* elapsed_ms);
 /* The recursive Cholesky of a dense q x q SPD matrix A (lower triangle read; overwritten with

@@ -137,6 +137,11 @@ SIGNATURES = {
                                  ctypes.POINTER(cggm_csc)]),
     "cggm_theta_cd": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, ctypes.POINTER(cggm_csc),
                               c_vp, c_vp, c_i64, c_d, c_i32, ctypes.POINTER(cggm_csc), ctypes.POINTER(c_d)]),
+    "cggm_gram_rows": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i64, c_vp,
+                               ctypes.POINTER(c_i64)]),
+    "cggm_theta_cd_rows": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
+                                   ctypes.POINTER(cggm_csc), c_vp, c_vp, c_i64, c_d, c_i32, ctypes.POINTER(cggm_csc),
+                                   ctypes.POINTER(c_d)]),
     "cggm_objective": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64,
                                ctypes.POINTER(cggm_csc), ctypes.POINTER(cggm_csc), c_d, c_d, c_i32,
                                c_vp, c_i64, ctypes.POINTER(cggm_objective_out)]),

@@ -543,6 +543,48 @@ class Context:
                                            int(passes), ctypes.byref(oc), ctypes.byref(l1)))
         return DeviceCsc(p, q, out.colptr, out.rowidx[:m], out.val[:m]), l1.value
 
+    def cggm_gram_rows(self, X, T_row, n_total=None, cache=None):
+        """On-demand S_xx: the columns X^T X_i / n of the distinct rows i of the active list T_row
+        (include/cggm.h).  Returns (Sxx_cols p x k, xmap int32 p); `cache` (a dict) keeps the buffers
+        across calls (grown on CGGM_ERR_CAPACITY)."""
+        self._sync_stream()
+        n, p = X.shape
+        n_total = n if n_total is None else n_total
+        cache = {} if cache is None else cache
+        if cache.get("xmap") is None or cache["xmap"].numel() != p:
+            cache["xmap"] = torch.empty(p, dtype=torch.int32, device=X.device)
+        while True:
+            cols = cache.get("cols")
+            cap = 0 if cols is None else cols.shape[1]
+            k = ctypes.c_int64()
+            st = self.lib.cggm_gram_rows(self.h, n, n_total, p, _ptr(X), ld_of(X), _ptr(T_row), int(T_row.numel()),
+                                         _ptr(cols), ld_of(cols) if cols is not None else max(p, 1), cap,
+                                         _ptr(cache["xmap"]), ctypes.byref(k))
+            if st == 6:
+                cache["cols"] = colmajor_empty(p, max(int(k.value), 1), device=X.device)
+                continue
+            self._check(st)
+            return (cache["cols"][:, :int(k.value)] if cache.get("cols") is not None else None), cache["xmap"]
+
+    def cggm_theta_cd_rows(self, Sigma, Sxx_cols, xmap, Sxy, Theta: DeviceCsc, T_row, T_col, lam_T, passes=1):
+        """cggm_theta_cd on the on-demand S_xx columns of cggm_gram_rows."""
+        self._sync_stream()
+        p, q = Theta.nrows, Theta.ncols
+        m = int(T_row.numel())
+        dev = Sigma.device
+        out = DeviceCsc(p, q, torch.zeros(q + 1, dtype=torch.int64, device=dev),
+                        torch.empty(max(m, 1), dtype=torch.int32, device=dev),
+                        torch.empty(max(m, 1), dtype=torch.float64, device=dev))
+        oc = _abi.cggm_csc(p, q, m, out.colptr.data_ptr(), out.rowidx.data_ptr(), out.val.data_ptr())
+        cs = Theta.c_struct()
+        l1 = ctypes.c_double()
+        k = 0 if Sxx_cols is None else int(Sxx_cols.shape[1])
+        self._check(self.lib.cggm_theta_cd_rows(
+            self.h, p, q, _ptr(Sigma), ld_of(Sigma), _ptr(Sxx_cols), ld_of(Sxx_cols) if k else 1, _ptr(xmap), k,
+            _ptr(Sxy), ld_of(Sxy), ctypes.byref(cs), _ptr(T_row), _ptr(T_col), m, float(lam_T), int(passes),
+            ctypes.byref(oc), ctypes.byref(l1)))
+        return DeviceCsc(p, q, out.colptr, out.rowidx[:m], out.val[:m]), l1.value
+
     # ---------------------------------------------------------------- composite
     def cggm_newton_eval(self, X, Y, Syy, Lam: DeviceCsc, Theta: DeviceCsc, lam_L, lam_T, penalize_diag=True,
                          tie_eps=1e-9, bufs=None, stream_grad_theta=False):

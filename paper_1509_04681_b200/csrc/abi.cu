@@ -181,7 +181,7 @@ cggm_status cggm_ctx_create(cggm_ctx** out, int device, cggm_dtype dtype, void* 
   if (const char* e = std::getenv("CGGM_CD_PREFETCH")) c->cd_prefetch = std::atoi(e);
   if (const char* e = std::getenv("CGGM_GRAPH_PROF")) c->graph_prof = std::atoi(e);
   if (const char* e = std::getenv("CGGM_TF32_CHUNK")) c->tf32_chunk = std::atoi(e);
-  if (const char* e = std::getenv("CGGM_NO_FUSE_GRADL")) c->no_fuse_gradl = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_FUSE_GRADL")) c->fuse_gradl = std::atoi(e);
   if (const char* e = std::getenv("CGGM_TF32_DEBUG")) c->tf32_dbg = std::atoi(e);
   if (const char* e = std::getenv("CGGM_F32_ENGINE")) c->f32_engine = std::string(e) == "ffma" ? 1 : 0;
   cudaDriverEntryPointQueryResult q;
@@ -603,19 +603,12 @@ cggm_status cggm_lambda_step(cggm_ctx* ctx, int64_t q, const cggm_csc* Lambda, c
   });
 }
 
-cggm_status cggm_theta_cd(cggm_ctx* ctx, int64_t p, int64_t q, const void* Sigma, int64_t ldsigma, const void* Sxx,
-                          int64_t ldsxx, const void* Sxy, int64_t ldsxy, const cggm_csc* Theta, const int32_t* T_row,
-                          const int32_t* T_col, int64_t m_T, double lam_T, int passes, cggm_csc* out,
-                          double* l1_theta) {
-  return guard(ctx, [&](Ctx* c) {
-    check_ctx_dtype(c);
-    if (q < 1 || p < 1 || passes < 0) fail(CGGM_ERR_INVALID_ARG, "need p, q >= 1, passes >= 0");
-    if (!(lam_T >= 0.0)) fail(CGGM_ERR_INVALID_ARG, "lam_T must be >= 0");
-    check_dense("Sigma", Sigma, q, q, ldsigma);
-    check_dense("Sxx", Sxx, p, p, ldsxx);
-    check_dense("Sxy", Sxy, p, q, ldsxy);
-    check_csc_host("Theta", Theta, p, q);
-    check_list("T", T_row, T_col, m_T);
+// the Theta sweep on S_xx columns Sxx (p x ncx, ldsxx): the full matrix (xmap null) or the compact
+// columns of the active rows (xmap device, p entries)
+static void theta_cd_run(Ctx* c, int64_t p, int64_t q, const void* Sigma, int64_t ldsigma, const void* Sxx,
+                         int64_t ldsxx, const int32_t* xmap, const void* Sxy, int64_t ldsxy, const cggm_csc* Theta,
+                         const int32_t* T_row, const int32_t* T_col, int64_t m_T, double lam_T, int passes,
+                         cggm_csc* out, double* l1_theta) {
     if (!out || out->nrows != p || out->ncols != q || !out->colptr) fail(CGGM_ERR_INVALID_ARG, "bad out CSC");
     if (m_T > 0 && (!out->rowidx || !out->val)) fail(CGGM_ERR_INVALID_ARG, "null out arrays");
     if (out->nnz < m_T) {
@@ -642,13 +635,14 @@ cggm_status cggm_theta_cd(cggm_ctx* ctx, int64_t p, int64_t q, const void* Sigma
       double* dmu = reinterpret_cast<double*>(lp + (q + 1));
       double* colbuf = dmu + std::max<int64_t>(m_T, 1);
       theta_cd_coop(c, (int)p, (int)q, static_cast<const double*>(Sigma), ldsigma, static_cast<const double*>(Sxx),
-                    ldsxx, static_cast<const double*>(Sxy), ldsxy, Theta, T_row, T_col, m_T, lam_T, passes, T, V, ldvr,
-                    coef, cnt2, scr, lp, dmu, colbuf, sc);
+                    ldsxx, xmap, static_cast<const double*>(Sxy), ldsxy, Theta, T_row, T_col, m_T, lam_T, passes, T,
+                    V, ldvr, coef, cnt2, scr, lp, dmu, colbuf, sc);
     } else {
       CGGM_CUDA_CHECK(cudaMemsetAsync(V, 0, (size_t)ldv * q * 8, c->stream));
       theta_sigma(c, (int)q, Theta, static_cast<const double*>(Sigma), ldsigma, V, ldv);
       theta_cd(c, (int)p, (int)q, static_cast<const double*>(Sigma), ldsigma, static_cast<const double*>(Sxx), ldsxx,
-               static_cast<const double*>(Sxy), ldsxy, Theta, T_row, T_col, m_T, lam_T, passes, T, V, ldv, coef, sc);
+               xmap, static_cast<const double*>(Sxy), ldsxy, Theta, T_row, T_col, m_T, lam_T, passes, T, V, ldv, coef,
+               sc);
     }
     list_to_csc(c, (int)q, T_row, T_col, m_T, false, nullptr, nullptr, 0.0, T, const_cast<int64_t*>(out->colptr),
                 const_cast<int32_t*>(out->rowidx), T, cnt, scan);
@@ -657,6 +651,73 @@ cggm_status cggm_theta_cd(cggm_ctx* ctx, int64_t p, int64_t q, const void* Sigma
     CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
     out->nnz = m_T;
     if (l1_theta) *l1_theta = h;
+}
+
+cggm_status cggm_theta_cd(cggm_ctx* ctx, int64_t p, int64_t q, const void* Sigma, int64_t ldsigma, const void* Sxx,
+                          int64_t ldsxx, const void* Sxy, int64_t ldsxy, const cggm_csc* Theta, const int32_t* T_row,
+                          const int32_t* T_col, int64_t m_T, double lam_T, int passes, cggm_csc* out,
+                          double* l1_theta) {
+  return guard(ctx, [&](Ctx* c) {
+    check_ctx_dtype(c);
+    if (q < 1 || p < 1 || passes < 0) fail(CGGM_ERR_INVALID_ARG, "need p, q >= 1, passes >= 0");
+    if (!(lam_T >= 0.0)) fail(CGGM_ERR_INVALID_ARG, "lam_T must be >= 0");
+    check_dense("Sigma", Sigma, q, q, ldsigma);
+    check_dense("Sxx", Sxx, p, p, ldsxx);
+    check_dense("Sxy", Sxy, p, q, ldsxy);
+    check_csc_host("Theta", Theta, p, q);
+    check_list("T", T_row, T_col, m_T);
+    theta_cd_run(c, p, q, Sigma, ldsigma, Sxx, ldsxx, nullptr, Sxy, ldsxy, Theta, T_row, T_col, m_T, lam_T, passes,
+                 out, l1_theta);
+  });
+}
+
+cggm_status cggm_gram_rows(cggm_ctx* ctx, int64_t n_local, int64_t n_total, int64_t p, const void* X, int64_t ldx,
+                           const int32_t* T_row, int64_t m_T, void* Sxx_cols, int64_t ldsxx, int64_t cap,
+                           int32_t* xmap, int64_t* n_cols) {
+  return guard(ctx, [&](Ctx* c) {
+    check_ctx_dtype(c);
+    if (n_local < 0 || p < 1 || m_T < 0 || cap < 0) fail(CGGM_ERR_INVALID_ARG, "negative dimension");
+    if (n_total < 1 || n_total < n_local) fail(CGGM_ERR_INVALID_ARG, "n_total must be >= max(1, n_local)");
+    check_dense("X", X, n_local, p, ldx);
+    if (m_T > 0 && !T_row) fail(CGGM_ERR_INVALID_ARG, "null T_row");
+    if (!xmap || !n_cols) fail(CGGM_ERR_INVALID_ARG, "null xmap / n_cols");
+    if (cap > 0) check_dense("Sxx_cols", Sxx_cols, p, cap, ldsxx);
+    int32_t* rows = static_cast<int32_t*>(ws_get(c, WS_CD_IDX, (size_t)p * 4 + 64));
+    long long* cnt = reinterpret_cast<long long*>(static_cast<char*>(ws_get(c, WS_CD_OUT, 64)) + 32);
+    row_map(c, (int)p, T_row, m_T, xmap, rows, cnt);
+    long long k = 0;
+    CGGM_CUDA_CHECK(cudaMemcpyAsync(c->host_scratch, cnt, 8, cudaMemcpyDeviceToHost, c->stream));
+    CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    std::memcpy(&k, c->host_scratch, 8);
+    *n_cols = k;
+    if (k > cap) fail(CGGM_ERR_CAPACITY, "more active rows than Sxx_cols columns (required count in n_cols)");
+    if (k == 0) return;
+    const int64_t ldg = pad_ld<double>(n_local > 0 ? n_local : 1);
+    double* G = static_cast<double*>(ws_get(c, WS_CD_U, (size_t)ldg * k * 8));
+    gather_cols(c, n_local, k, static_cast<const double*>(X), ldx, rows, G, ldg);
+    Epilogue e; e.out1 = static_cast<double*>(Sxx_cols); e.ld1 = ldsxx; e.a1 = 1.0 / (double)n_total;
+    gemm(c, true, false, p, k, n_local, static_cast<const double*>(X), ldx, G, ldg, e, 0);
+    if (comm_attached(c)) comm_allreduce(c, Sxx_cols, (k - 1) * ldsxx + p, 0);
+  });
+}
+
+cggm_status cggm_theta_cd_rows(cggm_ctx* ctx, int64_t p, int64_t q, const void* Sigma, int64_t ldsigma,
+                               const void* Sxx_cols, int64_t ldsxx, const int32_t* xmap, int64_t n_cols,
+                               const void* Sxy, int64_t ldsxy, const cggm_csc* Theta, const int32_t* T_row,
+                               const int32_t* T_col, int64_t m_T, double lam_T, int passes, cggm_csc* out,
+                               double* l1_theta) {
+  return guard(ctx, [&](Ctx* c) {
+    check_ctx_dtype(c);
+    if (q < 1 || p < 1 || passes < 0 || n_cols < 0) fail(CGGM_ERR_INVALID_ARG, "need p, q >= 1, passes >= 0");
+    if (!(lam_T >= 0.0)) fail(CGGM_ERR_INVALID_ARG, "lam_T must be >= 0");
+    if (!xmap) fail(CGGM_ERR_INVALID_ARG, "null xmap");
+    check_dense("Sigma", Sigma, q, q, ldsigma);
+    if (n_cols > 0) check_dense("Sxx_cols", Sxx_cols, p, n_cols, ldsxx);
+    check_dense("Sxy", Sxy, p, q, ldsxy);
+    check_csc_host("Theta", Theta, p, q);
+    check_list("T", T_row, T_col, m_T);
+    theta_cd_run(c, p, q, Sigma, ldsigma, n_cols > 0 ? Sxx_cols : Sigma, n_cols > 0 ? ldsxx : ldsigma, xmap, Sxy,
+                 ldsxy, Theta, T_row, T_col, m_T, lam_T, passes, out, l1_theta);
   });
 }
 
@@ -1004,12 +1065,13 @@ static void psi_enqueue(Ctx* c, int64_t n_local, int64_t n_total, int64_t p, int
       gemm(c, false, false, n_local, q, q, W, ldw, Sg, ldsigma, e, 0);
     }
   }
-  {  // a4/a5: Psi = R^T R (mirrored); grad_Lambda = S_yy - Sigma - Psi as the same GEMM's second
-     // epilogue output (-Psi + S_yy - Sigma per element, both triangles from one value;
-     // no separate 32 B/element streaming pass), unless Psi must first be all-reduced over the shards
+  {  // a4/a5: Psi = R^T R (mirrored), then grad_Lambda = (S_yy - Sigma) - Psi as one streaming pass;
+     // with CGGM_FUSE_GRADL=1 the same GEMM's second epilogue output instead (-Psi + S_yy -
+     // Sigma per element, both triangles from one value), unless Psi must first be all-reduced.  Measured
+     // at `large`: the fused epilogue adds 2.6 ms to the Psi GEMM and saves the 1.8 ms pass -> off
     Phase ph(c, TAG_PSI);
     EpilogueT<T> e; e.out1 = Psi; e.ld1 = ldpsi; e.a1 = 1.0;
-    const bool fuse_gl = GradL && !collective && !c->no_fuse_gradl;
+    const bool fuse_gl = GradL && !collective && c->fuse_gradl;
     if (fuse_gl) {
       e.out2 = GradL; e.ld2 = ldgl; e.a2 = -1.0;
       e.in2a = Syy; e.ld2a = ldsyy; e.b2 = 1.0;

@@ -228,15 +228,20 @@ __global__ void k_theta_sigma(int q, const int64_t* colptr, const int32_t* rowid
   }
 }
 
+// Column of S_xx holding row / column i: the full p x p matrix (xmap null), or the compact block of
+// the active rows' columns (cggm_gram_rows: xmap[i] = position of row i among them; NEXT-2 on-demand
+// (S_xx)_i = X^T X_i / n)
+__device__ __forceinline__ int64_t xcol(const int32_t* __restrict__ xmap, int i) { return xmap ? xmap[i] : i; }
+
 // Per-entry constants of the Theta sweep: a = 2 Sigma_jj (S_xx)_ii, 2 (S_xy)_ij, the current Theta_ij
 // (gathered from the CSC into T, the sweep's state) -- before the sequential walk.
 __global__ void k_theta_coefs(int64_t m, const double* __restrict__ S, int64_t lds, const double* __restrict__ Sxx,
-                              int64_t ldx, const double* __restrict__ Sxy, int64_t ldxy, const int64_t* colptr,
+                              int64_t ldx, const int32_t* __restrict__ xmap, const double* __restrict__ Sxy, int64_t ldxy, const int64_t* colptr,
                               const int32_t* rowidx, const double* tval, const int32_t* Tr, const int32_t* Tc,
                               double2* coef, double* T) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
     const int i = Tr[k], j = Tc[k];
-    coef[k] = make_double2(2.0 * S[j + (int64_t)j * lds] * Sxx[i + (int64_t)i * ldx], 2.0 * Sxy[i + (int64_t)j * ldxy]);
+    coef[k] = make_double2(2.0 * S[j + (int64_t)j * lds] * Sxx[i + xcol(xmap, i) * ldx], 2.0 * Sxy[i + (int64_t)j * ldxy]);
     T[k] = csc_at(colptr, rowidx, tval, i, j);
   }
 }
@@ -246,7 +251,8 @@ __global__ void k_theta_coefs(int64_t m, const double* __restrict__ S, int64_t l
 // the length-q row update is strided -- p > q on the paper's problems).  Same one-barrier-per-step
 // structure as the Lambda sweep.  out[0] = ||Theta_new||_1.
 __global__ void __launch_bounds__(CD_NT) k_theta_cd(int p, int q, const double* __restrict__ S, int64_t lds,
-                                                    const double* __restrict__ Sxx, int64_t ldx, const int32_t* Tr,
+                                                    const double* __restrict__ Sxx, int64_t ldx,
+                                                    const int32_t* __restrict__ xmap, const int32_t* Tr,
                                                     const int32_t* Tc, const double2* coef, int64_t m, double lam,
                                                     int passes, double* T, double* V, int64_t ldv, double* out) {
   __shared__ double red[2][CD_NW];
@@ -266,7 +272,7 @@ __global__ void __launch_bounds__(CD_NT) k_theta_cd(int p, int q, const double* 
         nc = coef[k + 1];
         nt = T[k + 1];
       }
-      const double* Xi = Sxx + (int64_t)i * ldx;   // row i of S_xx = column i
+      const double* Xi = Sxx + xcol(xmap, i) * ldx;   // row i of S_xx = column i
       const double* Vj = V + (int64_t)j * ldv;
       double v = 0.0;
       for (int t0 = threadIdx.x; t0 < p; t0 += CD_UNR * CD_NT) {
@@ -492,6 +498,7 @@ __global__ void k_theta_sigma_rm(int q, const int64_t* colptr, const int32_t* ro
 
 __global__ void __launch_bounds__(CO_NT) k_theta_sweep_coop(int p, int q, const double* __restrict__ S, int64_t lds,
                                                             const double* __restrict__ Sxx, int64_t ldx,
+                                                            const int32_t* __restrict__ xmap,
                                                             const int32_t* Tr, const double2* coef, const int64_t* lp,
                                                             double lam, int passes, double* T, double* dmu, double* V,
                                                             int64_t ldv, double* colbuf, int use_smem) {
@@ -512,7 +519,7 @@ __global__ void __launch_bounds__(CO_NT) k_theta_sweep_coop(int p, int q, const 
         for (int64_t k = k0; k < k1; ++k) {
           const int i = Tr[k];
           const double2 cf = coef[k];
-          const double* Xi = Sxx + (int64_t)i * ldx;
+          const double* Xi = Sxx + xcol(xmap, i) * ldx;
           double v = 0.0;
           for (int t0 = threadIdx.x; t0 < p; t0 += CO_UNR * CO_NT) {
             double xv[CO_UNR];
@@ -690,6 +697,7 @@ constexpr int CO_PMAX = CO_NT * CO_VU;
 
 __global__ void __launch_bounds__(CO_NT) k_theta_sweep_pf(int p, int q, const double* __restrict__ S, int64_t lds,
                                                           const double* __restrict__ Sxx, int64_t ldx,
+                                                          const int32_t* __restrict__ xmap,
                                                           const int32_t* Tr, const double2* coef, const int64_t* lp,
                                                           double lam, int passes, double* T, double* dmu, double* V,
                                                           int64_t ldv) {
@@ -703,7 +711,7 @@ __global__ void __launch_bounds__(CO_NT) k_theta_sweep_pf(int p, int q, const do
   const int x = threadIdx.x;
   // S_xx column i -> shared buffer b, 16-byte cp.async chunks (ldx even, so columns are aligned)
   auto fetch = [&](int i, int b) {
-    const double* src = Sxx + (int64_t)i * ldx;
+    const double* src = Sxx + xcol(xmap, i) * ldx;
     for (int c2 = x; 2 * c2 < p; c2 += CO_NT) {
       const int r = 2 * c2;
       ptx::cp_async16(buf[b] + r, src + r, (r + 1 < p) ? 16u : 8u);
@@ -899,17 +907,91 @@ void theta_sigma(Ctx* c, int q, const cggm_csc* Th, const double* S, int64_t lds
   post_launch(c, "k_theta_sigma");
 }
 
-void theta_cd(Ctx* c, int p, int q, const double* S, int64_t lds, const double* Sxx, int64_t ldx, const double* Sxy,
+void theta_cd(Ctx* c, int p, int q, const double* S, int64_t lds, const double* Sxx, int64_t ldx, const int32_t* xmap,
+              const double* Sxy,
               int64_t ldxy, const cggm_csc* Th, const int32_t* Tr, const int32_t* Tc, int64_t m, double lam, int passes,
               double* T, double* V, int64_t ldv, double* coef_ws, double* out) {
   Prof pr(c, TAG_MISC);
   double2* coef = reinterpret_cast<double2*>(coef_ws);
   if (m > 0)
-    k_theta_coefs<<<grid_for(m), 256, 0, c->stream>>>(m, S, lds, Sxx, ldx, Sxy, ldxy, Th->colptr, Th->rowidx,
+    k_theta_coefs<<<grid_for(m), 256, 0, c->stream>>>(m, S, lds, Sxx, ldx, xmap, Sxy, ldxy, Th->colptr, Th->rowidx,
                                                       static_cast<const double*>(Th->val), Tr, Tc, coef, T);
-  k_theta_cd<<<1, CD_NT, 0, c->stream>>>(p, q, S, lds, Sxx, ldx, Tr, Tc, coef, m, lam, passes, T, V, ldv, out);
+  k_theta_cd<<<1, CD_NT, 0, c->stream>>>(p, q, S, lds, Sxx, ldx, xmap, Tr, Tc, coef, m, lam, passes, T, V, ldv, out);
   c->launches += m > 0 ? 1 : 0;
   post_launch(c, "k_theta_cd");
+}
+
+namespace {
+__global__ void k_row_flags(int64_t m, const int32_t* __restrict__ Tr, int32_t* flags) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x)
+    flags[Tr[k]] = 1;
+}
+
+// one block: exclusive scan of the flags in 1024-entry rounds (warp shuffles), ascending row order
+__global__ void __launch_bounds__(1024) k_row_map_scan(int p, int32_t* xmap, int32_t* rows, long long* count) {
+  __shared__ int wsum[32];
+  __shared__ long long base;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int i0 = 0; i0 < p; i0 += 1024) {
+    const int i = i0 + threadIdx.x;
+    const int f = (i < p && xmap[i]) ? 1 : 0;
+    int x = f;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int v = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      wsum[lane] = v;
+    }
+    __syncthreads();
+    const long long pos = base + (w > 0 ? wsum[w - 1] : 0) + x - f;
+    if (i < p) {
+      xmap[i] = f ? (int32_t)pos : -1;
+      if (f) rows[pos] = i;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) base += wsum[31];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *count = base;
+}
+
+__global__ void k_gather_cols(int64_t n, int64_t k, const double* __restrict__ X, int64_t ldx,
+                              const int32_t* __restrict__ rows, double* __restrict__ G, int64_t ldg) {
+  const int64_t c = blockIdx.y;
+  const double* src = X + (int64_t)rows[c] * ldx;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    G[i + c * ldg] = src[i];
+}
+}  // namespace
+
+void row_map(Ctx* c, int p, const int32_t* T_row, int64_t m, int32_t* xmap, int32_t* rows, long long* count_dev) {
+  Prof pr(c, TAG_MISC);
+  CGGM_CUDA_CHECK(cudaMemsetAsync(xmap, 0, sizeof(int32_t) * (size_t)p, c->stream));
+  if (m > 0) k_row_flags<<<grid_for(m), 256, 0, c->stream>>>(m, T_row, xmap);
+  k_row_map_scan<<<1, 1024, 0, c->stream>>>(p, xmap, rows, count_dev);
+  c->launches += m > 0 ? 1 : 0;
+  post_launch(c, "k_row_map_scan");
+}
+
+void gather_cols(Ctx* c, int64_t n, int64_t k, const double* X, int64_t ldx, const int32_t* rows, double* G,
+                 int64_t ldg) {
+  if (n == 0 || k == 0) return;
+  Prof pr(c, TAG_MISC);
+  dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 8), (unsigned)k);
+  k_gather_cols<<<grid, 256, 0, c->stream>>>(n, k, X, ldx, rows, G, ldg);
+  post_launch(c, "k_gather_cols");
 }
 
 // list column pointers lp (n+1) of a column-major list: counts + scan (cnt: n ints, scr: n+1 int64)
@@ -975,7 +1057,7 @@ void lambda_cd_coop(Ctx* c, int q, const double* S, int64_t lds, const double* P
 }
 
 void theta_cd_coop(Ctx* c, int p, int q, const double* S, int64_t lds, const double* Sxx, int64_t ldx,
-                   const double* Sxy, int64_t ldxy, const cggm_csc* Th, const int32_t* Tr, const int32_t* Tc, int64_t m,
+                   const int32_t* xmap, const double* Sxy, int64_t ldxy, const cggm_csc* Th, const int32_t* Tr, const int32_t* Tc, int64_t m,
                    double lam, int passes, double* T, double* V, int64_t ldv, double* coef_ws, int* cnt, int64_t* scr,
                    int64_t* lp, double* dmu, double* colbuf, double* out) {
   Prof pr(c, TAG_MISC);
@@ -984,7 +1066,7 @@ void theta_cd_coop(Ctx* c, int p, int q, const double* S, int64_t lds, const dou
   k_theta_sigma_rm<<<(q + 7) / 8, 256, 0, c->stream>>>(q, Th->colptr, Th->rowidx, static_cast<const double*>(Th->val),
                                                        S, lds, V, ldv);
   if (m > 0) {
-    k_theta_coefs<<<grid_for(m), 256, 0, c->stream>>>(m, S, lds, Sxx, ldx, Sxy, ldxy, Th->colptr, Th->rowidx,
+    k_theta_coefs<<<grid_for(m), 256, 0, c->stream>>>(m, S, lds, Sxx, ldx, xmap, Sxy, ldxy, Th->colptr, Th->rowidx,
                                                       static_cast<const double*>(Th->val), Tr, Tc, coef, T);
     list_colptr(c, q, Tr, Tc, m, cnt, scr, lp);
     int grid = c->num_sms;
@@ -993,7 +1075,7 @@ void theta_cd_coop(Ctx* c, int p, int q, const double* S, int64_t lds, const dou
       CGGM_ONCE_PER_DEVICE({
         CGGM_CUDA_CHECK(cudaFuncSetAttribute(k_theta_sweep_pf, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       });
-      void* args[] = {&p, &q, &S, &lds, &Sxx, &ldx, &Tr, &coef, &lp, &lam, &passes, &T, &dmu, &V, &ldv};
+      void* args[] = {&p, &q, &S, &lds, &Sxx, &ldx, &xmap, &Tr, &coef, &lp, &lam, &passes, &T, &dmu, &V, &ldv};
       CGGM_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_theta_sweep_pf, dim3(grid), dim3(CO_NT), args, smem_pf,
                                                   c->stream));
       c->launches += 2;
@@ -1006,7 +1088,7 @@ void theta_cd_coop(Ctx* c, int p, int q, const double* S, int64_t lds, const dou
     CGGM_ONCE_PER_DEVICE({
       CGGM_CUDA_CHECK(cudaFuncSetAttribute(k_theta_sweep_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     });
-    void* args[] = {&p, &q, &S, &lds, &Sxx, &ldx, &Tr, &coef, &lp, &lam, &passes, &T, &dmu, &V, &ldv, &colbuf,
+    void* args[] = {&p, &q, &S, &lds, &Sxx, &ldx, &xmap, &Tr, &coef, &lp, &lam, &passes, &T, &dmu, &V, &ldv, &colbuf,
                     const_cast<int*>(&use_smem)};
     CGGM_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_theta_sweep_coop, dim3(grid), dim3(CO_NT), args,
                                                 use_smem ? smem : 0, c->stream));

@@ -113,7 +113,8 @@ struct Ctx {
   int no_split_k = 0;   // CGGM_NO_SPLIT_K=1: W Sigma without the split-k grid (A/B)
   int no_vec_epi = 0;
   int persist_tpc = 0;   // CGGM_PERSIST_TPC: tiles per CTA of the persistent warp-specialised GEMM (0: off)   // CGGM_NO_VEC_EPI=1: scalar GEMM epilogue everywhere (A/B)      // CGGM_ACT_ONEPASS=1: Lambda list by the single-pass look-back kernel (not the split one)    // test hook (CGGM_NO_ACTIVE_VEC=1): scalar active-set kernel only   // test hook (CGGM_NO_SMALL_ASYNC=1): direct-load small kernel only
-  int no_fuse_gradl = 0;   // CGGM_NO_FUSE_GRADL=1: grad_Lambda by its own streaming pass, not the Psi epilogue (A/B)
+  int fuse_gradl = 0;   // CGGM_FUSE_GRADL=1: grad_Lambda as the Psi GEMM's second epilogue output (measured: the
+                        // two-input mirrored epilogue costs the K = n GEMM more than the 1.8 ms pass it saves)
   int tf32_dbg = 0;     // CGGM_TF32_DEBUG (gemm_tf32.cu measurement aid)
   int tf32_chunk = 4;   // 3xTF32: k-tiles per drained TMEM partial (gemm_tf32.cu; CGGM_TF32_CHUNK, 0 = none)
   int f32_engine = 0;   // FP32 contractions: 0 = 3xTF32 on tcgen05 (gemm_tf32.cu), 1 = SIMT FFMA (CGGM_F32_ENGINE=ffma)

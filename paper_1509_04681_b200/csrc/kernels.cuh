@@ -67,16 +67,22 @@ void lambda_cd(Ctx* c, int q, const double* S, int64_t lds, const double* P, int
                const cggm_csc* Lam, const int32_t* Lr, const int32_t* Lc, int64_t m, double lam, int penalize_diag,
                int passes, double* D, double* U, int64_t ldu, double* coef_ws /* 4m doubles */, double* out);
 void theta_sigma(Ctx* c, int q, const cggm_csc* Th, const double* S, int64_t lds, double* V, int64_t ldv);
-void theta_cd(Ctx* c, int p, int q, const double* S, int64_t lds, const double* Sxx, int64_t ldx, const double* Sxy,
+void theta_cd(Ctx* c, int p, int q, const double* S, int64_t lds, const double* Sxx, int64_t ldx, const int32_t* xmap,
+              const double* Sxy,
               int64_t ldxy, const cggm_csc* Th, const int32_t* Tr, const int32_t* Tc, int64_t m, double lam, int passes,
               double* T, double* V, int64_t ldv, double* coef_ws /* 2m doubles */, double* out);
 bool coop_ok(Ctx* c);
+// NEXT-2 on-demand S_xx columns: xmap[i] = position of row i among the distinct rows of the list
+// T_row[0..m) in ascending order (-1 if absent), rows[0..count) those rows, *count_dev their number
+void row_map(Ctx* c, int p, const int32_t* T_row, int64_t m, int32_t* xmap, int32_t* rows, long long* count_dev);
+// G (n x k, ldg) = X[:, rows[0..k)]
+void gather_cols(Ctx* c, int64_t n, int64_t k, const double* X, int64_t ldx, const int32_t* rows, double* G, int64_t ldg);
 void lambda_cd_coop(Ctx* c, int q, const double* S, int64_t lds, const double* P, int64_t ldp, const double* G,
                     int64_t ldg, const cggm_csc* Lam, const int32_t* Lr, const int32_t* Lc, int64_t m, double lam,
                     int penalize_diag, int passes, double* D, double* U, double* Z, int64_t ldu, double* coef_ws,
                     int* cnt, int64_t* scr, int64_t* lp, double* dmu, double* colbuf, double* out);
 void theta_cd_coop(Ctx* c, int p, int q, const double* S, int64_t lds, const double* Sxx, int64_t ldx,
-                   const double* Sxy, int64_t ldxy, const cggm_csc* Th, const int32_t* Tr, const int32_t* Tc, int64_t m,
+                   const int32_t* xmap, const double* Sxy, int64_t ldxy, const cggm_csc* Th, const int32_t* Tr, const int32_t* Tc, int64_t m,
                    double lam, int passes, double* T, double* V, int64_t ldv, double* coef_ws, int* cnt, int64_t* scr,
                    int64_t* lp, double* dmu, double* colbuf, double* out);
 // sorted list (column-major) -> CSC: mirror = symmetric Lambda + alpha D from the upper-triangle list

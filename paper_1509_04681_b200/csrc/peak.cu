@@ -61,21 +61,27 @@ extern "C" cggm_status cggm_test_fp64_peak(cggm_ctx* ctx_, double seconds, doubl
   return cudaGetLastError() == cudaSuccess ? CGGM_OK : CGGM_ERR_CUDA;
 }
 
-// L2 -> SM read bandwidth (test/bench-only export): every SM streams 16-byte loads over a buffer that
-// fits in L2 (after a warm-up pass), as the SpMM's gathers do; the denominator of the SpMM's L2
+// L2 -> SM read bandwidth (test/bench-only export): every SM streams 16-byte loads (4 in flight per
+// thread) over a 24 MB buffer that stays in L2 after a warm-up pass, as the SpMM's gathers do; the denominator of the SpMM's L2
 // roofline (its algorithmic HBM bytes are far below its gathered bytes: it is L2-bound).
 namespace cggm {
 namespace {
 __global__ void __launch_bounds__(512) k_l2_read(const double2* __restrict__ buf, int64_t n16, int passes,
                                                  double* out) {
+  // 4 independent 16-byte loads in flight per thread, contiguous per warp (512 B per load group)
   double s0 = 0.0, s1 = 0.0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
   for (int p = 0; p < passes; ++p) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + (int64_t)p * 4096; i < n16 + (int64_t)p * 4096;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x) * 4 + threadIdx.x; i + 3 * (int64_t)blockDim.x < n16;
          i += stride) {
-      const double2 v = __ldcg(buf + (i % n16));
-      s0 += v.x;
-      s1 += v.y;
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcg(buf + i + u * (int64_t)blockDim.x);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        s0 += v[u].x;
+        s1 += v[u].y;
+      }
     }
   }
   if (s0 + s1 == 1234.5678) out[0] = s0;
@@ -86,7 +92,7 @@ __global__ void __launch_bounds__(512) k_l2_read(const double2* __restrict__ buf
 extern "C" cggm_status cggm_test_l2_peak(cggm_ctx* ctx_, double seconds, double* gbs, double* elapsed_ms) {
   if (!ctx_ || !gbs || !elapsed_ms || !(seconds > 0)) return CGGM_ERR_INVALID_ARG;
   Ctx* c = reinterpret_cast<Ctx*>(ctx_);
-  const int64_t bytes = 48ll << 20;   // 48 MB: resident in the 126 MB L2
+  const int64_t bytes = 24ll << 20;   // 24 MB: resident in the 126 MB L2 (both partitions)
   void* buf = nullptr;
   double* out = nullptr;
   if (cudaMalloc(&buf, bytes) != cudaSuccess) return CGGM_ERR_OOM;

@@ -238,3 +238,45 @@ def test_lambda_direction_medium_unpenalised_matches_oracle(ctx):
     vals, d_ref, _, _ = _medium_oracle_sweeps(s, P, False)
     assert np.linalg.norm(D.cpu().numpy() - vals) <= 1e-10 * np.linalg.norm(vals)
     assert delta == pytest.approx(d_ref, rel=1e-9)
+
+
+@pytest.mark.parametrize("name,k", [("small", 1), ("medium", 0)])
+def test_gram_rows_and_theta_sweep_on_demand(ctx, name, k):
+    """NEXT-2 on-demand S_xx: cggm_gram_rows forms only the columns X^T X_i / n of the
+    rows on the Theta list -- xmap is exact (row -> position among the distinct rows, ascending;
+    -1 elsewhere), the columns match the definition -- and the Theta sweep on them equals the oracle's
+    sweep on the full S_xx."""
+    P = problem(name)
+    s = _gpu_state(ctx, P, k)
+    act = s["active"]
+    cols, xmap = ctx.cggm_gram_rows(s["X"], act["T_row"])
+    rows = np.unique(act["T_row"].cpu().numpy())
+    want = np.full(P.p, -1, dtype=np.int64)
+    want[rows] = np.arange(rows.size)
+    np.testing.assert_array_equal(xmap.cpu().numpy(), want)
+    n = P.X.shape[0]
+    ref = P.X.T @ P.X[:, rows] / n
+    got = cols.cpu().numpy()
+    assert got.shape == ref.shape
+    assert np.linalg.norm(got - ref) <= 1e-13 * np.linalg.norm(ref)
+    Tn, l1 = ctx.cggm_theta_cd_rows(s["Sigma"], cols, xmap, s["Sxy"], s["Tg"], act["T_row"], act["T_col"], P.lam_T, 1)
+    trows, tcols = act["T_row"].cpu().numpy(), act["T_col"].cpu().numpy()
+    Tref, _ = A.theta_cd_sweep(s["Sigma"].cpu().numpy(), P.X.T @ P.X / n, P.X.T @ P.Y / n, s["th"].to_dense(), trows,
+                               tcols, P.lam_T, 1)
+    vals = Tref[trows, tcols]
+    assert np.linalg.norm(Tn.val.cpu().numpy() - vals) <= 1e-9 * np.linalg.norm(vals)
+    assert l1 == pytest.approx(np.abs(Tref).sum(), rel=1e-9)
+
+
+def test_algorithm1_on_demand_sxx_matches_dense(ctx):
+    """Algorithm 1 with on-demand S_xx columns and factor reuse gives the same iterates as with the
+    dense S_xx (same sweep kernel, S_xx entries from different GEMMs: rounding-level differences)."""
+    from paper_1509_04681_b200 import to_device_colmajor
+    from paper_1509_04681_b200.solver import ancd_fit
+    P = problem("tiny")
+    X, Y = to_device_colmajor(P.X), to_device_colmajor(P.Y)
+    a = ancd_fit(ctx, X, Y, P.lam_L, P.lam_T, max_iter=5, tol=0.0, sxx="rows")
+    b = ancd_fit(ctx, X, Y, P.lam_L, P.lam_T, max_iter=5, tol=0.0, sxx="dense")
+    for ha, hb in zip(a.history, b.history):
+        assert ha["f"] == pytest.approx(hb["f"], rel=1e-12)
+        assert ha["alpha"] == hb["alpha"] and (ha["m_L"], ha["m_T"]) == (hb["m_L"], hb["m_T"])
