@@ -1059,17 +1059,26 @@ void gemm_log(Ctx* c, int BM, int BN, int M, int N, int K, int flags, int grid, 
   if (!on) return;
   const int tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
   double fl = 0.0;
-  for (int I = 0; I < tm; ++I)
-    for (int J = 0; J < tn; ++J) {
-      if ((flags & SYM_LOWER) && I < J) continue;
-      const int m0 = I * BM, n0 = J * BN;
-      int kbeg = 0, kend = K;
-      if (flags & A_KGE_M) kbeg = std::max(kbeg, m0);
-      if (flags & B_KGE_N) kbeg = std::max(kbeg, n0);
-      if (flags & A_KLE_M) kend = std::min(kend, m0 + BM);
-      if (flags & B_KLE_N) kend = std::min(kend, n0 + BN);
-      if (kend > kbeg) fl += 2.0 * BM * BN * (double)(((kend - kbeg + 15) / 16) * 16);
-    }
+  auto tile = [&](int m0, int n0) {   // executed flops of one BM x BN tile (16-wide k-steps)
+    int kbeg = 0, kend = K;
+    if (flags & A_KGE_M) kbeg = std::max(kbeg, m0);
+    if (flags & B_KGE_N) kbeg = std::max(kbeg, n0);
+    if (flags & A_KLE_M) kend = std::min(kend, m0 + BM);
+    if (flags & B_KLE_N) kend = std::min(kend, n0 + BN);
+    if (kend > kbeg) fl += 2.0 * BM * BN * (double)(((kend - kbeg + 15) / 16) * 16);
+  };
+  if ((flags & SYM_LOWER) && BN * 2 == BM) {
+    // the sym_split walk (run_cfg): BM x BM squares I >= J, each as two BN-wide column halves
+    const int ts = (N + BM - 1) / BM;
+    for (int I = 0; I < tm; ++I)
+      for (int J = 0; J < ts && J <= I; ++J)
+        for (int h = 0; h < 2; ++h)
+          if (J * BM + h * BN < N) tile(I * BM, J * BM + h * BN);
+  } else {
+    for (int I = 0; I < tm; ++I)
+      for (int J = 0; J < tn; ++J)
+        if (!((flags & SYM_LOWER) && I < J)) tile(I * BM, J * BN);
+  }
   std::fprintf(stderr, "GEMMLOG tile=%dx%d M=%d N=%d K=%d flags=%d tA=%d tB=%d grid=%d exec_flops=%.6e lane=%d\n", BM, BN,
                M, N, K, flags, (int)tA, (int)tB, grid, fl, c->lane);
 }

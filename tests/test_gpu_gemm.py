@@ -16,8 +16,9 @@ A_KLE_M, A_KGE_M, B_KLE_N, B_KGE_N, SYM_LOWER, SYM_MIRROR = 1, 2, 4, 8, 16, 32
                 ids=["auto_small", "tile128", "tile128_square", "tile64", "tile128_2d", "tile64_2d", "auto_small_direct"])
 def ctx(request):
     """auto_small: small shapes on the cp.async kernel; auto_small_direct: on the direct-load one;
-    tile128: non-symmetric products on the two-CTA 128x64 tiles (the default), symmetric ones on
-    128x128; tile128_square: everything on 128x128 (CGGM_MID_TILE=0)."""
+    tile128: the two-CTA 128x64 tiles (the default, CGGM_MID_TILE=3) -- symmetric (SYM_LOWER) products
+    walk 128x128 squares in two column halves with per-element diagonal masking; tile128_square:
+    everything on 128x128 (CGGM_MID_TILE=0)."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import os
@@ -87,6 +88,20 @@ def test_gemm_sym_lower_mirror(ctx, q, K):
     low = np.tril(np.ones((q, q), dtype=bool))
     np.testing.assert_allclose(out2[low], (7.0 - ref)[low], rtol=1e-13, atol=1e-12)
     np.testing.assert_array_equal(out2[~low], 7.0)       # upper triangle untouched
+
+
+@pytest.mark.parametrize("q", [385, 200])
+def test_gemm_sym_lower_mirror_lauum_flags(ctx, q):
+    """The step's largest launch in miniature: Sigma = X^T X with X lower triangular (L^{-1}), the
+    lauum flags A_KGE_M | B_KGE_N (triangular k-ranges) on the symmetric lower / mirror walk, at ragged
+    q where the last square's right column half falls past N (q = 385: 4 squares, the last with one
+    valid column)."""
+    rng = np.random.default_rng(7 * q)
+    X = np.tril(rng.standard_normal((q, q)))
+    ref = X.T @ X
+    out = run(ctx, True, False, X, X, np.zeros((q, q)), 1.0, 0.0, SYM_LOWER | SYM_MIRROR | A_KGE_M | B_KGE_N, q, q, q)
+    np.testing.assert_array_equal(out, out.T)
+    assert np.linalg.norm(out - ref) / np.linalg.norm(ref) < 1e-14
 
 
 @pytest.mark.parametrize("flags", [A_KLE_M, A_KGE_M, B_KLE_N, B_KGE_N, A_KGE_M | B_KGE_N])
