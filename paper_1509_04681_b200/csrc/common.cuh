@@ -116,6 +116,7 @@ struct Ctx {
   int fuse_gradl = 0;   // CGGM_FUSE_GRADL=1: grad_Lambda as the Psi GEMM's second epilogue output (measured: the
                         // two-input mirrored epilogue costs the K = n GEMM more than the 1.8 ms pass it saves)
   int tf32_dbg = 0;     // CGGM_TF32_DEBUG (gemm_tf32.cu measurement aid)
+  int tf32_producer = 0;   // 3xTF32 operand producer: 0 = TMA raw ring + converters, 1 = register-staged loads (CGGM_TF32_PRODUCER=ldg)
   int tf32_chunk = 4;   // 3xTF32: k-tiles per drained TMEM partial (gemm_tf32.cu; CGGM_TF32_CHUNK, 0 = none)
   int f32_engine = 0;   // FP32 contractions: 0 = 3xTF32 on tcgen05 (gemm_tf32.cu), 1 = SIMT FFMA (CGGM_F32_ENGINE=ffma)
   int no_tma3d = 0;   // test hook: 1 = always use 16-wide 2-D boxes for MN-inner operands  // test hook: 0 auto, 1 = 128x128 tiles, 2 = 64x64 tiles
@@ -311,7 +312,8 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K,
 void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K,
           const float* A, int64_t lda, const float* B, int64_t ldb, const EpilogueT<float>& epi, int flags);
 void gemm_tf32x3(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
-                 const float* B, int64_t ldb, const EpilogueT<float>& epi, int flags);
+                 const float* B, int64_t ldb, const EpilogueT<float>& epi, int flags, const CUtensorMap& ma,
+                 const CUtensorMap& mb, int a3d, int b3d);
 
 // ------------------------------------------------------------------ Cholesky family (chol.cu)
 // In-place blocked recursive Cholesky of the lower triangle of A (q x q).

@@ -299,10 +299,6 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
   }
   if ((flags & SYM_LOWER) && (M < N || ((flags & SYM_MIRROR) && M != N)))
     throw CudaError{CGGM_ERR_SHAPE, "SYM_LOWER gemm needs M >= N (M == N with SYM_MIRROR)"};
-  if (c->f32_engine == 0) {
-    gemm_tf32x3(c, transA, transB, M, N, K, A, lda, B, ldb, epi, flags);
-    return;
-  }
   KParamsF P;
   P.M = (int)M; P.N = (int)N; P.K = (int)(K > 0 ? K : 0);
   P.flags = flags;
@@ -317,6 +313,10 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
                           : (P.a3d ? make_map_f_mn3d(c, A, lda, M, Keff) : make_map_f(c, A, lda, M, Keff, 32, FBK));
   CUtensorMap mb = transB ? (P.b3d ? make_map_f_mn3d(c, B, ldb, N, Keff) : make_map_f(c, B, ldb, N, Keff, 32, FBK))
                           : make_map_f(c, B, ldb, Keff, N, FBK, FBN);
+  if (c->f32_engine == 0) {   // 3xTF32 on the tensor cores (gemm_tf32.cu), the same operand maps
+    gemm_tf32x3(c, transA, transB, M, N, K, A, lda, B, ldb, epi, flags, ma, mb, P.a3d, P.b3d);
+    return;
+  }
   const bool AK = transA, BKI = !transB;
   if (AK && BKI) launch_f<true, true>(c, ma, mb, P, grid);
   else if (AK && !BKI) launch_f<true, false>(c, ma, mb, P, grid);

@@ -29,21 +29,29 @@ namespace cggm {
 namespace {
 
 constexpr int TBM = 128, TBN = 128, TBK = 32;
-constexpr int TSTAGES = 3;
-constexpr int T_OP = TBM * TBK * 4;          // 16 KB per operand half (hi or lo)
-constexpr int T_STAGE = 4 * T_OP;            // A_hi, A_lo, B_hi, B_lo
-constexpr int T_DATA = TSTAGES * T_STAGE;    // 192 KB
+constexpr int T_OP = TBM * TBK * 4;          // 16 KB per operand half (hi or lo) or raw operand tile
+constexpr int T_STAGE = 4 * T_OP;            // split stage: A_hi, A_lo, B_hi, B_lo
+constexpr int T_RAW = 2 * T_OP;              // raw stage (TMA producer): A, B fp32 tiles
 constexpr int T_EPI_LD = TBM + 1;
-static_assert(TBN * T_EPI_LD * 4 <= T_DATA, "epilogue tile must fit in the stage buffers");
-constexpr int T_SMEM = T_DATA + 1024 + 128;
-constexpr int T_PROD = 256;                  // producer threads (warps 0-7)
+constexpr int T_PROD = 256;                  // producer / converter threads (warps 0-7)
 constexpr int T_PER = TBM * TBK / 4 / T_PROD;   // float4 per operand per producer thread per k-tile (4)
 constexpr int T_DRAIN = 128;                 // accumulator-drain / epilogue threads (warps 8-11)
 constexpr int T_DW0 = T_PROD / 32;           // first drain warp
 constexpr int T_MMA_WARP = T_DW0 + 4;        // the MMA-issuing warp (12)
-constexpr int T_NT = T_PROD + T_DRAIN + 32;
+constexpr int T_TMA_WARP = T_MMA_WARP + 1;   // the TMA-issuing warp (13, TMA producer only)
 constexpr int T_GROUP_N = 8;
 constexpr uint32_t T_TMEM_COLS = 512;   // X0 (cols 0-127), D2 (128-255), X1 (256-383), running sum S (384-511)
+// Producer modes: LDG (registers, one k-tile ahead; 3 split stages) or TMA (raw fp32 tiles by TMA into
+// a 3-deep ring -- the loads no longer wait on the converters' registers -- converted from shared
+// memory into 2 split stages)
+template <bool TMA> struct TCfg {
+  static constexpr int NSPLIT = TMA ? 2 : 3;
+  static constexpr int NRAW = TMA ? 3 : 1;                         // (1: unused by the LDG producer)
+  static constexpr int DATA = NSPLIT * T_STAGE + (TMA ? NRAW * T_RAW : 0);   // LDG 192 KB, TMA 224 KB
+  static constexpr int SMEM = DATA + 1024 + 256;
+  static constexpr int NT = T_PROD + T_DRAIN + 32 + (TMA ? 32 : 0);
+  static_assert(TBN * T_EPI_LD * 4 <= DATA, "epilogue tile must fit in the stage buffers");
+};
 
 struct KParamsT {
   int M, N, K;
@@ -54,6 +62,7 @@ struct KParamsT {
   const float* B;
   int64_t ldb;
   int chunk;      // k-tiles per drained partial sum (0: one TMEM accumulator over the whole k-range)
+  int a3d, b3d;   // TMA producer: MN-inner operand as one 3-D box (extent a multiple of 32)
   int dbg;        // measurement aid (CGGM_TF32_DEBUG): bit 0 = hi*hi products only
   EpilogueT<float> epi;
 };
@@ -226,13 +235,49 @@ __device__ __forceinline__ void store_split(const float4 (&r)[T_PER], uint32_t h
   }
 }
 
-template <bool AK, bool BKI>
-__global__ void __launch_bounds__(T_NT, 1) gemm_tf32x3_kernel(const __grid_constant__ KParamsT P) {
+// raw tile in the TMA SWIZZLE_128B layout (16-byte atoms: chunk c of 128-byte row r at c ^ (r & 7))
+// -> hi / lo in the UMMA layouts (K-major: the same positions; MN-major: 32-byte atoms)
+template <bool KIN>
+__device__ __forceinline__ void convert_split(uint32_t raw, uint32_t hi, uint32_t lo, int tid) {
+#pragma unroll
+  for (int i = 0; i < T_PER; ++i) {
+    const int f = tid + T_PROD * i;
+    uint32_t ro, so;
+    if (KIN) {
+      const int row = f >> 3, c = f & 7;
+      ro = so = row * 128 + ((c ^ (row & 7)) << 4);
+    } else {
+      const int k = f >> 5, mc = f & 31, c = mc & 7;
+      const uint32_t base = (mc >> 3) * 4096 + k * 128;
+      ro = base + ((c ^ (k & 7)) << 4);
+      so = base + (((((c >> 1) ^ (k & 3)) << 1) | (c & 1)) << 4);
+    }
+    float v[4];
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "r"(raw + ro));
+    uint32_t h[4], l[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      h[e] = rna_tf32(v[e]);
+      l[e] = rna_tf32(v[e] - __uint_as_float(h[e]));
+    }
+    sts128(hi + so, h[0], h[1], h[2], h[3]);
+    sts128(lo + so, l[0], l[1], l[2], l[3]);
+  }
+}
+
+template <bool AK, bool BKI, bool TMA>
+__global__ void __launch_bounds__(TCfg<TMA>::NT, 1)
+    gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                       const __grid_constant__ KParamsT P) {
+  using C = TCfg<TMA>;
+  constexpr int TSTAGES = C::NSPLIT;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + T_DATA);
-  uint64_t* empty = full + TSTAGES;
-  uint64_t* cfull = empty + TSTAGES;    // chunk partial in X[b] complete
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATA);
+  uint64_t* empty = full + 3;
+  uint64_t* rfull = empty + 3;           // raw stage landed (TMA)
+  uint64_t* rempty = rfull + 3;          // raw stage converted
+  uint64_t* cfull = rempty + 3;          // chunk partial in X[b] complete
   uint64_t* cempty = cfull + 2;          // X[b] drained
   uint64_t* accf = cempty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
@@ -257,6 +302,10 @@ __global__ void __launch_bounds__(T_NT, 1) gemm_tf32x3_kernel(const __grid_const
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&cfull[b], 1);
       ptx::mbar_init(&cempty[b], T_DRAIN);
+    }
+    for (int r = 0; r < C::NRAW; ++r) {
+      ptx::mbar_init(&rfull[r], 1);
+      ptx::mbar_init(&rempty[r], T_PROD);
     }
     ptx::mbar_init(accf, 1);
     ptx::fence_barrier_init();
@@ -323,7 +372,7 @@ __global__ void __launch_bounds__(T_NT, 1) gemm_tf32x3_kernel(const __grid_const
       umma_commit(accf);
     }
     __syncwarp();
-  } else if (warp < T_DW0) {
+  } else if (warp < T_DW0 && !TMA) {
     // ---- producers (warps 0-7): operand k-tiles, one ahead in registers
     const float* A = P.A;
     const float* B = P.B;
@@ -353,6 +402,52 @@ __global__ void __launch_bounds__(T_NT, 1) gemm_tf32x3_kernel(const __grid_const
         }
       }
     }
+  } else if (warp < T_DW0) {
+    // ---- converters (warps 0-7, TMA producer): raw fp32 stage (TMA SWIZZLE_128B, 16-byte atoms) ->
+    // hi / lo in the UMMA layouts of the split stage
+    const uint32_t rbase = sbase + TSTAGES * T_STAGE;
+    for (int it = 0; it < nkt; ++it) {
+      const int s = it % TSTAGES, rs = it % C::NRAW;
+      ptx::mbar_wait(&rfull[rs], (it / C::NRAW) & 1);
+      if (it >= TSTAGES) ptx::mbar_wait(&empty[s], ((it / TSTAGES) - 1) & 1);
+      const uint32_t st = sbase + s * T_STAGE, rw = rbase + rs * T_RAW;
+      convert_split<AK>(rw, st, st + T_OP, tid);
+      convert_split<BKI>(rw + T_OP, st + 2 * T_OP, st + 3 * T_OP, tid);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      ptx::mbar_arrive(&full[s]);
+      ptx::mbar_arrive(&rempty[rs]);
+    }
+  } else if (TMA && warp == T_TMA_WARP) {
+    // ---- TMA warp: raw k-tiles into the 3-deep ring (K-inner: one {32, 128} box; MN-inner: one 3-D
+    // {32, 32, 4} box, or 32-wide 2-D boxes for a ragged extent; out-of-range k is zero-filled)
+    if (lane == 0 && nkt > 0) {
+      int a_boxes = 0, b_boxes = 0;
+      if (!AK)
+        for (int xb = 0; xb < TBM / 32; ++xb) a_boxes += (m0 + xb * 32 < P.M);
+      if (!BKI)
+        for (int xb = 0; xb < TBN / 32; ++xb) b_boxes += (n0 + xb * 32 < P.N);
+      const uint32_t txb = ((AK || P.a3d) ? T_OP : a_boxes * 4096) + ((BKI || P.b3d) ? T_OP : b_boxes * 4096);
+      ptx::prefetch_tmap(&tmA);
+      ptx::prefetch_tmap(&tmB);
+      uint8_t* rbase = smem + TSTAGES * T_STAGE;
+      for (int j = 0; j < nkt; ++j) {
+        const int rs = j % C::NRAW;
+        if (j >= C::NRAW) ptx::mbar_wait(&rempty[rs], ((j / C::NRAW) - 1) & 1);
+        uint8_t* sa = rbase + rs * T_RAW;
+        uint8_t* sb = sa + T_OP;
+        ptx::mbar_arrive_expect_tx(&rfull[rs], txb);
+        const int k = (kt0 + j) * TBK;
+        if (AK) ptx::tma_load_2d(sa, &tmA, &rfull[rs], k, m0);
+        else if (P.a3d) ptx::tma_load_3d(sa, &tmA, &rfull[rs], 0, k, m0 / 32);
+        else
+          for (int xb = 0; xb < a_boxes; ++xb) ptx::tma_load_2d(sa + xb * 4096, &tmA, &rfull[rs], m0 + xb * 32, k);
+        if (BKI) ptx::tma_load_2d(sb, &tmB, &rfull[rs], k, n0);
+        else if (P.b3d) ptx::tma_load_3d(sb, &tmB, &rfull[rs], 0, k, n0 / 32);
+        else
+          for (int xb = 0; xb < b_boxes; ++xb) ptx::tma_load_2d(sb + xb * 4096, &tmB, &rfull[rs], n0 + xb * 32, k);
+      }
+    }
+    __syncwarp();
   } else {
     // ---- drain warps 8-11 (warp w reads TMEM lanes 32 (w % 4)..: one accumulator row per thread):
     // the running fp32 sum S (TMEM cols 384-511) += each finished chunk, then + D2, then the epilogue
@@ -428,37 +523,47 @@ __global__ void __launch_bounds__(T_NT, 1) gemm_tf32x3_kernel(const __grid_const
   }
 }
 
-template <bool AK, bool BKI>
-void launch_t(Ctx* c, const KParamsT& P, int grid) {
+template <bool AK, bool BKI, bool TMA>
+void launch_t(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KParamsT& P, int grid) {
+  using C = TCfg<TMA>;
   CGGM_ONCE_PER_DEVICE({
-    CGGM_CUDA_CHECK(cudaFuncSetAttribute(gemm_tf32x3_kernel<AK, BKI>, cudaFuncAttributeMaxDynamicSharedMemorySize, T_SMEM));
+    CGGM_CUDA_CHECK(cudaFuncSetAttribute(gemm_tf32x3_kernel<AK, BKI, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM));
   });
   Prof pr(c, c->cur_tag);
-  gemm_tf32x3_kernel<AK, BKI><<<grid, T_NT, T_SMEM, c->stream>>>(P);
+  gemm_tf32x3_kernel<AK, BKI, TMA><<<grid, C::NT, C::SMEM, c->stream>>>(ma, mb, P);
   post_launch(c, "gemm_tf32x3_kernel");
 }
 
 }  // namespace
 
-// Operands 16-byte aligned with ld % 4 == 0 (gemm_f32.cu packs others first); same contract as gemm().
+// Operands 16-byte aligned with ld % 4 == 0 (gemm_f32.cu packs others first) and their TMA maps (the
+// FFMA engine's: K-inner {32, 128} boxes, MN-inner 3-D {32, 32, 4} or 2-D {32, 32}); same contract as
+// gemm().
 void gemm_tf32x3(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
-                 const float* B, int64_t ldb, const EpilogueT<float>& epi, int flags) {
+                 const float* B, int64_t ldb, const EpilogueT<float>& epi, int flags, const CUtensorMap& ma,
+                 const CUtensorMap& mb, int a3d, int b3d) {
   KParamsT P;
   P.M = (int)M; P.N = (int)N; P.K = (int)(K > 0 ? K : 0);
   P.flags = flags;
   P.A = A; P.lda = lda; P.B = B; P.ldb = ldb;
   P.chunk = c->tf32_chunk;
   P.dbg = c->tf32_dbg;
+  P.a3d = a3d; P.b3d = b3d;
   P.epi = epi;
   P.tilesM = (int)((M + TBM - 1) / TBM);
   P.tilesN = (int)((N + TBN - 1) / TBN);
   const int grid = (flags & SYM_LOWER) ? P.tilesN * (P.tilesN + 1) / 2 + (P.tilesM - P.tilesN) * P.tilesN
                                        : P.tilesM * P.tilesN;
-  const bool AK = transA, BKI = !transB;
-  if (AK && BKI) launch_t<true, true>(c, P, grid);
-  else if (AK && !BKI) launch_t<true, false>(c, P, grid);
-  else if (!AK && BKI) launch_t<false, true>(c, P, grid);
-  else launch_t<false, false>(c, P, grid);
+  const bool AK = transA, BKI = !transB, tma = c->tf32_producer == 0;
+#define CGGM_TF32_LAUNCH(a, b)                                     \
+  if (tma) launch_t<a, b, true>(c, ma, mb, P, grid);               \
+  else launch_t<a, b, false>(c, ma, mb, P, grid);
+  if (AK && BKI) { CGGM_TF32_LAUNCH(true, true) }
+  else if (AK && !BKI) { CGGM_TF32_LAUNCH(true, false) }
+  else if (!AK && BKI) { CGGM_TF32_LAUNCH(false, true) }
+  else { CGGM_TF32_LAUNCH(false, false) }
+#undef CGGM_TF32_LAUNCH
 }
 
 }  // namespace cggm

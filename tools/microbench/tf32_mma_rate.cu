@@ -16,13 +16,13 @@ __host__ __device__ constexpr uint32_t idesc_tf32(bool a_mn, bool b_mn, int M, i
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-template <int N, int MODE>   // MODE 0: SS K/K, 1: SS A-MN/B-K, 2: TS (A in TMEM)
+template <int N, int MODE>   // MODE 0: SS K/K, 1: SS A-MN/B-K, 2: TS (A in TMEM); +4: walk 12 distinct operand slices
 __global__ void k(long long* out, int iters) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint32_t slot;
   __shared__ __align__(8) uint64_t bar;
   uint8_t* s = (uint8_t*)(((uintptr_t)sm + 1023) & ~uintptr_t(1023));
-  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) ((float*)s)[i] = 1.0f;
+  for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x) ((float*)s)[i] = 1.0f;
   if (threadIdx.x < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(&slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
@@ -37,13 +37,17 @@ __global__ void k(long long* out, int iters) {
   asm volatile("tcgen05.fence::after_thread_sync;\n");
   const uint32_t tm = slot;
   if (threadIdx.x == 0) {
+    constexpr int M3 = MODE & 3;
+    constexpr bool WALK = MODE & 4;
     const uint32_t a = smem_u32(s), b = a + 32768;
-    const uint64_t da = MODE == 1 ? sdesc(a, 4096, 512, 1) : sdesc(a, 16, 1024, 2);
-    const uint64_t db = sdesc(b, 16, 1024, 2);
-    const uint32_t id = idesc_tf32(MODE == 1, false, 128, N);
+    const uint32_t id = idesc_tf32(M3 == 1, false, 128, N);
     long long t0 = clock64();
     for (int i = 0; i < iters; ++i) {
-      if (MODE == 2) {
+      // WALK: consecutive MMAs read different 4 KB A slices (32 KB region) and 4 KB B slices (+32 KB)
+      const uint32_t off = WALK ? (uint32_t)(i & 7) * 4096u : 0u;
+      const uint64_t da = M3 == 1 ? sdesc(a + off, 4096, 512, 1) : sdesc(a + off, 16, 1024, 2);
+      const uint64_t db = sdesc(b + (WALK ? (uint32_t)(i & 3) * 8192u : 0u), 16, 1024, 2);
+      if (M3 == 2) {
         asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tm),
                      "r"(tm + 256u + (uint32_t)(i & 3) * 8u), "l"(db), "r"(id), "r"(1));
@@ -89,5 +93,10 @@ int main() {
   run<256, 1>("SS A-MN/B-K", 148);
   run<128, 2>("TS (A in TMEM)", 148);
   run<256, 2>("TS (A in TMEM)", 148);
+  run<128, 4>("SS K/K walk", 148);
+  run<256, 4>("SS K/K walk", 148);
+  run<128, 5>("SS A-MN/B-K walk", 148);
+  run<128, 6>("TS walk", 148);
+  run<256, 6>("TS walk", 148);
   return 0;
 }
