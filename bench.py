@@ -672,18 +672,11 @@ def main():
 
     # ---------------------------------------------------------------- e2e through the public API
     e2e = None
-    need_gt = 8.0 * P.p * P.q if args.stream_grad_theta else 0.0
     from paper_1509_04681_b200 import HostCsc, host_colmajor
-    if not args.no_e2e and world == 1 and need_gt > 0.95 * torch.cuda.mem_get_info()[0]:
-        # the host-buffer entry point returns the dense grad_Theta; beside the streamed path's
-        # buffers it does not fit at this size
-        e2e = {"value": None, "unit": UNIT, "skipped": f"cggm_newton_eval_host stores the dense p x q grad_Theta "
-                                                       f"({need_gt / 2**30:.1f} GiB), more than the free device memory "
-                                                       f"beside the streamed evaluation's buffers"}
-    elif not args.no_e2e and world == 1:
+    if not args.no_e2e and world == 1:
         # the public host-buffer entry point: X, Y and the CSCs from page-locked host memory, uploaded
         # by the library (Lambda first, the factorisation overlapping the X / Y transfers), S_yy formed
-        # in the call, the scalar results read back
+        # in the call, the scalar results read back (grad_Theta streamed when the bench streams it)
         Xh, Yh = host_colmajor(P.X), host_colmajor(P.Y)
         Lh, Thh = HostCsc.from_host(lam_h), HostCsc.from_host(th_h)
         h2d = (Xh.numel() + Yh.numel()) * 8 + sum(t.numel() * t.element_size() for c_ in (Lh, Thh)
@@ -691,11 +684,10 @@ def main():
         d2h = ctypes.sizeof(_abi.cggm_objective_out) + ctypes.sizeof(_abi.cggm_active_out) + 8 + 4 + 8
         Syy_e = colmajor_empty(P.q, P.q)
         e2e_bufs = dict(bufs)
-        if args.stream_grad_theta:
-            e2e_bufs["GradT"] = colmajor_empty(P.p, P.q)
 
         def step_e2e():
-            return ctx.cggm_newton_eval_host(Xh, Yh, Lh, Thh, P.lam_L, P.lam_T, True, bufs=e2e_bufs, Syy=Syy_e)
+            return ctx.cggm_newton_eval_host(Xh, Yh, Lh, Thh, P.lam_L, P.lam_T, True, bufs=e2e_bufs, Syy=Syy_e,
+                                             stream_grad_theta=args.stream_grad_theta)
 
         step_e2e()
         step_e2e()
@@ -704,7 +696,8 @@ def main():
         e2e = {"value": e2_steps / (e2ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "steps": e2_steps,
                "includes": "cggm_newton_eval_host: H2D of X, Y, Lambda, Theta from page-locked host memory "
-                           "(overlapped with the factorisation) + S_yy + evaluation + D2H of scalars"}
+                           "(overlapped with the factorisation) + S_yy + evaluation + D2H of scalars"
+                           + ("; grad_Theta streamed (not stored)" if args.stream_grad_theta else "")}
     elif not args.no_e2e:
         # N > 1: every rank uploads its row block of X and Y and the two CSCs from page-locked host
         # memory each step, evaluates through the sharded evaluator (library calls + collectives) and

@@ -412,7 +412,8 @@ cggm_status cggm_newton_eval(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q,
  * asynchronous).  The library uploads into its workspace on an internal copy stream -- Lambda
  * first, so the factorisation starts while X and Y are still in flight -- forms S_yy = Y^T Y / n
  * into Syy (device, q x q, written), and evaluates exactly as cggm_newton_eval; the other
- * outputs (device) and the host scalars are those of cggm_newton_eval.  fp64 ctx only. */
+ * outputs (device) and the host scalars are those of cggm_newton_eval (GradT may be NULL: grad_Theta
+ * streamed into the active-set compaction, never stored).  fp64 ctx only. */
 cggm_status cggm_newton_eval_host(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q, const double* X, int64_t ldx,
                                   const double* Y, int64_t ldy, const cggm_csc* Lambda, const cggm_csc* Theta,
                                   void* Syy, int64_t ldsyy, void* Sigma, int64_t ldsigma, void* Psi, int64_t ldpsi,

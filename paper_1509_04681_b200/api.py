@@ -652,14 +652,19 @@ class Context:
                     active=self._active_result(ao, spec), objective=ob)
 
     def cggm_newton_eval_host(self, Xh, Yh, Lam: HostCsc, Theta: HostCsc, lam_L, lam_T, penalize_diag=True,
-                              tie_eps=1e-9, bufs=None, Syy=None):
+                              tie_eps=1e-9, bufs=None, Syy=None, stream_grad_theta=False):
         """cggm_newton_eval from host buffers (column-major CPU tensors, HostCsc): uploads overlap the
-        factorisation; S_yy is formed on the device into `Syy`.  Returns the cggm_newton_eval dict."""
+        factorisation; S_yy is formed on the device into `Syy`.  Returns the cggm_newton_eval dict.
+        stream_grad_theta: GradT = NULL, grad_Theta compacted chunk by chunk, never stored."""
         self._sync_stream()
         n, p = Xh.shape
         q = Yh.shape[1]
-        bufs = bufs if bufs is not None else {}
+        bufs = dict(bufs) if bufs is not None else {}
+        if stream_grad_theta:
+            bufs["GradT"] = None
         for k, shape in (("Sigma", (q, q)), ("Psi", (q, q)), ("GradL", (q, q)), ("GradT", (p, q))):
+            if k == "GradT" and stream_grad_theta:
+                continue
             if bufs.get(k) is None:
                 bufs[k] = colmajor_empty(*shape, device="cuda", dtype=self.tdtype)
         if Syy is None:
@@ -672,8 +677,8 @@ class Context:
         st = self.lib.cggm_newton_eval_host(
             self.h, n, p, q, _ptr(Xh), ld_of(Xh), _ptr(Yh), ld_of(Yh), ctypes.byref(ls), ctypes.byref(ts),
             _ptr(Syy), ld_of(Syy), _ptr(bufs["Sigma"]), ld_of(bufs["Sigma"]), _ptr(bufs["Psi"]), ld_of(bufs["Psi"]),
-            _ptr(bufs["GradL"]), ld_of(bufs["GradL"]), _ptr(bufs["GradT"]), ld_of(bufs["GradT"]), ctypes.byref(ao),
-            ctypes.byref(eo))
+            _ptr(bufs["GradL"]), ld_of(bufs["GradL"]), _ptr(bufs["GradT"]),
+            ld_of(bufs["GradT"]) if bufs["GradT"] is not None else 1, ctypes.byref(ao), ctypes.byref(eo))
         self.last_active_sizes = (int(ao.m_L), int(ao.m_T))
         self._check(st)
         o = eo.obj

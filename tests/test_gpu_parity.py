@@ -451,3 +451,30 @@ def test_host_buffer_graph_replay_sees_new_host_data(ctx):
     assert outs[4]["objective"]["f"] == ref["objective"]["f"]
     assert outs[4]["active"]["m_L"] == ref["active"]["m_L"] and outs[4]["active"]["m_T"] == ref["active"]["m_T"]
     assert not torch.equal(outs[4]["GradT"], outs[0]["GradT"])
+
+
+def test_host_buffer_evaluation_streamed_grad_theta(ctx):
+    """cggm_newton_eval_host with GradT = NULL (grad_Theta streamed into the compaction, never stored --
+    the form the `sharded` size needs) gives the same lists, statistic and objective as the device-path
+    streamed evaluation."""
+    from paper_1509_04681_b200 import DeviceCsc, HostCsc, host_colmajor, to_device_colmajor
+    from paper_1509_04681_b200.api import newton_evaluation
+    P = problem("medium")
+    label, lam, th = P.points[0]
+    X, Y = to_device_colmajor(P.X), to_device_colmajor(P.Y)
+    Syy, _ = ctx.cggm_covariances(X, Y, want_sxy=False)
+    cap = 4_000_000
+
+    def bufs():
+        return {k2: torch.empty(cap, dtype=torch.int32, device="cuda") for k2 in ("L_row", "L_col", "T_row", "T_col")}
+
+    a = newton_evaluation(ctx, X, Y, Syy, DeviceCsc.from_host(lam), DeviceCsc.from_host(th), P.lam_L, P.lam_T, True,
+                          bufs(), stream_grad_theta=True)
+    a = {kk: (v.clone() if torch.is_tensor(v) else v) for kk, v in a.items()}
+    b = ctx.cggm_newton_eval_host(host_colmajor(P.X), host_colmajor(P.Y), HostCsc.from_host(lam), HostCsc.from_host(th),
+                                  P.lam_L, P.lam_T, True, bufs=bufs(), stream_grad_theta=True)
+    assert b["GradT"] is None
+    for key in ("L_row", "L_col", "T_row", "T_col"):
+        assert torch.equal(a["active"][key], b["active"][key]), key
+    assert a["active"]["subgrad_l1"] == b["active"]["subgrad_l1"]
+    assert a["objective"]["f"] == b["objective"]["f"]
