@@ -63,9 +63,9 @@ HBM_PEAK_GBS = _hbm_peak()
 
 def _dominant_traffic():
     """dram read+write bytes per launch of the largest GEMM launch (lauum), from the committed ncu
-    --set full capture (profiles/r01_ncu_dominant.json); None if absent."""
+    --set full capture (profiles/r02_ncu_dominant.json); None if absent."""
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_dominant.json")))
+        d = json.load(open(os.path.join(ROOT, "profiles", "r02_ncu_dominant.json")))
         return d["dram_read_bytes"] + d["dram_write_bytes"]
     except Exception:
         return None
