@@ -19,9 +19,10 @@ cggm_status cggm_test_gemm(cggm_ctx* ctx, int transA, int transB, int64_t M, int
 cggm_status cggm_test_gemm_f32(cggm_ctx* ctx, int transA, int transB, int64_t M, int64_t N, int64_t K,
                                const float* A, int64_t lda, const float* B, int64_t ldb,
                                float* C, int64_t ldc, double alpha, double beta, int flags);
-/* FP32 contraction engine of an F32 ctx: 0 = 3xTF32 on the tcgen05 tensor cores with the TMA raw-tile
- * producer (default), 1 = SIMT FFMA (also CGGM_F32_ENGINE=ffma at context creation), 2 = 3xTF32 with
- * the register-staged producer (CGGM_TF32_PRODUCER=ldg). */
+/* FP32 contraction engine of an F32 ctx: 0 = 3xTF32 on the tcgen05 tensor cores (the ctx's producer:
+ * CGGM_TF32_PRODUCER at creation), 1 = SIMT FFMA (also CGGM_F32_ENGINE=ffma), 2 / 3 / 4 = 3xTF32 with
+ * the TMA raw-tile producer (SS MMA) / the register-staged producer (SS MMA) / the TS form (A from
+ * TMEM). */
 cggm_status cggm_test_set_f32_engine(cggm_ctx* ctx, int engine);
 /* Force the GEMM CTA tile: bits 0-1: 0 = automatic (small shapes use the 32x32 direct-load kernel),
  * 1 = 128x128 TMA (8 warps), 2 = 64x64 TMA (4 warps), 3 = automatic but K <= 256 small kernel only;

@@ -181,7 +181,10 @@ cggm_status cggm_ctx_create(cggm_ctx** out, int device, cggm_dtype dtype, void* 
   if (const char* e = std::getenv("CGGM_CD_PREFETCH")) c->cd_prefetch = std::atoi(e);
   if (const char* e = std::getenv("CGGM_GRAPH_PROF")) c->graph_prof = std::atoi(e);
   if (const char* e = std::getenv("CGGM_TF32_CHUNK")) c->tf32_chunk = std::atoi(e);
-  if (const char* e = std::getenv("CGGM_TF32_PRODUCER")) c->tf32_producer = std::string(e) == "ldg" ? 1 : 0;
+  if (const char* e = std::getenv("CGGM_TF32_MIN_TILES")) c->tf32_min_tiles = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_TF32_MIN_K")) c->tf32_min_k = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_TF32_PRODUCER"))
+    c->tf32_producer = std::string(e) == "ldg" ? 1 : std::string(e) == "tma" ? 0 : 2;
   if (const char* e = std::getenv("CGGM_FUSE_GRADL")) c->fuse_gradl = std::atoi(e);
   if (const char* e = std::getenv("CGGM_TF32_DEBUG")) c->tf32_dbg = std::atoi(e);
   if (const char* e = std::getenv("CGGM_F32_ENGINE")) c->f32_engine = std::string(e) == "ffma" ? 1 : 0;
@@ -2175,8 +2178,8 @@ extern "C" cggm_status cggm_test_set_tile(cggm_ctx* ctx, int mode) {
 }
 
 extern "C" cggm_status cggm_test_set_f32_engine(cggm_ctx* ctx, int engine) {
-  if (!ctx || engine < 0 || engine > 2) return CGGM_ERR_INVALID_ARG;
+  if (!ctx || engine < 0 || engine > 4) return CGGM_ERR_INVALID_ARG;
   ctx->impl.f32_engine = engine == 1 ? 1 : 0;
-  ctx->impl.tf32_producer = engine == 2 ? 1 : 0;
+  if (engine >= 2) ctx->impl.tf32_producer = engine - 2;   // 2: TMA, 3: register-staged, 4: TS form
   return CGGM_OK;
 }

@@ -313,7 +313,10 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
                           : (P.a3d ? make_map_f_mn3d(c, A, lda, M, Keff) : make_map_f(c, A, lda, M, Keff, 32, FBK));
   CUtensorMap mb = transB ? (P.b3d ? make_map_f_mn3d(c, B, ldb, N, Keff) : make_map_f(c, B, ldb, N, Keff, 32, FBK))
                           : make_map_f(c, B, ldb, Keff, N, FBK, FBN);
-  if (c->f32_engine == 0) {   // 3xTF32 on the tensor cores (gemm_tf32.cu), the same operand maps
+  // 3xTF32 on the tensor cores (gemm_tf32.cu, the same operand maps), except products too small to
+  // amortise its per-tile set-up (TMEM allocation, stage pipeline, drain): those keep the FFMA engine
+  const bool small = (int64_t)P.tilesM * P.tilesN < c->tf32_min_tiles || K < c->tf32_min_k;
+  if (c->f32_engine == 0 && !small) {
     gemm_tf32x3(c, transA, transB, M, N, K, A, lda, B, ldb, epi, flags, ma, mb, P.a3d, P.b3d);
     return;
   }

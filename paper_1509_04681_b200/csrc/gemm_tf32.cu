@@ -237,11 +237,11 @@ __device__ __forceinline__ void store_split(const float4 (&r)[T_PER], uint32_t h
 
 // raw tile in the TMA SWIZZLE_128B layout (16-byte atoms: chunk c of 128-byte row r at c ^ (r & 7))
 // -> hi / lo in the UMMA layouts (K-major: the same positions; MN-major: 32-byte atoms)
-template <bool KIN>
+template <bool KIN, int NTH = T_PROD>
 __device__ __forceinline__ void convert_split(uint32_t raw, uint32_t hi, uint32_t lo, int tid) {
 #pragma unroll
-  for (int i = 0; i < T_PER; ++i) {
-    const int f = tid + T_PROD * i;
+  for (int i = 0; i < TBM * TBK / 4 / NTH; ++i) {
+    const int f = tid + NTH * i;
     uint32_t ro, so;
     if (KIN) {
       const int row = f >> 3, c = f & 7;
@@ -523,6 +523,276 @@ __global__ void __launch_bounds__(TCfg<TMA>::NT, 1)
   }
 }
 
+// ---------------------------------------------------------------- TS form (A from TMEM)
+// The converters write A's hi / lo tiles into TMEM (tcgen05.st, one accumulator row per thread) and
+// only B's into shared memory; the MMA reads A from TMEM (tcgen05.mma ... [a_tmem], b_desc) -- the
+// SS form's A operand reads (half of its 122 B/clk of shared-memory traffic) disappear.  TMEM: chunk
+// accumulators X0, X1 (cols 0-255; hi*hi AND the corrections, chunks of TS_CH k-tiles drained into
+// fp32 registers) and 4 A stages of 64 columns (hi 32 + lo 32) at 256..511.
+constexpr int TS_CONV = 128;                 // converter threads (warps 0-3: TMEM lane quarters)
+constexpr int TS_NS = 4;                     // split stages (TMEM A, shared B)
+constexpr int TS_NRAW = 3;                   // raw TMA stages
+constexpr int TS_BSTAGE = 2 * T_OP;          // B hi + lo
+constexpr int TS_DATA = TS_NS * TS_BSTAGE + TS_NRAW * T_RAW;   // 128 + 96 KB
+static_assert(TBN * T_EPI_LD * 4 <= TS_DATA, "epilogue tile must fit");
+constexpr int TS_SMEM = TS_DATA + 1024 + 256;
+constexpr int TS_NT = TS_CONV + T_DRAIN + 64;  // + MMA warp (8) + TMA warp (9)
+constexpr int TS_DW0 = TS_CONV / 32, TS_MMA = TS_DW0 + 4, TS_TMAW = TS_MMA + 1;
+
+__device__ __forceinline__ void umma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                             uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void tmem_st32_nowait(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
+// row m of the raw A tile (TMA SWIZZLE_128B layout) -> 32 k-values
+template <bool AK>
+__device__ __forceinline__ void raw_a_row(uint32_t raw, int m, float (&v)[32]) {
+  if (AK) {   // K-inner: row m = one 128-byte row, 16-byte chunk c at c ^ (m & 7)
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                   : "=f"(v[4 * c]), "=f"(v[4 * c + 1]), "=f"(v[4 * c + 2]), "=f"(v[4 * c + 3])
+                   : "r"(raw + m * 128 + ((c ^ (m & 7)) << 4)));
+  } else {    // MN-inner: element (m, k) in chunk m / 32, row k, 16-byte chunk ((m % 32) / 4) ^ (k & 7)
+    const uint32_t base = (m >> 5) * 4096 + (m & 3) * 4;
+    const int mc = (m & 31) >> 2;
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+      asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(v[k]) : "r"(raw + base + k * 128 + ((mc ^ (k & 7)) << 4)));
+  }
+}
+
+template <bool AK, bool BKI>
+__global__ void __launch_bounds__(TS_NT, 1)
+    gemm_tf32x3_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                          const __grid_constant__ KParamsT P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TS_DATA);
+  uint64_t* empty = full + TS_NS;
+  uint64_t* rfull = empty + TS_NS;
+  uint64_t* rempty = rfull + TS_NRAW;
+  uint64_t* cfull = rempty + TS_NRAW;
+  uint64_t* cempty = cfull + 2;
+  uint64_t* accf = cempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  int I, J;
+  tile_coords_t(P, blockIdx.x, I, J);
+  const int m0 = I * TBM, n0 = J * TBN;
+  int kbeg = 0, kend = P.K;
+  if (P.flags & A_KGE_M) kbeg = max(kbeg, m0);
+  if (P.flags & B_KGE_N) kbeg = max(kbeg, n0);
+  if (P.flags & A_KLE_M) kend = min(kend, m0 + TBM);
+  if (P.flags & B_KLE_N) kend = min(kend, n0 + TBN);
+  const int kt0 = kbeg / TBK;
+  const int nkt = kend > kbeg ? (kend - kt0 * TBK + TBK - 1) / TBK : 0;
+  const int CH = P.chunk > 0 ? P.chunk : 1 << 30;
+  if (tid == 0) {
+    for (int s = 0; s < TS_NS; ++s) {
+      ptx::mbar_init(&full[s], TS_CONV);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int r = 0; r < TS_NRAW; ++r) {
+      ptx::mbar_init(&rfull[r], 1);
+      ptx::mbar_init(&rempty[r], TS_CONV);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&cfull[b], 1);
+      ptx::mbar_init(&cempty[b], T_DRAIN);
+    }
+    ptx::mbar_init(accf, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == TS_MMA) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(ptx::smem_u32(tmem_slot)),
+                 "n"(T_TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sbase = ptx::smem_u32(smem);
+  const uint32_t rbase = sbase + TS_NS * TS_BSTAGE;
+
+  if (warp == TS_MMA) {
+    if (lane == 0 && nkt > 0) {
+      constexpr uint32_t idesc = idesc_tf32(false, !BKI, TBM, TBN);
+      for (int j = 0; j < nkt; ++j) {
+        const int s = j % TS_NS;
+        const int c = j / CH;
+        const bool first = (j % CH == 0);
+        if (first && c >= 2) {
+          ptx::mbar_wait(&cempty[c & 1], ((c >> 1) - 1) & 1);
+          tc_fence_after();
+        }
+        ptx::mbar_wait(&full[s], (j / TS_NS) & 1);
+        tc_fence_after();
+        const uint32_t b_hi = sbase + s * TS_BSTAGE, b_lo = b_hi + T_OP;
+        const uint32_t a_hi = tmem + 256u + (uint32_t)s * 64u, a_lo = a_hi + 32u;
+        const uint32_t X = tmem + ((c & 1) ? 128u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < TBK / 8; ++kk) {
+          const uint32_t ob = kk * (BKI ? 32 : 1024);
+          const uint32_t lb = BKI ? 16 : 4096, sb = BKI ? 1024 : 512;
+          const uint64_t yb = BKI ? 2 : 1;
+          const uint64_t dbh = sdesc(b_hi + ob, lb, sb, yb), dbl = sdesc(b_lo + ob, lb, sb, yb);
+          umma_tf32_ts(X, a_lo + kk * 8u, dbh, idesc, (first && kk == 0) ? 0u : 1u);
+          umma_tf32_ts(X, a_hi + kk * 8u, dbl, idesc, 1u);
+          umma_tf32_ts(X, a_hi + kk * 8u, dbh, idesc, 1u);
+        }
+        umma_commit(&empty[s]);
+        if (j % CH == CH - 1 || j == nkt - 1) umma_commit(&cfull[c & 1]);
+      }
+      umma_commit(accf);
+    }
+    __syncwarp();
+  } else if (warp == TS_TMAW) {
+    if (lane == 0 && nkt > 0) {
+      int a_boxes = 0, b_boxes = 0;
+      if (!AK)
+        for (int xb = 0; xb < TBM / 32; ++xb) a_boxes += (m0 + xb * 32 < P.M);
+      if (!BKI)
+        for (int xb = 0; xb < TBN / 32; ++xb) b_boxes += (n0 + xb * 32 < P.N);
+      const uint32_t txb = ((AK || P.a3d) ? T_OP : a_boxes * 4096) + ((BKI || P.b3d) ? T_OP : b_boxes * 4096);
+      ptx::prefetch_tmap(&tmA);
+      ptx::prefetch_tmap(&tmB);
+      uint8_t* rb = smem + TS_NS * TS_BSTAGE;
+      for (int j = 0; j < nkt; ++j) {
+        const int rs = j % TS_NRAW;
+        if (j >= TS_NRAW) ptx::mbar_wait(&rempty[rs], ((j / TS_NRAW) - 1) & 1);
+        uint8_t* sa = rb + rs * T_RAW;
+        uint8_t* sbp = sa + T_OP;
+        ptx::mbar_arrive_expect_tx(&rfull[rs], txb);
+        const int k = (kt0 + j) * TBK;
+        if (AK) ptx::tma_load_2d(sa, &tmA, &rfull[rs], k, m0);
+        else if (P.a3d) ptx::tma_load_3d(sa, &tmA, &rfull[rs], 0, k, m0 / 32);
+        else
+          for (int xb = 0; xb < a_boxes; ++xb) ptx::tma_load_2d(sa + xb * 4096, &tmA, &rfull[rs], m0 + xb * 32, k);
+        if (BKI) ptx::tma_load_2d(sbp, &tmB, &rfull[rs], k, n0);
+        else if (P.b3d) ptx::tma_load_3d(sbp, &tmB, &rfull[rs], 0, k, n0 / 32);
+        else
+          for (int xb = 0; xb < b_boxes; ++xb) ptx::tma_load_2d(sbp + xb * 4096, &tmB, &rfull[rs], n0 + xb * 32, k);
+      }
+    }
+    __syncwarp();
+  } else if (warp < TS_DW0) {
+    // ---- converters: A row (32 k) of this thread's TMEM lane -> hi / lo columns of the stage; B tile
+    // -> hi / lo in shared memory
+    const int m = warp * 32 + lane;
+    const uint32_t lanebase = tmem + ((uint32_t)(warp * 32) << 16);
+    for (int it = 0; it < nkt; ++it) {
+      const int s = it % TS_NS, rs = it % TS_NRAW;
+      ptx::mbar_wait(&rfull[rs], (it / TS_NRAW) & 1);
+      if (it >= TS_NS) {
+        ptx::mbar_wait(&empty[s], ((it / TS_NS) - 1) & 1);
+        tc_fence_after();
+      }
+      const uint32_t rw = rbase + rs * T_RAW;
+      {
+        float v[32];
+        raw_a_row<AK>(rw, m, v);
+        uint32_t h[32], l[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          h[e] = rna_tf32(v[e]);
+          l[e] = rna_tf32(v[e] - __uint_as_float(h[e]));
+        }
+        const uint32_t ac = lanebase + 256u + (uint32_t)s * 64u;
+        tmem_st32_nowait(ac, h);
+        tmem_st32_nowait(ac + 32u, l);
+      }
+      const uint32_t st = sbase + s * TS_BSTAGE;
+      convert_split<BKI, TS_CONV>(rw + T_OP, st, st + T_OP, tid);
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      tc_fence_before();
+      ptx::mbar_arrive(&full[s]);
+      ptx::mbar_arrive(&rempty[rs]);
+    }
+  } else {
+    // ---- drain warps 4-7: chunk partials (TMEM X0 / X1) added into fp32 registers, then the epilogue
+    const int dt = tid - TS_CONV;
+    const int row = (warp - TS_DW0) * 32 + lane;
+    const uint32_t lanebase = tmem + ((uint32_t)((warp - TS_DW0) * 32) << 16);
+    float acc[TBN];
+#pragma unroll
+    for (int j = 0; j < TBN; ++j) acc[j] = 0.f;
+    const int nch = nkt > 0 ? (nkt + CH - 1) / CH : 0;
+    for (int c = 0; c < nch; ++c) {
+      ptx::mbar_wait(&cfull[c & 1], (c >> 1) & 1);
+      tc_fence_after();
+      const uint32_t xa = lanebase + ((c & 1) ? 128u : 0u);
+#pragma unroll
+      for (int g = 0; g < TBN / 32; ++g) {
+        uint32_t v[32];
+        tmem_ld32(xa + 32u * g, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[32 * g + j] += __uint_as_float(v[j]);
+      }
+      tc_fence_before();
+      ptx::mbar_arrive(&cempty[c & 1]);
+    }
+    if (nkt > 0) {
+      ptx::mbar_wait(accf, 0);   // every MMA done: the shared stage buffers are free for the tile
+      tc_fence_after();
+    }
+    float* Cs = reinterpret_cast<float*>(smem);
+#pragma unroll
+    for (int j = 0; j < TBN; ++j) Cs[j * T_EPI_LD + row] = acc[j];
+    asm volatile("bar.sync 1, %0;\n" ::"n"(T_DRAIN) : "memory");
+    const bool diag = (P.flags & SYM_LOWER) && I == J;
+    for (int idx = dt; idx < TBM * TBN; idx += T_DRAIN) {
+      const int mm = idx % TBM, nl = idx / TBM;
+      const int mr = m0 + mm, n = n0 + nl;
+      if (mr >= P.M || n >= P.N) continue;
+      if (diag && mr < n) continue;
+      epi_apply_t(P.epi, mr, n, Cs[nl * T_EPI_LD + mm]);
+    }
+    if (P.flags & SYM_MIRROR) {
+      for (int idx = dt; idx < TBM * TBN; idx += T_DRAIN) {
+        const int nl = idx % TBN, mm = idx / TBN;
+        const int mr = m0 + mm, n = n0 + nl;
+        if (mr >= P.M || n >= P.N) continue;
+        if (diag && mr <= n) continue;
+        epi_apply_t(P.epi, n, mr, Cs[nl * T_EPI_LD + mm]);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == TS_MMA) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(T_TMEM_COLS) : "memory");
+  }
+}
+
+template <bool AK, bool BKI>
+void launch_ts(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KParamsT& P, int grid) {
+  CGGM_ONCE_PER_DEVICE({
+    CGGM_CUDA_CHECK(cudaFuncSetAttribute(gemm_tf32x3_ts_kernel<AK, BKI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         TS_SMEM));
+  });
+  Prof pr(c, c->cur_tag);
+  gemm_tf32x3_ts_kernel<AK, BKI><<<grid, TS_NT, TS_SMEM, c->stream>>>(ma, mb, P);
+  post_launch(c, "gemm_tf32x3_ts_kernel");
+}
+
 template <bool AK, bool BKI, bool TMA>
 void launch_t(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KParamsT& P, int grid) {
   using C = TCfg<TMA>;
@@ -555,9 +825,11 @@ void gemm_tf32x3(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t
   P.tilesN = (int)((N + TBN - 1) / TBN);
   const int grid = (flags & SYM_LOWER) ? P.tilesN * (P.tilesN + 1) / 2 + (P.tilesM - P.tilesN) * P.tilesN
                                        : P.tilesM * P.tilesN;
-  const bool AK = transA, BKI = !transB, tma = c->tf32_producer == 0;
+  const bool AK = transA, BKI = !transB, tma = c->tf32_producer == 0, ts = c->tf32_producer == 2;
+  if (ts && P.chunk > 2) P.chunk = 2;   // the TS form accumulates all three products per chunk: shorter chunks
 #define CGGM_TF32_LAUNCH(a, b)                                     \
-  if (tma) launch_t<a, b, true>(c, ma, mb, P, grid);               \
+  if (ts) launch_ts<a, b>(c, ma, mb, P, grid);                     \
+  else if (tma) launch_t<a, b, true>(c, ma, mb, P, grid);          \
   else launch_t<a, b, false>(c, ma, mb, P, grid);
   if (AK && BKI) { CGGM_TF32_LAUNCH(true, true) }
   else if (AK && !BKI) { CGGM_TF32_LAUNCH(true, false) }

@@ -32,17 +32,17 @@ def ctx32():
     return Context(0, dtype="f32")
 
 
-ENGINES = {"tf32x3": 0, "ffma": 1, "tf32x3_ldg": 2}
+ENGINES = {"tf32x3": 2, "ffma": 1, "tf32x3_ldg": 3, "tf32x3_ts": 4}
 # 3xTF32: each product carries ~2^-22 relative error (the split's rounding and the dropped lo*lo);
 # FFMA: fp32 rounding only
-GEMM_TOL = {"tf32x3": 5e-6, "ffma": 2e-6, "tf32x3_ldg": 5e-6}
+GEMM_TOL = {"tf32x3": 5e-6, "ffma": 2e-6, "tf32x3_ldg": 5e-6, "tf32x3_ts": 5e-6}
 
 
 @pytest.fixture(params=list(ENGINES))
 def engine(request, ctx32):
     ctx32._check(ctx32.lib.cggm_test_set_f32_engine(ctx32.h, ENGINES[request.param]))
     yield request.param
-    ctx32._check(ctx32.lib.cggm_test_set_f32_engine(ctx32.h, 0))
+    ctx32._check(ctx32.lib.cggm_test_set_f32_engine(ctx32.h, 4))
 
 
 def run_f32(ctx, tA, tB, A, B, C0, alpha, beta, flags, M, N, K):
@@ -122,8 +122,8 @@ def oracle_point(name, k):
 
 @pytest.mark.parametrize("name,k", [("tiny", 1), ("small", 0), ("small", 1), ("medium", 0)])
 def test_fp32_parity(ctx32, engine, name, k):
-    if engine == "tf32x3_ldg" and name != "small":
-        pytest.skip("the register-staged producer's parity at small only (same MMA / drain / epilogue)")
+    if engine in ("tf32x3", "tf32x3_ldg") and name != "small":
+        pytest.skip("the SS-form producers' parity at small only (the default TS form runs every size)")
     from paper_1509_04681_b200 import DeviceCsc, to_device_colmajor
     from paper_1509_04681_b200.api import newton_evaluation
     P, ref = oracle_point(name, k)

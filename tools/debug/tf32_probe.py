@@ -9,7 +9,7 @@ from paper_1509_04681_b200.api import colmajor_empty, ld_of
 ctx = Context(0, dtype="f32")
 
 
-def run(tA, tB, A, B, M, N, K, eng=0):
+def run(tA, tB, A, B, M, N, K, eng=int(os.environ.get('TF32_ENGINE', '0'))):
     ctx._check(ctx.lib.cggm_test_set_f32_engine(ctx.h, eng))
     ts = []
     for a in (A, B, np.zeros((M, N))):

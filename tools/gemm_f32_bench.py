@@ -10,7 +10,7 @@ from paper_1509_04681_b200 import Context  # noqa
 from paper_1509_04681_b200.api import colmajor_empty, ld_of  # noqa
 
 ctx = Context(0, dtype="f32")
-for eng, (tA, tB, M, N, K) in [(e, s) for e in (0, 1) for s in [
+for eng, (tA, tB, M, N, K) in [(e, s) for e in (2, 4, 1) for s in [
         (1, 0, 8192, 8192, 8192), (0, 1, 8192, 8192, 8192), (0, 0, 8192, 8192, 8192), (1, 1, 8192, 8192, 8192),
         (1, 0, 40000, 20000, 1000), (0, 0, 1000, 20000, 20000)]]:
     ctx._check(ctx.lib.cggm_test_set_f32_engine(ctx.h, eng))
@@ -30,4 +30,4 @@ for eng, (tA, tB, M, N, K) in [(e, s) for e in (0, 1) for s in [
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 3
-    print(f"{('tf32x3', 'ffma')[eng]} tA={tA} tB={tB} {M}x{N}x{K}: {ms:.3f} ms {2.0 * M * N * K / ms / 1e9:.2f} TFLOP/s", flush=True)
+    print(f"{({1: 'ffma', 2: 'tf32x3', 3: 'tf32x3_ldg', 4: 'tf32x3_ts'})[eng]} tA={tA} tB={tB} {M}x{N}x{K}: {ms:.3f} ms {2.0 * M * N * K / ms / 1e9:.2f} TFLOP/s", flush=True)
