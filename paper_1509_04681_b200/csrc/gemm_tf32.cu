@@ -826,7 +826,7 @@ void gemm_tf32x3(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t
   const int grid = (flags & SYM_LOWER) ? P.tilesN * (P.tilesN + 1) / 2 + (P.tilesM - P.tilesN) * P.tilesN
                                        : P.tilesM * P.tilesN;
   const bool AK = transA, BKI = !transB, tma = c->tf32_producer == 0, ts = c->tf32_producer == 2;
-  if (ts && P.chunk > 2) P.chunk = 2;   // the TS form accumulates all three products per chunk: shorter chunks
+  if (ts) P.chunk = c->tf32_ts_chunk;   // the TS form accumulates all three products per chunk: shorter chunks
 #define CGGM_TF32_LAUNCH(a, b)                                     \
   if (ts) launch_ts<a, b>(c, ma, mb, P, grid);                     \
   else if (tma) launch_t<a, b, true>(c, ma, mb, P, grid);          \
