@@ -54,6 +54,11 @@ def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB
 
 
 if __name__ == "__main__":
+    # --debug: device-side invariant checks (-DCGGM_DEBUG, CGGM_DASSERT) into lib/debug/libcggm.so; load it
+    # with CGGM_LIB=<path> and run with CGGM_SYNC_CHECK=1 to attribute a fault to its kernel
+    if "--debug" in sys.argv:
+        sys.argv += ["-DCGGM_DEBUG", "--out=" + os.path.join(LIBDIR, "debug", "libcggm.so")]
+        os.makedirs(os.path.join(LIBDIR, "debug"), exist_ok=True)
     defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
     outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
     print(build(force="--force" in sys.argv or bool(defs), verbose="-v" in sys.argv, defines=defs,

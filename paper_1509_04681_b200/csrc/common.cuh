@@ -115,6 +115,7 @@ struct Ctx {
   int persist_tpc = 0;   // CGGM_PERSIST_TPC: tiles per CTA of the persistent warp-specialised GEMM (0: off)   // CGGM_NO_VEC_EPI=1: scalar GEMM epilogue everywhere (A/B)      // CGGM_ACT_ONEPASS=1: Lambda list by the single-pass look-back kernel (not the split one)    // test hook (CGGM_NO_ACTIVE_VEC=1): scalar active-set kernel only   // test hook (CGGM_NO_SMALL_ASYNC=1): direct-load small kernel only
   int fuse_gradl = 0;   // CGGM_FUSE_GRADL=1: grad_Lambda as the Psi GEMM's second epilogue output (measured: the
                         // two-input mirrored epilogue costs the K = n GEMM more than the 1.8 ms pass it saves)
+  int sync_check = 0;   // CGGM_SYNC_CHECK=1: synchronise after every launch (fault localisation, see post_launch)
   int tf32_dbg = 0;     // CGGM_TF32_DEBUG (gemm_tf32.cu measurement aid)
   int tf32_producer = 2;   // 3xTF32 form (CGGM_TF32_PRODUCER): 2 = TS (A hi / lo in TMEM, B in shared memory; default),
                            // 0 = SS with the TMA raw ring + converters ("tma"), 1 = SS with register-staged loads ("ldg")
@@ -265,11 +266,32 @@ struct CudaError {
   } while (0)
 
 // After every launch: count it and surface launch errors.
+// CGGM_SYNC_CHECK=1 (read at context creation; the stand-in for compute-sanitizer, which this pool
+// does not run): synchronise the stream after every launch outside graph capture, so an asynchronous
+// fault is reported by the call and kernel that caused it.
 inline void post_launch(Ctx* c, const char* what) {
   c->launches++;
   cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && c->sync_check) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(c->stream, &cs);
+    if (cs == cudaStreamCaptureStatusNone) e = cudaStreamSynchronize(c->stream);
+  }
   if (e != cudaSuccess) throw CudaError{CGGM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
 }
+
+// Device-side checks of a debug build (build.py --debug: -DCGGM_DEBUG): a violated invariant traps
+// (the launch then fails with an illegal-instruction error naming the kernel under CGGM_SYNC_CHECK).
+#ifdef CGGM_DEBUG
+#define CGGM_DASSERT(cond) \
+  do {                     \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define CGGM_DASSERT(cond) \
+  do {                     \
+  } while (0)
+#endif
 
 // ------------------------------------------------------------------ dense views
 template <typename T>

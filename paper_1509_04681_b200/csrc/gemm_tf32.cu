@@ -580,6 +580,7 @@ template <bool AK, bool BKI>
 __global__ void __launch_bounds__(TS_NT, 1)
     gemm_tf32x3_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ KParamsT P) {
+  CGGM_DASSERT(blockDim.x == TS_NT);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + TS_DATA);

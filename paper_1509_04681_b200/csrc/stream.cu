@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(SPMM_ROWS / 2) k_spmm_x_theta2(const T* __rest
     const int cnt = (int)((b - t0) < SPMM_ROWS ? (b - t0) : SPMM_ROWS);
     __syncthreads();
     for (int e = threadIdx.x; e < cnt; e += NT) {
+      CGGM_DASSERT(rowidx[t0 + e] >= 0);
       offs[e] = (int64_t)rowidx[t0 + e] * ldx;
       vals[e] = val[t0 + e];
     }
