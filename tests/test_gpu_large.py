@@ -193,3 +193,19 @@ def test_large_full_matrices_and_lists(run_large):
     assert rel["Sigma"] <= 1e-12
     for k in ("Psi", "GradL", "GradT"):
         assert rel[k] <= REL_F, (k, rel[k])
+
+
+def test_large_matches_the_full_oracle_evaluation(run_large):
+    """The whole `large` evaluation against one complete run of the CPU oracle itself (not closed forms):
+    objective, log-det, |S_Lambda|, |S_Theta| and ||grad^S||_1 from tests/golden/large_oracle_full.json
+    (written by tools/oracle_full_eval.py, which calls only oracle/ on the same seeded inputs)."""
+    import json
+    import os
+    P, res, _ = run_large
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "large_oracle_full.json")))
+    a = res["active"]
+    assert res["objective"]["f"] == pytest.approx(g["f"], rel=1e-10)
+    assert res["logdet"] == pytest.approx(g["logdet"], rel=1e-12)
+    assert a["ties_L"] == 0 and a["ties_T"] == 0
+    assert (a["m_L"], a["m_T"]) == (g["m_L"], g["m_T"])
+    assert a["subgrad_l1"] == pytest.approx(g["subgrad_l1"], rel=1e-9)
