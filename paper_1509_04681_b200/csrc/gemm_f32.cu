@@ -258,6 +258,115 @@ CUtensorMap make_map_f_mn3d(Ctx* c, const float* ptr, int64_t ld, int64_t X, int
   return m;
 }
 
+// ------------------------------------------------------------------ small-shape FP32 GEMM
+// The FP32 counterpart of gemm.cu's gemm_small_async_kernel, with the same routing: K <= 256 with
+// min(M, N) <= 128 (the bottom of the Cholesky recursion) and mid-size products whose 64-tile grid
+// is smaller than the SM count with K <= small_kmax.  Latency-bound work: 32x32 CTA tiles (16x the
+// CTAs of the 128x128 engines), 128 threads with a 2x4 FFMA register tile each (rows mi, mi+16;
+// columns nj, nj+8, nj+16, nj+24), the whole k-range of a CTA streamed through a 4-stage cp.async
+// ring of 16-byte chunks (no tensor-map fetch, no mbarrier prologue, no TMEM set-up).  Shared tiles
+// keep each operand's global contiguity.  fp32 accumulation in k order, like the FFMA engine.
+constexpr int SF_T = 32, SF_KC = 32, SF_LD = SF_T + 4, SF_STAGES = 4;
+constexpr int SF_TILE = SF_T * SF_LD;                   // floats per operand tile
+constexpr int SF_SMEM = SF_STAGES * 2 * SF_TILE * 4;   // 36 KB
+
+struct KParamsSF {
+  int M, N, K, flags;
+  EpilogueT<float> epi;
+};
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(128) gemm_small_f32_kernel(const float* __restrict__ A, int64_t lda,
+                                                              const float* __restrict__ B, int64_t ldb,
+                                                              const KParamsSF P) {
+  extern __shared__ __align__(16) float sf_smem[];
+  const int m0 = blockIdx.y * SF_T, n0 = blockIdx.x * SF_T;
+  if ((P.flags & SYM_LOWER) && m0 + SF_T - 1 < n0) return;   // tile strictly above the diagonal
+  int kbeg = 0, kend = P.K;
+  if (P.flags & A_KGE_M) kbeg = max(kbeg, m0);
+  if (P.flags & B_KGE_N) kbeg = max(kbeg, n0);
+  if (P.flags & A_KLE_M) kend = min(kend, m0 + SF_T);
+  if (P.flags & B_KLE_N) kend = min(kend, n0 + SF_T);
+  const int tid = threadIdx.x, mi = tid & 15, nj = tid >> 4;
+  const int nchunks = kend > kbeg ? (kend - kbeg + SF_KC - 1) / SF_KC : 0;
+  // chunk -> stage: A tile [k][m] (!TA, m contiguous) or [m][k] (TA); B tile [k][n] (TB) or [n][k];
+  // elements past kend / M / N are zero-filled by the copy's byte count
+  auto issue = [&](int chunk) {
+    const int kc = kbeg + chunk * SF_KC;
+    float* as = sf_smem + (chunk % SF_STAGES) * 2 * SF_TILE;
+    float* bs = as + SF_TILE;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int pidx = tid + 128 * u, row = pidx >> 3, c4 = 4 * (pidx & 7);
+      {
+        const int k = TA ? kc + c4 : kc + row, m = TA ? m0 + row : m0 + c4;
+        int bytes;
+        if (TA) bytes = (m < P.M) ? min(max(kend - k, 0), 4) * 4 : 0;
+        else bytes = (k < kend) ? min(max(P.M - m, 0), 4) * 4 : 0;
+        const float* src = bytes ? (TA ? A + k + (int64_t)m * lda : A + m + (int64_t)k * lda) : A;
+        ptx::cp_async16(as + row * SF_LD + c4, src, bytes);
+      }
+      {
+        const int k = TB ? kc + row : kc + c4, n = TB ? n0 + c4 : n0 + row;
+        int bytes;
+        if (TB) bytes = (k < kend) ? min(max(P.N - n, 0), 4) * 4 : 0;
+        else bytes = (n < P.N) ? min(max(kend - k, 0), 4) * 4 : 0;
+        const float* src = bytes ? (TB ? B + n + (int64_t)k * ldb : B + k + (int64_t)n * ldb) : B;
+        ptx::cp_async16(bs + row * SF_LD + c4, src, bytes);
+      }
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < SF_STAGES - 1; ++s) {
+    if (s < nchunks) issue(s);
+    ptx::cp_async_commit();
+  }
+  float acc[2][4];
+#pragma unroll
+  for (int f = 0; f < 2; ++f)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[f][j] = 0.f;
+  for (int i = 0; i < nchunks; ++i) {
+    ptx::cp_async_wait<SF_STAGES - 2>();
+    __syncthreads();   // chunk i landed for every thread; stage (i-1) % S is free
+    if (i + SF_STAGES - 1 < nchunks) issue(i + SF_STAGES - 1);
+    ptx::cp_async_commit();
+    const float* as = sf_smem + (i % SF_STAGES) * 2 * SF_TILE;
+    const float* bs = as + SF_TILE;
+#pragma unroll 8
+    for (int k = 0; k < SF_KC; ++k) {
+      float a[2], b[4];
+#pragma unroll
+      for (int f = 0; f < 2; ++f) a[f] = TA ? as[(mi + 16 * f) * SF_LD + k] : as[k * SF_LD + mi + 16 * f];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = TB ? bs[k * SF_LD + nj + 8 * j] : bs[(nj + 8 * j) * SF_LD + k];
+#pragma unroll
+      for (int f = 0; f < 2; ++f)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[f][j] = fmaf(a[f], b[j], acc[f][j]);
+    }
+  }
+  ptx::cp_async_wait<0>();
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+      const int m = m0 + mi + 16 * f, n = n0 + nj + 8 * j;
+      if (m >= P.M || n >= P.N) continue;
+      if ((P.flags & SYM_LOWER) && m < n) continue;
+      epi_apply_f(P.epi, m, n, acc[f][j]);
+      if ((P.flags & SYM_MIRROR) && m > n) epi_apply_f(P.epi, n, m, acc[f][j]);
+    }
+}
+
+template <bool TA, bool TB>
+void launch_small_f(Ctx* c, const float* A, int64_t lda, const float* B, int64_t ldb, const KParamsSF& P) {
+  dim3 grid((unsigned)((P.N + SF_T - 1) / SF_T), (unsigned)((P.M + SF_T - 1) / SF_T));
+  Prof pr(c, c->cur_tag);
+  gemm_small_f32_kernel<TA, TB><<<grid, 128, SF_SMEM, c->stream>>>(A, lda, B, ldb, P);
+  post_launch(c, "gemm_small_f32_kernel");
+}
+
 template <bool AK, bool BKI>
 void launch_f(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KParamsF& P, int grid) {
   CGGM_ONCE_PER_DEVICE({
@@ -277,6 +386,27 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
   if (M <= 0 || N <= 0) return;
   if (M > (1LL << 30) || N > (1LL << 30) || K > (1LL << 30))
     throw CudaError{CGGM_ERR_UNSUPPORTED, "gemm dimension too large"};
+  if ((flags & SYM_LOWER) && (M < N || ((flags & SYM_MIRROR) && M != N)))
+    throw CudaError{CGGM_ERR_SHAPE, "SYM_LOWER gemm needs M >= N (M == N with SYM_MIRROR)"};
+  {  // small shapes and mid-size products with a sub-wave 64-tile grid: the 32x32 cp.async kernel
+    // (an output aliasing an operand -- an in-place B := B X^T with N <= 64 -- needs one CTA per
+    // row panel, which only the 128-wide kernels guarantee)
+    const bool aliased = epi.out1 == A || epi.out1 == B || (epi.out2 && (epi.out2 == A || epi.out2 == B));
+    const int64_t tiles64 = ((M + 63) / 64) * ((N + 63) / 64);
+    const bool small_shape = K <= 256 && (M <= 128 || N <= 128);
+    const bool mid_shape = K <= c->small_kmax && tiles64 < c->num_sms;
+    const bool aligned = tma_ok_f(A, lda) && tma_ok_f(B, ldb);
+    if ((small_shape || mid_shape) && K > 0 && aligned && !aliased && !c->no_small_async && c->force_tile != 1 &&
+        c->force_tile != 2) {
+      KParamsSF S;
+      S.M = (int)M; S.N = (int)N; S.K = (int)K; S.flags = flags; S.epi = epi;
+      if (transA && transB) launch_small_f<true, true>(c, A, lda, B, ldb, S);
+      else if (transA) launch_small_f<true, false>(c, A, lda, B, ldb, S);
+      else if (transB) launch_small_f<false, true>(c, A, lda, B, ldb, S);
+      else launch_small_f<false, false>(c, A, lda, B, ldb, S);
+      return;
+    }
+  }
   static float* dummy = nullptr;
   if (K <= 0) {
     if (!dummy) CGGM_CUDA_CHECK(cudaMalloc(&dummy, 32 * 32 * 4));
@@ -297,8 +427,6 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
     CGGM_CUDA_CHECK(cudaMemcpy2DAsync(pk, ld * 4, B, ldb * 4, brows * 4, bcols, cudaMemcpyDeviceToDevice, c->stream));
     B = pk; ldb = ld;
   }
-  if ((flags & SYM_LOWER) && (M < N || ((flags & SYM_MIRROR) && M != N)))
-    throw CudaError{CGGM_ERR_SHAPE, "SYM_LOWER gemm needs M >= N (M == N with SYM_MIRROR)"};
   KParamsF P;
   P.M = (int)M; P.N = (int)N; P.K = (int)(K > 0 ? K : 0);
   P.flags = flags;

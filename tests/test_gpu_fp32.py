@@ -32,10 +32,19 @@ def ctx32():
     return Context(0, dtype="f32")
 
 
-ENGINES = {"tf32x3": 2, "ffma": 1, "tf32x3_ldg": 3, "tf32x3_ts": 4}
+ENGINES = {"tf32x3": 2, "ffma": 1, "tf32x3_ldg": 3, "tf32x3_ts": 4, "small": 4}
 # 3xTF32: each product carries ~2^-22 relative error (the split's rounding and the dropped lo*lo);
-# FFMA: fp32 rounding only
-GEMM_TOL = {"tf32x3": 5e-6, "ffma": 2e-6, "tf32x3_ldg": 5e-6, "tf32x3_ts": 5e-6}
+# FFMA (the 128x128 engine and the 32x32 small-shape kernel): fp32 rounding only
+GEMM_TOL = {"tf32x3": 5e-6, "ffma": 2e-6, "tf32x3_ldg": 5e-6, "tf32x3_ts": 5e-6, "small": 2e-6}
+
+
+def tile_mode(engine, mode):
+    """cggm_test_set_tile mode for a GEMM test: force_tile 1 keeps every product on the named engine
+    (no small-shape routing); "small" keeps the default routing, so the small and mid-size shapes
+    below run the 32x32 cp.async kernel (bit 4: 2-D TMA boxes, irrelevant to that kernel)."""
+    if engine == "small":
+        return mode & 4
+    return mode
 
 
 @pytest.fixture(params=list(ENGINES))
@@ -65,7 +74,7 @@ def run_f32(ctx, tA, tB, A, B, C0, alpha, beta, flags, M, N, K):
 @pytest.mark.parametrize("M,N,K", [(1, 1, 1), (37, 45, 29), (300, 260, 171), (256, 64, 300), (513, 129, 1000)])
 @pytest.mark.parametrize("mode", [1, 5])   # 3-D / 2-D TMA boxes for MN-inner operands (FFMA engine)
 def test_f32_gemm_variants(ctx32, engine, tA, tB, M, N, K, mode):
-    ctx32._check(ctx32.lib.cggm_test_set_tile(ctx32.h, mode))
+    ctx32._check(ctx32.lib.cggm_test_set_tile(ctx32.h, tile_mode(engine, mode)))
     rng = np.random.default_rng(M + 3 * N + 7 * K)
     A = rng.standard_normal((K, M) if tA else (M, K)).astype(np.float32).astype(np.float64)
     B = rng.standard_normal((N, K) if tB else (K, N)).astype(np.float32).astype(np.float64)
@@ -84,11 +93,23 @@ def test_f32_gemm_triangular(ctx32, engine, flags):
     B = rng.standard_normal((n, n)).astype(np.float32).astype(np.float64)
     A = np.tril(A) if flags & A_KLE_M else np.triu(A) if flags & A_KGE_M else A
     B = np.triu(B) if flags & B_KLE_N else np.tril(B) if flags & B_KGE_N else B
-    out = run_f32(ctx32, False, False, A, B, np.zeros((n, n)), 1.0, 0.0, flags, n, n, n)
+    ctx32._check(ctx32.lib.cggm_test_set_tile(ctx32.h, tile_mode(engine, 1)))
+    try:
+        out = run_f32(ctx32, False, False, A, B, np.zeros((n, n)), 1.0, 0.0, flags, n, n, n)
+    finally:
+        ctx32._check(ctx32.lib.cggm_test_set_tile(ctx32.h, 0))
     assert relf(out, A @ B) < GEMM_TOL[engine]
 
 
 def test_f32_gemm_sym_and_trapezoid(ctx32, engine):
+    ctx32._check(ctx32.lib.cggm_test_set_tile(ctx32.h, tile_mode(engine, 1)))
+    try:
+        _sym_and_trapezoid(ctx32, engine)
+    finally:
+        ctx32._check(ctx32.lib.cggm_test_set_tile(ctx32.h, 0))
+
+
+def _sym_and_trapezoid(ctx32, engine):
     rng = np.random.default_rng(3)
     q, K = 385, 300
     A = rng.standard_normal((K, q)).astype(np.float32).astype(np.float64)
@@ -124,6 +145,8 @@ def oracle_point(name, k):
 def test_fp32_parity(ctx32, engine, name, k):
     if engine in ("tf32x3", "tf32x3_ldg") and name != "small":
         pytest.skip("the SS-form producers' parity at small only (the default TS form runs every size)")
+    if engine == "small":
+        pytest.skip("the default routing (small-shape kernel included) is the tf32x3_ts case")
     from paper_1509_04681_b200 import DeviceCsc, to_device_colmajor
     from paper_1509_04681_b200.api import newton_evaluation
     P, ref = oracle_point(name, k)

@@ -14,6 +14,7 @@ from synth.cggm_inputs import make_problem  # noqa
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="large")
+ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--part", default="all", choices=["all", "invert", "psi", "objective", "active"])
@@ -21,12 +22,13 @@ args = ap.parse_args()
 
 P = make_problem(args.config)
 label, lam, th = [pt for pt in P.points if pt[0] == "truth"][0]
-ctx = Context(0)
-X, Y = to_device_colmajor(P.X), to_device_colmajor(P.Y)
-L, T = DeviceCsc.from_host(lam), DeviceCsc.from_host(th)
+ctx = Context(0, dtype=args.dtype)
+dt = torch.float32 if args.dtype == "f32" else torch.float64
+X, Y = to_device_colmajor(P.X, dtype=dt), to_device_colmajor(P.Y, dtype=dt)
+L, T = DeviceCsc.from_host(lam, dtype=dt), DeviceCsc.from_host(th, dtype=dt)
 Syy, _ = ctx.cggm_covariances(X, Y, want_sxy=False)
 q, p = P.q, P.p
-Sigma = colmajor_empty(q, q)
+Sigma = colmajor_empty(q, q, dtype=dt)
 r0 = ctx.cggm_psi_grad(X, Y, T, ctx.cggm_invert_logdet(L, Sigma=Sigma)[0], Syy=Syy)
 cnt = ctx.cggm_active_set(r0["GradL"], r0["GradT"], L, T, P.lam_L, P.lam_T)
 bufs = {"Sigma": Sigma, "Psi": r0["Psi"], "GradL": r0["GradL"], "GradT": r0["GradT"]}

@@ -15,13 +15,15 @@ from synth.cggm_inputs import make_problem  # noqa
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="large")
+ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
 ap.add_argument("--out", default="gpurun_out/timeline.csv")
 args = ap.parse_args()
 P = make_problem(args.config)
 label, lam, th = [pt for pt in P.points if pt[0] == "truth"][0]
-ctx = Context(0)
-X, Y = to_device_colmajor(P.X), to_device_colmajor(P.Y)
-L, T = DeviceCsc.from_host(lam), DeviceCsc.from_host(th)
+ctx = Context(0, dtype=args.dtype)
+dt = torch.float32 if args.dtype == "f32" else torch.float64
+X, Y = to_device_colmajor(P.X, dtype=dt), to_device_colmajor(P.Y, dtype=dt)
+L, T = DeviceCsc.from_host(lam, dtype=dt), DeviceCsc.from_host(th, dtype=dt)
 Syy, _ = ctx.cggm_covariances(X, Y, want_sxy=False)
 q = P.q
 bufs = {}
