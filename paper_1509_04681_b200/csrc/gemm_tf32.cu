@@ -114,6 +114,11 @@ __device__ __forceinline__ void epi_apply_t(const EpilogueT<float>& E, int64_t r
 // the 13 low bits (a mantissa carry moves into the exponent, as it should); two integer ops instead
 // of the conversion unit's cvt.rna.tf32 (the split runs on every operand element of every k-tile)
 __device__ __forceinline__ uint32_t rna_tf32(float x) { return (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u; }
+// lo of the split for an operand the tensor core reads (hi = rna_tf32(v), so v - hi is exact in
+// fp32): + half a tf32 ulp without the mask -- kind::tf32 ignores the 13 low mantissa bits of a
+// 32-bit operand (truncation, measured: tools/debug/tf32_trunc_probe.py), so the MMA multiplies
+// rna_tf32(lo) and the split costs one integer op less per element
+__device__ __forceinline__ uint32_t lo_tf32(float v, uint32_t hi) { return __float_as_uint(v - __uint_as_float(hi)) + 0x1000u; }
 
 // shared-memory matrix descriptor (tcgen05): start >> 4 [0,14), LBO >> 4 [16,30), SBO >> 4 [32,46),
 // version 1 [46,48), base offset 0, layout at [61,64): SWIZZLE_128B = 2 (K-major), SWIZZLE_128B with
@@ -141,6 +146,13 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                    ptx::smem_u32(bar))
                : "memory");
+}
+
+// one lane of the (converged) warp: true on exactly one lane
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p = 0;
+  asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n" : "=r"(p));
+  return p != 0;
 }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
@@ -263,6 +275,39 @@ __device__ __forceinline__ void convert_split(uint32_t raw, uint32_t hi, uint32_
     sts128(hi + so, h[0], h[1], h[2], h[3]);
     sts128(lo + so, l[0], l[1], l[2], l[3]);
   }
+}
+
+// raw B tile (TMA SWIZZLE_128B) -> registers, NTH threads, 16-byte chunks f = tid + NTH i; and the
+// split of those registers into the UMMA layouts of hi / lo (the convert_split positions)
+// one 16-byte chunk (i-th of this thread) of the raw B tile / of its hi / lo stores
+template <bool KIN, int NTH>
+__device__ __forceinline__ void raw_b_chunk(uint32_t raw, float (&v)[4], int tid, int i) {
+  const int f = tid + NTH * i;
+  uint32_t ro;
+  if (KIN) {
+    const int row = f >> 3, c = f & 7;
+    ro = row * 128 + ((c ^ (row & 7)) << 4);
+  } else {
+    const int k = f >> 5, mc = f & 31, c = mc & 7;
+    ro = (mc >> 3) * 4096 + k * 128 + ((c ^ (k & 7)) << 4);
+  }
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "r"(raw + ro));
+}
+
+template <bool KIN, int NTH>
+__device__ __forceinline__ void store_b_chunk(const uint32_t (&h)[4], const uint32_t (&l)[4], uint32_t hi, uint32_t lo,
+                                              int tid, int i) {
+  const int f = tid + NTH * i;
+  uint32_t so;
+  if (KIN) {
+    const int row = f >> 3, c = f & 7;
+    so = row * 128 + ((c ^ (row & 7)) << 4);
+  } else {
+    const int k = f >> 5, mc = f & 31, c = mc & 7;
+    so = (mc >> 3) * 4096 + k * 128 + (((((c >> 1) ^ (k & 3)) << 1) | (c & 1)) << 4);
+  }
+  sts128(hi + so, h[0], h[1], h[2], h[3]);
+  sts128(lo + so, l[0], l[1], l[2], l[3]);
 }
 
 template <bool AK, bool BKI, bool TMA>
@@ -533,6 +578,7 @@ constexpr int TS_CONV = 128;                 // converter threads (warps 0-3: TM
 constexpr int TS_NS = 4;                     // split stages (TMEM A, shared B)
 constexpr int TS_NRAW = 3;                   // raw TMA stages
 constexpr int TS_BSTAGE = 2 * T_OP;          // B hi + lo
+constexpr int TS_BPER = TBN * TBK / 4 / TS_CONV;   // raw B 16-byte chunks per converter thread (8)
 constexpr int TS_DATA = TS_NS * TS_BSTAGE + TS_NRAW * T_RAW;   // 128 + 96 KB
 static_assert(TBN * T_EPI_LD * 4 <= TS_DATA, "epilogue tile must fit");
 constexpr int TS_SMEM = TS_DATA + 1024 + 256;
@@ -633,8 +679,11 @@ __global__ void __launch_bounds__(TS_NT, 1)
   const uint32_t rbase = sbase + TS_NS * TS_BSTAGE;
 
   if (warp == TS_MMA) {
-    if (lane == 0 && nkt > 0) {
+    // the whole warp walks the loop (warp-uniform control flow: the descriptors stay in uniform
+    // registers); one elected lane issues the MMAs and their commits
+    if (nkt > 0) {
       constexpr uint32_t idesc = idesc_tf32(false, !BKI, TBM, TBN);
+      const bool leader = elect_one();
       for (int j = 0; j < nkt; ++j) {
         const int s = j % TS_NS;
         const int c = j / CH;
@@ -648,20 +697,23 @@ __global__ void __launch_bounds__(TS_NT, 1)
         const uint32_t b_hi = sbase + s * TS_BSTAGE, b_lo = b_hi + T_OP;
         const uint32_t a_hi = tmem + 256u + (uint32_t)s * 64u, a_lo = a_hi + 32u;
         const uint32_t X = tmem + ((c & 1) ? 128u : 0u);
+        if (leader) {
 #pragma unroll
-        for (int kk = 0; kk < TBK / 8; ++kk) {
-          const uint32_t ob = kk * (BKI ? 32 : 1024);
-          const uint32_t lb = BKI ? 16 : 4096, sb = BKI ? 1024 : 512;
-          const uint64_t yb = BKI ? 2 : 1;
-          const uint64_t dbh = sdesc(b_hi + ob, lb, sb, yb), dbl = sdesc(b_lo + ob, lb, sb, yb);
-          umma_tf32_ts(X, a_lo + kk * 8u, dbh, idesc, (first && kk == 0) ? 0u : 1u);
-          umma_tf32_ts(X, a_hi + kk * 8u, dbl, idesc, 1u);
-          umma_tf32_ts(X, a_hi + kk * 8u, dbh, idesc, 1u);
+          for (int kk = 0; kk < TBK / 8; ++kk) {
+            const uint32_t ob = kk * (BKI ? 32 : 1024);
+            const uint32_t lb = BKI ? 16 : 4096, sb = BKI ? 1024 : 512;
+            const uint64_t yb = BKI ? 2 : 1;
+            const uint64_t dbh = sdesc(b_hi + ob, lb, sb, yb), dbl = sdesc(b_lo + ob, lb, sb, yb);
+            umma_tf32_ts(X, a_lo + kk * 8u, dbh, idesc, (first && kk == 0) ? 0u : 1u);
+            umma_tf32_ts(X, a_hi + kk * 8u, dbl, idesc, 1u);
+            umma_tf32_ts(X, a_hi + kk * 8u, dbh, idesc, 1u);
+          }
+          umma_commit(&empty[s]);
+          if (j % CH == CH - 1 || j == nkt - 1) umma_commit(&cfull[c & 1]);
         }
-        umma_commit(&empty[s]);
-        if (j % CH == CH - 1 || j == nkt - 1) umma_commit(&cfull[c & 1]);
+        __syncwarp();
       }
-      umma_commit(accf);
+      if (leader) umma_commit(accf);
     }
     __syncwarp();
   } else if (warp == TS_TMAW) {
@@ -695,9 +747,13 @@ __global__ void __launch_bounds__(TS_NT, 1)
     __syncwarp();
   } else if (warp < TS_DW0) {
     // ---- converters: A row (32 k) of this thread's TMEM lane -> hi / lo columns of the stage; B tile
-    // -> hi / lo in shared memory
+    // -> hi / lo in shared memory, one 16-byte chunk at a time (issuing all raw loads of a k-tile
+    // first and storing after the split measured no faster)
     const int m = warp * 32 + lane;
     const uint32_t lanebase = tmem + ((uint32_t)(warp * 32) << 16);
+    // measurement aid (CGGM_TF32_DEBUG bit 1): hi = the fp32 bits unrounded, so lo = v - hi = 0 and
+    // the MMA sees the raw operand (how the tensor core reads the 13 low bits)
+    const uint32_t h_add = (P.dbg & 2) ? 0u : 0x1000u, h_mask = (P.dbg & 2) ? 0xFFFFFFFFu : 0xFFFFE000u;
     for (int it = 0; it < nkt; ++it) {
       const int s = it % TS_NS, rs = it % TS_NRAW;
       ptx::mbar_wait(&rfull[rs], (it / TS_NRAW) & 1);
@@ -712,15 +768,26 @@ __global__ void __launch_bounds__(TS_NT, 1)
         uint32_t h[32], l[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
-          h[e] = rna_tf32(v[e]);
-          l[e] = rna_tf32(v[e] - __uint_as_float(h[e]));
+          h[e] = (__float_as_uint(v[e]) + h_add) & h_mask;
+          l[e] = lo_tf32(v[e], h[e]);
         }
         const uint32_t ac = lanebase + 256u + (uint32_t)s * 64u;
         tmem_st32_nowait(ac, h);
         tmem_st32_nowait(ac + 32u, l);
       }
       const uint32_t st = sbase + s * TS_BSTAGE;
-      convert_split<BKI, TS_CONV>(rw + T_OP, st, st + T_OP, tid);
+#pragma unroll
+      for (int i = 0; i < TS_BPER; ++i) {
+        float vb[4];
+        uint32_t hb[4], lb[4];
+        raw_b_chunk<BKI, TS_CONV>(rw + T_OP, vb, tid, i);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          hb[e] = (__float_as_uint(vb[e]) + h_add) & h_mask;
+          lb[e] = lo_tf32(vb[e], hb[e]);
+        }
+        store_b_chunk<BKI, TS_CONV>(hb, lb, st, st + T_OP, tid, i);
+      }
       asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       tc_fence_before();
