@@ -762,6 +762,7 @@ __global__ void __launch_bounds__(TS_NT, 1)
         tc_fence_after();
       }
       const uint32_t rw = rbase + rs * T_RAW;
+      if (!(P.dbg & 4)) {   // (bit 2: measurement aid -- skip the split and the stores; garbage product)
       {
         float v[32];
         raw_a_row<AK>(rw, m, v);
@@ -788,6 +789,7 @@ __global__ void __launch_bounds__(TS_NT, 1)
         }
         store_b_chunk<BKI, TS_CONV>(hb, lb, st, st + T_OP, tid, i);
       }
+      }
       asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       tc_fence_before();
@@ -807,12 +809,14 @@ __global__ void __launch_bounds__(TS_NT, 1)
       ptx::mbar_wait(&cfull[c & 1], (c >> 1) & 1);
       tc_fence_after();
       const uint32_t xa = lanebase + ((c & 1) ? 128u : 0u);
+      if (!(P.dbg & 8)) {   // (bit 3: measurement aid -- no drain)
 #pragma unroll
-      for (int g = 0; g < TBN / 32; ++g) {
-        uint32_t v[32];
-        tmem_ld32(xa + 32u * g, v);
+        for (int g = 0; g < TBN / 32; ++g) {
+          uint32_t v[32];
+          tmem_ld32(xa + 32u * g, v);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) acc[32 * g + j] += __uint_as_float(v[j]);
+          for (int j = 0; j < 32; ++j) acc[32 * g + j] += __uint_as_float(v[j]);
+        }
       }
       tc_fence_before();
       ptx::mbar_arrive(&cempty[c & 1]);
