@@ -124,8 +124,16 @@ cggm_status cggm_ctx_set_validate(cggm_ctx* ctx, int level);
  *     (4/3) q^3 -> q^3 flop.  The CALLER guarantees that the next Lambda equals the previous call's
  *     Lambda (the accepted line-search trial); q must match, else the call falls back to a full
  *     inverse.  Setting the option (either value) forgets the kept factor.
+ *   CGGM_OPT_SIGMA_BLOCK: FP64 Sigma = L^{-T} L^{-1} of cggm_invert_logdet / cggm_newton_eval
+ *     is assembled inside the recursive inverse: a recursion node at least this wide forms its
+ *     off-diagonal block X22^T X21 and the update X21^T X21 of its leading block as soon as its
+ *     own L^{-1} block is final, its children likewise; narrower nodes form their whole block in one
+ *     product (default 4096; 0 = one symmetric product after the recursion; values below 128 are
+ *     refused).  Sums of the same products in a different split of the k-range only.
  * Unknown option -> CGGM_ERR_INVALID_ARG. */
-typedef enum cggm_option { CGGM_OPT_LOOKAHEAD_MIN = 0, CGGM_OPT_GRAPHS = 1, CGGM_OPT_FACTOR_REUSE = 2 } cggm_option;
+typedef enum cggm_option {
+  CGGM_OPT_LOOKAHEAD_MIN = 0, CGGM_OPT_GRAPHS = 1, CGGM_OPT_FACTOR_REUSE = 2, CGGM_OPT_SIGMA_BLOCK = 3
+} cggm_option;
 cggm_status cggm_ctx_set_option(cggm_ctx* ctx, int option, int64_t value);
 /* Number of library kernels launched on this ctx so far (for launch accounting). */
 cggm_status cggm_ctx_launch_count(cggm_ctx* ctx, int64_t* count);

@@ -15,6 +15,12 @@ extern "C" {
 cggm_status cggm_test_gemm(cggm_ctx* ctx, int transA, int transB, int64_t M, int64_t N, int64_t K,
                            const double* A, int64_t lda, const double* B, int64_t ldb,
                            double* C, int64_t ldc, double alpha, double beta, int flags);
+/* C (M x N, ldc) = alpha * op(A) op(B) and Cmir (N x M, ldc) = its transpose, written by the same
+ * epilogue (SYM_MIRROR without SYM_LOWER: the off-diagonal block of a symmetric result, as the
+ * Sigma assembly of the recursive inverse writes it).  flags: the triangular k-range bits only. */
+cggm_status cggm_test_gemm_mir(cggm_ctx* ctx, int transA, int transB, int64_t M, int64_t N, int64_t K,
+                               const double* A, int64_t lda, const double* B, int64_t ldb,
+                               double* C, int64_t ldc, double* Cmir, double alpha, int flags);
 /* FP32 variant of cggm_test_gemm (the ctx's FP32 engine, fp32 accumulation). */
 cggm_status cggm_test_gemm_f32(cggm_ctx* ctx, int transA, int transB, int64_t M, int64_t N, int64_t K,
                                const float* A, int64_t lda, const float* B, int64_t ldb,

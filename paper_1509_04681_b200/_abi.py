@@ -27,6 +27,7 @@ CGGM_F32 = 1
 CGGM_OPT_LOOKAHEAD_MIN = 0
 CGGM_OPT_GRAPHS = 1
 CGGM_OPT_FACTOR_REUSE = 2
+CGGM_OPT_SIGMA_BLOCK = 3
 # cggm_gemm structural flags
 A_KLE_M, A_KGE_M, B_KLE_N, B_KGE_N, SYM_LOWER, SYM_MIRROR = 1, 2, 4, 8, 16, 32
 PROF_NTAGS = 14
@@ -120,6 +121,8 @@ SIGNATURES = {
                                       c_vp, c_i64, ctypes.POINTER(cggm_active_out), ctypes.POINTER(cggm_eval_out)]),
     "cggm_test_gemm": (c_i32, [c_vp, c_i32, c_i32, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
                                c_d, c_d, c_i32]),
+    "cggm_test_gemm_mir": (c_i32, [c_vp, c_i32, c_i32, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
+                                   c_vp, c_d, c_i32]),
     "cggm_test_gemm_f32": (c_i32, [c_vp, c_i32, c_i32, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
                                    c_d, c_d, c_i32]),
     "cggm_test_set_tile": (c_i32, [c_vp, c_i32]),

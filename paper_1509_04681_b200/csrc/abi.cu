@@ -167,6 +167,8 @@ cggm_status cggm_ctx_create(cggm_ctx** out, int device, cggm_dtype dtype, void* 
   c->slots.resize(WS_NUM);
   if (const char* e = std::getenv("CGGM_PRIO")) c->prio_mode = std::atoi(e);
   if (const char* e = std::getenv("CGGM_LA_MIN")) c->la_min = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_GL_OVERLAP")) c->gl_overlap = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_SIGMA_REC")) c->sig_min = std::atoi(e) > 0 ? std::max(128, std::atoi(e)) : 0;
   if (const char* e = std::getenv("CGGM_NO_SMALL_ASYNC")) c->no_small_async = std::atoi(e);
   if (const char* e = std::getenv("CGGM_GRAPH")) c->use_graphs = std::atoi(e);
   if (const char* e = std::getenv("CGGM_SMALL_KMAX")) c->small_kmax = std::atoi(e);
@@ -226,6 +228,16 @@ cggm_status cggm_ctx_destroy(cggm_ctx* ctx) {
         cudaStreamSynchronize(st);
         cudaStreamDestroy(st);
       }
+  if (c->la_sig) {
+    cudaStreamSynchronize(c->la_sig);
+    cudaStreamDestroy(c->la_sig);
+  }
+  if (c->gl_side) {
+    cudaStreamSynchronize(c->gl_side);
+    cudaStreamDestroy(c->gl_side);
+    cudaEventDestroy(c->ev_gl0);
+    cudaEventDestroy(c->ev_gl1);
+  }
   for (auto e : c->la_events) cudaEventDestroy(e);
   if (c->copy) {
     cudaStreamSynchronize(c->copy);
@@ -279,6 +291,10 @@ cggm_status cggm_ctx_set_option(cggm_ctx* ctx, int option, int64_t value) {
       if (value != 0 && value != 1) return CGGM_ERR_INVALID_ARG;
       c->factor_reuse = (int)value;
       c->reuse_valid = 0;
+      return CGGM_OK;
+    case CGGM_OPT_SIGMA_BLOCK:
+      if (value != 0 && (value < 128 || value > (1 << 30))) return CGGM_ERR_INVALID_ARG;
+      c->sig_min = (int)value;
       return CGGM_OK;
     default:
       return CGGM_ERR_INVALID_ARG;
@@ -730,15 +746,15 @@ cggm_status cggm_theta_cd_rows(cggm_ctx* ctx, int64_t p, int64_t q, const void* 
 int cggm::stream_priority(int which) {
   // which: 0 chain tail (Sigma product, W Sigma, Psi, grad_Theta), 1 objective origin, 2-4 inverse
   // recursion (critical chain, deferred updates, background products), 5-7 the objective's
-  // recursion, 3 also S_yy.  The recursions' critical chains outrank the big throughput GEMMs, so
+  // recursion, 3 also S_yy, 8 the Sigma blocks formed inside the inverse recursion.  The recursions' critical chains outrank the big throughput GEMMs, so
   // their latency-bound kernels start as soon as SMs free up (measured 429.7 -> 426.1 ms at large
   // against {0, 5, 0, 1, 2, 3, 4, 5}).
-  static int off[8] = {4, 5, 1, 2, 3, 0, 4, 5};
+  static int off[9] = {4, 5, 1, 2, 3, 0, 4, 5, 3};
   static bool init = false;
   if (!init) {
     if (const char* e = std::getenv("CGGM_PRIO_SCHEME")) {
       int k = 0;
-      for (const char* q = e; *q && k < 8; ++k) {
+      for (const char* q = e; *q && k < 9; ++k) {
         off[k] = std::atoi(q);
         while (*q && *q != ',') ++q;
         if (*q == ',') ++q;
@@ -788,8 +804,13 @@ static void invert_enqueue(Ctx* c, int lane, const cggm_csc* Lambda, T* Sigma, i
     CGGM_CUDA_CHECK(cudaMemsetAsync(X, 0, (size_t)lda * q * sizeof(T), c->stream));
     const size_t tmp_elems = chol_tmp_elems(q);
     T* tmp = static_cast<T*>(ws_get(c, WS_TMP, tmp_elems * sizeof(T)));
-    potrf_recursive<T>(c, Av, ViewT<T>{X, lda, q, q}, true, nullptr, slots, s.fail, tmp, tmp_elems);
-    lauum<T>(c, ViewT<T>{X, lda, q, q}, ViewT<T>{Sigma, ldsigma, q, q});
+    if (sizeof(T) == 8 && c->sig_min > 0 && q >= c->sig_min) {   // Sigma assembled inside the recursion
+      potrf_recursive<T>(c, Av, ViewT<T>{X, lda, q, q}, true, nullptr, slots, s.fail, tmp, tmp_elems, nullptr, 0,
+                         nullptr, 0, Sigma, ldsigma);
+    } else {
+      potrf_recursive<T>(c, Av, ViewT<T>{X, lda, q, q}, true, nullptr, slots, s.fail, tmp, tmp_elems);
+      lauum<T>(c, ViewT<T>{X, lda, q, q}, ViewT<T>{Sigma, ldsigma, q, q});
+    }
   } else {
     T* leafinv = static_cast<T*>(ws_get(c, WS_LEAFINV, (size_t)nleaves * nb * nb * sizeof(T)));
     potrf_recursive<T>(c, Av, ViewT<T>{nullptr, lda, q, q}, false, leafinv, slots, s.fail, nullptr, 0);
@@ -1085,17 +1106,44 @@ static void psi_enqueue(Ctx* c, int64_t n_local, int64_t n_total, int64_t p, int
     }
     gemm(c, true, false, q, q, n_local, R, ldn, R, ldn, e, SYM_LOWER | SYM_MIRROR);
     if (collective) comm_allreduce(c, Psi, flat_count(q, q, ldpsi), dt);   // Psi = sum_r R_r^T R_r
-    if (GradL && !fuse_gl) {
-      Phase pg(c, TAG_GRADL);
-      grad_lambda(c, q, Syy, ldsyy, Sg, ldsigma, Psi, ldpsi, GradL, ldgl);
-    }
   }
   const cggm_active_out* o = fz ? fz->o : nullptr;
+  // grad_Lambda and the S_Lambda compaction (HBM-bound) depend only on Psi: with CGGM_GL_OVERLAP they
+  // run on a side stream beside the DMMA-bound X^T E GEMM, joined before the S_Theta part (measured
+  // neutral at `large`: 409.2-409.8 ms either way; off by default)
+  cudaStream_t chain = c->stream, side = nullptr;
+  struct StreamBack {
+    Ctx* c;
+    cudaStream_t s;
+    ~StreamBack() { c->stream = s; }
+  } stream_back{c, chain};
+  if (c->gl_overlap && fz && GradL && !collective && !c->fuse_gradl && GradT) {
+    if (!c->gl_side) {
+      int least = 0, greatest = 0;
+      CGGM_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+      CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->gl_side, cudaStreamNonBlocking,
+                                                   c->gl_overlap == 2 ? least : greatest));
+      CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_gl0, cudaEventDisableTiming));
+      CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_gl1, cudaEventDisableTiming));
+    }
+    side = c->gl_side;
+    CGGM_CUDA_CHECK(cudaEventRecord(c->ev_gl0, chain));
+    CGGM_CUDA_CHECK(cudaStreamWaitEvent(side, c->ev_gl0, 0));
+    c->stream = side;
+  }
+  if (GradL && !(c->fuse_gradl && !collective)) {   // (fused: the Psi GEMM's second output above)
+    Phase pg(c, TAG_GRADL);
+    grad_lambda(c, q, Syy, ldsyy, Sg, ldsigma, Psi, ldpsi, GradL, ldgl);
+  }
   if (fz) {
     Phase ph(c, TAG_ACTIVE);
     active_begin(c, q, fz->ws);
     active_lambda<T>(c, q, GradL, ldgl, fz->Lambda, o->lam_L, o->penalize_diag, o->tie_eps, fz->ws, o->L_row,
                      o->L_col, o->cap_L);
+  }
+  if (side) {
+    CGGM_CUDA_CHECK(cudaEventRecord(c->ev_gl1, side));
+    c->stream = chain;
   }
   // a5: GradT = (2/n) X^T E   (or 2 S_xy + (2/sqrt n) X^T R), columns [j0, j0 + nc) into `out`
   auto grad_theta = [&](int64_t j0, int64_t nc, T* out, int64_t ldo) {
@@ -1113,6 +1161,7 @@ static void psi_enqueue(Ctx* c, int64_t n_local, int64_t n_total, int64_t p, int
   };
   if (GradT) {
     grad_theta(0, q, GradT, ldgt);
+    if (side) CGGM_CUDA_CHECK(cudaStreamWaitEvent(chain, c->ev_gl1, 0));
     if (fz) {
       Phase ph(c, TAG_ACTIVE);
       active_theta_chunk<T>(c, p, 0, q, GradT, ldgt, fz->Theta, o->lam_T, o->tie_eps, fz->ws, o->T_row, o->T_col,
@@ -1706,7 +1755,7 @@ static void newton_eval_core(Ctx* c, int64_t n, int64_t p, int64_t q, const void
   // GPU works through it, so the second could not start alongside).  A new argument set runs
   // eagerly once (allocating anything missing), the second call with the same arguments captures.
   std::vector<int64_t> key = {n, p, q, ldx, ldy, ldsyy, ldsigma, ldpsi, ldgl, ldgt, (int64_t)c->ws_generation,
-                              (int64_t)c->dtype, c->prio_mode, c->la_min, (int64_t)s_caller};
+                              (int64_t)c->dtype, c->prio_mode, c->la_min, (int64_t)s_caller, c->sig_min};
   for (const void* ptr : {X, Y, Syy, (const void*)Sigma, (const void*)Psi, (const void*)GradL, (const void*)GradT})
     key.push_back((int64_t)ptr);
   for (const cggm_csc* m : {Lambda, Theta}) {
@@ -2087,6 +2136,17 @@ extern "C" cggm_status cggm_test_gemm(cggm_ctx* ctx, int transA, int transB, int
     e.out1 = C; e.ld1 = ldc; e.a1 = alpha;
     if (beta != 0.0) { e.in1a = C; e.ld1a = ldc; e.b1 = beta; }
     gemm(c, transA != 0, transB != 0, M, N, K, A, lda, B, ldb, e, flags);
+  });
+}
+
+extern "C" cggm_status cggm_test_gemm_mir(cggm_ctx* ctx, int transA, int transB, int64_t M, int64_t N, int64_t K,
+                                          const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                                          int64_t ldc, double* Cmir, double alpha, int flags) {
+  return guard(ctx, [&](Ctx* c) {
+    if (M < 0 || N < 0 || K < 0) fail(CGGM_ERR_INVALID_ARG, "negative dimension");
+    Epilogue e;
+    e.out1 = C; e.ld1 = ldc; e.a1 = alpha; e.mir1 = Cmir;
+    gemm(c, transA != 0, transB != 0, M, N, K, A, lda, B, ldb, e, flags | SYM_MIRROR);
   });
 }
 

@@ -496,8 +496,20 @@ __global__ void __launch_bounds__(LEAF_THREADS, CGGM_LEAF_MINB) leaf_rec_inverse
   }
 }
 
+// CGGM_SPLIT_PANEL = B > 0: nodes wider than 2B split off a leading panel of B columns instead of
+// halving (a right-looking recursion with recursive panels: each level's latency-bound panel
+// factorisation overlaps the previous level's deferred trailing update); 0 = halving everywhere
+int split_panel() {
+  static int v = [] {
+    const char* e = std::getenv("CGGM_SPLIT_PANEL");
+    return e ? std::max(0, std::atoi(e)) / 128 * 128 : 0;
+  }();
+  return v;
+}
+
 int split_point(int64_t n) {
   const int64_t gran = n > 4 * 128 ? 128 : NB;
+  if (split_panel() > 0 && n > 2 * split_panel()) return split_panel();
   int64_t n1 = (n / 2) / gran * gran;
   if (n1 <= 0) n1 = gran;
   if (n1 >= n) n1 = n - NB;
@@ -575,6 +587,12 @@ struct Rec {
   int64_t ldxd;
   T* tmp2;      // potrf-only: out-of-place product buffer for B := B Xblock^T
   size_t tmp2_elems;
+  // full-inverse mode with sig != null: Sigma = L^{-T} L^{-1} assembled block by block as the
+  // recursion finishes the blocks of L^{-1} (sig_node), on stream sgs (c->stream when null)
+  T* sig = nullptr;
+  int64_t ldsig = 0;
+  int64_t sig_min = 0;
+  cudaStream_t sgs = nullptr;
 };
 
 // B := B Xb^T for the inverse Xb (n x n, lower) of one diagonal block, out of place through tmp2
@@ -623,16 +641,76 @@ void leaf(Rec<T>& R, ViewT<T> A, ViewT<T> X, int64_t col0) {
   post_launch(R.c, "leaf_potrf_trtri");
 }
 
+// ---------------------------------------------------------------- Sigma interleaved with the recursion
+// For a node with X = L^{-1} of its diagonal block = [[X11, 0], [X21, X22]] (Sigma = Lambda^{-1}
+// = L^{-T} L^{-1}), its block of X^T X is
+//   S11 = X11^T X11 + X21^T X21,   S21 = X22^T X21 (S12 = S21^T),   S22 = X22^T X22.
+// X11^T X11 and X22^T X22 are the children's own blocks (formed as soon as each child's inverse is
+// final, recursively), so only S21 and the update S11 += X21^T X21 wait for X21, the node's last
+// product: the lauum work of the lower levels runs inside the recursion, in the SMs its
+// latency-bound stretches leave idle, instead of as one product after it.  Nodes below sig_min form
+// their block in one symmetric product.  Same arithmetic per entry as the one-shot product up to
+// the order of the k-sums (a block's sum is split at the child boundaries).
+template <typename T>
+void sig_enqueue_begin(Rec<T>& R, cudaStream_t& chain, cudaStream_t& prev) {
+  prev = R.c->stream;
+  chain = prev;
+  if (R.sgs) {
+    CGGM_CUDA_CHECK(cudaStreamWaitEvent(R.sgs, la_record(R.c, prev), 0));
+    R.c->stream = R.sgs;
+  }
+}
+
+template <typename T>
+void sig_block_product(Rec<T>& R, ViewT<T> X, int64_t col0) {   // S_node = X^T X (X lower triangular)
+  const int64_t n = X.rows;
+  cudaStream_t chain, prev;
+  sig_enqueue_begin(R, chain, prev);
+  {
+    Prof pr(R.c, TAG_LAUUM);
+    EpilogueT<T> e; e.out1 = R.sig + col0 + col0 * R.ldsig; e.ld1 = R.ldsig;
+    gemm(R.c, true, false, n, n, n, X.p, X.ld, X.p, X.ld, e, A_KGE_M | B_KGE_N | SYM_LOWER | SYM_MIRROR);
+  }
+  R.c->stream = prev;
+}
+
+template <typename T>
+void sig_node_pieces(Rec<T>& R, ViewT<T> X11, ViewT<T> X21, ViewT<T> X22, int64_t col0) {
+  const int64_t n1 = X11.rows, n2 = X22.rows;
+  T* S11 = R.sig + col0 + col0 * R.ldsig;
+  cudaStream_t chain, prev;
+  sig_enqueue_begin(R, chain, prev);
+  {
+    Prof pr(R.c, TAG_LAUUM);
+    {  // S21 = X22^T X21 (X22 lower: op(A) = X22^T has k >= m), S12 = S21^T by the mirrored epilogue
+      EpilogueT<T> e; e.out1 = S11 + n1; e.ld1 = R.ldsig; e.mir1 = S11 + n1 * R.ldsig;
+      gemm(R.c, true, false, n2, n1, n2, X22.p, X22.ld, X21.p, X21.ld, e, A_KGE_M | SYM_MIRROR);
+    }
+    {  // S11 += X21^T X21 (after X11^T X11, enqueued earlier on this stream)
+      EpilogueT<T> e; e.out1 = S11; e.ld1 = R.ldsig; e.in1a = S11; e.ld1a = R.ldsig; e.b1 = 1.0;
+      gemm(R.c, true, false, n1, n1, n2, X21.p, X21.ld, X21.p, X21.ld, e, SYM_LOWER | SYM_MIRROR);
+    }
+  }
+  R.c->stream = prev;
+}
+
 // A is (n + extra) x n: the square block being factored with `extra` appended rows below it
 // (potrf-only mode).  Factoring the augmented [Lambda; W] leaves Z = W L^{-T} in the bottom rows
 // (block Cholesky of [[Lambda, W^T], [W, .]]), so the objective's triangular solve is carried by
 // the same recursive GEMMs with taller panels.
 // pending: event of the parent's deferred update of this node's trailing block A[n1:, n1:]
 // (full-inverse lookahead); waited on before this node's own trailing update
+// sig (full-inverse mode with R.sig): this node owns its block of Sigma (see sig_node_pieces)
 template <typename T>
-void node(Rec<T>& R, ViewT<T> A, ViewT<T> X, int64_t col0, int depth = 0, cudaEvent_t pending = nullptr) {
+void node(Rec<T>& R, ViewT<T> A, ViewT<T> X, int64_t col0, int depth = 0, cudaEvent_t pending = nullptr,
+          bool sig = false) {
   const int64_t n = A.cols, extra = A.rows - A.cols;
   Ctx* c = R.c;
+  if (sig && n < R.sig_min) {   // the whole block in one product once this subtree's inverse is final
+    node(R, A, X, col0, depth, pending, false);
+    sig_block_product(R, X, col0);
+    return;
+  }
   if (!R.full_inverse && R.xdiag && n <= BINV) {
     // potrf-only: factor this diagonal subtree in full-inverse mode, keeping its inverse for the
     // triangular solves of the panels to its right and of the appended rows below
@@ -658,7 +736,7 @@ void node(Rec<T>& R, ViewT<T> A, ViewT<T> X, int64_t col0, int depth = 0, cudaEv
   if (R.full_inverse) {
     if (extra) throw CudaError{CGGM_ERR_UNSUPPORTED, "augmented rows need potrf-only mode"};
     ViewT<T> X11 = X.sub(0, 0, n1, n1), X21 = X.sub(n1, 0, n2, n1), X22 = X.sub(n1, n1, n2, n2);
-    node(R, A11, X11, col0, depth + 1);
+    node(R, A11, X11, col0, depth + 1, nullptr, sig);
     if ((size_t)depth >= R.tmp_off.size()) throw CudaError{CGGM_ERR_OOM, "recursion temp too small"};
     ViewT<T> Tm{R.tmp + R.tmp_off[depth], n2 + (n2 & 1), n2, n1};
     if (R.tmp_off[depth] + (size_t)(Tm.ld * n1) > R.tmp_elems) throw CudaError{CGGM_ERR_OOM, "recursion temp too small"};
@@ -703,12 +781,13 @@ void node(Rec<T>& R, ViewT<T> A, ViewT<T> X, int64_t col0, int depth = 0, cudaEv
         gemm(c, false, false, n2, n1, n1, Tm.p, Tm.ld, X11.p, X11.ld, e, B_KGE_N);
       }
     }
-    node(R, A22, X22, col0 + n1, depth + 1, ev_upd);
+    node(R, A22, X22, col0 + n1, depth + 1, ev_upd, sig);
     if (ev_a21) CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->stream, ev_a21, 0));
     {  // X21 = -X22 A21
       EpilogueT<T> e; e.out1 = X21.p; e.ld1 = X21.ld; e.a1 = -1.0;
       gemm(c, false, false, n2, n1, n2, X22.p, X22.ld, A21.p, A21.ld, e, A_KLE_M);
     }
+    if (sig) sig_node_pieces(R, X11, X21, X22, col0);
   } else {
     node(R, A11, X, col0, depth + 1);
     trsm_rec(R, A21, A11, col0);
@@ -755,14 +834,21 @@ int leaf_nb() { return NB; }
 template <typename T>
 void potrf_recursive(Ctx* c, ViewT<T> A, ViewT<T> Linv, bool full_inverse, T* leafinv, double* logdet_slots,
                      int* fail_col_dev, T* tmp, size_t tmp_elems, T* xdiag, int64_t ldxd, T* tmp2,
-                     size_t tmp2_elems) {
+                     size_t tmp2_elems, T* sigma, int64_t ldsigma) {
   Rec<T> R{c, full_inverse, leafinv, logdet_slots, fail_col_dev, tmp, tmp_elems, {}, nullptr, nullptr,
            xdiag, ldxd, tmp2, tmp2_elems};
   if (full_inverse) R.tmp_off = tmp_slices(A.cols, nullptr);
+  const bool sig = full_inverse && sigma != nullptr;
+  if (sig) {
+    if (c->sig_min < 2 * NB) throw CudaError{CGGM_ERR_INVALID_ARG, "interleaved Sigma needs sig_min >= 128"};
+    R.sig = sigma;
+    R.ldsig = ldsigma;
+    R.sig_min = c->sig_min;
+  }
   Phase ph(c, TAG_CHOL_GEMM);
   const int lane = c->lane;
   if (c->la_min <= 0) {
-    node(R, A, Linv, 0);
+    node(R, A, Linv, 0, 0, nullptr, sig);
     return;
   }
   // lookahead: the recursion's critical chain on a high-priority stream, deferred products on two
@@ -773,21 +859,25 @@ void potrf_recursive(Ctx* c, ViewT<T> A, ViewT<T> Linv, bool full_inverse, T* le
     CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->la_upd[lane], cudaStreamNonBlocking, stream_priority(b + 1)));
     CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->la_bg[lane], cudaStreamNonBlocking, stream_priority(b + 2)));
   }
+  if (sig && !c->la_sig) CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->la_sig, cudaStreamNonBlocking, stream_priority(8)));
   c->la_next = 0;
   cudaStream_t s_in = c->stream, chain = c->la_chain[lane];
   R.upd = c->la_upd[lane];
   R.bg = c->la_bg[lane];
+  R.sgs = sig ? c->la_sig : nullptr;
   cudaEvent_t ev_in = la_record(c, s_in);
   for (cudaStream_t st : std::initializer_list<cudaStream_t>{chain, R.upd, R.bg}) CGGM_CUDA_CHECK(cudaStreamWaitEvent(st, ev_in, 0));
+  if (sig) CGGM_CUDA_CHECK(cudaStreamWaitEvent(R.sgs, ev_in, 0));
   {
     OnStream os(c, chain, nullptr);
     const auto t0 = std::chrono::steady_clock::now();
-    node(R, A, Linv, 0);
+    node(R, A, Linv, 0, 0, nullptr, sig);
     if (std::getenv("CGGM_HOSTPROF"))
       std::fprintf(stderr, "potrf_recursive q=%lld full=%d host enqueue %.3f ms\n", (long long)A.cols, (int)full_inverse,
                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   }
   for (cudaStream_t st : std::initializer_list<cudaStream_t>{chain, R.upd, R.bg}) CGGM_CUDA_CHECK(cudaStreamWaitEvent(s_in, la_record(c, st), 0));
+  if (sig) CGGM_CUDA_CHECK(cudaStreamWaitEvent(s_in, la_record(c, R.sgs), 0));
 }
 
 size_t chol_tmp_elems(int64_t q) {
@@ -807,9 +897,9 @@ void lauum(Ctx* c, ViewT<T> Linv, ViewT<T> Sigma) {
 }
 
 template void potrf_recursive<double>(Ctx*, ViewT<double>, ViewT<double>, bool, double*, double*, int*, double*,
-                                      size_t, double*, int64_t, double*, size_t);
+                                      size_t, double*, int64_t, double*, size_t, double*, int64_t);
 template void potrf_recursive<float>(Ctx*, ViewT<float>, ViewT<float>, bool, float*, double*, int*, float*, size_t,
-                                     float*, int64_t, float*, size_t);
+                                     float*, int64_t, float*, size_t, float*, int64_t);
 template void lauum<double>(Ctx*, ViewT<double>, ViewT<double>);
 template void lauum<float>(Ctx*, ViewT<float>, ViewT<float>);
 

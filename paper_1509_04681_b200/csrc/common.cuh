@@ -79,6 +79,11 @@ struct Ctx {
   // streams (deferred trailing updates, deferred block products) at decreasing priorities, and a
   // pool of dependency events (reused across calls: every wait is enqueued before a re-record)
   cudaStream_t la_chain[2] = {nullptr, nullptr}, la_upd[2] = {nullptr, nullptr}, la_bg[2] = {nullptr, nullptr};
+  cudaStream_t la_sig = nullptr;   // interleaved Sigma assembly (chol.cu), priority slot 8
+  cudaStream_t gl_side = nullptr;  // composite: grad_Lambda + the S_Lambda compaction beside the X^T E GEMM
+  int gl_overlap = 0;              // CGGM_GL_OVERLAP: 1 = side stream at the greatest priority, 2 = at the least, 0 = in line
+  cudaEvent_t ev_gl0 = nullptr, ev_gl1 = nullptr;
+  int sig_min = 4096;              // CGGM_SIGMA_REC: nodes >= this split their Sigma block (0 = one lauum after the recursion)
   std::vector<cudaEvent_t> la_events;
   size_t la_next = 0;
   int la_min = 256;              // defer only when the deferred block is at least this wide (CGGM_LA_MIN; 0 = off)
@@ -311,7 +316,8 @@ enum GemmFlags : int {
   B_KLE_N = 4,          // op(B)[k][n] == 0 for k > n
   B_KGE_N = 8,          // op(B)[k][n] == 0 for k < n
   SYM_LOWER = 16,       // M == N: compute only tiles I >= J; diagonal tiles write m >= n only
-  SYM_MIRROR = 32,      // with SYM_LOWER: also write every value at its transposed position
+  SYM_MIRROR = 32,      // with SYM_LOWER: also write every value at its transposed position; without
+                        // SYM_LOWER (epilogue mir1 set): every value also at its transposed position in mir1
   SPLIT_K2 = 64,        // two CTAs per tile, each half of the k-range, out1 += a1 * partial by atomic
                         // add (out1 must hold zeros; out2 / inputs unsupported).  Two partials added
                         // to zero give a + b in either order: the result is deterministic
@@ -326,6 +332,10 @@ struct EpilogueT {
   T* out2 = nullptr; int64_t ld2 = 0; double a2 = 1.0;
   const T* in2a = nullptr; int64_t ld2a = 0; double b2 = 0.0;
   const T* in2b = nullptr; int64_t ld2b = 0; double c2 = 0.0;
+  // SYM_MIRROR without SYM_LOWER on a rectangular block: the transposed copy a1*acc goes to mir1
+  // (ld1) instead of out1 -- the off-diagonal block of a symmetric result (FP64 kernels only; no
+  // inputs, no out2)
+  T* mir1 = nullptr;
 };
 using Epilogue = EpilogueT<double>;
 
@@ -357,7 +367,9 @@ struct CholResult {
 template <typename T>
 void potrf_recursive(Ctx* c, ViewT<T> A, ViewT<T> Linv, bool full_inverse, T* leafinv, double* logdet_slots,
                      int* fail_col_dev, T* tmp, size_t tmp_elems, T* xdiag = nullptr, int64_t ldxd = 0,
-                     T* tmp2 = nullptr, size_t tmp2_elems = 0);
+                     T* tmp2 = nullptr, size_t tmp2_elems = 0, T* sigma = nullptr, int64_t ldsigma = 0);
+//  full_inverse with sigma != null (FP64; q >= Ctx::sig_min): Sigma = L^{-T} L^{-1} (both triangles)
+//  assembled block by block inside the recursion (chol.cu, sig_node_pieces) -- no separate lauum.
 int block_inverse_size();
 // Sigma = Linv^T Linv (full symmetric).
 template <typename T>
@@ -400,6 +412,11 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+
+// orders this thread's generic-proxy shared-memory accesses before later async-proxy (TMA) ones
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {

@@ -162,6 +162,13 @@ __device__ __forceinline__ void epi_apply(const Epilogue& E, int64_t r, int64_t 
   }
 }
 
+// the transposed copy of a SYM_MIRROR product: into the same output (symmetric square) or into
+// E.mir1 (the off-diagonal block of a symmetric result; host-checked to have no inputs / out2)
+__device__ __forceinline__ void epi_mirror(const Epilogue& E, int64_t r, int64_t c, double v) {
+  if (E.mir1) E.mir1[r + c * E.ld1] = __dmul_rn(E.a1, v);
+  else epi_apply(E, r, c, v);
+}
+
 // x offset (within the warp's 64/32-wide slab) of fragment f, fragment row/col index r
 template <bool KINNER>
 __device__ __forceinline__ int frag_x(int f, int r) {
@@ -339,6 +346,11 @@ __global__ void __launch_bounds__(C::LB_THREADS, C::LB_MINB)
             for (int fn = 0; fn < FN; ++fn) ptx::dmma_8x8x4(acc[fm][fn][0], acc[fm][fn][1], a[fm][s2], b[fn][s2]);
       }
       __syncwarp();
+      // the stage's generic-proxy reads (ld.shared) are ordered before the TMA (async proxy) that
+      // refills it once every consumer warp has arrived: without this proxy fence the refill could
+      // overwrite data still being read (observed: corrupted warp tiles when an HBM-streaming kernel
+      // ran beside the warp-specialised 128x64 tiles, tools/debug/gl_race.py)
+      ptx::fence_proxy_async();
       if (lane == 0) ptx::mbar_arrive(&empty[s]);
       if (!WS && threadIdx.x == 0) {
         const int j = i + STAGES - 1;
@@ -432,7 +444,7 @@ __global__ void __launch_bounds__(C::LB_THREADS, C::LB_MINB)
     }
   }
   if (P.flags & SYM_MIRROR) {
-    if (P.vec && !diag && m0 + BM <= P.M && n0 + BN <= P.N && !P.epi.in1a) {
+    if (P.vec && !diag && m0 + BM <= P.M && n0 + BN <= P.N) {
       // transposed copy: lane l of a warp reads row nl = nb + l of the staged tile at columns ml and
       // ml + 1 (consecutive lanes 129 doubles apart: conflict-free), then lane pairs swap one value
       // so that the even lane stores (nl, nl + 1) of output column ml and the odd lane those of
@@ -451,8 +463,15 @@ __global__ void __launch_bounds__(C::LB_THREADS, C::LB_MINB)
         const double pa = __shfl_xor_sync(0xffffffffu, a, 1), pb = __shfl_xor_sync(0xffffffffu, b, 1);
         const double lo = odd ? pb : a, hi = odd ? b : pa;   // rows (n, n + 1) of output column m
         const int64_t m = m0 + ml + (odd ? 1 : 0);
-        if (E.out1)
-          *reinterpret_cast<double2*>(E.out1 + n + m * E.ld1) = make_double2(__dmul_rn(E.a1, lo), __dmul_rn(E.a1, hi));
+        if (E.out1) {
+          double2 o = make_double2(__dmul_rn(E.a1, lo), __dmul_rn(E.a1, hi));
+          if (E.in1a) {   // in-place accumulation: the input at the written (transposed) position
+            const double2 x = *reinterpret_cast<const double2*>(E.in1a + n + m * E.ld1a);
+            o.x = __dadd_rn(o.x, __dmul_rn(E.b1, x.x));
+            o.y = __dadd_rn(o.y, __dmul_rn(E.b1, x.y));
+          }
+          *reinterpret_cast<double2*>((E.mir1 ? E.mir1 : E.out1) + n + m * E.ld1) = o;
+        }
         if (E.out2) {
           double2 o = make_double2(__dmul_rn(E.a2, lo), __dmul_rn(E.a2, hi));
           if (E.in2a) {   // the inputs at the written (transposed) position: contiguous along n
@@ -474,7 +493,7 @@ __global__ void __launch_bounds__(C::LB_THREADS, C::LB_MINB)
         const int m = m0 + ml, n = n0 + nl;
         if (m >= P.M || n >= P.N) continue;
         if (diag && m <= n) continue;
-        epi_apply(P.epi, n, m, Cs[nl * EPI_LD + ml]);
+        epi_mirror(P.epi, n, m, Cs[nl * EPI_LD + ml]);
       }
     }
   }
@@ -584,7 +603,7 @@ __global__ void __launch_bounds__(128) gemm_small_kernel(const double* __restric
         if (m >= P.M || n >= P.N) continue;
         if ((P.flags & SYM_LOWER) && m < n) continue;
         epi_apply(P.epi, m, n, acc[fm][fn][j]);
-        if ((P.flags & SYM_MIRROR) && m > n) epi_apply(P.epi, n, m, acc[fm][fn][j]);
+        if ((P.flags & SYM_MIRROR) && (m > n || P.epi.mir1)) epi_mirror(P.epi, n, m, acc[fm][fn][j]);
       }
 }
 
@@ -683,7 +702,7 @@ __global__ void __launch_bounds__(128) gemm_small_async_kernel(const double* __r
         if (m >= P.M || n >= P.N) continue;
         if ((P.flags & SYM_LOWER) && m < n) continue;
         epi_apply(P.epi, m, n, acc[fm][fn][j]);
-        if ((P.flags & SYM_MIRROR) && m > n) epi_apply(P.epi, n, m, acc[fm][fn][j]);
+        if ((P.flags & SYM_MIRROR) && (m > n || P.epi.mir1)) epi_mirror(P.epi, n, m, acc[fm][fn][j]);
       }
 }
 
@@ -911,6 +930,7 @@ __global__ void __launch_bounds__(C::NTHREADS + 128, 1)
             for (int fn = 0; fn < FN; ++fn) ptx::dmma_8x8x4(acc[fm][fn][0], acc[fm][fn][1], a[fm][s2], b[fn][s2]);
       }
       __syncwarp();
+      ptx::fence_proxy_async();   // (generic reads of the slot before its TMA refill, as above)
       if (lane == 0) ptx::mbar_arrive(&empty[slot]);
       if (++slot == STAGES) {
         slot = 0;
@@ -987,7 +1007,7 @@ __global__ void __launch_bounds__(C::NTHREADS + 128, 1)
         }
       }
       if (P.flags & SYM_MIRROR) {
-        if (interior && !E.in1a) {
+        if (interior) {
           constexpr int NWARPS = NTHREADS / 32, NBLK = SW / 32, GROUPS = NWARPS / NBLK, PAIRS = BM / 2 / GROUPS;
           const int nl = 32 * (warp % NBLK) + lane, grp = warp / NBLK;
           const bool odd = lane & 1;
@@ -999,8 +1019,15 @@ __global__ void __launch_bounds__(C::NTHREADS + 128, 1)
             const double pa = __shfl_xor_sync(0xffffffffu, a, 1), pb = __shfl_xor_sync(0xffffffffu, b, 1);
             const double lo = odd ? pb : a, hi = odd ? b : pa;
             const int64_t m = m0 + ml + (odd ? 1 : 0);
-            if (E.out1)
-              *reinterpret_cast<double2*>(E.out1 + n + m * E.ld1) = make_double2(__dmul_rn(E.a1, lo), __dmul_rn(E.a1, hi));
+            if (E.out1) {
+              double2 o = make_double2(__dmul_rn(E.a1, lo), __dmul_rn(E.a1, hi));
+              if (E.in1a) {
+                const double2 x = *reinterpret_cast<const double2*>(E.in1a + n + m * E.ld1a);
+                o.x = __dadd_rn(o.x, __dmul_rn(E.b1, x.x));
+                o.y = __dadd_rn(o.y, __dmul_rn(E.b1, x.y));
+              }
+              *reinterpret_cast<double2*>((E.mir1 ? E.mir1 : E.out1) + n + m * E.ld1) = o;
+            }
             if (E.out2) {
               double2 o = make_double2(__dmul_rn(E.a2, lo), __dmul_rn(E.a2, hi));
               if (E.in2a) {   // the inputs at the written (transposed) position: contiguous along n
@@ -1022,7 +1049,7 @@ __global__ void __launch_bounds__(C::NTHREADS + 128, 1)
             const int m = m0 + ml, n = nbase + nl;
             if (m >= P.M || n >= P.N) continue;
             if (diag && m <= n) continue;
-            epi_apply(E, n, m, Cs[nl * EPI_LD + ml]);
+            epi_mirror(E, n, m, Cs[nl * EPI_LD + ml]);
           }
         }
       }
@@ -1140,6 +1167,11 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
     throw CudaError{CGGM_ERR_UNSUPPORTED, "gemm dimension too large"};
   if ((flags & SYM_LOWER) && (M < N || ((flags & SYM_MIRROR) && M != N)))
     throw CudaError{CGGM_ERR_SHAPE, "SYM_LOWER gemm needs M >= N (M == N with SYM_MIRROR)"};
+  if (epi.mir1 && (!(flags & SYM_MIRROR) || (flags & (SYM_LOWER | SPLIT_K2)) || !epi.out1 || epi.out2 || epi.in1a ||
+                   epi.in1b))
+    throw CudaError{CGGM_ERR_UNSUPPORTED, "mir1: SYM_MIRROR without SYM_LOWER, plain out1 only"};
+  if (!(flags & SYM_LOWER) && (flags & SYM_MIRROR) && !epi.mir1)
+    throw CudaError{CGGM_ERR_UNSUPPORTED, "SYM_MIRROR without SYM_LOWER needs mir1"};
   // (an output aliasing an operand -- an in-place B := B X^T with N <= 64 -- needs one CTA per row
   // panel, which only the TMA kernels guarantee)
   const bool aliased = epi.out1 == A || epi.out1 == B || (epi.out2 && (epi.out2 == A || epi.out2 == B));
@@ -1190,7 +1222,7 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
   {
     auto al = [](const double* q, int64_t ld) { return !q || (reinterpret_cast<uintptr_t>(q) % 16 == 0 && ld % 2 == 0); };
     P.vec = !c->no_vec_epi && !epi.in1b && al(epi.out1, epi.ld1) && al(epi.out2, epi.ld2) &&
-            al(epi.in1a, epi.ld1a) && al(epi.in2a, epi.ld2a) && al(epi.in2b, epi.ld2b);
+            al(epi.in1a, epi.ld1a) && al(epi.in2a, epi.ld2a) && al(epi.in2b, epi.ld2b) && al(epi.mir1, epi.ld1);
   }
   if ((flags & SYM_LOWER) && (M < N || ((flags & SYM_MIRROR) && M != N)))
     throw CudaError{CGGM_ERR_SHAPE, "SYM_LOWER gemm needs M >= N (M == N with SYM_MIRROR)"};

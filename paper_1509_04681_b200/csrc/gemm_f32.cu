@@ -195,6 +195,7 @@ __global__ void __launch_bounds__(FNT, 1)
           for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[kk][i], b[kk][j], acc[i][j]);
     }
     __syncwarp();
+    ptx::fence_proxy_async();   // generic reads of the stage ordered before its TMA refill (gemm.cu)
     if (lane == 0) ptx::mbar_arrive(&empty[s]);
     if (threadIdx.x == 0) {
       const int jn = it + FSTAGES - 1;
@@ -388,6 +389,8 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
     throw CudaError{CGGM_ERR_UNSUPPORTED, "gemm dimension too large"};
   if ((flags & SYM_LOWER) && (M < N || ((flags & SYM_MIRROR) && M != N)))
     throw CudaError{CGGM_ERR_SHAPE, "SYM_LOWER gemm needs M >= N (M == N with SYM_MIRROR)"};
+  if (epi.mir1 || ((flags & SYM_MIRROR) && !(flags & SYM_LOWER)))
+    throw CudaError{CGGM_ERR_UNSUPPORTED, "FP32 engines: SYM_MIRROR only with SYM_LOWER (no mir1)"};
   {  // small shapes and mid-size products with a sub-wave 64-tile grid: the 32x32 cp.async kernel
     // (an output aliasing an operand -- an in-place B := B X^T with N <= 64 -- needs one CTA per
     // row panel, which only the 128-wide kernels guarantee)

@@ -1,0 +1,51 @@
+"""Concurrency regression: an HBM-streaming kernel running beside the warp-specialised 128x64 DMMA
+tiles (grad_Lambda + the S_Lambda compaction on a side stream next to the X^T E GEMM,
+CGGM_GL_OVERLAP=1) must not change a single bit of the result.  Before the consumers' proxy fence
+(gemm.cu: fence.proxy.async before releasing a TMA-filled stage) this corrupted whole warp tiles of
+grad_Theta in most runs (tools/debug/gl_race.py)."""
+import os
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from synth.cggm_inputs import make_problem  # noqa: E402
+
+
+def _ctx(overlap):
+    from paper_1509_04681_b200 import Context
+    os.environ["CGGM_GL_OVERLAP"] = str(overlap)
+    try:
+        return Context(0)
+    finally:
+        os.environ.pop("CGGM_GL_OVERLAP", None)
+
+
+@pytest.mark.parametrize("name", ["medium"])
+def test_side_stream_overlap_is_bit_identical(name):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1509_04681_b200 import DeviceCsc, to_device_colmajor
+    from paper_1509_04681_b200.api import newton_evaluation
+    P = make_problem(name)
+    label, lam, th = P.points[0]
+    X, Y = to_device_colmajor(P.X), to_device_colmajor(P.Y)
+    Lg, Tg = DeviceCsc.from_host(lam), DeviceCsc.from_host(th)
+    cap = 4_000_000
+
+    def bufs():
+        return {k: torch.empty(cap, dtype=torch.int32, device="cuda") for k in ("L_row", "L_col", "T_row", "T_col")}
+
+    ref_ctx = _ctx(0)
+    Syy, _ = ref_ctx.cggm_covariances(X, Y, want_sxy=False)
+    ref = newton_evaluation(ref_ctx, X, Y, Syy, Lg, Tg, P.lam_L, P.lam_T, True, bufs(), composite=False)
+    ctx = _ctx(1)
+    for composite in (False, True, False, True, True, True):
+        r = newton_evaluation(ctx, X, Y, Syy, Lg, Tg, P.lam_L, P.lam_T, True, bufs(), composite=composite)
+        torch.cuda.synchronize()
+        for key in ("Sigma", "Psi", "GradL", "GradT"):
+            assert torch.equal(r[key], ref[key]), (key, composite)
+        for key in ("L_row", "L_col", "T_row", "T_col"):
+            assert torch.equal(r["active"][key], ref["active"][key]), key
+        assert r["objective"]["f"] == ref["objective"]["f"]

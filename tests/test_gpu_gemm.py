@@ -104,6 +104,48 @@ def test_gemm_sym_lower_mirror_lauum_flags(ctx, q):
     assert np.linalg.norm(out - ref) / np.linalg.norm(ref) < 1e-14
 
 
+@pytest.mark.parametrize("n2,n1", [(385, 256), (200, 128), (130, 300), (64, 40)])
+def test_gemm_mirror_block(ctx, n2, n1):
+    """The off-diagonal piece of the interleaved Sigma assembly: S21 = X22^T X21 (X22 lower
+    triangular: A_KGE_M) into one block and its transpose into the mirror block (mir1), bit-identical;
+    ragged and sub-tile shapes on every kernel family."""
+    from paper_1509_04681_b200.api import ld_of
+    rng = np.random.default_rng(n2 * 3 + n1)
+    X22 = np.tril(rng.standard_normal((n2, n2)))
+    X21 = rng.standard_normal((n2, n1))
+    ref = X22.T @ X21
+    q = n1 + n2
+    S = torch.full((q, q), 5.0, dtype=torch.float64, device="cuda").t()   # column-major, ld = q
+    ldS = ld_of(S)
+    dA, dB = dev(X22), dev(X21)
+    base = S.data_ptr()
+    st = ctx.lib.cggm_test_gemm_mir(ctx.h, 1, 0, n2, n1, n2, ctypes.c_void_p(dA.data_ptr()), ld_of(dA),
+                                    ctypes.c_void_p(dB.data_ptr()), ld_of(dB), ctypes.c_void_p(base + 8 * n1), ldS,
+                                    ctypes.c_void_p(base + 8 * n1 * ldS), 1.0, A_KGE_M)
+    ctx._check(st)
+    torch.cuda.synchronize()
+    out = S.cpu().numpy()
+    blk, mir = out[n1:, :n1], out[:n1, n1:]
+    np.testing.assert_array_equal(blk, mir.T)
+    assert np.linalg.norm(blk - ref) / np.linalg.norm(ref) < 1e-14
+    np.testing.assert_array_equal(out[:n1, :n1], 5.0)     # diagonal blocks untouched
+    np.testing.assert_array_equal(out[n1:, n1:], 5.0)
+
+
+@pytest.mark.parametrize("q,K", [(385, 300), (200, 57), (256, 513)])
+def test_gemm_sym_mirror_accumulate(ctx, q, K):
+    """S11 += X21^T X21 in place on a full symmetric S11 (SYM_LOWER | SYM_MIRROR with the output as
+    its own input): both triangles updated, bit-identical."""
+    rng = np.random.default_rng(q + K)
+    A = rng.standard_normal((K, q))
+    S0 = rng.standard_normal((q, q))
+    S0 = S0 + S0.T
+    ref = S0 + A.T @ A
+    out = run(ctx, True, False, A, A, S0, 1.0, 1.0, SYM_LOWER | SYM_MIRROR, q, q, K)
+    np.testing.assert_array_equal(out, out.T)
+    assert np.linalg.norm(out - ref) / np.linalg.norm(ref) < 1e-14
+
+
 @pytest.mark.parametrize("flags", [A_KLE_M, A_KGE_M, B_KLE_N, B_KGE_N, A_KGE_M | B_KGE_N])
 def test_gemm_triangular_k_range(ctx, flags):
     """Triangular operands with exact zeros outside the triangle: the shortened k-range must
