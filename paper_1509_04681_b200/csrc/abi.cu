@@ -167,6 +167,7 @@ cggm_status cggm_ctx_create(cggm_ctx** out, int device, cggm_dtype dtype, void* 
   c->slots.resize(WS_NUM);
   if (const char* e = std::getenv("CGGM_PRIO")) c->prio_mode = std::atoi(e);
   if (const char* e = std::getenv("CGGM_LA_MIN")) c->la_min = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_OBJ_GATE")) c->gate_cols = std::atoll(e);
   if (const char* e = std::getenv("CGGM_GL_OVERLAP")) c->gl_overlap = std::atoi(e);
   if (const char* e = std::getenv("CGGM_SIGMA_REC")) c->sig_min = std::atoi(e) > 0 ? std::max(128, std::atoi(e)) : 0;
   if (const char* e = std::getenv("CGGM_NO_SMALL_ASYNC")) c->no_small_async = std::atoi(e);
@@ -232,6 +233,7 @@ cggm_status cggm_ctx_destroy(cggm_ctx* ctx) {
     cudaStreamSynchronize(c->la_sig);
     cudaStreamDestroy(c->la_sig);
   }
+  if (c->gate_ev) cudaEventDestroy(c->gate_ev);
   if (c->gl_side) {
     cudaStreamSynchronize(c->gl_side);
     cudaStreamDestroy(c->gl_side);
@@ -1672,8 +1674,11 @@ static void newton_eval_core(Ctx* c, int64_t n, int64_t p, int64_t q, const void
   // the whole evaluation, enqueue only: fork onto the chain / objective streams, join back into
   // the caller's stream, D2H of the scalars into pinned host memory
   unsigned hin_wait = 0;   // cudaEventWaitExternal while capturing (events recorded outside the graph)
+  const bool gated = c->gate_cols > 0 && !reuse_now;
+  if (gated && !c->gate_ev) CGGM_CUDA_CHECK(cudaEventCreateWithFlags(&c->gate_ev, cudaEventDisableTiming));
   auto enqueue = [&](cudaStream_t so) {
     c->stream = so;
+    c->gate_done = false;
     if (c->prio_mode) {
       CGGM_CUDA_CHECK(cudaEventRecord(c->ev_fork, so));
       CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->hi, c->ev_fork, 0));
@@ -1708,11 +1713,6 @@ static void newton_eval_core(Ctx* c, int64_t n, int64_t p, int64_t q, const void
           CGGM_CUDA_CHECK(cudaEventRecord(c->ev_syy, c->syys));
           c->stream = c->aux;
         }
-        if (c->factor_reuse)
-          objective_fullinv_enqueue<T>(c, 1, n, q, Yd, ldy, W, ldn, Lambda, Theta, active->penalize_diag, xs_next);
-        else
-          objective_enqueue<T>(c, 1, n, q, Yd, ldy, W, ldn, Lambda, Theta, active->penalize_diag);
-        CGGM_CUDA_CHECK(cudaEventRecord(c->ev_join, c->aux));
         c->stream = s0;
         c->lane = 0;
       } catch (...) {
@@ -1720,12 +1720,36 @@ static void newton_eval_core(Ctx* c, int64_t n, int64_t p, int64_t q, const void
         c->lane = 0;
         throw;
       }
+      auto objective_part = [&]() {
+        c->stream = c->aux;
+        c->lane = 1;
+        try {
+          if (gated) CGGM_CUDA_CHECK(cudaStreamWaitEvent(c->aux, c->gate_ev, 0));
+          if (c->factor_reuse)
+            objective_fullinv_enqueue<T>(c, 1, n, q, Yd, ldy, W, ldn, Lambda, Theta, active->penalize_diag, xs_next);
+          else
+            objective_enqueue<T>(c, 1, n, q, Yd, ldy, W, ldn, Lambda, Theta, active->penalize_diag);
+          CGGM_CUDA_CHECK(cudaEventRecord(c->ev_join, c->aux));
+        } catch (...) {
+          c->stream = s0;
+          c->lane = 0;
+          throw;
+        }
+        c->stream = s0;
+        c->lane = 0;
+      };
+      if (!gated) objective_part();
       // a3, a4/a5, a6 on the chain stream (lane 0)
       if (hin) CGGM_CUDA_CHECK(cudaStreamWaitEvent(s0, hin->ev_lam, hin_wait));
       if (reuse_now)
         invert_from_kept<T>(c, 0, q, static_cast<T*>(Sigma), ldsigma, xs_prev);
       else
         invert_enqueue<T>(c, 0, Lambda, static_cast<T*>(Sigma), ldsigma, c->factor_reuse ? xs_prev : (int)WS_LINV);
+      if (gated) {
+        if (!c->gate_done) CGGM_CUDA_CHECK(cudaEventRecord(c->gate_ev, s0));   // (q below the gate column)
+        c->gate_done = false;
+        objective_part();
+      }
       CGGM_CUDA_CHECK(cudaStreamWaitEvent(s0, c->ev_w, 0));
       if (hin) CGGM_CUDA_CHECK(cudaStreamWaitEvent(s0, c->ev_syy, 0));
       Fuse fz{Lambda, Theta, active, active_ws(c, q)};

@@ -612,6 +612,12 @@ void trsm_rec(Rec<T>& R, ViewT<T> B, ViewT<T> L, int64_t col0);
 template <typename T>
 void leaf(Rec<T>& R, ViewT<T> A, ViewT<T> X, int64_t col0) {
   const int nb = (int)A.rows;
+  // gate (Ctx::gate_ev): recorded on the chain when the recursion reaches the first leaf at or past
+  // column gate_cols -- another stream's work can be held back until the factorisation is that far
+  if (R.c->gate_ev && !R.c->gate_done && col0 >= R.c->gate_cols && R.full_inverse && R.c->lane == 0) {
+    CGGM_CUDA_CHECK(cudaEventRecord(R.c->gate_ev, R.c->stream));
+    R.c->gate_done = true;
+  }
   T* xp;
   int64_t ldx;
   if (R.full_inverse) {

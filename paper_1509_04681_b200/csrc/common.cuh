@@ -80,6 +80,11 @@ struct Ctx {
   // pool of dependency events (reused across calls: every wait is enqueued before a re-record)
   cudaStream_t la_chain[2] = {nullptr, nullptr}, la_upd[2] = {nullptr, nullptr}, la_bg[2] = {nullptr, nullptr};
   cudaStream_t la_sig = nullptr;   // interleaved Sigma assembly (chol.cu), priority slot 8
+  // composite: the objective's trial factorisation starts once the inverse recursion reaches column
+  // gate_cols (CGGM_OBJ_GATE; 0 = both start together)
+  int64_t gate_cols = 0;
+  cudaEvent_t gate_ev = nullptr;
+  bool gate_done = false;
   cudaStream_t gl_side = nullptr;  // composite: grad_Lambda + the S_Lambda compaction beside the X^T E GEMM
   int gl_overlap = 0;              // CGGM_GL_OVERLAP: 1 = side stream at the greatest priority, 2 = at the least, 0 = in line
   cudaEvent_t ev_gl0 = nullptr, ev_gl1 = nullptr;
