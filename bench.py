@@ -62,8 +62,8 @@ HBM_PEAK_GBS = _hbm_peak()
 
 
 def _dominant_traffic():
-    """dram read+write bytes per launch of the largest GEMM launch (lauum), from the committed ncu
-    --set full capture (profiles/r02_ncu_dominant.json); None if absent."""
+    """dram read+write bytes per launch of the largest GEMM launch (X^T E since Sigma is assembled inside
+    the recursion), from the committed ncu --set full capture (profiles/r02_ncu_dominant.json)."""
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "r02_ncu_dominant.json")))
         return d["dram_read_bytes"] + d["dram_write_bytes"]
@@ -552,7 +552,19 @@ def main():
         Lam.val.copy_(v0)
         last = step()
         torch.cuda.synchronize()
+        # the other grad_Theta form: stored (p x q) <-> not stored, S_Theta selected in the X^T E epilogue (K01)
+        other = not args.stream_grad_theta
+
+        def step_other():
+            return newton_evaluation(ctx, X, Y, Syy, Lam, Th, P.lam_L, P.lam_T, True, bufs, stream_grad_theta=other)
+        if other or "GradT" in bufs:
+            for _ in range(2):
+                step_other()
+            other_ms = timed(step_other, kv) / kv
+        else:
+            other_ms = None
         variants = {"graph_replay_ms": elapsed / args.steps, "eager_ms": eager_ms, "changing_lambda_ms": chg_ms,
+                    ("grad_theta_not_stored_ms" if other else "grad_theta_stored_ms"): other_ms,
                     "steps": kv,
                     "changing_lambda": "off-diagonal values of Lambda* scaled by 1, 0.998, ..., 0.992 in turn, "
                                        "written into the same CSC before each step (copy timed); the graph "
@@ -747,7 +759,7 @@ def main():
                                f"({world} GPU x {ms_step:.2f} ms)",
                 "peak_source": f"live DMMA.8x8x4 microbenchmark on this GPU ({args.peak_seconds:.1f} s, "
                                "2 CTAs/SM); MEASURED_PEAKS.json has no FP64 entry",
-                "traffic_source": "dram read+write bytes per launch of the largest launch (lauum) from the "
+                "traffic_source": "dram read+write bytes per launch of the largest launch (X^T E) from the "
                                   "committed ncu --set full capture"}
         if world == 1:
             gemm_ms = sum(phases[t]["ms_per_step"] for t in GEMM_TAGS if t in phases)

@@ -124,7 +124,7 @@ cggm_status cggm_ctx_set_validate(cggm_ctx* ctx, int level);
  *     (4/3) q^3 -> q^3 flop.  The CALLER guarantees that the next Lambda equals the previous call's
  *     Lambda (the accepted line-search trial); q must match, else the call falls back to a full
  *     inverse.  Setting the option (either value) forgets the kept factor.
- *   CGGM_OPT_SIGMA_BLOCK: FP64 Sigma = L^{-T} L^{-1} of cggm_invert_logdet / cggm_newton_eval
+ *   CGGM_OPT_SIGMA_BLOCK: Sigma = L^{-T} L^{-1} of cggm_invert_logdet / cggm_newton_eval
  *     is assembled inside the recursive inverse: a recursion node at least this wide forms its
  *     off-diagonal block X22^T X21 and the update X21^T X21 of its leading block as soon as its
  *     own L^{-1} block is final, its children likewise; narrower nodes form their whole block in one

@@ -167,6 +167,7 @@ cggm_status cggm_ctx_create(cggm_ctx** out, int device, cggm_dtype dtype, void* 
   c->slots.resize(WS_NUM);
   if (const char* e = std::getenv("CGGM_PRIO")) c->prio_mode = std::atoi(e);
   if (const char* e = std::getenv("CGGM_LA_MIN")) c->la_min = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_K01")) c->k01 = std::atoi(e);
   if (const char* e = std::getenv("CGGM_OBJ_GATE")) c->gate_cols = std::atoll(e);
   if (const char* e = std::getenv("CGGM_GL_OVERLAP")) c->gl_overlap = std::atoi(e);
   if (const char* e = std::getenv("CGGM_SIGMA_REC")) c->sig_min = std::atoi(e) > 0 ? std::max(128, std::atoi(e)) : 0;
@@ -806,7 +807,7 @@ static void invert_enqueue(Ctx* c, int lane, const cggm_csc* Lambda, T* Sigma, i
     CGGM_CUDA_CHECK(cudaMemsetAsync(X, 0, (size_t)lda * q * sizeof(T), c->stream));
     const size_t tmp_elems = chol_tmp_elems(q);
     T* tmp = static_cast<T*>(ws_get(c, WS_TMP, tmp_elems * sizeof(T)));
-    if (sizeof(T) == 8 && c->sig_min > 0 && q >= c->sig_min) {   // Sigma assembled inside the recursion
+    if (c->sig_min > 0 && q >= c->sig_min) {   // Sigma assembled inside the recursion
       potrf_recursive<T>(c, Av, ViewT<T>{X, lda, q, q}, true, nullptr, slots, s.fail, tmp, tmp_elems, nullptr, 0,
                          nullptr, 0, Sigma, ldsigma);
     } else {
@@ -1169,6 +1170,23 @@ static void psi_enqueue(Ctx* c, int64_t n_local, int64_t n_total, int64_t p, int
       active_theta_chunk<T>(c, p, 0, q, GradT, ldgt, fz->Theta, o->lam_T, o->tie_eps, fz->ws, o->T_row, o->T_col,
                             o->cap_T);
     }
+  } else if (fz && sizeof(T) == 8 && !collective && !Sxy && c->k01 && p > 0) {
+    // K01: grad_Theta never stored -- S_Theta, its ties and the subgradient taken in the X^T E
+    // epilogue while each tile is in shared memory (one GEMM over all q columns, no chunks)
+    const SelWs sw = sel_ws(c, p, q);
+    EpilogueT<T> e;
+    e.a1 = 2.0 / (double)n_total;
+    {
+      Phase ph(c, TAG_ACTIVE);
+      e.sel = select_begin(c, p, q, fz->ws, sw, fz->Theta, o->lam_T, o->tie_eps);
+    }
+    {
+      Phase ph(c, TAG_GRADT);
+      gemm(c, true, false, p, q, n_local, Xd, ldx, E, lde, e, 0);
+    }
+    if (side) CGGM_CUDA_CHECK(cudaStreamWaitEvent(chain, c->ev_gl1, 0));
+    Phase ph(c, TAG_ACTIVE);
+    select_end(c, p, q, fz->ws, sw, o->T_row, o->T_col, o->cap_T);
   } else if (fz) {
     const int64_t ldc = pad_ld<T>(p);
     T* chunk = static_cast<T*>(ws_get(c, WS_GTCHUNK, (size_t)ldc * std::min<int64_t>(GT_CHUNK, q) * sizeof(T)));
@@ -1655,7 +1673,8 @@ static void newton_eval_core(Ctx* c, int64_t n, int64_t p, int64_t q, const void
     active_ws(c, q);
     ws_get(c, WS_R, (size_t)ldn * q * es);
     ws_get(c, WS_E, (size_t)ldn * q * es);
-    if (!GradT) ws_get(c, WS_GTCHUNK, (size_t)pad_ld<T>(p) * std::min<int64_t>(GT_CHUNK, q) * es);
+    if (!GradT && es == 8 && c->k01 && p > 0) sel_ws(c, p, q);
+    else if (!GradT) ws_get(c, WS_GTCHUNK, (size_t)pad_ld<T>(p) * std::min<int64_t>(GT_CHUNK, q) * es);
     ws_get(c, WS_W, (size_t)ldn * q * es);
     if (es == 8 && split_wsigma(c, n, q)) ws_get(c, WS_ACC, (size_t)ldn * q * es);
     if (c->factor_reuse) {

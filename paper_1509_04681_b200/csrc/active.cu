@@ -594,12 +594,10 @@ __global__ void __launch_bounds__(1024) k_lam_scan(int64_t q, unsigned long long
   }
 }
 
-// (row, col) entries of column j from its flag words at base[j]
-__device__ __forceinline__ void k_lam_write_col(const uint32_t* __restrict__ flags, const long long* base,
+// (row, col) entries of column j from its nch chunks of flag words flg[2c], flg[2c + 1] at base[j]
+__device__ __forceinline__ void write_col_words(const uint32_t* __restrict__ flg, int nch, const long long* base,
                                                 int32_t* __restrict__ out_row, int32_t* __restrict__ out_col,
                                                 long long cap, int64_t j) {
-  const int nch = (int)((j + 1 + 63) >> 6);
-  const uint32_t* flg = flags + tri_words_before_i(j);
   __shared__ int wcnt[NW];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int per = (nch + NW - 1) / NW;
@@ -640,6 +638,29 @@ __device__ __forceinline__ void k_lam_write_col(const uint32_t* __restrict__ fla
       pos += __popc(m0) + __popc(m1);
     }
   }
+}
+
+__device__ __forceinline__ void k_lam_write_col(const uint32_t* __restrict__ flags, const long long* base,
+                                                int32_t* __restrict__ out_row, int32_t* __restrict__ out_col,
+                                                long long cap, int64_t j) {
+  write_col_words(flags + tri_words_before_i(j), (int)((j + 1 + 63) >> 6), base, out_row, out_col, cap, j);
+}
+
+// K01: S_Theta entries of column j from the words the X^T E epilogue wrote (wpc per column)
+__global__ void __launch_bounds__(NT) k_sel_write(const uint32_t* flags, int64_t wpc, int nch, const long long* base,
+                                                  int32_t* out_row, int32_t* out_col, long long cap) {
+  const int64_t j = blockIdx.x;
+  write_col_words(flags + j * wpc, nch, base, out_row, out_col, cap, j);
+}
+
+// K01: per-column subgradient = the row tiles' partials summed in row order (fixed: reproducible)
+__global__ void k_sel_sub(int64_t q, int64_t nrow, const double* __restrict__ subpart, int64_t ld,
+                          double* __restrict__ sub_col) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= q) return;
+  double acc = 0.0;
+  for (int64_t r = 0; r < nrow; ++r) acc += subpart[r * ld + j];
+  sub_col[j] = acc;
 }
 
 // (row, col) entries of columns k and q - 1 - k from their flag words at base[]
@@ -824,6 +845,50 @@ void active_theta_chunk(Ctx* c, int64_t p, int64_t col0, int64_t ncols, const T*
       p, G, ldg, Theta->colptr, Theta->rowidx, static_cast<const T*>(Theta->val), (T)lam_T, 1, (T)tie_eps,
       ws.stateT, T_row, T_col, capT, ws.tieT, ws.subT, col0);
   post_launch(c, "k_active_onepass<T>");
+}
+
+SelWs sel_ws(Ctx* c, int64_t p, int64_t q) {
+  SelWs w;
+  w.nch = (p + 63) / 64;
+  w.wpc = 2 * w.nch;
+  const size_t fbytes = ((size_t)q * w.wpc * 4 + 255) / 256 * 256, bbytes = ((size_t)(q + 1) * 8 + 255) / 256 * 256;
+  char* base = static_cast<char*>(ws_get(c, WS_SEL, fbytes + bbytes + (size_t)w.nch * q * 8));
+  w.flags = reinterpret_cast<uint32_t*>(base);
+  w.base = reinterpret_cast<long long*>(base + fbytes);
+  w.subpart = reinterpret_cast<double*>(base + fbytes + bbytes);
+  return w;
+}
+
+SelectT select_begin(Ctx* c, int64_t p, int64_t q, const ActWs& ws, const SelWs& sw, const cggm_csc* Theta,
+                     double lam_T, double tie_eps) {
+  // (ws.stateT is zeroed by active_begin)
+  CGGM_CUDA_CHECK(cudaMemsetAsync(ws.tieT, 0, (size_t)q * 8, c->stream));
+  CGGM_CUDA_CHECK(cudaMemsetAsync(sw.subpart, 0, (size_t)sw.nch * q * 8, c->stream));
+  SelectT S;
+  S.on = 1;
+  S.lam = lam_T;
+  S.tie_eps = tie_eps;
+  S.colptr = Theta->colptr;
+  S.rowidx = Theta->rowidx;
+  S.val = static_cast<const double*>(Theta->val);
+  S.flags = sw.flags;
+  S.wpc = sw.wpc;
+  S.cnt = ws.stateT;
+  S.ties = ws.tieT;
+  S.subpart = sw.subpart;
+  S.ldsub = q;
+  return S;
+}
+
+void select_end(Ctx* c, int64_t p, int64_t q, const ActWs& ws, const SelWs& sw, int32_t* T_row, int32_t* T_col,
+                long long capT) {
+  if (q == 0) return;
+  Prof pr(c, TAG_ACTIVE);
+  k_sel_sub<<<(unsigned)((q + 255) / 256), 256, 0, c->stream>>>(q, sw.nch, sw.subpart, q, ws.subT);
+  k_lam_scan<<<1, 1024, 0, c->stream>>>(q, ws.stateT, sw.base);
+  k_sel_write<<<(unsigned)q, NT, 0, c->stream>>>(sw.flags, sw.wpc, (int)sw.nch, sw.base, T_row, T_col, capT);
+  c->launches += 2;
+  post_launch(c, "k_sel_sub/scan/write");
 }
 
 void active_end(Ctx* c, int64_t q, const ActWs& ws) {

@@ -673,7 +673,7 @@ void sig_block_product(Rec<T>& R, ViewT<T> X, int64_t col0) {   // S_node = X^T 
   cudaStream_t chain, prev;
   sig_enqueue_begin(R, chain, prev);
   {
-    Prof pr(R.c, TAG_LAUUM);
+    Phase ph(R.c, TAG_LAUUM);   // (the GEMMs record under this tag)
     EpilogueT<T> e; e.out1 = R.sig + col0 + col0 * R.ldsig; e.ld1 = R.ldsig;
     gemm(R.c, true, false, n, n, n, X.p, X.ld, X.p, X.ld, e, A_KGE_M | B_KGE_N | SYM_LOWER | SYM_MIRROR);
   }
@@ -687,7 +687,7 @@ void sig_node_pieces(Rec<T>& R, ViewT<T> X11, ViewT<T> X21, ViewT<T> X22, int64_
   cudaStream_t chain, prev;
   sig_enqueue_begin(R, chain, prev);
   {
-    Prof pr(R.c, TAG_LAUUM);
+    Phase ph(R.c, TAG_LAUUM);   // (the GEMMs record under this tag)
     {  // S21 = X22^T X21 (X22 lower: op(A) = X22^T has k >= m), S12 = S21^T by the mirrored epilogue
       EpilogueT<T> e; e.out1 = S11 + n1; e.ld1 = R.ldsig; e.mir1 = S11 + n1 * R.ldsig;
       gemm(R.c, true, false, n2, n1, n2, X22.p, X22.ld, X21.p, X21.ld, e, A_KGE_M | SYM_MIRROR);

@@ -86,6 +86,8 @@ struct Ctx {
   cudaEvent_t gate_ev = nullptr;
   bool gate_done = false;
   cudaStream_t gl_side = nullptr;  // composite: grad_Lambda + the S_Lambda compaction beside the X^T E GEMM
+  int k01 = 0;                     // CGGM_K01=1: grad_Theta = NULL selects S_Theta in the X^T E epilogue (K01) instead of
+                                   // streaming column chunks through the scan (measured slower: see DESIGN §6)
   int gl_overlap = 0;              // CGGM_GL_OVERLAP: 1 = side stream at the greatest priority, 2 = at the least, 0 = in line
   cudaEvent_t ev_gl0 = nullptr, ev_gl1 = nullptr;
   int sig_min = 4096;              // CGGM_SIGMA_REC: nodes >= this split their Sigma block (0 = one lauum after the recursion)
@@ -223,6 +225,7 @@ enum Slot {
   WS_XDIAG,         // objective: inverses of the <= 512-column diagonal blocks (q x 512)
   WS_TMP_OBJ,       // objective: recursion temporaries (full-inverse subtrees + block products)
   WS_GTCHUNK,       // streamed grad_Theta column chunk (fused active sets without a stored p x q gradient)
+  WS_SEL,           // K01: S_Theta selected in the X^T E epilogue (flag words, column bases, subgradient partials)
   WS_SCAL2,         // scalar block of the auxiliary lane
   WS_CD_U,          // Lambda sweep: U = D Sigma (q x q)
   WS_CD_V,          // Theta sweep: V = Theta Sigma (p x q)
@@ -328,6 +331,25 @@ enum GemmFlags : int {
                         // to zero give a + b in either order: the result is deterministic
 };
 
+// K01: the S_Theta selection of P:296-303 taken in the X^T E GEMM epilogue on the
+// tile of grad_Theta = a1 * acc while it is in shared memory, instead of storing the p x q gradient
+// and scanning it again (FP64 TMA kernels only).  Per output element g: flag = |g| - lam > 0 or
+// Theta_ij != 0; tie = not stored and ||g| - lam| <= tie_eps; subgradient = |g + lam sign
+// Theta_ij| for a stored nonzero, else max(|g| - lam, 0).
+struct SelectT {
+  int on = 0;
+  double lam = 0.0, tie_eps = 0.0;
+  const int64_t* colptr = nullptr;   // Theta (rows = output rows, columns = output columns), device
+  const int32_t* rowidx = nullptr;
+  const double* val = nullptr;
+  uint32_t* flags = nullptr;          // column j's words at flags + j * wpc: 2 per 64-row chunk
+  int64_t wpc = 0;                    //   (word 2c: rows 64c + 2l, word 2c + 1: rows 64c + 2l + 1, bit l)
+  unsigned long long* cnt = nullptr;  // per column: flagged count (atomic adds onto zero)
+  long long* ties = nullptr;          // per column: tie count (atomic adds onto zero)
+  double* subpart = nullptr;          // [64-row chunk][column]: subgradient partials (ld ldsub)
+  int64_t ldsub = 0;
+};
+
 template <typename T>
 struct EpilogueT {
   // out1 = a1*acc + b1*in1a + c1*in1b ; out2 = a2*acc + b2*in2a + c2*in2b (null pointers skip terms)
@@ -338,9 +360,9 @@ struct EpilogueT {
   const T* in2a = nullptr; int64_t ld2a = 0; double b2 = 0.0;
   const T* in2b = nullptr; int64_t ld2b = 0; double c2 = 0.0;
   // SYM_MIRROR without SYM_LOWER on a rectangular block: the transposed copy a1*acc goes to mir1
-  // (ld1) instead of out1 -- the off-diagonal block of a symmetric result (FP64 kernels only; no
-  // inputs, no out2)
+  // (ld1) instead of out1 -- the off-diagonal block of a symmetric result (no inputs, no out2)
   T* mir1 = nullptr;
+  SelectT sel;   // K01 selection instead of the stores (FP64 TMA kernels; out1 ignored)
 };
 using Epilogue = EpilogueT<double>;
 
@@ -373,7 +395,7 @@ template <typename T>
 void potrf_recursive(Ctx* c, ViewT<T> A, ViewT<T> Linv, bool full_inverse, T* leafinv, double* logdet_slots,
                      int* fail_col_dev, T* tmp, size_t tmp_elems, T* xdiag = nullptr, int64_t ldxd = 0,
                      T* tmp2 = nullptr, size_t tmp2_elems = 0, T* sigma = nullptr, int64_t ldsigma = 0);
-//  full_inverse with sigma != null (FP64; q >= Ctx::sig_min): Sigma = L^{-T} L^{-1} (both triangles)
+//  full_inverse with sigma != null (q >= Ctx::sig_min): Sigma = L^{-T} L^{-1} (both triangles)
 //  assembled block by block inside the recursion (chol.cu, sig_node_pieces) -- no separate lauum.
 int block_inverse_size();
 // Sigma = Linv^T Linv (full symmetric).

@@ -55,7 +55,11 @@ struct Cfg {
   static constexpr int EPI_BYTES = BN * EPI_LD * 8;
   static constexpr int MAIN_BYTES = STAGES * STAGE_BYTES;
   static constexpr int DATA_BYTES = MAIN_BYTES > EPI_BYTES ? MAIN_BYTES : EPI_BYTES;
-  static constexpr int SMEM_BYTES = DATA_BYTES + 1024 + 2 * STAGES * 8;
+  // after the ring: full / empty barriers, the K01 bitmap barrier, then the K01 stored / negative
+  // bitmaps of the tile (BM / 32 words per column each), built during the main loop
+  static constexpr int BAR_BYTES = (2 * STAGES + 2) * 8;
+  static constexpr int SEL_BYTES = BM * BN / 4;
+  static constexpr int SMEM_BYTES = DATA_BYTES + 1024 + BAR_BYTES + SEL_BYTES;
   // register cap: a 128x128 CTA (8 warps x 192) leaves 16384 registers and ~95 KB of shared memory
   // on its SM, exactly one 64x64 CTA (4 warps x 128), so latency-bound kernels of a concurrent
   // stream co-reside with the big tiles instead of waiting for a whole SM
@@ -169,6 +173,104 @@ __device__ __forceinline__ void epi_mirror(const Epilogue& E, int64_t r, int64_t
   else epi_apply(E, r, c, v);
 }
 
+// K01: the S_Theta selection on the staged tile Cs (BM x BN, column nl at Cs + nl * EPI_LD) of
+// grad_Theta = a1 * acc, in place of the stores.  Same per-element decisions as the scan
+// (k_active_vec): flag = in && (|g| - lam > 0 || stored nonzero), tie = in && !stored && ||g| - lam|
+// <= tie_eps; subgradient |g + lam sign x| for a stored nonzero x, else max(|g| - lam, 0).  Warp w
+// takes tile columns w, w + NW, ...; per column: the flag words (written), the count and tie count
+// (atomic adds: integers, order-free), and the subgradient partial (fixed shuffle tree) at
+// subpart[64-row chunk][column].  The stored entries of the tile's rows come from the Theta CSC into two
+// shared bitmaps (sel_bits: stored; + BM / 32 * BN words: negative).
+// the tile's stored-nonzero / negative bitmaps from the Theta CSC: thread t of nt owns tile columns
+// t, t + nt, ... (their words only: no sharing, no zeroing pass)
+template <int BM, int BN>
+__device__ __forceinline__ void select_bitmaps(const KParams& P, uint32_t* sel_bits, int m0, int n0, int t, int nt) {
+  const SelectT& S = P.epi.sel;
+  constexpr int WPC = BM / 32;
+  uint32_t* neg_bits = sel_bits + WPC * BN;
+  for (int nl = t; nl < BN; nl += nt) {   // one thread per tile column: its stored rows in [m0, m0 + BM)
+    uint32_t* sw = sel_bits + nl * WPC;
+    uint32_t* nw = neg_bits + nl * WPC;
+#pragma unroll
+    for (int k = 0; k < WPC; ++k) sw[k] = nw[k] = 0u;
+    const int64_t j = (int64_t)n0 + nl;
+    if (j >= P.N) continue;
+    int64_t lo = S.colptr[j], hi = S.colptr[j + 1];
+    while (lo < hi) {   // first stored row >= m0
+      const int64_t mid = (lo + hi) >> 1;
+      if (S.rowidx[mid] < m0) lo = mid + 1;
+      else hi = mid;
+    }
+    for (int64_t e = lo; e < S.colptr[j + 1]; ++e) {
+      const int r = S.rowidx[e] - m0;
+      if (r >= BM) break;
+      const double x = S.val[e];
+      if (x == 0.0) continue;
+      sw[r >> 5] |= 1u << (r & 31);
+      if (x < 0.0) nw[r >> 5] |= 1u << (r & 31);
+    }
+  }
+}
+
+// the selection itself, on the staged tile and the finished bitmaps
+template <int BM, int BN, int NTHREADS, int EPI_LD>
+__device__ __forceinline__ void select_epilogue(const KParams& P, const double* Cs, const uint32_t* sel_bits, int m0,
+                                                int n0, int tid) {
+  const SelectT& S = P.epi.sel;
+  constexpr int WPC = BM / 32, NW = NTHREADS / 32;
+  const uint32_t* neg_bits = sel_bits + WPC * BN;
+  const int w = tid >> 5, lane = tid & 31;
+  const double a1 = P.epi.a1, lam = S.lam, teps = S.tie_eps;
+  // (measured: one column at a time with the cold-chunk vote, X^T E 45.7 -> 47.9 ms; four independent
+  // (column, chunk) items at a time without the vote 49.0 ms -- the per-element work, not latency,
+  // is what the store epilogue did not have)
+  for (int nl = w; nl < BN; nl += NW) {
+    const int64_t j = (int64_t)n0 + nl;
+    if (j >= P.N) break;   // (columns ascend with nl)
+    const double* cs = Cs + nl * EPI_LD;
+#pragma unroll
+    for (int c = 0; c < BM / 64; ++c) {
+      const int64_t chunk = m0 / 64 + c;
+      if (64 * chunk >= P.M) break;
+      const int rl = 64 * c + 2 * lane;
+      const int64_t r = (int64_t)m0 + rl;
+      const bool in0 = r < P.M, in1 = r + 1 < P.M;
+      const double g0 = __dmul_rn(a1, cs[rl]), g1 = __dmul_rn(a1, cs[rl + 1]);
+      const uint32_t sw = sel_bits[nl * WPC + (rl >> 5)] >> (rl & 31);
+      const uint32_t nw = neg_bits[nl * WPC + (rl >> 5)] >> (rl & 31);
+      const bool sp0 = sw & 1u, sp1 = (sw >> 1) & 1u;
+      const double d0 = fabs(g0) - lam, d1 = fabs(g1) - lam;
+      // cold chunk (most chunks: 0.7% of grad_Theta is active at `large`): nothing within the tie band
+      // or above the threshold, no stored nonzero -> zero words, no tie / subgradient share
+      if (!__any_sync(0xffffffffu, (sw & 3u) || d0 >= -teps || d1 >= -teps)) {
+        if (lane == 0) {
+          *reinterpret_cast<uint2*>(S.flags + j * S.wpc + 2 * chunk) = make_uint2(0u, 0u);
+          S.subpart[chunk * S.ldsub + j] = 0.0;
+        }
+        continue;
+      }
+      const bool f0 = in0 && (d0 > 0.0 || sp0), f1 = in1 && (d1 > 0.0 || sp1);
+      const unsigned b0 = __ballot_sync(0xffffffffu, f0), b1 = __ballot_sync(0xffffffffu, f1);
+      long long tc = (in0 && !sp0 && fabs(d0) <= teps) + (in1 && !sp1 && fabs(d1) <= teps);
+      double sub = 0.0;
+      if (in0) sub += sp0 ? fabs(g0 + ((nw & 1u) ? -lam : lam)) : fmax(d0, 0.0);
+      if (in1) sub += sp1 ? fabs(g1 + ((nw & 2u) ? -lam : lam)) : fmax(d1, 0.0);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sub += __shfl_down_sync(0xffffffffu, sub, o);
+        tc += __shfl_down_sync(0xffffffffu, tc, o);
+      }
+      if (lane == 0) {
+        *reinterpret_cast<uint2*>(S.flags + j * S.wpc + 2 * chunk) = make_uint2(b0, b1);
+        const int cnt = __popc(b0) + __popc(b1);
+        if (cnt) atomicAdd(S.cnt + j, (unsigned long long)cnt);
+        if (tc) atomicAdd(reinterpret_cast<unsigned long long*>(S.ties + j), (unsigned long long)tc);
+        S.subpart[chunk * S.ldsub + j] = sub;
+      }
+    }
+  }
+}
+
 // x offset (within the warp's 64/32-wide slab) of fragment f, fragment row/col index r
 template <bool KINNER>
 __device__ __forceinline__ int frag_x(int f, int r) {
@@ -189,6 +291,8 @@ __global__ void __launch_bounds__(C::LB_THREADS, C::LB_MINB)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + DATA_BYTES);
   uint64_t* empty = full + STAGES;
+  uint64_t* selbar = empty + STAGES;   // K01 bitmaps built (WS: producer warps 1-3)
+  uint32_t* sel_bits = reinterpret_cast<uint32_t*>(smem + DATA_BYTES + C::BAR_BYTES);
 
   const int tid = (int)threadIdx.x - (WS ? 128 : 0);   // consumer thread index
   const int warp = tid >> 5, lane = threadIdx.x & 31;
@@ -263,6 +367,7 @@ __global__ void __launch_bounds__(C::LB_THREADS, C::LB_MINB)
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], NCW);
     }
+    ptx::mbar_init(selbar, 96);
     ptx::fence_barrier_init();
     for (int i = 0; i < STAGES - 1 && i < nkt; ++i) issue(i);
   }
@@ -270,11 +375,15 @@ __global__ void __launch_bounds__(C::LB_THREADS, C::LB_MINB)
   if (WS) {
     if (threadIdx.x < 128) {   // producer warpgroup: 40 registers, thread 0 streams the k-tiles
       asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
-      if (threadIdx.x == 0)
+      if (threadIdx.x == 0) {
         for (int j = STAGES - 1; j < nkt; ++j) {
           if (j >= STAGES) ptx::mbar_wait(&empty[j % STAGES], ((j / STAGES) & 1) ^ 1);
           issue(j);
         }
+      } else if (threadIdx.x >= 32 && P.epi.sel.on) {   // K01: warps 1-3 build the tile's bitmaps meanwhile
+        select_bitmaps<BM, BN>(P, sel_bits, m0, n0, (int)threadIdx.x - 32, 96);
+        ptx::mbar_arrive(selbar);
+      }
       return;
     }
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(C::CONS_REG) : "memory");
@@ -379,6 +488,16 @@ __global__ void __launch_bounds__(C::LB_THREADS, C::LB_MINB)
     }
   }
   cbar();
+  if (P.epi.sel.on) {   // K01: select instead of storing
+    if (WS) {
+      ptx::mbar_wait(selbar, 0);
+    } else {
+      select_bitmaps<BM, BN>(P, sel_bits, m0, n0, tid, NTHREADS);
+      cbar();
+    }
+    select_epilogue<BM, BN, NTHREADS, EPI_LD>(P, Cs, sel_bits, m0, n0, tid);
+    return;
+  }
   const bool diag = (P.flags & SYM_LOWER) && m0 < n0 + BN;   // the tile reaches above the diagonal
   if (P.ksplit > 1) {   // partial sum of this k-half into out1 (zeros + two partials: order-free)
     for (int idx = tid; idx < BM * BN; idx += NTHREADS) {
@@ -1140,7 +1259,7 @@ void run_cfg(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t Kef
   const bool AK = transA, BKI = !transB;
   gemm_log(c, C::BM, C::BN, P.M, P.N, P.K, P.flags, grid, transA, transB);
   if constexpr (C::WSP) {
-    if (C::BN == 128 && c->persist_tpc > 0 && P.ksplit == 1 && grid >= 2 * c->num_sms) {
+    if (C::BN == 128 && c->persist_tpc > 0 && P.ksplit == 1 && grid >= 2 * c->num_sms && !P.epi.sel.on) {
       if (AK && BKI) launch_pws<true, true, C>(c, ma, mb, ma2, mb2, P, grid);
       else if (AK && !BKI) launch_pws<true, false, C>(c, ma, mb, ma2, mb2, P, grid);
       else if (!AK && BKI) launch_pws<false, true, C>(c, ma, mb, ma2, mb2, P, grid);
@@ -1182,7 +1301,10 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
   const bool mid_shape = K <= c->small_kmax && tiles64 < c->num_sms && !c->no_small_async &&
                          (reinterpret_cast<uintptr_t>(A) % 16 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0) &&
                          lda % 2 == 0 && ldb % 2 == 0;
-  if ((small_shape || mid_shape) && !aliased && !(flags & SPLIT_K2) && c->force_tile != 1 && c->force_tile != 2) {
+  if (epi.sel.on && (flags & (SYM_LOWER | SYM_MIRROR | SPLIT_K2)))
+    throw CudaError{CGGM_ERR_UNSUPPORTED, "K01 selection epilogue: plain products only"};
+  if ((small_shape || mid_shape) && !aliased && !(flags & SPLIT_K2) && !epi.sel.on && c->force_tile != 1 &&
+      c->force_tile != 2) {
     KParamsS S;
     S.M = (int)M; S.N = (int)N; S.K = (int)(K > 0 ? K : 0); S.flags = flags; S.epi = epi;
     if (transA && transB) launch_small<true, true>(c, A, lda, B, ldb, S);

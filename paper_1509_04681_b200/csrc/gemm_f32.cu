@@ -75,6 +75,11 @@ __device__ __forceinline__ void epi_apply_f(const EpilogueT<float>& E, int64_t r
   }
 }
 
+__device__ __forceinline__ void epi_mirror_f(const EpilogueT<float>& E, int64_t r, int64_t c, float v) {
+  if (E.mir1) E.mir1[r + c * E.ld1] = __fmul_rn((float)E.a1, v);
+  else epi_apply_f(E, r, c, v);
+}
+
 template <bool KINNER>
 __device__ __forceinline__ int fx(int tx, int r) {
   return KINNER ? tx + 16 * r : 4 * tx + 64 * (r >> 2) + (r & 3);
@@ -227,7 +232,7 @@ __global__ void __launch_bounds__(FNT, 1)
       const int m = m0 + ml, n = n0 + nl;
       if (m >= P.M || n >= P.N) continue;
       if (diag && m <= n) continue;
-      epi_apply_f(P.epi, n, m, Cs[nl * F_EPI_LD + ml]);
+      epi_mirror_f(P.epi, n, m, Cs[nl * F_EPI_LD + ml]);
     }
   }
 }
@@ -356,7 +361,7 @@ __global__ void __launch_bounds__(128) gemm_small_f32_kernel(const float* __rest
       if (m >= P.M || n >= P.N) continue;
       if ((P.flags & SYM_LOWER) && m < n) continue;
       epi_apply_f(P.epi, m, n, acc[f][j]);
-      if ((P.flags & SYM_MIRROR) && m > n) epi_apply_f(P.epi, n, m, acc[f][j]);
+      if ((P.flags & SYM_MIRROR) && (m > n || P.epi.mir1)) epi_mirror_f(P.epi, n, m, acc[f][j]);
     }
 }
 
@@ -389,8 +394,11 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
     throw CudaError{CGGM_ERR_UNSUPPORTED, "gemm dimension too large"};
   if ((flags & SYM_LOWER) && (M < N || ((flags & SYM_MIRROR) && M != N)))
     throw CudaError{CGGM_ERR_SHAPE, "SYM_LOWER gemm needs M >= N (M == N with SYM_MIRROR)"};
-  if (epi.mir1 || ((flags & SYM_MIRROR) && !(flags & SYM_LOWER)))
-    throw CudaError{CGGM_ERR_UNSUPPORTED, "FP32 engines: SYM_MIRROR only with SYM_LOWER (no mir1)"};
+  if (epi.mir1 && (!(flags & SYM_MIRROR) || (flags & (SYM_LOWER | SPLIT_K2)) || !epi.out1 || epi.out2 || epi.in1a ||
+                   epi.in1b))
+    throw CudaError{CGGM_ERR_UNSUPPORTED, "mir1: SYM_MIRROR without SYM_LOWER, plain out1 only"};
+  if (!(flags & SYM_LOWER) && (flags & SYM_MIRROR) && !epi.mir1)
+    throw CudaError{CGGM_ERR_UNSUPPORTED, "SYM_MIRROR without SYM_LOWER needs mir1"};
   {  // small shapes and mid-size products with a sub-wave 64-tile grid: the 32x32 cp.async kernel
     // (an output aliasing an operand -- an in-place B := B X^T with N <= 64 -- needs one CTA per
     // row panel, which only the 128-wide kernels guarantee)

@@ -109,6 +109,11 @@ __device__ __forceinline__ void epi_apply_t(const EpilogueT<float>& E, int64_t r
   }
 }
 
+__device__ __forceinline__ void epi_mirror_t(const EpilogueT<float>& E, int64_t r, int64_t c, float v) {
+  if (E.mir1) E.mir1[r + c * E.ld1] = __fmul_rn((float)E.a1, v);
+  else epi_apply_t(E, r, c, v);
+}
+
 // ---------------------------------------------------------------- tcgen05 / TMEM PTX
 // round-to-nearest (ties away) to tf32 on the bit pattern: +half an ulp of the 10-bit mantissa, clear
 // the 13 low bits (a mantissa carry moves into the exponent, as it should); two integer ops instead
@@ -557,7 +562,7 @@ __global__ void __launch_bounds__(TCfg<TMA>::NT, 1)
         const int m = m0 + mm, n = n0 + nl;
         if (m >= P.M || n >= P.N) continue;
         if (diag && m <= n) continue;
-        epi_apply_t(P.epi, n, m, Cs[nl * T_EPI_LD + mm]);
+        epi_mirror_t(P.epi, n, m, Cs[nl * T_EPI_LD + mm]);
       }
     }
   }
@@ -843,7 +848,7 @@ __global__ void __launch_bounds__(TS_NT, 1)
         const int mr = m0 + mm, n = n0 + nl;
         if (mr >= P.M || n >= P.N) continue;
         if (diag && mr <= n) continue;
-        epi_apply_t(P.epi, n, mr, Cs[nl * T_EPI_LD + mm]);
+        epi_mirror_t(P.epi, n, mr, Cs[nl * T_EPI_LD + mm]);
       }
     }
   }

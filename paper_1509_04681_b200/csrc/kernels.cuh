@@ -54,6 +54,20 @@ void active_theta_chunk(Ctx* c, int64_t p, int64_t col0, int64_t ncols, const T*
                         const cggm_csc* Theta, double lam_T, double tie_eps, const ActWs& ws, int32_t* T_row,
                         int32_t* T_col, long long capT);
 void active_end(Ctx* c, int64_t q, const ActWs& ws);
+// K01: S_Theta selected in the X^T E GEMM epilogue (FP64): select_begin zeroes the tie / subgradient
+// partials and returns the epilogue's SelectT (counts into ws.stateT); after the GEMM, select_end
+// reduces the subgradient partials, scans the counts and writes the list (then active_end as usual)
+struct SelWs {
+  uint32_t* flags;
+  long long* base;
+  double* subpart;
+  int64_t nch, wpc;
+};
+SelWs sel_ws(Ctx* c, int64_t p, int64_t q);
+SelectT select_begin(Ctx* c, int64_t p, int64_t q, const ActWs& ws, const SelWs& sw, const cggm_csc* Theta,
+                     double lam_T, double tie_eps);
+void select_end(Ctx* c, int64_t p, int64_t q, const ActWs& ws, const SelWs& sw, int32_t* T_row, int32_t* T_col,
+                long long capT);
 // Single-pass ordered compaction of both lists + totals (device).  Entries at positions >= cap are
 // not written (the caller reports CGGM_ERR_CAPACITY from the totals).
 template <typename T>

@@ -275,8 +275,26 @@ def test_streamed_grad_theta_matches_stored(ctx):
     assert b["GradT"] is None
     for key in ("L_row", "L_col", "T_row", "T_col"):
         assert torch.equal(a["active"][key], b["active"][key]), key
+    for key in ("m_L", "m_T", "ties_L", "ties_T"):
+        assert a["active"][key] == b["active"][key], key
+    # the column-chunk streaming runs the stored path's scan kernel: bit-identical statistic
     assert a["active"]["subgrad_l1"] == b["active"]["subgrad_l1"]
     assert a["objective"]["f"] == b["objective"]["f"]
+    # K01 (CGGM_K01=1): S_Theta selected in the X^T E epilogue -- the same per-element decisions on the
+    # same gradient values, the subgradient summed in another order
+    import os
+    from paper_1509_04681_b200 import Context
+    os.environ["CGGM_K01"] = "1"
+    try:
+        c1 = Context(0)
+    finally:
+        os.environ.pop("CGGM_K01", None)
+    d = newton_evaluation(c1, X, Y, Syy, Lg, Tg, P.lam_L, P.lam_T, True, bufs(), stream_grad_theta=True)
+    for key in ("L_row", "L_col", "T_row", "T_col"):
+        assert torch.equal(a["active"][key], d["active"][key]), key
+    for key in ("m_L", "m_T", "ties_L", "ties_T"):
+        assert a["active"][key] == d["active"][key], key
+    assert d["active"]["subgrad_l1"] == pytest.approx(a["active"]["subgrad_l1"], rel=1e-13)
 
 
 def test_composite_graph_replay(ctx):

@@ -127,3 +127,25 @@ def test_non_pd_reported_with_interleaved_sigma(ctx):
     lmin = 1.25 - math.cos(math.pi / (q + 1))
     Sg, ld, pd, fc = ctx.cggm_invert_logdet(DeviceCsc.from_host(csc_from_dense(A - (1 + 1e-6) * lmin * np.eye(q))))
     assert not pd and 0 <= fc < q
+
+
+@pytest.mark.parametrize("block", [128, 512])
+def test_fp32_variant_interleaved_sigma(block):
+    """The FP32 variant (3xTF32 / FFMA engines with the mirrored off-diagonal epilogue): the P4 chain
+    closed form within the FP32 contract (rel-F 1e-4) and the one-product FP32 Sigma to fp32 rounding."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1509_04681_b200 import Context, DeviceCsc, _abi
+    from tests.test_oracle_pins import chain_dense, chain_sigma_closed_form
+    c = Context(0, dtype="f32")
+    q = 2500
+    L = DeviceCsc.from_host(csc_from_dense(chain_dense(q)), dtype=torch.float32)
+    c.set_option(_abi.CGGM_OPT_SIGMA_BLOCK, 0)
+    S0 = c.cggm_invert_logdet(L)[0].double().cpu().numpy()
+    c.set_option(_abi.CGGM_OPT_SIGMA_BLOCK, block)
+    S1, ld, pd, fc = c.cggm_invert_logdet(L)
+    S1 = S1.double().cpu().numpy()
+    assert pd
+    np.testing.assert_array_equal(S1, S1.T)
+    assert relf(S1, chain_sigma_closed_form(q)) <= 1e-4
+    assert relf(S1, S0) <= 1e-5

@@ -14,11 +14,14 @@ from synth.cggm_inputs import make_problem  # noqa
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="large")
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--only", default="", help="f32 or f64: time one dtype only")
 args = ap.parse_args()
 P = make_problem(args.config)
 _, lam, th = [pt for pt in P.points if pt[0] == "truth"][0]
 out = {"config": args.config}
 for dt, tdt in (("f32", torch.float32), ("f64", torch.float64)):
+    if args.only and dt != args.only:
+        continue
     ctx = Context(0, dtype=dt)
     X, Y = to_device_colmajor(P.X, dtype=tdt), to_device_colmajor(P.Y, dtype=tdt)
     L, T = DeviceCsc.from_host(lam, dtype=tdt), DeviceCsc.from_host(th, dtype=tdt)
@@ -43,5 +46,6 @@ for dt, tdt in (("f32", torch.float32), ("f64", torch.float64)):
                "m_L": r["active"]["m_L"], "m_T": r["active"]["m_T"]}
     del ctx, X, Y, L, T, Syy, bufs, r
     torch.cuda.empty_cache()
-out["f_rel_diff"] = abs(out["f32"]["f"] - out["f64"]["f"]) / abs(out["f64"]["f"])
+if not args.only:
+    out["f_rel_diff"] = abs(out["f32"]["f"] - out["f64"]["f"]) / abs(out["f64"]["f"])
 print(json.dumps(out))

@@ -18,6 +18,7 @@ ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--part", default="all", choices=["all", "invert", "psi", "objective", "active"])
+ap.add_argument("--no-grad-theta", action="store_true", help="GradT = NULL (K01: S_Theta selected in the X^T E epilogue)")
 args = ap.parse_args()
 
 P = make_problem(args.config)
@@ -38,7 +39,7 @@ for k, c in (("L_row", cnt["m_L"]), ("L_col", cnt["m_L"]), ("T_row", cnt["m_T"])
 
 def step():
     if args.part == "all":
-        newton_evaluation(ctx, X, Y, Syy, L, T, P.lam_L, P.lam_T, True, bufs)
+        newton_evaluation(ctx, X, Y, Syy, L, T, P.lam_L, P.lam_T, True, bufs, stream_grad_theta=args.no_grad_theta)
     elif args.part == "invert":
         ctx.cggm_invert_logdet(L, Sigma=Sigma)
     elif args.part == "psi":
