@@ -128,8 +128,9 @@ cggm_status cggm_ctx_set_validate(cggm_ctx* ctx, int level);
  *     is assembled inside the recursive inverse: a recursion node at least this wide forms its
  *     off-diagonal block X22^T X21 and the update X21^T X21 of its leading block as soon as its
  *     own L^{-1} block is final, its children likewise; narrower nodes form their whole block in one
- *     product (default 4096; 0 = one symmetric product after the recursion; values below 128 are
- *     refused).  Sums of the same products in a different split of the k-range only.
+ *     product (default 4096 for FP64, 0 for the FP32 variant -- measured slower there; setting the
+ *     option sets both; 0 = one symmetric product after the recursion; values below 128 are refused).
+ *     Sums of the same products in a different split of the k-range only.
  * Unknown option -> CGGM_ERR_INVALID_ARG. */
 typedef enum cggm_option {
   CGGM_OPT_LOOKAHEAD_MIN = 0, CGGM_OPT_GRAPHS = 1, CGGM_OPT_FACTOR_REUSE = 2, CGGM_OPT_SIGMA_BLOCK = 3

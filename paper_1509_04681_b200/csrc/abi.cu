@@ -171,6 +171,8 @@ cggm_status cggm_ctx_create(cggm_ctx** out, int device, cggm_dtype dtype, void* 
   if (const char* e = std::getenv("CGGM_OBJ_GATE")) c->gate_cols = std::atoll(e);
   if (const char* e = std::getenv("CGGM_GL_OVERLAP")) c->gl_overlap = std::atoi(e);
   if (const char* e = std::getenv("CGGM_SIGMA_REC")) c->sig_min = std::atoi(e) > 0 ? std::max(128, std::atoi(e)) : 0;
+  if (const char* e = std::getenv("CGGM_SIGMA_REC_F32"))
+    c->sig_min_f32 = std::atoi(e) > 0 ? std::max(128, std::atoi(e)) : 0;
   if (const char* e = std::getenv("CGGM_NO_SMALL_ASYNC")) c->no_small_async = std::atoi(e);
   if (const char* e = std::getenv("CGGM_GRAPH")) c->use_graphs = std::atoi(e);
   if (const char* e = std::getenv("CGGM_SMALL_KMAX")) c->small_kmax = std::atoi(e);
@@ -297,7 +299,7 @@ cggm_status cggm_ctx_set_option(cggm_ctx* ctx, int option, int64_t value) {
       return CGGM_OK;
     case CGGM_OPT_SIGMA_BLOCK:
       if (value != 0 && (value < 128 || value > (1 << 30))) return CGGM_ERR_INVALID_ARG;
-      c->sig_min = (int)value;
+      c->sig_min = c->sig_min_f32 = (int)value;
       return CGGM_OK;
     default:
       return CGGM_ERR_INVALID_ARG;
@@ -807,7 +809,8 @@ static void invert_enqueue(Ctx* c, int lane, const cggm_csc* Lambda, T* Sigma, i
     CGGM_CUDA_CHECK(cudaMemsetAsync(X, 0, (size_t)lda * q * sizeof(T), c->stream));
     const size_t tmp_elems = chol_tmp_elems(q);
     T* tmp = static_cast<T*>(ws_get(c, WS_TMP, tmp_elems * sizeof(T)));
-    if (c->sig_min > 0 && q >= c->sig_min) {   // Sigma assembled inside the recursion
+    const int smin = sizeof(T) == 8 ? c->sig_min : c->sig_min_f32;
+    if (smin > 0 && q >= smin) {   // Sigma assembled inside the recursion
       potrf_recursive<T>(c, Av, ViewT<T>{X, lda, q, q}, true, nullptr, slots, s.fail, tmp, tmp_elems, nullptr, 0,
                          nullptr, 0, Sigma, ldsigma);
     } else {
@@ -1798,7 +1801,7 @@ static void newton_eval_core(Ctx* c, int64_t n, int64_t p, int64_t q, const void
   // GPU works through it, so the second could not start alongside).  A new argument set runs
   // eagerly once (allocating anything missing), the second call with the same arguments captures.
   std::vector<int64_t> key = {n, p, q, ldx, ldy, ldsyy, ldsigma, ldpsi, ldgl, ldgt, (int64_t)c->ws_generation,
-                              (int64_t)c->dtype, c->prio_mode, c->la_min, (int64_t)s_caller, c->sig_min};
+                              (int64_t)c->dtype, c->prio_mode, c->la_min, (int64_t)s_caller, c->sig_min, c->sig_min_f32};
   for (const void* ptr : {X, Y, Syy, (const void*)Sigma, (const void*)Psi, (const void*)GradL, (const void*)GradT})
     key.push_back((int64_t)ptr);
   for (const cggm_csc* m : {Lambda, Theta}) {

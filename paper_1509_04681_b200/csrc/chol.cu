@@ -846,10 +846,11 @@ void potrf_recursive(Ctx* c, ViewT<T> A, ViewT<T> Linv, bool full_inverse, T* le
   if (full_inverse) R.tmp_off = tmp_slices(A.cols, nullptr);
   const bool sig = full_inverse && sigma != nullptr;
   if (sig) {
-    if (c->sig_min < 2 * NB) throw CudaError{CGGM_ERR_INVALID_ARG, "interleaved Sigma needs sig_min >= 128"};
+    if ((sizeof(T) == 8 ? c->sig_min : c->sig_min_f32) < 2 * NB)
+      throw CudaError{CGGM_ERR_INVALID_ARG, "interleaved Sigma needs sig_min >= 128"};
     R.sig = sigma;
     R.ldsig = ldsigma;
-    R.sig_min = c->sig_min;
+    R.sig_min = sizeof(T) == 8 ? c->sig_min : c->sig_min_f32;
   }
   Phase ph(c, TAG_CHOL_GEMM);
   const int lane = c->lane;

@@ -91,6 +91,7 @@ struct Ctx {
   int gl_overlap = 0;              // CGGM_GL_OVERLAP: 1 = side stream at the greatest priority, 2 = at the least, 0 = in line
   cudaEvent_t ev_gl0 = nullptr, ev_gl1 = nullptr;
   int sig_min = 4096;              // CGGM_SIGMA_REC: nodes >= this split their Sigma block (0 = one lauum after the recursion)
+  int sig_min_f32 = 0;             // the same for the FP32 variant (CGGM_SIGMA_REC_F32; measured slower at `large`: off)
   std::vector<cudaEvent_t> la_events;
   size_t la_next = 0;
   int la_min = 256;              // defer only when the deferred block is at least this wide (CGGM_LA_MIN; 0 = off)
