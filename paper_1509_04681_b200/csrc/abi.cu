@@ -168,6 +168,7 @@ cggm_status cggm_ctx_create(cggm_ctx** out, int device, cggm_dtype dtype, void* 
   if (const char* e = std::getenv("CGGM_PRIO")) c->prio_mode = std::atoi(e);
   if (const char* e = std::getenv("CGGM_LA_MIN")) c->la_min = std::atoi(e);
   if (const char* e = std::getenv("CGGM_K01")) c->k01 = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_PDL")) c->pdl = std::atoi(e);
   if (const char* e = std::getenv("CGGM_OBJ_GATE")) c->gate_cols = std::atoll(e);
   if (const char* e = std::getenv("CGGM_GL_OVERLAP")) c->gl_overlap = std::atoi(e);
   if (const char* e = std::getenv("CGGM_SIGMA_REC")) c->sig_min = std::atoi(e) > 0 ? std::max(128, std::atoi(e)) : 0;

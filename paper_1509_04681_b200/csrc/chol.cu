@@ -66,6 +66,8 @@ __global__ void __launch_bounds__(LEAF_THREADS, CGGM_LEAF_MINB) leaf_potrf_trtri
   __shared__ T diag[NB], invd[NB];
   __shared__ int fail_sm;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  ptx::pdl_wait();
+  ptx::pdl_trigger();   // (one CTA: the successor may be scheduled now; it waits for this grid to complete)
 #ifdef CGGM_LEAF_TIMING
   long long lt_[8];
 #define LT(i) do { if (t == 0) lt_[i] = clock64(); } while (0)
@@ -451,6 +453,8 @@ __global__ void __launch_bounds__(LEAF_THREADS, CGGM_LEAF_MINB) leaf_rec_inverse
   __shared__ T diag[NB], invd[NB];
   __shared__ int fail_sm;
   const int t = threadIdx.x;
+  ptx::pdl_wait();
+  ptx::pdl_trigger();   // (one CTA: the successor may be scheduled now; it waits for this grid to complete)
   {
     constexpr int PER = NB * NB / LEAF_THREADS, HALF = PER / 2;
 #pragma unroll
@@ -636,14 +640,13 @@ void leaf(Rec<T>& R, ViewT<T> A, ViewT<T> X, int64_t col0) {
       CGGM_CUDA_CHECK(cudaFuncSetAttribute(leaf_rec_inverse<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            leaf_smem_bytes<T>()));
     });
-    leaf_rec_inverse<T><<<1, LEAF_THREADS, leaf_smem_bytes<T>(), R.c->stream>>>(A.p, A.ld, nb, xp, ldx,
-                                                                               R.logdet_slots + col0 / NB, R.fail_col,
-                                                                               (int)col0);
+    launch_pdl(R.c, leaf_rec_inverse<T>, dim3(1), dim3(LEAF_THREADS), leaf_smem_bytes<T>(), (const T*)A.p, A.ld, nb,
+               xp, ldx, R.logdet_slots + col0 / NB, R.fail_col, (int)col0);
     post_launch(R.c, "leaf_rec_inverse");
     return;
   }
-  leaf_potrf_trtri<T><<<1, LEAF_THREADS, leaf_smem_bytes<T>(), R.c->stream>>>(A.p, A.ld, nb, xp, ldx, R.full_inverse ? 0 : 1,
-                                                        R.logdet_slots + col0 / NB, R.fail_col, (int)col0);
+  launch_pdl(R.c, leaf_potrf_trtri<T>, dim3(1), dim3(LEAF_THREADS), leaf_smem_bytes<T>(), A.p, A.ld, nb, xp, ldx,
+             R.full_inverse ? 0 : 1, R.logdet_slots + col0 / NB, R.fail_col, (int)col0);
   post_launch(R.c, "leaf_potrf_trtri");
 }
 

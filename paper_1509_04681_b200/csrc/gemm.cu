@@ -288,6 +288,7 @@ __global__ void __launch_bounds__(C::LB_THREADS, C::LB_MINB)
   constexpr int EPI_LD = C::EPI_LD, NTHREADS = C::NTHREADS;
   constexpr bool WS = C::WSP;
   extern __shared__ uint8_t smem_raw[];
+  ptx::pdl_wait();   // (launched with the PDL attribute: the predecessor's output is visible from here)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + DATA_BYTES);
   uint64_t* empty = full + STAGES;
@@ -472,6 +473,9 @@ __global__ void __launch_bounds__(C::LB_THREADS, C::LB_MINB)
   }
 
   // ------------------------------------------------ epilogue through shared memory
+  // every CTA of the grid has been scheduled once this one reaches its epilogue: the successor's CTAs
+  // may be scheduled when all have (it still waits for this grid's completion in pdl_wait)
+  if (tid == 0) ptx::pdl_trigger();
   cbar();
   double* Cs = reinterpret_cast<double*>(smem);
   {
@@ -643,6 +647,8 @@ __global__ void __launch_bounds__(128) gemm_small_kernel(const double* __restric
   // so each chunk costs one L2 round trip overlapped with the DMMAs and one barrier
   __shared__ double As[2][SKC][SLD];
   __shared__ double Bs[2][SKC][SLD];
+  ptx::pdl_wait();
+  ptx::pdl_trigger();
   const int m0 = blockIdx.y * ST, n0 = blockIdx.x * ST;
   if ((P.flags & SYM_LOWER) && m0 + ST - 1 < n0) return;   // tile strictly above the diagonal
   int kbeg = 0, kend = P.K;
@@ -740,6 +746,8 @@ __global__ void __launch_bounds__(128) gemm_small_async_kernel(const double* __r
                                                                 const double* __restrict__ B, int64_t ldb,
                                                                 const KParamsS P) {
   extern __shared__ __align__(16) double sa_smem[];
+  ptx::pdl_wait();
+  ptx::pdl_trigger();   // (at most a wave of CTAs: the successor's CTAs queue behind this grid's)
   const int m0 = blockIdx.y * ST, n0 = blockIdx.x * ST;
   if ((P.flags & SYM_LOWER) && m0 + ST - 1 < n0) return;   // tile strictly above the diagonal
   int kbeg = 0, kend = P.K;
@@ -836,10 +844,10 @@ void launch_small(Ctx* c, const double* A, int64_t lda, const double* B, int64_t
       CGGM_CUDA_CHECK(cudaFuncSetAttribute(gemm_small_async_kernel<TA, TB>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, SA_SMEM));
     });
-    gemm_small_async_kernel<TA, TB><<<grid, 128, SA_SMEM, c->stream>>>(A, lda, B, ldb, P);
+    launch_pdl(c, gemm_small_async_kernel<TA, TB>, grid, dim3(128), SA_SMEM, A, lda, B, ldb, P);
     post_launch(c, "gemm_small_async_kernel");
   } else {
-    gemm_small_kernel<TA, TB><<<grid, 128, 0, c->stream>>>(A, lda, B, ldb, P);
+    launch_pdl(c, gemm_small_kernel<TA, TB>, grid, dim3(128), 0, A, lda, B, ldb, P);
     post_launch(c, "gemm_small_kernel");
   }
 }
@@ -884,7 +892,7 @@ void launch(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensor
                                          (int)cudaSharedmemCarveoutMaxShared));
   });
   Prof pr(c, c->cur_tag);
-  gemm_dmma_kernel<AK, BKI, C><<<grid, C::LB_THREADS, C::SMEM_BYTES, c->stream>>>(ma, mb, ma2, mb2, P);
+  launch_pdl(c, gemm_dmma_kernel<AK, BKI, C>, dim3(grid), dim3(C::LB_THREADS), C::SMEM_BYTES, ma, mb, ma2, mb2, P);
   post_launch(c, "gemm_dmma_kernel");
 }
 
