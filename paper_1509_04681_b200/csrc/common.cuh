@@ -88,7 +88,7 @@ struct Ctx {
   bool gate_done = false;
   cudaStream_t gl_side = nullptr;  // composite: grad_Lambda + the S_Lambda compaction beside the X^T E GEMM
   int pdl = 0;                     // CGGM_PDL=1: programmatic dependent launch for the recursion's kernels (leaves, FP64
-                                   // GEMMs): recursion latency -9..-13% alone, the `large` step unchanged, FP32 slower
+                                   // GEMMs): recursion latency -9..-13% alone, the `large` steps (FP64, FP32) unchanged
   int k01 = 0;                     // CGGM_K01=1: grad_Theta = NULL selects S_Theta in the X^T E epilogue (K01) instead of
                                    // streaming column chunks through the scan (measured slower: see DESIGN §6)
   int gl_overlap = 0;              // CGGM_GL_OVERLAP: 1 = side stream at the greatest priority, 2 = at the least, 0 = in line
