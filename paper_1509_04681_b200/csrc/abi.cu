@@ -752,15 +752,15 @@ cggm_status cggm_theta_cd_rows(cggm_ctx* ctx, int64_t p, int64_t q, const void* 
 int cggm::stream_priority(int which) {
   // which: 0 chain tail (Sigma product, W Sigma, Psi, grad_Theta), 1 objective origin, 2-4 inverse
   // recursion (critical chain, deferred updates, background products), 5-7 the objective's
-  // recursion, 3 also S_yy, 8 the Sigma blocks formed inside the inverse recursion.  The recursions' critical chains outrank the big throughput GEMMs, so
+  // recursion, 8 the Sigma blocks formed inside the inverse recursion, 9 the host-input S_yy.  The recursions' critical chains outrank the big throughput GEMMs, so
   // their latency-bound kernels start as soon as SMs free up (measured 429.7 -> 426.1 ms at large
   // against {0, 5, 0, 1, 2, 3, 4, 5}).
-  static int off[9] = {4, 5, 1, 2, 3, 0, 4, 5, 3};
+  static int off[10] = {4, 5, 1, 2, 3, 0, 4, 5, 3, 2};
   static bool init = false;
   if (!init) {
     if (const char* e = std::getenv("CGGM_PRIO_SCHEME")) {
       int k = 0;
-      for (const char* q = e; *q && k < 9; ++k) {
+      for (const char* q = e; *q && k < 10; ++k) {
         off[k] = std::atoi(q);
         while (*q && *q != ',') ++q;
         if (*q == ',') ++q;
@@ -2128,7 +2128,7 @@ cggm_status cggm_newton_eval_host(cggm_ctx* ctx, int64_t n, int64_t p, int64_t q
     check_csc_host("Theta", Theta, p, q);
     if (!c->copy) {
       CGGM_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
-      CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->syys, cudaStreamNonBlocking, stream_priority(3)));
+      CGGM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->syys, cudaStreamNonBlocking, stream_priority(9)));
       for (cudaEvent_t* e : {&c->ev_h_lam, &c->ev_h_xt, &c->ev_h_y})
         CGGM_CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }

@@ -149,3 +149,20 @@ def test_fp32_variant_interleaved_sigma(block):
     np.testing.assert_array_equal(S1, S1.T)
     assert relf(S1, chain_sigma_closed_form(q)) <= 1e-4
     assert relf(S1, S0) <= 1e-5
+
+
+@pytest.mark.parametrize("q,ld_extra", [(700, 1), (4097, 3)])
+def test_odd_leading_dimension_and_just_above_block(ctx, q, ld_extra):
+    """Sigma into a caller buffer with an odd leading dimension (the mirrored epilogue's scalar path)
+    and q just above the default block size (root split, one-product children): P4 closed form."""
+    from paper_1509_04681_b200 import DeviceCsc
+    from tests.test_oracle_pins import chain_dense, chain_sigma_closed_form
+    set_block(ctx, 128 if q < 1000 else 4096)
+    base = torch.full((q, q + ld_extra), -7.0, dtype=torch.float64, device="cuda")   # ld = q + ld_extra
+    Sg = base.t()[:q, :q]
+    S, ld, pd, fc = ctx.cggm_invert_logdet(DeviceCsc.from_host(csc_from_dense(chain_dense(q))), Sigma=Sg)
+    assert pd
+    out = S.cpu().numpy()
+    np.testing.assert_array_equal(out, out.T)
+    assert relf(out, chain_sigma_closed_form(q)) <= 1e-12
+    np.testing.assert_array_equal(base.t()[q:, :].cpu().numpy(), -7.0)   # padding rows untouched
