@@ -579,15 +579,23 @@ __global__ void __launch_bounds__(TCfg<TMA>::NT, 1)
 // SS form's A operand reads (half of its 122 B/clk of shared-memory traffic) disappear.  TMEM: chunk
 // accumulators X0, X1 (cols 0-255; hi*hi AND the corrections, chunks of TS_CH k-tiles drained into
 // fp32 registers) and 4 A stages of 64 columns (hi 32 + lo 32) at 256..511.
-constexpr int TS_CONV = 128;                 // converter threads (warps 0-3: TMEM lane quarters)
+// CGGM_TS_CONV8 = 1: eight converter warps (two per TMEM lane quarter, each taking half of the k-tile's
+// 32 k) instead of four -- the four were the bound (ncu, 8192^3: tensor pipe 57.7% active, the MMA
+// waiting on the split stages); 16 warps in four warpgroups then, registers rebalanced by setmaxnreg
+// (converters 96, drain 232, MMA / TMA / two idle warps 40)
+#ifndef CGGM_TS_CONV8
+#define CGGM_TS_CONV8 1
+#endif
+constexpr int TS_CONV = CGGM_TS_CONV8 ? 256 : 128;   // converter threads (warps 0-3 (and 4-7): TMEM lane quarters)
+constexpr int TS_KH = TS_CONV / 128;          // k-parts of a row (one per converter warp of a lane quarter)
 constexpr int TS_NS = 4;                     // split stages (TMEM A, shared B)
 constexpr int TS_NRAW = 3;                   // raw TMA stages
 constexpr int TS_BSTAGE = 2 * T_OP;          // B hi + lo
-constexpr int TS_BPER = TBN * TBK / 4 / TS_CONV;   // raw B 16-byte chunks per converter thread (8)
+constexpr int TS_BPER = TBN * TBK / 4 / TS_CONV;   // raw B 16-byte chunks per converter thread (8 / 4)
 constexpr int TS_DATA = TS_NS * TS_BSTAGE + TS_NRAW * T_RAW;   // 128 + 96 KB
 static_assert(TBN * T_EPI_LD * 4 <= TS_DATA, "epilogue tile must fit");
 constexpr int TS_SMEM = TS_DATA + 1024 + 256;
-constexpr int TS_NT = TS_CONV + T_DRAIN + 64;  // + MMA warp (8) + TMA warp (9)
+constexpr int TS_NT = CGGM_TS_CONV8 ? 512 : TS_CONV + T_DRAIN + 64;  // + MMA warp, TMA warp (+ 2 idle: whole warpgroups)
 constexpr int TS_DW0 = TS_CONV / 32, TS_MMA = TS_DW0 + 4, TS_TMAW = TS_MMA + 1;
 
 __device__ __forceinline__ void umma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
@@ -609,22 +617,35 @@ __device__ __forceinline__ void tmem_st32_nowait(uint32_t taddr, const uint32_t 
       : "memory");
 }
 
-// row m of the raw A tile (TMA SWIZZLE_128B layout) -> 32 k-values
-template <bool AK>
-__device__ __forceinline__ void raw_a_row(uint32_t raw, int m, float (&v)[32]) {
+// row m of the raw A tile (TMA SWIZZLE_128B layout) -> the KN k-values k0 .. k0 + KN - 1
+template <bool AK, int KN = 32>
+__device__ __forceinline__ void raw_a_row(uint32_t raw, int m, float (&v)[KN], int k0 = 0) {
   if (AK) {   // K-inner: row m = one 128-byte row, 16-byte chunk c at c ^ (m & 7)
 #pragma unroll
-    for (int c = 0; c < 8; ++c)
+    for (int c = 0; c < KN / 4; ++c) {
+      const int cc = k0 / 4 + c;
       asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
                    : "=f"(v[4 * c]), "=f"(v[4 * c + 1]), "=f"(v[4 * c + 2]), "=f"(v[4 * c + 3])
-                   : "r"(raw + m * 128 + ((c ^ (m & 7)) << 4)));
+                   : "r"(raw + m * 128 + ((cc ^ (m & 7)) << 4)));
+    }
   } else {    // MN-inner: element (m, k) in chunk m / 32, row k, 16-byte chunk ((m % 32) / 4) ^ (k & 7)
     const uint32_t base = (m >> 5) * 4096 + (m & 3) * 4;
     const int mc = (m & 31) >> 2;
 #pragma unroll
-    for (int k = 0; k < 32; ++k)
-      asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(v[k]) : "r"(raw + base + k * 128 + ((mc ^ (k & 7)) << 4)));
+    for (int e = 0; e < KN; ++e) {
+      const int k = k0 + e;
+      asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(v[e]) : "r"(raw + base + k * 128 + ((mc ^ (k & 7)) << 4)));
+    }
   }
+}
+
+__device__ __forceinline__ void tmem_st16_nowait(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
 }
 
 template <bool AK, bool BKI>
@@ -682,8 +703,7 @@ __global__ void __launch_bounds__(TS_NT, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t sbase = ptx::smem_u32(smem);
   const uint32_t rbase = sbase + TS_NS * TS_BSTAGE;
-
-  if (warp == TS_MMA) {
+  auto mma_role = [&]() {
     // the whole warp walks the loop (warp-uniform control flow: the descriptors stay in uniform
     // registers); one elected lane issues the MMAs and their commits
     if (nkt > 0) {
@@ -721,7 +741,8 @@ __global__ void __launch_bounds__(TS_NT, 1)
       if (leader) umma_commit(accf);
     }
     __syncwarp();
-  } else if (warp == TS_TMAW) {
+  };
+  auto tma_role = [&]() {
     if (lane == 0 && nkt > 0) {
       int a_boxes = 0, b_boxes = 0;
       if (!AK)
@@ -750,12 +771,14 @@ __global__ void __launch_bounds__(TS_NT, 1)
       }
     }
     __syncwarp();
-  } else if (warp < TS_DW0) {
+  };
+  auto conv_role = [&]() {
     // ---- converters: A row (32 k) of this thread's TMEM lane -> hi / lo columns of the stage; B tile
     // -> hi / lo in shared memory, one 16-byte chunk at a time (issuing all raw loads of a k-tile
     // first and storing after the split measured no faster)
-    const int m = warp * 32 + lane;
-    const uint32_t lanebase = tmem + ((uint32_t)(warp * 32) << 16);
+    const int lq = warp & 3, kh = warp >> 2;   // TMEM lane quarter, k-part of the rows
+    const int m = lq * 32 + lane;
+    const uint32_t lanebase = tmem + ((uint32_t)(lq * 32) << 16);
     // measurement aid (CGGM_TF32_DEBUG bit 1): hi = the fp32 bits unrounded, so lo = v - hi = 0 and
     // the MMA sees the raw operand (how the tensor core reads the 13 low bits)
     const uint32_t h_add = (P.dbg & 2) ? 0u : 0x1000u, h_mask = (P.dbg & 2) ? 0xFFFFFFFFu : 0xFFFFE000u;
@@ -768,9 +791,9 @@ __global__ void __launch_bounds__(TS_NT, 1)
       }
       const uint32_t rw = rbase + rs * T_RAW;
       if (!(P.dbg & 4)) {   // (bit 2: measurement aid -- skip the split and the stores; garbage product)
-      {
+      if (TS_KH == 1) {
         float v[32];
-        raw_a_row<AK>(rw, m, v);
+        raw_a_row<AK, 32>(rw, m, v);
         uint32_t h[32], l[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
@@ -780,6 +803,18 @@ __global__ void __launch_bounds__(TS_NT, 1)
         const uint32_t ac = lanebase + 256u + (uint32_t)s * 64u;
         tmem_st32_nowait(ac, h);
         tmem_st32_nowait(ac + 32u, l);
+      } else {   // this warp's 16 of the row's 32 k: hi at columns 16 kh .., lo at 32 + 16 kh ..
+        float v[16];
+        raw_a_row<AK, 16>(rw, m, v, 16 * kh);
+        uint32_t h[16], l[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          h[e] = (__float_as_uint(v[e]) + h_add) & h_mask;
+          l[e] = lo_tf32(v[e], h[e]);
+        }
+        const uint32_t ac = lanebase + 256u + (uint32_t)s * 64u + 16u * (uint32_t)kh;
+        tmem_st16_nowait(ac, h);
+        tmem_st16_nowait(ac + 32u, l);
       }
       const uint32_t st = sbase + s * TS_BSTAGE;
 #pragma unroll
@@ -801,7 +836,8 @@ __global__ void __launch_bounds__(TS_NT, 1)
       ptx::mbar_arrive(&full[s]);
       ptx::mbar_arrive(&rempty[rs]);
     }
-  } else {
+  };
+  auto drain_role = [&]() {
     // ---- drain warps 4-7: chunk partials (TMEM X0 / X1) added into fp32 registers, then the epilogue
     const int dt = tid - TS_CONV;
     const int row = (warp - TS_DW0) * 32 + lane;
@@ -851,6 +887,30 @@ __global__ void __launch_bounds__(TS_NT, 1)
         epi_mirror_t(P.epi, n, mr, Cs[nl * T_EPI_LD + mm]);
       }
     }
+  };
+  if (CGGM_TS_CONV8) {
+    // registers by warpgroup (each setmaxnreg executed by its whole warpgroup at one point, the role's
+    // code dominated by it): converters 96, drain 232, MMA / TMA / two idle warps 40
+    const int wg = warp >> 2;
+    if (wg < 2) {
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 96;\n" ::: "memory");
+      conv_role();
+    } else if (wg == 2) {
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+      drain_role();
+    } else {
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+      if (warp == TS_MMA) mma_role();
+      else if (warp == TS_TMAW) tma_role();
+    }
+  } else if (warp == TS_MMA) {
+    mma_role();
+  } else if (warp == TS_TMAW) {
+    tma_role();
+  } else if (warp < TS_DW0) {
+    conv_role();
+  } else {
+    drain_role();
   }
   __syncthreads();
   if (warp == TS_MMA) {
