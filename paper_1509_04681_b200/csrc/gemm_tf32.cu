@@ -609,8 +609,11 @@ __global__ void __launch_bounds__(TCfg<TMA>::NT, 1)
 #endif
 constexpr int TS_CONV = CGGM_TS_CONV8 ? 256 : 128;   // converter threads (warps 0-3 (and 4-7): TMEM lane quarters)
 constexpr int TS_KH = TS_CONV / 128;          // k-parts of a row (one per converter warp of a lane quarter)
-constexpr int TS_NS = 4;                     // split stages (TMEM A, shared B)
-constexpr int TS_NRAW = 3;                   // raw TMA stages
+#ifndef CGGM_TS_NS
+#define CGGM_TS_NS 4
+#endif
+constexpr int TS_NS = CGGM_TS_NS;            // split stages (TMEM A, shared B)
+constexpr int TS_NRAW = 7 - CGGM_TS_NS;      // raw TMA stages (the two rings share 224 KB of shared memory)
 constexpr int TS_BSTAGE = 2 * T_OP;          // B hi + lo
 constexpr int TS_BPER = TBN * TBK / 4 / TS_CONV;   // raw B 16-byte chunks per converter thread (8 / 4)
 constexpr int TS_DATA = TS_NS * TS_BSTAGE + TS_NRAW * T_RAW;   // 128 + 96 KB
