@@ -183,6 +183,7 @@ cggm_status cggm_ctx_create(cggm_ctx** out, int device, cggm_dtype dtype, void* 
   if (const char* e = std::getenv("CGGM_NO_VEC_EPI")) c->no_vec_epi = std::atoi(e);
   if (const char* e = std::getenv("CGGM_PERSIST_TPC")) c->persist_tpc = std::atoi(e);
   if (const char* e = std::getenv("CGGM_MID_TILE")) c->mid_tile = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_MID_MIN_WAVES")) c->mid_min_waves = std::atoi(e);
   if (const char* e = std::getenv("CGGM_LEAF_SWEEP")) c->leaf_sweep = std::atoi(e);
   if (const char* e = std::getenv("CGGM_CD_COOP")) c->cd_coop = std::atoi(e);
   if (const char* e = std::getenv("CGGM_CD_PREFETCH")) c->cd_prefetch = std::atoi(e);

@@ -122,6 +122,7 @@ struct Ctx {
   int leaf_sweep = 0;       // CGGM_LEAF_SWEEP=1: full-inverse leaves by the panel/sweep kernel (A/B)
   int cd_prefetch = 1;      // CGGM_CD_PREFETCH=0: cooperative Theta sweep without the register/prefetch variant
   int cd_coop = 1;          // CGGM_CD_COOP=0: single-CTA coordinate sweeps (no column batching)
+  int mid_min_waves = 0;    // CGGM_MID_MIN_WAVES: mid-size products on the 128x64 tiles from this many quarter waves (0 = off)
   int mid_tile = 3;         // CGGM_MID_TILE (3): 128x64 warp-specialised tiles, 2 CTAs/SM, for the large GEMMs (gemm.cu)
   int no_small_async = 0;
   int no_active_vec = 0;

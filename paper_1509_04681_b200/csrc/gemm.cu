@@ -1363,7 +1363,13 @@ void gemm(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t K, con
   // CTAs, 3 resident per SM) fills the machine better (profiles/r01_gemm_bench_tiles*.txt)
   const int64_t waves = (big_tiles + c->num_sms - 1) / c->num_sms;
   const double big_eff = (double)big_tiles / (double)(waves * c->num_sms);
-  const bool auto_big = big_tiles >= 3 * c->num_sms || big_eff >= 0.9;
+  bool auto_big = big_tiles >= 3 * c->num_sms || big_eff >= 0.9;
+  if (!auto_big && c->mid_min_waves > 0 && c->mid_tile) {
+    // mid-size products: the warp-specialised 128x64 tiles (two per SM) once their grid fills at least
+    // mid_min_waves / 4 waves (CGGM_MID_MIN_WAVES, quarter waves; 0 = the 128x128-tile rule above only)
+    const int64_t mt = (flags & SYM_LOWER) ? 2 * (tn * (tn + 1) / 2 + (tm - tn) * tn) : tm * ((N + 63) / 64);
+    auto_big = 4 * mt >= (int64_t)c->mid_min_waves * 2 * c->num_sms;
+  }
   const bool use_big = c->force_tile ? (c->force_tile == 1) : auto_big;
   // CGGM_MID_TILE (two-CTA 128x64 tiles for): 3 = every large product (default; the step 410.2 ->
   // 409.7 ms against 4, although lauum alone is 74.46 -> 74.58 ms: its k-loop hides the epilogue,

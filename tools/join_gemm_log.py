@@ -41,3 +41,7 @@ print(f"TOTAL {1e3 * tot_t:.2f} ms, {tot_f / tot_t / 1e12:.2f} TF/s")
 print("largest losses vs 37.1 TF/s (ms lost, ms, TF/s, launch):")
 for w in sorted(worst, reverse=True)[:15]:
     print(f"  {1e3 * w[0]:7.2f} {1e3 * w[1]:8.2f} {w[2]:6.2f}  {w[3]}")
+print("largest losses among the non-'big' launches (grid <= 2048 CTAs):")
+small = [w for w in worst if "grid=" in w[3] and int(re.search(r"grid=(\d+)", w[3]).group(1)) <= 2048]
+for w in sorted(small, reverse=True)[:25]:
+    print(f"  {1e3 * w[0]:7.2f} {1e3 * w[1]:8.2f} {w[2]:6.2f}  {w[3]}")
