@@ -660,21 +660,22 @@ void leaf(Rec<T>& R, ViewT<T> A, ViewT<T> X, int64_t col0) {
 // latency-bound stretches leave idle, instead of as one product after it.  Nodes below sig_min form
 // their block in one symmetric product.  Same arithmetic per entry as the one-shot product up to
 // the order of the k-sums (a block's sum is split at the child boundaries).
+// the Sigma pieces go to the Sigma stream after everything enqueued so far on the chain (the blocks
+// of L^{-1} they read); returns the chain stream to restore afterwards
 template <typename T>
-void sig_enqueue_begin(Rec<T>& R, cudaStream_t& chain, cudaStream_t& prev) {
-  prev = R.c->stream;
-  chain = prev;
+cudaStream_t sig_enqueue_begin(Rec<T>& R) {
+  const cudaStream_t prev = R.c->stream;
   if (R.sgs) {
     CGGM_CUDA_CHECK(cudaStreamWaitEvent(R.sgs, la_record(R.c, prev), 0));
     R.c->stream = R.sgs;
   }
+  return prev;
 }
 
 template <typename T>
 void sig_block_product(Rec<T>& R, ViewT<T> X, int64_t col0) {   // S_node = X^T X (X lower triangular)
   const int64_t n = X.rows;
-  cudaStream_t chain, prev;
-  sig_enqueue_begin(R, chain, prev);
+  const cudaStream_t prev = sig_enqueue_begin(R);
   {
     Phase ph(R.c, TAG_LAUUM);   // (the GEMMs record under this tag)
     EpilogueT<T> e; e.out1 = R.sig + col0 + col0 * R.ldsig; e.ld1 = R.ldsig;
@@ -687,8 +688,7 @@ template <typename T>
 void sig_node_pieces(Rec<T>& R, ViewT<T> X11, ViewT<T> X21, ViewT<T> X22, int64_t col0) {
   const int64_t n1 = X11.rows, n2 = X22.rows;
   T* S11 = R.sig + col0 + col0 * R.ldsig;
-  cudaStream_t chain, prev;
-  sig_enqueue_begin(R, chain, prev);
+  const cudaStream_t prev = sig_enqueue_begin(R);
   {
     Phase ph(R.c, TAG_LAUUM);   // (the GEMMs record under this tag)
     {  // S21 = X22^T X21 (X22 lower: op(A) = X22^T has k >= m), S12 = S21^T by the mirrored epilogue
