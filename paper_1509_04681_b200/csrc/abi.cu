@@ -190,6 +190,7 @@ cggm_status cggm_ctx_create(cggm_ctx** out, int device, cggm_dtype dtype, void* 
   if (const char* e = std::getenv("CGGM_GRAPH_PROF")) c->graph_prof = std::atoi(e);
   if (const char* e = std::getenv("CGGM_TF32_CHUNK")) c->tf32_chunk = std::atoi(e);
   if (const char* e = std::getenv("CGGM_SYNC_CHECK")) c->sync_check = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_TF32_CFREL")) c->tf32_cfrel = std::atoi(e);
   if (const char* e = std::getenv("CGGM_TF32_TS_CHUNK")) c->tf32_ts_chunk = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("CGGM_TF32_MIN_TILES")) c->tf32_min_tiles = std::atoi(e);
   if (const char* e = std::getenv("CGGM_TF32_MIN_K")) c->tf32_min_k = std::atoi(e);

@@ -138,6 +138,7 @@ struct Ctx {
                            // 0 = SS with the TMA raw ring + converters ("tma"), 1 = SS with register-staged loads ("ldg")
   int tf32_min_tiles = 0;  // FP32 products with fewer 128x128 tiles than this run on FFMA (CGGM_TF32_MIN_TILES)
   int tf32_min_k = 256;    // ... or with K below this (CGGM_TF32_MIN_K; 256 measured best: FP32 medium 9.5 ms, large 146 ms)
+  int tf32_cfrel = 0;      // CGGM_TF32_CFREL=1: TS split stages released by the chunk commits (measured neutral)
   int tf32_ts_chunk = 2;   // TS form: k-tiles per drained chunk (CGGM_TF32_TS_CHUNK)
   int tf32_chunk = 4;   // 3xTF32: k-tiles per drained TMEM partial (gemm_tf32.cu; CGGM_TF32_CHUNK, 0 = none)
   int f32_engine = 0;   // FP32 contractions: 0 = 3xTF32 on tcgen05 (gemm_tf32.cu), 1 = SIMT FFMA (CGGM_F32_ENGINE=ffma)

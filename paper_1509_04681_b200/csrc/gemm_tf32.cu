@@ -64,6 +64,7 @@ struct KParamsT {
   int chunk;      // k-tiles per drained partial sum (0: one TMEM accumulator over the whole k-range)
   int a3d, b3d;   // TMA producer: MN-inner operand as one 3-D box (extent a multiple of 32)
   int dbg;        // measurement aid (CGGM_TF32_DEBUG): bit 0 = hi*hi products only
+  int cfrel;      // TS form: split stages released by the chunk commits (Ctx::tf32_cfrel)
   EpilogueT<float> epi;
 };
 
@@ -699,6 +700,11 @@ __global__ void __launch_bounds__(TS_NT, 1)
   const int kt0 = kbeg / TBK;
   const int nkt = kend > kbeg ? (kend - kt0 * TBK + TBK - 1) / TBK : 0;
   const int CH = P.chunk > 0 ? P.chunk : 1 << 30;
+  // split stages released by the chunk commits (one commit per chunk instead of one per stage plus
+  // one per chunk) when a chunk spans whole stage groups and the converters cannot fall two phases
+  // behind on a chunk barrier: CH divides TS_NS and 2 CH >= TS_NS (CGGM_TF32_CFREL=1; measured neutral:
+  // the skeleton 235-248 TF/s either way)
+  const bool cf_rel = P.cfrel && CH <= TS_NS && TS_NS % CH == 0 && 2 * CH >= TS_NS;
   if (tid == 0) {
     for (int s = 0; s < TS_NS; ++s) {
       ptx::mbar_init(&full[s], TS_CONV);
@@ -757,7 +763,7 @@ __global__ void __launch_bounds__(TS_NT, 1)
             umma_tf32_ts(X, a_hi + kk * 8u, dbl, idesc, 1u);
             umma_tf32_ts(X, a_hi + kk * 8u, dbh, idesc, 1u);
           }
-          umma_commit(&empty[s]);
+          if (!cf_rel) umma_commit(&empty[s]);
           if (j % CH == CH - 1 || j == nkt - 1) umma_commit(&cfull[c & 1]);
         }
         __syncwarp();
@@ -810,7 +816,12 @@ __global__ void __launch_bounds__(TS_NT, 1)
       const int s = it % TS_NS, rs = it % TS_NRAW;
       ptx::mbar_wait(&rfull[rs], (it / TS_NRAW) & 1);
       if (it >= TS_NS) {
-        ptx::mbar_wait(&empty[s], ((it / TS_NS) - 1) & 1);
+        if (cf_rel) {   // the previous use of this stage lies in chunk cp: its completion frees the stage
+          const int cp = (it - TS_NS) / CH;
+          ptx::mbar_wait(&cfull[cp & 1], (cp >> 1) & 1);
+        } else {
+          ptx::mbar_wait(&empty[s], ((it / TS_NS) - 1) & 1);
+        }
         tc_fence_after();
       }
       const uint32_t rw = rbase + rs * T_RAW;
@@ -985,6 +996,7 @@ void gemm_tf32x3(Ctx* c, bool transA, bool transB, int64_t M, int64_t N, int64_t
   P.A = A; P.lda = lda; P.B = B; P.ldb = ldb;
   P.chunk = c->tf32_chunk;
   P.dbg = c->tf32_dbg;
+  P.cfrel = c->tf32_cfrel;
   P.a3d = a3d; P.b3d = b3d;
   P.epi = epi;
   P.tilesM = (int)((M + TBM - 1) / TBM);
