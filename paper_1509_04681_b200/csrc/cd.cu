@@ -786,6 +786,276 @@ __global__ void __launch_bounds__(CO_NT) k_theta_sweep_pf(int p, int q, const do
   }
 }
 
+// ---------------------------------------------------------------- entry-blocked cooperative sweeps
+// When the column vector no longer fits the register variants (q > CO_QMAX / p > CO_PMAX: large and
+// sharded), the column walk above leaves every dot product -- two length-q rows of Sigma / Psi, or a
+// length-p column of S_xx, straight from DRAM -- to the one CTA on the sequential chain (13.9 us per
+// update at large).  Within column j an update of entry m changes the column vector in two places
+// only, so the dot product of a later entry k' of the same column is its value against the vector
+// as it stood at the start of a block of entries plus one coupling term per earlier entry of the
+// block (Lambda sweep, u = U_{:,j}, z = Z_{:,j}, rows i_m of the block):
+//   b_k' = b0_k' + sum_{m < k'} mu_m c_{k'm},
+//   c_{k'm} = Sjj (Sigma + Psi)_{i_k' i_m} + Psi_jj Sigma_{i_k' i_m}
+//           + [i_m != j] (Sigma_{i_m j} (Sigma + Psi)_{i_k' j} + Psi_{i_m j} Sigma_{i_k' j})
+// (Theta sweep, v = V_{:,j}: c_{k'm} = 2 Sigma_jj (S_xx)_{i_k' i_m}).  Per block of BK_B entries:
+// phase 1 -- the whole grid, one warp per (entry, 1024-element chunk) item, forms the b0 partials
+// (the same bytes the chain used to read, now at the grid's bandwidth) and the coupling matrix
+// C (row m = the coefficients of mu_m, gathered from row i_m and row j); phase 2 -- one warp of CTA 0
+// runs the block's updates in list order with C in shared memory: per update one shuffle, the
+// closed-form coordinate minimiser (the same expression as above), and one FMA per later entry.
+// The column vector is then advanced by the block's changes, and after the column the deferred row
+// updates run as in the column walk.  Same updates in the same order; the dot products are summed
+// in a different (fixed) order, so results agree with the column walk to rounding and are bitwise
+// reproducible run to run.
+constexpr int BK_B = 128;              // entries per block
+constexpr int BK_R = BK_B / 32;        // block entries per lane in phase 2
+constexpr int BK_CH = 1024;            // dot-product elements per warp item
+constexpr int BK_U = 8;                // loads in flight per lane and operand
+constexpr size_t BK_SMEM = (size_t)BK_B * BK_B * 8 + (size_t)BK_B * (7 * 8 + 4);
+
+template <bool LAM>
+__global__ void __launch_bounds__(CO_NT) k_sweep_blk(int q, int nlen, const double* __restrict__ S, int64_t lds,
+                                                     const double* __restrict__ P, int64_t ldp,
+                                                     const int32_t* __restrict__ xmap, const int32_t* __restrict__ Lr,
+                                                     const double* __restrict__ coefv, const int64_t* __restrict__ lp,
+                                                     double lam, int passes, double* X, double* dmu, double* U,
+                                                     double* Z, int64_t ldu, double* ucol, double* part, double* Ct,
+                                                     double* sj) {
+  namespace cgx = cooperative_groups;
+  cgx::grid_group grid = cgx::this_grid();
+  extern __shared__ double bk_sm[];
+  double* sC = bk_sm;                         // [BK_B][BK_B]: row m = coefficients of mu_m
+  double* sB = sC + BK_B * BK_B;              // b0 + the entry's constant
+  double* sA = sB + BK_B;                     // 1 / a (0 when a <= 0: no update)
+  double* sT = sA + BK_B;                     // the entry's threshold / a
+  double* sY = sT + BK_B;                     // Lambda: Lambda_ij (+ D_ij below); Theta: current value
+  double* sW = sY + BK_B;                     // Lambda: c = Lambda_ij + D_ij
+  double* sSj = sW + BK_B;                    // Lambda: Sigma_{i j}, Psi_{i j} of the block's rows
+  double* sPj = sSj + BK_B;
+  int* sI = reinterpret_cast<int*>(sPj + BK_B);
+  double* zcol = ucol + nlen;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gtid = blockIdx.x * (int64_t)CO_NT + threadIdx.x, gsz = (int64_t)gridDim.x * CO_NT;
+  const int gw = blockIdx.x * CO_NW + warp, nwarps = gridDim.x * CO_NW;
+  const int nch = (nlen + BK_CH - 1) / BK_CH;
+  const double4* coef4 = reinterpret_cast<const double4*>(coefv);
+  const double2* coef2 = reinterpret_cast<const double2*>(coefv);
+  for (int pass = 0; pass < passes; ++pass) {
+    for (int j = 0; j < q; ++j) {
+      const int64_t k0 = lp[j], k1 = lp[j + 1];
+      if (k0 == k1) continue;
+      for (int64_t t = gtid; t < nlen; t += gsz) {
+        ucol[t] = __ldcg(U + t * ldu + j);
+        if (LAM) zcol[t] = __ldcg(Z + t * ldu + j);
+      }
+      const double Sjj = S[j + (int64_t)j * lds];
+      const double Pjj = LAM ? P[j + (int64_t)j * ldp] : 0.0;
+      grid.sync();
+      for (int64_t kb = k0; kb < k1; kb += BK_B) {
+        const int nb = (int)(k1 - kb < BK_B ? k1 - kb : BK_B);
+        // ---- phase 1: b0 partials against the block-start vector, and the coupling rows
+        const int nit = nb * (nch + 1);
+        for (int it = gw; it < nit; it += nwarps) {
+          const int kk = it / (nch + 1), ch = it - kk * (nch + 1);
+          const int i = Lr[kb + kk];
+          if (ch < nch) {
+            const int t0 = ch * BK_CH, t1 = min(nlen, t0 + BK_CH);
+            const double* Si = LAM ? S + (int64_t)i * lds : P + xcol(xmap, i) * ldp;
+            const double* Pi = LAM ? P + (int64_t)i * ldp : nullptr;
+            double v = 0.0;
+            for (int tb = t0; tb < t1; tb += 32 * BK_U) {
+              double sv[BK_U], pv[BK_U], uv[BK_U], zv[BK_U];
+#pragma unroll
+              for (int u = 0; u < BK_U; ++u) {
+                const int t = tb + lane + 32 * u;
+                const bool in = t < t1;
+                sv[u] = in ? Si[t] : 0.0;
+                uv[u] = in ? __ldcg(ucol + t) : 0.0;
+                if (LAM) {
+                  pv[u] = in ? Pi[t] : 0.0;
+                  zv[u] = in ? __ldcg(zcol + t) : 0.0;
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < BK_U; ++u) {
+                if (LAM) v = fma(sv[u] + pv[u], uv[u], fma(sv[u], zv[u], v));
+                else v = fma(sv[u], uv[u], v);
+              }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) part[(int64_t)kk * nch + ch] = v;
+          } else if (LAM) {
+            const double* Sm = S + (int64_t)i * lds;
+            const double* Pm = P + (int64_t)i * ldp;
+            const double smj = Sm[j], pmj = Pm[j];
+            if (lane == 0) {
+              sj[kk] = smj;
+              sj[BK_B + kk] = pmj;
+            }
+            for (int k2 = lane; k2 < nb; k2 += 32) {
+              const int i2 = Lr[kb + k2];
+              const double s = Sm[i2], pp = Pm[i2];
+              double cv = fma(Sjj, s + pp, Pjj * s);
+              if (i != j) {
+                const double sk = S[(int64_t)j * lds + i2], pk = P[(int64_t)j * ldp + i2];
+                cv += fma(smj, sk + pk, pmj * sk);
+              }
+              Ct[(int64_t)kk * BK_B + k2] = cv;
+            }
+          } else {
+            const double* Xm = P + xcol(xmap, i) * ldp;
+            for (int k2 = lane; k2 < nb; k2 += 32) Ct[(int64_t)kk * BK_B + k2] = 2.0 * Sjj * Xm[Lr[kb + k2]];
+          }
+        }
+        grid.sync();
+        // ---- phase 2: the block's updates in list order (CTA 0)
+        if (blockIdx.x == 0) {
+          for (int e = threadIdx.x; e < nb * BK_B; e += CO_NT) sC[e] = __ldcg(Ct + e);
+          for (int kk = threadIdx.x; kk < nb; kk += CO_NT) {
+            const int64_t k = kb + kk;
+            double s = 0.0;
+            for (int ch = 0; ch < nch; ++ch) s += __ldcg(part + (int64_t)kk * nch + ch);
+            if (LAM) {
+              const double4 cf = coef4[k];
+              sB[kk] = cf.z + s;
+              sA[kk] = cf.x > 0.0 ? 1.0 / cf.x : 0.0;
+              sT[kk] = cf.x > 0.0 ? cf.w / cf.x : 0.0;
+              sY[kk] = cf.y;
+              sW[kk] = cf.y + __ldcg(X + k);
+              sI[kk] = Lr[k];
+              sSj[kk] = __ldcg(sj + kk);
+              sPj[kk] = __ldcg(sj + BK_B + kk);
+            } else {
+              const double2 cf = coef2[k];
+              sB[kk] = cf.y + 2.0 * s;
+              sA[kk] = cf.x > 0.0 ? 1.0 / cf.x : 0.0;
+              sT[kk] = cf.x > 0.0 ? lam / cf.x : 0.0;
+              sY[kk] = __ldcg(X + k);
+              sI[kk] = Lr[k];
+            }
+          }
+          __syncthreads();
+          if (warp == 0) {
+            double corr[BK_R], mymu[BK_R];
+#pragma unroll
+            for (int r = 0; r < BK_R; ++r) {
+              const int kk = lane + 32 * r;
+              corr[r] = kk < nb ? sB[kk] : 0.0;
+              mymu[r] = 0.0;
+            }
+            double uj = 0.0, zj = 0.0;
+#pragma unroll
+            for (int r = 0; r < BK_R; ++r) {
+#pragma unroll 4
+              for (int s = 0; s < 32; ++s) {
+                const int kk = 32 * r + s;
+                if (kk >= nb) break;
+                const double b = __shfl_sync(0xffffffffu, corr[r], s);
+                // the coordinate minimiser -c + soft(c - b / a, w / a) with 1 / a and w / a formed
+                // off the chain (a <= 0: no update)
+                const double ia = sA[kk];
+                const double c = LAM ? sW[kk] : sY[kk];
+                const double mu = (ia > 0.0) ? -c + soft(fma(-b, ia, c), sT[kk]) : 0.0;
+                const double* crow = sC + kk * BK_B + lane;
+#pragma unroll
+                for (int r2 = 0; r2 < BK_R; ++r2) corr[r2] = fma(mu, crow[32 * r2], corr[r2]);
+                if (lane == s) mymu[r] = mu;
+                if (LAM) {
+                  const bool diag = sI[kk] == j;
+                  uj = fma(mu, diag ? Sjj : sSj[kk], uj);
+                  zj = fma(mu, diag ? Pjj : sPj[kk], zj);
+                }
+              }
+            }
+#pragma unroll
+            for (int r = 0; r < BK_R; ++r) {
+              const int kk = lane + 32 * r;
+              if (kk < nb) {
+                const int64_t k = kb + kk;
+                const double mu = mymu[r];
+                const int i = sI[kk];
+                if (LAM) {
+                  __stcg(X + k, sW[kk] - sY[kk] + mu);
+                  if (i != j) {
+                    __stcg(ucol + i, __ldcg(ucol + i) + mu * Sjj);
+                    __stcg(zcol + i, __ldcg(zcol + i) + mu * Pjj);
+                  }
+                } else {
+                  __stcg(X + k, sY[kk] + mu);
+                  __stcg(ucol + i, __ldcg(ucol + i) + mu * Sjj);
+                }
+                __stcg(dmu + k, mu);
+              }
+            }
+            if (LAM && lane == 0) {
+              __stcg(ucol + j, __ldcg(ucol + j) + uj);
+              __stcg(zcol + j, __ldcg(zcol + j) + zj);
+            }
+          }
+        }
+        grid.sync();
+      }
+      // ---- column end: write the column back, deferred row updates (disjoint elements)
+      for (int64_t t = gtid; t < nlen; t += gsz) {
+        __stcg(U + t * ldu + j, __ldcg(ucol + t));
+        if (LAM) __stcg(Z + t * ldu + j, __ldcg(zcol + t));
+      }
+      {
+        for (int64_t k = k0 + blockIdx.x; k < k1; k += gridDim.x) {
+          const int i = Lr[k];
+          const double mu = __ldcg(dmu + k);
+          if ((LAM && i == j) || mu == 0.0) continue;
+          for (int t = threadIdx.x; t < q; t += CO_NT) {
+            if (t == j) continue;
+            double* u = U + (int64_t)i * ldu + t;
+            __stcg(u, __ldcg(u) + mu * S[t + (int64_t)j * lds]);
+            if (LAM) {
+              double* z = Z + (int64_t)i * ldu + t;
+              __stcg(z, __ldcg(z) + mu * P[t + (int64_t)j * ldp]);
+            }
+          }
+        }
+        if (LAM) {
+          // row j: U[j, t] += sum_k mu_k Sigma[i_k, t] -- 128 columns t per CTA, the k-range split over
+          // the CTA's four thread groups (k = k0 + g mod 4), the group sums added in fixed order
+          double* rj = bk_sm;   // 2 x 4 x 128 (phase 2's shared memory is free here)
+          const int tl = threadIdx.x & 127, g = threadIdx.x >> 7;
+          for (int64_t tb = (int64_t)blockIdx.x * 128; tb < q; tb += (int64_t)gridDim.x * 128) {
+            const int64_t t = tb + tl;
+            double ua = 0.0, za = 0.0;
+            if (t < q) {
+              for (int64_t k = k0 + g; k < k1; k += CO_NT / 128) {
+                const double mu = __ldcg(dmu + k);
+                const int i = Lr[k];
+                ua = fma(mu, S[t + (int64_t)i * lds], ua);
+                za = fma(mu, P[t + (int64_t)i * ldp], za);
+              }
+            }
+            rj[g * 128 + tl] = ua;
+            rj[512 + g * 128 + tl] = za;
+            __syncthreads();
+            if (g == 0 && t < q && t != j) {
+              double su = rj[tl], sz = rj[512 + tl];
+#pragma unroll
+              for (int g2 = 1; g2 < CO_NT / 128; ++g2) {
+                su += rj[g2 * 128 + tl];
+                sz += rj[512 + g2 * 128 + tl];
+              }
+              double* u = U + (int64_t)j * ldu + t;
+              double* z = Z + (int64_t)j * ldu + t;
+              __stcg(u, __ldcg(u) + su);
+              __stcg(z, __ldcg(z) + sz);
+            }
+            __syncthreads();
+          }
+        }
+      }
+      grid.sync();
+    }
+  }
+}
+
 // ---------------------------------------------------------------- sparse bookkeeping
 // count list entries per column (cl) and mirrored entries per column (cm: entry (i, j), i < j,
 // mirrors into column i)
@@ -1026,6 +1296,27 @@ void lambda_cd_coop(Ctx* c, int q, const double* S, int64_t lds, const double* P
     k_lambda_coefs<<<grid_for(m), 256, 0, c->stream>>>(m, S, lds, P, ldp, G, ldg, Lam->colptr, Lam->rowidx, lv, Lr, Lc,
                                                        lam, penalize_diag, coef);
     list_colptr(c, q, Lr, Lc, m, cnt, scr, lp);
+    if (c->cd_block == 1 || (c->cd_block < 0 && q > CO_QMAX)) {
+      const int nch = (q + BK_CH - 1) / BK_CH;
+      double* part = static_cast<double*>(ws_get(c, WS_CD_BLK, ((size_t)BK_B * nch + BK_B * BK_B + 2 * BK_B) * 8));
+      double* Ct = part + (size_t)BK_B * nch;
+      double* sjw = Ct + BK_B * BK_B;
+      CGGM_ONCE_PER_DEVICE({
+        CGGM_CUDA_CHECK(cudaFuncSetAttribute(k_sweep_blk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BK_SMEM));
+      });
+      int grid = c->num_sms, nlen = q;
+      const int32_t* xm = nullptr;
+      double lamv = 0.0;
+      const double* cfd = coef_ws;
+      void* args[] = {&q, &nlen, &S, &lds, &P, &ldp, &xm, &Lr, &cfd, &lp, &lamv, &passes, &D, &dmu, &U, &Z, &ldu,
+                      &colbuf, &part, &Ct, &sjw};
+      CGGM_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_sweep_blk<true>, dim3(grid), dim3(CO_NT), args, BK_SMEM,
+                                                  c->stream));
+      c->launches += 2;
+      k_lambda_tail<<<1, CD_NT, 0, c->stream>>>(q, Lam->colptr, lv, Lr, Lc, coef, m, D, out);
+      post_launch(c, "k_sweep_blk<lambda>");
+      return;
+    }
     const size_t smem_pf = (size_t)4 * ((q + 1) & ~1) * 8;
     if (q >= 2048 && q <= CO_QMAX && smem_pf <= 200 * 1024 && lds % 2 == 0 && ldp % 2 == 0 && c->cd_prefetch) {
       CGGM_ONCE_PER_DEVICE({
@@ -1070,6 +1361,26 @@ void theta_cd_coop(Ctx* c, int p, int q, const double* S, int64_t lds, const dou
                                                       static_cast<const double*>(Th->val), Tr, Tc, coef, T);
     list_colptr(c, q, Tr, Tc, m, cnt, scr, lp);
     int grid = c->num_sms;
+    if (c->cd_block == 1 || (c->cd_block < 0 && p > CO_PMAX)) {
+      const int nch = (p + BK_CH - 1) / BK_CH;
+      double* part = static_cast<double*>(ws_get(c, WS_CD_BLK, ((size_t)BK_B * nch + BK_B * BK_B + 2 * BK_B) * 8));
+      double* Ct = part + (size_t)BK_B * nch;
+      double* sjw = Ct + BK_B * BK_B;
+      CGGM_ONCE_PER_DEVICE({
+        CGGM_CUDA_CHECK(cudaFuncSetAttribute(k_sweep_blk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BK_SMEM));
+      });
+      int nlen = p;
+      const double* cfd = coef_ws;
+      double* Zn = nullptr;
+      void* args[] = {&q, &nlen, &S, &lds, &Sxx, &ldx, &xmap, &Tr, &cfd, &lp, &lam, &passes, &T, &dmu, &V, &Zn, &ldv,
+                      &colbuf, &part, &Ct, &sjw};
+      CGGM_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_sweep_blk<false>, dim3(grid), dim3(CO_NT), args, BK_SMEM,
+                                                  c->stream));
+      c->launches += 2;
+      k_theta_l1<<<1, CD_NT, 0, c->stream>>>(T, m, out);
+      post_launch(c, "k_sweep_blk<theta>");
+      return;
+    }
     const size_t smem_pf = (size_t)2 * ((p + 1) & ~1) * 8;
     if (p >= 2048 && p <= CO_PMAX && smem_pf <= 200 * 1024 && ldx % 2 == 0 && c->cd_prefetch) {
       CGGM_ONCE_PER_DEVICE({

@@ -193,10 +193,10 @@ def _medium_oracle_sweeps(s, P, penalize_diag):
     return _P[key]
 
 
-@pytest.mark.parametrize("variant", [{"CGGM_CD_COOP": "0"}, {"CGGM_CD_PREFETCH": "0"}, {}])
+@pytest.mark.parametrize("variant", [{"CGGM_CD_COOP": "0"}, {"CGGM_CD_PREFETCH": "0"}, {"CGGM_CD_BLOCK": "1"}, {}])
 def test_sweep_variants_agree_medium(variant):
-    """The single-CTA sweeps, the column-batched cooperative sweeps and their register / prefetch
-    variants (taken at medium sizes, q, p >= 2048) give the same direction and Theta to summation-order
+    """The single-CTA sweeps, the column-batched cooperative sweeps, their register / prefetch
+    variants (taken at medium sizes, q, p >= 2048) and the entry-blocked sweeps give the same direction and Theta to summation-order
     rounding, and each matches the oracle's sweeps on the same lists."""
     import os
     from paper_1509_04681_b200 import Context
