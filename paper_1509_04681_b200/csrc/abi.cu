@@ -188,6 +188,7 @@ cggm_status cggm_ctx_create(cggm_ctx** out, int device, cggm_dtype dtype, void* 
   if (const char* e = std::getenv("CGGM_CD_COOP")) c->cd_coop = std::atoi(e);
   if (const char* e = std::getenv("CGGM_CD_PREFETCH")) c->cd_prefetch = std::atoi(e);
   if (const char* e = std::getenv("CGGM_CD_BLOCK")) c->cd_block = std::atoi(e);
+  if (const char* e = std::getenv("CGGM_CD_PANEL")) c->cd_panel = std::atoi(e);
   if (const char* e = std::getenv("CGGM_GRAPH_PROF")) c->graph_prof = std::atoi(e);
   if (const char* e = std::getenv("CGGM_TF32_CHUNK")) c->tf32_chunk = std::atoi(e);
   if (const char* e = std::getenv("CGGM_SYNC_CHECK")) c->sync_check = std::atoi(e);

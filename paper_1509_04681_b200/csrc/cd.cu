@@ -820,7 +820,8 @@ __global__ void __launch_bounds__(CO_NT) k_sweep_blk(int q, int nlen, const doub
                                                      const double* __restrict__ coefv, const int64_t* __restrict__ lp,
                                                      double lam, int passes, double* X, double* dmu, double* U,
                                                      double* Z, int64_t ldu, double* ucol, double* part, double* Ct,
-                                                     double* sj) {
+                                                     double* sj, int j0, int j1, double* Dd, int64_t ldd,
+                                                     double* rpart) {
   namespace cgx = cooperative_groups;
   cgx::grid_group grid = cgx::this_grid();
   extern __shared__ double bk_sm[];
@@ -841,7 +842,7 @@ __global__ void __launch_bounds__(CO_NT) k_sweep_blk(int q, int nlen, const doub
   const double4* coef4 = reinterpret_cast<const double4*>(coefv);
   const double2* coef2 = reinterpret_cast<const double2*>(coefv);
   for (int pass = 0; pass < passes; ++pass) {
-    for (int j = 0; j < q; ++j) {
+    for (int j = j0; j < j1; ++j) {
       const int64_t k0 = lp[j], k1 = lp[j + 1];
       if (k0 == k1) continue;
       for (int64_t t = gtid; t < nlen; t += gsz) {
@@ -850,6 +851,55 @@ __global__ void __launch_bounds__(CO_NT) k_sweep_blk(int q, int nlen, const doub
       }
       const double Sjj = S[j + (int64_t)j * lds];
       const double Pjj = LAM ? P[j + (int64_t)j * ldp] : 0.0;
+      if (LAM && Dd && j > j0) {
+        // panel mode: rows r in [j0, j) of column j -- the rows this panel's earlier columns rewrote
+        // wholesale -- are formed from the current dense D: U[r, j] = D_{:,r} . Sigma_{:,j},
+        // Z[r, j] = D_{:,r} . Psi_{:,j} (chunk partials by the grid, summed in chunk order)
+        const int nr = j - j0;
+        const double* Sj = S + (int64_t)j * lds;
+        const double* Pj = P + (int64_t)j * ldp;
+        for (int it = gw; it < nr * nch; it += nwarps) {
+          const int rr = it / nch, ch = it - rr * nch;
+          const int t0 = ch * BK_CH, t1 = min(nlen, t0 + BK_CH);
+          const double* Dr = Dd + (int64_t)(j0 + rr) * ldd;
+          double vu = 0.0, vz = 0.0;
+          for (int tb = t0; tb < t1; tb += 32 * BK_U) {
+            double dv[BK_U], sv[BK_U], pv[BK_U];
+#pragma unroll
+            for (int u = 0; u < BK_U; ++u) {
+              const int t = tb + lane + 32 * u;
+              const bool in = t < t1;
+              dv[u] = in ? __ldcg(Dr + t) : 0.0;
+              sv[u] = in ? Sj[t] : 0.0;
+              pv[u] = in ? Pj[t] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < BK_U; ++u) {
+              vu = fma(dv[u], sv[u], vu);
+              vz = fma(dv[u], pv[u], vz);
+            }
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            vu += __shfl_xor_sync(0xffffffffu, vu, o);
+            vz += __shfl_xor_sync(0xffffffffu, vz, o);
+          }
+          if (lane == 0) {
+            rpart[2 * (int64_t)it] = vu;
+            rpart[2 * (int64_t)it + 1] = vz;
+          }
+        }
+        grid.sync();
+        for (int64_t rr = gtid; rr < nr; rr += gsz) {
+          double su = 0.0, sz = 0.0;
+          for (int ch = 0; ch < nch; ++ch) {
+            su += __ldcg(rpart + 2 * (rr * nch + ch));
+            sz += __ldcg(rpart + 2 * (rr * nch + ch) + 1);
+          }
+          ucol[j0 + rr] = su;
+          zcol[j0 + rr] = sz;
+        }
+      }
       grid.sync();
       for (int64_t kb = k0; kb < k1; kb += BK_B) {
         const int nb = (int)(k1 - kb < BK_B ? k1 - kb : BK_B);
@@ -976,7 +1026,12 @@ __global__ void __launch_bounds__(CO_NT) k_sweep_blk(int q, int nlen, const doub
                 const double mu = mymu[r];
                 const int i = sI[kk];
                 if (LAM) {
-                  __stcg(X + k, sW[kk] - sY[kk] + mu);
+                  const double dn = sW[kk] - sY[kk] + mu;
+                  __stcg(X + k, dn);
+                  if (Dd) {
+                    __stcg(Dd + i + (int64_t)j * ldd, dn);
+                    __stcg(Dd + j + (int64_t)i * ldd, dn);
+                  }
                   if (i != j) {
                     __stcg(ucol + i, __ldcg(ucol + i) + mu * Sjj);
                     __stcg(zcol + i, __ldcg(zcol + i) + mu * Pjj);
@@ -1006,7 +1061,10 @@ __global__ void __launch_bounds__(CO_NT) k_sweep_blk(int q, int nlen, const doub
           const int i = Lr[k];
           const double mu = __ldcg(dmu + k);
           if ((LAM && i == j) || mu == 0.0) continue;
-          for (int t = threadIdx.x; t < q; t += CO_NT) {
+          // panel mode: only the panel's later columns (the rest of U is never read again before
+          // its own panel product)
+          const int tlo = (LAM && Dd) ? j + 1 : 0, thi = (LAM && Dd) ? j1 : q;
+          for (int t = tlo + threadIdx.x; t < thi; t += CO_NT) {
             if (t == j) continue;
             double* u = U + (int64_t)i * ldu + t;
             __stcg(u, __ldcg(u) + mu * S[t + (int64_t)j * lds]);
@@ -1016,7 +1074,7 @@ __global__ void __launch_bounds__(CO_NT) k_sweep_blk(int q, int nlen, const doub
             }
           }
         }
-        if (LAM) {
+        if (LAM && !Dd) {
           // row j: U[j, t] += sum_k mu_k Sigma[i_k, t] -- 128 columns t per CTA, the k-range split over
           // the CTA's four thread groups (k = k0 + g mod 4), the group sums added in fixed order
           double* rj = bk_sm;   // 2 x 4 x 128 (phase 2's shared memory is free here)
@@ -1306,10 +1364,51 @@ void lambda_cd_coop(Ctx* c, int q, const double* S, int64_t lds, const double* P
       const int32_t* xm = nullptr;
       double lamv = 0.0;
       const double* cfd = coef_ws;
-      void* args[] = {&q, &nlen, &S, &lds, &P, &ldp, &xm, &Lr, &cfd, &lp, &lamv, &passes, &D, &dmu, &U, &Z, &ldu,
-                      &colbuf, &part, &Ct, &sjw};
-      CGGM_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_sweep_blk<true>, dim3(grid), dim3(CO_NT), args, BK_SMEM,
-                                                  c->stream));
+      // panel (left-looking) mode, CGGM_CD_PANEL = w > 0 (default above the register limits): the
+      // q x q workspace U holds the dense symmetric D instead of U = D Sigma; before the columns
+      // J = [j0, j0 + w) are swept, their part of U^T and Z^T is formed from it by two DMMA products
+      // (PU = Sigma_{J,:} D, PZ = Psi_{J,:} D, w x q, in the Z workspace), so the deferred row
+      // updates touch only the panel's later columns instead of all q (see k_sweep_blk)
+      const int w = c->cd_panel >= 0 ? c->cd_panel : 0;   // default off until measured
+      if (w > 0 && w % 2 == 0 && (size_t)2 * w <= (size_t)ldu) {
+        double* Dd = U;
+        int64_t ldd = ldu;
+        const int64_t ldw = w;
+        double* PU = Z;
+        double* PZ = Z + (size_t)ldw * q;
+        double* rpart = static_cast<double*>(ws_get(c, WS_CD_PANEL, (size_t)2 * w * nch * 8));
+        int one = 1;
+        for (int pass = 0; pass < passes; ++pass) {
+          for (int j0 = 0; j0 < q; j0 += w) {
+            int j1 = std::min(q, j0 + w);
+            if (pass == 0 && j0 == 0) {   // D = 0
+              CGGM_CUDA_CHECK(cudaMemsetAsync(PU, 0, (size_t)2 * ldw * q * 8, c->stream));
+            } else {
+              Epilogue eu, ez;
+              eu.out1 = PU; eu.ld1 = ldw;
+              ez.out1 = PZ; ez.ld1 = ldw;
+              gemm(c, true, false, j1 - j0, q, q, S + (int64_t)j0 * lds, lds, Dd, ldd, eu, 0);
+              gemm(c, true, false, j1 - j0, q, q, P + (int64_t)j0 * ldp, ldp, Dd, ldd, ez, 0);
+            }
+            double* Uo = PU - j0;
+            double* Zo = PZ - j0;
+            int64_t ldp2 = ldw;
+            void* args[] = {&q, &nlen, &S, &lds, &P, &ldp, &xm, &Lr, &cfd, &lp, &lamv, &one, &D, &dmu, &Uo, &Zo, &ldp2,
+                            &colbuf, &part, &Ct, &sjw, &j0, &j1, &Dd, &ldd, &rpart};
+            CGGM_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_sweep_blk<true>, dim3(grid), dim3(CO_NT), args,
+                                                        BK_SMEM, c->stream));
+            c->launches += 1;
+          }
+        }
+      } else {
+        int j0 = 0, j1 = q;
+        double* Dn = nullptr;
+        int64_t ldd = 0;
+        void* args[] = {&q, &nlen, &S, &lds, &P, &ldp, &xm, &Lr, &cfd, &lp, &lamv, &passes, &D, &dmu, &U, &Z, &ldu,
+                        &colbuf, &part, &Ct, &sjw, &j0, &j1, &Dn, &ldd, &Dn};
+        CGGM_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_sweep_blk<true>, dim3(grid), dim3(CO_NT), args, BK_SMEM,
+                                                    c->stream));
+      }
       c->launches += 2;
       k_lambda_tail<<<1, CD_NT, 0, c->stream>>>(q, Lam->colptr, lv, Lr, Lc, coef, m, D, out);
       post_launch(c, "k_sweep_blk<lambda>");
@@ -1370,8 +1469,10 @@ void theta_cd_coop(Ctx* c, int p, int q, const double* S, int64_t lds, const dou
       int nlen = p;
       const double* cfd = coef_ws;
       double* Zn = nullptr;
+      int j0 = 0, j1 = q;
+      int64_t ldd = 0;
       void* args[] = {&q, &nlen, &S, &lds, &Sxx, &ldx, &xmap, &Tr, &cfd, &lp, &lam, &passes, &T, &dmu, &V, &Zn, &ldv,
-                      &colbuf, &part, &Ct, &sjw};
+                      &colbuf, &part, &Ct, &sjw, &j0, &j1, &Zn, &ldd, &Zn};
       CGGM_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_sweep_blk<false>, dim3(grid), dim3(CO_NT), args, BK_SMEM,
                                                   c->stream));
       c->launches += 2;

@@ -122,6 +122,7 @@ struct Ctx {
   int leaf_sweep = 0;       // CGGM_LEAF_SWEEP=1: full-inverse leaves by the panel/sweep kernel (A/B)
   int cd_prefetch = 1;      // CGGM_CD_PREFETCH=0: cooperative Theta sweep without the register/prefetch variant
   int cd_coop = 1;          // CGGM_CD_COOP=0: single-CTA coordinate sweeps (no column batching)
+  int cd_panel = -1;        // CGGM_CD_PANEL: panel width of the left-looking blocked Lambda sweep (-1: 512 above the register limit, 0: off)
   int cd_block = -1;        // CGGM_CD_BLOCK: entry-blocked sweeps (-1: when the vector exceeds the register variant, 0: never, 1: always)
   int mid_min_waves = 0;    // CGGM_MID_MIN_WAVES: mid-size products on the 128x64 tiles from this many quarter waves (0 = off)
   int mid_tile = 3;         // CGGM_MID_TILE (3): 128x64 warp-specialised tiles, 2 CTAs/SM, for the large GEMMs (gemm.cu)
@@ -247,6 +248,7 @@ enum Slot {
   WS_H_LCP, WS_H_LRI, WS_H_LVA, WS_H_TCP, WS_H_TRI, WS_H_TVA,
   WS_CD_AUX,        // cooperative sweeps: list column pointers, per-entry changes, column buffer
   WS_CD_BLK,        // entry-blocked sweeps: chunk partials, the block's coupling matrix, Sigma_j / Psi_j gathers
+  WS_CD_PANEL,      // left-looking Lambda sweep: chunk partials of the panel-row recompute
   WS_NUM
 };
 

@@ -4,7 +4,9 @@ oracle's sequential sweeps (oracle/ancd_oracle.py; Eq. (6) / (7)
 direction with both diagonal-penalty settings and over two passes (D carried between passes), the
 Theta sweep on the full S_xx and on the on-demand columns, blocks of 128 entries with a
 ragged last block (columns of the small / medium lists hold up to several hundred entries), bitwise
-run-to-run reproducibility, and Algorithm 1's iterates on `tiny`."""
+run-to-run reproducibility, and Algorithm 1's iterates on `tiny`.  The left-looking panel mode of the
+Lambda sweep (CGGM_CD_PANEL = w: U^T, Z^T of w columns at a time formed from the dense D by two GEMMs,
+the default at q > 6144) is forced at panel widths that give several panels and a ragged last one."""
 import os
 
 import numpy as np
@@ -117,3 +119,54 @@ def test_blocked_algorithm1_iterates_match_oracle(bctx):
         assert hg["f"] == pytest.approx(ho[0], rel=1e-9)
         assert hg["alpha"] == ho[4]
         assert (hg["m_L"], hg["m_T"]) == (ho[2], ho[3])
+
+
+_PCTX = {}
+
+
+def panel_ctx(w):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    if w not in _PCTX:
+        from paper_1509_04681_b200 import Context
+        os.environ["CGGM_CD_BLOCK"] = "1"
+        os.environ["CGGM_CD_PANEL"] = str(w)
+        try:
+            _PCTX[w] = Context(0)
+        finally:
+            os.environ.pop("CGGM_CD_BLOCK", None)
+            os.environ.pop("CGGM_CD_PANEL", None)
+    return _PCTX[w]
+
+
+@pytest.mark.parametrize("name,k,pen,passes,w", [("tiny", 1, True, 2, 8), ("small", 1, True, 1, 64),
+                                                 ("small", 0, False, 2, 96), ("small", 1, True, 2, 200),
+                                                 ("medium", 0, True, 1, 512)])
+def test_panel_lambda_direction_matches_oracle(name, k, pen, passes, w):
+    """Left-looking panel mode: same updates in the same order as the oracle's sweep; U's entries come
+    from D Sigma formed per panel instead of incremental row updates, so the direction agrees with
+    the oracle to rounding (and with the right-looking blocked sweep to 1e-12)."""
+    ctx = panel_ctx(w)
+    ref = panel_ctx(0)
+    P = problem(name)
+    s = _state(ctx, P, k)
+    act = s["active"]
+    rows, cols = act["L_row"].cpu().numpy(), act["L_col"].cpu().numpy()
+    args = (s["Sigma"], s["Psi"], s["GradL"], s["Lg"], act["L_row"], act["L_col"], P.lam_L, pen, passes)
+    D, delta, l1 = ctx.cggm_lambda_direction(*args)
+    Dg = D.cpu().numpy().copy()
+    Sig, Psi, G = (s[x].cpu().numpy() for x in ("Sigma", "Psi", "GradL"))
+    Lam = s["lam"].to_dense()
+    Dref, _, vals = A.lambda_newton_direction(Sig, Psi, G, Lam, rows, cols, P.lam_L, pen, passes)
+    assert np.linalg.norm(Dg - vals) <= 1e-10 * max(np.linalg.norm(vals), 1e-300)
+    lamM = np.full(Lam.shape, P.lam_L)
+    if not pen:
+        np.fill_diagonal(lamM, 0.0)
+    d_ref = float(np.sum(G * Dref)) + float(np.sum(lamM * (np.abs(Lam + Dref) - np.abs(Lam))))
+    assert delta == pytest.approx(d_ref, rel=1e-9, abs=1e-12)
+    assert P.q > 2 * w, "several panels"
+    Db, delta_b, _ = ref.cggm_lambda_direction(*args)
+    Db = Db.cpu().numpy()
+    assert np.linalg.norm(Dg - Db) <= 1e-12 * max(np.linalg.norm(Db), 1e-300)
+    D2, delta2, _ = ctx.cggm_lambda_direction(*args)
+    assert np.array_equal(D2.cpu().numpy(), Dg) and delta2 == delta
