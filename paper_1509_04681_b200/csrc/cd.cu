@@ -807,14 +807,23 @@ __global__ void __launch_bounds__(CO_NT) k_theta_sweep_pf(int p, int q, const do
 // updates run as in the column walk.  Same updates in the same order; the dot products are summed
 // in a different (fixed) order, so results agree with the column walk to rounding and are bitwise
 // reproducible run to run.
+// CGGM_CD_TIMING=1 (measurement aid): CTA 0 accumulates %globaltimer deltas per phase -- 0 column
+// load + panel-row recompute, 1 phase 1, 2 phase-2 staging, 3 phase-2 chain + barrier, 4 column end
+__device__ unsigned long long g_cd_tim[8];
+__device__ int g_cd_tim_on;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 constexpr int BK_B = 128;              // entries per block
 constexpr int BK_R = BK_B / 32;        // block entries per lane in phase 2
-constexpr int BK_CH = 1024;            // dot-product elements per warp item
+constexpr int BK_CH = 1280;            // dot-product elements per warp item (large: 128 x 17 items, one round of the grid's 2368 warps)
 constexpr int BK_U = 8;                // loads in flight per lane and operand
 constexpr size_t BK_SMEM = (size_t)BK_B * BK_B * 8 + (size_t)BK_B * (7 * 8 + 4);
 
 template <bool LAM>
-__global__ void __launch_bounds__(CO_NT) k_sweep_blk(int q, int nlen, const double* __restrict__ S, int64_t lds,
+__global__ void __launch_bounds__(CO_NT, 1) k_sweep_blk(int q, int nlen, const double* __restrict__ S, int64_t lds,
                                                      const double* __restrict__ P, int64_t ldp,
                                                      const int32_t* __restrict__ xmap, const int32_t* __restrict__ Lr,
                                                      const double* __restrict__ coefv, const int64_t* __restrict__ lp,
@@ -841,10 +850,19 @@ __global__ void __launch_bounds__(CO_NT) k_sweep_blk(int q, int nlen, const doub
   const int nch = (nlen + BK_CH - 1) / BK_CH;
   const double4* coef4 = reinterpret_cast<const double4*>(coefv);
   const double2* coef2 = reinterpret_cast<const double2*>(coefv);
+  const bool tim = g_cd_tim_on && blockIdx.x == 0 && threadIdx.x == 0;
+  unsigned long long tacc[5] = {0, 0, 0, 0, 0}, tl = 0;
+#define CD_TICK(slot)                 \
+  if (tim) {                          \
+    const unsigned long long tn = gtimer(); \
+    tacc[slot] += tn - tl;            \
+    tl = tn;                          \
+  }
   for (int pass = 0; pass < passes; ++pass) {
     for (int j = j0; j < j1; ++j) {
       const int64_t k0 = lp[j], k1 = lp[j + 1];
       if (k0 == k1) continue;
+      if (tim) tl = gtimer();
       for (int64_t t = gtid; t < nlen; t += gsz) {
         ucol[t] = __ldcg(U + t * ldu + j);
         if (LAM) zcol[t] = __ldcg(Z + t * ldu + j);
@@ -863,7 +881,22 @@ __global__ void __launch_bounds__(CO_NT) k_sweep_blk(int q, int nlen, const doub
           const int t0 = ch * BK_CH, t1 = min(nlen, t0 + BK_CH);
           const double* Dr = Dd + (int64_t)(j0 + rr) * ldd;
           double vu = 0.0, vz = 0.0;
-          for (int tb = t0; tb < t1; tb += 32 * BK_U) {
+          int tb = t0;
+          for (; tb + 32 * BK_U <= t1; tb += 32 * BK_U) {
+            double dv[BK_U], sv[BK_U], pv[BK_U];
+#pragma unroll
+            for (int u = 0; u < BK_U; ++u) dv[u] = __ldcg(Dr + tb + lane + 32 * u);
+#pragma unroll
+            for (int u = 0; u < BK_U; ++u) sv[u] = Sj[tb + lane + 32 * u];
+#pragma unroll
+            for (int u = 0; u < BK_U; ++u) pv[u] = Pj[tb + lane + 32 * u];
+#pragma unroll
+            for (int u = 0; u < BK_U; ++u) {
+              vu = fma(dv[u], sv[u], vu);
+              vz = fma(dv[u], pv[u], vz);
+            }
+          }
+          if (tb < t1) {
             double dv[BK_U], sv[BK_U], pv[BK_U];
 #pragma unroll
             for (int u = 0; u < BK_U; ++u) {
@@ -901,6 +934,7 @@ __global__ void __launch_bounds__(CO_NT) k_sweep_blk(int q, int nlen, const doub
         }
       }
       grid.sync();
+      CD_TICK(0)
       for (int64_t kb = k0; kb < k1; kb += BK_B) {
         const int nb = (int)(k1 - kb < BK_B ? k1 - kb : BK_B);
         // ---- phase 1: b0 partials against the block-start vector, and the coupling rows
@@ -913,7 +947,31 @@ __global__ void __launch_bounds__(CO_NT) k_sweep_blk(int q, int nlen, const doub
             const double* Si = LAM ? S + (int64_t)i * lds : P + xcol(xmap, i) * ldp;
             const double* Pi = LAM ? P + (int64_t)i * ldp : nullptr;
             double v = 0.0;
-            for (int tb = t0; tb < t1; tb += 32 * BK_U) {
+            int tb = t0;
+            // full 32 * BK_U-element steps without predicates, so that all of a step's loads are
+            // issued before the first use (with per-load predicates the compiler issued them four
+            // at a time, one DRAM round trip per group: phase 1 ran at 1.2 TB/s)
+            for (; tb + 32 * BK_U <= t1; tb += 32 * BK_U) {
+              double sv[BK_U], pv[BK_U], uv[BK_U], zv[BK_U];
+#pragma unroll
+              for (int u = 0; u < BK_U; ++u) sv[u] = Si[tb + lane + 32 * u];
+              if (LAM) {
+#pragma unroll
+                for (int u = 0; u < BK_U; ++u) pv[u] = Pi[tb + lane + 32 * u];
+              }
+#pragma unroll
+              for (int u = 0; u < BK_U; ++u) uv[u] = __ldcg(ucol + tb + lane + 32 * u);
+              if (LAM) {
+#pragma unroll
+                for (int u = 0; u < BK_U; ++u) zv[u] = __ldcg(zcol + tb + lane + 32 * u);
+              }
+#pragma unroll
+              for (int u = 0; u < BK_U; ++u) {
+                if (LAM) v = fma(sv[u] + pv[u], uv[u], fma(sv[u], zv[u], v));
+                else v = fma(sv[u], uv[u], v);
+              }
+            }
+            if (tb < t1) {
               double sv[BK_U], pv[BK_U], uv[BK_U], zv[BK_U];
 #pragma unroll
               for (int u = 0; u < BK_U; ++u) {
@@ -959,6 +1017,7 @@ __global__ void __launch_bounds__(CO_NT) k_sweep_blk(int q, int nlen, const doub
           }
         }
         grid.sync();
+        CD_TICK(1)
         // ---- phase 2: the block's updates in list order (CTA 0)
         if (blockIdx.x == 0) {
           for (int e = threadIdx.x; e < nb * BK_B; e += CO_NT) sC[e] = __ldcg(Ct + e);
@@ -986,6 +1045,7 @@ __global__ void __launch_bounds__(CO_NT) k_sweep_blk(int q, int nlen, const doub
             }
           }
           __syncthreads();
+          CD_TICK(2)
           if (warp == 0) {
             double corr[BK_R], mymu[BK_R];
 #pragma unroll
@@ -995,26 +1055,51 @@ __global__ void __launch_bounds__(CO_NT) k_sweep_blk(int q, int nlen, const doub
               mymu[r] = 0.0;
             }
             double uj = 0.0, zj = 0.0;
+            // the step's shared-memory operands are fetched one step ahead, so the chain per update
+            // is shuffle -> FMA -> soft threshold -> add -> FMA with no load on it
+            const double* sCc = LAM ? sW : sY;
+            double ia_n = sA[0], c_n = sCc[0], th_n = sT[0], cr_n[BK_R], su_n = 0.0, sp_n = 0.0;
+#pragma unroll
+            for (int r2 = 0; r2 < BK_R; ++r2) cr_n[r2] = sC[lane + 32 * r2];
+            if (LAM) {
+              const bool diag = sI[0] == j;
+              su_n = diag ? Sjj : sSj[0];
+              sp_n = diag ? Pjj : sPj[0];
+            }
 #pragma unroll
             for (int r = 0; r < BK_R; ++r) {
 #pragma unroll 4
               for (int s = 0; s < 32; ++s) {
                 const int kk = 32 * r + s;
                 if (kk >= nb) break;
+                const double ia = ia_n, c = c_n, th = th_n, su = su_n, sp = sp_n;
+                double cr[BK_R];
+#pragma unroll
+                for (int r2 = 0; r2 < BK_R; ++r2) cr[r2] = cr_n[r2];
+                {
+                  const int kn = min(kk + 1, BK_B - 1);
+                  ia_n = sA[kn];
+                  c_n = sCc[kn];
+                  th_n = sT[kn];
+#pragma unroll
+                  for (int r2 = 0; r2 < BK_R; ++r2) cr_n[r2] = sC[kn * BK_B + lane + 32 * r2];
+                  if (LAM) {
+                    const bool diag = sI[kn] == j;
+                    su_n = diag ? Sjj : sSj[kn];
+                    sp_n = diag ? Pjj : sPj[kn];
+                  }
+                }
                 const double b = __shfl_sync(0xffffffffu, corr[r], s);
                 // the coordinate minimiser -c + soft(c - b / a, w / a) with 1 / a and w / a formed
-                // off the chain (a <= 0: no update)
-                const double ia = sA[kk];
-                const double c = LAM ? sW[kk] : sY[kk];
-                const double mu = (ia > 0.0) ? -c + soft(fma(-b, ia, c), sT[kk]) : 0.0;
-                const double* crow = sC + kk * BK_B + lane;
+                // off the chain; a <= 0 (no update) is stored as 1 / a = w / a = 0, for which the
+                // expression is -c + c = 0 exactly
+                const double mu = -c + soft(fma(-b, ia, c), th);
 #pragma unroll
-                for (int r2 = 0; r2 < BK_R; ++r2) corr[r2] = fma(mu, crow[32 * r2], corr[r2]);
+                for (int r2 = 0; r2 < BK_R; ++r2) corr[r2] = fma(mu, cr[r2], corr[r2]);
                 if (lane == s) mymu[r] = mu;
                 if (LAM) {
-                  const bool diag = sI[kk] == j;
-                  uj = fma(mu, diag ? Sjj : sSj[kk], uj);
-                  zj = fma(mu, diag ? Pjj : sPj[kk], zj);
+                  uj = fma(mu, su, uj);
+                  zj = fma(mu, sp, zj);
                 }
               }
             }
@@ -1050,6 +1135,7 @@ __global__ void __launch_bounds__(CO_NT) k_sweep_blk(int q, int nlen, const doub
           }
         }
         grid.sync();
+        CD_TICK(3)
       }
       // ---- column end: write the column back, deferred row updates (disjoint elements)
       for (int64_t t = gtid; t < nlen; t += gsz) {
@@ -1110,8 +1196,12 @@ __global__ void __launch_bounds__(CO_NT) k_sweep_blk(int q, int nlen, const doub
         }
       }
       grid.sync();
+      CD_TICK(4)
     }
   }
+  if (tim)
+    for (int x = 0; x < 5; ++x) g_cd_tim[x] += tacc[x];
+#undef CD_TICK
 }
 
 // ---------------------------------------------------------------- sparse bookkeeping
@@ -1369,7 +1459,14 @@ void lambda_cd_coop(Ctx* c, int q, const double* S, int64_t lds, const double* P
       // J = [j0, j0 + w) are swept, their part of U^T and Z^T is formed from it by two DMMA products
       // (PU = Sigma_{J,:} D, PZ = Psi_{J,:} D, w x q, in the Z workspace), so the deferred row
       // updates touch only the panel's later columns instead of all q (see k_sweep_blk)
-      const int w = c->cd_panel >= 0 ? c->cd_panel : 0;   // default off until measured
+      const int w = c->cd_panel >= 0 ? c->cd_panel : (q > CO_QMAX ? 512 : 0);
+      static const int timing = [] { const char* e = std::getenv("CGGM_CD_TIMING"); return e ? std::atoi(e) : 0; }();
+      if (timing) {
+        unsigned long long z[8] = {0};
+        CGGM_CUDA_CHECK(cudaMemcpyToSymbolAsync(g_cd_tim, z, sizeof(z), 0, cudaMemcpyHostToDevice, c->stream));
+        CGGM_CUDA_CHECK(cudaMemcpyToSymbolAsync(g_cd_tim_on, &timing, sizeof(int), 0, cudaMemcpyHostToDevice, c->stream));
+        CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+      }
       if (w > 0 && w % 2 == 0 && (size_t)2 * w <= (size_t)ldu) {
         double* Dd = U;
         int64_t ldd = ldu;
@@ -1410,6 +1507,13 @@ void lambda_cd_coop(Ctx* c, int q, const double* S, int64_t lds, const double* P
                                                     c->stream));
       }
       c->launches += 2;
+      if (timing) {
+        unsigned long long t[8];
+        CGGM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        CGGM_CUDA_CHECK(cudaMemcpyFromSymbol(t, g_cd_tim, sizeof(t)));
+        std::fprintf(stderr, "CDTIMING lambda m=%lld panel=%d ms: column_start=%.2f phase1=%.2f stage=%.2f chain=%.2f column_end=%.2f\n",
+                     (long long)m, w, t[0] * 1e-6, t[1] * 1e-6, t[2] * 1e-6, t[3] * 1e-6, t[4] * 1e-6);
+      }
       k_lambda_tail<<<1, CD_NT, 0, c->stream>>>(q, Lam->colptr, lv, Lr, Lc, coef, m, D, out);
       post_launch(c, "k_sweep_blk<lambda>");
       return;
