@@ -1020,10 +1020,29 @@ __global__ void __launch_bounds__(CO_NT, 1) k_sweep_blk(int q, int nlen, const d
         CD_TICK(1)
         // ---- phase 2: the block's updates in list order (CTA 0)
         if (blockIdx.x == 0) {
-          for (int e = threadIdx.x; e < nb * BK_B; e += CO_NT) sC[e] = __ldcg(Ct + e);
+          {
+            // the coupling matrix, 16 bytes per load, eight loads in flight per thread
+            const double2* Ct2 = reinterpret_cast<const double2*>(Ct);
+            double2* sC2 = reinterpret_cast<double2*>(sC);
+            const int n2 = nb * BK_B / 2;
+            for (int e0 = threadIdx.x; e0 < n2; e0 += CO_NT * 8) {
+              double2 cv[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * CO_NT;
+                cv[u] = e < n2 ? __ldcg(Ct2 + e) : double2{0.0, 0.0};
+              }
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * CO_NT;
+                if (e < n2) sC2[e] = cv[u];
+              }
+            }
+          }
           for (int kk = threadIdx.x; kk < nb; kk += CO_NT) {
             const int64_t k = kb + kk;
             double s = 0.0;
+#pragma unroll 8
             for (int ch = 0; ch < nch; ++ch) s += __ldcg(part + (int64_t)kk * nch + ch);
             if (LAM) {
               const double4 cf = coef4[k];
