@@ -1076,8 +1076,12 @@ __global__ void __launch_bounds__(CO_NT, 1) k_sweep_blk(int q, int nlen, const d
             double uj = 0.0, zj = 0.0;
             // the step's shared-memory operands are fetched one step ahead, so the chain per update
             // is shuffle -> FMA -> soft threshold -> add -> FMA with no load on it
+            // and b of the next update is formed by every lane as fma(mu, C[kk][kk + 1], corr[kk + 1]
+            // before this update) -- the owner lane's own arithmetic -- with that corr value
+            // broadcast while mu is still being computed: the shuffle is off the chain too
             const double* sCc = LAM ? sW : sY;
             double ia_n = sA[0], c_n = sCc[0], th_n = sT[0], cr_n[BK_R], su_n = 0.0, sp_n = 0.0;
+            double cx_n = sC[1], b_cur = __shfl_sync(0xffffffffu, corr[0], 0);
 #pragma unroll
             for (int r2 = 0; r2 < BK_R; ++r2) cr_n[r2] = sC[lane + 32 * r2];
             if (LAM) {
@@ -1091,7 +1095,7 @@ __global__ void __launch_bounds__(CO_NT, 1) k_sweep_blk(int q, int nlen, const d
               for (int s = 0; s < 32; ++s) {
                 const int kk = 32 * r + s;
                 if (kk >= nb) break;
-                const double ia = ia_n, c = c_n, th = th_n, su = su_n, sp = sp_n;
+                const double ia = ia_n, c = c_n, th = th_n, su = su_n, sp = sp_n, cx = cx_n;
                 double cr[BK_R];
 #pragma unroll
                 for (int r2 = 0; r2 < BK_R; ++r2) cr[r2] = cr_n[r2];
@@ -1100,6 +1104,7 @@ __global__ void __launch_bounds__(CO_NT, 1) k_sweep_blk(int q, int nlen, const d
                   ia_n = sA[kn];
                   c_n = sCc[kn];
                   th_n = sT[kn];
+                  cx_n = sC[kn * BK_B + min(kn + 1, BK_B - 1)];
 #pragma unroll
                   for (int r2 = 0; r2 < BK_R; ++r2) cr_n[r2] = sC[kn * BK_B + lane + 32 * r2];
                   if (LAM) {
@@ -1108,11 +1113,15 @@ __global__ void __launch_bounds__(CO_NT, 1) k_sweep_blk(int q, int nlen, const d
                     sp_n = diag ? Pjj : sPj[kn];
                   }
                 }
-                const double b = __shfl_sync(0xffffffffu, corr[r], s);
+                const double b = b_cur;
+                double nx = corr[r];
+                if (r + 1 < BK_R && s == 31) nx = corr[r + 1 < BK_R ? r + 1 : r];
+                const double pre = __shfl_sync(0xffffffffu, nx, (s + 1) & 31);
                 // the coordinate minimiser -c + soft(c - b / a, w / a) with 1 / a and w / a formed
                 // off the chain; a <= 0 (no update) is stored as 1 / a = w / a = 0, for which the
                 // expression is -c + c = 0 exactly
                 const double mu = -c + soft(fma(-b, ia, c), th);
+                b_cur = fma(mu, cx, pre);
 #pragma unroll
                 for (int r2 = 0; r2 < BK_R; ++r2) corr[r2] = fma(mu, cr[r2], corr[r2]);
                 if (lane == s) mymu[r] = mu;
