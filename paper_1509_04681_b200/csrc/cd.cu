@@ -820,7 +820,7 @@ constexpr int BK_B = 128;              // entries per block
 constexpr int BK_R = BK_B / 32;        // block entries per lane in phase 2
 constexpr int BK_CH = 1280;            // dot-product elements per warp item (large: 128 x 17 items, one round of the grid's 2368 warps)
 constexpr int BK_U = 8;                // loads in flight per lane and operand
-constexpr size_t BK_SMEM = (size_t)BK_B * BK_B * 8 + (size_t)BK_B * (7 * 8 + 4);
+constexpr size_t BK_SMEM = (size_t)BK_B * BK_B * 8 + (size_t)BK_B * (7 * 8 + 4) + (size_t)BK_B * 64;
 
 template <bool LAM>
 __global__ void __launch_bounds__(CO_NT, 1) k_sweep_blk(int q, int nlen, const double* __restrict__ S, int64_t lds,
@@ -843,6 +843,9 @@ __global__ void __launch_bounds__(CO_NT, 1) k_sweep_blk(int q, int nlen, const d
   double* sSj = sW + BK_B;                    // Lambda: Sigma_{i j}, Psi_{i j} of the block's rows
   double* sPj = sSj + BK_B;
   int* sI = reinterpret_cast<int*>(sPj + BK_B);
+  // the chain's per-entry operands packed 64 bytes apiece (three 16-byte loads from one address):
+  // 1 / a, c, threshold / a, C[k][k + 1], and Lambda's column-j factors (the diagonal's already chosen)
+  double* sK = reinterpret_cast<double*>(sI + BK_B);
   double* zcol = ucol + nlen;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t gtid = blockIdx.x * (int64_t)CO_NT + threadIdx.x, gsz = (int64_t)gridDim.x * CO_NT;
@@ -1054,6 +1057,9 @@ __global__ void __launch_bounds__(CO_NT, 1) k_sweep_blk(int q, int nlen, const d
               sI[kk] = Lr[k];
               sSj[kk] = __ldcg(sj + kk);
               sPj[kk] = __ldcg(sj + BK_B + kk);
+              sK[8 * kk + 1] = sW[kk];
+              sK[8 * kk + 4] = sI[kk] == j ? Sjj : sSj[kk];
+              sK[8 * kk + 5] = sI[kk] == j ? Pjj : sPj[kk];
             } else {
               const double2 cf = coef2[k];
               sB[kk] = cf.y + 2.0 * s;
@@ -1061,7 +1067,11 @@ __global__ void __launch_bounds__(CO_NT, 1) k_sweep_blk(int q, int nlen, const d
               sT[kk] = cf.x > 0.0 ? lam / cf.x : 0.0;
               sY[kk] = __ldcg(X + k);
               sI[kk] = Lr[k];
+              sK[8 * kk + 1] = sY[kk];
             }
+            sK[8 * kk] = sA[kk];
+            sK[8 * kk + 2] = sT[kk];
+            sK[8 * kk + 3] = __ldcg(Ct + (int64_t)kk * BK_B + min(kk + 1, BK_B - 1));
           }
           __syncthreads();
           CD_TICK(2)
@@ -1079,16 +1089,12 @@ __global__ void __launch_bounds__(CO_NT, 1) k_sweep_blk(int q, int nlen, const d
             // and b of the next update is formed by every lane as fma(mu, C[kk][kk + 1], corr[kk + 1]
             // before this update) -- the owner lane's own arithmetic -- with that corr value
             // broadcast while mu is still being computed: the shuffle is off the chain too
-            const double* sCc = LAM ? sW : sY;
-            double ia_n = sA[0], c_n = sCc[0], th_n = sT[0], cr_n[BK_R], su_n = 0.0, sp_n = 0.0;
-            double cx_n = sC[1], b_cur = __shfl_sync(0xffffffffu, corr[0], 0);
+            const double2* sK2 = reinterpret_cast<const double2*>(sK);
+            double ia_n = sK2[0].x, c_n = sK2[0].y, th_n = sK2[1].x, cx_n = sK2[1].y, cr_n[BK_R];
+            double su_n = LAM ? sK2[2].x : 0.0, sp_n = LAM ? sK2[2].y : 0.0;
+            double b_cur = __shfl_sync(0xffffffffu, corr[0], 0);
 #pragma unroll
             for (int r2 = 0; r2 < BK_R; ++r2) cr_n[r2] = sC[lane + 32 * r2];
-            if (LAM) {
-              const bool diag = sI[0] == j;
-              su_n = diag ? Sjj : sSj[0];
-              sp_n = diag ? Pjj : sPj[0];
-            }
 #pragma unroll
             for (int r = 0; r < BK_R; ++r) {
 #pragma unroll 4
@@ -1101,16 +1107,17 @@ __global__ void __launch_bounds__(CO_NT, 1) k_sweep_blk(int q, int nlen, const d
                 for (int r2 = 0; r2 < BK_R; ++r2) cr[r2] = cr_n[r2];
                 {
                   const int kn = min(kk + 1, BK_B - 1);
-                  ia_n = sA[kn];
-                  c_n = sCc[kn];
-                  th_n = sT[kn];
-                  cx_n = sC[kn * BK_B + min(kn + 1, BK_B - 1)];
+                  const double2 k0v = sK2[4 * kn], k1v = sK2[4 * kn + 1];
+                  ia_n = k0v.x;
+                  c_n = k0v.y;
+                  th_n = k1v.x;
+                  cx_n = k1v.y;
 #pragma unroll
                   for (int r2 = 0; r2 < BK_R; ++r2) cr_n[r2] = sC[kn * BK_B + lane + 32 * r2];
                   if (LAM) {
-                    const bool diag = sI[kn] == j;
-                    su_n = diag ? Sjj : sSj[kn];
-                    sp_n = diag ? Pjj : sPj[kn];
+                    const double2 k2v = sK2[4 * kn + 2];
+                    su_n = k2v.x;
+                    sp_n = k2v.y;
                   }
                 }
                 const double b = b_cur;
