@@ -1030,15 +1030,18 @@ __global__ void __launch_bounds__(CO_NT, 1) k_sweep_blk(int q, int nlen, const d
             const int n2 = nb * BK_B / 2;
             for (int e0 = threadIdx.x; e0 < n2; e0 += CO_NT * 8) {
               double2 cv[8];
+              bool live[8];
 #pragma unroll
               for (int u = 0; u < 8; ++u) {
                 const int e = e0 + u * CO_NT;
-                cv[u] = e < n2 ? __ldcg(Ct2 + e) : double2{0.0, 0.0};
+                // update m touches only the later entries: pairs of columns <= m are never used
+                live[u] = e < n2 && 2 * (e & (BK_B / 2 - 1)) + 1 > e / (BK_B / 2);
+                cv[u] = live[u] ? __ldcg(Ct2 + e) : double2{0.0, 0.0};
               }
 #pragma unroll
               for (int u = 0; u < 8; ++u) {
                 const int e = e0 + u * CO_NT;
-                if (e < n2) sC2[e] = cv[u];
+                if (live[u]) sC2[e] = cv[u];
               }
             }
           }
